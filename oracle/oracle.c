@@ -1,0 +1,327 @@
+/*
+ * oracle.c -- CPU brute-force ray-casting ORACLE.  TEST INFRASTRUCTURE ONLY
+ * (see oracle.h for who may call it and for the definition it implements).
+ *
+ * Plain, slow and obviously correct: for each queried ray, every triangle of
+ * the ray's environment is tested in double precision.  No BVH, no blocking,
+ * no reordering beyond the plain definition of SURVEY.md §8(c).
+ *
+ * Paper passages followed (§III.D.1 "Exteroceptive Sensors"):
+ *   l.226  M^base_i = {M_j}; M_{i,t} = T_{i,t} o M^base_i -- every vertex of
+ *          sub-mesh j is transformed by T_{j,t}  -> world_triangles()
+ *   l.228  "individual rays are cast outwards per-pixel to evaluate
+ *          intersection with M_{i,t}"            -> make_ray(), cast_one()
+ *   l.228  range for ToF/LiDAR, depth = distance from the image plane
+ *                                                 -> make_ray() direction scaling
+ *   l.218  depth / segmentation / face-index images -> outputs
+ * Readings of silent or garbled points are DESIGN.md §"Readings" R1-R18.
+ */
+#include "oracle.h"
+
+#include <math.h>
+#include <pthread.h>
+#include <stdlib.h>
+#include <string.h>
+#include <unistd.h>
+
+static int64_t g_last_tests = 0;
+
+int64_t oracle_last_tests(void) { return g_last_tests; }
+
+/* ---- small FP64 vector helpers ---------------------------------------- */
+typedef struct { double x, y, z; } v3;
+
+static v3 vsub(v3 a, v3 b) { v3 r = {a.x - b.x, a.y - b.y, a.z - b.z}; return r; }
+static double vdot(v3 a, v3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+static v3 vcross(v3 a, v3 b) {
+    v3 r = {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x};
+    return r;
+}
+static double vnorm(v3 a) { return sqrt(vdot(a, a)); }
+
+/* ---- the env's merged mesh M_{e,t} in FP64 -------------- */
+typedef struct {
+    int64_t n_tri;
+    v3* v;          /* [n_tri][3] world (env-local) vertices */
+    int32_t* label; /* [n_tri] label of the owning instance  */
+    int64_t cap;
+} world_mesh;
+
+static int64_t env_tri_count(const oracle_scene* sc, int32_t e) {
+    int64_t n = 0;
+    for (int64_t j = sc->env_off[e]; j < sc->env_off[e + 1]; ++j) {
+        int32_t a = sc->inst_asset[j];
+        n += sc->face_off[a + 1] - sc->face_off[a];
+    }
+    return n;
+}
+
+/* Transform every vertex of every sub-mesh of env e: x' = A x + b, with the
+ * FP32 inputs promoted to double.  Triangles are laid out in the per-env face
+ * numbering of DESIGN.md reading R2: instances in creation order, faces in
+ * asset order, so triangle k of this array has face index k. */
+static int world_triangles(const oracle_scene* sc, int32_t e, world_mesh* w) {
+    int64_t n = env_tri_count(sc, e);
+    if (n > w->cap) {
+        free(w->v);
+        free(w->label);
+        w->v = (v3*)malloc(sizeof(v3) * 3 * (size_t)(n > 0 ? n : 1));
+        w->label = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n > 0 ? n : 1));
+        if (!w->v || !w->label) return -1;
+        w->cap = n;
+    }
+    int64_t k = 0;
+    for (int64_t j = sc->env_off[e]; j < sc->env_off[e + 1]; ++j) {
+        int32_t a = sc->inst_asset[j];
+        const float* T = sc->inst_T + 12 * j;
+        for (int64_t f = sc->face_off[a]; f < sc->face_off[a + 1]; ++f, ++k) {
+            for (int c = 0; c < 3; ++c) {
+                int64_t vi = sc->vert_off[a] + sc->faces[3 * f + c];
+                const float* p = sc->verts + 3 * vi;
+                double x = p[0], y = p[1], z = p[2];
+                v3 q;
+                q.x = (double)T[0] * x + (double)T[1] * y + (double)T[2] * z + (double)T[3];
+                q.y = (double)T[4] * x + (double)T[5] * y + (double)T[6] * z + (double)T[7];
+                q.z = (double)T[8] * x + (double)T[9] * y + (double)T[10] * z + (double)T[11];
+                w->v[3 * k + c] = q;
+            }
+            w->label[k] = sc->inst_label[j];
+        }
+    }
+    w->n_tri = n;
+    return 0;
+}
+
+/* ---- ray generation (readings R6-R9) ----- */
+static int64_t query_env(const oracle_rays* r, int64_t id) {
+    if (r->model == ORACLE_RAYS) return id / r->R;
+    if (r->model == ORACLE_PINHOLE) return id / ((int64_t)r->S * r->H * r->W);
+    return id / ((int64_t)r->S * r->C * r->K);
+}
+
+static void make_ray(const oracle_rays* r, int64_t id, v3* o, v3* d) {
+    if (r->model == ORACLE_RAYS) {
+        const float* po = r->orig + 3 * id;
+        const float* pd = r->dir + 3 * id;
+        o->x = po[0]; o->y = po[1]; o->z = po[2];
+        d->x = pd[0]; d->y = pd[1]; d->z = pd[2];
+        return;
+    }
+    v3 ds;
+    int64_t es; /* flat (env, sensor) index */
+    if (r->model == ORACLE_PINHOLE) {
+        int64_t u = id % r->W;
+        int64_t v = (id / r->W) % r->H;
+        es = id / ((int64_t)r->W * r->H);
+        /* pixel centre (u+0.5, v+0.5); x forward, y left (u right), z up (v down) */
+        double xs = ((double)u + 0.5 - (double)r->cx) / (double)r->fx;
+        double ys = ((double)v + 0.5 - (double)r->cy) / (double)r->fy;
+        ds.x = 1.0; ds.y = -xs; ds.z = -ys;
+        if (r->kind == ORACLE_RANGE) {
+            double n = vnorm(ds);
+            ds.x /= n; ds.y /= n; ds.z /= n;
+        }
+    } else {
+        int64_t k = id % r->K;
+        int64_t c = (id / r->K) % r->C;
+        es = id / ((int64_t)r->K * r->C);
+        const float* b = r->beams + 3 * (c * r->K + k);
+        ds.x = b[0]; ds.y = b[1]; ds.z = b[2];
+        double n = vnorm(ds);
+        ds.x /= n; ds.y /= n; ds.z /= n;
+    }
+    const float* P = r->poses + 12 * es; /* columns = sensor axes in env frame */
+    d->x = (double)P[0] * ds.x + (double)P[1] * ds.y + (double)P[2] * ds.z;
+    d->y = (double)P[4] * ds.x + (double)P[5] * ds.y + (double)P[6] * ds.z;
+    d->z = (double)P[8] * ds.x + (double)P[9] * ds.y + (double)P[10] * ds.z;
+    o->x = P[3]; o->y = P[7]; o->z = P[11];
+}
+
+/* ---- one ray against every triangle of the env ------------------------- */
+typedef struct {
+    double t;
+    int32_t seg, face, amb;
+    double t2, graze;
+} ray_result;
+
+static void cast_one(const world_mesh* w, v3 o, v3 d, double max_range,
+                     double eps, int want_graze, ray_result* out, int64_t* tests) {
+    double best_t = INFINITY, second_t = INFINITY, graze = INFINITY;
+    int64_t best_f = -1;
+    int near_zero = 0;
+    /* candidates within eps of max_range, kept to decide AMB_RANGE at the end */
+    double range_cand = INFINITY;
+    for (int64_t k = 0; k < w->n_tri; ++k) {
+        v3 a = w->v[3 * k], b = w->v[3 * k + 1], c = w->v[3 * k + 2];
+        v3 n = vcross(vsub(b, a), vsub(c, a));
+        double denom = vdot(n, d);
+        if (denom == 0.0) continue; /* parallel ray or zero-area triangle */
+        double t = vdot(n, vsub(a, o)) / denom;
+        v3 p = {o.x + t * d.x, o.y + t * d.y, o.z + t * d.z};
+        /* inclusive inside test: p on the inner side of all three edges */
+        double e0 = vdot(vcross(vsub(b, a), vsub(p, a)), n);
+        double e1 = vdot(vcross(vsub(c, b), vsub(p, b)), n);
+        double e2 = vdot(vcross(vsub(a, c), vsub(p, c)), n);
+        if (e0 >= 0.0 && e1 >= 0.0 && e2 >= 0.0) {
+            if (fabs(t) <= eps) near_zero = 1;
+            if (fabs(t - max_range) <= eps && t < range_cand) range_cand = t;
+            if (t > 0.0 && t <= max_range) {
+                if (t < best_t || (t == best_t && k < best_f)) {
+                    second_t = best_t;
+                    best_t = t;
+                    best_f = k;
+                } else if (t < second_t) {
+                    second_t = t;
+                }
+            }
+        }
+    }
+    *tests += w->n_tri;
+    if (want_graze) {
+        /* diagnostic second pass: how far outside its triangle the plane hit
+         * of any triangle in front of the winner lies (metres) */
+        double t_lim = best_f >= 0 ? best_t : max_range;
+        for (int64_t k = 0; k < w->n_tri; ++k) {
+            v3 a = w->v[3 * k], b = w->v[3 * k + 1], c = w->v[3 * k + 2];
+            v3 n = vcross(vsub(b, a), vsub(c, a));
+            double denom = vdot(n, d);
+            if (denom == 0.0) continue;
+            double t = vdot(n, vsub(a, o)) / denom;
+            if (!(t > 0.0 && t <= t_lim) || k == best_f) continue;
+            v3 p = {o.x + t * d.x, o.y + t * d.y, o.z + t * d.z};
+            double nn = vnorm(n), out_d = 0.0, s;
+            s = -vdot(vcross(vsub(b, a), vsub(p, a)), n) / (nn * vnorm(vsub(b, a))); if (s > out_d) out_d = s;
+            s = -vdot(vcross(vsub(c, b), vsub(p, b)), n) / (nn * vnorm(vsub(c, b))); if (s > out_d) out_d = s;
+            s = -vdot(vcross(vsub(a, c), vsub(p, c)), n) / (nn * vnorm(vsub(a, c))); if (s > out_d) out_d = s;
+            if (out_d > 0.0 && out_d < graze) graze = out_d;
+        }
+    }
+    int amb = 0;
+    if (second_t - best_t <= eps) amb |= ORACLE_AMB_TIE;
+    if (range_cand < INFINITY && range_cand <= best_t) amb |= ORACLE_AMB_RANGE;
+    if (near_zero) amb |= ORACLE_AMB_ZERO;
+    if (best_f >= 0) {
+        out->t = best_t;
+        out->seg = w->label[best_f];
+        out->face = (int32_t)best_f;
+    } else {
+        out->t = max_range;
+        out->seg = -1;
+        out->face = -1;
+    }
+    out->amb = amb;
+    out->t2 = second_t;
+    out->graze = graze;
+}
+
+/* ---- threading over the (env-sorted) query list ------------------------ */
+typedef struct {
+    const oracle_scene* sc;
+    const oracle_rays* r;
+    const int64_t* query;
+    const int64_t* order; /* query positions sorted by env */
+    int64_t lo, hi;
+    double eps;
+    double* t64; float* dist; int32_t* seg; int32_t* face; int32_t* amb;
+    double* t2; double* graze;
+    int64_t tests;
+    int status;
+} job;
+
+static void* worker(void* arg) {
+    job* jb = (job*)arg;
+    world_mesh w = {0, NULL, NULL, 0};
+    int64_t cur_env = -1;
+    jb->tests = 0;
+    jb->status = 0;
+    for (int64_t i = jb->lo; i < jb->hi; ++i) {
+        int64_t q = jb->order[i];
+        int64_t id = jb->query[q];
+        int64_t e = query_env(jb->r, id);
+        if (e != cur_env) {
+            if (world_triangles(jb->sc, (int32_t)e, &w) != 0) { jb->status = -1; break; }
+            cur_env = e;
+        }
+        v3 o, d;
+        make_ray(jb->r, id, &o, &d);
+        ray_result rr;
+        cast_one(&w, o, d, (double)jb->r->max_range, jb->eps, jb->graze != NULL, &rr, &jb->tests);
+        jb->t64[q] = rr.t;
+        jb->dist[q] = (float)rr.t;
+        jb->seg[q] = rr.seg;
+        jb->face[q] = rr.face;
+        jb->amb[q] = rr.amb;
+        if (jb->t2) jb->t2[q] = rr.t2;
+        if (jb->graze) jb->graze[q] = rr.graze;
+    }
+    free(w.v);
+    free(w.label);
+    return NULL;
+}
+
+static int validate(const oracle_scene* sc, const oracle_rays* r) {
+    if (!sc || !r || sc->n_assets < 0 || sc->n_envs < 0) return -1;
+    for (int32_t a = 0; a < sc->n_assets; ++a) {
+        int64_t nv = sc->vert_off[a + 1] - sc->vert_off[a];
+        for (int64_t f = sc->face_off[a]; f < sc->face_off[a + 1]; ++f)
+            for (int c = 0; c < 3; ++c)
+                if (sc->faces[3 * f + c] < 0 || sc->faces[3 * f + c] >= nv) return -1;
+    }
+    int64_t n_inst = sc->env_off[sc->n_envs];
+    for (int64_t j = 0; j < n_inst; ++j)
+        if (sc->inst_asset[j] < 0 || sc->inst_asset[j] >= sc->n_assets) return -1;
+    if (r->model == ORACLE_RAYS && r->R <= 0) return -1;
+    if (r->model == ORACLE_PINHOLE && (r->W <= 0 || r->H <= 0 || r->S <= 0)) return -1;
+    if (r->model == ORACLE_BEAMS && (r->C <= 0 || r->K <= 0 || r->S <= 0)) return -1;
+    if (r->model < 0 || r->model > 2) return -1;
+    return 0;
+}
+
+int oracle_cast(const oracle_scene* sc, const oracle_rays* r,
+                const int64_t* query, int64_t n_query, double eps,
+                int32_t n_threads, double* t64, float* dist, int32_t* seg,
+                int32_t* face, int32_t* amb, double* t2, double* graze) {
+    if (validate(sc, r) != 0) return -1;
+    int64_t n_rays_total;
+    if (r->model == ORACLE_RAYS) n_rays_total = (int64_t)sc->n_envs * r->R;
+    else if (r->model == ORACLE_PINHOLE) n_rays_total = (int64_t)sc->n_envs * r->S * r->H * r->W;
+    else n_rays_total = (int64_t)sc->n_envs * r->S * r->C * r->K;
+    for (int64_t q = 0; q < n_query; ++q)
+        if (query[q] < 0 || query[q] >= n_rays_total) return -1;
+
+    /* counting sort of query positions by env, so each env's mesh is
+     * transformed once per thread */
+    int64_t* count = (int64_t*)calloc((size_t)sc->n_envs + 1, sizeof(int64_t));
+    int64_t* order = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n_query > 0 ? n_query : 1));
+    if (!count || !order) { free(count); free(order); return -1; }
+    for (int64_t q = 0; q < n_query; ++q) count[query_env(r, query[q]) + 1]++;
+    for (int32_t e = 0; e < sc->n_envs; ++e) count[e + 1] += count[e];
+    for (int64_t q = 0; q < n_query; ++q) order[count[query_env(r, query[q])]++] = q;
+
+    if (n_threads <= 0) n_threads = (int32_t)sysconf(_SC_NPROCESSORS_ONLN);
+    if (n_threads < 1) n_threads = 1;
+    if (n_threads > n_query) n_threads = (int32_t)(n_query > 0 ? n_query : 1);
+    job* jobs = (job*)calloc((size_t)n_threads, sizeof(job));
+    pthread_t* th = (pthread_t*)calloc((size_t)n_threads, sizeof(pthread_t));
+    int status = 0;
+    for (int32_t i = 0; i < n_threads; ++i) {
+        job* jb = &jobs[i];
+        jb->sc = sc; jb->r = r; jb->query = query; jb->order = order;
+        jb->lo = n_query * i / n_threads;
+        jb->hi = n_query * (i + 1) / n_threads;
+        jb->eps = eps;
+        jb->t64 = t64; jb->dist = dist; jb->seg = seg; jb->face = face;
+        jb->amb = amb; jb->t2 = t2; jb->graze = graze;
+        if (n_threads == 1) worker(jb);
+        else if (pthread_create(&th[i], NULL, worker, jb) != 0) { jb->status = -1; th[i] = 0; }
+    }
+    int64_t tests = 0;
+    for (int32_t i = 0; i < n_threads; ++i) {
+        if (n_threads > 1 && th[i]) pthread_join(th[i], NULL);
+        if (jobs[i].status != 0) status = -1;
+        tests += jobs[i].tests;
+    }
+    g_last_tests = tests;
+    free(jobs); free(th); free(count); free(order);
+    return status;
+}

@@ -1,0 +1,109 @@
+/*
+ * oracle.h -- CPU brute-force ray-casting ORACLE (test infrastructure only).
+ *
+ * THIS IS TEST INFRASTRUCTURE.  Only tests/, __graft_entry__.smoke() and the
+ * cpu_baseline / --impl reference legs of bench.py may load or call it.  The
+ * product path (paper_2503_01471_b200/, libagr.so) never links, imports or
+ * executes anything under oracle/, and this file shares no code, header,
+ * table or constant with it.
+ *
+ * What it computes (the plain definition):
+ *   For environment e the scene is the merged mesh M_{e,t} = T_{e,t} o M^base_e
+ *   ("The vertices of the mesh are transformed to match the obstacles in the
+ *   simulator at time t", §III.D.1).  Every instance j of env e
+ *   is an asset mesh whose vertices are mapped x_env = A_j x + b_j (DESIGN.md
+ *   reading R1) in FP64 from the FP32 inputs.  "Individual rays are cast
+ *   outwards per-pixel to evaluate intersection with M_{i,t}":
+ *   for every ray the result is the smallest t with 0 < t <= max_range such
+ *   that o + t d lies on a closed, double-sided triangle of the env; equal t
+ *   goes to the lowest per-env face index.  The distance reported is "range
+ *   for ToF sensors and LiDARs" and "the distance of this point from the image
+ *   plane ... as depth": depth rays use the unnormalised
+ *   direction d_s = (1, -x', -y') so t is the depth; range rays use the unit
+ *   direction so t is the Euclidean range.  Misses report max_range, seg -1,
+ *   face -1 (readings R4, R5).
+ *
+ * Every ray is tested against every triangle of its env (no acceleration
+ * structure), in double precision.  The ray/triangle test is a plane
+ * intersection followed by an inclusive edge-function inside test; it is
+ * deliberately a different formula from the GPU's Moller-Trumbore test.
+ */
+#ifndef AGR_ORACLE_H
+#define AGR_ORACLE_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Scene description (all host memory, borrowed for the duration of a call). */
+typedef struct {
+    int32_t n_assets;
+    const float*   verts;      /* all assets' vertices, [sum V][3]            */
+    const int64_t* vert_off;   /* [n_assets+1] CSR into verts (in vertices)   */
+    const int32_t* faces;      /* all assets' faces, [sum F][3], asset-local  */
+    const int64_t* face_off;   /* [n_assets+1] CSR into faces (in faces)      */
+    int32_t n_envs;
+    const int64_t* env_off;    /* [n_envs+1] CSR of instances per env         */
+    const int32_t* inst_asset; /* [n_inst]                                    */
+    const int32_t* inst_label; /* [n_inst]                                    */
+    const float*   inst_T;     /* [n_inst][3][4] row-major: x' = A x + b      */
+} oracle_scene;
+
+/* Ray models. */
+enum { ORACLE_RAYS = 0, ORACLE_PINHOLE = 1, ORACLE_BEAMS = 2 };
+enum { ORACLE_DEPTH = 0, ORACLE_RANGE = 1 };
+
+typedef struct {
+    int32_t model;        /* ORACLE_RAYS / ORACLE_PINHOLE / ORACLE_BEAMS      */
+    /* ORACLE_RAYS: orig, dir [n_envs][R][3] env-local, t in units of |dir|.  */
+    const float* orig;
+    const float* dir;
+    int32_t R;
+    /* ORACLE_PINHOLE: W, H, fx, fy, cx, cy, kind; poses [n_envs][S][3][4].   */
+    int32_t W, H;
+    float fx, fy, cx, cy;
+    int32_t kind;
+    /* ORACLE_BEAMS: beam table [C][K][3] (sensor frame), poses.             */
+    const float* beams;
+    int32_t C, K;
+    const float* poses;   /* [n_envs][S][3][4] sensor -> env                 */
+    int32_t S;
+    float max_range;
+} oracle_rays;
+
+/* Ambiguity bits (SURVEY.md §8(c) parity rules). */
+enum {
+    ORACLE_AMB_TIE   = 1, /* best and second-best candidate t within amb_eps */
+    ORACLE_AMB_RANGE = 2, /* a candidate within amb_eps of max_range         */
+    ORACLE_AMB_ZERO  = 4  /* a candidate within amb_eps of t = 0             */
+};
+
+/*
+ * Cast the rays named by `query` (flat ray ids: for RAYS  id = e*R + r; for
+ * PINHOLE id = ((e*S + s)*H + v)*W + u; for BEAMS id = ((e*S + s)*C + c)*K + k).
+ * Per query it writes:
+ *   t64[q]   the winning t in double (max_range on a miss)
+ *   dist[q]  (float)t64[q]
+ *   seg[q]   instance label or -1;  face[q] per-env face index or -1
+ *   amb[q]   ORACLE_AMB_* bits computed with tolerance amb_eps (metres)
+ *   t2[q]    second-best candidate t (+inf if none)             [may be NULL]
+ *   graze[q] smallest distance (scene units) by which the plane hit of a
+ *            triangle closer than the winner lies outside that triangle
+ *            (diagnostic for silhouette rays; +inf if none)     [may be NULL]
+ * n_threads <= 0 uses all online cores.  Returns 0, or -1 on bad input.
+ */
+int oracle_cast(const oracle_scene* scene, const oracle_rays* rays,
+                const int64_t* query, int64_t n_query, double amb_eps,
+                int32_t n_threads,
+                double* t64, float* dist, int32_t* seg, int32_t* face,
+                int32_t* amb, double* t2, double* graze);
+
+/* Number of triangle tests the last oracle_cast call performed (for the
+ * cpu_baseline report: ray-triangle tests/s). */
+int64_t oracle_last_tests(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,63 @@
+"""Test helpers: turn scenegen sensor dicts into oracle ray specs, and the
+parity comparison rules of SURVEY.md §8(c) (written once, used by every
+GPU parity test).  Contains no ray-casting arithmetic."""
+from __future__ import annotations
+
+import numpy as np
+
+import oracle
+
+
+def oracle_rays(sensor: dict, kind: str = "depth") -> dict:
+    """scenegen sensor dict -> oracle.cast ``rays`` dict."""
+    if sensor["kind"] == "pinhole":
+        d = dict(model=oracle.PINHOLE, kind=oracle.DEPTH if kind == "depth" else oracle.RANGE,
+                 poses=sensor["poses"], max_range=sensor["max_range"])
+        d.update(sensor["cam"])
+        return d
+    if sensor["kind"] == "beams":
+        return dict(model=oracle.BEAMS, beams=sensor["beams"], poses=sensor["poses"],
+                    max_range=sensor["max_range"])
+    return dict(model=oracle.RAYS, orig=sensor["orig"], dir=sensor["dir"],
+                max_range=sensor["max_range"])
+
+
+# SURVEY.md §8(c) / BASELINE.json north_star: |d| <= max(1e-5 m, 1e-6 * ref)
+DIST_ABS = 1e-5
+DIST_REL = 1e-6
+
+
+def compare(ref: "oracle.OracleResult", dist, seg, face, what=""):
+    """Apply the parity rules; returns a dict of counts, raises on failure.
+
+    distance: every ray within max(1e-5, 1e-6*ref) of the oracle's FP64 t.
+    seg / face: bit-exact on every ray that is not ambiguous (oracle AMB_*).
+    """
+    dist = np.asarray(dist, np.float64).reshape(-1)
+    tol = np.maximum(DIST_ABS, DIST_REL * np.abs(ref.t64))
+    err = np.abs(dist - ref.t64)
+    bad_d = np.nonzero(err > tol)[0]
+    amb = ref.amb != 0
+    out = dict(n=len(dist), ambiguous=int(amb.sum()), max_err=float(err.max()) if len(err) else 0.0)
+    msgs = []
+    if len(bad_d):
+        i = bad_d[0]
+        msgs.append(f"{what}: {len(bad_d)} distance mismatches; first #{i}: gpu={dist[i]!r} "
+                    f"oracle={ref.t64[i]!r} seg {seg.reshape(-1)[i] if seg is not None else '-'}"
+                    f"/{ref.seg[i]} face {face.reshape(-1)[i] if face is not None else '-'}/{ref.face[i]} "
+                    f"amb={ref.amb[i]} t2={ref.t2[i]!r}")
+    for name, got, exp in (("seg", seg, ref.seg), ("face", face, ref.face)):
+        if got is None:
+            continue
+        got = np.asarray(got).reshape(-1)
+        bad = np.nonzero((got != exp) & ~amb)[0]
+        out[f"{name}_mismatch"] = int(len(bad))
+        out[f"{name}_diff_ambiguous"] = int(((got != exp) & amb).sum())
+        if len(bad):
+            i = bad[0]
+            msgs.append(f"{what}: {len(bad)} {name} mismatches; first #{i}: gpu={got[i]} "
+                        f"oracle={exp[i]} dist gpu={dist[i]!r} oracle={ref.t64[i]!r} "
+                        f"t2={ref.t2[i]!r} amb={ref.amb[i]}")
+    if msgs:
+        raise AssertionError("\n".join(msgs))
+    return out

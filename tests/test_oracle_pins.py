@@ -1,0 +1,518 @@
+"""Pins for the CPU oracle (-m "not gpu").
+
+The oracle (oracle/oracle.c) is checked here against things other than
+itself: closed forms, analytic geometry, invariants and an independent
+Moller-Trumbore brute force written in numpy.  Each test names the passage
+or DESIGN.md reading it pins.  A plausible mistake in the oracle (dropped
+term, wrong sign, transposed pose, wrong face numbering, wrong tie rule,
+wrong range/depth scaling) fails at least one of these.
+"""
+from __future__ import annotations
+
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import scenegen as sg
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def cast_pinhole(sc, cam, poses, kind=oracle.DEPTH, max_range=10.0, **kw):
+    rays = dict(model=oracle.PINHOLE, kind=kind, poses=poses, max_range=max_range, **cam)
+    return oracle.cast(sc, rays, **kw)
+
+
+def cast_rays(sc, orig, dirs, max_range=100.0, **kw):
+    return oracle.cast(sc, dict(model=oracle.RAYS, orig=orig, dir=dirs, max_range=max_range), **kw)
+
+
+def quad_mesh(size=100.0, name="quad"):
+    """Square in the plane x = 0 (normal +x), side `size`."""
+    h = size / 2
+    v = np.asarray([[0, -h, -h], [0, h, -h], [0, h, h], [0, -h, h]], np.float32)
+    return sg.Mesh(name, v, np.asarray([[0, 1, 2], [0, 2, 3]], np.int32))
+
+
+def _golden_c1():
+    vals = {}
+    with open(os.path.join(GOLDEN, "c1_camera.txt")) as f:
+        for line in f:
+            if line.startswith("#") or not line.strip():
+                continue
+            k, v = line.split(None, 1)
+            vals[k] = v.strip()
+    return vals
+
+
+# --------------------------------------------------------------------------
+# closed forms
+# --------------------------------------------------------------------------
+
+def test_c1_worked_example_golden():
+    """SURVEY.md §8(c) config-1 worked example (tests/golden/c1_camera.txt)."""
+    g = _golden_c1()
+    sc, s = sg.config1()
+    d = cast_pinhole(sc, s["cam"], s["poses"], oracle.DEPTH)
+    r = cast_pinhole(sc, s["cam"], s["poses"], oracle.RANGE)
+    depth = d.t64.reshape(16, 16)
+    rng_ = r.t64.reshape(16, 16)
+    hit = np.zeros((16, 16), bool)
+    hit[6:10, 6:10] = True
+    assert np.all(depth[hit] == float(g["depth"]))
+    assert np.all(depth[~hit] == float(g["miss_distance"]))
+    assert np.all(d.seg.reshape(16, 16)[hit] == int(g["label"]))
+    assert np.all(d.seg.reshape(16, 16)[~hit] == -1)
+    assert np.all(d.face.reshape(16, 16)[~hit] == -1)
+    # the near face is the cube's -x side = faces 0, 1 of box_mesh
+    assert set(np.unique(d.face.reshape(16, 16)[hit])) <= {0, 1}
+    want = {1: float(g["range_|x'|=1/16_|y'|=1/16"]), 3: float(g["range_|x'|=1/16_|y'|=3/16"]),
+            9: float(g["range_|x'|=3/16_|y'|=3/16"])}
+    for v in range(6, 10):
+        for u in range(6, 10):
+            a, b = abs(2 * u - 15), abs(2 * v - 15)  # 1 or 3 (in 1/16 units)
+            assert abs(rng_[v, u] - want[a * b]) < 1e-9, (u, v)
+    # the 4 pixels on the split diagonal of the near face are exact ties
+    amb = d.amb.reshape(16, 16)
+    assert amb[hit].astype(bool).sum() == 4
+    assert np.all(amb[~hit] == 0)
+
+
+@pytest.mark.parametrize("dist", [1.5, 3.7, 9.25])
+def test_plane_depth_constant_range_over_cos(dist):
+    """Camera facing a plane at distance d: depth = d at every pixel, range =
+    d / cos(theta) (north_star)."""
+    dist = float(np.float32(dist))  # the plane position is an FP32 input
+    cam = sg.pinhole(40, 30, 87.0)
+    sc = sg.assemble([quad_mesh()], [[(0, 7, sg.make_T(np.eye(3), (dist, 0, 0)))]])
+    poses = sg.identity_poses(1)
+    d = cast_pinhole(sc, cam, poses, oracle.DEPTH, max_range=100.0)
+    r = cast_pinhole(sc, cam, poses, oracle.RANGE, max_range=100.0)
+    assert np.all(np.abs(d.t64 - dist) < 1e-12)
+    # cos(theta) between the optical axis and the pixel ray, from the angle
+    u = np.arange(cam["W"]) + 0.5 - cam["cx"]
+    v = np.arange(cam["H"]) + 0.5 - cam["cy"]
+    V, U = np.meshgrid(v, u, indexing="ij")
+    ax = np.arctan2(np.hypot(U / cam["fx"], V / cam["fy"]), 1.0)
+    assert np.allclose(r.t64.reshape(cam["H"], cam["W"]), dist / np.cos(ax), rtol=0, atol=1e-12)
+    assert np.all(d.seg == 7)
+
+
+def test_plane_rotated_sensor_and_scene():
+    """Same plane pin with the pair (plane, camera) under a random rigid
+    motion: depth stays d within FP32 input rounding."""
+    rng = np.random.default_rng(5)
+    cam = sg.pinhole(32, 24, 70.0)
+    R = sg.random_rotation(rng)
+    p = rng.uniform(-5, 5, 3)
+    dist = 4.0
+    Tq = sg.make_T(R, R @ np.asarray([dist, 0, 0]) + p)
+    sc = sg.assemble([quad_mesh()], [[(0, 1, Tq)]])
+    poses = sg.make_T(R, p)[None, None]
+    d = cast_pinhole(sc, cam, poses, oracle.DEPTH)
+    assert np.all(np.abs(d.t64 - dist) < 2e-5)
+    assert np.all(d.seg == 1)
+
+
+def test_cube_slab_analytic():
+    """Axis-aligned cube: slab-method t and entry side."""
+    rng = np.random.default_rng(11)
+    lo, hi = np.asarray([1.0, -0.5, -0.25]), np.asarray([2.0, 0.75, 0.5])
+    box = sg.box_mesh("box", lo, hi)
+    sc = sg.assemble([box], [[(0, 3, sg.make_T(np.eye(3), (0, 0, 0)))]])
+    n = 4000
+    o = rng.uniform(-3, 4, (n, 3)).astype(np.float32)
+    target = rng.uniform(lo - 0.2, hi + 0.2, (n, 3))
+    d = (target - o).astype(np.float32)
+    res = cast_rays(sc, o[None], d[None])
+    o64, d64 = o.astype(np.float64), d.astype(np.float64)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        t0 = (lo - o64) / d64
+        t1 = (hi - o64) / d64
+    tn = np.minimum(t0, t1)
+    tf = np.maximum(t0, t1)
+    tmin = tn.max(1)
+    tmax = tf.min(1)
+    inside = np.all((o64 > lo) & (o64 < hi), 1)
+    checked = 0
+    for i in range(n):
+        if inside[i]:
+            continue
+        hit = tmin[i] <= tmax[i] and tmin[i] > 0
+        # skip rays within 1e-7 of an edge (tie between two sides)
+        srt = np.sort(tn[i])
+        if hit and (srt[2] - srt[1] < 1e-7 or tmax[i] - tmin[i] < 1e-7):
+            continue
+        if not hit:
+            if tmin[i] <= tmax[i] + 1e-7 and tmin[i] > -1e-7:
+                continue
+            assert res.face[i] == -1 and res.t64[i] == 100.0, i
+            continue
+        checked += 1
+        assert abs(res.t64[i] - tmin[i]) < 1e-9 * max(1, tmin[i]), i
+        axis = int(np.argmax(tn[i]))
+        side = 2 * axis + (1 if d64[i, axis] < 0 else 0)  # entering +x side when moving -x
+        assert res.face[i] // 2 == side, (i, res.face[i], side)
+        assert res.seg[i] == 3
+    assert checked > 500
+
+
+@pytest.mark.parametrize("subdiv,ratio", [(0, 0.79465), (1, 0.93417), (2, 0.98225), (3, 0.99547)])
+def test_icosphere_from_centre(subdiv, ratio):
+    """Camera at the centre of an icosphere of circumradius R: every ray hits,
+    r_in <= t <= R, and t * (n_f . d_hat) = distance of the reported face's
+    plane (SURVEY.md §8(c) sphere pin; inradius ratios are of the icosphere)."""
+    R = 2.0
+    mesh = sg.sphere_mesh(R, subdiv)
+    # inradius from the mesh: min plane distance over faces (independent check
+    # of the quoted ratio)
+    v = mesh.verts.astype(np.float64)
+    f = mesh.faces
+    n = np.cross(v[f[:, 1]] - v[f[:, 0]], v[f[:, 2]] - v[f[:, 0]])
+    nh = n / np.linalg.norm(n, axis=1, keepdims=True)
+    plane_d = np.abs(np.einsum("ij,ij->i", nh, v[f[:, 0]]))
+    assert abs(plane_d.min() / R - ratio) < 2e-4
+    sc = sg.assemble([mesh], [[(0, 2, sg.make_T(np.eye(3), (0, 0, 0)))]])
+    cam = sg.pinhole(24, 16, 100.0)
+    rng = np.random.default_rng(subdiv)
+    P = sg.make_T(sg.random_rotation(rng), (0, 0, 0))[None, None]
+    res = cast_pinhole(sc, cam, P, oracle.RANGE)
+    assert np.all(res.face >= 0)
+    assert np.all(res.t64 <= R * (1 + 1e-6)) and np.all(res.t64 >= R * ratio * (1 - 1e-3))
+    # recompute each ray direction independently: unit vector through the pixel
+    u = np.arange(cam["W"]) + 0.5 - cam["cx"]
+    vv = np.arange(cam["H"]) + 0.5 - cam["cy"]
+    V, U = np.meshgrid(vv, u, indexing="ij")
+    ds = np.stack([np.ones_like(U), -U / cam["fx"], -V / cam["fy"]], -1).reshape(-1, 3)
+    ds /= np.linalg.norm(ds, axis=1, keepdims=True)
+    dw = ds @ P[0, 0, :, :3].astype(np.float64).T
+    cosang = np.abs(np.einsum("ij,ij->i", nh[res.face], dw))
+    assert np.allclose(res.t64 * cosang, plane_d[res.face], atol=1e-9)
+
+
+def test_sphere_from_outside_bounds():
+    """Outside camera: hit t between the circumsphere and insphere entry
+    distances; rays missing the circumsphere miss."""
+    R, subdiv = 1.0, 2
+    r_in = 0.98225 * R
+    mesh = sg.sphere_mesh(R, subdiv)
+    c = np.asarray([4.0, 0.3, -0.2])
+    sc = sg.assemble([mesh], [[(0, 1, sg.make_T(np.eye(3), c))]])
+    rng = np.random.default_rng(3)
+    n = 3000
+    o = np.zeros((n, 3), np.float32)
+    d = (c + rng.uniform(-1.3, 1.3, (n, 3)) - 0).astype(np.float32)
+    res = cast_rays(sc, o[None], d[None])
+    d64 = d.astype(np.float64)
+    dh = d64 / np.linalg.norm(d64, axis=1, keepdims=True)
+    b = dh @ c
+    perp2 = np.dot(c, c) - b * b
+
+    def entry(rad):
+        disc = rad * rad - perp2
+        with np.errstate(invalid="ignore"):
+            return b - np.sqrt(disc)
+
+    tR = entry(R) / np.linalg.norm(d64, axis=1)
+    tr = entry(r_in) / np.linalg.norm(d64, axis=1)
+    miss_R = perp2 > R * R
+    assert np.all(res.face[miss_R] == -1)
+    hit_r = perp2 < (r_in * 0.999) ** 2
+    assert np.all(res.face[hit_r] >= 0)
+    h = res.face >= 0
+    assert np.all(res.t64[h] >= tR[h] - 1e-9)
+    ok = hit_r & h
+    assert np.all(res.t64[ok] <= tr[ok] + 1e-9)
+
+
+def test_lidar_wall_beam_zero():
+    """Beam (e=0, a=0) toward a wall at 2 m -> range 2.0."""
+    beams = sg.lidar_beams(8, 16)  # a_k = -180 + 22.5k: k = 8 is a = 0
+    sc = sg.assemble([quad_mesh()], [[(0, 1, sg.make_T(np.eye(3), (2.0, 0, 0)))]])
+    # 8 channels from -45 to 45: no exact 0; use a 9-channel table for e = 0
+    beams = sg.lidar_beams(9, 16)
+    res = oracle.cast(sc, dict(model=oracle.BEAMS, beams=beams, poses=sg.identity_poses(1),
+                               max_range=10.0))
+    rr = res.t64.reshape(9, 16)
+    assert abs(rr[4, 8] - 2.0) < 1e-7  # float32 beam table is cos/sin rounded
+    assert res.seg.reshape(9, 16)[4, 8] == 1
+
+
+@pytest.mark.parametrize("nseg", [16, 23])
+def test_lidar_ring_in_ngon_cylinder(nseg):
+    """Horizontal ring inside an n-gon cylinder of circumradius R: range =
+    R cos(pi/n) / cos(phi), phi = angle from the facet normal."""
+    R = 3.0
+    cyl = sg.cylinder_mesh("cyl", R, 4.0, nseg=nseg, closed=False, z0=-2.0)
+    sc = sg.assemble([cyl], [[(0, 1, sg.make_T(np.eye(3), (0, 0, 0)))]])
+    K = 360
+    beams = sg.lidar_beams(3, K, -10.0, 10.0)
+    res = oracle.cast(sc, dict(model=oracle.BEAMS, beams=beams, poses=sg.identity_poses(1),
+                               max_range=10.0))
+    rr = res.t64.reshape(3, K)[1]
+    az = np.radians(-180.0 + 360.0 * np.arange(K) / K)
+    seg_w = 2 * math.pi / nseg
+    # facet k spans [k seg_w, (k+1) seg_w]; its normal points at (k+0.5) seg_w
+    phi = (np.mod(az, seg_w) - seg_w / 2)
+    want = R * math.cos(math.pi / nseg) / np.cos(phi)
+    # beams with az on a facet boundary are ties: skip them
+    edge = np.abs(np.abs(phi) - seg_w / 2) < 1e-6
+    assert np.allclose(rr[~edge], want[~edge], atol=2e-6)
+    assert np.all((rr >= R * math.cos(math.pi / nseg) - 1e-6) & (rr <= R + 1e-6))
+
+
+def test_lidar_dome_under_ceiling():
+    """Dome pattern under a ceiling plane at height h: range = h / sin(e)
+    (PAPER.md:228 'Dome LiDAR')."""
+    h = 2.5
+    ceil = quad_mesh(200.0)
+    Rz = np.asarray([[0, 0, -1], [0, 1, 0], [1, 0, 0]], np.float64)  # +x normal -> -z
+    sc = sg.assemble([ceil], [[(0, 1, sg.make_T(Rz, (0, 0, h)))]])
+    beams = sg.dome_beams(8, 24)
+    res = oracle.cast(sc, dict(model=oracle.BEAMS, beams=beams, poses=sg.identity_poses(1),
+                               max_range=50.0))
+    C, K = 8, 24
+    e = np.radians(90.0 / C + (90.0 - 90.0 / C) * np.arange(C) / (C - 1))
+    want = np.repeat((h / np.sin(e))[:, None], K, 1)
+    assert np.allclose(res.t64.reshape(C, K), want, rtol=1e-6)
+
+
+# --------------------------------------------------------------------------
+# semantics: misses, max range, ties, degenerate faces, numbering
+# --------------------------------------------------------------------------
+
+def test_misses_empty_env_and_facing_away():
+    """Empty env and a camera facing away -> max_range, -1, -1."""
+    cam = sg.pinhole(8, 6, 60.0)
+    sc = sg.assemble([sg.cube_mesh()], [[], [(0, 1, sg.make_T(np.eye(3), (-3, 0, 0)))]])
+    res = cast_pinhole(sc, cam, sg.identity_poses(2), oracle.DEPTH, max_range=7.5)
+    assert np.all(res.t64 == 7.5) and np.all(res.seg == -1) and np.all(res.face == -1)
+
+
+def test_max_range_inclusive():
+    """A hit at exactly t = max_range counts; beyond it is a miss (reading R5);
+    hits within 1e-5 of max_range are flagged AMB_RANGE."""
+    def run(x, mr):
+        sc = sg.assemble([quad_mesh()], [[(0, 1, sg.make_T(np.eye(3), (x, 0, 0)))]])
+        o = np.asarray([[[0, 0.1, 0.3]]], np.float32)  # off the quad's diagonal
+        d = np.asarray([[[1, 0, 0]]], np.float32)
+        return cast_rays(sc, o, d, max_range=mr)
+    r = run(10.0, 10.0)
+    assert r.face[0] >= 0 and r.t64[0] == 10.0 and r.amb[0] & oracle.AMB_RANGE
+    r = run(10.5, 10.0)
+    assert r.face[0] == -1 and r.t64[0] == 10.0 and r.amb[0] == 0
+    r = run(10.000004, 10.0)
+    assert r.face[0] == -1 and r.amb[0] & oracle.AMB_RANGE
+    r = run(5.0, 10.0)
+    assert r.amb[0] == 0
+
+
+def test_tie_goes_to_lowest_face_and_is_flagged():
+    """Coincident triangles: equal t -> lowest per-env face index (reading
+    R11), flagged AMB_TIE."""
+    q = quad_mesh()
+    sc = sg.assemble([q, q], [[(1, 5, sg.make_T(np.eye(3), (3, 0, 0))),
+                               (0, 6, sg.make_T(np.eye(3), (3, 0, 0)))]])
+    o = np.zeros((1, 2, 3), np.float32)
+    d = np.asarray([[[1, 0.1, 0.05], [1, -0.1, -0.05]]], np.float32)
+    r = cast_rays(sc, o, d)
+    assert list(r.seg) == [5, 5]
+    # instance 0's faces are 0 (y > z half of the quad) and 1; instance 1's
+    # coincident copies are 2 and 3
+    assert list(r.face) == [0, 1]
+    assert np.all(r.amb & oracle.AMB_TIE)
+
+
+def test_degenerate_face_kept_for_numbering_never_hit():
+    """Zero-area faces keep the numbering and are never hit (reading R12)."""
+    v = np.asarray([[0, -5, -5], [0, 5, -5], [0, 5, 5], [0, -5, 5]], np.float32)
+    m = sg.Mesh("q", v, np.asarray([[0, 1, 1], [0, 2, 2], [0, 1, 2], [0, 2, 3]], np.int32))
+    sc = sg.assemble([m], [[(0, 1, sg.make_T(np.eye(3), (2, 0, 0)))]])
+    o = np.zeros((1, 2, 3), np.float32)
+    d = np.asarray([[[1, 0.2, -0.1], [1, -0.2, 0.1]]], np.float32)
+    r = cast_rays(sc, o, d)
+    assert list(r.face) == [2, 3]
+
+
+def test_double_sided():
+    """Triangles are hit from both sides (reading R10)."""
+    sc = sg.assemble([quad_mesh()], [[(0, 1, sg.make_T(np.eye(3), (0, 0, 0)))]])
+    o = np.asarray([[[-2, 0, 0], [2, 0.5, 0]]], np.float32)
+    d = np.asarray([[[1, 0, 0], [-1, 0, 0]]], np.float32)
+    r = cast_rays(sc, o, d)
+    assert np.all(r.face >= 0) and np.allclose(r.t64, 2.0)
+
+
+def test_face_numbering_across_instances_and_labels():
+    """Per-env face index = prefix sum of instance face counts + local index
+    (reading R2); seg = instance label (reading R3)."""
+    cube, cyl = sg.cube_mesh(), sg.closed_cylinder_92()
+    sc = sg.assemble([cube, cyl], [
+        [(1, 10, sg.make_T(np.eye(3), (5, 0, 0))), (0, 20, sg.make_T(np.eye(3), (3, 0, 0)))],
+        [(0, 30, sg.make_T(np.eye(3), (3, 0, 0)))]])
+    o = np.zeros((2, 1, 3), np.float32)
+    d = np.asarray([[[1, 0.01, 0.02]], [[1, 0.01, 0.02]]], np.float32)
+    r = cast_rays(sc, o, d)
+    # env 0: the cube (instance 1) is nearer; its faces follow the cylinder's 92
+    assert r.seg[0] == 20 and 92 <= r.face[0] < 92 + 12
+    assert r.face[0] - 92 in (0, 1)  # -x side of the cube
+    assert r.seg[1] == 30 and r.face[1] in (0, 1)
+    assert abs(r.t64[0] - 2.5) < 1e-9
+
+
+def test_origin_on_surface_flagged_zero():
+    """A candidate within 1e-5 of t = 0 sets AMB_ZERO (parity rule 3)."""
+    sc = sg.assemble([quad_mesh()], [[(0, 1, sg.make_T(np.eye(3), (0, 0, 0)))]])
+    o = np.asarray([[[1e-6, 0.1, 0.1]]], np.float32)
+    d = np.asarray([[[-1, 0.0, 0.0]]], np.float32)
+    r = cast_rays(sc, o, d)
+    assert r.amb[0] & oracle.AMB_ZERO
+
+
+def test_sensor_frame_axes():
+    """x forward, y left, z up; u grows to the right (-y), v downward (-z)
+    (reading R7): an object at (+x, -y, +z) lands in the top-right quadrant."""
+    cam = sg.pinhole(20, 20, 90.0)
+    sc = sg.assemble([sg.cube_mesh(0.5)], [[(0, 1, sg.make_T(np.eye(3), (4, -1.5, 1.5)))]])
+    r = cast_pinhole(sc, cam, sg.identity_poses(1))
+    img = r.seg.reshape(20, 20)
+    vs, us = np.nonzero(img == 1)
+    assert len(us) > 0 and us.min() >= 10 and vs.max() < 10
+
+
+def test_depth_le_range_and_principal_ray():
+    """depth <= range on every hit; equality on the optical axis."""
+    sc, s = sg.config2(n_envs=2)
+    cam = dict(s["cam"])
+    cam.update(W=41, H=21, cx=20.5, cy=10.5)
+    d = cast_pinhole(sc, cam, s["poses"], oracle.DEPTH)
+    r = cast_pinhole(sc, cam, s["poses"], oracle.RANGE)
+    hit = (d.face >= 0) & (r.face >= 0)
+    assert hit.sum() > 50
+    assert np.all(d.t64[hit] <= r.t64[hit] + 1e-12)
+    centre = (np.arange(2) * 21 + 10) * 41 + 20
+    for c in centre:
+        if d.face[c] >= 0:
+            assert abs(d.t64[c] - r.t64[c]) < 1e-12
+
+
+# --------------------------------------------------------------------------
+# independent brute force (different formula) and invariants
+# --------------------------------------------------------------------------
+
+def _mt_numpy(tris, o, d, max_range):
+    """Independent FP64 Moller-Trumbore (vectorised numpy), closest hit,
+    lowest index on equal t."""
+    v0, v1, v2 = tris[:, 0], tris[:, 1], tris[:, 2]
+    e1, e2 = v1 - v0, v2 - v0
+    out_t = np.full(len(o), max_range)
+    out_f = np.full(len(o), -1)
+    for i in range(len(o)):
+        p = np.cross(d[i], e2)
+        det = np.einsum("ij,ij->i", e1, p)
+        ok = det != 0
+        inv = np.where(ok, 1.0 / np.where(ok, det, 1.0), 0.0)
+        s = o[i] - v0
+        u = np.einsum("ij,ij->i", s, p) * inv
+        q = np.cross(s, e1)
+        v = (q @ d[i]) * inv
+        t = np.einsum("ij,ij->i", e2, q) * inv
+        hit = ok & (u >= 0) & (v >= 0) & (u + v <= 1) & (t > 0) & (t <= max_range)
+        if hit.any():
+            k = np.nonzero(hit)[0]
+            j = k[np.lexsort((k, t[k]))[0]]
+            out_t[i], out_f[i] = t[j], j
+    return out_t, out_f
+
+
+def test_matches_independent_moller_trumbore():
+    """1000 random rays vs a 50-triangle scene == an independent brute force
+    with a different intersection formula."""
+    rng = np.random.default_rng(42)
+    verts = rng.uniform(-2, 2, (150, 3)).astype(np.float32)
+    m = sg.Mesh("soup", verts, np.arange(150, dtype=np.int32).reshape(50, 3))
+    T = sg.make_T(sg.random_rotation(rng), rng.uniform(-1, 1, 3), 1.3)
+    sc = sg.assemble([m], [[(0, 4, T)]])
+    n = 1000
+    o = rng.uniform(-4, 4, (n, 3)).astype(np.float32)
+    d = rng.normal(size=(n, 3)).astype(np.float32)
+    res = cast_rays(sc, o[None], d[None], max_range=20.0)
+    A, b = T[:, :3].astype(np.float64), T[:, 3].astype(np.float64)
+    tris = (verts.astype(np.float64) @ A.T + b).reshape(50, 3, 3)
+    t, f = _mt_numpy(tris, o.astype(np.float64), d.astype(np.float64), 20.0)
+    amb = res.amb != 0
+    assert np.allclose(res.t64, t, rtol=1e-9, atol=1e-12)
+    assert np.all((res.face == f) | amb)
+    assert (f >= 0).sum() > 100
+
+
+def _rigid_exact(rng):
+    """Random signed axis permutation (a rotation): exact in FP32, so the
+    transformed inputs represent exactly the moved scene.  (A translation is
+    not FP32-exact in general: it is covered by the generic test.)"""
+    perm = rng.permutation(3)
+    R = np.zeros((3, 3))
+    R[np.arange(3), perm] = rng.choice([-1.0, 1.0], 3)
+    if np.linalg.det(R) < 0:
+        R[0] *= -1
+    return R, np.zeros(3)
+
+
+def _move(sc, poses, R, p):
+    T = sc.inst_T.astype(np.float64)
+    T2 = np.empty_like(T)
+    T2[:, :, :3] = np.einsum("ij,njk->nik", R, T[:, :, :3])
+    T2[:, :, 3] = T[:, :, 3] @ R.T + p
+    P = poses.astype(np.float64)
+    P2 = np.empty_like(P)
+    P2[..., :3] = np.einsum("ij,esjk->esik", R, P[..., :3])
+    P2[..., 3] = P[..., 3] @ R.T + p
+    sc2 = sg.Scene(sc.meshes, sc.env_off, sc.inst_asset, sc.inst_label, T2.astype(np.float32))
+    return sc2, P2.astype(np.float32)
+
+
+def test_rigid_invariance_exact_group():
+    """Scene + sensor moved by an FP32-exact rigid motion: identical outputs
+    within 1e-9 (north_star invariance pin)."""
+    sc, s = sg.config2(n_envs=3)
+    cam = dict(s["cam"], W=60, H=34, cx=30.0, cy=17.0)
+    a = cast_pinhole(sc, cam, s["poses"], oracle.RANGE)
+    rng = np.random.default_rng(9)
+    for _ in range(2):
+        R, p = _rigid_exact(rng)
+        sc2, P2 = _move(sc, s["poses"], R, p)
+        b = cast_pinhole(sc2, cam, P2, oracle.RANGE)
+        assert np.allclose(a.t64, b.t64, atol=1e-9, rtol=0)
+        ok = (a.amb == 0) & (b.amb == 0)
+        assert np.all(a.face[ok] == b.face[ok]) and np.all(a.seg[ok] == b.seg[ok])
+
+
+def test_rigid_invariance_generic():
+    """Generic rotation: equal within FP32 input rounding; seg/face equal away
+    from edges (graze > 1e-4) and ties."""
+    sc, s = sg.config2(n_envs=2)
+    cam = dict(s["cam"], W=60, H=34, cx=30.0, cy=17.0)
+    a = cast_pinhole(sc, cam, s["poses"], oracle.DEPTH, graze=True)
+    R = sg.random_rotation(np.random.default_rng(1))
+    sc2, P2 = _move(sc, s["poses"], R, np.asarray([0.7, -1.1, 0.3]))
+    b = cast_pinhole(sc2, cam, P2, oracle.DEPTH)
+    far_edge = (a.graze > 1e-4) & (a.amb == 0) & (b.amb == 0)
+    assert np.all(a.seg[far_edge] == b.seg[far_edge])
+    same = far_edge & (a.face == b.face)
+    assert np.allclose(a.t64[same], b.t64[same], atol=1e-4)
+
+
+def test_query_subset_equals_full():
+    """Sampled queries (any order) give the same per-ray answers as a full
+    cast -- the sampling used for full-size parity."""
+    sc, s = sg.config2(n_envs=4)
+    cam = dict(s["cam"], W=30, H=20, cx=15.0, cy=10.0)
+    full = cast_pinhole(sc, cam, s["poses"])
+    q = np.random.default_rng(0).choice(4 * 600, 300, replace=False)
+    sub = cast_pinhole(sc, cam, s["poses"], query=q)
+    assert np.array_equal(sub.t64, full.t64[q]) and np.array_equal(sub.face, full.face[q])
+    one = cast_pinhole(sc, cam, s["poses"], query=q, n_threads=1)
+    assert np.array_equal(one.t64, sub.t64)
