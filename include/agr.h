@@ -1,0 +1,251 @@
+/*
+ * agr.h -- C ABI of the B200-native batched ray caster (libagr.so).
+ *
+ * The hot path of the Aerial Gym Simulator renderer (arxiv 2503.01471,
+ * PAPER.md §III.D.1 "Exteroceptive Sensors", lines 226-228): per-environment
+ * meshes made of transformed sub-meshes, a bounding volume hierarchy over
+ * them, and rays "cast outwards per-pixel to evaluate intersection",
+ * reporting range (ToF / LiDAR) or depth (camera), segmentation and face
+ * index images (Fig. 3).
+ *
+ * Design: the paper's per-env merged mesh M_{i,t} = T o M^base
+ * is represented as instances of shared asset meshes.  Each asset gets a
+ * bottom-level BVH (BLAS, LBVH: 30-bit Morton codes, on-device radix sort,
+ * Karras hierarchy) built once at create; each environment gets a top-level
+ * BVH (TLAS) over its instances, rebuilt by agr_build or refit in place by
+ * agr_refit after agr_set_instance_transforms.  Casts are hand-written CUDA
+ * kernels for sm_100a; results equal the plain definition of DESIGN.md §3.
+ *
+ * Conventions (DESIGN.md §4 "Readings"):
+ *  - transforms are row-major float[3][4] T = [A | b], x' = A x + b
+ *    (object -> env-local for instances; sensor -> env-local for poses; the
+ *    columns of a pose's A are the sensor axes x forward, y left, z up);
+ *  - pinhole pixel (u, v) has its centre at (u + 0.5, v + 0.5), u to the
+ *    right (-y), v downward (-z); sensor-frame direction
+ *    d_s = (1, -(u + 0.5 - cx)/fx, -(v + 0.5 - cy)/fy);
+ *  - DEPTH reports t for d_s as written (= distance from the image plane);
+ *    RANGE and beams report t for the unit direction (= Euclidean range);
+ *  - a hit needs 0 < t <= max_range on a closed, double-sided triangle; the
+ *    smallest t wins, equal t goes to the lowest per-env face index;
+ *  - misses write max_range, seg -1, face -1;
+ *  - per-env face index = sum of face counts of the env's earlier instances
+ *    (creation order) + the asset-local face index; seg = instance label.
+ *
+ * Errors: every call returns agr_status.  Host-checkable argument errors
+ * return before any launch and leave the scene unchanged.  CUDA launch
+ * errors return AGR_ECUDA; asynchronous device faults surface at the
+ * caller's next synchronisation or at the next agr call.  No exceptions
+ * cross the ABI and the library never aborts.  agr_last_error() returns a
+ * thread-local message for the last failing call on this thread.
+ *
+ * Ownership: host arrays passed to agr_scene_create are copied before it
+ * returns.  Device buffers passed to set/cast calls are caller-owned and
+ * must stay alive until the work on `stream` completes; the library never
+ * frees them.  The library owns every BVH / instance buffer it allocates
+ * and frees them in agr_scene_destroy.  All device work is asynchronous on
+ * the caller's stream (a cudaStream_t passed as void*, NULL = legacy default
+ * stream) with no hidden synchronisation, except where a call says so.  One
+ * scene must be used by one stream at a time; different scenes may be used
+ * concurrently from different threads.
+ */
+#ifndef AGR_H
+#define AGR_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define AGR_ABI_VERSION 1
+
+typedef int32_t agr_status;
+enum {
+    AGR_OK = 0,
+    AGR_EINVAL = -1,       /* bad argument (null pointer, size, index)      */
+    AGR_ENOMEM = -2,       /* device or host allocation failed              */
+    AGR_ECUDA = -3,        /* CUDA runtime error (message in agr_last_error) */
+    AGR_ESTATE = -4,       /* call not valid in this state (e.g. no build)  */
+    AGR_EUNSUPPORTED = -5  /* a size beyond a documented limit              */
+};
+
+/* Documented limits. */
+#define AGR_MAX_INSTANCES_PER_ENV 1024 /* per-env TLAS is built in one CTA   */
+#define AGR_MAX_BVH_DEPTH 60           /* BLAS depth + TLAS depth + 1        */
+
+typedef struct agr_scene_s* agr_scene;
+
+/* One asset mesh (a sub-mesh M_j of PAPER.md:226), host memory. */
+typedef struct {
+    const float* verts;   /* [n_verts][3] object-space vertices (metres)    */
+    int32_t n_verts;      /* >= 3                                            */
+    const int32_t* faces; /* [n_faces][3] vertex indices in [0, n_verts)     */
+    int32_t n_faces;      /* >= 1; zero-area faces are kept for numbering
+                             and are never hit                               */
+} agr_mesh;
+
+/* One instance of an asset in an environment. */
+typedef struct {
+    int32_t asset;        /* index into the meshes array                     */
+    int32_t label;        /* segmentation id written for its hits (>= 0)     */
+} agr_instance;
+
+/* Pinhole intrinsics in pixels. */
+typedef struct {
+    int32_t width, height;
+    float fx, fy, cx, cy;
+} agr_pinhole;
+
+typedef enum { AGR_DEPTH = 0, AGR_RANGE = 1 } agr_distance;
+
+/* Output images.  Each pointer is caller-owned memory (device memory for
+ * the device casts, host memory for the *_host casts) laid out
+ * [n_envs][n_sensors][rows][cols] (pinhole rows = height, cols = width;
+ * beams rows = C channels, cols = K columns; rays: [n_envs][R]).  Any
+ * pointer may be NULL to skip that channel. */
+typedef struct {
+    float* dist;          /* depth / range (metres); max_range on a miss     */
+    int32_t* seg;         /* instance label, -1 on a miss                    */
+    int32_t* face;        /* per-env face index, -1 on a miss                */
+} agr_outputs;
+
+/* Scene statistics (sizes in elements / bytes of library-owned memory). */
+typedef struct {
+    int32_t n_assets, n_envs;
+    int64_t n_instances, n_blas_nodes, n_blas_tris, n_tlas_nodes;
+    int32_t blas_max_depth, tlas_max_depth;
+    int64_t device_bytes;
+    int32_t built;        /* 1 after the first agr_build                     */
+} agr_scene_info;
+
+int32_t agr_abi_version(void);
+
+/* Thread-local message describing the last failing call ("" if none). */
+const char* agr_last_error(void);
+
+/*
+ * Create a scene on CUDA device `device`: copies the asset meshes and the
+ * instance table, builds every BLAS (synchronous; returns when done).
+ *   env_offsets: host int64 [n_envs + 1], env e owns instances
+ *                [env_offsets[e], env_offsets[e+1]); env_offsets[0] == 0.
+ *   inst:        host [env_offsets[n_envs]] instance table.
+ * Instance transforms start as identity; call agr_set_instance_transforms
+ * and agr_build before the first cast.
+ * EINVAL: null pointers, n_meshes < 1, n_envs < 1, a face index out of
+ * range, a non-finite vertex, an asset index out of range, a negative
+ * label, non-monotone env_offsets.  EUNSUPPORTED: an env with more than
+ * AGR_MAX_INSTANCES_PER_ENV instances or a BLAS deeper than the traversal
+ * stack.  On error *out is set to NULL.
+ */
+agr_status agr_scene_create(int32_t device, const agr_mesh* meshes, int32_t n_meshes,
+                            int32_t n_envs, const int64_t* env_offsets,
+                            const agr_instance* inst, agr_scene* out);
+
+/* Free all device memory of the scene (synchronises its device). NULL: no-op. */
+agr_status agr_scene_destroy(agr_scene scene);
+
+agr_status agr_scene_get_info(agr_scene scene, agr_scene_info* info);
+
+/*
+ * Copy new instance transforms (device float [n_instances][3][4], row-major
+ * object -> env-local x' = A x + b; A must be invertible) into the scene
+ * and recompute the per-instance ray transforms and bounds.  Async on
+ * `stream`; T may be reused once the stream passes this point.  The TLAS is
+ * stale until agr_build or agr_refit.
+ */
+agr_status agr_set_instance_transforms(agr_scene scene, const float* T, void* stream);
+
+/* Full per-env TLAS rebuild (Morton order, Karras hierarchy, fit). Async. */
+agr_status agr_build(agr_scene scene, void* stream);
+
+/* In-place TLAS refit: keeps the topology of the last agr_build and
+ * recomputes all boxes bottom-up.  ESTATE before the first agr_build. */
+agr_status agr_refit(agr_scene scene, void* stream);
+
+/*
+ * Pinhole camera cast.  poses: device float
+ * [n_envs][n_sensors][3][4] (sensor -> env-local).  Outputs
+ * [n_envs][n_sensors][height][width].  max_range > 0 in the reported unit.
+ * ESTATE if transforms were set after the last build/refit.
+ */
+agr_status agr_cast_pinhole(agr_scene scene, const agr_pinhole* cam, agr_distance kind,
+                            const float* poses, int32_t n_sensors, float max_range,
+                            agr_outputs out, void* stream);
+
+/*
+ * Beam-table cast for LiDARs and other central projections (PAPER.md:215,
+ * :228 "customizable projection models (e.g., Dome LiDAR)").  dirs: device
+ * float [C][K][3] sensor-frame directions (normalised in FP64 by the
+ * library; need not be exactly unit).  Always reports range.  Outputs
+ * [n_envs][n_sensors][C][K].
+ */
+agr_status agr_cast_beams(agr_scene scene, const float* dirs, int32_t C, int32_t K,
+                          const float* poses, int32_t n_sensors, float max_range,
+                          agr_outputs out, void* stream);
+
+/*
+ * Explicit rays (test / debug entry, SPEC cast_rays): orig, dir device
+ * float [n_envs][R][3] in env-local coordinates; t is reported in units of
+ * |dir| (no normalisation).  Outputs [n_envs][R].
+ */
+agr_status agr_cast_rays(agr_scene scene, const float* orig, const float* dir, int32_t R,
+                         float max_range, agr_outputs out, void* stream);
+
+/*
+ * End-to-end pinhole cast through HOST buffers: copies `poses_host`
+ * (pageable or pinned host memory) to the device, casts, and copies the
+ * images back into the host pointers of `out_host`, pipelining the
+ * device->host copies with the casts of later env chunks on internal
+ * streams.  Synchronous: returns when out_host is filled.
+ */
+agr_status agr_cast_pinhole_host(agr_scene scene, const agr_pinhole* cam, agr_distance kind,
+                                 const float* poses_host, int32_t n_sensors, float max_range,
+                                 agr_outputs out_host);
+
+/* End-to-end beams cast through host buffers (see agr_cast_pinhole_host). */
+agr_status agr_cast_beams_host(agr_scene scene, const float* dirs_host, int32_t C, int32_t K,
+                               const float* poses_host, int32_t n_sensors, float max_range,
+                               agr_outputs out_host);
+
+/*
+ * Per-env order-independent 64-bit checksums of an output image set
+ * (device pointers as produced by a cast; NULL channels are skipped):
+ * sums[e] = sum over the env's elements of mix64(index, dist bits, seg,
+ * face).  sums: device uint64 [n_envs].  Used to compare runs bitwise
+ * across GPU counts without moving images.  Async.
+ */
+agr_status agr_checksum(agr_scene scene, agr_outputs out, int64_t elems_per_env,
+                        uint64_t* sums, void* stream);
+
+/*
+ * Numerics mode (test hook): 0 = FP32 filter + FP64 arbitration (default);
+ * 1 = exact mode, every leaf test in FP64 (slow; results must be identical).
+ */
+agr_status agr_set_exact_mode(agr_scene scene, int32_t exact);
+
+/*
+ * Counters of the last cast (test / profiling hook; device-side counters
+ * are collected only when enabled):  counters[0] rays, [1] internal nodes
+ * visited, [2] leaf (triangle) tests, [3] instance entries, [4] FP64
+ * arbitration tests, [5] rays that took the overflow slow path.
+ */
+agr_status agr_enable_counters(agr_scene scene, int32_t enable);
+agr_status agr_get_counters(agr_scene scene, int64_t counters[8]);
+
+/*
+ * Debug export of one asset's BLAS for structural tests (synchronous):
+ * nodes float [n_nodes][16] (packed 64-byte nodes), leaf_face int32
+ * [n_leaves] (asset-local face of each leaf in BVH order), morton uint32
+ * [n_leaves] (sorted codes).  Pass NULL to query sizes via *n_nodes and
+ * *n_leaves.  Node child refs: >= 0 node index relative to the asset's
+ * first node, < 0 leaf ~index relative to the asset's first leaf,
+ * INT32_MIN empty.
+ */
+agr_status agr_debug_export_blas(agr_scene scene, int32_t asset, float* nodes,
+                                 int32_t* leaf_face, uint32_t* morton,
+                                 int64_t* n_nodes, int64_t* n_leaves);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AGR_H */

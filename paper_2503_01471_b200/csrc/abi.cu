@@ -1,0 +1,759 @@
+// abi.cu -- the C ABI of libagr.so (include/agr.h) and the scene runtime
+// behind it: argument validation, device memory ownership, BLAS build at
+// create, TLAS build/refit, cast dispatch, the host-buffer end-to-end path
+// and debug/introspection hooks.  SURVEY.md §8(b) is the contract.
+#include "../../include/agr.h"
+#include "agr_internal.cuh"
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+using namespace agr;
+
+namespace {
+
+thread_local std::string g_err;
+
+agr_status fail(agr_status s, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+agr_status fail(agr_status s, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return s;
+}
+
+agr_status cuda_fail(cudaError_t e, const char* where) {
+    return fail(e == cudaErrorMemoryAllocation ? AGR_ENOMEM : AGR_ECUDA, "%s: %s", where,
+                cudaGetErrorString(e));
+}
+
+#define CK(call)                                            \
+    do {                                                    \
+        cudaError_t _e = (call);                            \
+        if (_e != cudaSuccess) return cuda_fail(_e, #call); \
+    } while (0)
+
+// Restores the caller's current device on scope exit.
+struct DeviceGuard {
+    int prev = -1;
+    bool ok = false;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        ok = cudaSetDevice(dev) == cudaSuccess;
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+}  // namespace
+
+struct agr_scene_s {
+    int device = 0;
+    int n_assets = 0, n_envs = 0;
+    int64_t n_inst = 0;
+    int nb_blas = 0, nt_tlas = 0, n_leaves_cap = 0, max_n = 0;
+    std::vector<AssetInfo> h_assets;
+    std::vector<int> h_env_off;
+    std::vector<int> h_tlas_off;
+    std::vector<void*> allocs;
+    size_t device_bytes = 0;
+    // device arrays
+    float4* nodes = nullptr;
+    float4* tris = nullptr;
+    float* triv = nullptr;
+    float4* irec = nullptr;
+    float* inst_T = nullptr;
+    float* inst_box = nullptr;
+    int* inst_asset = nullptr;
+    int* inst_label = nullptr;
+    int* inst_face_off = nullptr;
+    int* env_off = nullptr;
+    int* tlas_off = nullptr;
+    int* tlas_root = nullptr;
+    int* tlas_child = nullptr;
+    int* tlas_inst_parent = nullptr;
+    int* tlas_node_parent = nullptr;
+    int* tlas_depth = nullptr;
+    AssetInfo* assets = nullptr;
+    uint32_t* morton = nullptr;  // sorted BLAS Morton codes (debug export)
+    unsigned long long* counters = nullptr;
+    bool built = false, dirty = false;
+    int exact = 0;
+    bool counting = false;
+    // end-to-end staging (lazily allocated)
+    cudaStream_t e2e_stream[2] = {nullptr, nullptr};
+    cudaEvent_t e2e_event[4] = {nullptr, nullptr, nullptr, nullptr};
+    float* e2e_poses = nullptr;
+    size_t e2e_poses_bytes = 0;
+    void* e2e_out[2] = {nullptr, nullptr};
+    size_t e2e_out_bytes = 0;
+    void* e2e_host[2] = {nullptr, nullptr};
+    size_t e2e_host_bytes = 0;
+    float* e2e_beams = nullptr;
+    size_t e2e_beams_bytes = 0;
+
+    template <class T>
+    cudaError_t alloc(T** p, size_t n) {
+        size_t bytes = sizeof(T) * (n > 0 ? n : 1);
+        cudaError_t e = cudaMalloc((void**)p, bytes);
+        if (e == cudaSuccess) {
+            allocs.push_back(*p);
+            device_bytes += bytes;
+        }
+        return e;
+    }
+
+    SceneView view() const {
+        SceneView v;
+        v.nodes = nodes;
+        v.tris = tris;
+        v.triv = triv;
+        v.irec = irec;
+        v.inst_T = inst_T;
+        v.inst_face_off = inst_face_off;
+        v.inst_label = inst_label;
+        v.env_off = env_off;
+        v.tlas_root = tlas_root;
+        v.inst_asset = inst_asset;
+        v.assets = assets;
+        v.n_envs = n_envs;
+        return v;
+    }
+
+    TlasArgs tlas_args() const {
+        TlasArgs a;
+        a.nodes = nodes;
+        a.irec = irec;
+        a.inst_box = inst_box;
+        a.inst_T = inst_T;
+        a.inst_asset = inst_asset;
+        a.assets = assets;
+        a.env_off = env_off;
+        a.tlas_off = tlas_off;
+        a.nb_blas = nb_blas;
+        a.tlas_child = tlas_child;
+        a.tlas_inst_parent = tlas_inst_parent;
+        a.tlas_node_parent = tlas_node_parent;
+        a.tlas_depth = tlas_depth;
+        a.n_envs = n_envs;
+        a.max_n = max_n;
+        return a;
+    }
+
+    void release() {
+        for (void* p : allocs) cudaFree(p);
+        allocs.clear();
+        for (auto& s : e2e_stream)
+            if (s) cudaStreamDestroy(s);
+        for (auto& e : e2e_event)
+            if (e) cudaEventDestroy(e);
+        for (auto& h : e2e_host)
+            if (h) cudaFreeHost(h);
+        if (e2e_poses) cudaFree(e2e_poses);
+        if (e2e_beams) cudaFree(e2e_beams);
+        for (auto& o : e2e_out)
+            if (o) cudaFree(o);
+    }
+};
+
+extern "C" {
+
+int32_t agr_abi_version(void) { return AGR_ABI_VERSION; }
+
+const char* agr_last_error(void) { return g_err.c_str(); }
+
+agr_status agr_scene_create(int32_t device, const agr_mesh* meshes, int32_t n_meshes, int32_t n_envs,
+                            const int64_t* env_offsets, const agr_instance* inst, agr_scene* out) {
+    g_err.clear();
+    if (!out) return fail(AGR_EINVAL, "out is NULL");
+    *out = nullptr;
+    if (!meshes || n_meshes < 1) return fail(AGR_EINVAL, "need at least one mesh");
+    if (n_envs < 1 || !env_offsets) return fail(AGR_EINVAL, "need n_envs >= 1 and env_offsets");
+    if (env_offsets[0] != 0) return fail(AGR_EINVAL, "env_offsets[0] must be 0");
+    for (int e = 0; e < n_envs; ++e) {
+        if (env_offsets[e + 1] < env_offsets[e]) return fail(AGR_EINVAL, "env_offsets not monotone at %d", e);
+        if (env_offsets[e + 1] - env_offsets[e] > AGR_MAX_INSTANCES_PER_ENV)
+            return fail(AGR_EUNSUPPORTED, "env %d has %lld instances (limit %d)", e,
+                        (long long)(env_offsets[e + 1] - env_offsets[e]), AGR_MAX_INSTANCES_PER_ENV);
+    }
+    const int64_t n_inst = env_offsets[n_envs];
+    if (n_inst > 0x3FFFFFFF) return fail(AGR_EUNSUPPORTED, "too many instances");
+    if (n_inst > 0 && !inst) return fail(AGR_EINVAL, "inst is NULL");
+    int64_t faces_total = 0, verts_total = 0;
+    for (int a = 0; a < n_meshes; ++a) {
+        const agr_mesh& m = meshes[a];
+        if (!m.verts || !m.faces || m.n_verts < 3 || m.n_faces < 1)
+            return fail(AGR_EINVAL, "mesh %d: need verts, faces, n_verts >= 3, n_faces >= 1", a);
+        for (int64_t k = 0; k < 3LL * m.n_verts; ++k)
+            if (!std::isfinite(m.verts[k])) return fail(AGR_EINVAL, "mesh %d: non-finite vertex", a);
+        for (int64_t k = 0; k < 3LL * m.n_faces; ++k)
+            if (m.faces[k] < 0 || m.faces[k] >= m.n_verts)
+                return fail(AGR_EINVAL, "mesh %d: face index %d out of range", a, m.faces[k]);
+        faces_total += m.n_faces;
+        verts_total += m.n_verts;
+    }
+    if (faces_total > 0x3FFFFFFF) return fail(AGR_EUNSUPPORTED, "too many faces");
+    for (int64_t j = 0; j < n_inst; ++j) {
+        if (inst[j].asset < 0 || inst[j].asset >= n_meshes)
+            return fail(AGR_EINVAL, "instance %lld: asset %d out of range", (long long)j, inst[j].asset);
+        if (inst[j].label < 0) return fail(AGR_EINVAL, "instance %lld: negative label", (long long)j);
+    }
+    int dev_count = 0;
+    if (cudaGetDeviceCount(&dev_count) != cudaSuccess || device < 0 || device >= dev_count)
+        return fail(AGR_EINVAL, "device %d not available (%d CUDA devices)", device, dev_count);
+    DeviceGuard guard(device);
+    if (!guard.ok) return fail(AGR_ECUDA, "cudaSetDevice(%d) failed", device);
+
+    agr_scene_s* s = new agr_scene_s();
+    s->device = device;
+    s->n_assets = n_meshes;
+    s->n_envs = n_envs;
+    s->n_inst = n_inst;
+    // host-side layout
+    std::vector<int> node_base(n_meshes), leaf_base(n_meshes);
+    int nb = 0, nl = 0;
+    for (int a = 0; a < n_meshes; ++a) {
+        node_base[a] = nb;
+        leaf_base[a] = nl;
+        nb += meshes[a].n_faces > 1 ? meshes[a].n_faces - 1 : 1;
+        nl += meshes[a].n_faces;
+    }
+    s->nb_blas = nb;
+    s->n_leaves_cap = nl;
+    s->h_env_off.resize(n_envs + 1);
+    s->h_tlas_off.resize(n_envs);
+    int nt = 0, max_n = 0;
+    for (int e = 0; e < n_envs; ++e) {
+        int n = (int)(env_offsets[e + 1] - env_offsets[e]);
+        s->h_env_off[e] = (int)env_offsets[e];
+        s->h_tlas_off[e] = nt;
+        nt += n > 1 ? n - 1 : 1;
+        max_n = n > max_n ? n : max_n;
+    }
+    s->h_env_off[n_envs] = (int)n_inst;
+    s->nt_tlas = nt;
+    s->max_n = max_n;
+    std::vector<int> h_asset(n_inst), h_label(n_inst), h_face_off(n_inst), h_root(n_envs);
+    for (int e = 0; e < n_envs; ++e) {
+        int off = 0;
+        for (int64_t j = env_offsets[e]; j < env_offsets[e + 1]; ++j) {
+            h_asset[j] = inst[j].asset;
+            h_label[j] = inst[j].label;
+            h_face_off[j] = off;
+            off += meshes[inst[j].asset].n_faces;
+        }
+        h_root[e] = nb + s->h_tlas_off[e];
+    }
+
+    auto bail = [&](agr_status st) {
+        s->release();
+        delete s;
+        return st;
+    };
+#define CKB(call)                                                    \
+    do {                                                             \
+        cudaError_t _e = (call);                                     \
+        if (_e != cudaSuccess) return bail(cuda_fail(_e, #call));    \
+    } while (0)
+
+    CKB(s->alloc(&s->nodes, 4 * (size_t)(nb + nt)));
+    CKB(s->alloc(&s->tris, 3 * (size_t)nl));
+    CKB(s->alloc(&s->triv, 9 * (size_t)nl));
+    CKB(s->alloc(&s->irec, 4 * (size_t)n_inst));
+    CKB(s->alloc(&s->inst_T, 12 * (size_t)n_inst));
+    CKB(s->alloc(&s->inst_box, 6 * (size_t)n_inst));
+    CKB(s->alloc(&s->inst_asset, (size_t)n_inst));
+    CKB(s->alloc(&s->inst_label, (size_t)n_inst));
+    CKB(s->alloc(&s->inst_face_off, (size_t)n_inst));
+    CKB(s->alloc(&s->env_off, (size_t)n_envs + 1));
+    CKB(s->alloc(&s->tlas_off, (size_t)n_envs));
+    CKB(s->alloc(&s->tlas_root, (size_t)n_envs));
+    CKB(s->alloc(&s->tlas_child, 2 * (size_t)nt));
+    CKB(s->alloc(&s->tlas_inst_parent, (size_t)n_inst));
+    CKB(s->alloc(&s->tlas_node_parent, (size_t)nt));
+    CKB(s->alloc(&s->tlas_depth, (size_t)n_envs));
+    CKB(s->alloc(&s->assets, (size_t)n_meshes));
+    CKB(s->alloc(&s->morton, (size_t)nl));
+    CKB(s->alloc(&s->counters, 8));
+    CKB(cudaMemset(s->morton, 0xFF, sizeof(uint32_t) * (size_t)nl));
+    CKB(cudaMemset(s->tris, 0, sizeof(float4) * 3 * (size_t)nl));
+    CKB(cudaMemcpy(s->inst_asset, h_asset.data(), sizeof(int) * n_inst, cudaMemcpyHostToDevice));
+    CKB(cudaMemcpy(s->inst_label, h_label.data(), sizeof(int) * n_inst, cudaMemcpyHostToDevice));
+    CKB(cudaMemcpy(s->inst_face_off, h_face_off.data(), sizeof(int) * n_inst, cudaMemcpyHostToDevice));
+    CKB(cudaMemcpy(s->env_off, s->h_env_off.data(), sizeof(int) * (n_envs + 1), cudaMemcpyHostToDevice));
+    CKB(cudaMemcpy(s->tlas_off, s->h_tlas_off.data(), sizeof(int) * n_envs, cudaMemcpyHostToDevice));
+    CKB(cudaMemcpy(s->tlas_root, h_root.data(), sizeof(int) * n_envs, cudaMemcpyHostToDevice));
+
+    // BLAS build, one asset at a time on a private stream
+    cudaStream_t st;
+    CKB(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    size_t scratch_bytes = 0;
+    int maxF = 0, maxV = 0;
+    for (int a = 0; a < n_meshes; ++a) {
+        size_t b = blas_scratch_bytes(meshes[a].n_faces);
+        scratch_bytes = b > scratch_bytes ? b : scratch_bytes;
+        maxF = meshes[a].n_faces > maxF ? meshes[a].n_faces : maxF;
+        maxV = meshes[a].n_verts > maxV ? meshes[a].n_verts : maxV;
+    }
+    void* scratch = nullptr;
+    float* dverts = nullptr;
+    int* dfaces = nullptr;
+    cudaError_t err = cudaMalloc(&scratch, scratch_bytes);
+    if (err == cudaSuccess) err = cudaMalloc(&dverts, sizeof(float) * 3 * (size_t)maxV);
+    if (err == cudaSuccess) err = cudaMalloc(&dfaces, sizeof(int) * 3 * (size_t)maxF);
+    for (int a = 0; a < n_meshes && err == cudaSuccess; ++a) {
+        err = cudaMemcpyAsync(dverts, meshes[a].verts, sizeof(float) * 3 * meshes[a].n_verts,
+                              cudaMemcpyHostToDevice, st);
+        if (err != cudaSuccess) break;
+        err = cudaMemcpyAsync(dfaces, meshes[a].faces, sizeof(int) * 3 * meshes[a].n_faces,
+                              cudaMemcpyHostToDevice, st);
+        if (err != cudaSuccess) break;
+        BlasBuildArgs ba;
+        ba.verts = dverts;
+        ba.faces = dfaces;
+        ba.n_verts = meshes[a].n_verts;
+        ba.n_faces = meshes[a].n_faces;
+        ba.node_base = node_base[a];
+        ba.leaf_base = leaf_base[a];
+        ba.nodes = s->nodes;
+        ba.tris = s->tris;
+        ba.triv = s->triv;
+        ba.info_dev = s->assets + a;
+        ba.dbg_morton = s->morton + leaf_base[a];
+        int n_leaves = 0;
+        err = blas_build(ba, scratch, &n_leaves, st);
+        if (err == cudaSuccess) err = cudaStreamSynchronize(st);
+    }
+    if (err == cudaSuccess) err = cudaStreamSynchronize(st);
+    cudaFree(scratch);
+    cudaFree(dverts);
+    cudaFree(dfaces);
+    if (err != cudaSuccess) {
+        cudaStreamDestroy(st);
+        return bail(cuda_fail(err, "BLAS build"));
+    }
+    s->h_assets.resize(n_meshes);
+    CKB(cudaMemcpy(s->h_assets.data(), s->assets, sizeof(AssetInfo) * n_meshes, cudaMemcpyDeviceToHost));
+    int max_depth = 0;
+    for (auto& a : s->h_assets) max_depth = a.depth > max_depth ? a.depth : max_depth;
+    // identity transforms until the caller sets them
+    {
+        std::vector<float> I(12 * (size_t)n_inst, 0.0f);
+        for (int64_t j = 0; j < n_inst; ++j) I[12 * j + 0] = I[12 * j + 5] = I[12 * j + 10] = 1.0f;
+        CKB(cudaMemcpy(s->inst_T, I.data(), sizeof(float) * I.size(), cudaMemcpyHostToDevice));
+    }
+    err = instances_update(s->tlas_args(), (int)n_inst, st);
+    if (err == cudaSuccess) err = cudaStreamSynchronize(st);
+    cudaStreamDestroy(st);
+    if (err != cudaSuccess) return bail(cuda_fail(err, "instances_update"));
+    if (max_depth + 2 > STACK_SIZE)
+        return bail(fail(AGR_EUNSUPPORTED, "BLAS depth %d exceeds the traversal stack", max_depth));
+#undef CKB
+    *out = s;
+    return AGR_OK;
+}
+
+agr_status agr_scene_destroy(agr_scene s) {
+    g_err.clear();
+    if (!s) return AGR_OK;
+    DeviceGuard guard(s->device);
+    cudaDeviceSynchronize();
+    s->release();
+    delete s;
+    return AGR_OK;
+}
+
+agr_status agr_scene_get_info(agr_scene s, agr_scene_info* info) {
+    g_err.clear();
+    if (!s || !info) return fail(AGR_EINVAL, "NULL argument");
+    DeviceGuard guard(s->device);
+    info->n_assets = s->n_assets;
+    info->n_envs = s->n_envs;
+    info->n_instances = s->n_inst;
+    info->n_blas_nodes = s->nb_blas;
+    int64_t leaves = 0;
+    int bd = 0;
+    for (auto& a : s->h_assets) {
+        leaves += a.n_leaves;
+        bd = a.depth > bd ? a.depth : bd;
+    }
+    info->n_blas_tris = leaves;
+    info->n_tlas_nodes = s->nt_tlas;
+    info->blas_max_depth = bd;
+    info->tlas_max_depth = 0;
+    if (s->built) {
+        std::vector<int> d(s->n_envs);
+        CK(cudaMemcpy(d.data(), s->tlas_depth, sizeof(int) * s->n_envs, cudaMemcpyDeviceToHost));
+        for (int x : d) info->tlas_max_depth = x > info->tlas_max_depth ? x : info->tlas_max_depth;
+    }
+    info->device_bytes = (int64_t)s->device_bytes;
+    info->built = s->built ? 1 : 0;
+    return AGR_OK;
+}
+
+agr_status agr_set_instance_transforms(agr_scene s, const float* T, void* stream) {
+    g_err.clear();
+    if (!s) return fail(AGR_EINVAL, "scene is NULL");
+    if (s->n_inst == 0) return AGR_OK;
+    if (!T) return fail(AGR_EINVAL, "T is NULL");
+    DeviceGuard guard(s->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    CK(cudaMemcpyAsync(s->inst_T, T, sizeof(float) * 12 * s->n_inst, cudaMemcpyDeviceToDevice, st));
+    CK(instances_update(s->tlas_args(), (int)s->n_inst, st));
+    s->dirty = true;
+    return AGR_OK;
+}
+
+agr_status agr_build(agr_scene s, void* stream) {
+    g_err.clear();
+    if (!s) return fail(AGR_EINVAL, "scene is NULL");
+    DeviceGuard guard(s->device);
+    CK(tlas_build(s->tlas_args(), true, (cudaStream_t)stream));
+    s->built = true;
+    s->dirty = false;
+    return AGR_OK;
+}
+
+agr_status agr_refit(agr_scene s, void* stream) {
+    g_err.clear();
+    if (!s) return fail(AGR_EINVAL, "scene is NULL");
+    if (!s->built) return fail(AGR_ESTATE, "agr_refit before the first agr_build");
+    DeviceGuard guard(s->device);
+    CK(tlas_build(s->tlas_args(), false, (cudaStream_t)stream));
+    s->dirty = false;
+    return AGR_OK;
+}
+
+static agr_status check_cast_state(agr_scene s, float max_range) {
+    if (!s) return fail(AGR_EINVAL, "scene is NULL");
+    if (!s->built) return fail(AGR_ESTATE, "cast before the first agr_build");
+    if (s->dirty) return fail(AGR_ESTATE, "transforms changed since the last agr_build/agr_refit");
+    if (!(max_range > 0.0f) || !std::isfinite(max_range)) return fail(AGR_EINVAL, "max_range must be > 0");
+    return AGR_OK;
+}
+
+static agr_status run_cast(agr_scene s, CastArgs& a, cudaStream_t st) {
+    a.sv = s->view();
+    a.exact = s->exact;
+    a.counters = nullptr;
+    if (s->counting) {
+        CK(cudaMemsetAsync(s->counters, 0, sizeof(unsigned long long) * 8, st));
+        a.counters = s->counters;
+    }
+    CK(cast_launch(a, st));
+    return AGR_OK;
+}
+
+static CastArgs base_args(agr_scene s, float max_range, agr_outputs out) {
+    CastArgs a;
+    memset(&a, 0, sizeof a);
+    a.max_range = max_range;
+    a.out_dist = out.dist;
+    a.out_seg = out.seg;
+    a.out_face = out.face;
+    a.env_begin = 0;
+    a.env_end = s->n_envs;
+    a.S = 1;
+    return a;
+}
+
+agr_status agr_cast_pinhole(agr_scene s, const agr_pinhole* cam, agr_distance kind, const float* poses,
+                            int32_t n_sensors, float max_range, agr_outputs out, void* stream) {
+    g_err.clear();
+    agr_status st = check_cast_state(s, max_range);
+    if (st != AGR_OK) return st;
+    if (!cam || !poses || n_sensors < 1) return fail(AGR_EINVAL, "need cam, poses and n_sensors >= 1");
+    if (cam->width < 1 || cam->height < 1 || !(cam->fx > 0.0f) || !(cam->fy > 0.0f))
+        return fail(AGR_EINVAL, "bad pinhole intrinsics");
+    if (kind != AGR_DEPTH && kind != AGR_RANGE) return fail(AGR_EINVAL, "bad distance kind");
+    DeviceGuard guard(s->device);
+    CastArgs a = base_args(s, max_range, out);
+    a.model = 1;
+    a.kind = (int)kind;
+    a.W = cam->width;
+    a.H = cam->height;
+    a.fx = cam->fx;
+    a.fy = cam->fy;
+    a.cx = cam->cx;
+    a.cy = cam->cy;
+    a.poses = poses;
+    a.S = n_sensors;
+    return run_cast(s, a, (cudaStream_t)stream);
+}
+
+agr_status agr_cast_beams(agr_scene s, const float* dirs, int32_t C, int32_t K, const float* poses,
+                          int32_t n_sensors, float max_range, agr_outputs out, void* stream) {
+    g_err.clear();
+    agr_status st = check_cast_state(s, max_range);
+    if (st != AGR_OK) return st;
+    if (!dirs || !poses || C < 1 || K < 1 || n_sensors < 1)
+        return fail(AGR_EINVAL, "need dirs, poses, C, K, n_sensors >= 1");
+    DeviceGuard guard(s->device);
+    CastArgs a = base_args(s, max_range, out);
+    a.model = 2;
+    a.W = K;
+    a.H = C;
+    a.beams = dirs;
+    a.poses = poses;
+    a.S = n_sensors;
+    return run_cast(s, a, (cudaStream_t)stream);
+}
+
+agr_status agr_cast_rays(agr_scene s, const float* orig, const float* dir, int32_t R, float max_range,
+                         agr_outputs out, void* stream) {
+    g_err.clear();
+    agr_status st = check_cast_state(s, max_range);
+    if (st != AGR_OK) return st;
+    if (!orig || !dir || R < 1) return fail(AGR_EINVAL, "need orig, dir and R >= 1");
+    DeviceGuard guard(s->device);
+    CastArgs a = base_args(s, max_range, out);
+    a.model = 0;
+    a.orig = orig;
+    a.dir = dir;
+    a.R = R;
+    return run_cast(s, a, (cudaStream_t)stream);
+}
+
+// ---- end-to-end casts through host buffers ---------------------------------------
+static agr_status e2e_prepare(agr_scene s, size_t pose_bytes, size_t chunk_out_bytes) {
+    if (!s->e2e_stream[0]) {
+        for (auto& x : s->e2e_stream) CK(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
+        for (auto& x : s->e2e_event) CK(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+    }
+    if (pose_bytes > s->e2e_poses_bytes) {
+        if (s->e2e_poses) cudaFree(s->e2e_poses);
+        s->e2e_poses = nullptr;
+        CK(cudaMalloc(&s->e2e_poses, pose_bytes));
+        s->e2e_poses_bytes = pose_bytes;
+    }
+    if (chunk_out_bytes > s->e2e_out_bytes) {
+        for (auto& o : s->e2e_out) {
+            if (o) cudaFree(o);
+            o = nullptr;
+            CK(cudaMalloc(&o, chunk_out_bytes));
+        }
+        s->e2e_out_bytes = chunk_out_bytes;
+    }
+    return AGR_OK;
+}
+
+static bool is_pinned(const void* p) {
+    if (!p) return true;
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeHost;
+}
+
+// Casts env chunks into a double-buffered device area and streams each chunk
+// back to the host while the next one is traced.
+static agr_status e2e_run(agr_scene s, CastArgs& a, int64_t elems_per_env, agr_outputs out_host) {
+    const int E = s->n_envs;
+    const int64_t bytes_per_env = elems_per_env * ((out_host.dist ? 4 : 0) + (out_host.seg ? 4 : 0) +
+                                                   (out_host.face ? 4 : 0));
+    // ~8 chunks, at least 1 env each
+    int chunk = (E + 7) / 8;
+    if (chunk < 1) chunk = 1;
+    size_t chunk_bytes = (size_t)(chunk * bytes_per_env);
+    agr_status st = e2e_prepare(s, a.S * 12 * sizeof(float) * (size_t)E, chunk_bytes);
+    if (st != AGR_OK) return st;
+    const bool direct = is_pinned(out_host.dist) && is_pinned(out_host.seg) && is_pinned(out_host.face);
+    if (!direct && chunk_bytes > s->e2e_host_bytes) {
+        for (auto& h : s->e2e_host) {
+            if (h) cudaFreeHost(h);
+            h = nullptr;
+            CK(cudaMallocHost(&h, chunk_bytes));
+        }
+        s->e2e_host_bytes = chunk_bytes;
+    }
+    cudaStream_t cs = s->e2e_stream[0], xs = s->e2e_stream[1];
+    int k = 0;
+    for (int e0 = 0; e0 < E; e0 += chunk, ++k) {
+        int e1 = e0 + chunk < E ? e0 + chunk : E;
+        int slot = k & 1;
+        if (k >= 2) CK(cudaStreamWaitEvent(cs, s->e2e_event[2 + slot], 0));  // slot drained
+        char* base = (char*)s->e2e_out[slot];
+        int64_t n = (int64_t)(e1 - e0) * elems_per_env;
+        CastArgs c = a;
+        c.env_begin = e0;
+        c.env_end = e1;
+        // the chunk's outputs start at env e0 of the chunk buffer
+        c.out_env_base = e0;
+        char* p = base;
+        if (out_host.dist) { c.out_dist = (float*)p; p += 4 * n; }
+        if (out_host.seg) { c.out_seg = (int*)p; p += 4 * n; }
+        if (out_host.face) { c.out_face = (int*)p; p += 4 * n; }
+        c.sv = s->view();
+        c.exact = s->exact;
+        c.counters = nullptr;
+        CK(cast_launch(c, cs));
+        CK(cudaEventRecord(s->e2e_event[slot], cs));
+        CK(cudaStreamWaitEvent(xs, s->e2e_event[slot], 0));
+        p = base;
+        const int64_t off = (int64_t)e0 * elems_per_env;
+        if (direct) {
+            if (out_host.dist) { CK(cudaMemcpyAsync(out_host.dist + off, p, 4 * n, cudaMemcpyDeviceToHost, xs)); p += 4 * n; }
+            if (out_host.seg) { CK(cudaMemcpyAsync(out_host.seg + off, p, 4 * n, cudaMemcpyDeviceToHost, xs)); p += 4 * n; }
+            if (out_host.face) { CK(cudaMemcpyAsync(out_host.face + off, p, 4 * n, cudaMemcpyDeviceToHost, xs)); p += 4 * n; }
+            CK(cudaEventRecord(s->e2e_event[2 + slot], xs));
+        } else {
+            const size_t chunk_n_bytes =
+                (size_t)((out_host.dist ? 4 : 0) + (out_host.seg ? 4 : 0) + (out_host.face ? 4 : 0)) * n;
+            CK(cudaMemcpyAsync(s->e2e_host[slot], base, chunk_n_bytes, cudaMemcpyDeviceToHost, xs));
+            CK(cudaEventRecord(s->e2e_event[2 + slot], xs));
+            CK(cudaEventSynchronize(s->e2e_event[2 + slot]));
+            char* h = (char*)s->e2e_host[slot];
+            if (out_host.dist) { memcpy(out_host.dist + off, h, 4 * n); h += 4 * n; }
+            if (out_host.seg) { memcpy(out_host.seg + off, h, 4 * n); h += 4 * n; }
+            if (out_host.face) { memcpy(out_host.face + off, h, 4 * n); h += 4 * n; }
+        }
+    }
+    CK(cudaStreamSynchronize(xs));
+    CK(cudaStreamSynchronize(cs));
+    return AGR_OK;
+}
+
+agr_status agr_cast_pinhole_host(agr_scene s, const agr_pinhole* cam, agr_distance kind,
+                                 const float* poses_host, int32_t n_sensors, float max_range,
+                                 agr_outputs out_host) {
+    g_err.clear();
+    agr_status st = check_cast_state(s, max_range);
+    if (st != AGR_OK) return st;
+    if (!cam || !poses_host || n_sensors < 1) return fail(AGR_EINVAL, "need cam, poses and n_sensors >= 1");
+    if (cam->width < 1 || cam->height < 1 || !(cam->fx > 0.0f) || !(cam->fy > 0.0f))
+        return fail(AGR_EINVAL, "bad pinhole intrinsics");
+    DeviceGuard guard(s->device);
+    st = e2e_prepare(s, sizeof(float) * 12 * (size_t)n_sensors * s->n_envs, 0);
+    if (st != AGR_OK) return st;
+    CK(cudaMemcpyAsync(s->e2e_poses, poses_host, sizeof(float) * 12 * (size_t)n_sensors * s->n_envs,
+                       cudaMemcpyHostToDevice, s->e2e_stream[0]));
+    CastArgs a = base_args(s, max_range, agr_outputs{nullptr, nullptr, nullptr});
+    a.model = 1;
+    a.kind = (int)kind;
+    a.W = cam->width;
+    a.H = cam->height;
+    a.fx = cam->fx;
+    a.fy = cam->fy;
+    a.cx = cam->cx;
+    a.cy = cam->cy;
+    a.poses = s->e2e_poses;
+    a.S = n_sensors;
+    return e2e_run(s, a, (int64_t)n_sensors * cam->width * cam->height, out_host);
+}
+
+agr_status agr_cast_beams_host(agr_scene s, const float* dirs_host, int32_t C, int32_t K,
+                               const float* poses_host, int32_t n_sensors, float max_range,
+                               agr_outputs out_host) {
+    g_err.clear();
+    agr_status st = check_cast_state(s, max_range);
+    if (st != AGR_OK) return st;
+    if (!dirs_host || !poses_host || C < 1 || K < 1 || n_sensors < 1)
+        return fail(AGR_EINVAL, "need dirs, poses, C, K, n_sensors >= 1");
+    DeviceGuard guard(s->device);
+    st = e2e_prepare(s, sizeof(float) * 12 * (size_t)n_sensors * s->n_envs, 0);
+    if (st != AGR_OK) return st;
+    size_t bb = sizeof(float) * 3 * (size_t)C * K;
+    if (bb > s->e2e_beams_bytes) {
+        if (s->e2e_beams) cudaFree(s->e2e_beams);
+        s->e2e_beams = nullptr;
+        CK(cudaMalloc(&s->e2e_beams, bb));
+        s->e2e_beams_bytes = bb;
+    }
+    CK(cudaMemcpyAsync(s->e2e_beams, dirs_host, bb, cudaMemcpyHostToDevice, s->e2e_stream[0]));
+    CK(cudaMemcpyAsync(s->e2e_poses, poses_host, sizeof(float) * 12 * (size_t)n_sensors * s->n_envs,
+                       cudaMemcpyHostToDevice, s->e2e_stream[0]));
+    CastArgs a = base_args(s, max_range, agr_outputs{nullptr, nullptr, nullptr});
+    a.model = 2;
+    a.W = K;
+    a.H = C;
+    a.beams = s->e2e_beams;
+    a.poses = s->e2e_poses;
+    a.S = n_sensors;
+    return e2e_run(s, a, (int64_t)n_sensors * C * K, out_host);
+}
+
+agr_status agr_checksum(agr_scene s, agr_outputs out, int64_t elems_per_env, uint64_t* sums, void* stream) {
+    g_err.clear();
+    if (!s || !sums || elems_per_env < 0) return fail(AGR_EINVAL, "bad argument");
+    DeviceGuard guard(s->device);
+    CK(checksum_launch(out.dist, out.seg, out.face, elems_per_env, s->n_envs,
+                       (unsigned long long*)sums, (cudaStream_t)stream));
+    return AGR_OK;
+}
+
+agr_status agr_set_exact_mode(agr_scene s, int32_t exact) {
+    g_err.clear();
+    if (!s) return fail(AGR_EINVAL, "scene is NULL");
+    s->exact = exact ? 1 : 0;
+    return AGR_OK;
+}
+
+agr_status agr_enable_counters(agr_scene s, int32_t enable) {
+    g_err.clear();
+    if (!s) return fail(AGR_EINVAL, "scene is NULL");
+    s->counting = enable != 0;
+    return AGR_OK;
+}
+
+agr_status agr_get_counters(agr_scene s, int64_t counters[8]) {
+    g_err.clear();
+    if (!s || !counters) return fail(AGR_EINVAL, "bad argument");
+    DeviceGuard guard(s->device);
+    unsigned long long c[8];
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(c, s->counters, sizeof c, cudaMemcpyDeviceToHost));
+    for (int k = 0; k < 8; ++k) counters[k] = (int64_t)c[k];
+    return AGR_OK;
+}
+
+agr_status agr_debug_export_blas(agr_scene s, int32_t asset, float* nodes, int32_t* leaf_face,
+                                 uint32_t* morton, int64_t* n_nodes, int64_t* n_leaves) {
+    g_err.clear();
+    if (!s || !n_nodes || !n_leaves) return fail(AGR_EINVAL, "bad argument");
+    if (asset < 0 || asset >= s->n_assets) return fail(AGR_EINVAL, "asset out of range");
+    DeviceGuard guard(s->device);
+    const AssetInfo& a = s->h_assets[asset];
+    int64_t nn = a.n_leaves > 1 ? a.n_leaves - 1 : 1;
+    *n_nodes = nn;
+    *n_leaves = a.n_leaves;
+    if (!nodes && !leaf_face && !morton) return AGR_OK;
+    CK(cudaDeviceSynchronize());
+    if (nodes) {
+        std::vector<float4> h(4 * nn);
+        CK(cudaMemcpy(h.data(), s->nodes + 4 * (size_t)a.node_base, sizeof(float4) * 4 * nn,
+                      cudaMemcpyDeviceToHost));
+        for (int64_t i = 0; i < nn; ++i) {
+            memcpy(nodes + 16 * i, &h[4 * i], 64);
+            // make child refs asset-relative
+            int* ref = (int*)(nodes + 16 * i + 12);
+            for (int c = 0; c < 2; ++c) {
+                if (ref[c] == REF_EMPTY) continue;
+                ref[c] = ref[c] >= 0 ? ref[c] - a.node_base : ~(~ref[c] - a.leaf_base);
+            }
+        }
+    }
+    if (leaf_face && a.n_leaves > 0) {
+        std::vector<float4> h(3 * (size_t)a.n_leaves);
+        CK(cudaMemcpy(h.data(), s->tris + 3 * (size_t)a.leaf_base, sizeof(float4) * 3 * a.n_leaves,
+                      cudaMemcpyDeviceToHost));
+        for (int i = 0; i < a.n_leaves; ++i) {
+            float w = h[3 * i + 2].w;
+            memcpy(&leaf_face[i], &w, 4);
+        }
+    }
+    if (morton && a.n_leaves > 0)
+        CK(cudaMemcpy(morton, s->morton + a.leaf_base, sizeof(uint32_t) * a.n_leaves, cudaMemcpyDeviceToHost));
+    return AGR_OK;
+}
+
+}  // extern "C"

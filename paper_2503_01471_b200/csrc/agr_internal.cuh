@@ -1,0 +1,191 @@
+// agr_internal.cuh -- device data layouts and small helpers shared by the
+// libagr.so translation units (BLAS build, TLAS build/refit, casts, ABI).
+//
+// Nothing here is shared with oracle/ (the oracle and the CUDA
+// path share no code).
+//
+// HBM layout:
+//   nodes   float4[4] per node, 64 B, BLAS nodes of every asset first, then
+//           every env's TLAS nodes.  A node holds the boxes of its two
+//           children and their refs:
+//             n0 = (c0.lo.x, c0.hi.x, c0.lo.y, c0.hi.y)
+//             n1 = (c0.lo.z, c0.hi.z, c1.lo.x, c1.hi.x)
+//             n2 = (c1.lo.y, c1.hi.y, c1.lo.z, c1.hi.z)
+//             n3 = (ref0, ref1, -, -) as int bits
+//           ref >= 0: global node index; ref < 0: leaf ~index (triangle
+//           record for BLAS nodes, global instance for TLAS nodes);
+//           REF_EMPTY: no child (its box is +inf everywhere, never hit).
+//   tris    float4[3] per BLAS leaf, 48 B (FP32 filter test, object space):
+//             t0 = (v0.xyz, inv_min_alt)   inv_min_alt = 1 / min altitude
+//             t1 = (e1.xyz, two_area)      e1 = v1 - v0, two_area = |e1 x e2|
+//             t2 = (e2.xyz, local face id as int bits)
+//   triv    float[9] per BLAS leaf: the exact FP32 input vertices v0 v1 v2
+//           (read only by the FP64 arbitration / epilogue).
+//   irec    float4[4] per instance, 64 B (ray -> object space):
+//             r0..r2 = rows of [Ainv | binv] (FP64 inverse rounded to FP32)
+//             r3 = (blas root node (int bits), nAinv, err_off, -)
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define AGR_HD __host__ __device__ __forceinline__
+
+namespace agr {
+
+constexpr int REF_EMPTY = (int)0x80000000;  // INT32_MIN
+constexpr int STACK_SIZE = 64;              // traversal stack entries per ray
+constexpr int MAX_TLAS_N = 1024;            // AGR_MAX_INSTANCES_PER_ENV
+
+// Relative error budget of the FP32 object-space ray:
+// position error <= K_ERR * (nAinv * (|o|_1 + |b|_1 + t_max |d|_1) + r_asset).
+constexpr float K_ERR = 7.62939453125e-06f;  // 2^-17
+// Relative slack on FP32 t values (ray direction rounding etc.).
+constexpr float T_REL = 9.5367431640625e-07f;  // 2^-20
+
+struct AssetInfo {
+    int node_base;   // global index of the asset's root node
+    int leaf_base;   // global index of the asset's first leaf record
+    int n_leaves;    // non-degenerate triangles in the BLAS
+    int n_faces;     // faces in the asset (numbering)
+    float lo[3], hi[3];  // root box (object space, exact min/max)
+    float radius;    // max |v| over the asset's vertices (object units)
+    int depth;       // BLAS depth (edges from root to deepest leaf)
+};
+
+// Read-only view of a scene passed by value to kernels.
+struct SceneView {
+    const float4* nodes;      // [n_nodes][4]
+    const float4* tris;       // [n_leaves][3]
+    const float* triv;        // [n_leaves][9]
+    const float4* irec;       // [n_inst][4]
+    const float* inst_T;      // [n_inst][12] forward transforms (FP32 input)
+    const int* inst_face_off; // [n_inst] per-env face offset of the instance
+    const int* inst_label;    // [n_inst]
+    const int* env_off;       // [n_envs + 1]
+    const int* tlas_root;     // [n_envs] global node index of the env's TLAS root
+    const int* inst_asset;    // [n_inst]
+    const AssetInfo* assets;  // [n_assets]
+    int n_envs;
+};
+
+// ---- small vector helpers --------------------------------------------------
+struct f3 { float x, y, z; };
+struct d3 { double x, y, z; };
+
+AGR_HD f3 mk(float x, float y, float z) { f3 r; r.x = x; r.y = y; r.z = z; return r; }
+AGR_HD f3 sub(f3 a, f3 b) { return mk(a.x - b.x, a.y - b.y, a.z - b.z); }
+AGR_HD float dot(f3 a, f3 b) { return fmaf(a.x, b.x, fmaf(a.y, b.y, a.z * b.z)); }
+AGR_HD f3 cross(f3 a, f3 b) {
+    return mk(fmaf(a.y, b.z, -a.z * b.y), fmaf(a.z, b.x, -a.x * b.z), fmaf(a.x, b.y, -a.y * b.x));
+}
+AGR_HD d3 mkd(double x, double y, double z) { d3 r; r.x = x; r.y = y; r.z = z; return r; }
+AGR_HD d3 subd(d3 a, d3 b) { return mkd(a.x - b.x, a.y - b.y, a.z - b.z); }
+AGR_HD double dotd(d3 a, d3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+AGR_HD d3 crossd(d3 a, d3 b) {
+    return mkd(a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x);
+}
+
+// ---- 30-bit Morton code (10 bits per axis) -------------------------------
+AGR_HD uint32_t expand_bits10(uint32_t v) {
+    v = (v * 0x00010001u) & 0xFF0000FFu;
+    v = (v * 0x00000101u) & 0x0F00F00Fu;
+    v = (v * 0x00000011u) & 0xC30C30C3u;
+    v = (v * 0x00000005u) & 0x49249249u;
+    return v;
+}
+// x, y, z in [0, 1]: quantise min(floor(x * 1024), 1023); x in bit 2 of
+// each triple (x most significant), as in Karras 2012.
+AGR_HD uint32_t morton30(float x, float y, float z) {
+    uint32_t xi = (uint32_t)fminf(fmaxf(floorf(x * 1024.0f), 0.0f), 1023.0f);
+    uint32_t yi = (uint32_t)fminf(fmaxf(floorf(y * 1024.0f), 0.0f), 1023.0f);
+    uint32_t zi = (uint32_t)fminf(fmaxf(floorf(z * 1024.0f), 0.0f), 1023.0f);
+    return (expand_bits10(xi) << 2) | (expand_bits10(yi) << 1) | expand_bits10(zi);
+}
+
+// Normalise a centroid coordinate to the centroid bounds; a zero-extent axis
+// uses extent 1.
+AGR_HD float unit_coord(float c, float lo, float hi) {
+    float ext = hi - lo;
+    return ext > 0.0f ? (c - lo) / ext : 0.0f;
+}
+
+// ---- float <-> orderable uint for atomic min/max ---------------------------
+__device__ __forceinline__ uint32_t float_to_ordered(float f) {
+    uint32_t u = __float_as_uint(f);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float ordered_to_float(uint32_t u) {
+    return __uint_as_float((u & 0x80000000u) ? (u & 0x7FFFFFFFu) : ~u);
+}
+
+}  // namespace agr
+
+// Host launch wrappers implemented in the .cu files (all async on `stream`).
+namespace agr {
+struct BlasBuildArgs {
+    const float* verts;    // device [V][3]
+    const int* faces;      // device [F][3]
+    int n_verts, n_faces;
+    int node_base;         // global node index of this asset's first node
+    int leaf_base;         // global leaf-record index of this asset's first leaf
+    float4* nodes;         // global node array
+    float4* tris;          // global tri record array
+    float* triv;           // global exact-vertex array
+    AssetInfo* info_dev;   // this asset's AssetInfo (device)
+    uint32_t* dbg_morton;  // optional: sorted codes [n_leaves] (device) or null
+};
+// Builds one asset's BLAS.  `scratch` must hold blas_scratch_bytes(F) bytes.
+size_t blas_scratch_bytes(int n_faces);
+cudaError_t blas_build(const BlasBuildArgs& a, void* scratch, int* n_leaves_out,
+                       cudaStream_t stream);
+
+struct TlasArgs {
+    float4* nodes;            // global node array (TLAS part written)
+    float4* irec;             // [n_inst][4] written
+    float* inst_box;          // [n_inst][6] written
+    const float* inst_T;      // [n_inst][12]
+    const int* inst_asset;    // [n_inst]
+    const AssetInfo* assets;  // [n_assets]
+    const int* env_off;       // [n_envs+1]
+    const int* tlas_off;      // [n_envs] offset of the env's first node within the TLAS part
+    int nb_blas;              // number of BLAS nodes (TLAS node j of env e is global
+                              // node nb_blas + tlas_off[e] + j)
+    int* tlas_child;          // [2 * n_tlas_nodes] local child refs (>=0 node, <0 ~local inst)
+    int* tlas_inst_parent;    // [n_inst] local parent (internal node) of each instance leaf
+    int* tlas_node_parent;    // [n_tlas_nodes] local parent of each internal node
+    int* tlas_depth;          // [n_envs] depth of each env's TLAS (written by build)
+    int n_envs;
+    int max_n;                // max instances in one env (sizes shared memory)
+};
+cudaError_t instances_update(const TlasArgs& a, int n_inst, cudaStream_t stream);
+cudaError_t tlas_build(const TlasArgs& a, bool rebuild, cudaStream_t stream);
+
+// Casts.  Model: 0 rays, 1 pinhole, 2 beams.
+struct CastArgs {
+    SceneView sv;
+    int model;
+    int kind;             // pinhole: 0 depth, 1 range
+    int W, H;             // pinhole image / beams (W = K columns, H = C channels)
+    float fx, fy, cx, cy;
+    const float* beams;   // [C][K][3]
+    const float* poses;   // [n_envs][S][12]
+    int S;
+    const float* orig;    // rays [n_envs][R][3]
+    const float* dir;
+    int R;
+    float max_range;
+    float* out_dist;
+    int* out_seg;
+    int* out_face;
+    int env_begin, env_end;  // envs cast by this launch (chunking)
+    int out_env_base;        // outputs are indexed from this env (0: global indexing)
+    unsigned long long* counters;  // optional [8]
+    int exact;
+};
+cudaError_t cast_launch(const CastArgs& a, cudaStream_t stream);
+
+cudaError_t checksum_launch(const float* dist, const int* seg, const int* face,
+                            int64_t elems_per_env, int n_envs, unsigned long long* sums,
+                            cudaStream_t stream);
+}  // namespace agr

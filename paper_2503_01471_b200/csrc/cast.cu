@@ -1,0 +1,472 @@
+// cast.cu -- the hot path: fused ray generation + two-level BVH traversal +
+// FP64 arbitration/epilogue + coalesced stores (SURVEY.md §8(a) a4-a6,
+// kernels K9 pinhole, K10 beams, K9b explicit rays).
+//
+// PAPER.md:228 (§III.D.1): "individual rays are cast outwards per-pixel to
+// evaluate intersection with M_{i,t}.  The distance between the sensor and
+// the point-of-intersection is reported as range for ToF sensors and
+// LiDARs, while the distance of this point from the image plane is reported
+// as depth"; PAPER.md:218 (Fig. 3): depth, segmentation, face-index images;
+// PAPER.md:215 / :228: LiDAR and custom projection models.
+//
+// Numerics: traversal and Moller-Trumbore tests run in FP32
+// in object space, with every decision FP32 cannot certify deferred: boxes
+// are widened by the ray's error bound delta, and a triangle test is
+//   * rejected only if FP32 proves a miss (outside by more than the error
+//     band, or t provably beyond the current bound U),
+//   * "certain" if FP32 proves a hit (inside by more than the band and t
+//     provably in (0, max_range]) -- only these tighten U,
+//   * otherwise kept as a candidate.
+// Candidates with t_lo <= U live in a 4-slot per-lane list; at the end each
+// surviving candidate is re-tested in FP64 on the world-space triangle
+// (A v + b from the FP32 inputs) with the FP64 ray, and the smallest
+// (t, face) wins.  A lane whose list overflows re-traverses in exact mode
+// (every leaf tested in FP64).  The reported distance is the FP64 t rounded
+// to FP32.
+#include "agr_internal.cuh"
+
+namespace agr {
+namespace {
+
+constexpr int CAST_THREADS = 128;
+constexpr int NSLOT = 4;
+constexpr int SENTINEL = REF_EMPTY;  // "return to the TLAS" marker on the stack
+
+__device__ __forceinline__ float inf_f() { return __int_as_float(0x7f800000); }
+
+// Ray state for box tests at one level (env or object space).
+struct SlabRay {
+    float idx, idy, idz;      // 1 / d (zero components clamped)
+    float lox, loy, loz;      // -(o + delta) * id
+    float hix, hiy, hiz;      // -(o - delta) * id
+};
+
+__device__ __forceinline__ float safe_inv(float d) {
+    float ad = fabsf(d);
+    float dd = ad < 1e-20f ? copysignf(1e-20f, d) : d;
+    return __frcp_rn(dd);
+}
+
+__device__ __forceinline__ SlabRay make_slab(f3 o, f3 d, float delta) {
+    SlabRay s;
+    s.idx = safe_inv(d.x);
+    s.idy = safe_inv(d.y);
+    s.idz = safe_inv(d.z);
+    s.lox = -(o.x + delta) * s.idx;
+    s.loy = -(o.y + delta) * s.idy;
+    s.loz = -(o.z + delta) * s.idz;
+    s.hix = -(o.x - delta) * s.idx;
+    s.hiy = -(o.y - delta) * s.idy;
+    s.hiz = -(o.z - delta) * s.idz;
+    return s;
+}
+
+// Slab test of one child box (lo/hi per axis) against [0, U].
+__device__ __forceinline__ bool slab(const SlabRay& r, float lx, float hx, float ly, float hy,
+                                     float lz, float hz, float U, float& tnear) {
+    float ax = fmaf(lx, r.idx, r.lox), bx = fmaf(hx, r.idx, r.hix);
+    float ay = fmaf(ly, r.idy, r.loy), by = fmaf(hy, r.idy, r.hiy);
+    float az = fmaf(lz, r.idz, r.loz), bz = fmaf(hz, r.idz, r.hiz);
+    float tn = fmaxf(fmaxf(fminf(ax, bx), fminf(ay, by)), fmaxf(fminf(az, bz), 0.0f));
+    float tf = fminf(fminf(fmaxf(ax, bx), fmaxf(ay, by)), fminf(fmaxf(az, bz), U));
+    tnear = tn;
+    return tn <= tf;
+}
+
+// ---- FP64 ray and FP64 world-space triangle test ----------------------------
+struct Ray64 { d3 o, d; };
+
+__device__ __forceinline__ bool test64(const SceneView& sv, int inst, int leaf, const Ray64& r,
+                                       double tmax, double& t) {
+    const float* T = sv.inst_T + 12 * inst;
+    const float* v = sv.triv + 9 * leaf;
+    double A[12];
+#pragma unroll
+    for (int k = 0; k < 12; ++k) A[k] = (double)__ldg(T + k);
+    d3 w[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        double x = __ldg(v + 3 * c), y = __ldg(v + 3 * c + 1), z = __ldg(v + 3 * c + 2);
+        w[c].x = A[0] * x + A[1] * y + A[2] * z + A[3];
+        w[c].y = A[4] * x + A[5] * y + A[6] * z + A[7];
+        w[c].z = A[8] * x + A[9] * y + A[10] * z + A[11];
+    }
+    d3 e1 = subd(w[1], w[0]), e2 = subd(w[2], w[0]);
+    d3 p = crossd(r.d, e2);
+    double det = dotd(e1, p);
+    if (det == 0.0) return false;
+    d3 s = subd(r.o, w[0]);
+    double u = dotd(s, p);
+    d3 q = crossd(s, e1);
+    double vv = dotd(r.d, q);
+    double tn = dotd(e2, q);
+    if (det < 0.0) { det = -det; u = -u; vv = -vv; tn = -tn; }
+    if (u < 0.0 || vv < 0.0 || u + vv > det) return false;
+    t = tn / det;
+    return t > 0.0 && t <= tmax;
+}
+
+// ---- per-lane candidate list ---------------------------------------------------
+struct Slots {
+    float tl[NSLOT];
+    int inst[NSLOT];
+    int leaf[NSLOT];
+};
+
+// ---- traversal ---------------------------------------------------------------------
+struct Counters { unsigned nodes, leaves, insts, f64, overflow; };
+
+struct Best64 {
+    double t;
+    int face;   // per-env face index, -1 none
+    int inst;
+    int leaf;
+};
+
+__device__ __forceinline__ bool better(double t, int face, const Best64& b) {
+    return b.face < 0 || t < b.t || (t == b.t && face < b.face);
+}
+
+__device__ __forceinline__ void consider64(const SceneView& sv, int inst, int leaf, const Ray64& r64,
+                                           double tmax, Best64& best) {
+    double t;
+    if (test64(sv, inst, leaf, r64, tmax, t)) {
+        int face = __ldg(sv.inst_face_off + inst) + __float_as_int(__ldg(&sv.tris[3 * leaf + 2].w));
+        if (better(t, face, best)) { best.t = t; best.face = face; best.inst = inst; best.leaf = leaf; }
+    }
+}
+
+// Brute force over every triangle of the env in FP64: the path of last resort
+// when a traversal stack would overflow (a pathological TLAS/BLAS depth).
+__device__ __noinline__ void brute64(const SceneView& sv, int env, const Ray64& r64, double tmax,
+                                     Best64& best) {
+    for (int inst = __ldg(sv.env_off + env); inst < __ldg(sv.env_off + env + 1); ++inst) {
+        const AssetInfo& as = sv.assets[__ldg(sv.inst_asset + inst)];
+        for (int l = 0; l < as.n_leaves; ++l) consider64(sv, inst, as.leaf_base + l, r64, tmax, best);
+    }
+}
+
+template <bool EXACT, bool COUNT>
+__device__ __forceinline__ void traverse(const SceneView& sv, int env, f3 o, f3 d, float tmax,
+                                         const Ray64& r64, Slots& sl, bool& overflow,
+                                         bool& stack_overflow, Best64& best, Counters& cnt) {
+    int stack[STACK_SIZE];
+    int sp = 0;
+    // env-level error bound: direction rounding (origin exact) -- DESIGN.md §5.2
+    const float q = fabsf(o.x) + fabsf(o.y) + fabsf(o.z) + tmax * (fabsf(d.x) + fabsf(d.y) + fabsf(d.z));
+    const SlabRay env_slab = make_slab(o, d, K_ERR * q);
+    SlabRay sr = env_slab;
+    // object-space ray of the current instance
+    f3 oo = o, od = d;
+    float delta = 0.0f, dlen = 0.0f;
+    int cur_inst = -1;
+    float U = tmax;
+    int node = __ldg(sv.tlas_root + env);
+    for (;;) {
+        if (node >= 0) {
+            if (COUNT) cnt.nodes++;
+            const float4* np = sv.nodes + 4 * node;
+            float4 n0 = __ldg(np), n1 = __ldg(np + 1), n2 = __ldg(np + 2), n3 = __ldg(np + 3);
+            float t0, t1;
+            bool h0 = slab(sr, n0.x, n0.y, n0.z, n0.w, n1.x, n1.y, U, t0);
+            bool h1 = slab(sr, n1.z, n1.w, n2.x, n2.y, n2.z, n2.w, U, t1);
+            int c0 = __float_as_int(n3.x), c1 = __float_as_int(n3.y);
+            if (h0 && h1) {
+                int far_c = t0 <= t1 ? c1 : c0;
+                node = t0 <= t1 ? c0 : c1;
+                if (sp < STACK_SIZE) stack[sp++] = far_c;
+                else stack_overflow = true;
+            } else if (h0) {
+                node = c0;
+            } else if (h1) {
+                node = c1;
+            } else {
+                if (sp == 0) break;
+                node = stack[--sp];
+            }
+            continue;
+        }
+        if (node == SENTINEL) {  // leave the instance: back to the env-level ray
+            sr = env_slab;
+            cur_inst = -1;
+            if (sp == 0) break;
+            node = stack[--sp];
+            continue;
+        }
+        const int leaf = ~node;
+        if (cur_inst < 0) {
+            // TLAS leaf: enter instance `leaf`, move the ray to object space
+            if (COUNT) cnt.insts++;
+            const float4* rp = sv.irec + 4 * leaf;
+            float4 r0 = __ldg(rp), r1 = __ldg(rp + 1), r2 = __ldg(rp + 2), r3 = __ldg(rp + 3);
+            oo = mk(fmaf(r0.x, o.x, fmaf(r0.y, o.y, fmaf(r0.z, o.z, r0.w))),
+                    fmaf(r1.x, o.x, fmaf(r1.y, o.y, fmaf(r1.z, o.z, r1.w))),
+                    fmaf(r2.x, o.x, fmaf(r2.y, o.y, fmaf(r2.z, o.z, r2.w))));
+            od = mk(fmaf(r0.x, d.x, fmaf(r0.y, d.y, r0.z * d.z)),
+                    fmaf(r1.x, d.x, fmaf(r1.y, d.y, r1.z * d.z)),
+                    fmaf(r2.x, d.x, fmaf(r2.y, d.y, r2.z * d.z)));
+            delta = K_ERR * fmaf(r3.y, q, r3.z);
+            dlen = sqrtf(dot(od, od));
+            sr = make_slab(oo, od, delta);
+            cur_inst = leaf;
+            if (sp < STACK_SIZE) stack[sp++] = SENTINEL;
+            else { stack_overflow = true; break; }
+            node = __float_as_int(r3.x);
+            continue;
+        }
+        // BLAS leaf: triangle record `leaf` of instance cur_inst
+        if (COUNT) cnt.leaves++;
+        if (EXACT) {
+            if (COUNT) cnt.f64++;
+            consider64(sv, cur_inst, leaf, r64, (double)tmax, best);
+            if (best.face >= 0) U = fminf(tmax, __double2float_ru(best.t));
+        } else {
+            const float4* tp = sv.tris + 3 * leaf;
+            float4 a = __ldg(tp), b = __ldg(tp + 1), c = __ldg(tp + 2);
+            f3 v0 = mk(a.x, a.y, a.z), e1 = mk(b.x, b.y, b.z), e2 = mk(c.x, c.y, c.z);
+            f3 p = cross(od, e2);
+            float det = dot(e1, p);
+            f3 s = sub(oo, v0);
+            bool keep = false, certain = false;
+            float tl = 0.0f, th = 0.0f;
+            if (det != 0.0f) {
+                float inv = __frcp_rn(det);
+                f3 qv = cross(s, e1);
+                float u = dot(s, p) * inv;
+                float v = dot(od, qv) * inv;
+                float t = dot(e2, qv) * inv;
+                float g = delta * b.w * fabsf(inv);           // t error bound
+                float beta = g * dlen * a.w;                     // barycentric band
+                float terr = fmaf(fabsf(t), T_REL, g);
+                tl = t - terr;
+                th = t + terr;
+                bool out = u < -beta || v < -beta || u + v > 1.0f + beta || th < 0.0f || tl > U;
+                keep = !out;
+                if (!(tl == tl)) tl = 0.0f;  // NaN (denormal det): keep conservatively
+                certain = keep && u > beta && v > beta && u + v < 1.0f - beta && tl > 0.0f && th <= tmax;
+            } else {
+                // ray parallel in FP32: keep only if the origin is within delta of the plane
+                f3 nn = cross(e1, e2);
+                float h = fabsf(dot(s, nn));
+                keep = h <= delta * b.w;
+                tl = 0.0f;
+            }
+            if (keep) {
+                if (certain && th < U) U = th;
+                bool placed = false;
+#pragma unroll
+                for (int k = 0; k < NSLOT; ++k) {
+                    // a slot is free if empty (+inf) or pruned by the current U
+                    if (!placed && !(sl.tl[k] <= U)) {
+                        sl.tl[k] = tl;
+                        sl.inst[k] = cur_inst;
+                        sl.leaf[k] = leaf;
+                        placed = true;
+                    }
+                }
+                if (!placed) overflow = true;
+            }
+        }
+        if (sp == 0) break;
+        node = stack[--sp];
+    }
+    if (!EXACT) {
+        // slots pruned after insertion are dead; mark them empty
+#pragma unroll
+        for (int k = 0; k < NSLOT; ++k)
+            if (!(sl.tl[k] <= U)) sl.tl[k] = inf_f();
+    }
+}
+
+// ---- ray generation -----------------------------------------------------------------
+struct RayId {
+    int env;
+    int64_t out;     // output element index
+    bool active;
+    int col, row, sensor;
+};
+
+__device__ __forceinline__ void pose_ray(const float* P, f3 ds, f3& o, f3& d) {
+    o = mk(__ldg(P + 3), __ldg(P + 7), __ldg(P + 11));
+    d = mk(fmaf(__ldg(P + 0), ds.x, fmaf(__ldg(P + 1), ds.y, __ldg(P + 2) * ds.z)),
+           fmaf(__ldg(P + 4), ds.x, fmaf(__ldg(P + 5), ds.y, __ldg(P + 6) * ds.z)),
+           fmaf(__ldg(P + 8), ds.x, fmaf(__ldg(P + 9), ds.y, __ldg(P + 10) * ds.z)));
+}
+
+__device__ __forceinline__ void pose_ray64(const float* P, d3 ds, Ray64& r) {
+    double p[12];
+#pragma unroll
+    for (int k = 0; k < 12; ++k) p[k] = (double)__ldg(P + k);
+    r.o = mkd(p[3], p[7], p[11]);
+    r.d = mkd(p[0] * ds.x + p[1] * ds.y + p[2] * ds.z,
+              p[4] * ds.x + p[5] * ds.y + p[6] * ds.z,
+              p[8] * ds.x + p[9] * ds.y + p[10] * ds.z);
+}
+
+template <int MODEL>
+__device__ __forceinline__ void gen_ray(const CastArgs& a, const RayId& id, f3& o, f3& d, Ray64& r64) {
+    if (MODEL == 0) {
+        const float* po = a.orig + 3 * id.out;
+        const float* pd = a.dir + 3 * id.out;
+        o = mk(__ldg(po), __ldg(po + 1), __ldg(po + 2));
+        d = mk(__ldg(pd), __ldg(pd + 1), __ldg(pd + 2));
+        r64.o = mkd(o.x, o.y, o.z);
+        r64.d = mkd(d.x, d.y, d.z);
+        return;
+    }
+    const float* P = a.poses + 12 * ((int64_t)id.env * a.S + id.sensor);
+    f3 ds;
+    d3 ds64;
+    if (MODEL == 1) {
+        float xs = ((float)id.col + 0.5f - a.cx) / a.fx;
+        float ys = ((float)id.row + 0.5f - a.cy) / a.fy;
+        ds = mk(1.0f, -xs, -ys);
+        double xs64 = ((double)id.col + 0.5 - (double)a.cx) / (double)a.fx;
+        double ys64 = ((double)id.row + 0.5 - (double)a.cy) / (double)a.fy;
+        ds64 = mkd(1.0, -xs64, -ys64);
+        if (a.kind == 1) {
+            float rn = rsqrtf(dot(ds, ds));
+            ds = mk(ds.x * rn, ds.y * rn, ds.z * rn);
+            double n = sqrt(dotd(ds64, ds64));
+            ds64 = mkd(ds64.x / n, ds64.y / n, ds64.z / n);
+        }
+    } else {
+        const float* b = a.beams + 3 * ((int64_t)id.row * a.W + id.col);
+        ds = mk(__ldg(b), __ldg(b + 1), __ldg(b + 2));
+        ds64 = mkd(ds.x, ds.y, ds.z);
+        float rn = rsqrtf(dot(ds, ds));
+        ds = mk(ds.x * rn, ds.y * rn, ds.z * rn);
+        double n = sqrt(dotd(ds64, ds64));
+        ds64 = mkd(ds64.x / n, ds64.y / n, ds64.z / n);
+    }
+    pose_ray(P, ds, o, d);
+    pose_ray64(P, ds64, r64);
+}
+
+template <int MODEL>
+__device__ __forceinline__ RayId ray_id(const CastArgs& a) {
+    RayId id;
+    id.sensor = 0;
+    id.col = id.row = 0;
+    if (MODEL == 0) {
+        int bpe = (a.R + CAST_THREADS - 1) / CAST_THREADS;
+        int e = a.env_begin + blockIdx.x / bpe;
+        int r = (blockIdx.x % bpe) * CAST_THREADS + threadIdx.x;
+        id.env = e;
+        id.active = r < a.R && e < a.env_end;
+        id.out = (int64_t)(e - a.out_env_base) * a.R + (id.active ? r : 0);
+        return id;
+    }
+    const int tiles_x = (a.W + 7) >> 3, tiles_y = (a.H + 3) >> 2;
+    const int64_t tiles_img = (int64_t)tiles_x * tiles_y;
+    const int64_t warp = (int64_t)blockIdx.x * (CAST_THREADS / 32) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    const int64_t img = warp / tiles_img;
+    const int tile = (int)(warp - img * tiles_img);
+    const int ty = tile / tiles_x, tx = tile - ty * tiles_x;
+    id.env = a.env_begin + (int)(img / a.S);
+    id.sensor = (int)(img % a.S);
+    id.col = tx * 8 + (lane & 7);
+    id.row = ty * 4 + (lane >> 3);
+    id.active = id.env < a.env_end && id.col < a.W && id.row < a.H;
+    id.out = (((int64_t)(id.env - a.out_env_base) * a.S + id.sensor) * a.H + id.row) * a.W + id.col;
+    return id;
+}
+
+template <int MODEL, bool COUNT>
+__global__ void __launch_bounds__(CAST_THREADS) k_cast(CastArgs a) {
+    RayId id = ray_id<MODEL>(a);
+    // ragged tile lanes keep the warp whole for the traversal: they trace a
+    // copy of a valid pixel and store nothing
+    const bool trace = id.env < a.env_end && (id.active || MODEL != 0);
+    id.col = min(id.col, a.W - 1);
+    id.row = min(id.row, a.H - 1);
+    Counters cnt = {0, 0, 0, 0, 0};
+    Best64 best;
+    best.t = 0.0;
+    best.face = -1;
+    best.inst = -1;
+    best.leaf = -1;
+    if (trace) {
+        f3 o, d;
+        Ray64 r64;
+        gen_ray<MODEL>(a, id, o, d, r64);
+        const float tmax = a.max_range;
+        bool overflow = false, sovf = false;
+        Slots sl;
+        if (a.exact) {
+            traverse<true, COUNT>(a.sv, id.env, o, d, tmax, r64, sl, overflow, sovf, best, cnt);
+        } else {
+#pragma unroll
+            for (int k = 0; k < NSLOT; ++k) { sl.tl[k] = inf_f(); sl.inst[k] = -1; sl.leaf[k] = -1; }
+            traverse<false, COUNT>(a.sv, id.env, o, d, tmax, r64, sl, overflow, sovf, best, cnt);
+            // FP64 arbitration of the surviving candidates (warp-uniform slot loop)
+#pragma unroll
+            for (int k = 0; k < NSLOT; ++k) {
+                if (sl.tl[k] <= tmax) {
+                    if (COUNT) cnt.f64++;
+                    consider64(a.sv, sl.inst[k], sl.leaf[k], r64, (double)tmax, best);
+                }
+            }
+            if (overflow && !sovf) {
+                // candidate list overflow: re-traverse with every leaf tested in FP64
+                if (COUNT) cnt.overflow++;
+                best.face = -1;
+                traverse<true, COUNT>(a.sv, id.env, o, d, tmax, r64, sl, overflow, sovf, best, cnt);
+            }
+        }
+        if (sovf) {
+            if (COUNT) cnt.overflow++;
+            best.face = -1;
+            brute64(a.sv, id.env, r64, (double)tmax, best);
+        }
+    }
+    if (COUNT) {
+        unsigned v[5] = {cnt.nodes, cnt.leaves, cnt.insts, cnt.f64, cnt.overflow};
+        unsigned rays = id.active ? 1u : 0u;
+        for (int o2 = 16; o2 > 0; o2 >>= 1) {
+            rays += __shfl_xor_sync(0xFFFFFFFFu, rays, o2);
+            for (int k = 0; k < 5; ++k) v[k] += __shfl_xor_sync(0xFFFFFFFFu, v[k], o2);
+        }
+        if ((threadIdx.x & 31) == 0) {
+            atomicAdd(a.counters + 0, (unsigned long long)rays);
+            for (int k = 0; k < 5; ++k) atomicAdd(a.counters + 1 + k, (unsigned long long)v[k]);
+        }
+    }
+    if (!id.active) return;
+    const bool hit = best.face >= 0;
+    if (a.out_dist) a.out_dist[id.out] = hit ? (float)best.t : a.max_range;
+    if (a.out_seg) a.out_seg[id.out] = hit ? __ldg(a.sv.inst_label + best.inst) : -1;
+    if (a.out_face) a.out_face[id.out] = hit ? best.face : -1;
+}
+
+template <int MODEL>
+cudaError_t launch_model(const CastArgs& a, cudaStream_t stream) {
+    int64_t blocks;
+    int n_envs = a.env_end - a.env_begin;
+    if (n_envs <= 0) return cudaSuccess;
+    if (MODEL == 0) {
+        blocks = (int64_t)n_envs * ((a.R + CAST_THREADS - 1) / CAST_THREADS);
+    } else {
+        int64_t tiles = (int64_t)((a.W + 7) >> 3) * ((a.H + 3) >> 2) * n_envs * a.S;
+        blocks = (tiles + CAST_THREADS / 32 - 1) / (CAST_THREADS / 32);
+    }
+    if (blocks <= 0) return cudaSuccess;
+    if (blocks > 0x7FFFFFFF) return cudaErrorInvalidValue;
+    if (a.counters) k_cast<MODEL, true><<<(unsigned)blocks, CAST_THREADS, 0, stream>>>(a);
+    else k_cast<MODEL, false><<<(unsigned)blocks, CAST_THREADS, 0, stream>>>(a);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t cast_launch(const CastArgs& a, cudaStream_t stream) {
+    switch (a.model) {
+        case 0: return launch_model<0>(a, stream);
+        case 1: return launch_model<1>(a, stream);
+        case 2: return launch_model<2>(a, stream);
+    }
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace agr

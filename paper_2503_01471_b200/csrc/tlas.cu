@@ -1,0 +1,320 @@
+// tlas.cu -- per-instance ray transforms and the per-env top-level BVH.
+//
+// PAPER.md:226 (§III.D.1): transformations T_{j,t} are kept for each
+// sub-mesh, "the vertices of the mesh are transformed to match the obstacles
+// in the simulator at time t" and a BVH is computed over M_{i,t}.  Here the
+// vertices are not rewritten: each instance stores the inverse transform so
+// rays are moved into object space instead, and each env
+// gets a TLAS over its instance boxes (north_star: "a per-env TLAS over
+// instances, refit in place when obstacles are re-posed").
+//   K6 k_instances   inverse affine (FP64 -> FP32), conservative world box
+//   K7 k_tlas        (rebuild) per-env Morton sort + Karras + fit, one CTA/env
+//   K8 k_tlas        (refit)   same CTA shape, stored topology, boxes only
+#include "agr_internal.cuh"
+
+#include <cfloat>
+
+namespace agr {
+namespace {
+
+constexpr int TLAS_THREADS = 256;
+
+__device__ __forceinline__ float inf_f() { return __int_as_float(0x7f800000); }
+
+// ---- K6: per-instance record and world box ------------------------------------
+__global__ void k_instances(TlasArgs a, int n_inst) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_inst) return;
+    const float* T = a.inst_T + 12 * i;
+    const AssetInfo& as = a.assets[a.inst_asset[i]];
+    double A[3][3], b[3];
+    for (int r = 0; r < 3; ++r) {
+        for (int c = 0; c < 3; ++c) A[r][c] = T[4 * r + c];
+        b[r] = T[4 * r + 3];
+    }
+    double c00 = A[1][1] * A[2][2] - A[1][2] * A[2][1];
+    double c01 = A[1][2] * A[2][0] - A[1][0] * A[2][2];
+    double c02 = A[1][0] * A[2][1] - A[1][1] * A[2][0];
+    double det = A[0][0] * c00 + A[0][1] * c01 + A[0][2] * c02;
+    float4* rec = a.irec + 4 * i;
+    float* box = a.inst_box + 6 * i;
+    bool ok = det != 0.0 && isfinite(det) && as.n_leaves > 0;
+    if (!ok) {
+        // singular transform or an all-degenerate asset: the instance is never hit
+        for (int k = 0; k < 6; ++k) box[k] = inf_f();
+        for (int k = 0; k < 4; ++k) rec[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+        return;
+    }
+    double inv[3][3];
+    double id = 1.0 / det;
+    inv[0][0] = c00 * id;
+    inv[1][0] = c01 * id;
+    inv[2][0] = c02 * id;
+    inv[0][1] = (A[0][2] * A[2][1] - A[0][1] * A[2][2]) * id;
+    inv[1][1] = (A[0][0] * A[2][2] - A[0][2] * A[2][0]) * id;
+    inv[2][1] = (A[0][1] * A[2][0] - A[0][0] * A[2][1]) * id;
+    inv[0][2] = (A[0][1] * A[1][2] - A[0][2] * A[1][1]) * id;
+    inv[1][2] = (A[0][2] * A[1][0] - A[0][0] * A[1][2]) * id;
+    inv[2][2] = (A[0][0] * A[1][1] - A[0][1] * A[1][0]) * id;
+    double nrm2 = 0.0, b1 = fabs(b[0]) + fabs(b[1]) + fabs(b[2]);
+    for (int r = 0; r < 3; ++r) {
+        double binv = -(inv[r][0] * b[0] + inv[r][1] * b[1] + inv[r][2] * b[2]);
+        rec[r] = make_float4((float)inv[r][0], (float)inv[r][1], (float)inv[r][2], (float)binv);
+        for (int c = 0; c < 3; ++c) nrm2 += inv[r][c] * inv[r][c];
+    }
+    double nAinv = sqrt(nrm2) * (1.0 + 1e-6);
+    double err_off = nAinv * b1 + (double)as.radius;
+    rec[3] = make_float4(__int_as_float(as.node_base), (float)nAinv, (float)(err_off * (1.0 + 1e-6)), 0.f);
+    // conservative world box: centre/extent form, rounded outward
+    for (int r = 0; r < 3; ++r) {
+        double c = b[r], e = 0.0;
+        for (int k = 0; k < 3; ++k) {
+            double ck = 0.5 * ((double)as.lo[k] + (double)as.hi[k]);
+            double ek = 0.5 * ((double)as.hi[k] - (double)as.lo[k]);
+            c += A[r][k] * ck;
+            e += fabs(A[r][k]) * ek;
+        }
+        double lo = c - e, hi = c + e;
+        double pad = (fabs(lo) + fabs(hi)) * 1e-12 + 1e-30;
+        box[r] = __double2float_rd(lo - pad);
+        box[3 + r] = __double2float_ru(hi + pad);
+    }
+}
+
+// ---- K7/K8: per-env TLAS build / refit -----------------------------------------
+struct TlasSmem {
+    float* box;      // [n][6] instance boxes (local index)
+    float* ibox;     // [n-1][6] internal boxes
+    uint64_t* keys;  // [P] Morton<<32 | local index
+    int* child;      // [2(n-1)]
+    int* nparent;    // [n-1]
+    int* lparent;    // [n]
+    int* flags;      // [n-1]
+};
+
+__device__ __forceinline__ int kdelta64(const uint64_t* k, int n, int i, int j) {
+    if (j < 0 || j >= n) return -1;
+    return __clzll(k[i] ^ k[j]);  // keys are distinct (local index in the low bits)
+}
+
+__device__ void write_tlas_node(float4* nodes, int g, const float* a, const float* b, int ra, int rb) {
+    nodes[4 * g + 0] = make_float4(a[0], a[3], a[1], a[4]);
+    nodes[4 * g + 1] = make_float4(a[2], a[5], b[0], b[3]);
+    nodes[4 * g + 2] = make_float4(b[1], b[4], b[2], b[5]);
+    nodes[4 * g + 3] = make_float4(__int_as_float(ra), __int_as_float(rb), 0.0f, 0.0f);
+}
+
+__global__ void k_tlas(TlasArgs a, int rebuild) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int e = blockIdx.x;
+    const int i0 = a.env_off[e];
+    const int n = a.env_off[e + 1] - i0;
+    const int nodebase = a.nb_blas + a.tlas_off[e];
+    const int toff = a.tlas_off[e];
+    const int tid = threadIdx.x;
+    const float EMPTY[6] = {inf_f(), inf_f(), inf_f(), inf_f(), inf_f(), inf_f()};
+
+    if (n <= 1) {
+        if (tid == 0) {
+            if (n == 1) {
+                float b[6];
+                for (int k = 0; k < 6; ++k) b[k] = a.inst_box[6 * i0 + k];
+                write_tlas_node(a.nodes, nodebase, b, EMPTY, ~i0, REF_EMPTY);
+                a.tlas_inst_parent[i0] = 0;
+            } else {
+                write_tlas_node(a.nodes, nodebase, EMPTY, EMPTY, REF_EMPTY, REF_EMPTY);
+            }
+            a.tlas_node_parent[toff] = -1;
+            if (rebuild) a.tlas_depth[e] = 1;
+        }
+        return;
+    }
+    int P = 1;
+    while (P < n) P <<= 1;
+    TlasSmem s;
+    unsigned char* p = smem_raw;
+    s.keys = (uint64_t*)p; p += sizeof(uint64_t) * P;
+    s.box = (float*)p; p += sizeof(float) * 6 * n;
+    s.ibox = (float*)p; p += sizeof(float) * 6 * (n - 1);
+    s.child = (int*)p; p += sizeof(int) * 2 * (n - 1);
+    s.nparent = (int*)p; p += sizeof(int) * (n - 1);
+    s.lparent = (int*)p; p += sizeof(int) * n;
+    s.flags = (int*)p;
+
+    for (int i = tid; i < n; i += blockDim.x)
+        for (int k = 0; k < 6; ++k) s.box[6 * i + k] = a.inst_box[6 * (i0 + i) + k];
+    for (int j = tid; j < n - 1; j += blockDim.x) s.flags[j] = 0;
+    __syncthreads();
+
+    if (rebuild) {
+        // centroid bounds of the instance boxes (empty boxes excluded)
+        __shared__ float red[2][3][TLAS_THREADS / 32];
+        float lo[3] = {FLT_MAX, FLT_MAX, FLT_MAX}, hi[3] = {-FLT_MAX, -FLT_MAX, -FLT_MAX};
+        for (int i = tid; i < n; i += blockDim.x) {
+            if (isinf(s.box[6 * i])) continue;
+            for (int k = 0; k < 3; ++k) {
+                float c = 0.5f * s.box[6 * i + k] + 0.5f * s.box[6 * i + 3 + k];
+                lo[k] = fminf(lo[k], c);
+                hi[k] = fmaxf(hi[k], c);
+            }
+        }
+        for (int o = 16; o > 0; o >>= 1)
+            for (int k = 0; k < 3; ++k) {
+                lo[k] = fminf(lo[k], __shfl_xor_sync(0xFFFFFFFFu, lo[k], o));
+                hi[k] = fmaxf(hi[k], __shfl_xor_sync(0xFFFFFFFFu, hi[k], o));
+            }
+        if ((tid & 31) == 0)
+            for (int k = 0; k < 3; ++k) { red[0][k][tid >> 5] = lo[k]; red[1][k][tid >> 5] = hi[k]; }
+        __syncthreads();
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w)
+            for (int k = 0; k < 3; ++k) {
+                lo[k] = fminf(lo[k], red[0][k][w]);
+                hi[k] = fmaxf(hi[k], red[1][k][w]);
+            }
+        for (int i = tid; i < P; i += blockDim.x) {
+            uint64_t key = ~0ull;
+            if (i < n) {
+                uint32_t code = 0xFFFFFFFFu;  // empty boxes sort last
+                if (!isinf(s.box[6 * i])) {
+                    float u[3];
+                    for (int k = 0; k < 3; ++k) {
+                        float c = 0.5f * s.box[6 * i + k] + 0.5f * s.box[6 * i + 3 + k];
+                        u[k] = unit_coord(c, lo[k], hi[k]);
+                    }
+                    code = morton30(u[0], u[1], u[2]);
+                }
+                key = ((uint64_t)code << 32) | (uint32_t)i;
+            }
+            s.keys[i] = key;
+        }
+        __syncthreads();
+        // bitonic sort of P keys (ascending)
+        for (int k = 2; k <= P; k <<= 1) {
+            for (int j = k >> 1; j > 0; j >>= 1) {
+                for (int i = tid; i < P; i += blockDim.x) {
+                    int ixj = i ^ j;
+                    if (ixj > i) {
+                        uint64_t x = s.keys[i], y = s.keys[ixj];
+                        bool up = (i & k) == 0;
+                        if ((x > y) == up) { s.keys[i] = y; s.keys[ixj] = x; }
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        // Karras hierarchy over the n sorted keys
+        for (int i = tid; i < n - 1; i += blockDim.x) {
+            const uint64_t* k = s.keys;
+            int d = (kdelta64(k, n, i, i + 1) - kdelta64(k, n, i, i - 1)) >= 0 ? 1 : -1;
+            int dmin = kdelta64(k, n, i, i - d);
+            int lmax = 2;
+            while (kdelta64(k, n, i, i + lmax * d) > dmin) lmax <<= 1;
+            int l = 0;
+            for (int t = lmax >> 1; t >= 1; t >>= 1)
+                if (kdelta64(k, n, i, i + (l + t) * d) > dmin) l += t;
+            int j = i + l * d;
+            int dnode = kdelta64(k, n, i, j);
+            int sp = 0, t = l;
+            do {
+                t = (t + 1) >> 1;
+                if (kdelta64(k, n, i, i + (sp + t) * d) > dnode) sp += t;
+            } while (t > 1);
+            int gamma = i + sp * d + (d < 0 ? -1 : 0);
+            int lo_i = min(i, j), hi_i = max(i, j);
+            int left = (lo_i == gamma) ? ~(int)(uint32_t)k[gamma] : gamma;
+            int right = (hi_i == gamma + 1) ? ~(int)(uint32_t)k[gamma + 1] : gamma + 1;
+            s.child[2 * i] = left;
+            s.child[2 * i + 1] = right;
+            if (left < 0) s.lparent[~left] = i; else s.nparent[left] = i;
+            if (right < 0) s.lparent[~right] = i; else s.nparent[right] = i;
+        }
+        if (tid == 0) s.nparent[0] = -1;
+        __syncthreads();
+        for (int j = tid; j < n - 1; j += blockDim.x) {
+            a.tlas_child[2 * (toff + j)] = s.child[2 * j];
+            a.tlas_child[2 * (toff + j) + 1] = s.child[2 * j + 1];
+            a.tlas_node_parent[toff + j] = s.nparent[j];
+        }
+        for (int i = tid; i < n; i += blockDim.x) a.tlas_inst_parent[i0 + i] = s.lparent[i];
+        // depth: longest leaf-to-root path
+        int dmax = 0;
+        for (int i = tid; i < n; i += blockDim.x) {
+            int dd = 0;
+            for (int q = s.lparent[i]; q >= 0; q = s.nparent[q]) ++dd;
+            dmax = max(dmax, dd);
+        }
+        for (int o = 16; o > 0; o >>= 1) dmax = max(dmax, __shfl_xor_sync(0xFFFFFFFFu, dmax, o));
+        if ((tid & 31) == 0) atomicMax(&a.tlas_depth[e], dmax);
+    } else {
+        for (int j = tid; j < n - 1; j += blockDim.x) {
+            s.child[2 * j] = a.tlas_child[2 * (toff + j)];
+            s.child[2 * j + 1] = a.tlas_child[2 * (toff + j) + 1];
+            s.nparent[j] = a.tlas_node_parent[toff + j];
+        }
+        for (int i = tid; i < n; i += blockDim.x) s.lparent[i] = a.tlas_inst_parent[i0 + i];
+        __syncthreads();
+    }
+
+    // bottom-up fit: the second child to arrive at a node unions the boxes
+    for (int i = tid; i < n; i += blockDim.x) {
+        int node = s.lparent[i];
+        while (node >= 0) {
+            __threadfence_block();
+            if (atomicAdd(&s.flags[node], 1) == 0) break;
+            __threadfence_block();
+            volatile float* vb = s.box;
+            volatile float* vi = s.ibox;
+            float b[6], c[6];
+            int ra = s.child[2 * node], rb = s.child[2 * node + 1];
+            for (int k = 0; k < 6; ++k) {
+                b[k] = ra < 0 ? vb[6 * ~ra + k] : vi[6 * ra + k];
+                c[k] = rb < 0 ? vb[6 * ~rb + k] : vi[6 * rb + k];
+            }
+            for (int k = 0; k < 3; ++k) {
+                vi[6 * node + k] = fminf(b[k], c[k]);
+                vi[6 * node + 3 + k] = fmaxf(b[3 + k], c[3 + k]);
+            }
+            node = s.nparent[node];
+        }
+    }
+    __syncthreads();
+    for (int j = tid; j < n - 1; j += blockDim.x) {
+        int ra = s.child[2 * j], rb = s.child[2 * j + 1];
+        const float* ba = ra < 0 ? s.box + 6 * ~ra : s.ibox + 6 * ra;
+        const float* bb = rb < 0 ? s.box + 6 * ~rb : s.ibox + 6 * rb;
+        int ga = ra < 0 ? ~(i0 + ~ra) : nodebase + ra;
+        int gb = rb < 0 ? ~(i0 + ~rb) : nodebase + rb;
+        write_tlas_node(a.nodes, nodebase + j, ba, bb, ga, gb);
+    }
+}
+
+size_t tlas_smem_bytes(int n) {
+    if (n <= 1) return 16;
+    int P = 1;
+    while (P < n) P <<= 1;
+    return sizeof(uint64_t) * P + sizeof(float) * 6 * n + sizeof(float) * 6 * (n - 1) +
+           sizeof(int) * 2 * (n - 1) + sizeof(int) * (n - 1) + sizeof(int) * n + sizeof(int) * (n - 1);
+}
+
+}  // namespace
+
+cudaError_t instances_update(const TlasArgs& a, int n_inst, cudaStream_t stream) {
+    if (n_inst > 0) k_instances<<<(n_inst + 127) / 128, 128, 0, stream>>>(a, n_inst);
+    return cudaGetLastError();
+}
+
+cudaError_t tlas_build(const TlasArgs& a, bool rebuild, cudaStream_t stream) {
+    size_t smem = tlas_smem_bytes(a.max_n);
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(k_tlas, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    if (rebuild) {
+        cudaError_t e = cudaMemsetAsync(a.tlas_depth, 0, sizeof(int) * a.n_envs, stream);
+        if (e != cudaSuccess) return e;
+    }
+    k_tlas<<<a.n_envs, TLAS_THREADS, smem, stream>>>(a, rebuild ? 1 : 0);
+    return cudaGetLastError();
+}
+
+}  // namespace agr

@@ -1,0 +1,157 @@
+"""Structural checks of the GPU LBVH (BLAS) against brute force on small
+inputs (SURVEY.md §4 unit layer; §8(c) 'BVH pieces'): Morton codes of known
+points, sorted order, every non-degenerate face in exactly one leaf,
+boxes containing their children, Karras topology == recursive split."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import scenegen as sg
+from gpu_util import make_scene
+
+pytestmark = pytest.mark.gpu
+
+
+def _expand(v):
+    out = 0
+    for b in range(10):
+        out |= ((v >> b) & 1) << (3 * b)
+    return out
+
+
+def morton_ref(p):
+    """Independent bit-loop Morton code of a point in [0, 1]^3 (x in bit 2)."""
+    q = [min(int(np.floor(c * 1024.0)), 1023) for c in p]
+    q = [max(0, c) for c in q]
+    return (_expand(q[0]) << 2) | (_expand(q[1]) << 1) | _expand(q[2])
+
+
+def test_morton_ref_known_values():
+    assert morton_ref((0.9999, 0.9999, 0.9999)) == 0x3FFFFFFF
+    assert morton_ref((1 / 1024, 0, 0)) == 4  # lowest x bit lands in bit 2
+
+
+def _check_blas(mesh):
+    sc = sg.assemble([mesh], [[(0, 0, sg.make_T(np.eye(3), (0, 0, 0)))]])
+    s = make_scene(sc, build=False)
+    nodes, leaf_face, codes = s.debug_export_blas(0)
+    v = mesh.verts
+    tri = v[mesh.faces]
+    area2 = np.linalg.norm(np.cross((tri[:, 1] - tri[:, 0]).astype(np.float64),
+                                    (tri[:, 2] - tri[:, 0]).astype(np.float64)), axis=1)
+    valid = np.nonzero(area2 > 0)[0]
+    # every non-degenerate face in exactly one leaf
+    assert sorted(leaf_face.tolist()) == sorted(valid.tolist())
+    n = len(leaf_face)
+    # codes sorted, and equal to the Morton code of the centroid in the
+    # centroid bounds (computed independently here)
+    lo_t, hi_t = tri.min(1), tri.max(1)
+    cent = 0.5 * lo_t + 0.5 * hi_t
+    cv = cent[valid]
+    clo, chi = cv.min(0), cv.max(0)
+    ext = chi - clo
+    for i, f in enumerate(leaf_face):
+        u = [(cent[f][k] - clo[k]) / ext[k] if ext[k] > 0 else 0.0 for k in range(3)]
+        assert codes[i] == morton_ref(np.asarray(u, np.float32)), i
+    assert np.all(np.diff(codes.astype(np.int64)) >= 0)
+    # equal codes keep ascending face order (stable sort)
+    for i in range(n - 1):
+        if codes[i] == codes[i + 1]:
+            assert leaf_face[i] < leaf_face[i + 1]
+    if n < 2:
+        return nodes, leaf_face
+    # boxes: child boxes contain their subtree's triangles exactly
+    refs = nodes[:, 12:14].view(np.int32)
+
+    def box_of(ref):
+        if ref < 0:
+            f = leaf_face[~ref]
+            return lo_t[f], hi_t[f], [f]
+        b0lo, b0hi, f0 = box_of(refs[ref, 0])
+        b1lo, b1hi, f1 = box_of(refs[ref, 1])
+        nd = nodes[ref]
+        c0lo, c0hi = nd[[0, 2, 4]], nd[[1, 3, 5]]
+        c1lo, c1hi = nd[[6, 8, 10]], nd[[7, 9, 11]]
+        assert np.array_equal(c0lo, b0lo) and np.array_equal(c0hi, b0hi)
+        assert np.array_equal(c1lo, b1lo) and np.array_equal(c1hi, b1hi)
+        return np.minimum(b0lo, b1lo), np.maximum(b0hi, b1hi), f0 + f1
+
+    lo, hi, fs = box_of(0)
+    assert sorted(fs) == sorted(valid.tolist())
+    assert np.array_equal(lo, lo_t[valid].min(0)) and np.array_equal(hi, hi_t[valid].max(0))
+
+    # Karras topology == recursive split of the sorted keys (brute force)
+    keys = [(int(c) << 32) | i for i, c in enumerate(codes)]
+
+    def split(first, last):
+        a, b = keys[first], keys[last]
+        common = 64 - (a ^ b).bit_length()
+        s = first
+        for k in range(first, last):
+            if 64 - (a ^ keys[k + 1]).bit_length() > common:
+                s = k + 1
+            else:
+                break
+        return s
+
+    def rec(first, last):
+        """returns set of (lo, hi) leaf ranges of internal nodes"""
+        if first == last:
+            return []
+        sp = split(first, last)
+        return [(first, last)] + rec(first, sp) + rec(sp + 1, last)
+
+    def ranges(ref):
+        if ref < 0:
+            return (~ref, ~ref), []
+        (a0, b0), r0 = ranges(refs[ref, 0])
+        (a1, b1), r1 = ranges(refs[ref, 1])
+        assert b0 + 1 == a1
+        return (a0, b1), [(a0, b1)] + r0 + r1
+
+    (a, b), got = ranges(0)
+    assert (a, b) == (0, n - 1)
+    assert sorted(got) == sorted(rec(0, n - 1))
+    return nodes, leaf_face
+
+
+@pytest.mark.parametrize("mesh_fn", [
+    lambda: sg.cube_mesh(),
+    lambda: sg.closed_cylinder_92(),
+    lambda: sg.sphere_mesh(1.0, 2),
+    lambda: sg.tree_mesh(np.random.default_rng(1)),
+    lambda: sg.ground_mesh(),
+])
+def test_blas_structure(mesh_fn):
+    _check_blas(mesh_fn())
+
+
+def test_blas_duplicate_codes_and_degenerates():
+    """Many identical centroids (duplicate Morton codes) + zero-area faces."""
+    rng = np.random.default_rng(0)
+    base = rng.uniform(-1, 1, (3, 3)).astype(np.float32)
+    tris = np.concatenate([np.tile(base, (40, 1, 1)), rng.uniform(-1, 1, (30, 3, 3)).astype(np.float32)])
+    tris[5, 2] = tris[5, 1]  # degenerate (repeated vertex)
+    tris[50, 1] = tris[50, 0]
+    v = tris.reshape(-1, 3)
+    f = np.arange(len(v), dtype=np.int32).reshape(-1, 3)
+    _check_blas(sg.Mesh("dup", v, f))
+
+
+def test_blas_single_triangle_and_flat_axis():
+    v = np.asarray([[0, 0, 0], [1, 0, 0], [0, 1, 0]], np.float32)
+    nodes, lf = _check_blas(sg.Mesh("one", v, np.asarray([[0, 1, 2]], np.int32)))
+    assert list(lf) == [0]
+
+
+def test_large_mesh_multiblock_sort():
+    """A mesh big enough for a multi-block radix sort (> 1024 keys per tile)."""
+    m = sg.sphere_mesh(2.0, 5)  # 20480 faces
+    sc = sg.assemble([m], [[(0, 0, sg.make_T(np.eye(3), (0, 0, 0)))]])
+    s = make_scene(sc, build=False)
+    nodes, leaf_face, codes = s.debug_export_blas(0)
+    assert sorted(leaf_face.tolist()) == list(range(len(m.faces)))
+    assert np.all(np.diff(codes.astype(np.int64)) >= 0)
+    for i in np.nonzero(np.diff(codes.astype(np.int64)) == 0)[0]:
+        assert leaf_face[i] < leaf_face[i + 1]

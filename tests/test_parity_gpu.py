@@ -1,0 +1,296 @@
+"""GPU parity: the CUDA path (through the C ABI) against the FP64 oracle,
+element by element on seeded inputs (SURVEY.md §8(c) parity rules):
+  distance within max(1e-5 m, 1e-6 * ref) on every ray;
+  seg / face bit-exact on every ray the oracle does not flag ambiguous.
+Small configs are compared in full; BASELINE's full-size configs are cast
+in the launch configuration bench.py times and compared on sampled rays.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_2503_01471_b200 as agr
+import scenegen as sg
+from helpers import compare, oracle_rays
+from gpu_util import cast_sensor, dev, make_scene, to_np
+
+pytestmark = pytest.mark.gpu
+
+
+def _check_full(sc, sensor, kind="depth", what=""):
+    s = make_scene(sc)
+    got = to_np(cast_sensor(s, sensor, kind))
+    ref = oracle.cast(sc, oracle_rays(sensor, kind))
+    res = compare(ref, got["dist"], got["seg"], got["face"], what)
+    s.close()
+    return res, got, ref
+
+
+@pytest.mark.parametrize("kind", ["depth", "range"])
+def test_c1_full(kind):
+    sc, sensor = sg.config1()
+    res, got, ref = _check_full(sc, sensor, kind, f"c1 {kind}")
+    d = got["dist"].reshape(16, 16)
+    assert np.all(d[6:10, 6:10] < 3.0) and d[0, 0] == 10.0
+    if kind == "depth":
+        assert np.all(d[6:10, 6:10] == 2.0)
+
+
+@pytest.mark.parametrize("kind", ["depth", "range"])
+def test_c2_full(kind):
+    sc, sensor = sg.config2()
+    res, got, ref = _check_full(sc, sensor, kind, f"c2 {kind}")
+    assert (ref.face >= 0).mean() > 0.1
+
+
+def test_ragged_multisensor_random_poses():
+    """Image sizes that are not tile multiples, 2 sensors per env, random poses."""
+    sc, sensor = sg.config2(n_envs=6)
+    rng = np.random.default_rng(3)
+    poses = np.zeros((6, 2, 3, 4), np.float32)
+    for e in range(6):
+        for k in range(2):
+            poses[e, k] = sg.make_T(sg.rot_z(rng.uniform(-0.6, 0.6)) @ sg.rot_y(rng.uniform(-0.3, 0.3)),
+                                    rng.uniform([-1, -1, -1], [1, 1, 1]))
+    sensor = dict(sensor, poses=poses, cam=sg.pinhole(37, 19, 100.0))
+    for kind in ("depth", "range"):
+        _check_full(sc, sensor, kind, f"ragged {kind}")
+
+
+def test_explicit_rays_random():
+    sc, _ = sg.config2(n_envs=8)
+    rng = np.random.default_rng(7)
+    R = 4000
+    o = rng.uniform([-1, -3, -2], [4, 3, 2], (8, R, 3)).astype(np.float32)
+    tgt = rng.uniform([2, -3, -1.5], [8, 3, 1.5], (8, R, 3))
+    d = (tgt - o).astype(np.float32)
+    s = make_scene(sc)
+    out = s.cast_rays(torch.from_numpy(o).to(dev()), torch.from_numpy(d).to(dev()), 2.0)
+    got = to_np(out)
+    ref = oracle.cast(sc, dict(model=oracle.RAYS, orig=o, dir=d, max_range=2.0))
+    compare(ref, got["dist"], got["seg"], got["face"], "rays")
+
+
+def _edge_targeted_rays(sc, n_per_env, rng, eps_list=(0.0, 1e-7, -1e-7, 1e-6, -1e-6, 1e-5, -1e-5)):
+    """Rays aimed at points on triangle edges and vertices (world space, FP64),
+    nudged across the edge by eps (relative to the edge length): the cases
+    where an FP32 test could flip hit <-> miss."""
+    E = sc.n_envs
+    o = np.zeros((E, n_per_env, 3), np.float32)
+    d = np.zeros((E, n_per_env, 3), np.float32)
+    verts, faces = sc.verts.astype(np.float64), sc.faces
+    voff, foff = sc.vert_off, sc.face_off
+    for e in range(E):
+        j0, j1 = sc.env_off[e], sc.env_off[e + 1]
+        for r in range(n_per_env):
+            j = rng.integers(j0, j1)
+            a = sc.inst_asset[j]
+            f = rng.integers(foff[a], foff[a + 1])
+            T = sc.inst_T[j].astype(np.float64)
+            tri = verts[voff[a] + faces[f]] @ T[:, :3].T + T[:, 3]
+            k = rng.integers(0, 3)
+            p0, p1, p2 = tri[k], tri[(k + 1) % 3], tri[(k + 2) % 3]
+            w = rng.uniform(0, 1) if rng.uniform() < 0.8 else float(rng.integers(0, 2))
+            on_edge = p0 + w * (p1 - p0)
+            inward = (p2 - on_edge)
+            eps = eps_list[rng.integers(0, len(eps_list))]
+            target = on_edge + eps * inward
+            org = rng.uniform([-1, -3, -2], [1.5, 3, 2])
+            o[e, r] = org
+            d[e, r] = target - org
+    return o, d
+
+
+def test_edge_and_vertex_targeted_rays():
+    """Silhouette and shared-edge rays: the FP32 filter must defer every
+    decision it cannot certify, so seg/face stay exact off the near-ties."""
+    sc, _ = sg.config2(n_envs=16)
+    rng = np.random.default_rng(11)
+    o, d = _edge_targeted_rays(sc, 3000, rng)
+    s = make_scene(sc)
+    got = to_np(s.cast_rays(torch.from_numpy(o).to(dev()), torch.from_numpy(d).to(dev()), 12.0))
+    ref = oracle.cast(sc, dict(model=oracle.RAYS, orig=o, dir=d, max_range=12.0))
+    res = compare(ref, got["dist"], got["seg"], got["face"], "edge rays")
+    assert res["ambiguous"] > 100  # the generator really produces near-ties
+
+
+def test_exact_mode_equals_filter_mode():
+    """FP32 filter + FP64 arbitration == all-FP64 traversal, bitwise."""
+    sc, sensor = sg.config2(n_envs=16)
+    s = make_scene(sc)
+    a = to_np(cast_sensor(s, sensor, "range"))
+    s.set_exact_mode(True)
+    b = to_np(cast_sensor(s, sensor, "range"))
+    for k in a:
+        assert np.array_equal(a[k], b[k]), k
+
+
+def test_refit_equals_rebuild_and_repeat_is_deterministic():
+    """After new transforms, refit (old topology) == rebuild, bitwise; a
+    repeated cast is bitwise identical (SURVEY.md §8(c) GPU self-invariants)."""
+    sc, sensor = sg.config5(n_envs=32, ring=3)
+    ring = sc.extra["ring_T"]
+    s = make_scene(sc)
+    for step in (1, 2):
+        s.set_instance_transforms(torch.from_numpy(ring[step]).to(dev()))
+        s.refit()
+        a = to_np(cast_sensor(s, sensor, "depth"))
+        a2 = to_np(cast_sensor(s, sensor, "depth"))
+        s.set_instance_transforms(torch.from_numpy(ring[step]).to(dev()))
+        s.build()
+        b = to_np(cast_sensor(s, sensor, "depth"))
+        for k in a:
+            assert np.array_equal(a[k], a2[k]) and np.array_equal(a[k], b[k]), (step, k)
+        sc2 = sg.Scene(sc.meshes, sc.env_off, sc.inst_asset, sc.inst_label, ring[step])
+        ref = oracle.cast(sc2, oracle_rays(sensor, "depth"))
+        compare(ref, a["dist"], a["seg"], a["face"], f"c5 step {step}")
+
+
+def test_null_channels_and_channel_independence():
+    sc, sensor = sg.config2(n_envs=4)
+    s = make_scene(sc)
+    full = to_np(cast_sensor(s, sensor))
+    only_d = to_np(cast_sensor(s, sensor, channels=("dist",)))
+    only_f = to_np(cast_sensor(s, sensor, channels=("face",)))
+    assert np.array_equal(full["dist"], only_d["dist"])
+    assert np.array_equal(full["face"], only_f["face"])
+
+
+def test_empty_and_single_instance_envs():
+    """Envs with 0, 1 and several instances side by side."""
+    cube = sg.cube_mesh()
+    per_env = [[], [(0, 3, sg.make_T(np.eye(3), (3, 0, 0)))],
+               [(0, 4, sg.make_T(sg.rot_z(0.3), (4, 0.5, 0), 1.2)),
+                (0, 5, sg.make_T(np.eye(3), (2.5, -0.6, 0.2), 0.5))], []]
+    sc = sg.assemble([cube], per_env)
+    sensor = dict(kind="pinhole", cam=sg.pinhole(24, 16, 90.0), poses=sg.identity_poses(4),
+                  max_range=10.0)
+    res, got, ref = _check_full(sc, sensor, "depth", "empty/single")
+    assert np.all(got["seg"].reshape(4, -1)[0] == -1) and np.all(got["seg"].reshape(4, -1)[3] == -1)
+    assert (got["seg"].reshape(4, -1)[1] == 3).any()
+
+
+def test_degenerate_faces_and_max_range_boundary():
+    v = np.asarray([[0, -5, -5], [0, 5, -5], [0, 5, 5], [0, -5, 5]], np.float32)
+    m = sg.Mesh("q", v, np.asarray([[0, 1, 1], [0, 2, 2], [0, 1, 2], [0, 2, 3]], np.int32))
+    sc = sg.assemble([m], [[(0, 1, sg.make_T(np.eye(3), (10.0, 0, 0)))],
+                           [(0, 2, sg.make_T(np.eye(3), (10.0 + 2e-6, 0, 0)))],
+                           [(0, 3, sg.make_T(np.eye(3), (9.99, 0, 0)))]])
+    o = np.zeros((3, 64, 3), np.float32)
+    rng = np.random.default_rng(1)
+    d = np.concatenate([np.ones((3, 64, 1)), rng.uniform(-0.3, 0.3, (3, 64, 2))], -1).astype(np.float32)
+    s = make_scene(sc)
+    got = to_np(s.cast_rays(torch.from_numpy(o).to(dev()), torch.from_numpy(d).to(dev()), 10.0))
+    ref = oracle.cast(sc, dict(model=oracle.RAYS, orig=o, dir=d, max_range=10.0))
+    compare(ref, got["dist"], got["seg"], got["face"], "degenerate/max-range")
+    f = got["face"].reshape(3, 64)
+    assert set(np.unique(f[2])) <= {2, 3}
+
+
+def test_lidar_beams_small():
+    sc, sensor = sg.config4(n_envs=8)
+    sensor = dict(sensor, beams=sg.lidar_beams(32, 64))
+    _check_full(sc, sensor, "range", "c4 small")
+
+
+def test_dome_lidar_small():
+    sc, sensor = sg.config4(n_envs=4)
+    sensor = dict(sensor, beams=sg.dome_beams(16, 48))
+    _check_full(sc, sensor, "range", "dome")
+
+
+def test_host_buffer_path_equals_device_path():
+    """agr_cast_pinhole_host (H2D poses, chunked cast, D2H images) gives the
+    device path's bytes."""
+    sc, sensor = sg.config2(n_envs=20)
+    s = make_scene(sc)
+    a = to_np(cast_sensor(s, sensor, "depth"))
+    poses = torch.from_numpy(np.ascontiguousarray(sensor["poses"])).pin_memory()
+    out = s.cast_pinhole_host(sensor["cam"], poses, sensor["max_range"], agr.AGR_DEPTH)
+    for k in a:
+        assert np.array_equal(a[k], out[k].numpy().reshape(-1)), k
+    # pageable host outputs take the staging path
+    H, W = sensor["cam"]["H"], sensor["cam"]["W"]
+    pageable = {k: torch.empty((20, 1, H, W), dtype=torch.float32 if k == "dist" else torch.int32)
+                for k in ("dist", "seg", "face")}
+    s.cast_pinhole_host(sensor["cam"], poses.clone(), sensor["max_range"], agr.AGR_DEPTH, out=pageable)
+    for k in a:
+        assert np.array_equal(a[k], pageable[k].numpy().reshape(-1)), k
+    beams = sg.lidar_beams(16, 32)
+    sc4, s4sensor = sg.config4(n_envs=5)
+    s4 = make_scene(sc4)
+    dev_out = to_np(cast_sensor(s4, dict(s4sensor, beams=beams), "range"))
+    host_out = s4.cast_beams_host(torch.from_numpy(beams), torch.from_numpy(s4sensor["poses"]),
+                                  s4sensor["max_range"])
+    for k in dev_out:
+        assert np.array_equal(dev_out[k], host_out[k].numpy().reshape(-1)), k
+
+
+def test_checksums_independent_of_sharding():
+    """Per-env checksums of one scene == those of the same envs split into two
+    scenes (the 1-GPU vs n-GPU bitwise check, run on one GPU)."""
+    sc, sensor = sg.config2(n_envs=12)
+    s = make_scene(sc)
+    out = cast_sensor(s, sensor)
+    per_env = sensor["cam"]["W"] * sensor["cam"]["H"]
+    full = s.checksum(out, per_env).cpu().numpy()
+    parts = []
+    for e0, e1 in ((0, 5), (5, 12)):
+        sub = sc.env_slice(e0, e1)
+        ss = make_scene(sub)
+        o = cast_sensor(ss, dict(sensor, poses=sensor["poses"][e0:e1]))
+        parts.append(ss.checksum(o, per_env).cpu().numpy())
+    assert np.array_equal(full, np.concatenate(parts))
+    assert len(set(full.tolist())) == 12
+
+
+# ---- BASELINE full-size configs, sampled -------------------------------------
+
+def _sampled(sc, sensor, kind, n_sample, seed, what):
+    s = make_scene(sc)
+    got = to_np(cast_sensor(s, sensor, kind))
+    n = len(got["dist"])
+    q = np.random.default_rng(seed).choice(n, n_sample, replace=False)
+    ref = oracle.cast(sc, oracle_rays(sensor, kind), query=q)
+    res = compare(ref, got["dist"][q], got["seg"][q], got["face"][q], what)
+    s.close()
+    return res, got
+
+
+@pytest.mark.slow
+def test_c3_full_size_sampled():
+    """c3: 1024 envs, 270x480 depth camera, forest (bench workload)."""
+    sc, sensor = sg.config3()
+    res, got = _sampled(sc, sensor, "depth", 30000, 3, "c3")
+    hit = got["face"] >= 0
+    assert 0.3 < hit.mean() < 0.99
+    # every output is either max range or a plausible depth
+    assert np.all((got["dist"] > 0) & (got["dist"] <= 10.0))
+
+
+@pytest.mark.slow
+def test_c4_full_size_sampled():
+    sc, sensor = sg.config4()
+    _sampled(sc, sensor, "range", 40000, 4, "c4")
+
+
+@pytest.mark.slow
+def test_c5_sampled_with_refit_steps():
+    """c5 (per GPU at 8 GPUs: 2048 envs), obstacles re-posed every step."""
+    sc, sensor = sg.config5(n_envs=2048, ring=4)
+    ring = sc.extra["ring_T"]
+    s = make_scene(sc)
+    rng = np.random.default_rng(5)
+    for step in range(1, 4):
+        s.set_instance_transforms(torch.from_numpy(ring[step]).to(dev()))
+        s.refit()
+        got = to_np(cast_sensor(s, sensor, "depth"))
+        q = rng.choice(len(got["dist"]), 20000, replace=False)
+        sc2 = sg.Scene(sc.meshes, sc.env_off, sc.inst_asset, sc.inst_label, ring[step])
+        ref = oracle.cast(sc2, oracle_rays(sensor, "depth"), query=q)
+        compare(ref, got["dist"][q], got["seg"][q], got["face"][q], f"c5 step {step}")
