@@ -1,0 +1,412 @@
+#!/usr/bin/env python
+"""Benchmark of the batched ray-casting hot path (BASELINE.json metric:
+rays/sec and env-frames/sec at 1/2/4/8 B200; % of roofline).
+
+One step = one pass of the whole per-step hot path over one batch of envs
+(SURVEY.md §8(a)): set the instance transforms (a3) + per-env TLAS build
+(a2; c5 uses the in-place refit) + one fused cast (a4 ray generation, a5
+traversal, a6 FP64 epilogue + stores).  The per-asset BLAS (a1) is built
+once at scene creation, as in the paper (the BVH is computed
+"exclusively for randomization").
+
+Default workload (N=1): config 3 -- 1024 envs per GPU, forest scene (ground
++ 40 trees + 10 rocks, ~56k triangles per env), 270x480 D455-like depth
+camera, depth + segmentation + face index (BASELINE.json configs[2], the
+north-star target).  Multi-GPU: one process per GPU (torchrun), each rank
+casts its own block of envs (weak scaling: per-GPU work fixed); the step
+time is the max over ranks; no data-path collective (envs are independent,
+PAPER.md:226).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 3|4|5]
+    python bench.py --impl reference ...   # the CPU oracle arm
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import scenegen as sg  # noqa: E402
+
+METRIC = "rays/sec and env-frames/sec at 1/2/4/8 B200; % of HBM/FP32 roofline"
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+TRAFFIC_PATH = os.path.join(ROOT, "profiles", "cast_traffic.json")
+
+# Algorithmic thread-instruction costs of one unit of traversal work
+# (DESIGN.md §8 "ALU roofline"): per child box test, per
+# stack pop, per triangle test, per instance entry, per ray (generation +
+# epilogue).  Multiplied by the counted units of a launch.
+C_BOX, C_LOOP, C_TRI, C_XF, C_RAY = 20, 15, 40, 25, 70
+
+WORKLOADS = {
+    3: "c3: forest, 1024 envs/GPU (ground + 40 trees + 10 rocks, ~56k tri/env), "
+       "270x480 D455-like pinhole (87 deg hfov) depth + seg + face, max 10 m",
+    4: "c4: Table II-shaped room + 15 floating obstacles, 512 envs/GPU (4096 over 8 GPUs), "
+       "OS0-128-style LiDAR 128x512 range + seg, max 10 m",
+    5: "c5: Table I-shaped 20 cubes/env re-posed every step (TLAS refit), 2048 envs/GPU "
+       "(16384 over 8 GPUs), 135x240 depth + seg + face, max 10 m",
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=3, choices=[3, 4, 5])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--envs", type=int, default=None, help="envs per GPU (default: config's)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-counters", action="store_true")
+    ap.add_argument("--traversal", default="auto", choices=["auto", "lane"],
+                    help="auto: warp packets for camera / LiDAR tiles; lane: one ray per lane")
+    return ap.parse_args()
+
+
+def envs_per_gpu(args):
+    if args.envs:
+        return args.envs
+    return {3: 1024, 4: 512, 5: 2048}[args.config]
+
+
+def make_workload(cfg, n_envs, env_base):
+    if cfg == 3:
+        return sg.config3(n_envs=n_envs, env_base=env_base)
+    if cfg == 4:
+        return sg.config4(n_envs=n_envs, env_base=env_base)
+    return sg.config5(n_envs=n_envs, env_base=env_base, ring=8)
+
+
+def rays_per_env(sensor):
+    if sensor["kind"] == "pinhole":
+        return sensor["cam"]["W"] * sensor["cam"]["H"] * sensor["poses"].shape[1]
+    return sensor["beams"].shape[0] * sensor["beams"].shape[1] * sensor["poses"].shape[1]
+
+
+def channels_for(cfg):
+    return ("dist", "seg") if cfg == 4 else ("dist", "seg", "face")
+
+
+# --------------------------------------------------------------------------
+# clocks sampled during the timed region (NVML)
+# --------------------------------------------------------------------------
+class ClockSampler:
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+        0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+        0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception as e:  # pragma: no cover
+            self.nv = None
+            self.err = str(e)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.05)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.nv:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.nv:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+# --------------------------------------------------------------------------
+# CPU oracle (reported baseline; never the target)
+# --------------------------------------------------------------------------
+def oracle_rate(sc, sensor, kind, n_rays, seed):
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import oracle
+    from helpers import oracle_rays
+    total = sc.n_envs * rays_per_env(sensor)
+    q = np.random.default_rng(seed).choice(total, min(n_rays, total), replace=False)
+    t0 = time.perf_counter()
+    r = oracle.cast(sc, oracle_rays(sensor, kind), query=q)
+    dt = time.perf_counter() - t0
+    return len(q) / dt, r.tests / dt, dt, len(q)
+
+
+def cpu_cores():
+    return os.cpu_count() or 1
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    cfg = args.config
+    E = envs_per_gpu(args)
+    sc, sensor = make_workload(cfg, E, 0)
+    kind = "range" if cfg == 4 else "depth"
+    per_step = {3: 2500, 4: 20000, 5: 20000}[cfg]
+    for w in range(args.warmup):
+        oracle_rate(sc, sensor, kind, per_step // 4, 100 + w)
+    times, rays = [], 0
+    for k in range(args.steps):
+        _, _, dt, n = oracle_rate(sc, sensor, kind, per_step, 1000 + k)
+        times.append(dt)
+        rays += n
+    tot = sum(times)
+    value = rays / tot
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "rays/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000 * tot / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOADS[cfg], "envs_per_gpu": E,
+                   "rays_per_step": per_step, "sample": "uniform random rays of the workload"},
+        "cpu_baseline": {"value": value, "unit": "rays/s", "cores": cpu_cores(), "kind": "oracle",
+                         "sample": f"{per_step} random rays per step of the {E}-env workload"},
+        "e2e": {"value": value, "unit": "rays/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+# --------------------------------------------------------------------------
+# our arm
+# --------------------------------------------------------------------------
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+    import paper_2503_01471_b200 as agr
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE={world}"
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    cfg = args.config
+    E = envs_per_gpu(args)
+    sc, sensor = make_workload(cfg, E, rank * E)  # this rank's block of global envs
+    kind = agr.AGR_RANGE if cfg == 4 else agr.AGR_DEPTH
+    chans = channels_for(cfg)
+    scene = agr.Scene.from_scenegen(sc, device=local)
+    scene.set_traversal(0 if args.traversal == "auto" else 1)
+    rpe = rays_per_env(sensor)
+    rays_per_step = E * rpe
+    # inputs resident in HBM before timing
+    if cfg == 5:
+        ring = torch.from_numpy(sc.extra["ring_T"]).to(dev)
+        T_steps = [ring[k] for k in range(ring.shape[0])]
+    else:
+        T_steps = [torch.from_numpy(sc.inst_T).to(dev)]
+    poses = torch.from_numpy(sensor["poses"]).to(dev)
+    beams = torch.from_numpy(sensor["beams"]).to(dev) if sensor["kind"] == "beams" else None
+    scene.set_instance_transforms(T_steps[0])
+    scene.build()
+    shape = (E, poses.shape[1]) + ((sensor["cam"]["H"], sensor["cam"]["W"]) if beams is None
+                                   else tuple(beams.shape[:2]))
+    out = {c: torch.empty(shape, dtype=torch.float32 if c == "dist" else torch.int32, device=dev)
+           for c in chans}
+    stream = torch.cuda.current_stream(dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def step(k):
+        scene.set_instance_transforms(T_steps[k % len(T_steps)], stream)
+        if cfg == 5:
+            scene.refit(stream)
+        else:
+            scene.build(stream)
+        if beams is None:
+            scene.cast_pinhole(sensor["cam"], poses, sensor["max_range"], kind, out=out, stream=stream)
+        else:
+            scene.cast_beams(beams, poses, sensor["max_range"], out=out, stream=stream)
+
+    LAUNCHES_PER_STEP = 3  # k_instances + k_tlas + k_cast
+    for w in range(args.warmup):
+        step(w)
+    torch.cuda.synchronize()
+
+    # ---- timed region: K steps, L2 flushed (untimed) between steps -------
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+           torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            flush.zero_()
+            e0, e1, e2 = ev[k]
+            e0.record(stream)
+            scene.set_instance_transforms(T_steps[k % len(T_steps)], stream)
+            if cfg == 5:
+                scene.refit(stream)
+            else:
+                scene.build(stream)
+            e1.record(stream)
+            if beams is None:
+                scene.cast_pinhole(sensor["cam"], poses, sensor["max_range"], kind, out=out, stream=stream)
+            else:
+                scene.cast_beams(beams, poses, sensor["max_range"], out=out, stream=stream)
+            e2.record(stream)
+        torch.cuda.synchronize()
+    step_ms = [a.elapsed_time(c) for a, b, c in ev]
+    cast_ms = [b.elapsed_time(c) for a, b, c in ev]
+    total_ms = sum(step_ms)
+    cast_total = sum(cast_ms)
+    t = torch.tensor([total_ms, cast_total], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.barrier()
+    total_ms, cast_total = float(t[0]), float(t[1])
+    ms_per_step = total_ms / args.steps
+    value = rays_per_step * world / (total_ms / 1e3 / args.steps)
+
+    # ---- per-ray work counters (separate, untimed counting launch) --------
+    counters = None
+    if not args.no_counters:
+        scene.enable_counters(True)
+        step(0)
+        torch.cuda.synchronize()
+        counters = scene.counters()
+        scene.enable_counters(False)
+
+    # ---- end to end through the public C ABI with host buffers ------------
+    e2e = None
+    if not args.no_e2e:
+        poses_h = torch.from_numpy(sensor["poses"]).pin_memory()
+        out_h = {c: torch.empty(shape, dtype=torch.float32 if c == "dist" else torch.int32,
+                                pin_memory=True) for c in chans}
+        beams_h = torch.from_numpy(sensor["beams"]).pin_memory() if beams is not None else None
+
+        def e2e_step(k):
+            scene.set_instance_transforms(T_steps[k % len(T_steps)], stream)
+            scene.refit(stream) if cfg == 5 else scene.build(stream)
+            stream.synchronize()
+            if beams_h is None:
+                scene.cast_pinhole_host(sensor["cam"], poses_h, sensor["max_range"], kind, out=out_h)
+            else:
+                scene.cast_beams_host(beams_h, poses_h, sensor["max_range"], out=out_h)
+
+        for w in range(min(args.warmup, 2)):
+            e2e_step(w)
+        n_e2e = max(3, min(args.steps, 10))
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for k in range(n_e2e):
+            e2e_step(k)
+        dt = time.perf_counter() - t0
+        tt = torch.tensor([dt], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        dt = float(tt[0])
+        h2d = poses_h.numel() * 4 + (beams_h.numel() * 4 if beams_h is not None else 0)
+        d2h = sum(v.numel() * 4 for v in out_h.values())
+        e2e = {"value": rays_per_step * world * n_e2e / dt, "unit": "rays/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": n_e2e,
+               "note": "agr_cast_*_host: H2D poses, chunked cast, D2H of every output image"}
+
+    if world > 1:
+        dist.destroy_process_group()
+    if rank != 0:
+        return 0
+
+    # ---- roofline of the dominant kernel (k_cast) -------------------------
+    peaks = json.load(open(PEAKS_PATH)) if os.path.exists(PEAKS_PATH) else {}
+    clocks = clk.summary()
+    cast_s = cast_total / 1e3 / args.steps  # per launch (per rank)
+    roof = None
+    if counters and counters["rays"] > 0:
+        per = {k: counters[k] / counters["rays"] for k in ("nodes", "leaves", "instances")}
+        pops = per["nodes"] + per["leaves"] + per["instances"]
+        w_ray = 2 * C_BOX * per["nodes"] + C_LOOP * pops + C_TRI * per["leaves"] + \
+            C_XF * per["instances"] + C_RAY
+        achieved = w_ray * rays_per_step / cast_s / 1e12
+        mhz = clocks.get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)
+        peak = 148 * 128 * mhz * 1e6 / 1e12
+        traffic = None
+        if os.path.exists(TRAFFIC_PATH):
+            traffic = json.load(open(TRAFFIC_PATH)).get(f"c{cfg}")
+        roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tinst/s",
+                "frac": achieved / peak, "traffic": traffic,
+                "kernel": "k_cast", "kernel_ms": 1e3 * cast_s,
+                "work_per_ray_inst": w_ray, "per_ray": per,
+                "peak_note": "148 SMs x 128 FP32/INT lanes x measured median SM clock "
+                             "(DESIGN.md §8); algorithmic instr = counted units x unit costs"}
+        out_bytes = rays_per_step * 4 * len(chans)
+        hbm_peak = peaks.get("hbm_gbs", 6553.3)
+        roof["hbm"] = {"achieved_gbs": out_bytes / cast_s / 1e9, "peak_gbs": hbm_peak,
+                       "frac": out_bytes / cast_s / 1e9 / hbm_peak,
+                       "bytes_per_launch": out_bytes, "peak_note": "of measured (MEASURED_PEAKS.json)"}
+
+    cpu = None
+    if not args.no_cpu_baseline:
+        kind_s = "range" if cfg == 4 else "depth"
+        n_cpu = {3: 40000, 4: 200000, 5: 200000}[cfg]
+        rate, tests_rate, dt, n = oracle_rate(sc, sensor, kind_s, n_cpu, 7)
+        cpu = {"value": rate, "unit": "rays/s", "cores": cpu_cores(), "kind": "oracle",
+               "sample": f"{n} uniform random rays of this rank's {E}-env workload ({dt:.1f} s wall)",
+               "tri_tests_per_s": tests_rate}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "rays/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32+f64",
+        "data": "synthetic",
+        "config": {"workload": WORKLOADS[cfg], "envs_per_gpu": E, "rays_per_step_per_gpu": rays_per_step,
+                   "channels": list(chans), "parallelism": f"env-sharded x{world}",
+                   "l2": "flushed between timed steps (256 MB write, untimed); step = "
+                         "set_transforms + TLAS " + ("refit" if cfg == 5 else "build") + " + cast"},
+        "env_frames_per_sec": E * poses.shape[1] * world / (ms_per_step / 1e3),
+        "cast_ms_per_step": cast_total / args.steps,
+        "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+        "gpu_launches": LAUNCHES_PER_STEP * args.steps, "clocks": clocks,
+        "counters_per_ray": ({k: v / counters["rays"] for k, v in counters.items() if k != "rays"}
+                             if counters else None),
+    }
+    print(json.dumps(line))
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -224,6 +224,13 @@ agr_status agr_checksum(agr_scene scene, agr_outputs out, int64_t elems_per_env,
 agr_status agr_set_exact_mode(agr_scene scene, int32_t exact);
 
 /*
+ * Traversal schedule (results are identical either way): 0 = auto (default;
+ * the 32 rays of an 8x4 pinhole / beam tile traverse as one warp packet),
+ * 1 = one independent ray per lane.  Explicit rays always use 1.
+ */
+agr_status agr_set_traversal(agr_scene scene, int32_t mode);
+
+/*
  * Counters of the last cast (test / profiling hook; device-side counters
  * are collected only when enabled):  counters[0] rays, [1] internal nodes
  * visited, [2] leaf (triangle) tests, [3] instance entries, [4] FP64

@@ -21,6 +21,8 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "lib", "libagr.so")
+# experiments only: load an alternative build of the same library
+LIB_PATH = os.environ.get("AGR_LIB_PATH", LIB_PATH)
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "agr.h")
 
 AGR_OK, AGR_EINVAL, AGR_ENOMEM, AGR_ECUDA, AGR_ESTATE, AGR_EUNSUPPORTED = 0, -1, -2, -3, -4, -5
@@ -83,6 +85,7 @@ _SIGS = {
     "agr_cast_beams_host": (_I32, [_P, _P, _I32, _I32, _P, _I32, ctypes.c_float, agr_outputs]),
     "agr_checksum": (_I32, [_P, agr_outputs, ctypes.c_int64, _P, _P]),
     "agr_set_exact_mode": (_I32, [_P, _I32]),
+    "agr_set_traversal": (_I32, [_P, _I32]),
     "agr_enable_counters": (_I32, [_P, _I32]),
     "agr_get_counters": (_I32, [_P, _P]),
     "agr_debug_export_blas": (_I32, [_P, _I32, _P, _P, _P, ctypes.POINTER(ctypes.c_int64),
@@ -288,6 +291,10 @@ class Scene:
     # ---- test / profiling hooks --------------------------------------------
     def set_exact_mode(self, exact: bool):
         _check(load().agr_set_exact_mode(self.handle, 1 if exact else 0))
+
+    def set_traversal(self, mode: int):
+        """0 auto (warp packets for pinhole / beam tiles), 1 per-lane rays."""
+        _check(load().agr_set_traversal(self.handle, int(mode)))
 
     def enable_counters(self, enable: bool):
         _check(load().agr_enable_counters(self.handle, 1 if enable else 0))

@@ -87,6 +87,7 @@ struct agr_scene_s {
     unsigned long long* counters = nullptr;
     bool built = false, dirty = false;
     int exact = 0;
+    int traversal = 0;  // 0 auto (warp packets for pinhole / beams), 1 per-lane
     bool counting = false;
     // end-to-end staging (lazily allocated)
     cudaStream_t e2e_stream[2] = {nullptr, nullptr};
@@ -443,6 +444,7 @@ static agr_status check_cast_state(agr_scene s, float max_range) {
 static agr_status run_cast(agr_scene s, CastArgs& a, cudaStream_t st) {
     a.sv = s->view();
     a.exact = s->exact;
+    a.packet = s->traversal == 0 ? 1 : 0;
     a.counters = nullptr;
     if (s->counting) {
         CK(cudaMemsetAsync(s->counters, 0, sizeof(unsigned long long) * 8, st));
@@ -595,6 +597,7 @@ static agr_status e2e_run(agr_scene s, CastArgs& a, int64_t elems_per_env, agr_o
         if (out_host.face) { c.out_face = (int*)p; p += 4 * n; }
         c.sv = s->view();
         c.exact = s->exact;
+        c.packet = s->traversal == 0 ? 1 : 0;
         c.counters = nullptr;
         CK(cast_launch(c, cs));
         CK(cudaEventRecord(s->e2e_event[slot], cs));
@@ -695,6 +698,14 @@ agr_status agr_set_exact_mode(agr_scene s, int32_t exact) {
     g_err.clear();
     if (!s) return fail(AGR_EINVAL, "scene is NULL");
     s->exact = exact ? 1 : 0;
+    return AGR_OK;
+}
+
+agr_status agr_set_traversal(agr_scene s, int32_t mode) {
+    g_err.clear();
+    if (!s) return fail(AGR_EINVAL, "scene is NULL");
+    if (mode != 0 && mode != 1) return fail(AGR_EINVAL, "traversal mode must be 0 or 1");
+    s->traversal = mode;
     return AGR_OK;
 }
 

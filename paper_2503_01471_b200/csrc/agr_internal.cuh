@@ -182,6 +182,7 @@ struct CastArgs {
     int out_env_base;        // outputs are indexed from this env (0: global indexing)
     unsigned long long* counters;  // optional [8]
     int exact;
+    int packet;           // 1: warp-packet traversal for pinhole / beams tiles
 };
 cudaError_t cast_launch(const CastArgs& a, cudaStream_t stream);
 

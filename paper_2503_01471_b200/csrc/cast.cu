@@ -29,6 +29,9 @@ namespace agr {
 namespace {
 
 constexpr int CAST_THREADS = 128;
+#ifndef CAST_MIN_BLOCKS
+#define CAST_MIN_BLOCKS 8
+#endif
 constexpr int NSLOT = 4;
 constexpr int SENTINEL = REF_EMPTY;  // "return to the TLAS" marker on the stack
 
@@ -41,10 +44,18 @@ struct SlabRay {
     float hix, hiy, hiz;      // -(o - delta) * id
 };
 
+// Approximate reciprocal (MUFU.RCP, ~1 ulp): every FP32 quantity it feeds is
+// covered by the error budget of DESIGN.md §5.2, so no IEEE division.
+__device__ __forceinline__ float rcp_approx(float x) {
+    float r;
+    asm("rcp.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
 __device__ __forceinline__ float safe_inv(float d) {
     float ad = fabsf(d);
     float dd = ad < 1e-20f ? copysignf(1e-20f, d) : d;
-    return __frcp_rn(dd);
+    return rcp_approx(dd);
 }
 
 __device__ __forceinline__ SlabRay make_slab(f3 o, f3 d, float delta) {
@@ -106,14 +117,13 @@ __device__ __forceinline__ bool test64(const SceneView& sv, int inst, int leaf, 
     return t > 0.0 && t <= tmax;
 }
 
-// ---- per-lane candidate list ---------------------------------------------------
+// ---- per-lane candidate list and resolved best ---------------------------------
 struct Slots {
     float tl[NSLOT];
     int inst[NSLOT];
     int leaf[NSLOT];
 };
 
-// ---- traversal ---------------------------------------------------------------------
 struct Counters { unsigned nodes, leaves, insts, f64, overflow; };
 
 struct Best64 {
@@ -138,44 +148,235 @@ __device__ __forceinline__ void consider64(const SceneView& sv, int inst, int le
 
 // Brute force over every triangle of the env in FP64: the path of last resort
 // when a traversal stack would overflow (a pathological TLAS/BLAS depth).
-__device__ __noinline__ void brute64(const SceneView& sv, int env, const Ray64& r64, double tmax,
-                                     Best64& best) {
+__device__ __noinline__ void brute64(SceneView sv, int env, Ray64 r64, double tmax, Best64* best) {
+    Best64 b = *best;
     for (int inst = __ldg(sv.env_off + env); inst < __ldg(sv.env_off + env + 1); ++inst) {
         const AssetInfo& as = sv.assets[__ldg(sv.inst_asset + inst)];
-        for (int l = 0; l < as.n_leaves; ++l) consider64(sv, inst, as.leaf_base + l, r64, tmax, best);
+        for (int l = 0; l < as.n_leaves; ++l) consider64(sv, inst, as.leaf_base + l, r64, tmax, b);
     }
+    *best = b;
 }
 
-template <bool EXACT, bool COUNT>
-__device__ __forceinline__ void traverse(const SceneView& sv, int env, f3 o, f3 d, float tmax,
-                                         const Ray64& r64, Slots& sl, bool& overflow,
-                                         bool& stack_overflow, Best64& best, Counters& cnt) {
+// ---- per-ray traversal state (shared by the per-lane and the packet drivers) -----
+// Hot state (used at every node) lives in registers; cold state (the object-
+// space ray for triangle tests, the candidate list and the FP64-resolved
+// best) lives in a per-lane column of shared memory so the node loop stays
+// within 64 registers without spills.
+enum ColdField {
+    C_OX, C_OY, C_OZ, C_DX, C_DY, C_DZ, C_Q,
+    C_OOX, C_OOY, C_OOZ, C_ODX, C_ODY, C_ODZ, C_DELTA, C_DLEN,
+    C_SR0, C_SR_END = C_SR0 + 9,
+    C_TL0, C_INST0 = C_TL0 + NSLOT, C_LEAF0 = C_INST0 + NSLOT,
+    C_FACE = C_LEAF0 + NSLOT, C_BINST, C_BLEAF, N_COLD
+};
+
+struct Cold {
+    float* p;     // &s_cold[0][lane of block]
+    double* bt;   // &s_best_t[lane of block]
+    __device__ __forceinline__ float& f(int k) const { return p[k * CAST_THREADS]; }
+    __device__ __forceinline__ int& i(int k) const { return *reinterpret_cast<int*>(&p[k * CAST_THREADS]); }
+
+    __device__ __forceinline__ Best64 best() const {
+        Best64 b;
+        b.t = *bt;
+        b.face = i(C_FACE);
+        b.inst = i(C_BINST);
+        b.leaf = i(C_BLEAF);
+        return b;
+    }
+    __device__ __forceinline__ void set_best(const Best64& b) const {
+        *bt = b.t;
+        i(C_FACE) = b.face;
+        i(C_BINST) = b.inst;
+        i(C_BLEAF) = b.leaf;
+    }
+};
+
+struct RayState {
+    float tmax;
+    float U;          // upper bound on the winning t (certain FP32 hits, FP64 hits)
+    SlabRay sr;       // box-test state of the current level
+    int cur_inst;     // -1 at the TLAS level
+    Cold c;           // env-level ray o, d, q; object-space ray; candidates; best
+
+    __device__ __forceinline__ f3 o() const { return mk(c.f(C_OX), c.f(C_OY), c.f(C_OZ)); }
+    __device__ __forceinline__ f3 d() const { return mk(c.f(C_DX), c.f(C_DY), c.f(C_DZ)); }
+
+    __device__ __forceinline__ void init(f3 o, f3 d, float tmax_, Cold cold) {
+        c = cold;
+        tmax = tmax_;
+        U = tmax_;
+        // |o|_1 + tmax |d|_1: scale of the FP32 ray's position error
+        const float q = fabsf(o.x) + fabsf(o.y) + fabsf(o.z) + tmax * (fabsf(d.x) + fabsf(d.y) + fabsf(d.z));
+        c.f(C_OX) = o.x; c.f(C_OY) = o.y; c.f(C_OZ) = o.z;
+        c.f(C_DX) = d.x; c.f(C_DY) = d.y; c.f(C_DZ) = d.z;
+        c.f(C_Q) = q;
+        // env level: the origin is an exact input, the direction carries rounding
+        sr = make_slab(o, d, K_ERR * q);
+        cur_inst = -1;
+#pragma unroll
+        for (int k = 0; k < NSLOT; ++k) { c.f(C_TL0 + k) = inf_f(); c.i(C_INST0 + k) = -1; c.i(C_LEAF0 + k) = -1; }
+        Best64 b;
+        b.t = 0.0;
+        b.face = -1;
+        b.inst = -1;
+        b.leaf = -1;
+        c.set_best(b);
+    }
+
+    __device__ __forceinline__ void exit_instance() {
+        sr = make_slab(o(), d(), K_ERR * c.f(C_Q));
+        cur_inst = -1;
+    }
+
+    // TLAS leaf: move the ray into instance `inst`'s object space; returns the
+    // BLAS root node.
+    __device__ __forceinline__ int enter_instance(const SceneView& sv, int inst) {
+        const float4* rp = sv.irec + 4 * inst;
+        float4 r0 = __ldg(rp), r1 = __ldg(rp + 1), r2 = __ldg(rp + 2), r3 = __ldg(rp + 3);
+        const f3 o = this->o(), d = this->d();
+        const float q = c.f(C_Q);
+        f3 oo = mk(fmaf(r0.x, o.x, fmaf(r0.y, o.y, fmaf(r0.z, o.z, r0.w))),
+                   fmaf(r1.x, o.x, fmaf(r1.y, o.y, fmaf(r1.z, o.z, r1.w))),
+                   fmaf(r2.x, o.x, fmaf(r2.y, o.y, fmaf(r2.z, o.z, r2.w))));
+        f3 od = mk(fmaf(r0.x, d.x, fmaf(r0.y, d.y, r0.z * d.z)),
+                   fmaf(r1.x, d.x, fmaf(r1.y, d.y, r1.z * d.z)),
+                   fmaf(r2.x, d.x, fmaf(r2.y, d.y, r2.z * d.z)));
+        // object-space position error bound
+        float delta = K_ERR * fmaf(r3.y, q, r3.z);
+        c.f(C_OOX) = oo.x; c.f(C_OOY) = oo.y; c.f(C_OOZ) = oo.z;
+        c.f(C_ODX) = od.x; c.f(C_ODY) = od.y; c.f(C_ODZ) = od.z;
+        c.f(C_DELTA) = delta;
+        const float dd = dot(od, od);
+        c.f(C_DLEN) = dd > 0.0f ? dd * rsqrtf(dd) * 1.000001f : 0.0f;
+        sr = make_slab(oo, od, delta);
+        save_slab();
+        cur_inst = inst;
+        return __float_as_int(r3.x);
+    }
+
+    // The box-test state is parked in shared memory while a triangle is
+    // tested and reloaded afterwards, so it holds no registers there.
+    __device__ __forceinline__ void save_slab() const {
+        c.f(C_SR0 + 0) = sr.idx; c.f(C_SR0 + 1) = sr.idy; c.f(C_SR0 + 2) = sr.idz;
+        c.f(C_SR0 + 3) = sr.lox; c.f(C_SR0 + 4) = sr.loy; c.f(C_SR0 + 5) = sr.loz;
+        c.f(C_SR0 + 6) = sr.hix; c.f(C_SR0 + 7) = sr.hiy; c.f(C_SR0 + 8) = sr.hiz;
+    }
+    __device__ __forceinline__ void load_slab() {
+        sr.idx = c.f(C_SR0 + 0); sr.idy = c.f(C_SR0 + 1); sr.idz = c.f(C_SR0 + 2);
+        sr.lox = c.f(C_SR0 + 3); sr.loy = c.f(C_SR0 + 4); sr.loz = c.f(C_SR0 + 5);
+        sr.hix = c.f(C_SR0 + 6); sr.hiy = c.f(C_SR0 + 7); sr.hiz = c.f(C_SR0 + 8);
+    }
+
+    __device__ __forceinline__ void node_test(const float4& n0, const float4& n1, const float4& n2,
+                                              bool& h0, bool& h1, float& t0, float& t1) const {
+        h0 = slab(sr, n0.x, n0.y, n0.z, n0.w, n1.x, n1.y, U, t0);
+        h1 = slab(sr, n1.z, n1.w, n2.x, n2.y, n2.z, n2.w, U, t1);
+    }
+
+    // Resolve leaf `leaf` of the current instance in FP64 now (exact mode,
+    // full candidate list); `res` is the out-of-line FP64 tester.
+    template <class RES>
+    __device__ __forceinline__ void resolve64(int leaf, const RES& res) {
+        Best64 b = c.best();
+        res(cur_inst, leaf, b);
+        c.set_best(b);
+        if (b.face >= 0) U = fminf(U, __double2float_ru(b.t));
+    }
+
+    // FP32 filter test of BLAS leaf `leaf`: reject what FP32
+    // proves a miss, tighten U with what it proves a hit, keep the rest as
+    // candidates for FP64 arbitration.  A full list resolves in FP64 inline.
+    template <bool COUNT, class RES>
+    __device__ __forceinline__ void leaf_filter(const SceneView& sv, int leaf, const RES& res,
+                                                Counters& cnt) {
+        const float4* tp = sv.tris + 3 * leaf;
+        float4 a = __ldg(tp), b = __ldg(tp + 1), cc = __ldg(tp + 2);
+        const f3 oo = mk(c.f(C_OOX), c.f(C_OOY), c.f(C_OOZ));
+        const f3 od = mk(c.f(C_ODX), c.f(C_ODY), c.f(C_ODZ));
+        const float delta = c.f(C_DELTA);
+        f3 v0 = mk(a.x, a.y, a.z), e1 = mk(b.x, b.y, b.z), e2 = mk(cc.x, cc.y, cc.z);
+        f3 p = cross(od, e2);
+        float det = dot(e1, p);
+        f3 s = sub(oo, v0);
+        bool keep, certain = false;
+        float tl = 0.0f, th = 0.0f;
+        if (det != 0.0f) {
+            float inv = rcp_approx(det);
+            f3 qv = cross(s, e1);
+            float u = dot(s, p) * inv;
+            float v = dot(od, qv) * inv;
+            float t = dot(e2, qv) * inv;
+            float g = delta * b.w * fabsf(inv);          // t error bound
+            float beta = g * c.f(C_DLEN) * a.w;          // barycentric band
+            float terr = fmaf(fabsf(t), T_REL, g);
+            tl = t - terr;
+            th = t + terr;
+            bool out = u < -beta || v < -beta || u + v > 1.0f + beta || th < 0.0f || tl > U;
+            keep = !out;
+            if (!(tl == tl)) tl = 0.0f;  // NaN (denormal det): keep conservatively
+            certain = keep && u > beta && v > beta && u + v < 1.0f - beta && tl > 0.0f && th <= tmax;
+        } else {
+            // parallel in FP32: keep only if the origin is within delta of the plane
+            f3 nn = cross(e1, e2);
+            keep = fabsf(dot(s, nn)) <= delta * b.w;
+        }
+        if (keep) {
+            if (certain && th < U) U = th;
+            int slot = -1;
+#pragma unroll
+            for (int k = NSLOT - 1; k >= 0; --k)  // lowest free slot: empty or pruned by U
+                if (!(c.f(C_TL0 + k) <= U)) slot = k;
+            if (slot >= 0) {
+                c.f(C_TL0 + slot) = tl;
+                c.i(C_INST0 + slot) = cur_inst;
+                c.i(C_LEAF0 + slot) = leaf;
+            } else {
+                if (COUNT) cnt.overflow++;
+                if (COUNT) cnt.f64++;
+                resolve64(leaf, res);
+            }
+        }
+    }
+
+    // FP64 arbitration of the surviving candidates (slot loop, warp-uniform).
+    template <bool COUNT, class RES>
+    __device__ __forceinline__ Best64 arbitrate(const RES& res, Counters& cnt) {
+        Best64 b = c.best();
+#pragma unroll
+        for (int k = 0; k < NSLOT; ++k) {
+            if (c.f(C_TL0 + k) <= U) {
+                if (COUNT) cnt.f64++;
+                res(c.i(C_INST0 + k), c.i(C_LEAF0 + k), b);
+            }
+        }
+        return b;
+    }
+};
+
+// ---- per-lane traversal (explicit rays; exact-mode fallback) -------------------
+// Ordered stackful traversal of the two-level BVH, one independent ray per
+// lane (Aila & Laine style, stack in local memory).
+template <bool EXACT, bool COUNT, class RES>
+__device__ __forceinline__ void traverse_lane(const SceneView& sv, int env, RayState& rs,
+                                              const RES& res, bool& sovf, Counters& cnt) {
     int stack[STACK_SIZE];
     int sp = 0;
-    // env-level error bound: direction rounding (origin exact) -- DESIGN.md §5.2
-    const float q = fabsf(o.x) + fabsf(o.y) + fabsf(o.z) + tmax * (fabsf(d.x) + fabsf(d.y) + fabsf(d.z));
-    const SlabRay env_slab = make_slab(o, d, K_ERR * q);
-    SlabRay sr = env_slab;
-    // object-space ray of the current instance
-    f3 oo = o, od = d;
-    float delta = 0.0f, dlen = 0.0f;
-    int cur_inst = -1;
-    float U = tmax;
     int node = __ldg(sv.tlas_root + env);
     for (;;) {
         if (node >= 0) {
             if (COUNT) cnt.nodes++;
             const float4* np = sv.nodes + 4 * node;
             float4 n0 = __ldg(np), n1 = __ldg(np + 1), n2 = __ldg(np + 2), n3 = __ldg(np + 3);
+            bool h0, h1;
             float t0, t1;
-            bool h0 = slab(sr, n0.x, n0.y, n0.z, n0.w, n1.x, n1.y, U, t0);
-            bool h1 = slab(sr, n1.z, n1.w, n2.x, n2.y, n2.z, n2.w, U, t1);
+            rs.node_test(n0, n1, n2, h0, h1, t0, t1);
             int c0 = __float_as_int(n3.x), c1 = __float_as_int(n3.y);
             if (h0 && h1) {
                 int far_c = t0 <= t1 ? c1 : c0;
                 node = t0 <= t1 ? c0 : c1;
                 if (sp < STACK_SIZE) stack[sp++] = far_c;
-                else stack_overflow = true;
+                else sovf = true;
             } else if (h0) {
                 node = c0;
             } else if (h1) {
@@ -187,94 +388,106 @@ __device__ __forceinline__ void traverse(const SceneView& sv, int env, f3 o, f3 
             continue;
         }
         if (node == SENTINEL) {  // leave the instance: back to the env-level ray
-            sr = env_slab;
-            cur_inst = -1;
+            rs.exit_instance();
             if (sp == 0) break;
             node = stack[--sp];
             continue;
         }
         const int leaf = ~node;
-        if (cur_inst < 0) {
-            // TLAS leaf: enter instance `leaf`, move the ray to object space
+        if (rs.cur_inst < 0) {
             if (COUNT) cnt.insts++;
-            const float4* rp = sv.irec + 4 * leaf;
-            float4 r0 = __ldg(rp), r1 = __ldg(rp + 1), r2 = __ldg(rp + 2), r3 = __ldg(rp + 3);
-            oo = mk(fmaf(r0.x, o.x, fmaf(r0.y, o.y, fmaf(r0.z, o.z, r0.w))),
-                    fmaf(r1.x, o.x, fmaf(r1.y, o.y, fmaf(r1.z, o.z, r1.w))),
-                    fmaf(r2.x, o.x, fmaf(r2.y, o.y, fmaf(r2.z, o.z, r2.w))));
-            od = mk(fmaf(r0.x, d.x, fmaf(r0.y, d.y, r0.z * d.z)),
-                    fmaf(r1.x, d.x, fmaf(r1.y, d.y, r1.z * d.z)),
-                    fmaf(r2.x, d.x, fmaf(r2.y, d.y, r2.z * d.z)));
-            delta = K_ERR * fmaf(r3.y, q, r3.z);
-            dlen = sqrtf(dot(od, od));
-            sr = make_slab(oo, od, delta);
-            cur_inst = leaf;
             if (sp < STACK_SIZE) stack[sp++] = SENTINEL;
-            else { stack_overflow = true; break; }
-            node = __float_as_int(r3.x);
+            else { sovf = true; break; }
+            node = rs.enter_instance(sv, leaf);
             continue;
         }
-        // BLAS leaf: triangle record `leaf` of instance cur_inst
         if (COUNT) cnt.leaves++;
         if (EXACT) {
             if (COUNT) cnt.f64++;
-            consider64(sv, cur_inst, leaf, r64, (double)tmax, best);
-            if (best.face >= 0) U = fminf(tmax, __double2float_ru(best.t));
+            rs.resolve64(leaf, res);
         } else {
-            const float4* tp = sv.tris + 3 * leaf;
-            float4 a = __ldg(tp), b = __ldg(tp + 1), c = __ldg(tp + 2);
-            f3 v0 = mk(a.x, a.y, a.z), e1 = mk(b.x, b.y, b.z), e2 = mk(c.x, c.y, c.z);
-            f3 p = cross(od, e2);
-            float det = dot(e1, p);
-            f3 s = sub(oo, v0);
-            bool keep = false, certain = false;
-            float tl = 0.0f, th = 0.0f;
-            if (det != 0.0f) {
-                float inv = __frcp_rn(det);
-                f3 qv = cross(s, e1);
-                float u = dot(s, p) * inv;
-                float v = dot(od, qv) * inv;
-                float t = dot(e2, qv) * inv;
-                float g = delta * b.w * fabsf(inv);           // t error bound
-                float beta = g * dlen * a.w;                     // barycentric band
-                float terr = fmaf(fabsf(t), T_REL, g);
-                tl = t - terr;
-                th = t + terr;
-                bool out = u < -beta || v < -beta || u + v > 1.0f + beta || th < 0.0f || tl > U;
-                keep = !out;
-                if (!(tl == tl)) tl = 0.0f;  // NaN (denormal det): keep conservatively
-                certain = keep && u > beta && v > beta && u + v < 1.0f - beta && tl > 0.0f && th <= tmax;
-            } else {
-                // ray parallel in FP32: keep only if the origin is within delta of the plane
-                f3 nn = cross(e1, e2);
-                float h = fabsf(dot(s, nn));
-                keep = h <= delta * b.w;
-                tl = 0.0f;
-            }
-            if (keep) {
-                if (certain && th < U) U = th;
-                bool placed = false;
-#pragma unroll
-                for (int k = 0; k < NSLOT; ++k) {
-                    // a slot is free if empty (+inf) or pruned by the current U
-                    if (!placed && !(sl.tl[k] <= U)) {
-                        sl.tl[k] = tl;
-                        sl.inst[k] = cur_inst;
-                        sl.leaf[k] = leaf;
-                        placed = true;
-                    }
-                }
-                if (!placed) overflow = true;
-            }
+            rs.leaf_filter<COUNT>(sv, leaf, res, cnt);
         }
+        rs.load_slab();
         if (sp == 0) break;
         node = stack[--sp];
     }
-    if (!EXACT) {
-        // slots pruned after insertion are dead; mark them empty
-#pragma unroll
-        for (int k = 0; k < NSLOT; ++k)
-            if (!(sl.tl[k] <= U)) sl.tl[k] = inf_f();
+}
+
+// ---- packet traversal (pinhole / beams tiles) ------------------------------------
+// The 32 rays of an 8x4 tile traverse together: the warp visits a node if any
+// lane's ray hits it (ballot), descends first into the child most lanes reach
+// first, and keeps ONE stack per warp in shared memory.  Control flow is
+// warp-uniform (no divergence in the traversal loop); every node / triangle
+// fetch is a broadcast load.  Each lane still does its own exact-filter box
+// and triangle tests, so results equal the per-lane traversal.
+constexpr int PSTACK = 96;
+
+template <bool COUNT, class RES>
+__device__ __forceinline__ void traverse_packet(const SceneView& sv, int env, RayState& rs,
+                                                const RES& res, bool& sovf, int* wstack,
+                                                Counters& cnt) {
+    const unsigned FULL = 0xFFFFFFFFu;
+    const bool leader = (threadIdx.x & 31) == 0;
+    int sp = 0;
+    int node = __ldg(sv.tlas_root + env);
+    for (;;) {
+        if (node >= 0) {
+            if (COUNT) cnt.nodes++;
+            const float4* np = sv.nodes + 4 * node;
+            float4 n0 = __ldg(np), n1 = __ldg(np + 1), n2 = __ldg(np + 2), n3 = __ldg(np + 3);
+            bool h0, h1;
+            float t0, t1;
+            rs.node_test(n0, n1, n2, h0, h1, t0, t1);
+            const int c0 = __float_as_int(n3.x), c1 = __float_as_int(n3.y);
+            const unsigned m0 = __ballot_sync(FULL, h0), m1 = __ballot_sync(FULL, h1);
+            if (m0 && m1) {
+                const unsigned pref0 = __ballot_sync(FULL, h0 && (!h1 || t0 <= t1));
+                const bool first0 = 2 * __popc(pref0) >= __popc(m0 | m1);
+                if (sp < PSTACK) {
+                    if (leader) wstack[sp] = first0 ? c1 : c0;
+                    ++sp;
+                } else {
+                    sovf = true;
+                }
+                node = first0 ? c0 : c1;
+            } else if (m0) {
+                node = c0;
+            } else if (m1) {
+                node = c1;
+            } else {
+                if (sp == 0) break;
+                __syncwarp();
+                node = wstack[--sp];
+            }
+            continue;
+        }
+        if (node == SENTINEL) {
+            rs.exit_instance();
+            if (sp == 0) break;
+            __syncwarp();
+            node = wstack[--sp];
+            continue;
+        }
+        const int leaf = ~node;
+        if (rs.cur_inst < 0) {
+            if (COUNT) cnt.insts++;
+            if (sp < PSTACK) {
+                if (leader) wstack[sp] = SENTINEL;
+                ++sp;
+            } else {
+                sovf = true;
+                break;
+            }
+            node = rs.enter_instance(sv, leaf);
+            continue;
+        }
+        if (COUNT) cnt.leaves++;
+        rs.leaf_filter<COUNT>(sv, leaf, res, cnt);
+        rs.load_slab();
+        if (sp == 0) break;
+        __syncwarp();
+        node = wstack[--sp];
     }
 }
 
@@ -303,44 +516,82 @@ __device__ __forceinline__ void pose_ray64(const float* P, d3 ds, Ray64& r) {
               p[8] * ds.x + p[9] * ds.y + p[10] * ds.z);
 }
 
+// FP32 ray for traversal (a4: raygen fused into the cast; registers only).
 template <int MODEL>
-__device__ __forceinline__ void gen_ray(const CastArgs& a, const RayId& id, f3& o, f3& d, Ray64& r64) {
+__device__ __forceinline__ void gen_ray(const CastArgs& a, const RayId& id, f3& o, f3& d) {
     if (MODEL == 0) {
         const float* po = a.orig + 3 * id.out;
         const float* pd = a.dir + 3 * id.out;
         o = mk(__ldg(po), __ldg(po + 1), __ldg(po + 2));
         d = mk(__ldg(pd), __ldg(pd + 1), __ldg(pd + 2));
-        r64.o = mkd(o.x, o.y, o.z);
-        r64.d = mkd(d.x, d.y, d.z);
         return;
     }
     const float* P = a.poses + 12 * ((int64_t)id.env * a.S + id.sensor);
     f3 ds;
+    if (MODEL == 1) {
+        float xs = __fdividef((float)id.col + 0.5f - a.cx, a.fx);
+        float ys = __fdividef((float)id.row + 0.5f - a.cy, a.fy);
+        ds = mk(1.0f, -xs, -ys);
+        if (a.kind == 1) {
+            float rn = rsqrtf(dot(ds, ds));
+            ds = mk(ds.x * rn, ds.y * rn, ds.z * rn);
+        }
+    } else {
+        const float* b = a.beams + 3 * ((int64_t)id.row * a.W + id.col);
+        ds = mk(__ldg(b), __ldg(b + 1), __ldg(b + 2));
+        float rn = rsqrtf(dot(ds, ds));
+        ds = mk(ds.x * rn, ds.y * rn, ds.z * rn);
+    }
+    pose_ray(P, ds, o, d);
+}
+
+// FP64 ray of the same pixel / beam from the same FP32 inputs (DESIGN.md §3:
+// the plain definition promotes the inputs to FP64); built lazily, only when
+// a candidate is arbitrated, so it holds no registers during traversal.
+template <int MODEL>
+__device__ __forceinline__ Ray64 gen_ray64(const CastArgs& a, const RayId& id) {
+    Ray64 r64;
+    if (MODEL == 0) {
+        const float* po = a.orig + 3 * id.out;
+        const float* pd = a.dir + 3 * id.out;
+        r64.o = mkd(__ldg(po), __ldg(po + 1), __ldg(po + 2));
+        r64.d = mkd(__ldg(pd), __ldg(pd + 1), __ldg(pd + 2));
+        return r64;
+    }
+    const float* P = a.poses + 12 * ((int64_t)id.env * a.S + id.sensor);
     d3 ds64;
     if (MODEL == 1) {
-        float xs = ((float)id.col + 0.5f - a.cx) / a.fx;
-        float ys = ((float)id.row + 0.5f - a.cy) / a.fy;
-        ds = mk(1.0f, -xs, -ys);
         double xs64 = ((double)id.col + 0.5 - (double)a.cx) / (double)a.fx;
         double ys64 = ((double)id.row + 0.5 - (double)a.cy) / (double)a.fy;
         ds64 = mkd(1.0, -xs64, -ys64);
         if (a.kind == 1) {
-            float rn = rsqrtf(dot(ds, ds));
-            ds = mk(ds.x * rn, ds.y * rn, ds.z * rn);
             double n = sqrt(dotd(ds64, ds64));
             ds64 = mkd(ds64.x / n, ds64.y / n, ds64.z / n);
         }
     } else {
         const float* b = a.beams + 3 * ((int64_t)id.row * a.W + id.col);
-        ds = mk(__ldg(b), __ldg(b + 1), __ldg(b + 2));
-        ds64 = mkd(ds.x, ds.y, ds.z);
-        float rn = rsqrtf(dot(ds, ds));
-        ds = mk(ds.x * rn, ds.y * rn, ds.z * rn);
+        ds64 = mkd(__ldg(b), __ldg(b + 1), __ldg(b + 2));
         double n = sqrt(dotd(ds64, ds64));
         ds64 = mkd(ds64.x / n, ds64.y / n, ds64.z / n);
     }
-    pose_ray(P, ds, o, d);
     pose_ray64(P, ds64, r64);
+    return r64;
+}
+
+// Out-of-line FP64 test of (inst, leaf) for the ray `id`: keeps the FP64
+// registers out of the traversal loop's allocation.
+template <int MODEL>
+__device__ __forceinline__ RayId ray_id(const CastArgs& a);
+
+template <int MODEL>
+__device__ __noinline__ void resolve_leaf64(const CastArgs* a, int inst, int leaf, Best64* best) {
+    RayId id = ray_id<MODEL>(*a);
+    id.col = min(id.col, a->W - 1);
+    id.row = min(id.row, a->H - 1);
+    const Ray64 r = gen_ray64<MODEL>(*a, id);
+    Best64 b = *best;
+    consider64(a->sv, inst, leaf, r, (double)a->max_range, b);
+    *best = b;
 }
 
 template <int MODEL>
@@ -373,8 +624,12 @@ __device__ __forceinline__ RayId ray_id(const CastArgs& a) {
     return id;
 }
 
-template <int MODEL, bool COUNT>
-__global__ void __launch_bounds__(CAST_THREADS) k_cast(CastArgs a) {
+// TRAV: 0 per-lane FP32 filter, 1 warp packet (pinhole / beams), 2 exact (FP64 leaves)
+template <int MODEL, int TRAV, bool COUNT>
+__global__ void __launch_bounds__(CAST_THREADS, CAST_MIN_BLOCKS) k_cast(const __grid_constant__ CastArgs a) {
+    __shared__ int s_stack[TRAV == 1 ? CAST_THREADS / 32 : 1][TRAV == 1 ? PSTACK : 1];
+    __shared__ float s_cold[N_COLD][CAST_THREADS];
+    __shared__ double s_best_t[CAST_THREADS];
     RayId id = ray_id<MODEL>(a);
     // ragged tile lanes keep the warp whole for the traversal: they trace a
     // copy of a valid pixel and store nothing
@@ -382,43 +637,37 @@ __global__ void __launch_bounds__(CAST_THREADS) k_cast(CastArgs a) {
     id.col = min(id.col, a.W - 1);
     id.row = min(id.row, a.H - 1);
     Counters cnt = {0, 0, 0, 0, 0};
+    RayState rs;
     Best64 best;
-    best.t = 0.0;
     best.face = -1;
     best.inst = -1;
-    best.leaf = -1;
+    best.t = 0.0;
     if (trace) {
         f3 o, d;
-        Ray64 r64;
-        gen_ray<MODEL>(a, id, o, d, r64);
-        const float tmax = a.max_range;
-        bool overflow = false, sovf = false;
-        Slots sl;
-        if (a.exact) {
-            traverse<true, COUNT>(a.sv, id.env, o, d, tmax, r64, sl, overflow, sovf, best, cnt);
+        gen_ray<MODEL>(a, id, o, d);
+        Cold cold;
+        cold.p = &s_cold[0][threadIdx.x];
+        cold.bt = &s_best_t[threadIdx.x];
+        rs.init(o, d, a.max_range, cold);
+        const CastArgs* ap = &a;
+        auto res = [ap](int inst, int leaf, Best64& b) { resolve_leaf64<MODEL>(ap, inst, leaf, &b); };
+        bool sovf = false;
+        if (TRAV == 2) {
+            traverse_lane<true, COUNT>(a.sv, id.env, rs, res, sovf, cnt);
+            best = cold.best();
         } else {
-#pragma unroll
-            for (int k = 0; k < NSLOT; ++k) { sl.tl[k] = inf_f(); sl.inst[k] = -1; sl.leaf[k] = -1; }
-            traverse<false, COUNT>(a.sv, id.env, o, d, tmax, r64, sl, overflow, sovf, best, cnt);
-            // FP64 arbitration of the surviving candidates (warp-uniform slot loop)
-#pragma unroll
-            for (int k = 0; k < NSLOT; ++k) {
-                if (sl.tl[k] <= tmax) {
-                    if (COUNT) cnt.f64++;
-                    consider64(a.sv, sl.inst[k], sl.leaf[k], r64, (double)tmax, best);
-                }
+            if (TRAV == 1) {
+                // whole warps share (env, sensor): pinhole / beams tiles
+                traverse_packet<COUNT>(a.sv, id.env, rs, res, sovf, s_stack[threadIdx.x >> 5], cnt);
+            } else {
+                traverse_lane<false, COUNT>(a.sv, id.env, rs, res, sovf, cnt);
             }
-            if (overflow && !sovf) {
-                // candidate list overflow: re-traverse with every leaf tested in FP64
-                if (COUNT) cnt.overflow++;
-                best.face = -1;
-                traverse<true, COUNT>(a.sv, id.env, o, d, tmax, r64, sl, overflow, sovf, best, cnt);
-            }
+            best = rs.arbitrate<COUNT>(res, cnt);
         }
         if (sovf) {
             if (COUNT) cnt.overflow++;
             best.face = -1;
-            brute64(a.sv, id.env, r64, (double)tmax, best);
+            brute64(a.sv, id.env, gen_ray64<MODEL>(a, id), (double)a.max_range, &best);
         }
     }
     if (COUNT) {
@@ -453,8 +702,17 @@ cudaError_t launch_model(const CastArgs& a, cudaStream_t stream) {
     }
     if (blocks <= 0) return cudaSuccess;
     if (blocks > 0x7FFFFFFF) return cudaErrorInvalidValue;
-    if (a.counters) k_cast<MODEL, true><<<(unsigned)blocks, CAST_THREADS, 0, stream>>>(a);
-    else k_cast<MODEL, false><<<(unsigned)blocks, CAST_THREADS, 0, stream>>>(a);
+    const int trav = a.exact ? 2 : (MODEL != 0 && a.packet ? 1 : 0);
+    const unsigned g = (unsigned)blocks;
+    if (a.counters) {
+        if (trav == 2) k_cast<MODEL, 2, true><<<g, CAST_THREADS, 0, stream>>>(a);
+        else if (trav == 1) k_cast<MODEL, 1, true><<<g, CAST_THREADS, 0, stream>>>(a);
+        else k_cast<MODEL, 0, true><<<g, CAST_THREADS, 0, stream>>>(a);
+    } else {
+        if (trav == 2) k_cast<MODEL, 2, false><<<g, CAST_THREADS, 0, stream>>>(a);
+        else if (trav == 1) k_cast<MODEL, 1, false><<<g, CAST_THREADS, 0, stream>>>(a);
+        else k_cast<MODEL, 0, false><<<g, CAST_THREADS, 0, stream>>>(a);
+    }
     return cudaGetLastError();
 }
 
