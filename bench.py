@@ -87,6 +87,19 @@ def make_workload(cfg, n_envs, env_base):
     return sg.config5(n_envs=n_envs, env_base=env_base, ring=8)
 
 
+def env_base(rank, envs_per_rank):
+    """Weak scaling: rank r owns global envs [r E, (r+1) E)."""
+    return rank * envs_per_rank
+
+
+def reduce_max(t, world):
+    """Max over ranks (step times are max-over-ranks, never wall clock)."""
+    if world > 1:
+        import torch.distributed as dist
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return t
+
+
 def rays_per_env(sensor):
     if sensor["kind"] == "pinhole":
         return sensor["cam"]["W"] * sensor["cam"]["H"] * sensor["poses"].shape[1]
@@ -226,7 +239,7 @@ def main():
 
     cfg = args.config
     E = envs_per_gpu(args)
-    sc, sensor = make_workload(cfg, E, rank * E)  # this rank's block of global envs
+    sc, sensor = make_workload(cfg, E, env_base(rank, E))  # this rank's block of global envs
     kind = agr.AGR_RANGE if cfg == 4 else agr.AGR_DEPTH
     chans = channels_for(cfg)
     scene = agr.Scene.from_scenegen(sc, device=local)
@@ -293,9 +306,8 @@ def main():
     cast_ms = [b.elapsed_time(c) for a, b, c in ev]
     total_ms = sum(step_ms)
     cast_total = sum(cast_ms)
-    t = torch.tensor([total_ms, cast_total], dtype=torch.float64, device=dev)
+    t = reduce_max(torch.tensor([total_ms, cast_total], dtype=torch.float64, device=dev), world)
     if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dist.barrier()
     total_ms, cast_total = float(t[0]), float(t[1])
     ms_per_step = total_ms / args.steps
@@ -336,9 +348,7 @@ def main():
         for k in range(n_e2e):
             e2e_step(k)
         dt = time.perf_counter() - t0
-        tt = torch.tensor([dt], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        tt = reduce_max(torch.tensor([dt], dtype=torch.float64, device=dev), world)
         dt = float(tt[0])
         h2d = poses_h.numel() * 4 + (beams_h.numel() * 4 if beams_h is not None else 0)
         d2h = sum(v.numel() * 4 for v in out_h.values())

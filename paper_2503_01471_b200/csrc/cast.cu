@@ -28,9 +28,13 @@
 namespace agr {
 namespace {
 
-constexpr int CAST_THREADS = 128;
+#ifndef CAST_BLOCK
+#define CAST_BLOCK 64
+#endif
+constexpr int CAST_THREADS = CAST_BLOCK;
+// 32 resident warps per SM: 64 registers per thread
 #ifndef CAST_MIN_BLOCKS
-#define CAST_MIN_BLOCKS 8
+#define CAST_MIN_BLOCKS (1024 / CAST_BLOCK)
 #endif
 constexpr int NSLOT = 4;
 constexpr int SENTINEL = REF_EMPTY;  // "return to the TLAS" marker on the stack

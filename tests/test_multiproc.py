@@ -1,0 +1,79 @@
+"""World-size-2 `gloo` tests (CPU) of the multi-GPU host logic used by
+bench.py: env sharding (weak scaling, contiguous global env
+blocks per rank), per-env input independence from the sharding, and the
+max-over-ranks step-time reduction."""
+from __future__ import annotations
+
+import hashlib
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import bench
+import scenegen as sg
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _env_digest(sc, e):
+    i0, i1 = int(sc.env_off[e]), int(sc.env_off[e + 1])
+    h = hashlib.sha256()
+    h.update(sc.inst_asset[i0:i1].tobytes())
+    h.update(sc.inst_label[i0:i1].tobytes())
+    h.update(sc.inst_T[i0:i1].tobytes())
+    return np.frombuffer(h.digest()[:8], np.int64)[0]
+
+
+def _worker(rank, world, port, cfg, E, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    sc, sensor = bench.make_workload(cfg, E, bench.env_base(rank, E))
+    dig = torch.tensor([_env_digest(sc, e) for e in range(E)], dtype=torch.int64)
+    poses = torch.from_numpy(sensor["poses"].reshape(E, -1).copy())
+    gathered = [torch.zeros_like(dig) for _ in range(world)]
+    dist.all_gather(gathered, dig)
+    pg = [torch.zeros_like(poses) for _ in range(world)]
+    dist.all_gather(pg, poses)
+    t = torch.tensor([10.0 * (rank + 1), 1.0 + rank], dtype=torch.float64)
+    tmax = bench.reduce_max(t, world)
+    if rank == 0:
+        q.put((torch.cat(gathered).numpy(), torch.cat(pg).numpy(), tmax.numpy()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("cfg", [3, 5])
+def test_two_rank_sharding_matches_single_process(cfg):
+    E = 6
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, cfg, E, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    dig, poses, tmax = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    # the 2-rank job covers global envs [0, 2E) exactly once, with the same
+    # per-env content as a single process generating all 2E envs
+    sc, sensor = bench.make_workload(cfg, 2 * E, 0)
+    ref = np.asarray([_env_digest(sc, e) for e in range(2 * E)])
+    assert np.array_equal(dig, ref)
+    assert np.array_equal(poses, sensor["poses"].reshape(2 * E, -1))
+    assert list(tmax) == [20.0, 2.0]  # max over ranks
+
+
+def test_env_base_is_weak_scaling():
+    assert [bench.env_base(r, 1024) for r in range(4)] == [0, 1024, 2048, 3072]
