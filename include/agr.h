@@ -252,6 +252,17 @@ agr_status agr_debug_export_blas(agr_scene scene, int32_t asset, float* nodes,
                                  int32_t* leaf_face, uint32_t* morton,
                                  int64_t* n_nodes, int64_t* n_leaves);
 
+/*
+ * Debug export of the traversal BVH4 (synchronous).  which >= 0: the BLAS of
+ * asset `which`; which < 0: the TLAS of env (-1 - which) (after agr_build).
+ * nodes float [n_nodes][32]: per node lo.x[4] hi.x[4] lo.y[4] hi.y[4]
+ * lo.z[4] hi.z[4] ref[4] (int bits) cnt; refs are global (>= 0 node index,
+ * < 0 ~leaf: triangle record or global instance; INT32_MIN empty).
+ * *root = global index of node 0 of the export.  NULL nodes: size query.
+ */
+agr_status agr_debug_export_bvh4(agr_scene scene, int32_t which, float* nodes, int32_t* root,
+                                 int64_t* n_nodes);
+
 #ifdef __cplusplus
 }
 #endif

@@ -90,6 +90,8 @@ _SIGS = {
     "agr_get_counters": (_I32, [_P, _P]),
     "agr_debug_export_blas": (_I32, [_P, _I32, _P, _P, _P, ctypes.POINTER(ctypes.c_int64),
                                      ctypes.POINTER(ctypes.c_int64)]),
+    "agr_debug_export_bvh4": (_I32, [_P, _I32, _P, ctypes.POINTER(ctypes.c_int32),
+                                     ctypes.POINTER(ctypes.c_int64)]),
 }
 
 _lib = None
@@ -316,6 +318,18 @@ class Scene:
         _check(lib.agr_debug_export_blas(self.handle, asset, nodes.ctypes.data, faces.ctypes.data,
                                          codes.ctypes.data, ctypes.byref(nn), ctypes.byref(nl)))
         return nodes, faces[:nl.value], codes[:nl.value]
+
+
+    def debug_export_bvh4(self, which: int):
+        """BVH4 nodes of asset `which` (>= 0) or of env (-1 - which)'s TLAS."""
+        n = ctypes.c_int64()
+        root = ctypes.c_int32()
+        lib = load()
+        _check(lib.agr_debug_export_bvh4(self.handle, which, None, ctypes.byref(root), ctypes.byref(n)))
+        nodes = np.zeros((n.value, 32), np.float32)
+        _check(lib.agr_debug_export_bvh4(self.handle, which, nodes.ctypes.data, ctypes.byref(root),
+                                         ctypes.byref(n)))
+        return nodes, root.value
 
 
 def abi_version() -> int:

@@ -66,7 +66,8 @@ struct agr_scene_s {
     std::vector<void*> allocs;
     size_t device_bytes = 0;
     // device arrays
-    float4* nodes = nullptr;
+    float4* nodes = nullptr;   // BVH4 (BLAS then TLAS), 8 float4 per node
+    float4* bnodes = nullptr;  // binary BLAS nodes, 4 float4 per node (debug export)
     float4* tris = nullptr;
     float* triv = nullptr;
     float4* irec = nullptr;
@@ -265,7 +266,8 @@ agr_status agr_scene_create(int32_t device, const agr_mesh* meshes, int32_t n_me
         if (_e != cudaSuccess) return bail(cuda_fail(_e, #call));    \
     } while (0)
 
-    CKB(s->alloc(&s->nodes, 4 * (size_t)(nb + nt)));
+    CKB(s->alloc(&s->nodes, 8 * (size_t)(nb + nt)));
+    CKB(s->alloc(&s->bnodes, 4 * (size_t)nb));
     CKB(s->alloc(&s->tris, 3 * (size_t)nl));
     CKB(s->alloc(&s->triv, 9 * (size_t)nl));
     CKB(s->alloc(&s->irec, 4 * (size_t)n_inst));
@@ -325,6 +327,7 @@ agr_status agr_scene_create(int32_t device, const agr_mesh* meshes, int32_t n_me
         ba.node_base = node_base[a];
         ba.leaf_base = leaf_base[a];
         ba.nodes = s->nodes;
+        ba.bnodes = s->bnodes;
         ba.tris = s->tris;
         ba.triv = s->triv;
         ba.info_dev = s->assets + a;
@@ -741,7 +744,7 @@ agr_status agr_debug_export_blas(agr_scene s, int32_t asset, float* nodes, int32
     CK(cudaDeviceSynchronize());
     if (nodes) {
         std::vector<float4> h(4 * nn);
-        CK(cudaMemcpy(h.data(), s->nodes + 4 * (size_t)a.node_base, sizeof(float4) * 4 * nn,
+        CK(cudaMemcpy(h.data(), s->bnodes + 4 * (size_t)a.node_base, sizeof(float4) * 4 * nn,
                       cudaMemcpyDeviceToHost));
         for (int64_t i = 0; i < nn; ++i) {
             memcpy(nodes + 16 * i, &h[4 * i], 64);
@@ -764,6 +767,33 @@ agr_status agr_debug_export_blas(agr_scene s, int32_t asset, float* nodes, int32
     }
     if (morton && a.n_leaves > 0)
         CK(cudaMemcpy(morton, s->morton + a.leaf_base, sizeof(uint32_t) * a.n_leaves, cudaMemcpyDeviceToHost));
+    return AGR_OK;
+}
+
+agr_status agr_debug_export_bvh4(agr_scene s, int32_t which, float* nodes, int32_t* root,
+                                 int64_t* n_nodes) {
+    g_err.clear();
+    if (!s || !n_nodes) return fail(AGR_EINVAL, "bad argument");
+    int64_t base, count;
+    if (which >= 0) {
+        if (which >= s->n_assets) return fail(AGR_EINVAL, "asset out of range");
+        const AssetInfo& a = s->h_assets[which];
+        base = a.node_base;
+        count = a.n_leaves > 1 ? a.n_leaves - 1 : 1;
+    } else {
+        const int e = -1 - which;
+        if (e >= s->n_envs) return fail(AGR_EINVAL, "env out of range");
+        if (!s->built) return fail(AGR_ESTATE, "TLAS not built");
+        int n = s->h_env_off[e + 1] - s->h_env_off[e];
+        base = (int64_t)s->nb_blas + s->h_tlas_off[e];
+        count = n > 1 ? n - 1 : 1;
+    }
+    *n_nodes = count;
+    if (root) *root = (int32_t)base;
+    if (!nodes) return AGR_OK;
+    DeviceGuard guard(s->device);
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(nodes, s->nodes + 8 * (size_t)base, sizeof(float4) * 8 * count, cudaMemcpyDeviceToHost));
     return AGR_OK;
 }
 

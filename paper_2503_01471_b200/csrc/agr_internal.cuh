@@ -5,16 +5,17 @@
 // path share no code).
 //
 // HBM layout:
-//   nodes   float4[4] per node, 64 B, BLAS nodes of every asset first, then
-//           every env's TLAS nodes.  A node holds the boxes of its two
-//           children and their refs:
-//             n0 = (c0.lo.x, c0.hi.x, c0.lo.y, c0.hi.y)
-//             n1 = (c0.lo.z, c0.hi.z, c1.lo.x, c1.hi.x)
-//             n2 = (c1.lo.y, c1.hi.y, c1.lo.z, c1.hi.z)
-//             n3 = (ref0, ref1, -, -) as int bits
+//   nodes   BVH4 nodes, float4[8] = 128 B, BLAS nodes of every asset first,
+//           then every env's TLAS nodes.  BVH4 node j is the greedy 4-wide
+//           collapse of binary LBVH node j (only nodes reachable from the
+//           root are visited).  Boxes of the 4 children stored per axis:
+//             f0 = lo.x[4], f1 = hi.x[4], f2 = lo.y[4], f3 = hi.y[4],
+//             f4 = lo.z[4], f5 = hi.z[4], f6 = ref[4] (int bits), f7 = (n, -)
 //           ref >= 0: global node index; ref < 0: leaf ~index (triangle
 //           record for BLAS nodes, global instance for TLAS nodes);
 //           REF_EMPTY: no child (its box is +inf everywhere, never hit).
+//   bnodes  the binary LBVH of every BLAS (64-B nodes: child boxes + refs),
+//           kept for structural checks (agr_debug_export_blas).
 //   tris    float4[3] per BLAS leaf, 48 B (FP32 filter test, object space):
 //             t0 = (v0.xyz, inv_min_alt)   inv_min_alt = 1 / min altitude
 //             t1 = (e1.xyz, two_area)      e1 = v1 - v0, two_area = |e1 x e2|
@@ -34,7 +35,7 @@
 namespace agr {
 
 constexpr int REF_EMPTY = (int)0x80000000;  // INT32_MIN
-constexpr int STACK_SIZE = 64;              // traversal stack entries per ray
+constexpr int STACK_SIZE = 96;              // traversal stack entries per ray
 constexpr int MAX_TLAS_N = 1024;            // AGR_MAX_INSTANCES_PER_ENV
 
 // Relative error budget of the FP32 object-space ray:
@@ -119,6 +120,57 @@ __device__ __forceinline__ float ordered_to_float(uint32_t u) {
     return __uint_as_float((u & 0x80000000u) ? (u & 0x7FFFFFFFu) : ~u);
 }
 
+// ---- 4-wide collapse of a binary LBVH node -----------------------------------------
+AGR_HD float half_area(const float b[6]) {
+    float dx = b[3] - b[0], dy = b[4] - b[1], dz = b[5] - b[2];
+    return dx * dy + dy * dz + dz * dx;
+}
+
+// Greedy collapse of binary node j into up to 4 children: repeatedly open the
+// internal child with the largest surface area (the SAH's choice), keeping
+// the children in left-to-right (Morton) order.  Refs are local: >= 0 binary
+// internal node, < 0 leaf.  child(r, side) and box(r, b[6]) read the binary
+// tree.  Returns the number of children; unused refs are REF_EMPTY.
+template <class CHILD, class BOX>
+__device__ __forceinline__ int collapse4(int j, const CHILD& child, const BOX& box, int refs[4]) {
+    refs[0] = child(j, 0);
+    refs[1] = child(j, 1);
+    refs[2] = refs[3] = REF_EMPTY;
+    int cnt = 2;
+    while (cnt < 4) {
+        int best = -1;
+        float best_a = -1.0f;
+        for (int k = 0; k < cnt; ++k) {
+            if (refs[k] >= 0) {
+                float b[6];
+                box(refs[k], b);
+                float a = half_area(b);
+                if (a > best_a) { best_a = a; best = k; }
+            }
+        }
+        if (best < 0) break;
+        const int r = refs[best];
+        for (int k = cnt; k > best + 1; --k) refs[k] = refs[k - 1];
+        refs[best] = child(r, 0);
+        refs[best + 1] = child(r, 1);
+        ++cnt;
+    }
+    return cnt;
+}
+
+// Writes BVH4 node g: boxes b[k][6] (lo xyz, hi xyz) and global refs.
+__device__ __forceinline__ void write_node4(float4* nodes, int g, const float b[4][6], const int ref[4], int cnt) {
+    float4* p = nodes + 8 * (size_t)g;
+    p[0] = make_float4(b[0][0], b[1][0], b[2][0], b[3][0]);
+    p[1] = make_float4(b[0][3], b[1][3], b[2][3], b[3][3]);
+    p[2] = make_float4(b[0][1], b[1][1], b[2][1], b[3][1]);
+    p[3] = make_float4(b[0][4], b[1][4], b[2][4], b[3][4]);
+    p[4] = make_float4(b[0][2], b[1][2], b[2][2], b[3][2]);
+    p[5] = make_float4(b[0][5], b[1][5], b[2][5], b[3][5]);
+    p[6] = make_float4(__int_as_float(ref[0]), __int_as_float(ref[1]), __int_as_float(ref[2]), __int_as_float(ref[3]));
+    p[7] = make_float4(__int_as_float(cnt), 0.0f, 0.0f, 0.0f);
+}
+
 }  // namespace agr
 
 // Host launch wrappers implemented in the .cu files (all async on `stream`).
@@ -129,7 +181,8 @@ struct BlasBuildArgs {
     int n_verts, n_faces;
     int node_base;         // global node index of this asset's first node
     int leaf_base;         // global leaf-record index of this asset's first leaf
-    float4* nodes;         // global node array
+    float4* nodes;         // global BVH4 node array
+    float4* bnodes;        // global binary BLAS node array (debug export)
     float4* tris;          // global tri record array
     float* triv;           // global exact-vertex array
     AssetInfo* info_dev;   // this asset's AssetInfo (device)

@@ -368,6 +368,35 @@ __global__ void k_pack_nodes(int n, const uint32_t* __restrict__ sorted_prim,
                global_ref(rb, node_base, leaf_base));
 }
 
+// K5b: BVH4 node j = greedy 4-wide collapse of binary node j.
+__global__ void k_collapse4(int n, const uint32_t* __restrict__ sorted_prim, const float* tri_box,
+                            const int* __restrict__ child, const float* ibox, float4* nodes,
+                            int node_base, int leaf_base) {
+    int j = blockIdx.x * blockDim.x + threadIdx.x;
+    int n_int = n > 1 ? n - 1 : 1;
+    if (j >= n_int) return;
+    int refs[4];
+    int cnt;
+    if (n > 1) {
+        auto ch = [&](int r, int side) { return __ldg(child + 2 * r + side); };
+        auto bx = [&](int r, float bb[6]) {
+            for (int k = 0; k < 6; ++k) bb[k] = __ldcg(ibox + 6 * r + k);
+        };
+        cnt = collapse4(j, ch, bx, refs);
+    } else {
+        refs[0] = n == 1 ? ~0 : REF_EMPTY;
+        refs[1] = refs[2] = refs[3] = REF_EMPTY;
+        cnt = n == 1 ? 1 : 0;
+    }
+    float boxes[4][6];
+    int g[4];
+    for (int k = 0; k < 4; ++k) {
+        child_box(refs[k], sorted_prim, tri_box, ibox, boxes[k]);
+        g[k] = global_ref(refs[k], node_base, leaf_base);
+    }
+    write_node4(nodes, node_base + j, boxes, g, cnt);
+}
+
 __global__ void k_pack_tris(int n, const uint32_t* __restrict__ sorted_prim,
                             const float* __restrict__ verts, const int* __restrict__ faces,
                             float4* tris, float* triv, int leaf_base) {
@@ -467,7 +496,9 @@ cudaError_t blas_build(const BlasBuildArgs& a, void* scratch, int* n_leaves_out,
     }
     int n_int = n > 1 ? n - 1 : 1;
     k_pack_nodes<<<(n_int + T_BLK - 1) / T_BLK, T_BLK, 0, stream>>>(n, sv, s.tri_box, s.child, s.ibox,
-                                                                    a.nodes, a.node_base, a.leaf_base);
+                                                                    a.bnodes, a.node_base, a.leaf_base);
+    k_collapse4<<<(n_int + T_BLK - 1) / T_BLK, T_BLK, 0, stream>>>(n, sv, s.tri_box, s.child, s.ibox,
+                                                                  a.nodes, a.node_base, a.leaf_base);
     if (n > 0)
         k_pack_tris<<<(n + T_BLK - 1) / T_BLK, T_BLK, 0, stream>>>(n, sv, a.verts, a.faces, a.tris,
                                                                   a.triv, a.leaf_base);

@@ -272,10 +272,12 @@ struct RayState {
         sr.hix = c.f(C_SR0 + 6); sr.hiy = c.f(C_SR0 + 7); sr.hiz = c.f(C_SR0 + 8);
     }
 
-    __device__ __forceinline__ void node_test(const float4& n0, const float4& n1, const float4& n2,
-                                              bool& h0, bool& h1, float& t0, float& t1) const {
-        h0 = slab(sr, n0.x, n0.y, n0.z, n0.w, n1.x, n1.y, U, t0);
-        h1 = slab(sr, n1.z, n1.w, n2.x, n2.y, n2.z, n2.w, U, t1);
+    // Slab tests of the 4 children of a BVH4 node (boxes stored per axis).
+    __device__ __forceinline__ void node4_test(const float4* f, float tn[4], bool h[4]) const {
+        h[0] = slab(sr, f[0].x, f[1].x, f[2].x, f[3].x, f[4].x, f[5].x, U, tn[0]);
+        h[1] = slab(sr, f[0].y, f[1].y, f[2].y, f[3].y, f[4].y, f[5].y, U, tn[1]);
+        h[2] = slab(sr, f[0].z, f[1].z, f[2].z, f[3].z, f[4].z, f[5].z, U, tn[2]);
+        h[3] = slab(sr, f[0].w, f[1].w, f[2].w, f[3].w, f[4].w, f[5].w, U, tn[3]);
     }
 
     // Resolve leaf `leaf` of the current instance in FP64 now (exact mode,
@@ -358,6 +360,40 @@ struct RayState {
     }
 };
 
+// Load the 6 box float4s and the refs of BVH4 node `node` (broadcast loads
+// in packet mode).
+__device__ __forceinline__ void load_node4(const SceneView& sv, int node, float4 f[6], int ref[4]) {
+    const float4* np = sv.nodes + 8 * (size_t)node;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) f[k] = __ldg(np + k);
+    const float4 r = __ldg(np + 6);
+    ref[0] = __float_as_int(r.x);
+    ref[1] = __float_as_int(r.y);
+    ref[2] = __float_as_int(r.z);
+    ref[3] = __float_as_int(r.w);
+}
+
+__device__ __forceinline__ void cswap(unsigned& ka, int& ra, unsigned& kb, int& rb) {
+    const bool sw = kb < ka;
+    const unsigned k = sw ? kb : ka;
+    const int r = sw ? rb : ra;
+    kb = sw ? ka : kb;
+    rb = sw ? ra : rb;
+    ka = k;
+    ra = r;
+}
+
+// Ascending sort of 4 (key, ref) pairs (5 compare-exchanges).
+__device__ __forceinline__ void sort4(unsigned k[4], int r[4]) {
+    cswap(k[0], r[0], k[1], r[1]);
+    cswap(k[2], r[2], k[3], r[3]);
+    cswap(k[0], r[0], k[2], r[2]);
+    cswap(k[1], r[1], k[3], r[3]);
+    cswap(k[1], r[1], k[2], r[2]);
+}
+
+constexpr unsigned KEY_MISS = 0x7f800000u;  // +inf bits: sorts after every hit (t >= 0)
+
 // ---- per-lane traversal (explicit rays; exact-mode fallback) -------------------
 // Ordered stackful traversal of the two-level BVH, one independent ray per
 // lane (Aila & Laine style, stack in local memory).
@@ -370,25 +406,34 @@ __device__ __forceinline__ void traverse_lane(const SceneView& sv, int env, RayS
     for (;;) {
         if (node >= 0) {
             if (COUNT) cnt.nodes++;
-            const float4* np = sv.nodes + 4 * node;
-            float4 n0 = __ldg(np), n1 = __ldg(np + 1), n2 = __ldg(np + 2), n3 = __ldg(np + 3);
-            bool h0, h1;
-            float t0, t1;
-            rs.node_test(n0, n1, n2, h0, h1, t0, t1);
-            int c0 = __float_as_int(n3.x), c1 = __float_as_int(n3.y);
-            if (h0 && h1) {
-                int far_c = t0 <= t1 ? c1 : c0;
-                node = t0 <= t1 ? c0 : c1;
-                if (sp < STACK_SIZE) stack[sp++] = far_c;
-                else sovf = true;
-            } else if (h0) {
-                node = c0;
-            } else if (h1) {
-                node = c1;
-            } else {
+            float4 f[6];
+            int ref[4];
+            load_node4(sv, node, f, ref);
+            float tn[4];
+            bool h[4];
+            rs.node4_test(f, tn, h);
+            unsigned key[4];
+            int nh = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                key[k] = h[k] ? __float_as_uint(tn[k]) : KEY_MISS;
+                nh += h[k] ? 1 : 0;
+            }
+            if (nh == 0) {
                 if (sp == 0) break;
                 node = stack[--sp];
+                continue;
             }
+            sort4(key, ref);
+            // push the farther hit children (farthest first), descend the nearest
+#pragma unroll
+            for (int k = 3; k >= 1; --k) {
+                if (k < nh) {
+                    if (sp < STACK_SIZE) stack[sp++] = ref[k];
+                    else sovf = true;
+                }
+            }
+            node = ref[0];
             continue;
         }
         if (node == SENTINEL) {  // leave the instance: back to the env-level ray
@@ -438,32 +483,50 @@ __device__ __forceinline__ void traverse_packet(const SceneView& sv, int env, Ra
     for (;;) {
         if (node >= 0) {
             if (COUNT) cnt.nodes++;
-            const float4* np = sv.nodes + 4 * node;
-            float4 n0 = __ldg(np), n1 = __ldg(np + 1), n2 = __ldg(np + 2), n3 = __ldg(np + 3);
-            bool h0, h1;
-            float t0, t1;
-            rs.node_test(n0, n1, n2, h0, h1, t0, t1);
-            const int c0 = __float_as_int(n3.x), c1 = __float_as_int(n3.y);
-            const unsigned m0 = __ballot_sync(FULL, h0), m1 = __ballot_sync(FULL, h1);
-            if (m0 && m1) {
-                const unsigned pref0 = __ballot_sync(FULL, h0 && (!h1 || t0 <= t1));
-                const bool first0 = 2 * __popc(pref0) >= __popc(m0 | m1);
-                if (sp < PSTACK) {
-                    if (leader) wstack[sp] = first0 ? c1 : c0;
-                    ++sp;
-                } else {
-                    sovf = true;
-                }
-                node = first0 ? c0 : c1;
-            } else if (m0) {
-                node = c0;
-            } else if (m1) {
-                node = c1;
-            } else {
+            float4 f[6];
+            int ref[4];
+            load_node4(sv, node, f, ref);
+            float tn[4];
+            bool h[4];
+            rs.node4_test(f, tn, h);
+            unsigned m[4];
+            int nh = 0, only = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                m[k] = __ballot_sync(FULL, h[k]);
+                if (m[k]) { ++nh; only = k; }
+            }
+            if (nh == 0) {
                 if (sp == 0) break;
                 __syncwarp();
                 node = wstack[--sp];
+                continue;
             }
+            if (nh == 1) {
+                node = ref[0];
+#pragma unroll
+                for (int k = 1; k < 4; ++k)
+                    if (only == k) node = ref[k];
+                continue;
+            }
+            // order the children by the nearest entry over the lanes that hit them
+            unsigned key[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                key[k] = m[k] ? __reduce_min_sync(FULL, h[k] ? __float_as_uint(tn[k]) : KEY_MISS) : KEY_MISS;
+            sort4(key, ref);
+#pragma unroll
+            for (int k = 3; k >= 1; --k) {
+                if (k < nh) {
+                    if (sp < PSTACK) {
+                        if (leader) wstack[sp] = ref[k];
+                        ++sp;
+                    } else {
+                        sovf = true;
+                    }
+                }
+            }
+            node = ref[0];
             continue;
         }
         if (node == SENTINEL) {

@@ -97,13 +97,6 @@ __device__ __forceinline__ int kdelta64(const uint64_t* k, int n, int i, int j) 
     return __clzll(k[i] ^ k[j]);  // keys are distinct (local index in the low bits)
 }
 
-__device__ void write_tlas_node(float4* nodes, int g, const float* a, const float* b, int ra, int rb) {
-    nodes[4 * g + 0] = make_float4(a[0], a[3], a[1], a[4]);
-    nodes[4 * g + 1] = make_float4(a[2], a[5], b[0], b[3]);
-    nodes[4 * g + 2] = make_float4(b[1], b[4], b[2], b[5]);
-    nodes[4 * g + 3] = make_float4(__int_as_float(ra), __int_as_float(rb), 0.0f, 0.0f);
-}
-
 __global__ void k_tlas(TlasArgs a, int rebuild) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int e = blockIdx.x;
@@ -116,14 +109,16 @@ __global__ void k_tlas(TlasArgs a, int rebuild) {
 
     if (n <= 1) {
         if (tid == 0) {
+            float b[4][6];
+            int refs[4] = {REF_EMPTY, REF_EMPTY, REF_EMPTY, REF_EMPTY};
+            for (int c = 0; c < 4; ++c)
+                for (int k = 0; k < 6; ++k) b[c][k] = EMPTY[k];
             if (n == 1) {
-                float b[6];
-                for (int k = 0; k < 6; ++k) b[k] = a.inst_box[6 * i0 + k];
-                write_tlas_node(a.nodes, nodebase, b, EMPTY, ~i0, REF_EMPTY);
+                for (int k = 0; k < 6; ++k) b[0][k] = a.inst_box[6 * i0 + k];
+                refs[0] = ~i0;
                 a.tlas_inst_parent[i0] = 0;
-            } else {
-                write_tlas_node(a.nodes, nodebase, EMPTY, EMPTY, REF_EMPTY, REF_EMPTY);
             }
+            write_node4(a.nodes, nodebase, b, refs, n);
             a.tlas_node_parent[toff] = -1;
             if (rebuild) a.tlas_depth[e] = 1;
         }
@@ -278,13 +273,23 @@ __global__ void k_tlas(TlasArgs a, int rebuild) {
         }
     }
     __syncthreads();
+    // BVH4 node j = greedy 4-wide collapse of binary node j
+    auto ch = [&](int r, int side) { return s.child[2 * r + side]; };
+    auto bx = [&](int r, float b[6]) {
+        for (int k = 0; k < 6; ++k) b[k] = s.ibox[6 * r + k];
+    };
     for (int j = tid; j < n - 1; j += blockDim.x) {
-        int ra = s.child[2 * j], rb = s.child[2 * j + 1];
-        const float* ba = ra < 0 ? s.box + 6 * ~ra : s.ibox + 6 * ra;
-        const float* bb = rb < 0 ? s.box + 6 * ~rb : s.ibox + 6 * rb;
-        int ga = ra < 0 ? ~(i0 + ~ra) : nodebase + ra;
-        int gb = rb < 0 ? ~(i0 + ~rb) : nodebase + rb;
-        write_tlas_node(a.nodes, nodebase + j, ba, bb, ga, gb);
+        int refs[4];
+        const int cnt = collapse4(j, ch, bx, refs);
+        float b[4][6];
+        int g[4];
+        for (int c = 0; c < 4; ++c) {
+            const int r = refs[c];
+            const float* src = r == REF_EMPTY ? EMPTY : (r < 0 ? s.box + 6 * ~r : s.ibox + 6 * r);
+            for (int k = 0; k < 6; ++k) b[c][k] = src[k];
+            g[c] = r == REF_EMPTY ? REF_EMPTY : (r < 0 ? ~(i0 + ~r) : nodebase + r);
+        }
+        write_node4(a.nodes, nodebase + j, b, g, cnt);
     }
 }
 

@@ -155,3 +155,64 @@ def test_large_mesh_multiblock_sort():
     assert np.all(np.diff(codes.astype(np.int64)) >= 0)
     for i in np.nonzero(np.diff(codes.astype(np.int64)) == 0)[0]:
         assert leaf_face[i] < leaf_face[i + 1]
+
+
+def _walk_bvh4(nodes, root, leaf_boxes=None):
+    """Collect leaves reachable from BVH4 node 0; check every child box
+    contains the boxes of its subtree (exactly: the union)."""
+    refs = nodes[:, 24:28].view(np.int32)
+    leaves = []
+
+    def box(n, k):
+        lo = np.asarray([nodes[n, 0 + k], nodes[n, 8 + k], nodes[n, 16 + k]])
+        hi = np.asarray([nodes[n, 4 + k], nodes[n, 12 + k], nodes[n, 20 + k]])
+        return lo, hi
+
+    def rec(n):
+        lo_all, hi_all = np.full(3, np.inf), np.full(3, -np.inf)
+        for k in range(4):
+            r = refs[n, k]
+            if r == np.iinfo(np.int32).min:
+                lo, hi = box(n, k)
+                assert np.all(np.isinf(lo)) and np.all(np.isinf(hi))
+                continue
+            lo, hi = box(n, k)
+            if r < 0:
+                leaves.append(~r)
+                if leaf_boxes is not None:
+                    blo, bhi = leaf_boxes(~r)
+                    assert np.array_equal(lo, blo) and np.array_equal(hi, bhi)
+            else:
+                clo, chi = rec(r - root)
+                assert np.array_equal(lo, clo) and np.array_equal(hi, chi)
+            lo_all, hi_all = np.minimum(lo_all, lo), np.maximum(hi_all, hi)
+        return lo_all, hi_all
+
+    rec(0)
+    return leaves
+
+
+@pytest.mark.parametrize("mesh_fn", [lambda: sg.cube_mesh(), lambda: sg.tree_mesh(np.random.default_rng(2)),
+                                     lambda: sg.sphere_mesh(1.0, 4)])
+def test_bvh4_blas_covers_every_leaf_once(mesh_fn):
+    mesh = mesh_fn()
+    sc = sg.assemble([mesh], [[(0, 0, sg.make_T(np.eye(3), (0, 0, 0)))]])
+    s = make_scene(sc, build=False)
+    _, leaf_face, _ = s.debug_export_blas(0)
+    nodes, root = s.debug_export_bvh4(0)
+    tri = mesh.verts[mesh.faces]
+    lo_t, hi_t = tri.min(1), tri.max(1)
+    leaves = _walk_bvh4(nodes, root, lambda l: (lo_t[leaf_face[l]], hi_t[leaf_face[l]]))
+    assert sorted(leaves) == list(range(len(leaf_face)))
+    # greedy collapse: nodes have up to 4 children, most internal nodes 4
+    cnt = nodes[:, 28].view(np.int32)
+    assert cnt.max() <= 4
+
+
+def test_bvh4_tlas_covers_every_instance_once():
+    sc, _ = sg.config2(n_envs=5)
+    s = make_scene(sc)
+    for e in range(5):
+        nodes, root = s.debug_export_bvh4(-1 - e)
+        leaves = _walk_bvh4(nodes, root)
+        assert sorted(leaves) == list(range(int(sc.env_off[e]), int(sc.env_off[e + 1])))
