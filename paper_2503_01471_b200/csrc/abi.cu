@@ -489,6 +489,8 @@ agr_status agr_cast_pinhole(agr_scene s, const agr_pinhole* cam, agr_distance ki
     a.fy = cam->fy;
     a.cx = cam->cx;
     a.cy = cam->cy;
+    a.inv_fx64 = 1.0 / (double)cam->fx;
+    a.inv_fy64 = 1.0 / (double)cam->fy;
     a.poses = poses;
     a.S = n_sensors;
     return run_cast(s, a, (cudaStream_t)stream);
@@ -652,6 +654,8 @@ agr_status agr_cast_pinhole_host(agr_scene s, const agr_pinhole* cam, agr_distan
     a.fy = cam->fy;
     a.cx = cam->cx;
     a.cy = cam->cy;
+    a.inv_fx64 = 1.0 / (double)cam->fx;
+    a.inv_fy64 = 1.0 / (double)cam->fy;
     a.poses = s->e2e_poses;
     a.S = n_sensors;
     return e2e_run(s, a, (int64_t)n_sensors * cam->width * cam->height, out_host);

@@ -221,6 +221,7 @@ struct CastArgs {
     int kind;             // pinhole: 0 depth, 1 range
     int W, H;             // pinhole image / beams (W = K columns, H = C channels)
     float fx, fy, cx, cy;
+    double inv_fx64, inv_fy64;  // 1 / (double)fx, 1 / (double)fy (FP64 raygen)
     const float* beams;   // [C][K][3]
     const float* poses;   // [n_envs][S][12]
     int S;

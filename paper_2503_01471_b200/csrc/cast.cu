@@ -169,7 +169,7 @@ __device__ __noinline__ void brute64(SceneView sv, int env, Ray64 r64, double tm
 enum ColdField {
     C_OX, C_OY, C_OZ, C_DX, C_DY, C_DZ, C_Q,
     C_OOX, C_OOY, C_OOZ, C_ODX, C_ODY, C_ODZ, C_DELTA, C_DLEN,
-    C_SR0, C_SR_END = C_SR0 + 9,
+    C_SR0, C_ESR0 = C_SR0 + 9, C_ESR_END = C_ESR0 + 9,
     C_TL0, C_INST0 = C_TL0 + NSLOT, C_LEAF0 = C_INST0 + NSLOT,
     C_FACE = C_LEAF0 + NSLOT, C_BINST, C_BLEAF, N_COLD
 };
@@ -217,6 +217,7 @@ struct RayState {
         c.f(C_Q) = q;
         // env level: the origin is an exact input, the direction carries rounding
         sr = make_slab(o, d, K_ERR * q);
+        save_slab(C_ESR0);
         cur_inst = -1;
 #pragma unroll
         for (int k = 0; k < NSLOT; ++k) { c.f(C_TL0 + k) = inf_f(); c.i(C_INST0 + k) = -1; c.i(C_LEAF0 + k) = -1; }
@@ -229,7 +230,7 @@ struct RayState {
     }
 
     __device__ __forceinline__ void exit_instance() {
-        sr = make_slab(o(), d(), K_ERR * c.f(C_Q));
+        load_slab(C_ESR0);  // the env-level box-test state saved by init()
         cur_inst = -1;
     }
 
@@ -254,22 +255,22 @@ struct RayState {
         const float dd = dot(od, od);
         c.f(C_DLEN) = dd > 0.0f ? dd * rsqrtf(dd) * 1.000001f : 0.0f;
         sr = make_slab(oo, od, delta);
-        save_slab();
+        save_slab(C_SR0);
         cur_inst = inst;
         return __float_as_int(r3.x);
     }
 
     // The box-test state is parked in shared memory while a triangle is
     // tested and reloaded afterwards, so it holds no registers there.
-    __device__ __forceinline__ void save_slab() const {
-        c.f(C_SR0 + 0) = sr.idx; c.f(C_SR0 + 1) = sr.idy; c.f(C_SR0 + 2) = sr.idz;
-        c.f(C_SR0 + 3) = sr.lox; c.f(C_SR0 + 4) = sr.loy; c.f(C_SR0 + 5) = sr.loz;
-        c.f(C_SR0 + 6) = sr.hix; c.f(C_SR0 + 7) = sr.hiy; c.f(C_SR0 + 8) = sr.hiz;
+    __device__ __forceinline__ void save_slab(int at) const {
+        c.f(at + 0) = sr.idx; c.f(at + 1) = sr.idy; c.f(at + 2) = sr.idz;
+        c.f(at + 3) = sr.lox; c.f(at + 4) = sr.loy; c.f(at + 5) = sr.loz;
+        c.f(at + 6) = sr.hix; c.f(at + 7) = sr.hiy; c.f(at + 8) = sr.hiz;
     }
-    __device__ __forceinline__ void load_slab() {
-        sr.idx = c.f(C_SR0 + 0); sr.idy = c.f(C_SR0 + 1); sr.idz = c.f(C_SR0 + 2);
-        sr.lox = c.f(C_SR0 + 3); sr.loy = c.f(C_SR0 + 4); sr.loz = c.f(C_SR0 + 5);
-        sr.hix = c.f(C_SR0 + 6); sr.hiy = c.f(C_SR0 + 7); sr.hiz = c.f(C_SR0 + 8);
+    __device__ __forceinline__ void load_slab(int at = C_SR0) {
+        sr.idx = c.f(at + 0); sr.idy = c.f(at + 1); sr.idz = c.f(at + 2);
+        sr.lox = c.f(at + 3); sr.loy = c.f(at + 4); sr.loz = c.f(at + 5);
+        sr.hix = c.f(at + 6); sr.hiy = c.f(at + 7); sr.hiz = c.f(at + 8);
     }
 
     // Slab tests of the 4 children of a BVH4 node (boxes stored per axis).
@@ -515,16 +516,17 @@ __device__ __forceinline__ void traverse_packet(const SceneView& sv, int env, Ra
             for (int k = 0; k < 4; ++k)
                 key[k] = m[k] ? __reduce_min_sync(FULL, h[k] ? __float_as_uint(tn[k]) : KEY_MISS) : KEY_MISS;
             sort4(key, ref);
-#pragma unroll
-            for (int k = 3; k >= 1; --k) {
-                if (k < nh) {
-                    if (sp < PSTACK) {
-                        if (leader) wstack[sp] = ref[k];
-                        ++sp;
-                    } else {
-                        sovf = true;
-                    }
+            // push the farther children, farthest first
+            if (sp + 3 <= PSTACK) {
+                if (leader) {
+                    int q = sp;
+                    if (nh > 3) wstack[q++] = ref[3];
+                    if (nh > 2) wstack[q++] = ref[2];
+                    wstack[q] = ref[1];
                 }
+                sp += nh - 1;  // nh is warp-uniform
+            } else {
+                sovf = true;
             }
             node = ref[0];
             continue;
@@ -628,8 +630,8 @@ __device__ __forceinline__ Ray64 gen_ray64(const CastArgs& a, const RayId& id) {
     const float* P = a.poses + 12 * ((int64_t)id.env * a.S + id.sensor);
     d3 ds64;
     if (MODEL == 1) {
-        double xs64 = ((double)id.col + 0.5 - (double)a.cx) / (double)a.fx;
-        double ys64 = ((double)id.row + 0.5 - (double)a.cy) / (double)a.fy;
+        double xs64 = ((double)id.col + 0.5 - (double)a.cx) * a.inv_fx64;
+        double ys64 = ((double)id.row + 0.5 - (double)a.cy) * a.inv_fy64;
         ds64 = mkd(1.0, -xs64, -ys64);
         if (a.kind == 1) {
             double n = sqrt(dotd(ds64, ds64));
