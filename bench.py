@@ -43,9 +43,12 @@ TRAFFIC_PATH = os.path.join(ROOT, "profiles", "cast_traffic.json")
 
 # Algorithmic thread-instruction costs of one unit of traversal work
 # (DESIGN.md §8 "ALU roofline"): per child box test, per
-# stack pop, per triangle test, per instance entry, per ray (generation +
-# epilogue).  Multiplied by the counted units of a launch.
+# node pop, per triangle test, per instance entry, per ray (generation +
+# epilogue).  Multiplied by each ray's OWN traversal units (counted with one
+# ray per lane, so packet over-visits are not counted as useful work); a
+# BVH4 node visit is 4 child box tests.
 C_BOX, C_LOOP, C_TRI, C_XF, C_RAY = 20, 15, 40, 25, 70
+BVH_WIDTH = 4
 
 WORKLOADS = {
     3: "c3: forest, 1024 envs/GPU (ground + 40 trees + 10 rocks, ~56k tri/env), "
@@ -314,12 +317,17 @@ def main():
     value = rays_per_step * world / (total_ms / 1e3 / args.steps)
 
     # ---- per-ray work counters (separate, untimed counting launch) --------
-    counters = None
+    counters = lane_counters = None
     if not args.no_counters:
         scene.enable_counters(True)
         step(0)
         torch.cuda.synchronize()
         counters = scene.counters()
+        scene.set_traversal(1)  # each ray's own units (algorithmic work)
+        step(0)
+        torch.cuda.synchronize()
+        lane_counters = scene.counters()
+        scene.set_traversal(0 if args.traversal == "auto" else 1)
         scene.enable_counters(False)
 
     # ---- end to end through the public C ABI with host buffers ------------
@@ -366,10 +374,10 @@ def main():
     clocks = clk.summary()
     cast_s = cast_total / 1e3 / args.steps  # per launch (per rank)
     roof = None
-    if counters and counters["rays"] > 0:
-        per = {k: counters[k] / counters["rays"] for k in ("nodes", "leaves", "instances")}
+    if lane_counters and lane_counters["rays"] > 0:
+        per = {k: lane_counters[k] / lane_counters["rays"] for k in ("nodes", "leaves", "instances")}
         pops = per["nodes"] + per["leaves"] + per["instances"]
-        w_ray = 2 * C_BOX * per["nodes"] + C_LOOP * pops + C_TRI * per["leaves"] + \
+        w_ray = BVH_WIDTH * C_BOX * per["nodes"] + C_LOOP * pops + C_TRI * per["leaves"] + \
             C_XF * per["instances"] + C_RAY
         achieved = w_ray * rays_per_step / cast_s / 1e12
         mhz = clocks.get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)
@@ -413,6 +421,8 @@ def main():
         "gpu_launches": LAUNCHES_PER_STEP * args.steps, "clocks": clocks,
         "counters_per_ray": ({k: v / counters["rays"] for k, v in counters.items() if k != "rays"}
                              if counters else None),
+        "counters_per_ray_own": ({k: v / lane_counters["rays"] for k, v in lane_counters.items()
+                                  if k != "rays"} if lane_counters else None),
     }
     print(json.dumps(line))
     return 0

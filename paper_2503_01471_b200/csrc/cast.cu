@@ -128,7 +128,7 @@ struct Slots {
     int leaf[NSLOT];
 };
 
-struct Counters { unsigned nodes, leaves, insts, f64, overflow; };
+struct Counters { unsigned nodes, leaves, insts, f64, overflow, tnodes; };
 
 struct Best64 {
     double t;
@@ -407,6 +407,7 @@ __device__ __forceinline__ void traverse_lane(const SceneView& sv, int env, RayS
     for (;;) {
         if (node >= 0) {
             if (COUNT) cnt.nodes++;
+            if (COUNT && rs.cur_inst < 0) cnt.tnodes++;
             float4 f[6];
             int ref[4];
             load_node4(sv, node, f, ref);
@@ -484,6 +485,7 @@ __device__ __forceinline__ void traverse_packet(const SceneView& sv, int env, Ra
     for (;;) {
         if (node >= 0) {
             if (COUNT) cnt.nodes++;
+            if (COUNT && rs.cur_inst < 0) cnt.tnodes++;
             float4 f[6];
             int ref[4];
             load_node4(sv, node, f, ref);
@@ -705,7 +707,7 @@ __global__ void __launch_bounds__(CAST_THREADS, CAST_MIN_BLOCKS) k_cast(const __
     const bool trace = id.env < a.env_end && (id.active || MODEL != 0);
     id.col = min(id.col, a.W - 1);
     id.row = min(id.row, a.H - 1);
-    Counters cnt = {0, 0, 0, 0, 0};
+    Counters cnt = {0, 0, 0, 0, 0, 0};
     RayState rs;
     Best64 best;
     best.face = -1;
@@ -740,22 +742,24 @@ __global__ void __launch_bounds__(CAST_THREADS, CAST_MIN_BLOCKS) k_cast(const __
         }
     }
     if (COUNT) {
-        unsigned v[5] = {cnt.nodes, cnt.leaves, cnt.insts, cnt.f64, cnt.overflow};
+        unsigned v[6] = {cnt.nodes, cnt.leaves, cnt.insts, cnt.f64, cnt.overflow, cnt.tnodes};
         unsigned rays = id.active ? 1u : 0u;
         for (int o2 = 16; o2 > 0; o2 >>= 1) {
             rays += __shfl_xor_sync(0xFFFFFFFFu, rays, o2);
-            for (int k = 0; k < 5; ++k) v[k] += __shfl_xor_sync(0xFFFFFFFFu, v[k], o2);
+            for (int k = 0; k < 6; ++k) v[k] += __shfl_xor_sync(0xFFFFFFFFu, v[k], o2);
         }
         if ((threadIdx.x & 31) == 0) {
             atomicAdd(a.counters + 0, (unsigned long long)rays);
-            for (int k = 0; k < 5; ++k) atomicAdd(a.counters + 1 + k, (unsigned long long)v[k]);
+            for (int k = 0; k < 6; ++k) atomicAdd(a.counters + 1 + k, (unsigned long long)v[k]);
         }
     }
     if (!id.active) return;
     const bool hit = best.face >= 0;
-    if (a.out_dist) a.out_dist[id.out] = hit ? (float)best.t : a.max_range;
-    if (a.out_seg) a.out_seg[id.out] = hit ? __ldg(a.sv.inst_label + best.inst) : -1;
-    if (a.out_face) a.out_face[id.out] = hit ? best.face : -1;
+    // streaming stores: the images are written once and must not evict the
+    // L2-resident BVH
+    if (a.out_dist) __stcs(a.out_dist + id.out, hit ? (float)best.t : a.max_range);
+    if (a.out_seg) __stcs(a.out_seg + id.out, hit ? __ldg(a.sv.inst_label + best.inst) : -1);
+    if (a.out_face) __stcs(a.out_face + id.out, hit ? best.face : -1);
 }
 
 template <int MODEL>
