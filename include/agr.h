@@ -57,7 +57,7 @@
 extern "C" {
 #endif
 
-#define AGR_ABI_VERSION 1
+#define AGR_ABI_VERSION 2
 
 typedef int32_t agr_status;
 enum {
@@ -101,12 +101,23 @@ typedef enum { AGR_DEPTH = 0, AGR_RANGE = 1 } agr_distance;
 /* Output images.  Each pointer is caller-owned memory (device memory for
  * the device casts, host memory for the *_host casts) laid out
  * [n_envs][n_sensors][rows][cols] (pinhole rows = height, cols = width;
- * beams rows = C channels, cols = K columns; rays: [n_envs][R]).  Any
- * pointer may be NULL to skip that channel. */
+ * beams rows = C channels, cols = K columns; rays: [n_envs][R]), with a
+ * trailing vector dimension for normal / bary / point.  Any pointer may be
+ * NULL to skip that channel.  Channels after `face` are the per-hit data
+ * of PAPER.md:218 / :228 (surface normals, barycentric coordinates, point
+ * clouds), computed in FP64 from the winning triangle. */
 typedef struct {
     float* dist;          /* depth / range (metres); max_range on a miss     */
     int32_t* seg;         /* instance label, -1 on a miss                    */
     int32_t* face;        /* per-env face index, -1 on a miss                */
+    float* normal;        /* [..][3] unit geometric normal of the hit face in
+                             the env frame, oriented towards the ray origin
+                             (n . d < 0); (0,0,0) on a miss                  */
+    float* bary;          /* [..][2] (b1, b2): hit = (1-b1-b2) v0 + b1 v1 +
+                             b2 v2 over the face's vertices in face order;
+                             (-1,-1) on a miss                               */
+    float* point;         /* [..][3] o + dist * d in the env frame (the hit
+                             point; the max-range point on a miss)           */
 } agr_outputs;
 
 /* Scene statistics (sizes in elements / bytes of library-owned memory). */

@@ -77,7 +77,7 @@ def _load():
         _lib.oracle_cast.restype = ctypes.c_int
         _lib.oracle_cast.argtypes = [ctypes.POINTER(_Scene), ctypes.POINTER(_Rays),
                                      ctypes.c_void_p, ctypes.c_int64, ctypes.c_double,
-                                     ctypes.c_int32] + [ctypes.c_void_p] * 7
+                                     ctypes.c_int32] + [ctypes.c_void_p] * 10
         _lib.oracle_last_tests.restype = ctypes.c_int64
     return _lib
 
@@ -96,10 +96,13 @@ class OracleResult:
     t2: np.ndarray     # float64 second-best candidate t
     graze: np.ndarray  # float64 silhouette diagnostic
     tests: int         # ray/triangle tests performed
+    normal: np.ndarray = None  # float64 [n][3] (extras=True)
+    bary: np.ndarray = None    # float64 [n][2]
+    point: np.ndarray = None   # float64 [n][3]
 
 
 def cast(scene, rays: dict, query=None, n_threads: int = 0, amb_eps: float = AMB_EPS,
-         graze: bool = False) -> OracleResult:
+         graze: bool = False, extras: bool = False) -> OracleResult:
     """Run the oracle.
 
     ``scene``: an object with numpy fields ``verts, vert_off, faces, face_off,
@@ -152,9 +155,14 @@ def cast(scene, rays: dict, query=None, n_threads: int = 0, amb_eps: float = AMB
                        np.empty(n, np.int32), np.empty(n, np.int32),
                        np.empty(n, np.int32), np.empty(n, np.float64),
                        np.full(n, np.inf), 0)
+    if extras:
+        out.normal = np.empty((n, 3), np.float64)
+        out.bary = np.empty((n, 2), np.float64)
+        out.point = np.empty((n, 3), np.float64)
     rc = lib.oracle_cast(ctypes.byref(sc), ctypes.byref(r), _ptr(q), n, amb_eps, n_threads,
                          _ptr(out.t64), _ptr(out.dist), _ptr(out.seg), _ptr(out.face),
-                         _ptr(out.amb), _ptr(out.t2), _ptr(out.graze) if graze else None)
+                         _ptr(out.amb), _ptr(out.t2), _ptr(out.graze) if graze else None,
+                         _ptr(out.normal), _ptr(out.bary), _ptr(out.point))
     if rc != 0:
         raise ValueError("oracle_cast rejected its input")
     out.tests = int(lib.oracle_last_tests())

@@ -142,6 +142,7 @@ typedef struct {
     double t;
     int32_t seg, face, amb;
     double t2, graze;
+    double normal[3], bary[2], point[3];
 } ray_result;
 
 static void cast_one(const world_mesh* w, v3 o, v3 d, double max_range,
@@ -212,6 +213,25 @@ static void cast_one(const world_mesh* w, v3 o, v3 d, double max_range,
     out->amb = amb;
     out->t2 = second_t;
     out->graze = graze;
+    /* per-hit channels of the winning face */
+    out->point[0] = o.x + out->t * d.x;
+    out->point[1] = o.y + out->t * d.y;
+    out->point[2] = o.z + out->t * d.z;
+    if (best_f >= 0) {
+        v3 a = w->v[3 * best_f], b = w->v[3 * best_f + 1], c = w->v[3 * best_f + 2];
+        v3 n = vcross(vsub(b, a), vsub(c, a));
+        double nn = vdot(n, n);
+        double s = 1.0 / sqrt(nn);
+        if (vdot(n, d) > 0.0) s = -s;
+        out->normal[0] = n.x * s; out->normal[1] = n.y * s; out->normal[2] = n.z * s;
+        v3 p = {out->point[0], out->point[1], out->point[2]};
+        /* p = a + b1 (b - a) + b2 (c - a): cross with (c - a), resp. (b - a) */
+        out->bary[0] = vdot(vcross(vsub(p, a), vsub(c, a)), n) / nn;
+        out->bary[1] = vdot(vcross(vsub(b, a), vsub(p, a)), n) / nn;
+    } else {
+        out->normal[0] = out->normal[1] = out->normal[2] = 0.0;
+        out->bary[0] = out->bary[1] = -1.0;
+    }
 }
 
 /* ---- threading over the (env-sorted) query list ------------------------ */
@@ -224,6 +244,7 @@ typedef struct {
     double eps;
     double* t64; float* dist; int32_t* seg; int32_t* face; int32_t* amb;
     double* t2; double* graze;
+    double* normal; double* bary; double* point;
     int64_t tests;
     int status;
 } job;
@@ -253,6 +274,11 @@ static void* worker(void* arg) {
         jb->amb[q] = rr.amb;
         if (jb->t2) jb->t2[q] = rr.t2;
         if (jb->graze) jb->graze[q] = rr.graze;
+        for (int k = 0; k < 3; ++k) {
+            if (jb->normal) jb->normal[3 * q + k] = rr.normal[k];
+            if (jb->point) jb->point[3 * q + k] = rr.point[k];
+        }
+        if (jb->bary) { jb->bary[2 * q] = rr.bary[0]; jb->bary[2 * q + 1] = rr.bary[1]; }
     }
     free(w.v);
     free(w.label);
@@ -280,7 +306,8 @@ static int validate(const oracle_scene* sc, const oracle_rays* r) {
 int oracle_cast(const oracle_scene* sc, const oracle_rays* r,
                 const int64_t* query, int64_t n_query, double eps,
                 int32_t n_threads, double* t64, float* dist, int32_t* seg,
-                int32_t* face, int32_t* amb, double* t2, double* graze) {
+                int32_t* face, int32_t* amb, double* t2, double* graze,
+                double* normal, double* bary, double* point) {
     if (validate(sc, r) != 0) return -1;
     int64_t n_rays_total;
     if (r->model == ORACLE_RAYS) n_rays_total = (int64_t)sc->n_envs * r->R;
@@ -312,6 +339,7 @@ int oracle_cast(const oracle_scene* sc, const oracle_rays* r,
         jb->eps = eps;
         jb->t64 = t64; jb->dist = dist; jb->seg = seg; jb->face = face;
         jb->amb = amb; jb->t2 = t2; jb->graze = graze;
+        jb->normal = normal; jb->bary = bary; jb->point = point;
         if (n_threads == 1) worker(jb);
         else if (pthread_create(&th[i], NULL, worker, jb) != 0) { jb->status = -1; th[i] = 0; }
     }

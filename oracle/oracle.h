@@ -91,13 +91,22 @@ enum {
  *   graze[q] smallest distance (scene units) by which the plane hit of a
  *            triangle closer than the winner lies outside that triangle
  *            (diagnostic for silhouette rays; +inf if none)     [may be NULL]
+ *   normal[3q..] unit geometric normal of the winning face, oriented so
+ *            that n . d < 0 (towards the ray origin); 0 on a miss [may be NULL]
+ *   bary[2q..] (b1, b2) with hit = (1-b1-b2) v0 + b1 v1 + b2 v2 over the
+ *            face's vertices, from the plane hit point by cross-product
+ *            area ratios; -1 on a miss                          [may be NULL]
+ *   point[3q..] o + t d (t = the reported distance)             [may be NULL]
+ * (PAPER.md:218 surface normals; :228 "barycentric coordinates of
+ * intersecting rays", "point clouds and surface normals".)
  * n_threads <= 0 uses all online cores.  Returns 0, or -1 on bad input.
  */
 int oracle_cast(const oracle_scene* scene, const oracle_rays* rays,
                 const int64_t* query, int64_t n_query, double amb_eps,
                 int32_t n_threads,
                 double* t64, float* dist, int32_t* seg, int32_t* face,
-                int32_t* amb, double* t2, double* graze);
+                int32_t* amb, double* t2, double* graze,
+                double* normal, double* bary, double* point);
 
 /* Number of triangle tests the last oracle_cast call performed (for the
  * cpu_baseline report: ray-triangle tests/s). */

@@ -53,7 +53,13 @@ class agr_pinhole(ctypes.Structure):
 
 
 class agr_outputs(ctypes.Structure):
-    _fields_ = [("dist", ctypes.c_void_p), ("seg", ctypes.c_void_p), ("face", ctypes.c_void_p)]
+    _fields_ = [("dist", ctypes.c_void_p), ("seg", ctypes.c_void_p), ("face", ctypes.c_void_p),
+                ("normal", ctypes.c_void_p), ("bary", ctypes.c_void_p), ("point", ctypes.c_void_p)]
+
+
+# channel -> (torch dtype name, trailing vector size)
+CHANNELS = {"dist": ("float32", None), "seg": ("int32", None), "face": ("int32", None),
+            "normal": ("float32", 3), "bary": ("float32", 2), "point": ("float32", 3)}
 
 
 class agr_scene_info(ctypes.Structure):
@@ -144,8 +150,8 @@ def _stream_handle(stream):
     return stream.cuda_stream
 
 
-def _outputs(dist, seg, face):
-    return agr_outputs(_ptr(dist), _ptr(seg), _ptr(face))
+def _outputs(out: dict):
+    return agr_outputs(*(_ptr(out.get(k)) for k in CHANNELS))
 
 
 class Scene:
@@ -216,8 +222,10 @@ class Scene:
         dev = torch.device("cuda", self.device) if device_tensors else torch.device("cpu")
         out = {}
         for ch in channels:
-            dt = torch.float32 if ch == "dist" else torch.int32
-            out[ch] = torch.empty(shape, dtype=dt, device=dev, pin_memory=pin and not device_tensors)
+            dt, vec = CHANNELS[ch]
+            shp = tuple(shape) + ((vec,) if vec else ())
+            out[ch] = torch.empty(shp, dtype=getattr(torch, dt), device=dev,
+                                  pin_memory=pin and not device_tensors)
         return out
 
     def cast_pinhole(self, cam: dict, poses, max_range: float, kind: int = AGR_DEPTH,
@@ -229,7 +237,7 @@ class Scene:
         c = agr_pinhole(cam["W"], cam["H"], cam["fx"], cam["fy"], cam["cx"], cam["cy"])
         _check(load().agr_cast_pinhole(self.handle, ctypes.byref(c), kind, _ptr(poses), S,
                                        float(max_range),
-                                       _outputs(out.get("dist"), out.get("seg"), out.get("face")),
+                                       _outputs(out),
                                        _stream_handle(stream)))
         return out
 
@@ -242,7 +250,7 @@ class Scene:
             out = self._alloc((self.n_envs, S, C, K), channels)
         _check(load().agr_cast_beams(self.handle, _ptr(beams), C, K, _ptr(poses), S,
                                      float(max_range),
-                                     _outputs(out.get("dist"), out.get("seg"), out.get("face")),
+                                     _outputs(out),
                                      _stream_handle(stream)))
         return out
 
@@ -253,7 +261,7 @@ class Scene:
         if out is None:
             out = self._alloc((self.n_envs, R), channels)
         _check(load().agr_cast_rays(self.handle, _ptr(orig), _ptr(dirs), R, float(max_range),
-                                    _outputs(out.get("dist"), out.get("seg"), out.get("face")),
+                                    _outputs(out),
                                     _stream_handle(stream)))
         return out
 
@@ -268,7 +276,7 @@ class Scene:
         c = agr_pinhole(cam["W"], cam["H"], cam["fx"], cam["fy"], cam["cx"], cam["cy"])
         _check(load().agr_cast_pinhole_host(self.handle, ctypes.byref(c), kind, _ptr(poses_host), S,
                                             float(max_range),
-                                            _outputs(out.get("dist"), out.get("seg"), out.get("face"))))
+                                            _outputs(out)))
         return out
 
     def cast_beams_host(self, beams_host, poses_host, max_range: float, out=None,
@@ -279,14 +287,14 @@ class Scene:
             out = self._alloc((self.n_envs, S, C, K), channels, False, pin=True)
         _check(load().agr_cast_beams_host(self.handle, _ptr(beams_host), C, K, _ptr(poses_host), S,
                                           float(max_range),
-                                          _outputs(out.get("dist"), out.get("seg"), out.get("face"))))
+                                          _outputs(out)))
         return out
 
     def checksum(self, out: dict, elems_per_env: int, stream=None):
         import torch
         sums = torch.zeros(self.n_envs, dtype=torch.int64, device=torch.device("cuda", self.device))
         _check(load().agr_checksum(self.handle,
-                                   _outputs(out.get("dist"), out.get("seg"), out.get("face")),
+                                   _outputs(out),
                                    int(elems_per_env), _ptr(sums), _stream_handle(stream)))
         return sums
 

@@ -464,6 +464,9 @@ static CastArgs base_args(agr_scene s, float max_range, agr_outputs out) {
     a.out_dist = out.dist;
     a.out_seg = out.seg;
     a.out_face = out.face;
+    a.out_normal = out.normal;
+    a.out_bary = out.bary;
+    a.out_point = out.point;
     a.env_begin = 0;
     a.env_end = s->n_envs;
     a.S = 1;
@@ -564,17 +567,28 @@ static bool is_pinned(const void* p) {
 
 // Casts env chunks into a double-buffered device area and streams each chunk
 // back to the host while the next one is traced.
+struct E2EChannel {
+    void* host;   // caller's host pointer (whole output)
+    int bytes;    // bytes per element
+};
+
 static agr_status e2e_run(agr_scene s, CastArgs& a, int64_t elems_per_env, agr_outputs out_host) {
     const int E = s->n_envs;
-    const int64_t bytes_per_env = elems_per_env * ((out_host.dist ? 4 : 0) + (out_host.seg ? 4 : 0) +
-                                                   (out_host.face ? 4 : 0));
+    E2EChannel ch[6] = {{out_host.dist, 4}, {out_host.seg, 4}, {out_host.face, 4},
+                        {out_host.normal, 12}, {out_host.bary, 8}, {out_host.point, 12}};
+    int64_t bytes_per_elem = 0;
+    bool direct = true;
+    for (auto& c : ch)
+        if (c.host) {
+            bytes_per_elem += c.bytes;
+            direct = direct && is_pinned(c.host);
+        }
     // ~8 chunks, at least 1 env each
     int chunk = (E + 7) / 8;
     if (chunk < 1) chunk = 1;
-    size_t chunk_bytes = (size_t)(chunk * bytes_per_env);
+    size_t chunk_bytes = (size_t)(chunk * elems_per_env * bytes_per_elem);
     agr_status st = e2e_prepare(s, a.S * 12 * sizeof(float) * (size_t)E, chunk_bytes);
     if (st != AGR_OK) return st;
-    const bool direct = is_pinned(out_host.dist) && is_pinned(out_host.seg) && is_pinned(out_host.face);
     if (!direct && chunk_bytes > s->e2e_host_bytes) {
         for (auto& h : s->e2e_host) {
             if (h) cudaFreeHost(h);
@@ -590,16 +604,23 @@ static agr_status e2e_run(agr_scene s, CastArgs& a, int64_t elems_per_env, agr_o
         int slot = k & 1;
         if (k >= 2) CK(cudaStreamWaitEvent(cs, s->e2e_event[2 + slot], 0));  // slot drained
         char* base = (char*)s->e2e_out[slot];
-        int64_t n = (int64_t)(e1 - e0) * elems_per_env;
+        const int64_t n = (int64_t)(e1 - e0) * elems_per_env;
         CastArgs c = a;
         c.env_begin = e0;
         c.env_end = e1;
-        // the chunk's outputs start at env e0 of the chunk buffer
-        c.out_env_base = e0;
+        c.out_env_base = e0;  // the chunk's outputs start at env e0 of the chunk buffer
+        char* dev[6];
         char* p = base;
-        if (out_host.dist) { c.out_dist = (float*)p; p += 4 * n; }
-        if (out_host.seg) { c.out_seg = (int*)p; p += 4 * n; }
-        if (out_host.face) { c.out_face = (int*)p; p += 4 * n; }
+        for (int q = 0; q < 6; ++q) {
+            dev[q] = ch[q].host ? p : nullptr;
+            if (ch[q].host) p += ch[q].bytes * n;
+        }
+        c.out_dist = (float*)dev[0];
+        c.out_seg = (int*)dev[1];
+        c.out_face = (int*)dev[2];
+        c.out_normal = (float*)dev[3];
+        c.out_bary = (float*)dev[4];
+        c.out_point = (float*)dev[5];
         c.sv = s->view();
         c.exact = s->exact;
         c.packet = s->traversal == 0 ? 1 : 0;
@@ -607,23 +628,23 @@ static agr_status e2e_run(agr_scene s, CastArgs& a, int64_t elems_per_env, agr_o
         CK(cast_launch(c, cs));
         CK(cudaEventRecord(s->e2e_event[slot], cs));
         CK(cudaStreamWaitEvent(xs, s->e2e_event[slot], 0));
-        p = base;
         const int64_t off = (int64_t)e0 * elems_per_env;
         if (direct) {
-            if (out_host.dist) { CK(cudaMemcpyAsync(out_host.dist + off, p, 4 * n, cudaMemcpyDeviceToHost, xs)); p += 4 * n; }
-            if (out_host.seg) { CK(cudaMemcpyAsync(out_host.seg + off, p, 4 * n, cudaMemcpyDeviceToHost, xs)); p += 4 * n; }
-            if (out_host.face) { CK(cudaMemcpyAsync(out_host.face + off, p, 4 * n, cudaMemcpyDeviceToHost, xs)); p += 4 * n; }
+            for (int q = 0; q < 6; ++q)
+                if (ch[q].host)
+                    CK(cudaMemcpyAsync((char*)ch[q].host + off * ch[q].bytes, dev[q], ch[q].bytes * n,
+                                       cudaMemcpyDeviceToHost, xs));
             CK(cudaEventRecord(s->e2e_event[2 + slot], xs));
         } else {
-            const size_t chunk_n_bytes =
-                (size_t)((out_host.dist ? 4 : 0) + (out_host.seg ? 4 : 0) + (out_host.face ? 4 : 0)) * n;
-            CK(cudaMemcpyAsync(s->e2e_host[slot], base, chunk_n_bytes, cudaMemcpyDeviceToHost, xs));
+            CK(cudaMemcpyAsync(s->e2e_host[slot], base, (size_t)(p - base), cudaMemcpyDeviceToHost, xs));
             CK(cudaEventRecord(s->e2e_event[2 + slot], xs));
             CK(cudaEventSynchronize(s->e2e_event[2 + slot]));
-            char* h = (char*)s->e2e_host[slot];
-            if (out_host.dist) { memcpy(out_host.dist + off, h, 4 * n); h += 4 * n; }
-            if (out_host.seg) { memcpy(out_host.seg + off, h, 4 * n); h += 4 * n; }
-            if (out_host.face) { memcpy(out_host.face + off, h, 4 * n); h += 4 * n; }
+            const char* hsrc = (const char*)s->e2e_host[slot];
+            for (int q = 0; q < 6; ++q)
+                if (ch[q].host) {
+                    memcpy((char*)ch[q].host + off * ch[q].bytes, hsrc, ch[q].bytes * n);
+                    hsrc += ch[q].bytes * n;
+                }
         }
     }
     CK(cudaStreamSynchronize(xs));
@@ -645,7 +666,7 @@ agr_status agr_cast_pinhole_host(agr_scene s, const agr_pinhole* cam, agr_distan
     if (st != AGR_OK) return st;
     CK(cudaMemcpyAsync(s->e2e_poses, poses_host, sizeof(float) * 12 * (size_t)n_sensors * s->n_envs,
                        cudaMemcpyHostToDevice, s->e2e_stream[0]));
-    CastArgs a = base_args(s, max_range, agr_outputs{nullptr, nullptr, nullptr});
+    CastArgs a = base_args(s, max_range, agr_outputs{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr});
     a.model = 1;
     a.kind = (int)kind;
     a.W = cam->width;
@@ -682,7 +703,7 @@ agr_status agr_cast_beams_host(agr_scene s, const float* dirs_host, int32_t C, i
     CK(cudaMemcpyAsync(s->e2e_beams, dirs_host, bb, cudaMemcpyHostToDevice, s->e2e_stream[0]));
     CK(cudaMemcpyAsync(s->e2e_poses, poses_host, sizeof(float) * 12 * (size_t)n_sensors * s->n_envs,
                        cudaMemcpyHostToDevice, s->e2e_stream[0]));
-    CastArgs a = base_args(s, max_range, agr_outputs{nullptr, nullptr, nullptr});
+    CastArgs a = base_args(s, max_range, agr_outputs{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr});
     a.model = 2;
     a.W = K;
     a.H = C;

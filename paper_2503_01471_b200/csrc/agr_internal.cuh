@@ -232,6 +232,9 @@ struct CastArgs {
     float* out_dist;
     int* out_seg;
     int* out_face;
+    float* out_normal;    // [..][3]
+    float* out_bary;      // [..][2]
+    float* out_point;     // [..][3]
     int env_begin, env_end;  // envs cast by this launch (chunking)
     int out_env_base;        // outputs are indexed from this env (0: global indexing)
     unsigned long long* counters;  // optional [8]

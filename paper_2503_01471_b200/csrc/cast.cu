@@ -665,6 +665,55 @@ __device__ __noinline__ void resolve_leaf64(const CastArgs* a, int inst, int lea
     *best = b;
 }
 
+// Per-hit channels of PAPER.md:218 / :228 (surface normal, barycentrics,
+// point cloud), in FP64 from the winning triangle (reading R20).
+template <int MODEL>
+__device__ __noinline__ void write_extra(const CastArgs* a, RayId id, Best64 best) {
+    const Ray64 r = gen_ray64<MODEL>(*a, id);
+    const int64_t o = id.out;
+    double t = best.face >= 0 ? best.t : (double)a->max_range;
+    if (a->out_point) {
+        a->out_point[3 * o + 0] = (float)(r.o.x + t * r.d.x);
+        a->out_point[3 * o + 1] = (float)(r.o.y + t * r.d.y);
+        a->out_point[3 * o + 2] = (float)(r.o.z + t * r.d.z);
+    }
+    if (!a->out_normal && !a->out_bary) return;
+    if (best.face < 0) {
+        if (a->out_normal) a->out_normal[3 * o] = a->out_normal[3 * o + 1] = a->out_normal[3 * o + 2] = 0.0f;
+        if (a->out_bary) a->out_bary[2 * o] = a->out_bary[2 * o + 1] = -1.0f;
+        return;
+    }
+    const float* T = a->sv.inst_T + 12 * best.inst;
+    const float* v = a->sv.triv + 9 * best.leaf;
+    d3 w[3];
+    for (int c = 0; c < 3; ++c) {
+        double x = v[3 * c], y = v[3 * c + 1], z = v[3 * c + 2];
+        w[c].x = (double)T[0] * x + (double)T[1] * y + (double)T[2] * z + (double)T[3];
+        w[c].y = (double)T[4] * x + (double)T[5] * y + (double)T[6] * z + (double)T[7];
+        w[c].z = (double)T[8] * x + (double)T[9] * y + (double)T[10] * z + (double)T[11];
+    }
+    const d3 e1 = subd(w[1], w[0]), e2 = subd(w[2], w[0]);
+    d3 n = crossd(e1, e2);
+    if (a->out_normal) {
+        double s = 1.0 / sqrt(dotd(n, n));
+        if (dotd(n, r.d) > 0.0) s = -s;  // face the ray origin
+        a->out_normal[3 * o + 0] = (float)(n.x * s);
+        a->out_normal[3 * o + 1] = (float)(n.y * s);
+        a->out_normal[3 * o + 2] = (float)(n.z * s);
+    }
+    if (a->out_bary) {
+        // Moller-Trumbore barycentrics of the FP64 ray: weights of v1, v2
+        const d3 p = crossd(r.d, e2);
+        const double det = dotd(e1, p);
+        const d3 s = subd(r.o, w[0]);
+        const double b1 = dotd(s, p) / det;
+        const d3 q = crossd(s, e1);
+        const double b2 = dotd(r.d, q) / det;
+        a->out_bary[2 * o + 0] = (float)b1;
+        a->out_bary[2 * o + 1] = (float)b2;
+    }
+}
+
 template <int MODEL>
 __device__ __forceinline__ RayId ray_id(const CastArgs& a) {
     RayId id;
@@ -760,6 +809,7 @@ __global__ void __launch_bounds__(CAST_THREADS, CAST_MIN_BLOCKS) k_cast(const __
     if (a.out_dist) __stcs(a.out_dist + id.out, hit ? (float)best.t : a.max_range);
     if (a.out_seg) __stcs(a.out_seg + id.out, hit ? __ldg(a.sv.inst_label + best.inst) : -1);
     if (a.out_face) __stcs(a.out_face + id.out, hit ? best.face : -1);
+    if (a.out_normal || a.out_bary || a.out_point) write_extra<MODEL>(&a, id, best);
 }
 
 template <int MODEL>

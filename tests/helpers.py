@@ -61,3 +61,33 @@ def compare(ref: "oracle.OracleResult", dist, seg, face, what=""):
     if msgs:
         raise AssertionError("\n".join(msgs))
     return out
+
+
+def compare_extras(ref: "oracle.OracleResult", normal=None, bary=None, point=None, face=None, what=""):
+    """Per-hit channels on every ray whose face equals the oracle's (all
+    non-ambiguous rays, by compare()): normal within 1e-6 per component,
+    barycentrics within 1e-6 absolute, point within max(1e-5, 1e-6 |p|)."""
+    same = np.ones(len(ref.t64), bool) if face is None else (np.asarray(face).reshape(-1) == ref.face)
+    msgs = []
+    if normal is not None:
+        n = np.asarray(normal, np.float64).reshape(-1, 3)
+        err = np.abs(n - ref.normal).max(1)
+        bad = np.nonzero(same & (err > 1e-6))[0]
+        if len(bad):
+            msgs.append(f"{what}: {len(bad)} normal mismatches, first {bad[0]}: {n[bad[0]]} vs {ref.normal[bad[0]]}")
+    if bary is not None:
+        b = np.asarray(bary, np.float64).reshape(-1, 2)
+        err = np.abs(b - ref.bary).max(1)
+        bad = np.nonzero(same & (err > 1e-6))[0]
+        if len(bad):
+            msgs.append(f"{what}: {len(bad)} bary mismatches, first {bad[0]}: {b[bad[0]]} vs {ref.bary[bad[0]]}")
+    if point is not None:
+        p = np.asarray(point, np.float64).reshape(-1, 3)
+        err = np.abs(p - ref.point).max(1)
+        tol = np.maximum(DIST_ABS, DIST_REL * np.abs(ref.point).max(1))
+        bad = np.nonzero(same & (err > tol))[0]
+        if len(bad):
+            msgs.append(f"{what}: {len(bad)} point mismatches, first {bad[0]}: {p[bad[0]]} vs {ref.point[bad[0]]}")
+    if msgs:
+        raise AssertionError("\n".join(msgs))
+    return int(same.sum())

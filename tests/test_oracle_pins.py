@@ -516,3 +516,79 @@ def test_query_subset_equals_full():
     assert np.array_equal(sub.t64, full.t64[q]) and np.array_equal(sub.face, full.face[q])
     one = cast_pinhole(sc, cam, s["poses"], query=q, n_threads=1)
     assert np.array_equal(one.t64, sub.t64)
+
+
+# --------------------------------------------------------------------------
+# per-hit channels: normal, barycentrics, point
+# --------------------------------------------------------------------------
+
+def test_plane_normal_and_point_closed_form():
+    """Camera facing a plane at distance d: the normal faces the camera,
+    (-1, 0, 0); the point is (d, -x' d, -y' d) (PAPER.md:218 normals, :228
+    point clouds)."""
+    dist = 3.0
+    cam = sg.pinhole(12, 8, 80.0)
+    sc = sg.assemble([quad_mesh()], [[(0, 1, sg.make_T(np.eye(3), (dist, 0, 0)))]])
+    r = cast_pinhole(sc, cam, sg.identity_poses(1), oracle.DEPTH, extras=True)
+    assert np.allclose(r.normal, [-1.0, 0.0, 0.0], atol=1e-15)
+    u = np.arange(cam["W"]) + 0.5 - cam["cx"]
+    v = np.arange(cam["H"]) + 0.5 - cam["cy"]
+    V, U = np.meshgrid(v, u, indexing="ij")
+    want = np.stack([np.full(U.shape, dist), -U / cam["fx"] * dist, -V / cam["fy"] * dist], -1)
+    assert np.allclose(r.point, want.reshape(-1, 3), atol=1e-12)
+
+
+def test_barycentric_reproduces_hit_point_and_linear_field():
+    """hit = (1-b1-b2) v0 + b1 v1 + b2 v2 over the face's world vertices, and
+    a linear per-vertex field interpolates to its value at the hit (SPEC
+    S:555-556 'linear-reproduction oracle')."""
+    rng = np.random.default_rng(21)
+    verts = rng.uniform(-1, 1, (60, 3)).astype(np.float32)
+    m = sg.Mesh("soup", verts, np.arange(60, dtype=np.int32).reshape(20, 3))
+    T = sg.make_T(sg.random_rotation(rng), (3.0, 0.2, -0.1), 1.1)
+    sc = sg.assemble([m], [[(0, 2, T)]])
+    o = np.zeros((1, 2000, 3), np.float32)
+    d = (rng.uniform([2.0, -1.5, -1.5], [4.0, 1.5, 1.5], (1, 2000, 3))).astype(np.float32)
+    r = cast_rays(sc, o, d, extras=True)
+    hit = r.face >= 0
+    assert hit.sum() > 100
+    A, b = T[:, :3].astype(np.float64), T[:, 3].astype(np.float64)
+    W = verts.astype(np.float64) @ A.T + b
+    tri = W.reshape(20, 3, 3)[r.face[hit]]
+    b1, b2 = r.bary[hit, 0], r.bary[hit, 1]
+    p = (1 - b1 - b2)[:, None] * tri[:, 0] + b1[:, None] * tri[:, 1] + b2[:, None] * tri[:, 2]
+    assert np.allclose(p, r.point[hit], atol=1e-9)
+    assert np.all((b1 >= -1e-12) & (b2 >= -1e-12) & (b1 + b2 <= 1 + 1e-12))
+    field = 0.7 * tri[..., 0] - 0.2 * tri[..., 2] + 0.5  # linear in position
+    interp = (1 - b1 - b2) * field[:, 0] + b1 * field[:, 1] + b2 * field[:, 2]
+    assert np.allclose(interp, 0.7 * r.point[hit, 0] - 0.2 * r.point[hit, 2] + 0.5, atol=1e-9)
+    assert np.all(r.bary[~hit] == -1.0) and np.all(r.normal[~hit] == 0.0)
+
+
+def test_vertex_aimed_ray_barycentrics():
+    """A ray through vertex v1 (resp. v2) of an isolated triangle has
+    barycentrics (1, 0) (resp. (0, 1))."""
+    v = np.asarray([[2, -1, -1], [2, 1, -1], [2, 0, 1]], np.float32)
+    sc = sg.assemble([sg.Mesh("t", v, np.asarray([[0, 1, 2]], np.int32))],
+                     [[(0, 1, sg.make_T(np.eye(3), (0, 0, 0)))]])
+    o = np.zeros((1, 3, 3), np.float32)
+    d = v[None].copy()
+    r = cast_rays(sc, o, d, extras=True)
+    assert np.allclose(r.bary, [[0, 0], [1, 0], [0, 1]], atol=1e-12)
+    assert np.allclose(r.t64, 1.0)
+
+
+def test_sphere_normals_face_the_origin():
+    """Inside an icosphere every normal points back at the camera (n . d <
+    0) and equals the reported face's unit normal up to sign."""
+    mesh = sg.sphere_mesh(2.0, 2)
+    sc = sg.assemble([mesh], [[(0, 1, sg.make_T(np.eye(3), (0, 0, 0)))]])
+    cam = sg.pinhole(16, 12, 100.0)
+    r = cast_pinhole(sc, cam, sg.identity_poses(1), oracle.RANGE, extras=True)
+    v = mesh.verts.astype(np.float64)[mesh.faces[r.face]]
+    n = np.cross(v[:, 1] - v[:, 0], v[:, 2] - v[:, 0])
+    n /= np.linalg.norm(n, axis=1, keepdims=True)
+    assert np.allclose(np.abs(np.einsum("ij,ij->i", n, r.normal)), 1.0, atol=1e-12)
+    # direction of each ray = point / |point| (camera at the origin)
+    dirs = r.point / np.linalg.norm(r.point, axis=1, keepdims=True)
+    assert np.all(np.einsum("ij,ij->i", r.normal, dirs) < 0)

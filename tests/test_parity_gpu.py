@@ -16,7 +16,7 @@ import torch
 import oracle
 import paper_2503_01471_b200 as agr
 import scenegen as sg
-from helpers import compare, oracle_rays
+from helpers import compare, compare_extras, oracle_rays
 from gpu_util import cast_sensor, dev, make_scene, to_np
 
 pytestmark = pytest.mark.gpu
@@ -294,3 +294,54 @@ def test_c5_sampled_with_refit_steps():
         sc2 = sg.Scene(sc.meshes, sc.env_off, sc.inst_asset, sc.inst_label, ring[step])
         ref = oracle.cast(sc2, oracle_rays(sensor, "depth"), query=q)
         compare(ref, got["dist"][q], got["seg"][q], got["face"][q], f"c5 step {step}")
+
+
+# ---- per-hit channels (normal, barycentrics, point cloud) -------------------
+
+ALL = ("dist", "seg", "face", "normal", "bary", "point")
+
+
+@pytest.mark.parametrize("kind", ["depth", "range"])
+def test_extras_c2_full(kind):
+    """Normals facing the sensor, barycentrics and points vs the oracle
+    (PAPER.md:218 Fig. 3a normals; :228 barycentrics, point clouds)."""
+    sc, sensor = sg.config2(n_envs=16)
+    s = make_scene(sc)
+    got = to_np(cast_sensor(s, sensor, kind, channels=ALL))
+    ref = oracle.cast(sc, oracle_rays(sensor, kind), extras=True)
+    compare(ref, got["dist"], got["seg"], got["face"], f"extras {kind}")
+    n = compare_extras(ref, got["normal"], got["bary"], got["point"], got["face"], f"extras {kind}")
+    assert n > 10000
+    # the extras do not change the core channels
+    core = to_np(cast_sensor(s, sensor, kind))
+    for k in core:
+        assert np.array_equal(core[k], got[k]), k
+
+
+def test_extras_lidar_and_rays():
+    sc, sensor = sg.config4(n_envs=6)
+    sensor = dict(sensor, beams=sg.lidar_beams(24, 64))
+    s = make_scene(sc)
+    got = to_np(cast_sensor(s, sensor, "range", channels=ALL))
+    ref = oracle.cast(sc, oracle_rays(sensor, "range"), extras=True)
+    compare(ref, got["dist"], got["seg"], got["face"], "lidar extras")
+    compare_extras(ref, got["normal"], got["bary"], got["point"], got["face"], "lidar extras")
+    sc2, _ = sg.config2(n_envs=4)
+    rng = np.random.default_rng(17)
+    o, d = _edge_targeted_rays(sc2, 2000, rng)
+    s2 = make_scene(sc2)
+    out = s2.cast_rays(torch.from_numpy(o).to(dev()), torch.from_numpy(d).to(dev()), 12.0, channels=ALL)
+    got = to_np(out)
+    ref = oracle.cast(sc2, dict(model=oracle.RAYS, orig=o, dir=d, max_range=12.0), extras=True)
+    compare(ref, got["dist"], got["seg"], got["face"], "edge extras")
+    compare_extras(ref, got["normal"], got["bary"], got["point"], got["face"], "edge extras")
+
+
+def test_extras_host_path():
+    sc, sensor = sg.config2(n_envs=9)
+    s = make_scene(sc)
+    a = to_np(cast_sensor(s, sensor, "range", channels=ALL))
+    poses = torch.from_numpy(np.ascontiguousarray(sensor["poses"])).pin_memory()
+    out = s.cast_pinhole_host(sensor["cam"], poses, sensor["max_range"], agr.AGR_RANGE, channels=ALL)
+    for k in a:
+        assert np.array_equal(a[k], out[k].numpy().reshape(-1)), k
