@@ -2,7 +2,7 @@
 NVCC ?= /usr/local/cuda/bin/nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall \
-           --expt-relaxed-constexpr -Xptxas -warn-spills
+           --expt-relaxed-constexpr
 PKG := paper_2503_01471_b200
 SRC := $(PKG)/csrc/blas.cu $(PKG)/csrc/tlas.cu $(PKG)/csrc/cast.cu \
        $(PKG)/csrc/checksum.cu $(PKG)/csrc/abi.cu

@@ -118,6 +118,12 @@ typedef struct {
                              (-1,-1) on a miss                               */
     float* point;         /* [..][3] o + dist * d in the env frame (the hit
                              point; the max-range point on a miss)           */
+    int32_t* valid;       /* stereo shadow mask: 0 if the
+                             segment from the hit point to the second sensor
+                             (agr_set_stereo) hits the scene at a distance in
+                             (eps, L - eps) from the hit point, else 1; 1 on
+                             a miss.  Pinhole and beam casts only (explicit
+                             rays write 1).                                  */
 } agr_outputs;
 
 /* Scene statistics (sizes in elements / bytes of library-owned memory). */
@@ -227,6 +233,14 @@ agr_status agr_cast_beams_host(agr_scene scene, const float* dirs_host, int32_t 
  */
 agr_status agr_checksum(agr_scene scene, agr_outputs out, int64_t elems_per_env,
                         uint64_t* sums, void* stream);
+
+/*
+ * Second sensor of a stereo pair for the `valid` output channel: its origin
+ * is (ox, oy, oz) in each pose's sensor frame (x forward, y left, z up;
+ * e.g. (0, -0.095, 0) for a right camera 95 mm away), and eps > 0 is the
+ * self-hit guard in metres.  Defaults: (0, -0.095, 0), 1e-4.
+ */
+agr_status agr_set_stereo(agr_scene scene, float ox, float oy, float oz, float eps);
 
 /*
  * Numerics mode (test hook): 0 = FP32 filter + FP64 arbitration (default);

@@ -27,7 +27,7 @@ _LIB_PATH = os.path.join(_HERE, "liboracle.so")
 
 RAYS, PINHOLE, BEAMS = 0, 1, 2
 DEPTH, RANGE = 0, 1
-AMB_TIE, AMB_RANGE, AMB_ZERO = 1, 2, 4
+AMB_TIE, AMB_RANGE, AMB_ZERO, AMB_SHADOW = 1, 2, 4, 8
 AMB_EPS = 1e-5  # metres, SURVEY.md §8(c) parity rules / BASELINE.json north_star
 
 
@@ -64,6 +64,7 @@ class _Rays(ctypes.Structure):
         ("beams", ctypes.c_void_p), ("C", ctypes.c_int32), ("K", ctypes.c_int32),
         ("poses", ctypes.c_void_p), ("S", ctypes.c_int32),
         ("max_range", ctypes.c_float),
+        ("stereo", ctypes.c_float * 3), ("stereo_eps", ctypes.c_float),
     ]
 
 
@@ -77,7 +78,7 @@ def _load():
         _lib.oracle_cast.restype = ctypes.c_int
         _lib.oracle_cast.argtypes = [ctypes.POINTER(_Scene), ctypes.POINTER(_Rays),
                                      ctypes.c_void_p, ctypes.c_int64, ctypes.c_double,
-                                     ctypes.c_int32] + [ctypes.c_void_p] * 10
+                                     ctypes.c_int32] + [ctypes.c_void_p] * 11
         _lib.oracle_last_tests.restype = ctypes.c_int64
     return _lib
 
@@ -99,16 +100,18 @@ class OracleResult:
     normal: np.ndarray = None  # float64 [n][3] (extras=True)
     bary: np.ndarray = None    # float64 [n][2]
     point: np.ndarray = None   # float64 [n][3]
+    valid: np.ndarray = None   # int32 [n] stereo shadow mask (stereo=...)
 
 
 def cast(scene, rays: dict, query=None, n_threads: int = 0, amb_eps: float = AMB_EPS,
-         graze: bool = False, extras: bool = False) -> OracleResult:
+         graze: bool = False, extras: bool = False, stereo=None) -> OracleResult:
     """Run the oracle.
 
     ``scene``: an object with numpy fields ``verts, vert_off, faces, face_off,
     env_off, inst_asset, inst_label, inst_T`` (see scenegen.Scene).
     ``rays``: dict with ``model`` and the fields of oracle_rays.
     ``query``: int64 flat ray ids (default: every ray).
+    ``stereo``: (offset xyz in the sensor frame, eps) -> also the shadow mask.
     """
     lib = _load()
     keep = []
@@ -155,6 +158,9 @@ def cast(scene, rays: dict, query=None, n_threads: int = 0, amb_eps: float = AMB
                        np.empty(n, np.int32), np.empty(n, np.int32),
                        np.empty(n, np.int32), np.empty(n, np.float64),
                        np.full(n, np.inf), 0)
+    if stereo is not None:
+        (r.stereo[0], r.stereo[1], r.stereo[2]), r.stereo_eps = stereo[0], stereo[1]
+        out.valid = np.empty(n, np.int32)
     if extras:
         out.normal = np.empty((n, 3), np.float64)
         out.bary = np.empty((n, 2), np.float64)
@@ -162,7 +168,7 @@ def cast(scene, rays: dict, query=None, n_threads: int = 0, amb_eps: float = AMB
     rc = lib.oracle_cast(ctypes.byref(sc), ctypes.byref(r), _ptr(q), n, amb_eps, n_threads,
                          _ptr(out.t64), _ptr(out.dist), _ptr(out.seg), _ptr(out.face),
                          _ptr(out.amb), _ptr(out.t2), _ptr(out.graze) if graze else None,
-                         _ptr(out.normal), _ptr(out.bary), _ptr(out.point))
+                         _ptr(out.normal), _ptr(out.bary), _ptr(out.point), _ptr(out.valid))
     if rc != 0:
         raise ValueError("oracle_cast rejected its input")
     out.tests = int(lib.oracle_last_tests())

@@ -234,6 +234,48 @@ static void cast_one(const world_mesh* w, v3 o, v3 d, double max_range,
     }
 }
 
+/* ---- stereo shadow mask --------------------------------- */
+/* "Shadows observed in stereo-camera systems are simulated by projecting
+ * rays back from the points-of-intersection towards the second sensor and
+ * marking pixels corresponding to the rays that intersect with the
+ * environment as invalid."  Segment from the FP64 hit point p to the second
+ * sensor's origin o2; invalid if any closed triangle meets it at a distance
+ * in (eps, L - eps) from p (reading R21). */
+static int32_t stereo_valid(const oracle_rays* r, int64_t id, const world_mesh* w,
+                            const ray_result* rr, v3 o, v3 d, double amb_eps, int* amb) {
+    *amb = 0;
+    if (r->model == ORACLE_RAYS || rr->face < 0) return 1;
+    int64_t es = r->model == ORACLE_PINHOLE ? id / ((int64_t)r->W * r->H)
+                                            : id / ((int64_t)r->K * r->C);
+    const float* P = r->poses + 12 * es;
+    double ox = r->stereo[0], oy = r->stereo[1], oz = r->stereo[2];
+    v3 o2 = {(double)P[0] * ox + (double)P[1] * oy + (double)P[2] * oz + (double)P[3],
+             (double)P[4] * ox + (double)P[5] * oy + (double)P[6] * oz + (double)P[7],
+             (double)P[8] * ox + (double)P[9] * oy + (double)P[10] * oz + (double)P[11]};
+    v3 p = {o.x + rr->t * d.x, o.y + rr->t * d.y, o.z + rr->t * d.z};
+    v3 v = vsub(o2, p);
+    double L = vnorm(v);
+    double eps = (double)r->stereo_eps;
+    if (!(L > 2.0 * eps)) return 1;
+    v3 u = {v.x / L, v.y / L, v.z / L};
+    int32_t valid = 1;
+    for (int64_t k = 0; k < w->n_tri; ++k) {
+        v3 a = w->v[3 * k], b = w->v[3 * k + 1], c = w->v[3 * k + 2];
+        v3 n = vcross(vsub(b, a), vsub(c, a));
+        double denom = vdot(n, u);
+        if (denom == 0.0) continue;
+        double t = vdot(n, vsub(a, p)) / denom;
+        v3 q = {p.x + t * u.x, p.y + t * u.y, p.z + t * u.z};
+        if (vdot(vcross(vsub(b, a), vsub(q, a)), n) >= 0.0 &&
+            vdot(vcross(vsub(c, b), vsub(q, b)), n) >= 0.0 &&
+            vdot(vcross(vsub(a, c), vsub(q, c)), n) >= 0.0) {
+            if (fabs(t - eps) <= amb_eps || fabs(t - (L - eps)) <= amb_eps) *amb = ORACLE_AMB_SHADOW;
+            if (t > eps && t < L - eps) valid = 0;
+        }
+    }
+    return valid;
+}
+
 /* ---- threading over the (env-sorted) query list ------------------------ */
 typedef struct {
     const oracle_scene* sc;
@@ -244,7 +286,7 @@ typedef struct {
     double eps;
     double* t64; float* dist; int32_t* seg; int32_t* face; int32_t* amb;
     double* t2; double* graze;
-    double* normal; double* bary; double* point;
+    double* normal; double* bary; double* point; int32_t* valid;
     int64_t tests;
     int status;
 } job;
@@ -279,6 +321,11 @@ static void* worker(void* arg) {
             if (jb->point) jb->point[3 * q + k] = rr.point[k];
         }
         if (jb->bary) { jb->bary[2 * q] = rr.bary[0]; jb->bary[2 * q + 1] = rr.bary[1]; }
+        if (jb->valid) {
+            int shadow_amb = 0;
+            jb->valid[q] = stereo_valid(jb->r, id, &w, &rr, o, d, jb->eps, &shadow_amb);
+            jb->amb[q] |= shadow_amb;
+        }
     }
     free(w.v);
     free(w.label);
@@ -307,7 +354,7 @@ int oracle_cast(const oracle_scene* sc, const oracle_rays* r,
                 const int64_t* query, int64_t n_query, double eps,
                 int32_t n_threads, double* t64, float* dist, int32_t* seg,
                 int32_t* face, int32_t* amb, double* t2, double* graze,
-                double* normal, double* bary, double* point) {
+                double* normal, double* bary, double* point, int32_t* valid) {
     if (validate(sc, r) != 0) return -1;
     int64_t n_rays_total;
     if (r->model == ORACLE_RAYS) n_rays_total = (int64_t)sc->n_envs * r->R;
@@ -339,7 +386,7 @@ int oracle_cast(const oracle_scene* sc, const oracle_rays* r,
         jb->eps = eps;
         jb->t64 = t64; jb->dist = dist; jb->seg = seg; jb->face = face;
         jb->amb = amb; jb->t2 = t2; jb->graze = graze;
-        jb->normal = normal; jb->bary = bary; jb->point = point;
+        jb->normal = normal; jb->bary = bary; jb->point = point; jb->valid = valid;
         if (n_threads == 1) worker(jb);
         else if (pthread_create(&th[i], NULL, worker, jb) != 0) { jb->status = -1; th[i] = 0; }
     }

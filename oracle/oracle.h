@@ -70,13 +70,19 @@ typedef struct {
     const float* poses;   /* [n_envs][S][3][4] sensor -> env                 */
     int32_t S;
     float max_range;
+    /* stereo shadow mask: second sensor origin in the sensor
+     * frame and the self-hit guard (metres); used when `valid` is requested */
+    float stereo[3];
+    float stereo_eps;
 } oracle_rays;
 
 /* Ambiguity bits (SURVEY.md §8(c) parity rules). */
 enum {
     ORACLE_AMB_TIE   = 1, /* best and second-best candidate t within amb_eps */
     ORACLE_AMB_RANGE = 2, /* a candidate within amb_eps of max_range         */
-    ORACLE_AMB_ZERO  = 4  /* a candidate within amb_eps of t = 0             */
+    ORACLE_AMB_ZERO  = 4, /* a candidate within amb_eps of t = 0             */
+    ORACLE_AMB_SHADOW = 8 /* a shadow-segment candidate within amb_eps of eps
+                             or of L - eps                                   */
 };
 
 /*
@@ -97,6 +103,10 @@ enum {
  *            face's vertices, from the plane hit point by cross-product
  *            area ratios; -1 on a miss                          [may be NULL]
  *   point[3q..] o + t d (t = the reported distance)             [may be NULL]
+ *   valid[q] stereo shadow mask: 0 if the segment from the hit point p to
+ *            the second sensor o2 = P (stereo) hits a triangle at a distance
+ *            in (eps, |o2 - p| - eps) from p, else 1 (1 on a miss; PINHOLE
+ *            and BEAMS only)                                    [may be NULL]
  * (PAPER.md:218 surface normals; :228 "barycentric coordinates of
  * intersecting rays", "point clouds and surface normals".)
  * n_threads <= 0 uses all online cores.  Returns 0, or -1 on bad input.
@@ -106,7 +116,7 @@ int oracle_cast(const oracle_scene* scene, const oracle_rays* rays,
                 int32_t n_threads,
                 double* t64, float* dist, int32_t* seg, int32_t* face,
                 int32_t* amb, double* t2, double* graze,
-                double* normal, double* bary, double* point);
+                double* normal, double* bary, double* point, int32_t* valid);
 
 /* Number of triangle tests the last oracle_cast call performed (for the
  * cpu_baseline report: ray-triangle tests/s). */

@@ -54,12 +54,14 @@ class agr_pinhole(ctypes.Structure):
 
 class agr_outputs(ctypes.Structure):
     _fields_ = [("dist", ctypes.c_void_p), ("seg", ctypes.c_void_p), ("face", ctypes.c_void_p),
-                ("normal", ctypes.c_void_p), ("bary", ctypes.c_void_p), ("point", ctypes.c_void_p)]
+                ("normal", ctypes.c_void_p), ("bary", ctypes.c_void_p), ("point", ctypes.c_void_p),
+                ("valid", ctypes.c_void_p)]
 
 
 # channel -> (torch dtype name, trailing vector size)
 CHANNELS = {"dist": ("float32", None), "seg": ("int32", None), "face": ("int32", None),
-            "normal": ("float32", 3), "bary": ("float32", 2), "point": ("float32", 3)}
+            "normal": ("float32", 3), "bary": ("float32", 2), "point": ("float32", 3),
+            "valid": ("int32", None)}
 
 
 class agr_scene_info(ctypes.Structure):
@@ -92,6 +94,7 @@ _SIGS = {
     "agr_checksum": (_I32, [_P, agr_outputs, ctypes.c_int64, _P, _P]),
     "agr_set_exact_mode": (_I32, [_P, _I32]),
     "agr_set_traversal": (_I32, [_P, _I32]),
+    "agr_set_stereo": (_I32, [_P, ctypes.c_float, ctypes.c_float, ctypes.c_float, ctypes.c_float]),
     "agr_enable_counters": (_I32, [_P, _I32]),
     "agr_get_counters": (_I32, [_P, _P]),
     "agr_debug_export_blas": (_I32, [_P, _I32, _P, _P, _P, ctypes.POINTER(ctypes.c_int64),
@@ -301,6 +304,10 @@ class Scene:
     # ---- test / profiling hooks --------------------------------------------
     def set_exact_mode(self, exact: bool):
         _check(load().agr_set_exact_mode(self.handle, 1 if exact else 0))
+
+    def set_stereo(self, offset=(0.0, -0.095, 0.0), eps: float = 1e-4):
+        """Second sensor origin (sensor frame) and self-hit guard for `valid`."""
+        _check(load().agr_set_stereo(self.handle, *(float(x) for x in offset), float(eps)))
 
     def set_traversal(self, mode: int):
         """0 auto (warp packets for pinhole / beam tiles), 1 per-lane rays."""

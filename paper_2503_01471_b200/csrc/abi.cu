@@ -88,6 +88,8 @@ struct agr_scene_s {
     unsigned long long* counters = nullptr;
     bool built = false, dirty = false;
     int exact = 0;
+    float stereo[3] = {0.0f, -0.095f, 0.0f};
+    float stereo_eps = 1e-4f;
     int traversal = 0;  // 0 auto (warp packets for pinhole / beams), 1 per-lane
     bool counting = false;
     // end-to-end staging (lazily allocated)
@@ -467,6 +469,9 @@ static CastArgs base_args(agr_scene s, float max_range, agr_outputs out) {
     a.out_normal = out.normal;
     a.out_bary = out.bary;
     a.out_point = out.point;
+    a.out_valid = out.valid;
+    for (int k = 0; k < 3; ++k) a.stereo[k] = s->stereo[k];
+    a.stereo_eps = s->stereo_eps;
     a.env_begin = 0;
     a.env_end = s->n_envs;
     a.S = 1;
@@ -574,8 +579,9 @@ struct E2EChannel {
 
 static agr_status e2e_run(agr_scene s, CastArgs& a, int64_t elems_per_env, agr_outputs out_host) {
     const int E = s->n_envs;
-    E2EChannel ch[6] = {{out_host.dist, 4}, {out_host.seg, 4}, {out_host.face, 4},
-                        {out_host.normal, 12}, {out_host.bary, 8}, {out_host.point, 12}};
+    E2EChannel ch[7] = {{out_host.dist, 4}, {out_host.seg, 4}, {out_host.face, 4},
+                        {out_host.normal, 12}, {out_host.bary, 8}, {out_host.point, 12},
+                        {out_host.valid, 4}};
     int64_t bytes_per_elem = 0;
     bool direct = true;
     for (auto& c : ch)
@@ -609,9 +615,9 @@ static agr_status e2e_run(agr_scene s, CastArgs& a, int64_t elems_per_env, agr_o
         c.env_begin = e0;
         c.env_end = e1;
         c.out_env_base = e0;  // the chunk's outputs start at env e0 of the chunk buffer
-        char* dev[6];
+        char* dev[7];
         char* p = base;
-        for (int q = 0; q < 6; ++q) {
+        for (int q = 0; q < 7; ++q) {
             dev[q] = ch[q].host ? p : nullptr;
             if (ch[q].host) p += ch[q].bytes * n;
         }
@@ -621,6 +627,7 @@ static agr_status e2e_run(agr_scene s, CastArgs& a, int64_t elems_per_env, agr_o
         c.out_normal = (float*)dev[3];
         c.out_bary = (float*)dev[4];
         c.out_point = (float*)dev[5];
+        c.out_valid = (int*)dev[6];
         c.sv = s->view();
         c.exact = s->exact;
         c.packet = s->traversal == 0 ? 1 : 0;
@@ -630,7 +637,7 @@ static agr_status e2e_run(agr_scene s, CastArgs& a, int64_t elems_per_env, agr_o
         CK(cudaStreamWaitEvent(xs, s->e2e_event[slot], 0));
         const int64_t off = (int64_t)e0 * elems_per_env;
         if (direct) {
-            for (int q = 0; q < 6; ++q)
+            for (int q = 0; q < 7; ++q)
                 if (ch[q].host)
                     CK(cudaMemcpyAsync((char*)ch[q].host + off * ch[q].bytes, dev[q], ch[q].bytes * n,
                                        cudaMemcpyDeviceToHost, xs));
@@ -640,7 +647,7 @@ static agr_status e2e_run(agr_scene s, CastArgs& a, int64_t elems_per_env, agr_o
             CK(cudaEventRecord(s->e2e_event[2 + slot], xs));
             CK(cudaEventSynchronize(s->e2e_event[2 + slot]));
             const char* hsrc = (const char*)s->e2e_host[slot];
-            for (int q = 0; q < 6; ++q)
+            for (int q = 0; q < 7; ++q)
                 if (ch[q].host) {
                     memcpy((char*)ch[q].host + off * ch[q].bytes, hsrc, ch[q].bytes * n);
                     hsrc += ch[q].bytes * n;
@@ -666,7 +673,7 @@ agr_status agr_cast_pinhole_host(agr_scene s, const agr_pinhole* cam, agr_distan
     if (st != AGR_OK) return st;
     CK(cudaMemcpyAsync(s->e2e_poses, poses_host, sizeof(float) * 12 * (size_t)n_sensors * s->n_envs,
                        cudaMemcpyHostToDevice, s->e2e_stream[0]));
-    CastArgs a = base_args(s, max_range, agr_outputs{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr});
+    CastArgs a = base_args(s, max_range, agr_outputs{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr});
     a.model = 1;
     a.kind = (int)kind;
     a.W = cam->width;
@@ -703,7 +710,7 @@ agr_status agr_cast_beams_host(agr_scene s, const float* dirs_host, int32_t C, i
     CK(cudaMemcpyAsync(s->e2e_beams, dirs_host, bb, cudaMemcpyHostToDevice, s->e2e_stream[0]));
     CK(cudaMemcpyAsync(s->e2e_poses, poses_host, sizeof(float) * 12 * (size_t)n_sensors * s->n_envs,
                        cudaMemcpyHostToDevice, s->e2e_stream[0]));
-    CastArgs a = base_args(s, max_range, agr_outputs{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr});
+    CastArgs a = base_args(s, max_range, agr_outputs{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr});
     a.model = 2;
     a.W = K;
     a.H = C;
@@ -726,6 +733,18 @@ agr_status agr_set_exact_mode(agr_scene s, int32_t exact) {
     g_err.clear();
     if (!s) return fail(AGR_EINVAL, "scene is NULL");
     s->exact = exact ? 1 : 0;
+    return AGR_OK;
+}
+
+agr_status agr_set_stereo(agr_scene s, float ox, float oy, float oz, float eps) {
+    g_err.clear();
+    if (!s) return fail(AGR_EINVAL, "scene is NULL");
+    if (!std::isfinite(ox) || !std::isfinite(oy) || !std::isfinite(oz) || !(eps > 0.0f) || !std::isfinite(eps))
+        return fail(AGR_EINVAL, "stereo offset must be finite and eps > 0");
+    s->stereo[0] = ox;
+    s->stereo[1] = oy;
+    s->stereo[2] = oz;
+    s->stereo_eps = eps;
     return AGR_OK;
 }
 

@@ -235,6 +235,9 @@ struct CastArgs {
     float* out_normal;    // [..][3]
     float* out_bary;      // [..][2]
     float* out_point;     // [..][3]
+    int* out_valid;       // stereo shadow mask (1 valid, 0 shadowed)
+    float stereo[3];      // second sensor origin in the sensor frame
+    float stereo_eps;     // self-hit guard (metres)
     int env_begin, env_end;  // envs cast by this launch (chunking)
     int out_env_base;        // outputs are indexed from this env (0: global indexing)
     unsigned long long* counters;  // optional [8]

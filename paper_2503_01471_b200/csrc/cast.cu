@@ -91,8 +91,9 @@ __device__ __forceinline__ bool slab(const SlabRay& r, float lx, float hx, float
 // ---- FP64 ray and FP64 world-space triangle test ----------------------------
 struct Ray64 { d3 o, d; };
 
-__device__ __forceinline__ bool test64(const SceneView& sv, int inst, int leaf, const Ray64& r,
-                                       double tmax, double& t) {
+// FP64 Moller-Trumbore on the world-space triangle A v + b (closed,
+// double-sided); returns the ray parameter t of the plane hit.
+__device__ __forceinline__ bool tri64(const SceneView& sv, int inst, int leaf, const Ray64& r, double& t) {
     const float* T = sv.inst_T + 12 * inst;
     const float* v = sv.triv + 9 * leaf;
     double A[12];
@@ -118,7 +119,12 @@ __device__ __forceinline__ bool test64(const SceneView& sv, int inst, int leaf, 
     if (det < 0.0) { det = -det; u = -u; vv = -vv; tn = -tn; }
     if (u < 0.0 || vv < 0.0 || u + vv > det) return false;
     t = tn / det;
-    return t > 0.0 && t <= tmax;
+    return true;
+}
+
+__device__ __forceinline__ bool test64(const SceneView& sv, int inst, int leaf, const Ray64& r,
+                                       double tmax, double& t) {
+    return tri64(sv, inst, leaf, r, t) && t > 0.0 && t <= tmax;
 }
 
 // ---- per-lane candidate list and resolved best ---------------------------------
@@ -197,6 +203,7 @@ struct Cold {
 };
 
 struct RayState {
+    float tmin;       // any-hit (shadow) queries: hits must have t in (tmin, tmax)
     float tmax;
     float U;          // upper bound on the winning t (certain FP32 hits, FP64 hits)
     SlabRay sr;       // box-test state of the current level
@@ -208,6 +215,7 @@ struct RayState {
 
     __device__ __forceinline__ void init(f3 o, f3 d, float tmax_, Cold cold) {
         c = cold;
+        tmin = 0.0f;
         tmax = tmax_;
         U = tmax_;
         // |o|_1 + tmax |d|_1: scale of the FP32 ray's position error
@@ -346,6 +354,47 @@ struct RayState {
         }
     }
 
+    // Any-hit FP32 filter for shadow segments (f2 stereo mask): a hit needs t
+    // in (tmin, tmax).  A certain hit ends the query (U = -1 culls every
+    // box); an uncertain one is decided by the out-of-line FP64 test `res`.
+    template <bool COUNT, class RES>
+    __device__ __forceinline__ void leaf_anyhit(const SceneView& sv, int leaf, const RES& res, Counters& cnt) {
+        if (U < 0.0f) return;
+        const float4* tp = sv.tris + 3 * leaf;
+        float4 a = __ldg(tp), b = __ldg(tp + 1), cc = __ldg(tp + 2);
+        const f3 oo = mk(c.f(C_OOX), c.f(C_OOY), c.f(C_OOZ));
+        const f3 od = mk(c.f(C_ODX), c.f(C_ODY), c.f(C_ODZ));
+        const float delta = c.f(C_DELTA);
+        f3 v0 = mk(a.x, a.y, a.z), e1 = mk(b.x, b.y, b.z), e2 = mk(cc.x, cc.y, cc.z);
+        f3 p = cross(od, e2);
+        float det = dot(e1, p);
+        f3 s = sub(oo, v0);
+        bool keep, certain = false;
+        if (det != 0.0f) {
+            float inv = rcp_approx(det);
+            f3 qv = cross(s, e1);
+            float u = dot(s, p) * inv;
+            float v = dot(od, qv) * inv;
+            float t = dot(e2, qv) * inv;
+            float g = delta * b.w * fabsf(inv);
+            float beta = g * c.f(C_DLEN) * a.w;
+            float terr = fmaf(fabsf(t), T_REL, g);
+            float tl = t - terr, th = t + terr;
+            bool out = u < -beta || v < -beta || u + v > 1.0f + beta || th <= tmin || tl >= tmax;
+            keep = !out;
+            certain = keep && u > beta && v > beta && u + v < 1.0f - beta && tl > tmin && th < tmax;
+        } else {
+            f3 nn = cross(e1, e2);
+            keep = fabsf(dot(s, nn)) <= delta * b.w;
+        }
+        if (certain) {
+            U = -1.0f;
+        } else if (keep) {
+            if (COUNT) cnt.f64++;
+            if (res(cur_inst, leaf)) U = -1.0f;
+        }
+    }
+
     // FP64 arbitration of the surviving candidates (slot loop, warp-uniform).
     template <bool COUNT, class RES>
     __device__ __forceinline__ Best64 arbitrate(const RES& res, Counters& cnt) {
@@ -398,9 +447,11 @@ constexpr unsigned KEY_MISS = 0x7f800000u;  // +inf bits: sorts after every hit 
 // ---- per-lane traversal (explicit rays; exact-mode fallback) -------------------
 // Ordered stackful traversal of the two-level BVH, one independent ray per
 // lane (Aila & Laine style, stack in local memory).
-template <bool EXACT, bool COUNT, class RES>
+// LEAF(leaf) tests BLAS leaf `leaf` of rs.cur_inst; ANYHIT stops a ray once
+// its U < 0 (shadow queries).
+template <bool ANYHIT, bool COUNT, class LEAF>
 __device__ __forceinline__ void traverse_lane(const SceneView& sv, int env, RayState& rs,
-                                              const RES& res, bool& sovf, Counters& cnt) {
+                                              const LEAF& leaf_fn, bool& sovf, Counters& cnt) {
     int stack[STACK_SIZE];
     int sp = 0;
     int node = __ldg(sv.tlas_root + env);
@@ -453,14 +504,9 @@ __device__ __forceinline__ void traverse_lane(const SceneView& sv, int env, RayS
             continue;
         }
         if (COUNT) cnt.leaves++;
-        if (EXACT) {
-            if (COUNT) cnt.f64++;
-            rs.resolve64(leaf, res);
-        } else {
-            rs.leaf_filter<COUNT>(sv, leaf, res, cnt);
-        }
+        leaf_fn(leaf);
         rs.load_slab();
-        if (sp == 0) break;
+        if (sp == 0 || (ANYHIT && rs.U < 0.0f)) break;
         node = stack[--sp];
     }
 }
@@ -474,9 +520,9 @@ __device__ __forceinline__ void traverse_lane(const SceneView& sv, int env, RayS
 // and triangle tests, so results equal the per-lane traversal.
 constexpr int PSTACK = 96;
 
-template <bool COUNT, class RES>
+template <bool ANYHIT, bool COUNT, class LEAF>
 __device__ __forceinline__ void traverse_packet(const SceneView& sv, int env, RayState& rs,
-                                                const RES& res, bool& sovf, int* wstack,
+                                                const LEAF& leaf_fn, bool& sovf, int* wstack,
                                                 Counters& cnt) {
     const unsigned FULL = 0xFFFFFFFFu;
     const bool leader = (threadIdx.x & 31) == 0;
@@ -554,9 +600,9 @@ __device__ __forceinline__ void traverse_packet(const SceneView& sv, int env, Ra
             continue;
         }
         if (COUNT) cnt.leaves++;
-        rs.leaf_filter<COUNT>(sv, leaf, res, cnt);
+        leaf_fn(leaf);
         rs.load_slab();
-        if (sp == 0) break;
+        if (sp == 0 || (ANYHIT && __all_sync(FULL, rs.U < 0.0f))) break;
         __syncwarp();
         node = wstack[--sp];
     }
@@ -649,11 +695,81 @@ __device__ __forceinline__ Ray64 gen_ray64(const CastArgs& a, const RayId& id) {
     return r64;
 }
 
-// Out-of-line FP64 test of (inst, leaf) for the ray `id`: keeps the FP64
-// registers out of the traversal loop's allocation.
+// ---- f2: stereo shadow segments ------------------------------------------------------
+// FP64 segment from the FP64 hit point p = o + t d towards the second
+// sensor's origin o2 = P (stereo offset) (reading R21).
+// Returns its length L (<= 0 when undefined) and the unit direction.
+template <int MODEL>
+__device__ __forceinline__ double shadow_ray64(const CastArgs* a, int env, int sensor, int col, int row,
+                                               double t_hit, Ray64& sr) {
+    RayId id;
+    id.env = env;
+    id.sensor = sensor;
+    id.col = col;
+    id.row = row;
+    id.out = 0;
+    id.active = true;
+    const Ray64 r = gen_ray64<MODEL>(*a, id);
+    const float* P = a->poses + 12 * ((int64_t)env * a->S + sensor);
+    const d3 off = mkd(a->stereo[0], a->stereo[1], a->stereo[2]);
+    const d3 o2 = mkd((double)P[0] * off.x + (double)P[1] * off.y + (double)P[2] * off.z + (double)P[3],
+                      (double)P[4] * off.x + (double)P[5] * off.y + (double)P[6] * off.z + (double)P[7],
+                      (double)P[8] * off.x + (double)P[9] * off.y + (double)P[10] * off.z + (double)P[11]);
+    const d3 p = mkd(r.o.x + t_hit * r.d.x, r.o.y + t_hit * r.d.y, r.o.z + t_hit * r.d.z);
+    const d3 v = subd(o2, p);
+    const double L = sqrt(dotd(v, v));
+    sr.o = p;
+    sr.d = L > 0.0 ? mkd(v.x / L, v.y / L, v.z / L) : mkd(1.0, 0.0, 0.0);
+    return L;
+}
+
+template <int MODEL>
+__device__ __noinline__ float shadow_segment(const CastArgs* a, int env, int sensor, int col, int row,
+                                             double t_hit, float3* o32, float3* d32) {
+    Ray64 sr;
+    const double L = shadow_ray64<MODEL>(a, env, sensor, col, row, t_hit, sr);
+    *o32 = make_float3((float)sr.o.x, (float)sr.o.y, (float)sr.o.z);
+    *d32 = make_float3((float)sr.d.x, (float)sr.d.y, (float)sr.d.z);
+    return (float)L;
+}
+
+// FP64 decision for an uncertain shadow candidate: hit with t in (eps, L - eps).
 template <int MODEL>
 __device__ __forceinline__ RayId ray_id(const CastArgs& a);
 
+template <int MODEL>
+__device__ __noinline__ bool shadow_test64(const CastArgs* a, double t_hit, int inst, int leaf) {
+    RayId id = ray_id<MODEL>(*a);
+    id.col = min(id.col, a->W - 1);
+    id.row = min(id.row, a->H - 1);
+    Ray64 sr;
+    const double L = shadow_ray64<MODEL>(a, id.env, id.sensor, id.col, id.row, t_hit, sr);
+    double t;
+    const double eps = (double)a->stereo_eps;
+    return tri64(a->sv, inst, leaf, sr, t) && t > eps && t < L - eps;
+}
+
+// Stack-overflow fallback of the shadow query: every triangle of the env.
+template <int MODEL>
+__device__ __noinline__ bool shadow_brute64(const CastArgs* a, int env, double t_hit) {
+    RayId id = ray_id<MODEL>(*a);
+    id.col = min(id.col, a->W - 1);
+    id.row = min(id.row, a->H - 1);
+    Ray64 sr;
+    const double L = shadow_ray64<MODEL>(a, env, id.sensor, id.col, id.row, t_hit, sr);
+    const double eps = (double)a->stereo_eps;
+    for (int inst = __ldg(a->sv.env_off + env); inst < __ldg(a->sv.env_off + env + 1); ++inst) {
+        const AssetInfo& as = a->sv.assets[__ldg(a->sv.inst_asset + inst)];
+        for (int l = 0; l < as.n_leaves; ++l) {
+            double t;
+            if (tri64(a->sv, inst, as.leaf_base + l, sr, t) && t > eps && t < L - eps) return true;
+        }
+    }
+    return false;
+}
+
+// Out-of-line FP64 test of (inst, leaf) for the ray `id`: keeps the FP64
+// registers out of the traversal loop's allocation.
 template <int MODEL>
 __device__ __noinline__ void resolve_leaf64(const CastArgs* a, int inst, int leaf, Best64* best) {
     RayId id = ray_id<MODEL>(*a);
@@ -745,7 +861,7 @@ __device__ __forceinline__ RayId ray_id(const CastArgs& a) {
 }
 
 // TRAV: 0 per-lane FP32 filter, 1 warp packet (pinhole / beams), 2 exact (FP64 leaves)
-template <int MODEL, int TRAV, bool COUNT>
+template <int MODEL, int TRAV, bool COUNT, bool STEREO>
 __global__ void __launch_bounds__(CAST_THREADS, CAST_MIN_BLOCKS) k_cast(const __grid_constant__ CastArgs a) {
     __shared__ int s_stack[TRAV == 1 ? CAST_THREADS / 32 : 1][TRAV == 1 ? PSTACK : 1];
     __shared__ float s_cold[N_COLD][CAST_THREADS];
@@ -773,14 +889,19 @@ __global__ void __launch_bounds__(CAST_THREADS, CAST_MIN_BLOCKS) k_cast(const __
         auto res = [ap](int inst, int leaf, Best64& b) { resolve_leaf64<MODEL>(ap, inst, leaf, &b); };
         bool sovf = false;
         if (TRAV == 2) {
-            traverse_lane<true, COUNT>(a.sv, id.env, rs, res, sovf, cnt);
+            auto leaf_fn = [&](int leaf) {
+                if (COUNT) cnt.f64++;
+                rs.resolve64(leaf, res);
+            };
+            traverse_lane<false, COUNT>(a.sv, id.env, rs, leaf_fn, sovf, cnt);
             best = cold.best();
         } else {
+            auto leaf_fn = [&](int leaf) { rs.leaf_filter<COUNT>(a.sv, leaf, res, cnt); };
             if (TRAV == 1) {
                 // whole warps share (env, sensor): pinhole / beams tiles
-                traverse_packet<COUNT>(a.sv, id.env, rs, res, sovf, s_stack[threadIdx.x >> 5], cnt);
+                traverse_packet<false, COUNT>(a.sv, id.env, rs, leaf_fn, sovf, s_stack[threadIdx.x >> 5], cnt);
             } else {
-                traverse_lane<false, COUNT>(a.sv, id.env, rs, res, sovf, cnt);
+                traverse_lane<false, COUNT>(a.sv, id.env, rs, leaf_fn, sovf, cnt);
             }
             best = rs.arbitrate<COUNT>(res, cnt);
         }
@@ -789,6 +910,36 @@ __global__ void __launch_bounds__(CAST_THREADS, CAST_MIN_BLOCKS) k_cast(const __
             best.face = -1;
             brute64(a.sv, id.env, gen_ray64<MODEL>(a, id), (double)a.max_range, &best);
         }
+    }
+    // f2: stereo shadow mask -- an any-hit segment from the hit
+    // point to the second sensor; every lane of the warp takes part.
+    bool valid = true;
+    if (STEREO && MODEL != 0 && id.env < a.env_end) {
+        // recomputed (not kept live across the primary traversal)
+        id = ray_id<MODEL>(a);
+        id.col = min(id.col, a.W - 1);
+        id.row = min(id.row, a.H - 1);
+        float3 sp32, sd32;
+        float seg_max = -1.0f;
+        if (trace && best.face >= 0) seg_max = shadow_segment<MODEL>(&a, id.env, id.sensor, id.col, id.row, best.t, &sp32, &sd32);
+        if (!(seg_max > a.stereo_eps)) { sp32 = make_float3(0.f, 0.f, 0.f); sd32 = make_float3(1.f, 0.f, 0.f); }
+        Cold cold;
+        cold.p = &s_cold[0][threadIdx.x];
+        cold.bt = &s_best_t[threadIdx.x];
+        RayState ss;
+        ss.init(mk(sp32.x, sp32.y, sp32.z), mk(sd32.x, sd32.y, sd32.z), fmaxf(seg_max - a.stereo_eps, 0.0f), cold);
+        ss.tmin = a.stereo_eps;
+        const bool tested = seg_max > 2.0f * a.stereo_eps;
+        if (!tested) ss.U = -1.0f;  // nothing to test: valid
+        const CastArgs* ap = &a;
+        const Best64 prim = best;
+        auto sres = [ap, prim](int inst, int leaf) { return shadow_test64<MODEL>(ap, prim.t, inst, leaf); };
+        auto leaf_fn = [&](int leaf) { ss.leaf_anyhit<COUNT>(a.sv, leaf, sres, cnt); };
+        bool sovf2 = false;
+        if (TRAV == 1) traverse_packet<true, COUNT>(a.sv, id.env, ss, leaf_fn, sovf2, s_stack[threadIdx.x >> 5], cnt);
+        else traverse_lane<true, COUNT>(a.sv, id.env, ss, leaf_fn, sovf2, cnt);
+        valid = !tested || ss.U >= 0.0f;
+        if (sovf2 && tested) valid = !shadow_brute64<MODEL>(&a, id.env, best.t);
     }
     if (COUNT) {
         unsigned v[6] = {cnt.nodes, cnt.leaves, cnt.insts, cnt.f64, cnt.overflow, cnt.tnodes};
@@ -810,6 +961,7 @@ __global__ void __launch_bounds__(CAST_THREADS, CAST_MIN_BLOCKS) k_cast(const __
     if (a.out_seg) __stcs(a.out_seg + id.out, hit ? __ldg(a.sv.inst_label + best.inst) : -1);
     if (a.out_face) __stcs(a.out_face + id.out, hit ? best.face : -1);
     if (a.out_normal || a.out_bary || a.out_point) write_extra<MODEL>(&a, id, best);
+    if (a.out_valid) __stcs(a.out_valid + id.out, valid ? 1 : 0);  // 1 without STEREO (explicit rays)
 }
 
 template <int MODEL>
@@ -827,15 +979,30 @@ cudaError_t launch_model(const CastArgs& a, cudaStream_t stream) {
     if (blocks > 0x7FFFFFFF) return cudaErrorInvalidValue;
     const int trav = a.exact ? 2 : (MODEL != 0 && a.packet ? 1 : 0);
     const unsigned g = (unsigned)blocks;
+    const bool stereo = MODEL != 0 && a.out_valid != nullptr;
+#define AGR_LAUNCH(T, C, S) k_cast<MODEL, T, C, S><<<g, CAST_THREADS, 0, stream>>>(a)
     if (a.counters) {
-        if (trav == 2) k_cast<MODEL, 2, true><<<g, CAST_THREADS, 0, stream>>>(a);
-        else if (trav == 1) k_cast<MODEL, 1, true><<<g, CAST_THREADS, 0, stream>>>(a);
-        else k_cast<MODEL, 0, true><<<g, CAST_THREADS, 0, stream>>>(a);
+        if (stereo) {
+            if (trav == 2) AGR_LAUNCH(2, true, true);
+            else if (trav == 1) AGR_LAUNCH(1, true, true);
+            else AGR_LAUNCH(0, true, true);
+        } else {
+            if (trav == 2) AGR_LAUNCH(2, true, false);
+            else if (trav == 1) AGR_LAUNCH(1, true, false);
+            else AGR_LAUNCH(0, true, false);
+        }
     } else {
-        if (trav == 2) k_cast<MODEL, 2, false><<<g, CAST_THREADS, 0, stream>>>(a);
-        else if (trav == 1) k_cast<MODEL, 1, false><<<g, CAST_THREADS, 0, stream>>>(a);
-        else k_cast<MODEL, 0, false><<<g, CAST_THREADS, 0, stream>>>(a);
+        if (stereo) {
+            if (trav == 2) AGR_LAUNCH(2, false, true);
+            else if (trav == 1) AGR_LAUNCH(1, false, true);
+            else AGR_LAUNCH(0, false, true);
+        } else {
+            if (trav == 2) AGR_LAUNCH(2, false, false);
+            else if (trav == 1) AGR_LAUNCH(1, false, false);
+            else AGR_LAUNCH(0, false, false);
+        }
     }
+#undef AGR_LAUNCH
     return cudaGetLastError();
 }
 

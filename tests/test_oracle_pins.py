@@ -592,3 +592,51 @@ def test_sphere_normals_face_the_origin():
     # direction of each ray = point / |point| (camera at the origin)
     dirs = r.point / np.linalg.norm(r.point, axis=1, keepdims=True)
     assert np.all(np.einsum("ij,ij->i", r.normal, dirs) < 0)
+
+
+# --------------------------------------------------------------------------
+# stereo shadow mask
+# --------------------------------------------------------------------------
+
+def _post_and_wall(wall_x=6.0, post_x=3.0, half_w=0.1):
+    wall = quad_mesh(200.0)
+    post = sg.box_mesh("post", (-0.01, -half_w, -5.0), (0.01, half_w, 5.0))
+    return sg.assemble([wall, post], [[(0, 1, sg.make_T(np.eye(3), (wall_x, 0, 0))),
+                                       (1, 2, sg.make_T(np.eye(3), (post_x, 0, 0)))]])
+
+
+def test_stereo_wall_only_all_valid_and_zero_baseline():
+    """One wall and nothing else: every pixel valid; with baseline 0
+    every hit pixel is valid."""
+    cam = sg.pinhole(32, 8, 70.0)
+    sc = sg.assemble([quad_mesh(200.0)], [[(0, 1, sg.make_T(np.eye(3), (4.0, 0, 0)))]])
+    r = cast_pinhole(sc, cam, sg.identity_poses(1), stereo=((0.0, -0.2, 0.0), 1e-4))
+    assert np.all(r.valid == 1)
+    sc2 = _post_and_wall()
+    r = cast_pinhole(sc2, cam, sg.identity_poses(1), stereo=((0.0, 0.0, 0.0), 1e-4))
+    assert np.all(r.valid == 1)
+
+
+@pytest.mark.parametrize("baseline", [0.1, 0.3])
+def test_stereo_post_shadow_band_closed_form(baseline):
+    """Thin post (half-width h at x = P) before a wall (x = W), right camera
+    at (0, -b, 0): a wall point at height y is hidden from it iff the
+    segment to the camera crosses the post, i.e. |y P/W - b (1 - P/W)| <= h
+    (S:546 'band width grows with baseline')."""
+    W_, P_, h = 6.0, 3.0, 0.1
+    cam = sg.pinhole(400, 4, 60.0)
+    sc = _post_and_wall(W_, P_, h)
+    r = cast_pinhole(sc, cam, sg.identity_poses(1), max_range=20.0,
+                     stereo=((0.0, -baseline, 0.0), 1e-4), extras=True)
+    row = np.arange(400) + (1 * 400)  # v = 1
+    on_wall = r.seg[row] == 1
+    y = r.point[row, 1]
+    yp = y * P_ / W_ - baseline * (1 - P_ / W_)
+    shadow = np.abs(yp) <= h
+    far = np.abs(np.abs(yp) - h) > 2e-3  # away from the band's edges
+    sel = on_wall & far
+    assert sel.sum() > 200
+    assert np.array_equal(r.valid[row][sel] == 0, shadow[sel])
+    assert (shadow & on_wall).sum() >= 3
+    # the post itself is seen by both cameras: valid
+    assert np.all(r.valid[row][r.seg[row] == 2] == 1)

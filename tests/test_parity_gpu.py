@@ -345,3 +345,44 @@ def test_extras_host_path():
     out = s.cast_pinhole_host(sensor["cam"], poses, sensor["max_range"], agr.AGR_RANGE, channels=ALL)
     for k in a:
         assert np.array_equal(a[k], out[k].numpy().reshape(-1)), k
+
+
+# ---- f2: stereo shadow mask --------------------------------------------------------
+
+def _valid_compare(ref, got, what):
+    amb = ref.amb != 0
+    bad = np.nonzero((got["valid"] != ref.valid) & ~amb)[0]
+    assert len(bad) == 0, f"{what}: {len(bad)} valid mismatches, first {bad[:5]}"
+    return int((ref.valid == 0).sum())
+
+
+@pytest.mark.parametrize("baseline", [0.095, 0.5])
+def test_stereo_mask_c2(baseline):
+    """Stereo shadow mask vs the oracle on c2 envs."""
+    sc, sensor = sg.config2(n_envs=12)
+    s = make_scene(sc)
+    s.set_stereo((0.0, -baseline, 0.0), 1e-4)
+    got = to_np(cast_sensor(s, sensor, "depth", channels=("dist", "seg", "face", "valid")))
+    ref = oracle.cast(sc, oracle_rays(sensor, "depth"), stereo=((0.0, -baseline, 0.0), 1e-4))
+    compare(ref, got["dist"], got["seg"], got["face"], "stereo")
+    n_shadow = _valid_compare(ref, got, f"stereo b={baseline}")
+    assert n_shadow > 100
+    # the mask does not change the other channels
+    core = to_np(cast_sensor(s, sensor, "depth"))
+    for k in core:
+        assert np.array_equal(core[k], got[k]), k
+
+
+def test_stereo_mask_lidar_and_lane_mode():
+    sc, sensor = sg.config4(n_envs=4)
+    sensor = dict(sensor, beams=sg.lidar_beams(16, 64))
+    s = make_scene(sc)
+    s.set_stereo((0.0, 0.0, 0.3), 1e-4)
+    chans = ("dist", "seg", "face", "valid")
+    got = to_np(cast_sensor(s, sensor, "range", channels=chans))
+    ref = oracle.cast(sc, oracle_rays(sensor, "range"), stereo=((0.0, 0.0, 0.3), 1e-4))
+    _valid_compare(ref, got, "lidar stereo")
+    s.set_traversal(1)
+    lane = to_np(cast_sensor(s, sensor, "range", channels=chans))
+    for k in got:
+        assert np.array_equal(got[k], lane[k]), k
