@@ -57,9 +57,8 @@ __device__ __forceinline__ float rcp_approx(float x) {
 }
 
 __device__ __forceinline__ float safe_inv(float d) {
-    float ad = fabsf(d);
-    float dd = ad < 1e-20f ? copysignf(1e-20f, d) : d;
-    return rcp_approx(dd);
+    // d + copysign(1e-30, d) == d unless |d| < ~1e-22: never a zero divisor
+    return rcp_approx(d + copysignf(1e-30f, d));
 }
 
 __device__ __forceinline__ SlabRay make_slab(f3 o, f3 d, float delta) {
@@ -538,13 +537,10 @@ __device__ __forceinline__ void traverse_packet(const SceneView& sv, int env, Ra
             float tn[4];
             bool h[4];
             rs.node4_test(f, tn, h);
-            unsigned m[4];
-            int nh = 0, only = 0;
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                m[k] = __ballot_sync(FULL, h[k]);
-                if (m[k]) { ++nh; only = k; }
-            }
+            // 4-bit mask of the children some lane hits
+            const unsigned cm = (__ballot_sync(FULL, h[0]) ? 1u : 0u) | (__ballot_sync(FULL, h[1]) ? 2u : 0u) |
+                                (__ballot_sync(FULL, h[2]) ? 4u : 0u) | (__ballot_sync(FULL, h[3]) ? 8u : 0u);
+            const int nh = __popc(cm);
             if (nh == 0) {
                 if (sp == 0) break;
                 __syncwarp();
@@ -552,17 +548,18 @@ __device__ __forceinline__ void traverse_packet(const SceneView& sv, int env, Ra
                 continue;
             }
             if (nh == 1) {
-                node = ref[0];
-#pragma unroll
-                for (int k = 1; k < 4; ++k)
-                    if (only == k) node = ref[k];
+                const int only = __ffs(cm) - 1;
+                node = only == 0 ? ref[0] : only == 1 ? ref[1] : only == 2 ? ref[2] : ref[3];
                 continue;
             }
-            // order the children by the nearest entry over the lanes that hit them
+            // order the children by the entry distance of the tile's centre
+            // ray (lane 11: column 3, row 1), misses last
             unsigned key[4];
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
-                key[k] = m[k] ? __reduce_min_sync(FULL, h[k] ? __float_as_uint(tn[k]) : KEY_MISS) : KEY_MISS;
+            for (int k = 0; k < 4; ++k) {
+                const unsigned kc = __shfl_sync(FULL, __float_as_uint(tn[k]), 11);
+                key[k] = (cm >> k) & 1u ? kc : KEY_MISS;
+            }
             sort4(key, ref);
             // push the farther children, farthest first
             if (sp + 3 <= PSTACK) {
