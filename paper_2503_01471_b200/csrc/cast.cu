@@ -174,7 +174,6 @@ __device__ __noinline__ void brute64(SceneView sv, int env, Ray64 r64, double tm
 enum ColdField {
     C_OX, C_OY, C_OZ, C_DX, C_DY, C_DZ, C_Q,
     C_OOX, C_OOY, C_OOZ, C_ODX, C_ODY, C_ODZ, C_DELTA, C_DLEN,
-    C_SR0, C_ESR0 = C_SR0 + 9, C_ESR_END = C_ESR0 + 9,
     C_TL0, C_INST0 = C_TL0 + NSLOT, C_LEAF0 = C_INST0 + NSLOT,
     C_FACE = C_LEAF0 + NSLOT, C_BINST, C_BLEAF, N_COLD
 };
@@ -224,7 +223,6 @@ struct RayState {
         c.f(C_Q) = q;
         // env level: the origin is an exact input, the direction carries rounding
         sr = make_slab(o, d, K_ERR * q);
-        save_slab(C_ESR0);
         cur_inst = -1;
 #pragma unroll
         for (int k = 0; k < NSLOT; ++k) { c.f(C_TL0 + k) = inf_f(); c.i(C_INST0 + k) = -1; c.i(C_LEAF0 + k) = -1; }
@@ -237,7 +235,7 @@ struct RayState {
     }
 
     __device__ __forceinline__ void exit_instance() {
-        load_slab(C_ESR0);  // the env-level box-test state saved by init()
+        sr = make_slab(this->o(), this->d(), K_ERR * c.f(C_Q));  // env-level box-test state
         cur_inst = -1;
     }
 
@@ -262,25 +260,19 @@ struct RayState {
         const float dd = dot(od, od);
         c.f(C_DLEN) = dd > 0.0f ? dd * rsqrtf(dd) * 1.000001f : 0.0f;
         sr = make_slab(oo, od, delta);
-        save_slab(C_SR0);
         cur_inst = inst;
         return __float_as_int(r3.x);
     }
 
     // The box-test state is parked in shared memory while a triangle is
     // tested and reloaded afterwards, so it holds no registers there.
-    __device__ __forceinline__ void save_slab(int at) const {
-        c.f(at + 0) = sr.idx; c.f(at + 1) = sr.idy; c.f(at + 2) = sr.idz;
-        c.f(at + 3) = sr.lox; c.f(at + 4) = sr.loy; c.f(at + 5) = sr.loz;
-        c.f(at + 6) = sr.hix; c.f(at + 7) = sr.hiy; c.f(at + 8) = sr.hiz;
-    }
-    __device__ __forceinline__ void load_slab(int at = C_SR0) {
-        sr.idx = c.f(at + 0); sr.idy = c.f(at + 1); sr.idz = c.f(at + 2);
-        sr.lox = c.f(at + 3); sr.loy = c.f(at + 4); sr.loz = c.f(at + 5);
-        sr.hix = c.f(at + 6); sr.hiy = c.f(at + 7); sr.hiz = c.f(at + 8);
+    // The box-test state is not kept live across a triangle test (register
+    // pressure): it is rebuilt from the object-space ray in shared memory.
+    __device__ __forceinline__ void load_slab() {
+        sr = make_slab(mk(c.f(C_OOX), c.f(C_OOY), c.f(C_OOZ)), mk(c.f(C_ODX), c.f(C_ODY), c.f(C_ODZ)),
+                       c.f(C_DELTA));
     }
 
-    // Slab tests of the 4 children of a BVH4 node (boxes stored per axis).
     __device__ __forceinline__ void node4_test(const float4* f, float tn[4], bool h[4]) const {
         h[0] = slab(sr, f[0].x, f[1].x, f[2].x, f[3].x, f[4].x, f[5].x, U, tn[0]);
         h[1] = slab(sr, f[0].y, f[1].y, f[2].y, f[3].y, f[4].y, f[5].y, U, tn[1]);
