@@ -172,7 +172,10 @@ agr_status agr_scene_get_info(agr_scene scene, agr_scene_info* info);
  */
 agr_status agr_set_instance_transforms(agr_scene scene, const float* T, void* stream);
 
-/* Full per-env TLAS rebuild (Morton order, Karras hierarchy, fit). Async. */
+/* Full per-env TLAS rebuild (one CTA per env: LBVH -- Morton order + Karras
+ * hierarchy -- or, after agr_set_tlas_builder(scene, 1), a binned-SAH
+ * top-down split of the instance boxes), bottom-up fit and 4-wide collapse.
+ * Async. */
 agr_status agr_build(agr_scene scene, void* stream);
 
 /* In-place TLAS refit: keeps the topology of the last agr_build and
@@ -247,6 +250,12 @@ agr_status agr_set_stereo(agr_scene scene, float ox, float oy, float oz, float e
  * 1 = exact mode, every leaf test in FP64 (slow; results must be identical).
  */
 agr_status agr_set_exact_mode(agr_scene scene, int32_t exact);
+
+/* TLAS builder used by the next agr_build: 0 = LBVH (default), 1 = binned
+ * SAH.  Results are identical either way; only the speed differs (on the c3
+ * forest the SAH TLAS saves 4 % of the TLAS node visits but its build costs
+ * ~1 ms per 1024 envs, so LBVH is the default). */
+agr_status agr_set_tlas_builder(agr_scene scene, int32_t builder);
 
 /*
  * Traversal schedule (results are identical either way): 0 = auto (default;

@@ -94,6 +94,7 @@ _SIGS = {
     "agr_checksum": (_I32, [_P, agr_outputs, ctypes.c_int64, _P, _P]),
     "agr_set_exact_mode": (_I32, [_P, _I32]),
     "agr_set_traversal": (_I32, [_P, _I32]),
+    "agr_set_tlas_builder": (_I32, [_P, _I32]),
     "agr_set_stereo": (_I32, [_P, ctypes.c_float, ctypes.c_float, ctypes.c_float, ctypes.c_float]),
     "agr_enable_counters": (_I32, [_P, _I32]),
     "agr_get_counters": (_I32, [_P, _P]),
@@ -308,6 +309,10 @@ class Scene:
     def set_stereo(self, offset=(0.0, -0.095, 0.0), eps: float = 1e-4):
         """Second sensor origin (sensor frame) and self-hit guard for `valid`."""
         _check(load().agr_set_stereo(self.handle, *(float(x) for x in offset), float(eps)))
+
+    def set_tlas_builder(self, builder: int):
+        """1 binned SAH (default), 0 LBVH (Morton + Karras) for agr_build."""
+        _check(load().agr_set_tlas_builder(self.handle, int(builder)))
 
     def set_traversal(self, mode: int):
         """0 auto (warp packets for pinhole / beam tiles), 1 per-lane rays."""

@@ -91,6 +91,7 @@ struct agr_scene_s {
     float stereo[3] = {0.0f, -0.095f, 0.0f};
     float stereo_eps = 1e-4f;
     int traversal = 0;  // 0 auto (warp packets for pinhole / beams), 1 per-lane
+    int tlas_builder = 0;  // 0 LBVH (default), 1 binned SAH
     bool counting = false;
     // end-to-end staging (lazily allocated)
     cudaStream_t e2e_stream[2] = {nullptr, nullptr};
@@ -149,6 +150,7 @@ struct agr_scene_s {
         a.tlas_depth = tlas_depth;
         a.n_envs = n_envs;
         a.max_n = max_n;
+        a.builder = tlas_builder;
         return a;
     }
 
@@ -745,6 +747,14 @@ agr_status agr_set_stereo(agr_scene s, float ox, float oy, float oz, float eps) 
     s->stereo[1] = oy;
     s->stereo[2] = oz;
     s->stereo_eps = eps;
+    return AGR_OK;
+}
+
+agr_status agr_set_tlas_builder(agr_scene s, int32_t builder) {
+    g_err.clear();
+    if (!s) return fail(AGR_EINVAL, "scene is NULL");
+    if (builder != 0 && builder != 1) return fail(AGR_EINVAL, "TLAS builder must be 0 (LBVH) or 1 (SAH)");
+    s->tlas_builder = builder;
     return AGR_OK;
 }
 

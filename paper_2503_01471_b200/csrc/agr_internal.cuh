@@ -210,6 +210,7 @@ struct TlasArgs {
     int* tlas_depth;          // [n_envs] depth of each env's TLAS (written by build)
     int n_envs;
     int max_n;                // max instances in one env (sizes shared memory)
+    int builder;              // 0: LBVH (Morton + Karras), 1: binned SAH (default)
 };
 cudaError_t instances_update(const TlasArgs& a, int n_inst, cudaStream_t stream);
 cudaError_t tlas_build(const TlasArgs& a, bool rebuild, cudaStream_t stream);

@@ -83,6 +83,7 @@ __global__ void k_instances(TlasArgs a, int n_inst) {
 
 // ---- K7/K8: per-env TLAS build / refit -----------------------------------------
 struct TlasSmem {
+    int* task;       // [4 (n-1)] SAH build tasks (start, end, ready, -) by node id
     float* box;      // [n][6] instance boxes (local index)
     float* ibox;     // [n-1][6] internal boxes
     uint64_t* keys;  // [P] Morton<<32 | local index
@@ -95,6 +96,179 @@ struct TlasSmem {
 __device__ __forceinline__ int kdelta64(const uint64_t* k, int n, int i, int j) {
     if (j < 0 || j >= n) return -1;
     return __clzll(k[i] ^ k[j]);  // keys are distinct (local index in the low bits)
+}
+
+// ---- K7 (default): binned-SAH top-down build of one env's TLAS in one CTA --------
+// Each internal node is one task; warps claim tasks in node-id order from a
+// shared-memory queue (a child's id is always larger than its parent's, so a
+// waiting warp always waits on a warp that is running).  A task bins the
+// centroids of its items into 16 bins per axis, takes the split with the
+// lowest SAH cost A_L N_L + A_R N_R, and partitions the items stably.  The
+// result is the same binary form as the Karras build (child refs + parents),
+// so the fit, the BVH4 collapse and the refit are shared.
+constexpr int SAH_BINS = 16;
+
+__device__ void sah_build_cta(const TlasSmem& s, int n) {
+    __shared__ int q_head, next_node;
+    __shared__ float bins[TLAS_THREADS / 32][3 * SAH_BINS][7];  // count + box per (axis, bin)
+    int* perm = (int*)s.keys;          // [n] item order
+    int* tmp = perm + n;               // [n] partition scratch
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const unsigned FULL = 0xFFFFFFFFu;
+    for (int i = tid; i < n; i += blockDim.x) perm[i] = i;
+    for (int j = tid; j < n - 1; j += blockDim.x) s.task[4 * j + 2] = 0;
+    __syncthreads();
+    if (tid == 0) {
+        q_head = 0;
+        next_node = 1;
+        s.task[0] = 0;
+        s.task[1] = n;
+        __threadfence_block();
+        ((volatile int*)s.task)[2] = 1;
+        s.nparent[0] = -1;
+    }
+    __syncthreads();
+    volatile int* vtask = s.task;
+    for (;;) {
+        int k = 0;
+        if (lane == 0) k = atomicAdd(&q_head, 1);
+        k = __shfl_sync(FULL, k, 0);
+        if (k >= n - 1) break;
+        if (lane == 0)
+            while (vtask[4 * k + 2] == 0) { }
+        __syncwarp();
+        __threadfence_block();
+        const int start = vtask[4 * k], end = vtask[4 * k + 1];
+        const int m = end - start;
+        // centroid bounds of the task's items
+        float clo[3] = {FLT_MAX, FLT_MAX, FLT_MAX}, chi[3] = {-FLT_MAX, -FLT_MAX, -FLT_MAX};
+        for (int i = start + lane; i < end; i += 32) {
+            const float* b = s.box + 6 * perm[i];
+            for (int c = 0; c < 3; ++c) {
+                float x = 0.5f * b[c] + 0.5f * b[3 + c];
+                if (isfinite(x)) { clo[c] = fminf(clo[c], x); chi[c] = fmaxf(chi[c], x); }
+            }
+        }
+        for (int o = 16; o > 0; o >>= 1)
+            for (int c = 0; c < 3; ++c) {
+                clo[c] = fminf(clo[c], __shfl_xor_sync(FULL, clo[c], o));
+                chi[c] = fmaxf(chi[c], __shfl_xor_sync(FULL, chi[c], o));
+            }
+        auto bin_of = [&](int item, int axis) {
+            const float* b = s.box + 6 * item;
+            const float x = 0.5f * b[axis] + 0.5f * b[3 + axis];
+            const float ext = chi[axis] - clo[axis];
+            if (!isfinite(x)) return SAH_BINS - 1;
+            if (!(ext > 0.0f)) return 0;
+            int bi = (int)((x - clo[axis]) / ext * (float)SAH_BINS);
+            return bi < 0 ? 0 : (bi >= SAH_BINS ? SAH_BINS - 1 : bi);
+        };
+        // per (axis, bin) count and box: lane owns pairs lane, lane + 32
+        for (int pp = lane; pp < 3 * SAH_BINS; pp += 32) {
+            const int axis = pp / SAH_BINS, bi = pp % SAH_BINS;
+            float cnt = 0.0f, bl[3] = {FLT_MAX, FLT_MAX, FLT_MAX}, bh[3] = {-FLT_MAX, -FLT_MAX, -FLT_MAX};
+            for (int i = start; i < end; ++i) {
+                const int it = perm[i];
+                if (bin_of(it, axis) != bi) continue;
+                const float* b = s.box + 6 * it;
+                cnt += 1.0f;
+                for (int c = 0; c < 3; ++c) { bl[c] = fminf(bl[c], b[c]); bh[c] = fmaxf(bh[c], b[3 + c]); }
+            }
+            bins[w][pp][0] = cnt;
+            for (int c = 0; c < 3; ++c) { bins[w][pp][1 + c] = bl[c]; bins[w][pp][4 + c] = bh[c]; }
+        }
+        __syncwarp();
+        // SAH sweep per axis (lanes 0..2): split after bin p, p = 0..SAH_BINS-2
+        float best_cost = INFINITY;
+        int best_split = -1;
+        if (lane < 3) {
+            const int axis = lane;
+            float rcnt[SAH_BINS], rarea[SAH_BINS];
+            float l[3] = {FLT_MAX, FLT_MAX, FLT_MAX}, h[3] = {-FLT_MAX, -FLT_MAX, -FLT_MAX}, c = 0.0f;
+            for (int bi = SAH_BINS - 1; bi >= 1; --bi) {
+                const float* bb = bins[w][axis * SAH_BINS + bi];
+                c += bb[0];
+                for (int q = 0; q < 3; ++q) { l[q] = fminf(l[q], bb[1 + q]); h[q] = fmaxf(h[q], bb[4 + q]); }
+                const float bx[6] = {l[0], l[1], l[2], h[0], h[1], h[2]};
+                rcnt[bi] = c;
+                rarea[bi] = c > 0.0f ? half_area(bx) : 0.0f;
+            }
+            for (int q = 0; q < 3; ++q) { l[q] = FLT_MAX; h[q] = -FLT_MAX; }
+            c = 0.0f;
+            for (int bi = 0; bi < SAH_BINS - 1; ++bi) {
+                const float* bb = bins[w][axis * SAH_BINS + bi];
+                c += bb[0];
+                for (int q = 0; q < 3; ++q) { l[q] = fminf(l[q], bb[1 + q]); h[q] = fmaxf(h[q], bb[4 + q]); }
+                if (c <= 0.0f || rcnt[bi + 1] <= 0.0f) continue;
+                const float bx[6] = {l[0], l[1], l[2], h[0], h[1], h[2]};
+                const float cost = half_area(bx) * c + rarea[bi + 1] * rcnt[bi + 1];
+                if (cost < best_cost) { best_cost = cost; best_split = axis * SAH_BINS + bi; }
+            }
+        }
+        for (int o = 1; o < 4; o <<= 1) {
+            const float oc = __shfl_xor_sync(FULL, best_cost, o);
+            const int os = __shfl_xor_sync(FULL, best_split, o);
+            if (oc < best_cost || (oc == best_cost && os >= 0 && (best_split < 0 || os < best_split))) {
+                best_cost = oc;
+                best_split = os;
+            }
+        }
+        best_split = __shfl_sync(FULL, best_split, 0);
+        // stable partition of perm[start, end) into tmp
+        int mid;
+        if (best_split >= 0) {
+            const int axis = best_split / SAH_BINS, sb = best_split % SAH_BINS;
+            int nl = 0, nr = 0;
+            // left side first, then the right side, both in the current order
+            for (int base = start; base < end; base += 32) {
+                const int i = base + lane;
+                const bool valid = i < end;
+                const int it = valid ? perm[i] : 0;
+                const bool left = valid && bin_of(it, axis) <= sb;
+                const unsigned ml = __ballot_sync(FULL, left);
+                if (left) tmp[start + nl + __popc(ml & ((1u << lane) - 1u))] = it;
+                nl += __popc(ml);
+            }
+            mid = start + nl;
+            for (int base = start; base < end; base += 32) {
+                const int i = base + lane;
+                const bool valid = i < end;
+                const int it = valid ? perm[i] : 0;
+                const bool right = valid && bin_of(it, axis) > sb;
+                const unsigned mr = __ballot_sync(FULL, right);
+                if (right) tmp[mid + nr + __popc(mr & ((1u << lane) - 1u))] = it;
+                nr += __popc(mr);
+            }
+            __syncwarp();
+            for (int i = start + lane; i < end; i += 32) perm[i] = tmp[i];
+            __syncwarp();
+        } else {
+            mid = start + m / 2;  // no useful split (coincident centroids): halve
+        }
+        // children: single items are leaves, ranges are new tasks
+        for (int side = 0; side < 2; ++side) {
+            const int cs = side == 0 ? start : mid, ce = side == 0 ? mid : end;
+            int ref;
+            if (ce - cs == 1) {
+                ref = ~perm[cs];
+                if (lane == 0) s.lparent[perm[cs]] = k;
+            } else {
+                int id = 0;
+                if (lane == 0) {
+                    id = atomicAdd(&next_node, 1);
+                    s.task[4 * id] = cs;
+                    s.task[4 * id + 1] = ce;
+                    s.nparent[id] = k;
+                    __threadfence_block();
+                    vtask[4 * id + 2] = 1;
+                }
+                ref = __shfl_sync(FULL, id, 0);
+            }
+            if (lane == 0) s.child[2 * k + side] = ref;
+        }
+        __syncwarp();
+    }
+    __syncthreads();
 }
 
 __global__ void k_tlas(TlasArgs a, int rebuild) {
@@ -129,6 +303,7 @@ __global__ void k_tlas(TlasArgs a, int rebuild) {
     TlasSmem s;
     unsigned char* p = smem_raw;
     s.keys = (uint64_t*)p; p += sizeof(uint64_t) * P;
+    s.task = (int*)p; p += sizeof(int) * 4 * (n - 1);
     s.box = (float*)p; p += sizeof(float) * 6 * n;
     s.ibox = (float*)p; p += sizeof(float) * 6 * (n - 1);
     s.child = (int*)p; p += sizeof(int) * 2 * (n - 1);
@@ -141,7 +316,9 @@ __global__ void k_tlas(TlasArgs a, int rebuild) {
     for (int j = tid; j < n - 1; j += blockDim.x) s.flags[j] = 0;
     __syncthreads();
 
-    if (rebuild) {
+    if (rebuild && a.builder == 1) {
+        sah_build_cta(s, n);
+    } else if (rebuild) {
         // centroid bounds of the instance boxes (empty boxes excluded)
         __shared__ float red[2][3][TLAS_THREADS / 32];
         float lo[3] = {FLT_MAX, FLT_MAX, FLT_MAX}, hi[3] = {-FLT_MAX, -FLT_MAX, -FLT_MAX};
@@ -225,6 +402,8 @@ __global__ void k_tlas(TlasArgs a, int rebuild) {
         }
         if (tid == 0) s.nparent[0] = -1;
         __syncthreads();
+    }
+    if (rebuild) {
         for (int j = tid; j < n - 1; j += blockDim.x) {
             a.tlas_child[2 * (toff + j)] = s.child[2 * j];
             a.tlas_child[2 * (toff + j) + 1] = s.child[2 * j + 1];
@@ -297,7 +476,7 @@ size_t tlas_smem_bytes(int n) {
     if (n <= 1) return 16;
     int P = 1;
     while (P < n) P <<= 1;
-    return sizeof(uint64_t) * P + sizeof(float) * 6 * n + sizeof(float) * 6 * (n - 1) +
+    return sizeof(uint64_t) * P + sizeof(int) * 4 * (n - 1) + sizeof(float) * 6 * n + sizeof(float) * 6 * (n - 1) +
            sizeof(int) * 2 * (n - 1) + sizeof(int) * (n - 1) + sizeof(int) * n + sizeof(int) * (n - 1);
 }
 

@@ -386,3 +386,19 @@ def test_stereo_mask_lidar_and_lane_mode():
     lane = to_np(cast_sensor(s, sensor, "range", channels=chans))
     for k in got:
         assert np.array_equal(got[k], lane[k]), k
+
+
+def test_tlas_builders_sah_and_lbvh_agree():
+    """The LBVH TLAS (default) and the binned-SAH TLAS give bitwise identical
+    images (the BVH only accelerates the plain definition); c3-shaped envs."""
+    sc, sensor = sg.config3(n_envs=6)
+    s = make_scene(sc)
+    a = to_np(cast_sensor(s, sensor, "depth"))
+    s.set_tlas_builder(1)
+    s.build()
+    b = to_np(cast_sensor(s, sensor, "depth"))
+    for k in a:
+        assert np.array_equal(a[k], b[k]), k
+    q = np.random.default_rng(2).choice(len(a["dist"]), 20000, replace=False)
+    ref = oracle.cast(sc, oracle_rays(sensor, "depth"), query=q)
+    compare(ref, a["dist"][q], a["seg"][q], a["face"][q], "c3 small SAH TLAS")
