@@ -97,8 +97,8 @@ def env_base(rank, envs_per_rank):
 
 def reduce_max(t, world):
     """Max over ranks (step times are max-over-ranks, never wall clock)."""
-    if world > 1:
-        import torch.distributed as dist
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return t
 
@@ -237,7 +237,10 @@ def main():
     assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE={world}"
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    # one process per GPU under torchrun (also for a 1-process torchrun, so
+    # the NCCL path is exercised); plain `python bench.py` runs without it
+    distributed = "RANK" in os.environ and "MASTER_ADDR" in os.environ
+    if distributed:
         dist.init_process_group("nccl", device_id=dev)
 
     cfg = args.config
@@ -285,7 +288,7 @@ def main():
     # ---- timed region: K steps, L2 flushed (untimed) between steps -------
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
            torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    if world > 1:
+    if distributed:
         dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
@@ -310,7 +313,7 @@ def main():
     total_ms = sum(step_ms)
     cast_total = sum(cast_ms)
     t = reduce_max(torch.tensor([total_ms, cast_total], dtype=torch.float64, device=dev), world)
-    if world > 1:
+    if distributed:
         dist.barrier()
     total_ms, cast_total = float(t[0]), float(t[1])
     ms_per_step = total_ms / args.steps
@@ -350,7 +353,7 @@ def main():
         for w in range(min(args.warmup, 2)):
             e2e_step(w)
         n_e2e = max(3, min(args.steps, 10))
-        if world > 1:
+        if distributed:
             dist.barrier()
         t0 = time.perf_counter()
         for k in range(n_e2e):
@@ -364,7 +367,7 @@ def main():
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": n_e2e,
                "note": "agr_cast_*_host: H2D poses, chunked cast, D2H of every output image"}
 
-    if world > 1:
+    if distributed:
         dist.destroy_process_group()
     if rank != 0:
         return 0
