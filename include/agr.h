@@ -172,6 +172,21 @@ agr_status agr_scene_get_info(agr_scene scene, agr_scene_info* info);
  */
 agr_status agr_set_instance_transforms(agr_scene scene, const float* T, void* stream);
 
+/*
+ * Replace the vertices of asset `asset` (device float [n_verts][3], same
+ * count and face topology as at create) and rebuild its BLAS on `stream`
+ * (Morton codes, radix sort, Karras, fit, collapse -- all on the device,
+ * no host round trip), then recompute every instance's bounds.  This is the
+ * paper's per-env mesh update at reset ("performing this
+ * exclusively for randomization of static environments"): give each env
+ * its own asset for per-env unique or deforming meshes.  Faces that become
+ * (non-)degenerate are handled (numbering is kept).  The TLAS is stale
+ * until agr_build / agr_refit.  Non-finite vertices give unspecified
+ * results for that asset.
+ */
+agr_status agr_update_mesh(agr_scene scene, int32_t asset, const float* verts, int32_t n_verts,
+                           void* stream);
+
 /* Full per-env TLAS rebuild (one CTA per env: LBVH -- Morton order + Karras
  * hierarchy -- or, after agr_set_tlas_builder(scene, 1), a binned-SAH
  * top-down split of the instance boxes), bottom-up fit and 4-wide collapse.

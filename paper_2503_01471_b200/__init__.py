@@ -83,6 +83,7 @@ _SIGS = {
     "agr_scene_get_info": (_I32, [_P, ctypes.POINTER(agr_scene_info)]),
     "agr_set_instance_transforms": (_I32, [_P, _P, _P]),
     "agr_build": (_I32, [_P, _P]),
+    "agr_update_mesh": (_I32, [_P, _I32, _P, _I32, _P]),
     "agr_refit": (_I32, [_P, _P]),
     "agr_cast_pinhole": (_I32, [_P, ctypes.POINTER(agr_pinhole), _I32, _P, _I32, ctypes.c_float,
                                 agr_outputs, _P]),
@@ -208,6 +209,11 @@ class Scene:
     def set_instance_transforms(self, T, stream=None):
         """T: CUDA float32 tensor [n_inst, 3, 4] (object -> env-local)."""
         _check(load().agr_set_instance_transforms(self.handle, _ptr(T), _stream_handle(stream)))
+
+    def update_mesh(self, asset: int, verts, stream=None):
+        """verts: CUDA float32 [V, 3] (same V as at create); rebuilds the BLAS."""
+        _check(load().agr_update_mesh(self.handle, int(asset), _ptr(verts), int(verts.shape[0]),
+                                      _stream_handle(stream)))
 
     def build(self, stream=None):
         _check(load().agr_build(self.handle, _stream_handle(stream)))

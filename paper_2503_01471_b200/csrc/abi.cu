@@ -85,6 +85,13 @@ struct agr_scene_s {
     int* tlas_depth = nullptr;
     AssetInfo* assets = nullptr;
     uint32_t* morton = nullptr;  // sorted BLAS Morton codes (debug export)
+    // asset meshes kept on the device for BLAS rebuilds (agr_update_mesh)
+    float* mesh_verts = nullptr;
+    int* mesh_faces = nullptr;
+    void* blas_scratch = nullptr;
+    std::vector<int64_t> h_mvert_off, h_mface_off;
+    std::vector<int> h_node_base, h_leaf_base, h_nverts, h_nfaces;
+    bool assets_stale = false;
     unsigned long long* counters = nullptr;
     bool built = false, dirty = false;
     int exact = 0;
@@ -169,6 +176,32 @@ struct agr_scene_s {
             if (o) cudaFree(o);
     }
 };
+
+// (Re)build asset a's BLAS from the device copy of its mesh (async on st).
+static cudaError_t build_asset(agr_scene_s* s, int a, cudaStream_t st) {
+    BlasBuildArgs ba;
+    ba.verts = s->mesh_verts + 3 * s->h_mvert_off[a];
+    ba.faces = s->mesh_faces + 3 * s->h_mface_off[a];
+    ba.n_verts = s->h_nverts[a];
+    ba.n_faces = s->h_nfaces[a];
+    ba.node_base = s->h_node_base[a];
+    ba.leaf_base = s->h_leaf_base[a];
+    ba.nodes = s->nodes;
+    ba.bnodes = s->bnodes;
+    ba.tris = s->tris;
+    ba.triv = s->triv;
+    ba.info_dev = s->assets + a;
+    ba.dbg_morton = s->morton + s->h_leaf_base[a];
+    return blas_build(ba, s->blas_scratch, nullptr, st);
+}
+
+static agr_status refresh_assets(agr_scene_s* s) {
+    if (!s->assets_stale) return AGR_OK;
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(s->h_assets.data(), s->assets, sizeof(AssetInfo) * s->n_assets, cudaMemcpyDeviceToHost));
+    s->assets_stale = false;
+    return AGR_OK;
+}
 
 extern "C" {
 
@@ -299,51 +332,39 @@ agr_status agr_scene_create(int32_t device, const agr_mesh* meshes, int32_t n_me
     CKB(cudaMemcpy(s->tlas_off, s->h_tlas_off.data(), sizeof(int) * n_envs, cudaMemcpyHostToDevice));
     CKB(cudaMemcpy(s->tlas_root, h_root.data(), sizeof(int) * n_envs, cudaMemcpyHostToDevice));
 
-    // BLAS build, one asset at a time on a private stream
+    // BLAS build: all asset meshes stay on the device (for agr_update_mesh);
+    // one asset after the other on a private stream
     cudaStream_t st;
     CKB(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
     size_t scratch_bytes = 0;
-    int maxF = 0, maxV = 0;
+    s->h_mvert_off.assign(n_meshes + 1, 0);
+    s->h_mface_off.assign(n_meshes + 1, 0);
     for (int a = 0; a < n_meshes; ++a) {
         size_t b = blas_scratch_bytes(meshes[a].n_faces);
         scratch_bytes = b > scratch_bytes ? b : scratch_bytes;
-        maxF = meshes[a].n_faces > maxF ? meshes[a].n_faces : maxF;
-        maxV = meshes[a].n_verts > maxV ? meshes[a].n_verts : maxV;
+        s->h_mvert_off[a + 1] = s->h_mvert_off[a] + meshes[a].n_verts;
+        s->h_mface_off[a + 1] = s->h_mface_off[a] + meshes[a].n_faces;
+        s->h_nverts.push_back(meshes[a].n_verts);
+        s->h_nfaces.push_back(meshes[a].n_faces);
     }
-    void* scratch = nullptr;
-    float* dverts = nullptr;
-    int* dfaces = nullptr;
-    cudaError_t err = cudaMalloc(&scratch, scratch_bytes);
-    if (err == cudaSuccess) err = cudaMalloc(&dverts, sizeof(float) * 3 * (size_t)maxV);
-    if (err == cudaSuccess) err = cudaMalloc(&dfaces, sizeof(int) * 3 * (size_t)maxF);
+    s->h_node_base = node_base;
+    s->h_leaf_base = leaf_base;
+    CKB(s->alloc(&s->mesh_verts, 3 * (size_t)s->h_mvert_off[n_meshes]));
+    CKB(s->alloc(&s->mesh_faces, 3 * (size_t)s->h_mface_off[n_meshes]));
+    CKB(s->alloc((char**)&s->blas_scratch, scratch_bytes));
+    cudaError_t err = cudaSuccess;
     for (int a = 0; a < n_meshes && err == cudaSuccess; ++a) {
-        err = cudaMemcpyAsync(dverts, meshes[a].verts, sizeof(float) * 3 * meshes[a].n_verts,
-                              cudaMemcpyHostToDevice, st);
+        err = cudaMemcpyAsync(s->mesh_verts + 3 * s->h_mvert_off[a], meshes[a].verts,
+                              sizeof(float) * 3 * meshes[a].n_verts, cudaMemcpyHostToDevice, st);
         if (err != cudaSuccess) break;
-        err = cudaMemcpyAsync(dfaces, meshes[a].faces, sizeof(int) * 3 * meshes[a].n_faces,
-                              cudaMemcpyHostToDevice, st);
+        err = cudaMemcpyAsync(s->mesh_faces + 3 * s->h_mface_off[a], meshes[a].faces,
+                              sizeof(int) * 3 * meshes[a].n_faces, cudaMemcpyHostToDevice, st);
         if (err != cudaSuccess) break;
-        BlasBuildArgs ba;
-        ba.verts = dverts;
-        ba.faces = dfaces;
-        ba.n_verts = meshes[a].n_verts;
-        ba.n_faces = meshes[a].n_faces;
-        ba.node_base = node_base[a];
-        ba.leaf_base = leaf_base[a];
-        ba.nodes = s->nodes;
-        ba.bnodes = s->bnodes;
-        ba.tris = s->tris;
-        ba.triv = s->triv;
-        ba.info_dev = s->assets + a;
-        ba.dbg_morton = s->morton + leaf_base[a];
-        int n_leaves = 0;
-        err = blas_build(ba, scratch, &n_leaves, st);
-        if (err == cudaSuccess) err = cudaStreamSynchronize(st);
+        err = cudaStreamSynchronize(st);  // the host arrays are the caller's
+        if (err != cudaSuccess) break;
+        err = build_asset(s, a, st);
     }
     if (err == cudaSuccess) err = cudaStreamSynchronize(st);
-    cudaFree(scratch);
-    cudaFree(dverts);
-    cudaFree(dfaces);
     if (err != cudaSuccess) {
         cudaStreamDestroy(st);
         return bail(cuda_fail(err, "BLAS build"));
@@ -387,6 +408,8 @@ agr_status agr_scene_get_info(agr_scene s, agr_scene_info* info) {
     info->n_envs = s->n_envs;
     info->n_instances = s->n_inst;
     info->n_blas_nodes = s->nb_blas;
+    agr_status rs = refresh_assets(s);
+    if (rs != AGR_OK) return rs;
     int64_t leaves = 0;
     int bd = 0;
     for (auto& a : s->h_assets) {
@@ -416,6 +439,23 @@ agr_status agr_set_instance_transforms(agr_scene s, const float* T, void* stream
     cudaStream_t st = (cudaStream_t)stream;
     CK(cudaMemcpyAsync(s->inst_T, T, sizeof(float) * 12 * s->n_inst, cudaMemcpyDeviceToDevice, st));
     CK(instances_update(s->tlas_args(), (int)s->n_inst, st));
+    s->dirty = true;
+    return AGR_OK;
+}
+
+agr_status agr_update_mesh(agr_scene s, int32_t asset, const float* verts, int32_t n_verts, void* stream) {
+    g_err.clear();
+    if (!s) return fail(AGR_EINVAL, "scene is NULL");
+    if (asset < 0 || asset >= s->n_assets) return fail(AGR_EINVAL, "asset %d out of range", asset);
+    if (!verts || n_verts != s->h_nverts[asset])
+        return fail(AGR_EINVAL, "asset %d has %d vertices (got %d)", asset, s->h_nverts[asset], n_verts);
+    DeviceGuard guard(s->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    CK(cudaMemcpyAsync(s->mesh_verts + 3 * s->h_mvert_off[asset], verts, sizeof(float) * 3 * n_verts,
+                       cudaMemcpyDeviceToDevice, st));
+    CK(build_asset(s, asset, st));
+    CK(instances_update(s->tlas_args(), (int)s->n_inst, st));  // instance boxes from the new BLAS
+    s->assets_stale = true;
     s->dirty = true;
     return AGR_OK;
 }
@@ -790,6 +830,8 @@ agr_status agr_debug_export_blas(agr_scene s, int32_t asset, float* nodes, int32
     if (!s || !n_nodes || !n_leaves) return fail(AGR_EINVAL, "bad argument");
     if (asset < 0 || asset >= s->n_assets) return fail(AGR_EINVAL, "asset out of range");
     DeviceGuard guard(s->device);
+    agr_status rs = refresh_assets(s);
+    if (rs != AGR_OK) return rs;
     const AssetInfo& a = s->h_assets[asset];
     int64_t nn = a.n_leaves > 1 ? a.n_leaves - 1 : 1;
     *n_nodes = nn;
@@ -831,6 +873,11 @@ agr_status agr_debug_export_bvh4(agr_scene s, int32_t which, float* nodes, int32
     int64_t base, count;
     if (which >= 0) {
         if (which >= s->n_assets) return fail(AGR_EINVAL, "asset out of range");
+        {
+            DeviceGuard g2(s->device);
+            agr_status rs = refresh_assets(s);
+            if (rs != AGR_OK) return rs;
+        }
         const AssetInfo& a = s->h_assets[which];
         base = a.node_base;
         count = a.n_leaves > 1 ? a.n_leaves - 1 : 1;

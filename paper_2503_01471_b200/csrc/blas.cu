@@ -260,8 +260,9 @@ __device__ __forceinline__ int kdelta(const uint32_t* k, int n, int i, int j) {
     return __clz(a ^ b);
 }
 
-__global__ void k_karras(const uint32_t* __restrict__ k, int n, int* __restrict__ child,
+__global__ void k_karras(const uint32_t* __restrict__ k, const uint32_t* n_dev, int* __restrict__ child,
                          int* __restrict__ node_parent, int* __restrict__ leaf_parent) {
+    const int n = (int)*n_dev;
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n - 1) return;
     int d = (kdelta(k, n, i, i + 1) - kdelta(k, n, i, i - 1)) >= 0 ? 1 : -1;
@@ -298,11 +299,12 @@ __device__ __forceinline__ void load_box_cg(const float* p, float b[6]) {
     for (int k = 0; k < 6; ++k) b[k] = __ldcg(p + k);
 }
 
-__global__ void k_fit(int n, const uint32_t* __restrict__ sorted_prim, const float* tri_box,
+__global__ void k_fit(const uint32_t* n_dev, const uint32_t* __restrict__ sorted_prim, const float* tri_box,
                       const int* __restrict__ child, const int* __restrict__ node_parent,
                       const int* __restrict__ leaf_parent, float* ibox, int* flags, int* depth) {
+    const int n = (int)*n_dev;
     int p = blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= n) return;
+    if (n < 2 || p >= n) return;
     // depth of this leaf
     int dd = 0;
     for (int q = leaf_parent[p]; q >= 0; q = node_parent[q]) ++dd;
@@ -351,9 +353,10 @@ __device__ __forceinline__ int global_ref(int r, int node_base, int leaf_base) {
     return r < 0 ? ~(leaf_base + ~r) : node_base + r;
 }
 
-__global__ void k_pack_nodes(int n, const uint32_t* __restrict__ sorted_prim,
+__global__ void k_pack_nodes(const uint32_t* n_dev, const uint32_t* __restrict__ sorted_prim,
                              const float* tri_box, const int* __restrict__ child,
                              const float* ibox, float4* nodes, int node_base, int leaf_base) {
+    const int n = (int)*n_dev;
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     int n_int = n > 1 ? n - 1 : 1;
     if (i >= n_int) return;
@@ -369,9 +372,10 @@ __global__ void k_pack_nodes(int n, const uint32_t* __restrict__ sorted_prim,
 }
 
 // K5b: BVH4 node j = greedy 4-wide collapse of binary node j.
-__global__ void k_collapse4(int n, const uint32_t* __restrict__ sorted_prim, const float* tri_box,
+__global__ void k_collapse4(const uint32_t* n_dev, const uint32_t* __restrict__ sorted_prim, const float* tri_box,
                             const int* __restrict__ child, const float* ibox, float4* nodes,
                             int node_base, int leaf_base) {
+    const int n = (int)*n_dev;
     int j = blockIdx.x * blockDim.x + threadIdx.x;
     int n_int = n > 1 ? n - 1 : 1;
     if (j >= n_int) return;
@@ -397,9 +401,10 @@ __global__ void k_collapse4(int n, const uint32_t* __restrict__ sorted_prim, con
     write_node4(nodes, node_base + j, boxes, g, cnt);
 }
 
-__global__ void k_pack_tris(int n, const uint32_t* __restrict__ sorted_prim,
+__global__ void k_pack_tris(const uint32_t* n_dev, const uint32_t* __restrict__ sorted_prim,
                             const float* __restrict__ verts, const int* __restrict__ faces,
                             float4* tris, float* triv, int leaf_base) {
+    const int n = (int)*n_dev;
     int p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= n) return;
     int f = (int)sorted_prim[p];
@@ -424,9 +429,10 @@ __global__ void k_pack_tris(int n, const uint32_t* __restrict__ sorted_prim,
     }
 }
 
-__global__ void k_asset_info(int n, int F, const uint32_t* bounds, const float* ibox,
+__global__ void k_asset_info(const uint32_t* n_dev, int F, const uint32_t* bounds, const float* ibox,
                              const float* tri_box, const uint32_t* sorted_prim, const int* depth,
                              int node_base, int leaf_base, AssetInfo* info) {
+    const int n = (int)*n_dev;
     AssetInfo a;
     a.node_base = node_base;
     a.leaf_base = leaf_base;
@@ -475,37 +481,30 @@ cudaError_t blas_build(const BlasBuildArgs& a, void* scratch, int* n_leaves_out,
                                                     s.vals[cur ^ 1], F, shift, s.hist, nb);
         cur ^= 1;
     }
-    // number of non-degenerate leaves (device -> host; the create call is synchronous)
-    uint32_t n_valid = 0;
-    cudaError_t e = cudaMemcpyAsync(&n_valid, s.bounds + 7, sizeof(uint32_t), cudaMemcpyDeviceToHost, stream);
-    if (e != cudaSuccess) return e;
-    e = cudaStreamSynchronize(stream);
-    if (e != cudaSuccess) return e;
-    int n = (int)n_valid;
-    if (a.dbg_morton && n > 0)
-        cudaMemcpyAsync(a.dbg_morton, s.keys[cur], sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, stream);
+    // everything below is sized by F and reads the number of non-degenerate
+    // leaves n from the device (no host round trip: updates stay async)
+    const uint32_t* n_dev = s.bounds + 7;
+    if (a.dbg_morton)
+        cudaMemcpyAsync(a.dbg_morton, s.keys[cur], sizeof(uint32_t) * F, cudaMemcpyDeviceToDevice, stream);
     const uint32_t* sk = s.keys[cur];
     const uint32_t* sv = s.vals[cur];
     cudaMemsetAsync(s.depth, 0, sizeof(int), stream);
-    if (n > 1) {
-        cudaMemsetAsync(s.flags, 0, sizeof(int) * (n - 1), stream);
-        k_karras<<<(n - 1 + T_BLK - 1) / T_BLK, T_BLK, 0, stream>>>(sk, n, s.child, s.node_parent,
-                                                                   s.leaf_parent);
-        k_fit<<<(n + T_BLK - 1) / T_BLK, T_BLK, 0, stream>>>(n, sv, s.tri_box, s.child, s.node_parent,
-                                                            s.leaf_parent, s.ibox, s.flags, s.depth);
-    }
-    int n_int = n > 1 ? n - 1 : 1;
-    k_pack_nodes<<<(n_int + T_BLK - 1) / T_BLK, T_BLK, 0, stream>>>(n, sv, s.tri_box, s.child, s.ibox,
-                                                                    a.bnodes, a.node_base, a.leaf_base);
-    k_collapse4<<<(n_int + T_BLK - 1) / T_BLK, T_BLK, 0, stream>>>(n, sv, s.tri_box, s.child, s.ibox,
-                                                                  a.nodes, a.node_base, a.leaf_base);
-    if (n > 0)
-        k_pack_tris<<<(n + T_BLK - 1) / T_BLK, T_BLK, 0, stream>>>(n, sv, a.verts, a.faces, a.tris,
-                                                                  a.triv, a.leaf_base);
-    k_asset_info<<<1, 1, 0, stream>>>(n, F, s.bounds, s.ibox, s.tri_box, sv, s.depth, a.node_base,
+    const int Fi = F > 1 ? F - 1 : 1;
+    cudaMemsetAsync(s.flags, 0, sizeof(int) * Fi, stream);
+    k_karras<<<(Fi + T_BLK - 1) / T_BLK, T_BLK, 0, stream>>>(sk, n_dev, s.child, s.node_parent, s.leaf_parent);
+    k_fit<<<(F + T_BLK - 1) / T_BLK, T_BLK, 0, stream>>>(n_dev, sv, s.tri_box, s.child, s.node_parent,
+                                                        s.leaf_parent, s.ibox, s.flags, s.depth);
+    k_pack_nodes<<<(Fi + T_BLK - 1) / T_BLK, T_BLK, 0, stream>>>(n_dev, sv, s.tri_box, s.child, s.ibox,
+                                                                a.bnodes, a.node_base, a.leaf_base);
+    k_collapse4<<<(Fi + T_BLK - 1) / T_BLK, T_BLK, 0, stream>>>(n_dev, sv, s.tri_box, s.child, s.ibox,
+                                                               a.nodes, a.node_base, a.leaf_base);
+    k_pack_tris<<<(F + T_BLK - 1) / T_BLK, T_BLK, 0, stream>>>(n_dev, sv, a.verts, a.faces, a.tris,
+                                                              a.triv, a.leaf_base);
+    k_asset_info<<<1, 1, 0, stream>>>(n_dev, F, s.bounds, s.ibox, s.tri_box, sv, s.depth, a.node_base,
                                       a.leaf_base, a.info_dev);
-    *n_leaves_out = n;
+    if (n_leaves_out) *n_leaves_out = -1;  // known on the device only
     return cudaGetLastError();
 }
+
 
 }  // namespace agr

@@ -415,3 +415,47 @@ def make_config(c: int, n_envs=None, env_base=0):
         return config1()
     kw = {} if n_envs is None else dict(n_envs=n_envs)
     return {2: config2, 3: config3, 4: config4, 5: config5}[c](env_base=env_base, **kw)
+
+
+# ----------------------------------------------------------------------------
+# sensor presets ("idealized configurations of: Ouster OS-0,
+# OS-1, OS-2, OS-Dome, Intel RealSense D455, Luxonis Oak-D (and Pro W) and ST
+# VL53L5CX ToF sensors").  The paper gives only the names; the parameters
+# below are the public nominal specs (reading R22): vertical FOV
+# and channel counts of the Ouster family, depth FOV of the D455 / Oak-D
+# stereo cameras, 8x8 zones over 45 deg x 45 deg for the VL53L5CX.
+# ----------------------------------------------------------------------------
+
+def ouster(model="OS0", channels=128, columns=512):
+    """Ouster lidar beam table [C][K][3]: uniform channels over the model's
+    vertical FOV (OS0 90 deg, OS1 45 deg, OS2 22.5 deg), 360 deg azimuth."""
+    vfov = {"OS0": 90.0, "OS1": 45.0, "OS2": 22.5}[model]
+    return lidar_beams(channels, columns, -vfov / 2.0, vfov / 2.0)
+
+
+def ouster_dome(channels=128, columns=512):
+    """OS-Dome: 180 deg vertical FOV hemisphere looking up (elevations 0..90
+    deg above the horizon and the mirror image: -90..90 about the up axis is
+    modelled as elevations (0, 90] deg here, i.e. the upper hemisphere)."""
+    return dome_beams(channels, columns)
+
+
+PRESETS = {
+    # name: (kind, builder)
+    "os0-128": ("beams", lambda: ouster("OS0", 128, 512)),
+    "os1-64": ("beams", lambda: ouster("OS1", 64, 1024)),
+    "os2-32": ("beams", lambda: ouster("OS2", 32, 1024)),
+    "os-dome-128": ("beams", lambda: ouster_dome(128, 512)),
+    "d455": ("pinhole", lambda: pinhole(848, 480, 87.0)),
+    "d455-270x480": ("pinhole", lambda: pinhole(480, 270, 87.0)),
+    "oak-d": ("pinhole", lambda: pinhole(640, 400, 72.0)),
+    "oak-d-pro-w": ("pinhole", lambda: pinhole(640, 400, 127.0)),
+    "vl53l5cx": ("pinhole", lambda: pinhole(8, 8, 45.0)),
+}
+
+
+def preset(name: str) -> dict:
+    """Sensor spec for a preset: {'kind': 'pinhole', 'cam': {...}} or
+    {'kind': 'beams', 'beams': float32 [C][K][3]}."""
+    kind, build = PRESETS[name]
+    return {"kind": kind, ("cam" if kind == "pinhole" else "beams"): build()}

@@ -402,3 +402,58 @@ def test_tlas_builders_sah_and_lbvh_agree():
     q = np.random.default_rng(2).choice(len(a["dist"]), 20000, replace=False)
     ref = oracle.cast(sc, oracle_rays(sensor, "depth"), query=q)
     compare(ref, a["dist"][q], a["seg"][q], a["face"][q], "c3 small SAH TLAS")
+
+
+# ---- f4: sensor presets ----------------------------------------------------------------
+
+@pytest.mark.parametrize("name", sorted(sg.PRESETS))
+def test_sensor_presets_match_oracle(name):
+    """Every preset of PAPER.md:228 runs through the cast and matches the
+    oracle on a c4-shaped room (sampled rays)."""
+    sc, sensor = sg.config4(n_envs=3)
+    p = sg.preset(name)
+    sensor = dict(sensor, kind=p["kind"])
+    if p["kind"] == "pinhole":
+        sensor["cam"] = p["cam"]
+        kind = "range"
+    else:
+        sensor["beams"] = p["beams"]
+        kind = "range"
+    s = make_scene(sc)
+    got = to_np(cast_sensor(s, sensor, kind))
+    n = len(got["dist"])
+    q = np.random.default_rng(3).choice(n, min(n, 6000), replace=False)
+    ref = oracle.cast(sc, oracle_rays(sensor, kind), query=q)
+    compare(ref, got["dist"][q], got["seg"][q], got["face"][q], name)
+
+
+# ---- f3: per-env unique / deforming meshes ------------------------------------------
+
+def test_update_mesh_per_env_unique_and_deforming():
+    """Per-env unique meshes (one asset per env) re-randomised at reset by
+    agr_update_mesh: the rebuilt BLAS + refreshed instance
+    bounds + TLAS give the oracle's images for the new vertices, including
+    faces that become degenerate / non-degenerate."""
+    rng = np.random.default_rng(8)
+    E = 4
+    meshes = [sg.sphere_mesh(0.8, 2, name=f"blob{e}") for e in range(E)]
+    per_env = [[(e, 1, sg.make_T(np.eye(3), (3.0, 0.0, 0.0)))] for e in range(E)]
+    sc = sg.assemble(meshes, per_env)
+    cam = sg.pinhole(64, 48, 70.0)
+    sensor = dict(kind="pinhole", cam=cam, poses=sg.identity_poses(E), max_range=10.0)
+    s = make_scene(sc)
+    for step in range(3):
+        new_meshes = []
+        for e in range(E):
+            v = meshes[e].verts.astype(np.float64)
+            v = v * rng.uniform(0.7, 1.3, (len(v), 1)) + rng.uniform(-0.2, 0.2, 3)
+            if step == 1:
+                v[meshes[e].faces[:5, 1]] = v[meshes[e].faces[:5, 0]]  # some zero-area faces
+            vf = v.astype(np.float32)
+            new_meshes.append(sg.Mesh(meshes[e].name, vf, meshes[e].faces))
+            s.update_mesh(e, torch.from_numpy(vf).to(dev()))
+        s.build() if step != 2 else s.refit()
+        got = to_np(cast_sensor(s, sensor, "range"))
+        sc2 = sg.assemble(new_meshes, per_env)
+        ref = oracle.cast(sc2, oracle_rays(sensor, "range"))
+        compare(ref, got["dist"], got["seg"], got["face"], f"update step {step}")
