@@ -158,6 +158,20 @@ agr_status agr_scene_create(int32_t device, const agr_mesh* meshes, int32_t n_me
                             int32_t n_envs, const int64_t* env_offsets,
                             const agr_instance* inst, agr_scene* out);
 
+/* Creation options (agr_scene_create uses the defaults). */
+typedef struct {
+    int32_t trbvh_rounds; /* treelet-restructuring passes applied to every
+                             BLAS after the LBVH (Karras & Aila 2013; SAH-
+                             optimal treelets of 7 subtrees), 0..16; default 3.
+                             0 keeps the plain Karras LBVH.                  */
+    int32_t reserved[7];  /* must be 0                                        */
+} agr_create_options;
+
+agr_status agr_scene_create_ex(int32_t device, const agr_mesh* meshes, int32_t n_meshes,
+                               int32_t n_envs, const int64_t* env_offsets,
+                               const agr_instance* inst, const agr_create_options* opts,
+                               agr_scene* out);
+
 /* Free all device memory of the scene (synchronises its device). NULL: no-op. */
 agr_status agr_scene_destroy(agr_scene scene);
 

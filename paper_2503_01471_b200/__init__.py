@@ -64,6 +64,10 @@ CHANNELS = {"dist": ("float32", None), "seg": ("int32", None), "face": ("int32",
             "valid": ("int32", None)}
 
 
+class agr_create_options(ctypes.Structure):
+    _fields_ = [("trbvh_rounds", ctypes.c_int32), ("reserved", ctypes.c_int32 * 7)]
+
+
 class agr_scene_info(ctypes.Structure):
     _fields_ = [("n_assets", ctypes.c_int32), ("n_envs", ctypes.c_int32),
                 ("n_instances", ctypes.c_int64), ("n_blas_nodes", ctypes.c_int64),
@@ -79,6 +83,9 @@ _SIGS = {
     "agr_last_error": (ctypes.c_char_p, []),
     "agr_scene_create": (_I32, [_I32, ctypes.POINTER(agr_mesh), _I32, _I32, _P,
                                 ctypes.POINTER(agr_instance), ctypes.POINTER(_P)]),
+    "agr_scene_create_ex": (_I32, [_I32, ctypes.POINTER(agr_mesh), _I32, _I32, _P,
+                                   ctypes.POINTER(agr_instance), ctypes.POINTER(agr_create_options),
+                                   ctypes.POINTER(_P)]),
     "agr_scene_destroy": (_I32, [_P]),
     "agr_scene_get_info": (_I32, [_P, ctypes.POINTER(agr_scene_info)]),
     "agr_set_instance_transforms": (_I32, [_P, _P, _P]),
@@ -162,8 +169,10 @@ def _outputs(out: dict):
 class Scene:
     """Owner of an ``agr_scene`` handle (one CUDA device)."""
 
-    def __init__(self, meshes, env_offsets, inst_asset, inst_label, device: int = 0):
-        """meshes: list of (verts float32 [V][3], faces int32 [F][3]) host arrays."""
+    def __init__(self, meshes, env_offsets, inst_asset, inst_label, device: int = 0,
+                 trbvh_rounds: int = 3):
+        """meshes: list of (verts float32 [V][3], faces int32 [F][3]) host arrays.
+        trbvh_rounds: treelet-restructuring passes on every BLAS (0 = LBVH)."""
         lib = load()
         self._keep = []
         arr = (agr_mesh * len(meshes))()
@@ -180,8 +189,9 @@ class Scene:
         for j in range(n_inst):
             inst[j] = agr_instance(int(ia[j]), int(il[j]))
         h = _P()
-        _check(lib.agr_scene_create(device, arr, len(meshes), len(env_offsets) - 1,
-                                    env_offsets.ctypes.data, inst, ctypes.byref(h)))
+        opts = agr_create_options(int(trbvh_rounds))
+        _check(lib.agr_scene_create_ex(device, arr, len(meshes), len(env_offsets) - 1,
+                                       env_offsets.ctypes.data, inst, ctypes.byref(opts), ctypes.byref(h)))
         self._keep = []
         self.handle = h
         self.device = device
@@ -189,10 +199,10 @@ class Scene:
         self.n_inst = n_inst
 
     @classmethod
-    def from_scenegen(cls, sc, device: int = 0):
+    def from_scenegen(cls, sc, device: int = 0, trbvh_rounds: int = 3):
         """Build from a ``scenegen.Scene`` (inputs only; no arithmetic)."""
         return cls([(m.verts, m.faces) for m in sc.meshes], sc.env_off, sc.inst_asset,
-                   sc.inst_label, device)
+                   sc.inst_label, device, trbvh_rounds)
 
     def close(self):
         if getattr(self, "handle", None):

@@ -92,6 +92,7 @@ struct agr_scene_s {
     std::vector<int64_t> h_mvert_off, h_mface_off;
     std::vector<int> h_node_base, h_leaf_base, h_nverts, h_nfaces;
     bool assets_stale = false;
+    int trbvh_rounds = 3;
     unsigned long long* counters = nullptr;
     bool built = false, dirty = false;
     int exact = 0;
@@ -192,6 +193,7 @@ static cudaError_t build_asset(agr_scene_s* s, int a, cudaStream_t st) {
     ba.triv = s->triv;
     ba.info_dev = s->assets + a;
     ba.dbg_morton = s->morton + s->h_leaf_base[a];
+    ba.trbvh_rounds = s->trbvh_rounds;
     return blas_build(ba, s->blas_scratch, nullptr, st);
 }
 
@@ -211,6 +213,12 @@ const char* agr_last_error(void) { return g_err.c_str(); }
 
 agr_status agr_scene_create(int32_t device, const agr_mesh* meshes, int32_t n_meshes, int32_t n_envs,
                             const int64_t* env_offsets, const agr_instance* inst, agr_scene* out) {
+    return agr_scene_create_ex(device, meshes, n_meshes, n_envs, env_offsets, inst, nullptr, out);
+}
+
+agr_status agr_scene_create_ex(int32_t device, const agr_mesh* meshes, int32_t n_meshes, int32_t n_envs,
+                               const int64_t* env_offsets, const agr_instance* inst,
+                               const agr_create_options* opts, agr_scene* out) {
     g_err.clear();
     if (!out) return fail(AGR_EINVAL, "out is NULL");
     *out = nullptr;
@@ -251,8 +259,11 @@ agr_status agr_scene_create(int32_t device, const agr_mesh* meshes, int32_t n_me
     DeviceGuard guard(device);
     if (!guard.ok) return fail(AGR_ECUDA, "cudaSetDevice(%d) failed", device);
 
+    if (opts && (opts->trbvh_rounds < 0 || opts->trbvh_rounds > 16))
+        return fail(AGR_EINVAL, "trbvh_rounds must be in [0, 16]");
     agr_scene_s* s = new agr_scene_s();
     s->device = device;
+    if (opts) s->trbvh_rounds = opts->trbvh_rounds;
     s->n_assets = n_meshes;
     s->n_envs = n_envs;
     s->n_inst = n_inst;

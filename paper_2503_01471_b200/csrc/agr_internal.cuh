@@ -187,6 +187,7 @@ struct BlasBuildArgs {
     float* triv;           // global exact-vertex array
     AssetInfo* info_dev;   // this asset's AssetInfo (device)
     uint32_t* dbg_morton;  // optional: sorted codes [n_leaves] (device) or null
+    int trbvh_rounds;      // treelet-restructuring passes after the LBVH (0 = plain LBVH)
 };
 // Builds one asset's BLAS.  `scratch` must hold blas_scratch_bytes(F) bytes.
 size_t blas_scratch_bytes(int n_faces);

@@ -40,6 +40,7 @@ struct Scratch {
     float* ibox;         // [F-1][6]
     int* flags;          // [F-1]
     int* depth;          // [1]
+    float* cost;         // [F-1] SAH cost of each internal node's subtree (TRBVH)
 };
 
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
@@ -60,6 +61,7 @@ Scratch carve(void* base, int F) {
     s.ibox = (float*)p; p += align_up(sizeof(float) * 6 * Fi);
     s.flags = (int*)p; p += align_up(sizeof(int) * Fi);
     s.depth = (int*)p; p += align_up(sizeof(int));
+    s.cost = (float*)p; p += align_up(sizeof(float) * Fi);
     return s;
 }
 
@@ -329,6 +331,155 @@ __global__ void k_fit(const uint32_t* n_dev, const uint32_t* __restrict__ sorted
     }
 }
 
+// ---- K4b: treelet restructuring (TRBVH) ------------------------------------------------
+// Karras & Aila, "Fast parallel construction of high-quality bounding volume
+// hierarchies" (HPG 2013): after the LBVH, every internal node (bottom-up,
+// second arrival as in the fit) forms a treelet of up to 7 subtrees by
+// repeatedly opening the largest-area one, and replaces the treelet's
+// topology by the SAH-optimal one found by dynamic programming over all
+// subsets.  Boxes of the treelet's new internal nodes are the unions of
+// their subsets, so nothing outside the treelet changes.
+// f3 "BLAS quality (treelet restructuring)".
+constexpr float SAH_CI = 1.2f, SAH_CT = 1.0f;
+constexpr int TREELET = 7;
+
+__device__ __forceinline__ float box_area(const float b[6]) {
+    float dx = b[3] - b[0], dy = b[4] - b[1], dz = b[5] - b[2];
+    return dx * dy + dy * dz + dz * dx;
+}
+
+__global__ void k_trbvh(const uint32_t* n_dev, const uint32_t* __restrict__ sorted_prim,
+                        const float* __restrict__ tri_box, int* child, int* node_parent,
+                        int* leaf_parent, float* ibox, float* cost, int* flags) {
+    const int n = (int)*n_dev;
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (n < 2 || p >= n) return;
+    int node = __ldcg(leaf_parent + p);
+    while (node >= 0) {
+        __threadfence();
+        if (atomicAdd(&flags[node], 1) == 0) return;  // the sibling subtree is not final yet
+        __threadfence();
+        // treelet leaves (subtree roots) and internal nodes
+        int L[TREELET], I[TREELET - 1];
+        int m = 2, ni = 1;
+        L[0] = __ldcg(child + 2 * node);
+        L[1] = __ldcg(child + 2 * node + 1);
+        I[0] = node;
+        while (m < TREELET) {
+            int best = -1;
+            float ba = -1.0f;
+            for (int k = 0; k < m; ++k) {
+                if (L[k] < 0) continue;
+                float b[6];
+                for (int c = 0; c < 6; ++c) b[c] = __ldcg(ibox + 6 * L[k] + c);
+                const float a = box_area(b);
+                if (a > ba) { ba = a; best = k; }
+            }
+            if (best < 0) break;
+            const int r = L[best];
+            I[ni++] = r;
+            L[best] = __ldcg(child + 2 * r);
+            L[m++] = __ldcg(child + 2 * r + 1);
+        }
+        // leaf boxes / costs
+        float lb[TREELET][6], lc[TREELET];
+        for (int k = 0; k < m; ++k) {
+            const float* src = L[k] < 0 ? tri_box + 6 * sorted_prim[~L[k]] : ibox + 6 * L[k];
+            for (int c = 0; c < 6; ++c) lb[k][c] = __ldcg(src + c);
+            lc[k] = L[k] < 0 ? SAH_CT * box_area(lb[k]) : __ldcg(cost + L[k]);
+        }
+        // the node's current cost (children final)
+        float nb[6];
+        for (int c = 0; c < 6; ++c) nb[c] = __ldcg(ibox + 6 * node + c);
+        float ccur;
+        {
+            const int c0 = __ldcg(child + 2 * node), c1 = __ldcg(child + 2 * node + 1);
+            auto sub_cost = [&](int r) {
+                if (r < 0) {
+                    float b[6];
+                    for (int c = 0; c < 6; ++c) b[c] = __ldcg(tri_box + 6 * sorted_prim[~r] + c);
+                    return SAH_CT * box_area(b);
+                }
+                return __ldcg(cost + r);
+            };
+            ccur = SAH_CI * box_area(nb) + sub_cost(c0) + sub_cost(c1);
+        }
+        if (m >= 3) {
+            const int full = (1 << m) - 1;
+            float sb[1 << TREELET][6];
+            float copt[1 << TREELET];
+            unsigned char part[1 << TREELET];
+            for (int sset = 1; sset <= full; ++sset) {
+                const int low = __ffs(sset) - 1;
+                const int rest = sset & (sset - 1);
+                if (rest == 0) {
+                    for (int c = 0; c < 6; ++c) sb[sset][c] = lb[low][c];
+                    copt[sset] = lc[low];
+                    part[sset] = 0;
+                    continue;
+                }
+                for (int c = 0; c < 3; ++c) {
+                    sb[sset][c] = fminf(sb[rest][c], lb[low][c]);
+                    sb[sset][3 + c] = fmaxf(sb[rest][3 + c], lb[low][3 + c]);
+                }
+                const int lsb = sset & -sset;
+                float best = INFINITY;
+                int bp = 0;
+                for (int q = (sset - 1) & sset; q; q = (q - 1) & sset) {
+                    if (!(q & lsb)) continue;  // each unordered partition once
+                    const float cc = copt[q] + copt[sset ^ q];
+                    if (cc < best) { best = cc; bp = q; }
+                }
+                copt[sset] = SAH_CI * box_area(sb[sset]) + best;
+                part[sset] = (unsigned char)bp;
+            }
+            if (copt[full] < ccur * (1.0f - 1e-6f)) {
+                // rebuild the treelet: root keeps its id, the others are reused
+                int st_s[TREELET], st_n[TREELET], sp = 0, pool = 1;
+                st_s[sp] = full;
+                st_n[sp++] = node;
+                while (sp > 0) {
+                    --sp;
+                    const int sset = st_s[sp], nd = st_n[sp];
+                    const int q0 = part[sset], q1 = sset ^ q0;
+                    for (int side = 0; side < 2; ++side) {
+                        const int sub = side == 0 ? q0 : q1;
+                        int c;
+                        if ((sub & (sub - 1)) == 0) {
+                            c = L[__ffs(sub) - 1];
+                        } else {
+                            c = I[pool++];
+                            st_s[sp] = sub;
+                            st_n[sp++] = c;
+                            for (int k = 0; k < 6; ++k) __stcg(ibox + 6 * c + k, sb[sub][k]);
+                            __stcg(cost + c, copt[sub]);
+                        }
+                        __stcg(child + 2 * nd + side, c);
+                        if (c < 0) __stcg(leaf_parent + ~c, nd);
+                        else __stcg(node_parent + c, nd);
+                    }
+                }
+                __stcg(cost + node, copt[full]);
+            } else {
+                __stcg(cost + node, ccur);
+            }
+        } else {
+            __stcg(cost + node, ccur);
+        }
+        __threadfence();
+        node = __ldcg(node_parent + node);
+    }
+}
+
+__global__ void k_depth(const uint32_t* n_dev, const int* leaf_parent, const int* node_parent, int* depth) {
+    const int n = (int)*n_dev;
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (n < 2 || p >= n) return;
+    int dd = 0;
+    for (int q = leaf_parent[p]; q >= 0; q = node_parent[q]) ++dd;
+    atomicMax(depth, dd);
+}
+
 // ---- K5: pack -------------------------------------------------------------------------
 __device__ __forceinline__ void child_box(int r, const uint32_t* sorted_prim, const float* tri_box,
                                           const float* ibox, float b[6]) {
@@ -459,7 +610,7 @@ size_t blas_scratch_bytes(int F) {
     return align_up(sizeof(float) * 6 * F) + align_up(32) + 4 * align_up(sizeof(uint32_t) * F) +
            align_up(sizeof(uint32_t) * 256 * nb) + align_up(sizeof(int) * 2 * Fi) +
            align_up(sizeof(int) * Fi) + align_up(sizeof(int) * F) + align_up(sizeof(float) * 6 * Fi) +
-           align_up(sizeof(int) * Fi) + align_up(sizeof(int)) + 256;
+           align_up(sizeof(int) * Fi) + align_up(sizeof(int)) + align_up(sizeof(float) * Fi) + 256;
 }
 
 cudaError_t blas_build(const BlasBuildArgs& a, void* scratch, int* n_leaves_out,
@@ -494,6 +645,15 @@ cudaError_t blas_build(const BlasBuildArgs& a, void* scratch, int* n_leaves_out,
     k_karras<<<(Fi + T_BLK - 1) / T_BLK, T_BLK, 0, stream>>>(sk, n_dev, s.child, s.node_parent, s.leaf_parent);
     k_fit<<<(F + T_BLK - 1) / T_BLK, T_BLK, 0, stream>>>(n_dev, sv, s.tri_box, s.child, s.node_parent,
                                                         s.leaf_parent, s.ibox, s.flags, s.depth);
+    for (int round = 0; round < a.trbvh_rounds; ++round) {
+        cudaMemsetAsync(s.flags, 0, sizeof(int) * Fi, stream);
+        k_trbvh<<<(F + 63) / 64, 64, 0, stream>>>(n_dev, sv, s.tri_box, s.child, s.node_parent, s.leaf_parent,
+                                                  s.ibox, s.cost, s.flags);
+    }
+    if (a.trbvh_rounds > 0) {
+        cudaMemsetAsync(s.depth, 0, sizeof(int), stream);
+        k_depth<<<(F + T_BLK - 1) / T_BLK, T_BLK, 0, stream>>>(n_dev, s.leaf_parent, s.node_parent, s.depth);
+    }
     k_pack_nodes<<<(Fi + T_BLK - 1) / T_BLK, T_BLK, 0, stream>>>(n_dev, sv, s.tri_box, s.child, s.ibox,
                                                                 a.bnodes, a.node_base, a.leaf_base);
     k_collapse4<<<(Fi + T_BLK - 1) / T_BLK, T_BLK, 0, stream>>>(n_dev, sv, s.tri_box, s.child, s.ibox,

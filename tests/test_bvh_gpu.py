@@ -33,8 +33,9 @@ def test_morton_ref_known_values():
 
 
 def _check_blas(mesh):
+    """Plain LBVH (no treelet restructuring): the Karras topology is checked."""
     sc = sg.assemble([mesh], [[(0, 0, sg.make_T(np.eye(3), (0, 0, 0)))]])
-    s = make_scene(sc, build=False)
+    s = make_scene(sc, build=False, trbvh_rounds=0)
     nodes, leaf_face, codes = s.debug_export_blas(0)
     v = mesh.verts
     tri = v[mesh.faces]
@@ -216,3 +217,59 @@ def test_bvh4_tlas_covers_every_instance_once():
         nodes, root = s.debug_export_bvh4(-1 - e)
         leaves = _walk_bvh4(nodes, root)
         assert sorted(leaves) == list(range(int(sc.env_off[e]), int(sc.env_off[e + 1])))
+
+
+def _sah_cost(nodes, refs, leaf_face, lo_t, hi_t, ci=1.2, ct=1.0):
+    def area(lo, hi):
+        d = hi - lo
+        return d[0] * d[1] + d[1] * d[2] + d[2] * d[0]
+
+    def rec(ref):
+        if ref < 0:
+            f = leaf_face[~ref]
+            return ct * area(lo_t[f], hi_t[f]), lo_t[f], hi_t[f]
+        c0, l0, h0 = rec(refs[ref, 0])
+        c1, l1, h1 = rec(refs[ref, 1])
+        lo, hi = np.minimum(l0, l1), np.maximum(h0, h1)
+        return ci * area(lo, hi) + c0 + c1, lo, hi
+
+    c, lo, hi = rec(0)
+    return c / area(lo, hi)
+
+
+@pytest.mark.parametrize("mesh_fn", [lambda: sg.tree_mesh(np.random.default_rng(1)),
+                                     lambda: sg.rock_mesh(np.random.default_rng(2)),
+                                     lambda: sg.sphere_mesh(1.0, 3)])
+def test_trbvh_keeps_leaves_and_boxes_and_lowers_sah(mesh_fn):
+    """Treelet restructuring (f3 BLAS quality): every face still in exactly one
+    leaf, every child box the exact union of its subtree, BVH4 consistent, and
+    the SAH cost of the binary tree lower than the plain LBVH's."""
+    mesh = mesh_fn()
+    tri = mesh.verts[mesh.faces]
+    lo_t, hi_t = tri.min(1).astype(np.float64), tri.max(1).astype(np.float64)
+    costs = {}
+    for rounds in (0, 3):
+        sc = sg.assemble([mesh], [[(0, 0, sg.make_T(np.eye(3), (0, 0, 0)))]])
+        s = make_scene(sc, build=False, trbvh_rounds=rounds)
+        nodes, leaf_face, _ = s.debug_export_blas(0)
+        refs = nodes[:, 12:14].view(np.int32)
+        seen = []
+
+        def walk(ref):
+            if ref < 0:
+                seen.append(leaf_face[~ref])
+                f = leaf_face[~ref]
+                return lo_t[f], hi_t[f]
+            l0, h0 = walk(refs[ref, 0])
+            l1, h1 = walk(refs[ref, 1])
+            nd = nodes[ref]
+            assert np.array_equal(nd[[0, 2, 4]], l0) and np.array_equal(nd[[1, 3, 5]], h0)
+            assert np.array_equal(nd[[6, 8, 10]], l1) and np.array_equal(nd[[7, 9, 11]], h1)
+            return np.minimum(l0, l1), np.maximum(h0, h1)
+
+        walk(0)
+        assert sorted(seen) == list(range(len(mesh.faces)))
+        b4, root = s.debug_export_bvh4(0)
+        assert sorted(_walk_bvh4(b4, root)) == list(range(len(mesh.faces)))
+        costs[rounds] = _sah_cost(nodes, refs, leaf_face, lo_t, hi_t)
+    assert costs[3] < costs[0] * 0.97, costs
