@@ -71,6 +71,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-counters", action="store_true")
+    ap.add_argument("--trbvh-rounds", type=int, default=3,
+                    help="treelet-restructuring passes on each BLAS (0 = plain LBVH)")
     ap.add_argument("--traversal", default="auto", choices=["auto", "lane"],
                     help="auto: warp packets for camera / LiDAR tiles; lane: one ray per lane")
     return ap.parse_args()
@@ -248,7 +250,7 @@ def main():
     sc, sensor = make_workload(cfg, E, env_base(rank, E))  # this rank's block of global envs
     kind = agr.AGR_RANGE if cfg == 4 else agr.AGR_DEPTH
     chans = channels_for(cfg)
-    scene = agr.Scene.from_scenegen(sc, device=local)
+    scene = agr.Scene.from_scenegen(sc, device=local, trbvh_rounds=args.trbvh_rounds)
     scene.set_traversal(0 if args.traversal == "auto" else 1)
     rpe = rays_per_env(sensor)
     rays_per_step = E * rpe
