@@ -555,6 +555,7 @@ __device__ __forceinline__ void traverse_packet(const SceneView& sv, int env, Ra
             sort4(key, ref);
             // push the farther children, farthest first
             if (sp + 3 <= PSTACK) {
+                __syncwarp();  // every lane has read the slots before they are reused
                 if (leader) {
                     int q = sp;
                     if (nh > 3) wstack[q++] = ref[3];
@@ -579,6 +580,7 @@ __device__ __forceinline__ void traverse_packet(const SceneView& sv, int env, Ra
         if (rs.cur_inst < 0) {
             if (COUNT) cnt.insts++;
             if (sp < PSTACK) {
+                __syncwarp();  // every lane has read the slot before it is reused
                 if (leader) wstack[sp] = SENTINEL;
                 ++sp;
             } else {
