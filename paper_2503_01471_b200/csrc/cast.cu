@@ -32,6 +32,12 @@ namespace {
 #define CAST_BLOCK 64
 #endif
 constexpr int CAST_THREADS = CAST_BLOCK;
+// Tile of one warp: TILE_W x TILE_H pixels (beams: columns x channels).
+#ifndef TILE_W
+#define TILE_W 4
+#endif
+constexpr int TILE_H = 32 / TILE_W;
+constexpr int TILE_CENTRE_LANE = (TILE_H / 2 - 1) * TILE_W + TILE_W / 2 - 1;
 // 32 resident warps per SM: 64 registers per thread
 #ifndef CAST_MIN_BLOCKS
 #define CAST_MIN_BLOCKS (1024 / CAST_BLOCK)
@@ -503,7 +509,7 @@ __device__ __forceinline__ void traverse_lane(const SceneView& sv, int env, RayS
 }
 
 // ---- packet traversal (pinhole / beams tiles) ------------------------------------
-// The 32 rays of an 8x4 tile traverse together: the warp visits a node if any
+// The 32 rays of a 4x8 tile (TILE_W x TILE_H) traverse together: the warp visits a node if any
 // lane's ray hits it (ballot), descends first into the child most lanes reach
 // first, and keeps ONE stack per warp in shared memory.  Control flow is
 // warp-uniform (no divergence in the traversal loop); every node / triangle
@@ -545,11 +551,11 @@ __device__ __forceinline__ void traverse_packet(const SceneView& sv, int env, Ra
                 continue;
             }
             // order the children by the entry distance of the tile's centre
-            // ray (lane 11: column 3, row 1), misses last
+            // ray (TILE_CENTRE_LANE), misses last
             unsigned key[4];
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-                const unsigned kc = __shfl_sync(FULL, __float_as_uint(tn[k]), 11);
+                const unsigned kc = __shfl_sync(FULL, __float_as_uint(tn[k]), TILE_CENTRE_LANE);
                 key[k] = (cm >> k) & 1u ? kc : KEY_MISS;
             }
             sort4(key, ref);
@@ -835,7 +841,7 @@ __device__ __forceinline__ RayId ray_id(const CastArgs& a) {
         id.out = (int64_t)(e - a.out_env_base) * a.R + (id.active ? r : 0);
         return id;
     }
-    const int tiles_x = (a.W + 7) >> 3, tiles_y = (a.H + 3) >> 2;
+    const int tiles_x = (a.W + TILE_W - 1) / TILE_W, tiles_y = (a.H + TILE_H - 1) / TILE_H;
     const int64_t tiles_img = (int64_t)tiles_x * tiles_y;
     const int64_t warp = (int64_t)blockIdx.x * (CAST_THREADS / 32) + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
@@ -844,8 +850,8 @@ __device__ __forceinline__ RayId ray_id(const CastArgs& a) {
     const int ty = tile / tiles_x, tx = tile - ty * tiles_x;
     id.env = a.env_begin + (int)(img / a.S);
     id.sensor = (int)(img % a.S);
-    id.col = tx * 8 + (lane & 7);
-    id.row = ty * 4 + (lane >> 3);
+    id.col = tx * TILE_W + (lane % TILE_W);
+    id.row = ty * TILE_H + (lane / TILE_W);
     id.active = id.env < a.env_end && id.col < a.W && id.row < a.H;
     id.out = (((int64_t)(id.env - a.out_env_base) * a.S + id.sensor) * a.H + id.row) * a.W + id.col;
     return id;
@@ -963,7 +969,7 @@ cudaError_t launch_model(const CastArgs& a, cudaStream_t stream) {
     if (MODEL == 0) {
         blocks = (int64_t)n_envs * ((a.R + CAST_THREADS - 1) / CAST_THREADS);
     } else {
-        int64_t tiles = (int64_t)((a.W + 7) >> 3) * ((a.H + 3) >> 2) * n_envs * a.S;
+        int64_t tiles = (int64_t)((a.W + TILE_W - 1) / TILE_W) * ((a.H + TILE_H - 1) / TILE_H) * n_envs * a.S;
         blocks = (tiles + CAST_THREADS / 32 - 1) / (CAST_THREADS / 32);
     }
     if (blocks <= 0) return cudaSuccess;
