@@ -73,6 +73,12 @@ def parse():
     ap.add_argument("--no-counters", action="store_true")
     ap.add_argument("--trbvh-rounds", type=int, default=3,
                     help="treelet-restructuring passes on each BLAS (0 = plain LBVH)")
+    ap.add_argument("--tlas-builder", default=None, choices=["lbvh", "sah"],
+                    help="TLAS builder for agr_build (default: sah for the static c3/c4 "
+                         "scenes, lbvh for c5, whose TLAS is rebuilt every step)")
+    ap.add_argument("--tlas-step", default=None, choices=["build", "refit"],
+                    help="per-step TLAS update (default: refit for c3/c4, whose obstacles "
+                         "keep their poses; rebuild for c5, re-posed every step)")
     ap.add_argument("--traversal", default="auto", choices=["auto", "lane"],
                     help="auto: warp packets for camera / LiDAR tiles; lane: one ray per lane")
     return ap.parse_args()
@@ -252,6 +258,9 @@ def main():
     chans = channels_for(cfg)
     scene = agr.Scene.from_scenegen(sc, device=local, trbvh_rounds=args.trbvh_rounds)
     scene.set_traversal(0 if args.traversal == "auto" else 1)
+    tlas_builder = args.tlas_builder or ("lbvh" if cfg == 5 else "sah")
+    scene.set_tlas_builder(1 if tlas_builder == "sah" else 0)
+    step_refit = (args.tlas_step or ("build" if cfg == 5 else "refit")) == "refit"
     rpe = rays_per_env(sensor)
     rays_per_step = E * rpe
     # inputs resident in HBM before timing
@@ -273,7 +282,7 @@ def main():
 
     def step(k):
         scene.set_instance_transforms(T_steps[k % len(T_steps)], stream)
-        if cfg == 5:
+        if step_refit:
             scene.refit(stream)
         else:
             scene.build(stream)
@@ -299,7 +308,7 @@ def main():
             e0, e1, e2 = ev[k]
             e0.record(stream)
             scene.set_instance_transforms(T_steps[k % len(T_steps)], stream)
-            if cfg == 5:
+            if step_refit:
                 scene.refit(stream)
             else:
                 scene.build(stream)
@@ -345,7 +354,7 @@ def main():
 
         def e2e_step(k):
             scene.set_instance_transforms(T_steps[k % len(T_steps)], stream)
-            scene.refit(stream) if cfg == 5 else scene.build(stream)
+            scene.refit(stream) if step_refit else scene.build(stream)
             stream.synchronize()
             if beams_h is None:
                 scene.cast_pinhole_host(sensor["cam"], poses_h, sensor["max_range"], kind, out=out_h)
@@ -418,8 +427,9 @@ def main():
         "data": "synthetic",
         "config": {"workload": WORKLOADS[cfg], "envs_per_gpu": E, "rays_per_step_per_gpu": rays_per_step,
                    "channels": list(chans), "parallelism": f"env-sharded x{world}",
-                   "l2": "flushed between timed steps (256 MB write, untimed); step = "
-                         "set_transforms + TLAS " + ("refit" if cfg == 5 else "build") + " + cast"},
+                   "l2": "flushed between timed steps (256 MB write, untimed)",
+                   "step": "set_instance_transforms + TLAS " + ("refit" if step_refit else "rebuild") +
+                           " + cast (TLAS builder: " + tlas_builder + ")"},
         "env_frames_per_sec": E * poses.shape[1] * world / (ms_per_step / 1e3),
         "cast_ms_per_step": cast_total / args.steps,
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,

@@ -80,6 +80,10 @@ def _load():
                                      ctypes.c_void_p, ctypes.c_int64, ctypes.c_double,
                                      ctypes.c_int32] + [ctypes.c_void_p] * 11
         _lib.oracle_last_tests.restype = ctypes.c_int64
+        _lib.oracle_certify.restype = ctypes.c_int
+        _lib.oracle_certify.argtypes = [ctypes.POINTER(_Scene), ctypes.POINTER(_Rays),
+                                        ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
+                                        ctypes.c_int32] + [ctypes.c_void_p] * 3
     return _lib
 
 
@@ -114,6 +118,54 @@ def cast(scene, rays: dict, query=None, n_threads: int = 0, amb_eps: float = AMB
     ``stereo``: (offset xyz in the sensor frame, eps) -> also the shadow mask.
     """
     lib = _load()
+    sc, r, keep, total = _marshal(scene, rays)
+    if query is None:
+        query = np.arange(total, dtype=np.int64)
+    q = np.ascontiguousarray(query, dtype=np.int64)
+    n = len(q)
+    out = OracleResult(np.empty(n, np.float64), np.empty(n, np.float32),
+                       np.empty(n, np.int32), np.empty(n, np.int32),
+                       np.empty(n, np.int32), np.empty(n, np.float64),
+                       np.full(n, np.inf), 0)
+    if stereo is not None:
+        (r.stereo[0], r.stereo[1], r.stereo[2]), r.stereo_eps = stereo[0], stereo[1]
+        out.valid = np.empty(n, np.int32)
+    if extras:
+        out.normal = np.empty((n, 3), np.float64)
+        out.bary = np.empty((n, 2), np.float64)
+        out.point = np.empty((n, 3), np.float64)
+    rc = lib.oracle_cast(ctypes.byref(sc), ctypes.byref(r), _ptr(q), n, amb_eps, n_threads,
+                         _ptr(out.t64), _ptr(out.dist), _ptr(out.seg), _ptr(out.face),
+                         _ptr(out.amb), _ptr(out.t2), _ptr(out.graze) if graze else None,
+                         _ptr(out.normal), _ptr(out.bary), _ptr(out.point), _ptr(out.valid))
+    if rc != 0:
+        raise ValueError("oracle_cast rejected its input")
+    out.tests = int(lib.oracle_last_tests())
+    return out
+
+
+def certify(scene, rays: dict, face, query=None, n_threads: int = 0):
+    """Certificate of reported faces (oracle.h oracle_certify): returns
+    ``(t_face, outside, label)`` -- the FP64 plane-hit t of each reported face,
+    how far that hit lies outside the face (<= 0 inside) and its label."""
+    lib = _load()
+    sc, r, keep, total = _marshal(scene, rays)
+    if query is None:
+        query = np.arange(total, dtype=np.int64)
+    q = np.ascontiguousarray(query, dtype=np.int64)
+    f = np.ascontiguousarray(face, dtype=np.int32).reshape(-1)
+    if len(f) != len(q):
+        raise ValueError("one face per queried ray")
+    n = len(q)
+    t_face, outside, label = np.empty(n, np.float64), np.empty(n, np.float64), np.empty(n, np.int32)
+    rc = lib.oracle_certify(ctypes.byref(sc), ctypes.byref(r), _ptr(q), n, _ptr(f), n_threads,
+                            _ptr(t_face), _ptr(outside), _ptr(label))
+    if rc != 0:
+        raise ValueError("oracle_certify rejected its input")
+    return t_face, outside, label
+
+
+def _marshal(scene, rays):
     keep = []
 
     def arr(x, dt):
@@ -150,26 +202,4 @@ def cast(scene, rays: dict, query=None, n_threads: int = 0, amb_eps: float = AMB
             b = arr(rays["beams"], np.float32)
             r.beams, r.C, r.K = _ptr(b), b.shape[0], b.shape[1]
             total = n_envs * r.S * r.C * r.K
-    if query is None:
-        query = np.arange(total, dtype=np.int64)
-    q = arr(query, np.int64)
-    n = len(q)
-    out = OracleResult(np.empty(n, np.float64), np.empty(n, np.float32),
-                       np.empty(n, np.int32), np.empty(n, np.int32),
-                       np.empty(n, np.int32), np.empty(n, np.float64),
-                       np.full(n, np.inf), 0)
-    if stereo is not None:
-        (r.stereo[0], r.stereo[1], r.stereo[2]), r.stereo_eps = stereo[0], stereo[1]
-        out.valid = np.empty(n, np.int32)
-    if extras:
-        out.normal = np.empty((n, 3), np.float64)
-        out.bary = np.empty((n, 2), np.float64)
-        out.point = np.empty((n, 3), np.float64)
-    rc = lib.oracle_cast(ctypes.byref(sc), ctypes.byref(r), _ptr(q), n, amb_eps, n_threads,
-                         _ptr(out.t64), _ptr(out.dist), _ptr(out.seg), _ptr(out.face),
-                         _ptr(out.amb), _ptr(out.t2), _ptr(out.graze) if graze else None,
-                         _ptr(out.normal), _ptr(out.bary), _ptr(out.point), _ptr(out.valid))
-    if rc != 0:
-        raise ValueError("oracle_cast rejected its input")
-    out.tests = int(lib.oracle_last_tests())
-    return out
+    return sc, r, keep, total

@@ -400,3 +400,98 @@ int oracle_cast(const oracle_scene* sc, const oracle_rays* r,
     free(jobs); free(th); free(count); free(order);
     return status;
 }
+
+/* ---- certificate of a reported face (SURVEY.md §8(c) "Full-scale
+ * certificate"): for ray id query[q] and the face reported for it, the FP64
+ * plane-hit t of that face of M_{e,t}, how far (scene units)
+ * the plane hit lies outside the face (<= 0: inside), and the face's label.
+ * Costs one triangle per ray, so it runs on every ray of a full-size cast. */
+typedef struct {
+    const oracle_scene* sc;
+    const oracle_rays* r;
+    const int64_t* query;
+    const int64_t* order;
+    const int32_t* face;
+    int64_t lo, hi;
+    double* t_face; double* outside; int32_t* label;
+    int status;
+} cert_job;
+
+static void* cert_worker(void* arg) {
+    cert_job* jb = (cert_job*)arg;
+    world_mesh w = {0, NULL, NULL, 0};
+    int64_t cur_env = -1;
+    jb->status = 0;
+    for (int64_t i = jb->lo; i < jb->hi; ++i) {
+        int64_t q = jb->order[i];
+        int64_t id = jb->query[q];
+        int32_t f = jb->face[q];
+        jb->t_face[q] = NAN;
+        jb->outside[q] = INFINITY;
+        jb->label[q] = -1;
+        if (f < 0) continue;
+        int64_t e = query_env(jb->r, id);
+        if (e != cur_env) {
+            if (world_triangles(jb->sc, (int32_t)e, &w) != 0) { jb->status = -1; break; }
+            cur_env = e;
+        }
+        if (f >= w.n_tri) continue;
+        v3 o, d;
+        make_ray(jb->r, id, &o, &d);
+        v3 a = w.v[3 * f], b = w.v[3 * f + 1], c = w.v[3 * f + 2];
+        v3 n = vcross(vsub(b, a), vsub(c, a));
+        double denom = vdot(n, d);
+        jb->label[q] = w.label[f];
+        if (denom == 0.0) continue;
+        double t = vdot(n, vsub(a, o)) / denom;
+        v3 p = {o.x + t * d.x, o.y + t * d.y, o.z + t * d.z};
+        double nn = vnorm(n), out_d = -INFINITY, s;
+        s = -vdot(vcross(vsub(b, a), vsub(p, a)), n) / (nn * vnorm(vsub(b, a))); if (s > out_d) out_d = s;
+        s = -vdot(vcross(vsub(c, b), vsub(p, b)), n) / (nn * vnorm(vsub(c, b))); if (s > out_d) out_d = s;
+        s = -vdot(vcross(vsub(a, c), vsub(p, c)), n) / (nn * vnorm(vsub(a, c))); if (s > out_d) out_d = s;
+        jb->t_face[q] = t;
+        jb->outside[q] = out_d;
+    }
+    free(w.v);
+    free(w.label);
+    return NULL;
+}
+
+int oracle_certify(const oracle_scene* sc, const oracle_rays* r, const int64_t* query,
+                   int64_t n_query, const int32_t* face, int32_t n_threads,
+                   double* t_face, double* outside, int32_t* label) {
+    if (validate(sc, r) != 0) return -1;
+    int64_t n_rays_total;
+    if (r->model == ORACLE_RAYS) n_rays_total = (int64_t)sc->n_envs * r->R;
+    else if (r->model == ORACLE_PINHOLE) n_rays_total = (int64_t)sc->n_envs * r->S * r->H * r->W;
+    else n_rays_total = (int64_t)sc->n_envs * r->S * r->C * r->K;
+    for (int64_t q = 0; q < n_query; ++q)
+        if (query[q] < 0 || query[q] >= n_rays_total) return -1;
+    int64_t* count = (int64_t*)calloc((size_t)sc->n_envs + 1, sizeof(int64_t));
+    int64_t* order = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n_query > 0 ? n_query : 1));
+    if (!count || !order) { free(count); free(order); return -1; }
+    for (int64_t q = 0; q < n_query; ++q) count[query_env(r, query[q]) + 1]++;
+    for (int32_t e = 0; e < sc->n_envs; ++e) count[e + 1] += count[e];
+    for (int64_t q = 0; q < n_query; ++q) order[count[query_env(r, query[q])]++] = q;
+    if (n_threads <= 0) n_threads = (int32_t)sysconf(_SC_NPROCESSORS_ONLN);
+    if (n_threads < 1) n_threads = 1;
+    if (n_threads > n_query) n_threads = (int32_t)(n_query > 0 ? n_query : 1);
+    cert_job* jobs = (cert_job*)calloc((size_t)n_threads, sizeof(cert_job));
+    pthread_t* th = (pthread_t*)calloc((size_t)n_threads, sizeof(pthread_t));
+    int status = 0;
+    for (int32_t i = 0; i < n_threads; ++i) {
+        cert_job* jb = &jobs[i];
+        jb->sc = sc; jb->r = r; jb->query = query; jb->order = order; jb->face = face;
+        jb->lo = n_query * i / n_threads;
+        jb->hi = n_query * (i + 1) / n_threads;
+        jb->t_face = t_face; jb->outside = outside; jb->label = label;
+        if (n_threads == 1) cert_worker(jb);
+        else if (pthread_create(&th[i], NULL, cert_worker, jb) != 0) { jb->status = -1; th[i] = 0; }
+    }
+    for (int32_t i = 0; i < n_threads; ++i) {
+        if (n_threads > 1 && th[i]) pthread_join(th[i], NULL);
+        if (jobs[i].status != 0) status = -1;
+    }
+    free(jobs); free(th); free(count); free(order);
+    return status;
+}

@@ -118,6 +118,23 @@ int oracle_cast(const oracle_scene* scene, const oracle_rays* rays,
                 int32_t* amb, double* t2, double* graze,
                 double* normal, double* bary, double* point, int32_t* valid);
 
+/*
+ * Certificate of a reported face (SURVEY.md §8(c) "Full-scale certificate",
+ * one triangle per ray, so it covers every ray of a full-size cast): for ray
+ * query[q] and face[q] (per-env face index, -1 = miss), writes
+ *   t_face[q]  FP64 plane-hit t of that face (NaN on a miss or when the ray
+ *              is parallel to the face's plane)
+ *   outside[q] how far (scene units) that plane hit lies outside the face:
+ *              max over the three edges of the signed distance, <= 0 inside
+ *              (+inf on a miss)
+ *   label[q]   label of the face's instance (-1 on a miss)
+ * It proves the hit is real and its distance right; optimality (no closer
+ * face) is oracle_cast's job on samples.  Returns 0, or -1 on bad input.
+ */
+int oracle_certify(const oracle_scene* scene, const oracle_rays* rays,
+                   const int64_t* query, int64_t n_query, const int32_t* face,
+                   int32_t n_threads, double* t_face, double* outside, int32_t* label);
+
 /* Number of triangle tests the last oracle_cast call performed (for the
  * cpu_baseline report: ray-triangle tests/s). */
 int64_t oracle_last_tests(void);

@@ -841,17 +841,20 @@ __device__ __forceinline__ RayId ray_id(const CastArgs& a) {
         id.out = (int64_t)(e - a.out_env_base) * a.R + (id.active ? r : 0);
         return id;
     }
-    const int tiles_x = (a.W + TILE_W - 1) / TILE_W, tiles_y = (a.H + TILE_H - 1) / TILE_H;
-    const int64_t tiles_img = (int64_t)tiles_x * tiles_y;
-    const int64_t warp = (int64_t)blockIdx.x * (CAST_THREADS / 32) + (threadIdx.x >> 5);
+    // 32-bit index math: a launch covers < 2^32 warps (grid.x < 2^31 blocks
+    // of CAST_THREADS / 32 = 2 warps) and tiles_img < 2^31 (cast_launch)
+    const unsigned tiles_x = (unsigned)(a.W + TILE_W - 1) / TILE_W;
+    const unsigned tiles_img = tiles_x * (unsigned)((a.H + TILE_H - 1) / TILE_H);
+    const unsigned warp = blockIdx.x * (unsigned)(CAST_THREADS / 32) + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
-    const int64_t img = warp / tiles_img;
-    const int tile = (int)(warp - img * tiles_img);
-    const int ty = tile / tiles_x, tx = tile - ty * tiles_x;
-    id.env = a.env_begin + (int)(img / a.S);
-    id.sensor = (int)(img % a.S);
-    id.col = tx * TILE_W + (lane % TILE_W);
-    id.row = ty * TILE_H + (lane / TILE_W);
+    const unsigned img = warp / tiles_img;
+    const unsigned tile = warp - img * tiles_img;
+    const unsigned ty = tile / tiles_x, tx = tile - ty * tiles_x;
+    const unsigned env_rel = a.S == 1 ? img : img / (unsigned)a.S;
+    id.env = a.env_begin + (int)env_rel;
+    id.sensor = (int)(img - env_rel * (unsigned)a.S);
+    id.col = (int)tx * TILE_W + (lane % TILE_W);
+    id.row = (int)ty * TILE_H + (lane / TILE_W);
     id.active = id.env < a.env_end && id.col < a.W && id.row < a.H;
     id.out = (((int64_t)(id.env - a.out_env_base) * a.S + id.sensor) * a.H + id.row) * a.W + id.col;
     return id;
@@ -969,7 +972,9 @@ cudaError_t launch_model(const CastArgs& a, cudaStream_t stream) {
     if (MODEL == 0) {
         blocks = (int64_t)n_envs * ((a.R + CAST_THREADS - 1) / CAST_THREADS);
     } else {
-        int64_t tiles = (int64_t)((a.W + TILE_W - 1) / TILE_W) * ((a.H + TILE_H - 1) / TILE_H) * n_envs * a.S;
+        const int64_t tiles_img = (int64_t)((a.W + TILE_W - 1) / TILE_W) * ((a.H + TILE_H - 1) / TILE_H);
+        if (tiles_img > 0x7FFFFFFF) return cudaErrorInvalidValue;  // ray_id's 32-bit math
+        int64_t tiles = tiles_img * n_envs * a.S;
         blocks = (tiles + CAST_THREADS / 32 - 1) / (CAST_THREADS / 32);
     }
     if (blocks <= 0) return cudaSuccess;

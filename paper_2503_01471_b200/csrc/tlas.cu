@@ -135,7 +135,7 @@ __device__ void sah_build_cta(const TlasSmem& s, int n) {
         k = __shfl_sync(FULL, k, 0);
         if (k >= n - 1) break;
         if (lane == 0)
-            while (vtask[4 * k + 2] == 0) { }
+            while (vtask[4 * k + 2] == 0) __nanosleep(64);  // leave the issue slots to the producer
         __syncwarp();
         __threadfence_block();
         const int start = vtask[4 * k], end = vtask[4 * k + 1];
@@ -154,28 +154,50 @@ __device__ void sah_build_cta(const TlasSmem& s, int n) {
                 clo[c] = fminf(clo[c], __shfl_xor_sync(FULL, clo[c], o));
                 chi[c] = fmaxf(chi[c], __shfl_xor_sync(FULL, chi[c], o));
             }
+        float scale[3];
+        for (int c = 0; c < 3; ++c) {
+            const float ext = chi[c] - clo[c];
+            scale[c] = ext > 0.0f ? (float)SAH_BINS / ext : 0.0f;
+        }
         auto bin_of = [&](int item, int axis) {
             const float* b = s.box + 6 * item;
             const float x = 0.5f * b[axis] + 0.5f * b[3 + axis];
-            const float ext = chi[axis] - clo[axis];
             if (!isfinite(x)) return SAH_BINS - 1;
-            if (!(ext > 0.0f)) return 0;
-            int bi = (int)((x - clo[axis]) / ext * (float)SAH_BINS);
+            const int bi = (int)((x - clo[axis]) * scale[axis]);
             return bi < 0 ? 0 : (bi >= SAH_BINS ? SAH_BINS - 1 : bi);
         };
-        // per (axis, bin) count and box: lane owns pairs lane, lane + 32
+        // per (axis, bin) count and box: each lane bins its items with
+        // shared-memory atomics (boxes as order-preserving integers)
+        unsigned* ub = reinterpret_cast<unsigned*>(&bins[w][0][0]);
         for (int pp = lane; pp < 3 * SAH_BINS; pp += 32) {
-            const int axis = pp / SAH_BINS, bi = pp % SAH_BINS;
-            float cnt = 0.0f, bl[3] = {FLT_MAX, FLT_MAX, FLT_MAX}, bh[3] = {-FLT_MAX, -FLT_MAX, -FLT_MAX};
-            for (int i = start; i < end; ++i) {
-                const int it = perm[i];
-                if (bin_of(it, axis) != bi) continue;
-                const float* b = s.box + 6 * it;
-                cnt += 1.0f;
-                for (int c = 0; c < 3; ++c) { bl[c] = fminf(bl[c], b[c]); bh[c] = fmaxf(bh[c], b[3 + c]); }
+            ub[7 * pp] = 0u;
+            for (int c = 0; c < 3; ++c) {
+                ub[7 * pp + 1 + c] = float_to_ordered(FLT_MAX);
+                ub[7 * pp + 4 + c] = float_to_ordered(-FLT_MAX);
             }
-            bins[w][pp][0] = cnt;
-            for (int c = 0; c < 3; ++c) { bins[w][pp][1 + c] = bl[c]; bins[w][pp][4 + c] = bh[c]; }
+        }
+        __syncwarp();
+        for (int i = start + lane; i < end; i += 32) {
+            const int it = perm[i];
+            const float* b = s.box + 6 * it;
+            unsigned lo_o[3], hi_o[3];
+            for (int c = 0; c < 3; ++c) {
+                lo_o[c] = float_to_ordered(b[c]);
+                hi_o[c] = float_to_ordered(b[3 + c]);
+            }
+            for (int axis = 0; axis < 3; ++axis) {
+                unsigned* bb = ub + 7 * (axis * SAH_BINS + bin_of(it, axis));
+                atomicAdd(bb, 1u);
+                for (int c = 0; c < 3; ++c) {
+                    atomicMin(bb + 1 + c, lo_o[c]);
+                    atomicMax(bb + 4 + c, hi_o[c]);
+                }
+            }
+        }
+        __syncwarp();
+        for (int pp = lane; pp < 3 * SAH_BINS; pp += 32) {
+            bins[w][pp][0] = (float)ub[7 * pp];
+            for (int c = 0; c < 6; ++c) bins[w][pp][1 + c] = ordered_to_float(ub[7 * pp + 1 + c]);
         }
         __syncwarp();
         // SAH sweep per axis (lanes 0..2): split after bin p, p = 0..SAH_BINS-2

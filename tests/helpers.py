@@ -91,3 +91,45 @@ def compare_extras(ref: "oracle.OracleResult", normal=None, bary=None, point=Non
     if msgs:
         raise AssertionError("\n".join(msgs))
     return int(same.sum())
+
+
+# SURVEY.md §8(c) "Full-scale certificate": the reported hit lies on the
+# reported face within the 1e-5 m parity band.
+CERT_BAND = 1e-5
+
+
+def certify_all(sc, sensor, kind, dist, seg, face, what="", env_chunk=64):
+    """Certificate of EVERY ray of a full-size cast: for
+    each hit, the oracle's FP64 plane-hit t of the reported face equals the
+    reported distance within the parity tolerance, the hit lies on that face
+    (within CERT_BAND), and seg is that face's label; each miss reports
+    max_range, -1, -1.  Optimality (no closer face) is checked by oracle.cast
+    on samples.  Returns the number of certified hits."""
+    rays = oracle_rays(sensor, kind)
+    n_env = len(sc.env_off) - 1
+    per_env = len(dist) // n_env
+    max_range = np.float32(sensor["max_range"])
+    hits = 0
+    for e0 in range(0, n_env, env_chunk):
+        e1 = min(n_env, e0 + env_chunk)
+        q = np.arange(e0 * per_env, e1 * per_env, dtype=np.int64)
+        d, s, f = dist[q].astype(np.float64), seg[q], face[q]
+        miss = f < 0
+        bad = np.nonzero(miss & ((dist[q] != max_range) | (s != -1)))[0]
+        assert len(bad) == 0, f"{what}: miss #{q[bad[0]]} reports {dist[q][bad[0]]!r}/{s[bad[0]]}"
+        t_face, outside, label = oracle.certify(sc, rays, f, query=q)
+        h = ~miss
+        tol = np.maximum(DIST_ABS, DIST_REL * np.abs(t_face))
+        with np.errstate(invalid="ignore"):
+            bad_t = np.nonzero(h & ~(np.abs(d - t_face) <= tol))[0]
+            bad_in = np.nonzero(h & ~(outside <= CERT_BAND))[0]
+            bad_rng = np.nonzero(h & ~((t_face > 0) & (t_face <= max_range + DIST_ABS)))[0]
+        bad_seg = np.nonzero(h & (label != s))[0]
+        for name, b, info in (("distance", bad_t, t_face), ("on-face", bad_in, outside),
+                              ("range", bad_rng, t_face), ("label", bad_seg, label)):
+            if len(b):
+                i = b[0]
+                raise AssertionError(f"{what}: {len(b)} {name} certificate failures; first ray "
+                                     f"{q[i]}: dist={d[i]!r} face={f[i]} seg={s[i]} oracle={info[i]!r}")
+        hits += int(h.sum())
+    return hits

@@ -640,3 +640,52 @@ def test_stereo_post_shadow_band_closed_form(baseline):
     assert (shadow & on_wall).sum() >= 3
     # the post itself is seen by both cameras: valid
     assert np.all(r.valid[row][r.seg[row] == 2] == 1)
+
+
+# --------------------------------------------------------------------------
+# certificate of a reported face (oracle.certify)
+# --------------------------------------------------------------------------
+
+def test_certify_single_triangle_closed_form():
+    """One triangle in the plane x = 5 with legs along +y and +z: the ray
+    through (5, y, z) has t = 1 (direction (5, y, z)), and the plane hit lies
+    outside the face by max(-y, -z, (y + z - 1)/sqrt 2) (signed distances to
+    the three edges)."""
+    v = np.asarray([[5, 0, 0], [5, 1, 0], [5, 0, 1]], np.float32)
+    m = sg.Mesh("tri", v, np.asarray([[0, 1, 2]], np.int32))
+    sc = sg.assemble([m, m], [[(0, 7, sg.make_T(np.eye(3), (0, 0, 0))),
+                               (1, 9, sg.make_T(np.eye(3), (2.0, 0, 0)))]])
+    pts = np.asarray([[0.25, 0.25], [0.8, 0.6], [-0.1, 0.3], [0.0, 0.0], [0.5, 0.5]])
+    d = np.concatenate([np.full((len(pts), 1), 5.0), pts], 1)[None].astype(np.float32)
+    o = np.zeros_like(d)
+    rays = dict(model=oracle.RAYS, orig=o, dir=d, max_range=100.0)
+    t, out, lab = oracle.certify(sc, rays, np.zeros(len(pts), np.int32))
+    def want_out(k):  # the hit is (5k, k y, k z) on a face with unit legs
+        return np.maximum(np.maximum(-k * pts[:, 0], -k * pts[:, 1]), (k * pts.sum(1) - 1) / math.sqrt(2))
+    assert np.allclose(t, 1.0, atol=1e-15)
+    assert np.allclose(out, want_out(1.0), atol=1e-7)  # FP32 direction inputs
+    assert np.all(lab == 7)
+    # face 1 is the second instance's copy at x = 7: t = 7/5, label 9
+    t1, out1, lab1 = oracle.certify(sc, rays, np.ones(len(pts), np.int32))
+    assert np.allclose(t1, 1.4, atol=1e-14) and np.all(lab1 == 9)
+    assert np.allclose(out1, want_out(1.4), atol=1e-7)
+    # a miss certifies nothing
+    tm, outm, labm = oracle.certify(sc, rays, np.full(len(pts), -1, np.int32))
+    assert np.all(np.isnan(tm)) and np.all(np.isinf(outm)) and np.all(labm == -1)
+
+
+def test_certify_agrees_with_cast_on_its_own_answer():
+    """On the oracle's own winners (random c2-like scene, 2 envs) the
+    certificate reproduces t exactly (same FP64 plane formula), finds every
+    hit inside its face and returns the cast's seg."""
+    sc, s = sg.config2(n_envs=2)
+    cam = sg.pinhole(24, 16, 87.0)
+    rays = dict(model=oracle.PINHOLE, kind=oracle.RANGE, poses=s["poses"], max_range=10.0, **cam)
+    r = oracle.cast(sc, rays)
+    t, out, lab = oracle.certify(sc, rays, r.face)
+    hit = r.face >= 0
+    assert hit.sum() > 50
+    assert np.array_equal(t[hit], r.t64[hit])
+    assert np.all(out[hit] <= 1e-12)
+    assert np.array_equal(lab, r.seg)
+    assert np.all(np.isnan(t[~hit]))

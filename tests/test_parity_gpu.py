@@ -16,7 +16,7 @@ import torch
 import oracle
 import paper_2503_01471_b200 as agr
 import scenegen as sg
-from helpers import compare, compare_extras, oracle_rays
+from helpers import certify_all, compare, compare_extras, oracle_rays
 from gpu_util import cast_sensor, dev, make_scene, to_np
 
 pytestmark = pytest.mark.gpu
@@ -271,12 +271,15 @@ def test_c3_full_size_sampled():
     assert 0.3 < hit.mean() < 0.99
     # every output is either max range or a plausible depth
     assert np.all((got["dist"] > 0) & (got["dist"] <= 10.0))
+    # every one of the 132.7 M rays: the reported hit is on the reported face
+    assert certify_all(sc, sensor, "depth", got["dist"], got["seg"], got["face"], "c3") == hit.sum()
 
 
 @pytest.mark.slow
 def test_c4_full_size_sampled():
     sc, sensor = sg.config4()
-    _sampled(sc, sensor, "range", 40000, 4, "c4")
+    _, got = _sampled(sc, sensor, "range", 40000, 4, "c4")
+    certify_all(sc, sensor, "range", got["dist"], got["seg"], got["face"], "c4")
 
 
 @pytest.mark.slow
@@ -294,6 +297,7 @@ def test_c5_sampled_with_refit_steps():
         sc2 = sg.Scene(sc.meshes, sc.env_off, sc.inst_asset, sc.inst_label, ring[step])
         ref = oracle.cast(sc2, oracle_rays(sensor, "depth"), query=q)
         compare(ref, got["dist"][q], got["seg"][q], got["face"][q], f"c5 step {step}")
+        certify_all(sc2, sensor, "depth", got["dist"], got["seg"], got["face"], f"c5 step {step}")
 
 
 # ---- per-hit channels (normal, barycentrics, point cloud) -------------------
