@@ -201,6 +201,20 @@ agr_status agr_set_instance_transforms(agr_scene scene, const float* T, void* st
 agr_status agr_update_mesh(agr_scene scene, int32_t asset, const float* verts, int32_t n_verts,
                            void* stream);
 
+/*
+ * Batched agr_update_mesh: replace the vertices of the n distinct assets
+ * `assets` (host int32 [n]) with `verts` (device float [sum of their vertex
+ * counts][3], the assets' vertex arrays concatenated in the order of
+ * `assets`) and rebuild all n BLAS in ONE set of launches (the build's
+ * kernels run over the concatenated faces; each asset's tree is exactly the
+ * one agr_update_mesh would build).  This is the reset path for per-env
+ * unique meshes: n = number of envs being reset.
+ * EINVAL on n < 0, a NULL pointer with n > 0, an asset out of range or
+ * listed twice.  Async on `stream`; `assets` is read before return.
+ */
+agr_status agr_update_meshes(agr_scene scene, int32_t n, const int32_t* assets, const float* verts,
+                             void* stream);
+
 /* Full per-env TLAS rebuild (one CTA per env: LBVH -- Morton order + Karras
  * hierarchy -- or, after agr_set_tlas_builder(scene, 1), a binned-SAH
  * top-down split of the instance boxes), bottom-up fit and 4-wide collapse.

@@ -91,6 +91,7 @@ _SIGS = {
     "agr_set_instance_transforms": (_I32, [_P, _P, _P]),
     "agr_build": (_I32, [_P, _P]),
     "agr_update_mesh": (_I32, [_P, _I32, _P, _I32, _P]),
+    "agr_update_meshes": (_I32, [_P, _I32, _P, _P, _P]),
     "agr_refit": (_I32, [_P, _P]),
     "agr_cast_pinhole": (_I32, [_P, ctypes.POINTER(agr_pinhole), _I32, _P, _I32, ctypes.c_float,
                                 agr_outputs, _P]),
@@ -224,6 +225,14 @@ class Scene:
         """verts: CUDA float32 [V, 3] (same V as at create); rebuilds the BLAS."""
         _check(load().agr_update_mesh(self.handle, int(asset), _ptr(verts), int(verts.shape[0]),
                                       _stream_handle(stream)))
+
+    def update_meshes(self, assets, verts, stream=None):
+        """Batched update_mesh: ``assets`` a sequence of distinct asset ids,
+        ``verts`` CUDA float32 [sum V, 3] (their vertex arrays concatenated in
+        that order); all BLAS are rebuilt in one set of launches."""
+        a = np.ascontiguousarray(assets, dtype=np.int32)
+        _check(load().agr_update_meshes(self.handle, len(a), a.ctypes.data, _ptr(verts),
+                                        _stream_handle(stream)))
 
     def build(self, stream=None):
         _check(load().agr_build(self.handle, _stream_handle(stream)))

@@ -179,22 +179,28 @@ struct agr_scene_s {
 };
 
 // (Re)build asset a's BLAS from the device copy of its mesh (async on st).
-static cudaError_t build_asset(agr_scene_s* s, int a, cudaStream_t st) {
-    BlasBuildArgs ba;
-    ba.verts = s->mesh_verts + 3 * s->h_mvert_off[a];
-    ba.faces = s->mesh_faces + 3 * s->h_mface_off[a];
-    ba.n_verts = s->h_nverts[a];
-    ba.n_faces = s->h_nfaces[a];
-    ba.node_base = s->h_node_base[a];
-    ba.leaf_base = s->h_leaf_base[a];
+static cudaError_t build_assets(agr_scene_s* s, const int* assets, int n, cudaStream_t st) {
+    std::vector<BlasSeg> segs(n);
+    for (int k = 0; k < n; ++k) {
+        const int a = assets[k];
+        BlasSeg& g = segs[k];
+        g.verts = s->mesh_verts + 3 * s->h_mvert_off[a];
+        g.faces = s->mesh_faces + 3 * s->h_mface_off[a];
+        g.n_verts = s->h_nverts[a];
+        g.n_faces = s->h_nfaces[a];
+        g.off = 0;
+        g.node_base = s->h_node_base[a];
+        g.leaf_base = s->h_leaf_base[a];
+        g.info = s->assets + a;
+    }
+    BlasBatchArgs ba;
     ba.nodes = s->nodes;
     ba.bnodes = s->bnodes;
     ba.tris = s->tris;
     ba.triv = s->triv;
-    ba.info_dev = s->assets + a;
-    ba.dbg_morton = s->morton + s->h_leaf_base[a];
+    ba.dbg_morton = s->morton;
     ba.trbvh_rounds = s->trbvh_rounds;
-    return blas_build(ba, s->blas_scratch, nullptr, st);
+    return blas_build_batch(segs.data(), n, ba, s->blas_scratch, st);
 }
 
 static agr_status refresh_assets(agr_scene_s* s) {
@@ -343,16 +349,13 @@ agr_status agr_scene_create_ex(int32_t device, const agr_mesh* meshes, int32_t n
     CKB(cudaMemcpy(s->tlas_off, s->h_tlas_off.data(), sizeof(int) * n_envs, cudaMemcpyHostToDevice));
     CKB(cudaMemcpy(s->tlas_root, h_root.data(), sizeof(int) * n_envs, cudaMemcpyHostToDevice));
 
-    // BLAS build: all asset meshes stay on the device (for agr_update_mesh);
-    // one asset after the other on a private stream
+    // BLAS build: all asset meshes stay on the device (for agr_update_mesh),
+    // and every asset is built in one batch (one set of launches)
     cudaStream_t st;
     CKB(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-    size_t scratch_bytes = 0;
     s->h_mvert_off.assign(n_meshes + 1, 0);
     s->h_mface_off.assign(n_meshes + 1, 0);
     for (int a = 0; a < n_meshes; ++a) {
-        size_t b = blas_scratch_bytes(meshes[a].n_faces);
-        scratch_bytes = b > scratch_bytes ? b : scratch_bytes;
         s->h_mvert_off[a + 1] = s->h_mvert_off[a] + meshes[a].n_verts;
         s->h_mface_off[a + 1] = s->h_mface_off[a] + meshes[a].n_faces;
         s->h_nverts.push_back(meshes[a].n_verts);
@@ -362,7 +365,8 @@ agr_status agr_scene_create_ex(int32_t device, const agr_mesh* meshes, int32_t n
     s->h_leaf_base = leaf_base;
     CKB(s->alloc(&s->mesh_verts, 3 * (size_t)s->h_mvert_off[n_meshes]));
     CKB(s->alloc(&s->mesh_faces, 3 * (size_t)s->h_mface_off[n_meshes]));
-    CKB(s->alloc((char**)&s->blas_scratch, scratch_bytes));
+    // scratch for a batch of every asset (any update batch fits in it)
+    CKB(s->alloc((char**)&s->blas_scratch, blas_scratch_bytes(s->h_mface_off[n_meshes], n_meshes)));
     cudaError_t err = cudaSuccess;
     for (int a = 0; a < n_meshes && err == cudaSuccess; ++a) {
         err = cudaMemcpyAsync(s->mesh_verts + 3 * s->h_mvert_off[a], meshes[a].verts,
@@ -370,10 +374,12 @@ agr_status agr_scene_create_ex(int32_t device, const agr_mesh* meshes, int32_t n
         if (err != cudaSuccess) break;
         err = cudaMemcpyAsync(s->mesh_faces + 3 * s->h_mface_off[a], meshes[a].faces,
                               sizeof(int) * 3 * meshes[a].n_faces, cudaMemcpyHostToDevice, st);
-        if (err != cudaSuccess) break;
-        err = cudaStreamSynchronize(st);  // the host arrays are the caller's
-        if (err != cudaSuccess) break;
-        err = build_asset(s, a, st);
+    }
+    if (err == cudaSuccess) err = cudaStreamSynchronize(st);  // the host arrays are the caller's
+    if (err == cudaSuccess) {
+        std::vector<int> all(n_meshes);
+        for (int a = 0; a < n_meshes; ++a) all[a] = a;
+        err = build_assets(s, all.data(), n_meshes, st);
     }
     if (err == cudaSuccess) err = cudaStreamSynchronize(st);
     if (err != cudaSuccess) {
@@ -460,11 +466,30 @@ agr_status agr_update_mesh(agr_scene s, int32_t asset, const float* verts, int32
     if (asset < 0 || asset >= s->n_assets) return fail(AGR_EINVAL, "asset %d out of range", asset);
     if (!verts || n_verts != s->h_nverts[asset])
         return fail(AGR_EINVAL, "asset %d has %d vertices (got %d)", asset, s->h_nverts[asset], n_verts);
+    return agr_update_meshes(s, 1, &asset, verts, stream);
+}
+
+agr_status agr_update_meshes(agr_scene s, int32_t n, const int32_t* assets, const float* verts, void* stream) {
+    g_err.clear();
+    if (!s) return fail(AGR_EINVAL, "scene is NULL");
+    if (n == 0) return AGR_OK;
+    if (n < 0 || !assets || !verts) return fail(AGR_EINVAL, "need n > 0, assets and verts");
+    std::vector<char> seen(s->n_assets, 0);
+    for (int k = 0; k < n; ++k) {
+        if (assets[k] < 0 || assets[k] >= s->n_assets) return fail(AGR_EINVAL, "asset %d out of range", assets[k]);
+        if (seen[assets[k]]) return fail(AGR_EINVAL, "asset %d listed twice", assets[k]);
+        seen[assets[k]] = 1;
+    }
     DeviceGuard guard(s->device);
     cudaStream_t st = (cudaStream_t)stream;
-    CK(cudaMemcpyAsync(s->mesh_verts + 3 * s->h_mvert_off[asset], verts, sizeof(float) * 3 * n_verts,
-                       cudaMemcpyDeviceToDevice, st));
-    CK(build_asset(s, asset, st));
+    int64_t v = 0;
+    for (int k = 0; k < n; ++k) {
+        const int a = assets[k];
+        CK(cudaMemcpyAsync(s->mesh_verts + 3 * s->h_mvert_off[a], verts + 3 * v,
+                           sizeof(float) * 3 * s->h_nverts[a], cudaMemcpyDeviceToDevice, st));
+        v += s->h_nverts[a];
+    }
+    CK(build_assets(s, assets, n, st));
     CK(instances_update(s->tlas_args(), (int)s->n_inst, st));  // instance boxes from the new BLAS
     s->assets_stale = true;
     s->dirty = true;

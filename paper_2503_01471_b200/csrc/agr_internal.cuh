@@ -175,24 +175,32 @@ __device__ __forceinline__ void write_node4(float4* nodes, int g, const float b[
 
 // Host launch wrappers implemented in the .cu files (all async on `stream`).
 namespace agr {
-struct BlasBuildArgs {
+// One asset of a batched BLAS build: all kernels of the build run once over
+// the concatenation of the batch's faces (face g of the batch belongs to the
+// asset whose [off, off + n_faces) contains it).
+struct BlasSeg {
     const float* verts;    // device [V][3]
-    const int* faces;      // device [F][3]
+    const int* faces;      // device [F][3], asset-local vertex ids
     int n_verts, n_faces;
-    int node_base;         // global node index of this asset's first node
-    int leaf_base;         // global leaf-record index of this asset's first leaf
+    int off;               // first batch face of this asset (set by blas_build_batch)
+    int node_base;         // global index of this asset's first node (F - 1 reserved, >= 1)
+    int leaf_base;         // global leaf-record index of this asset's first leaf (F reserved)
+    AssetInfo* info;       // this asset's AssetInfo (device)
+};
+struct BlasBatchArgs {
     float4* nodes;         // global BVH4 node array
     float4* bnodes;        // global binary BLAS node array (debug export)
     float4* tris;          // global tri record array
     float* triv;           // global exact-vertex array
-    AssetInfo* info_dev;   // this asset's AssetInfo (device)
-    uint32_t* dbg_morton;  // optional: sorted codes [n_leaves] (device) or null
+    uint32_t* dbg_morton;  // optional: sorted codes at leaf_base + p (device) or null
     int trbvh_rounds;      // treelet-restructuring passes after the LBVH (0 = plain LBVH)
 };
-// Builds one asset's BLAS.  `scratch` must hold blas_scratch_bytes(F) bytes.
-size_t blas_scratch_bytes(int n_faces);
-cudaError_t blas_build(const BlasBuildArgs& a, void* scratch, int* n_leaves_out,
-                       cudaStream_t stream);
+// Builds the BLAS of every asset in h_segs[0, n) (host array; `off` is
+// filled in) in one set of launches.  `scratch` must hold
+// blas_scratch_bytes(sum of n_faces, n) bytes.  Async on `stream`.
+size_t blas_scratch_bytes(int64_t total_faces, int n_segs);
+cudaError_t blas_build_batch(BlasSeg* h_segs, int n_segs, const BlasBatchArgs& a, void* scratch,
+                             cudaStream_t stream);
 
 struct TlasArgs {
     float4* nodes;            // global node array (TLAS part written)

@@ -1,4 +1,4 @@
-// blas.cu -- per-asset bottom-level BVH (BLAS) build on the GPU.
+// blas.cu -- bottom-level BVH (BLAS) builds on the GPU, batched over assets.
 //
 // PAPER.md:226 (§III.D.1): "a bounding volume hierarchy is calculated for
 // M_{i,t} for efficient ray-casting".  The paper's Warp BVH algorithm is not
@@ -11,13 +11,23 @@
 //   K2 radix sort   LSD, 8-bit digits, stable (hist / scan / scatter)
 //   K3 karras       radix-tree topology, ties broken by leaf index
 //   K4 fit          bottom-up boxes: 2nd-arriving child unions (atomic flag)
-//   K5 pack         64-B nodes + 48-B triangle records + exact vertices
+//   K4b trbvh       treelet restructuring
+//   K5 pack         BVH4 nodes + 48-B triangle records + exact vertices
 // Zero-area faces (exactly, in FP64 from the FP32 inputs) are left out of
 // the tree: they can never be hit, and the face numbering is kept by the
 // per-leaf local face id.
+//
+// Batching (per-env unique meshes rebuilt at reset):
+// every kernel runs once over the concatenated faces of all assets in the
+// batch; face g belongs to segment seg_of[g].  The sort orders (asset,
+// Morton code) by an LSD pass over the codes followed by passes over the
+// segment id (stable), so each asset's leaf order -- and therefore its tree
+// -- is exactly what a build of that asset alone produces.  Per-segment
+// scratch (tree topology, boxes, flags) lives at the segment's face offset.
 #include "agr_internal.cuh"
 
 #include <cfloat>
+#include <vector>
 
 namespace agr {
 namespace {
@@ -27,142 +37,187 @@ constexpr int RS_THREADS = 256;
 constexpr int RS_ROUNDS = 4;
 constexpr int RS_TILE = RS_THREADS * RS_ROUNDS;
 constexpr uint32_t DEGENERATE_KEY = 0xFFFFFFFFu;
+constexpr unsigned FULL = 0xFFFFFFFFu;
 
 struct Scratch {
-    float* tri_box;      // [F][6] (lo xyz, hi xyz)
-    uint32_t* bounds;    // [8]: ordered-int centroid lo xyz, hi xyz, radius, n_valid
-    uint32_t* keys[2];   // [F]
-    uint32_t* vals[2];   // [F]
+    float* tri_box;      // [Ftot][6] (lo xyz, hi xyz), by batch face
+    uint32_t* bounds;    // [B][8]: ordered-int centroid lo xyz, hi xyz, radius, n_valid
+    uint32_t* mcode;     // [Ftot] Morton code of each batch face
+    uint32_t* keys[2];   // [Ftot]
+    uint32_t* vals[2];   // [Ftot] batch face ids
     uint32_t* hist;      // [256 * nblocks]
-    int* child;          // [2 * (F-1)] local refs
-    int* node_parent;    // [F-1]
-    int* leaf_parent;    // [F]
-    float* ibox;         // [F-1][6]
-    int* flags;          // [F-1]
-    int* depth;          // [1]
-    float* cost;         // [F-1] SAH cost of each internal node's subtree (TRBVH)
+    int* seg_of;         // [Ftot] segment of each batch face
+    BlasSeg* segs;       // [B]
+    int* child;          // [2 Ftot] local refs; segment s at 2 off_s
+    int* node_parent;    // [Ftot]   segment s at off_s
+    int* leaf_parent;    // [Ftot]
+    float* ibox;         // [Ftot][6]
+    int* flags;          // [Ftot]
+    int* depth;          // [B]
+    float* cost;         // [Ftot] SAH cost of each internal node's subtree (TRBVH)
 };
 
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
-Scratch carve(void* base, int F) {
+size_t scratch_layout(int64_t F, int B, void* base, Scratch* out) {
     char* p = (char*)base;
-    size_t nb = (F + RS_TILE - 1) / RS_TILE;
-    int Fi = F > 1 ? F - 1 : 1;
+    size_t used = 0;
+    const size_t nb = (size_t)((F + RS_TILE - 1) / RS_TILE);
+    auto take = [&](size_t bytes) {
+        char* q = p ? p + used : nullptr;
+        used += align_up(bytes);
+        return q;
+    };
     Scratch s;
-    s.tri_box = (float*)p; p += align_up(sizeof(float) * 6 * F);
-    s.bounds = (uint32_t*)p; p += align_up(sizeof(uint32_t) * 8);
-    for (int i = 0; i < 2; ++i) { s.keys[i] = (uint32_t*)p; p += align_up(sizeof(uint32_t) * F); }
-    for (int i = 0; i < 2; ++i) { s.vals[i] = (uint32_t*)p; p += align_up(sizeof(uint32_t) * F); }
-    s.hist = (uint32_t*)p; p += align_up(sizeof(uint32_t) * 256 * nb);
-    s.child = (int*)p; p += align_up(sizeof(int) * 2 * Fi);
-    s.node_parent = (int*)p; p += align_up(sizeof(int) * Fi);
-    s.leaf_parent = (int*)p; p += align_up(sizeof(int) * F);
-    s.ibox = (float*)p; p += align_up(sizeof(float) * 6 * Fi);
-    s.flags = (int*)p; p += align_up(sizeof(int) * Fi);
-    s.depth = (int*)p; p += align_up(sizeof(int));
-    s.cost = (float*)p; p += align_up(sizeof(float) * Fi);
-    return s;
+    s.tri_box = (float*)take(sizeof(float) * 6 * F);
+    s.bounds = (uint32_t*)take(sizeof(uint32_t) * 8 * B);
+    s.mcode = (uint32_t*)take(sizeof(uint32_t) * F);
+    for (int i = 0; i < 2; ++i) s.keys[i] = (uint32_t*)take(sizeof(uint32_t) * F);
+    for (int i = 0; i < 2; ++i) s.vals[i] = (uint32_t*)take(sizeof(uint32_t) * F);
+    s.hist = (uint32_t*)take(sizeof(uint32_t) * 256 * nb);
+    s.seg_of = (int*)take(sizeof(int) * F);
+    s.segs = (BlasSeg*)take(sizeof(BlasSeg) * B);
+    s.child = (int*)take(sizeof(int) * 2 * F);
+    s.node_parent = (int*)take(sizeof(int) * F);
+    s.leaf_parent = (int*)take(sizeof(int) * F);
+    s.ibox = (float*)take(sizeof(float) * 6 * F);
+    s.flags = (int*)take(sizeof(int) * F);
+    s.depth = (int*)take(sizeof(int) * B);
+    s.cost = (float*)take(sizeof(float) * F);
+    if (out) *out = s;
+    return used + 256;
 }
 
-// ---- K1: triangle prep ------------------------------------------------------
-__global__ void k_init_bounds(uint32_t* b) {
-    int i = threadIdx.x;
-    if (i < 3) b[i] = float_to_ordered(FLT_MAX);
-    else if (i < 6) b[i] = float_to_ordered(-FLT_MAX);
-    else if (i == 6) b[i] = float_to_ordered(0.0f);
-    else if (i == 7) b[i] = 0u;
+// Segment context of batch face g.
+struct SegCtx {
+    int s;        // segment
+    int off;      // its first batch face
+    int F;        // its faces
+    int n;        // its non-degenerate leaves (after K1)
+};
+__device__ __forceinline__ SegCtx seg_ctx(const BlasSeg* segs, const int* seg_of, const uint32_t* bounds,
+                                          int g) {
+    SegCtx c;
+    c.s = __ldg(seg_of + g);
+    c.off = segs[c.s].off;
+    c.F = segs[c.s].n_faces;
+    c.n = (int)bounds[8 * c.s + 7];
+    return c;
 }
 
-__global__ void k_tri_prep(const float* __restrict__ verts, const int* __restrict__ faces, int F,
-                           int V, float* __restrict__ tri_box, uint32_t* __restrict__ vflag,
-                           uint32_t* bounds) {
-    int f = blockIdx.x * blockDim.x + threadIdx.x;
-    // asset radius over vertices
+// ---- K0: segment ids, bounds init -----------------------------------------
+__global__ void k_seg_of(const BlasSeg* segs, int* seg_of) {
+    const int s = blockIdx.x;
+    const int off = segs[s].off, F = segs[s].n_faces;
+    for (int i = threadIdx.x; i < F; i += blockDim.x) seg_of[off + i] = s;
+}
+
+__global__ void k_init_bounds(uint32_t* b, int B) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= 8 * B) return;
+    int k = i & 7;
+    if (k < 3) b[i] = float_to_ordered(FLT_MAX);
+    else if (k < 6) b[i] = float_to_ordered(-FLT_MAX);
+    else if (k == 6) b[i] = float_to_ordered(0.0f);
+    else b[i] = 0u;
+}
+
+// ---- K1: triangle prep --------------------------------------------------------
+// asset radius over its vertices: one CTA per segment
+__global__ void k_radius(const BlasSeg* segs, uint32_t* bounds) {
+    const int s = blockIdx.x;
+    const float* verts = segs[s].verts;
+    const int V = segs[s].n_verts;
     float r = 0.0f;
-    for (int v = f; v < V; v += gridDim.x * blockDim.x) {
+    for (int v = threadIdx.x; v < V; v += blockDim.x) {
         float x = verts[3 * v], y = verts[3 * v + 1], z = verts[3 * v + 2];
         r = fmaxf(r, sqrtf(x * x + y * y + z * z) * 1.000001f);
     }
+    for (int o = 16; o > 0; o >>= 1) r = fmaxf(r, __shfl_xor_sync(FULL, r, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(&bounds[8 * s + 6], float_to_ordered(r));
+}
+
+__global__ void k_tri_prep(const BlasSeg* segs, const int* seg_of, int Ftot, float* __restrict__ tri_box,
+                           uint32_t* __restrict__ vflag, uint32_t* bounds) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    const int s = g < Ftot ? __ldg(seg_of + g) : -1;
     float clo[3] = {FLT_MAX, FLT_MAX, FLT_MAX}, chi[3] = {-FLT_MAX, -FLT_MAX, -FLT_MAX};
     bool valid = false;
-    if (f < F) {
-        const float* a = verts + 3 * faces[3 * f];
-        const float* b = verts + 3 * faces[3 * f + 1];
-        const float* c = verts + 3 * faces[3 * f + 2];
+    if (s >= 0) {
+        const BlasSeg& S = segs[s];
+        const int f = g - S.off;
+        const float* a = S.verts + 3 * S.faces[3 * f];
+        const float* b = S.verts + 3 * S.faces[3 * f + 1];
+        const float* c = S.verts + 3 * S.faces[3 * f + 2];
         // exact-input FP64 area: zero only for genuinely degenerate input
         d3 A = mkd(a[0], a[1], a[2]), B = mkd(b[0], b[1], b[2]), C = mkd(c[0], c[1], c[2]);
         d3 n = crossd(subd(B, A), subd(C, A));
         valid = (n.x != 0.0 || n.y != 0.0 || n.z != 0.0);
-        float lo[3], hi[3];
         for (int k = 0; k < 3; ++k) {
-            lo[k] = fminf(a[k], fminf(b[k], c[k]));
-            hi[k] = fmaxf(a[k], fmaxf(b[k], c[k]));
-            tri_box[6 * f + k] = lo[k];
-            tri_box[6 * f + 3 + k] = hi[k];
-            if (valid) {
-                float cc = 0.5f * lo[k] + 0.5f * hi[k];
-                clo[k] = cc;
-                chi[k] = cc;
-            }
+            const float lo = fminf(a[k], fminf(b[k], c[k]));
+            const float hi = fmaxf(a[k], fmaxf(b[k], c[k]));
+            tri_box[6 * g + k] = lo;
+            tri_box[6 * g + 3 + k] = hi;
+            if (valid) clo[k] = chi[k] = 0.5f * lo + 0.5f * hi;
         }
-        vflag[f] = valid ? 1u : 0u;
+        vflag[g] = valid ? 1u : 0u;
     }
-    // block reduce bounds, radius and valid count
-    __shared__ float s_lo[3][T_BLK / 32], s_hi[3][T_BLK / 32], s_r[T_BLK / 32];
-    __shared__ unsigned s_cnt[T_BLK / 32];
-    unsigned cnt = __popc(__ballot_sync(0xFFFFFFFFu, valid));
-    for (int o = 16; o > 0; o >>= 1) {
-        for (int k = 0; k < 3; ++k) {
-            clo[k] = fminf(clo[k], __shfl_xor_sync(0xFFFFFFFFu, clo[k], o));
-            chi[k] = fmaxf(chi[k], __shfl_xor_sync(0xFFFFFFFFu, chi[k], o));
-        }
-        r = fmaxf(r, __shfl_xor_sync(0xFFFFFFFFu, r, o));
-    }
-    int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-    if (l == 0) {
-        for (int k = 0; k < 3; ++k) { s_lo[k][w] = clo[k]; s_hi[k][w] = chi[k]; }
-        s_r[w] = r;
-        s_cnt[w] = cnt;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        unsigned tot = 0;
-        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) {
+    // centroid bounds and valid count: one set of atomics per warp when the
+    // warp lies in one segment (the common case), else per thread
+    const int s0 = __shfl_sync(FULL, s, 0);
+    if (__all_sync(FULL, s == s0)) {
+        unsigned cnt = __popc(__ballot_sync(FULL, valid));
+        for (int o = 16; o > 0; o >>= 1)
             for (int k = 0; k < 3; ++k) {
-                clo[k] = fminf(clo[k], s_lo[k][i]);
-                chi[k] = fmaxf(chi[k], s_hi[k][i]);
+                clo[k] = fminf(clo[k], __shfl_xor_sync(FULL, clo[k], o));
+                chi[k] = fmaxf(chi[k], __shfl_xor_sync(FULL, chi[k], o));
             }
-            r = fmaxf(r, s_r[i]);
-            tot += s_cnt[i];
+        if ((threadIdx.x & 31) == 0 && cnt > 0) {
+            for (int k = 0; k < 3; ++k) {
+                atomicMin(&bounds[8 * s0 + k], float_to_ordered(clo[k]));
+                atomicMax(&bounds[8 * s0 + 3 + k], float_to_ordered(chi[k]));
+            }
+            atomicAdd(&bounds[8 * s0 + 7], cnt);
         }
+    } else if (valid) {
         for (int k = 0; k < 3; ++k) {
-            atomicMin(&bounds[k], float_to_ordered(clo[k]));
-            atomicMax(&bounds[3 + k], float_to_ordered(chi[k]));
+            atomicMin(&bounds[8 * s + k], float_to_ordered(clo[k]));
+            atomicMax(&bounds[8 * s + 3 + k], float_to_ordered(chi[k]));
         }
-        atomicMax(&bounds[6], float_to_ordered(r));
-        atomicAdd(&bounds[7], tot);
+        atomicAdd(&bounds[8 * s + 7], 1u);
     }
 }
 
 // ---- K1b: Morton codes ------------------------------------------------------
-__global__ void k_morton(const float* __restrict__ tri_box, const uint32_t* __restrict__ vflag,
-                         int F, const uint32_t* __restrict__ bounds, uint32_t* __restrict__ keys,
-                         uint32_t* __restrict__ vals) {
-    int f = blockIdx.x * blockDim.x + threadIdx.x;
-    if (f >= F) return;
+__global__ void k_morton(const int* seg_of, const float* __restrict__ tri_box, const uint32_t* __restrict__ vflag,
+                         int Ftot, const uint32_t* __restrict__ bounds, uint32_t* __restrict__ mcode,
+                         uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= Ftot) return;
+    const uint32_t* b = bounds + 8 * __ldg(seg_of + g);
     uint32_t key = DEGENERATE_KEY;
-    if (vflag[f]) {
+    if (vflag[g]) {
         float u[3];
         for (int k = 0; k < 3; ++k) {
-            float lo = ordered_to_float(bounds[k]), hi = ordered_to_float(bounds[3 + k]);
-            float c = 0.5f * tri_box[6 * f + k] + 0.5f * tri_box[6 * f + 3 + k];
+            float lo = ordered_to_float(b[k]), hi = ordered_to_float(b[3 + k]);
+            float c = 0.5f * tri_box[6 * g + k] + 0.5f * tri_box[6 * g + 3 + k];
             u[k] = unit_coord(c, lo, hi);
         }
         key = morton30(u[0], u[1], u[2]);
     }
-    keys[f] = key;
-    vals[f] = (uint32_t)f;
+    mcode[g] = key;
+    keys[g] = key;
+    vals[g] = (uint32_t)g;
+}
+
+// key of each sorted element := its segment (for the segment passes), or
+// back to its Morton code (after them)
+__global__ void k_key_from(const uint32_t* __restrict__ vals, const uint32_t* __restrict__ table_u,
+                           const int* __restrict__ table_i, int Ftot, uint32_t* __restrict__ keys) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= Ftot) return;
+    const uint32_t g = vals[i];
+    keys[i] = table_u ? table_u[g] : (uint32_t)table_i[g];
 }
 
 // ---- K2: stable LSD radix sort (8-bit digits) --------------------------------
@@ -254,7 +309,7 @@ __global__ void k_rs_scatter(const uint32_t* __restrict__ kin, const uint32_t* _
     }
 }
 
-// ---- K3: Karras radix tree ------------------------------------------------------
+// ---- K3: Karras radix tree (per segment) ------------------------------------------
 __device__ __forceinline__ int kdelta(const uint32_t* k, int n, int i, int j) {
     if (j < 0 || j >= n) return -1;
     uint32_t a = k[i], b = k[j];
@@ -262,11 +317,18 @@ __device__ __forceinline__ int kdelta(const uint32_t* k, int n, int i, int j) {
     return __clz(a ^ b);
 }
 
-__global__ void k_karras(const uint32_t* __restrict__ k, const uint32_t* n_dev, int* __restrict__ child,
-                         int* __restrict__ node_parent, int* __restrict__ leaf_parent) {
-    const int n = (int)*n_dev;
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
+__global__ void k_karras(const BlasSeg* segs, const int* seg_of, const uint32_t* bounds, int Ftot,
+                         const uint32_t* __restrict__ sk, int* __restrict__ child_all,
+                         int* __restrict__ node_parent_all, int* __restrict__ leaf_parent_all) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= Ftot) return;
+    const SegCtx c = seg_ctx(segs, seg_of, bounds, g);
+    const int n = c.n, i = g - c.off;
     if (i >= n - 1) return;
+    const uint32_t* k = sk + c.off;
+    int* child = child_all + 2 * c.off;
+    int* node_parent = node_parent_all + c.off;
+    int* leaf_parent = leaf_parent_all + c.off;
     int d = (kdelta(k, n, i, i + 1) - kdelta(k, n, i, i - 1)) >= 0 ? 1 : -1;
     int dmin = kdelta(k, n, i, i - d);
     int lmax = 2;
@@ -296,36 +358,51 @@ __global__ void k_karras(const uint32_t* __restrict__ k, const uint32_t* n_dev, 
     if (i == 0) node_parent[0] = -1;
 }
 
-// ---- K4: bottom-up fit ------------------------------------------------------------
+// ---- K4: bottom-up fit (per segment) ------------------------------------------------
 __device__ __forceinline__ void load_box_cg(const float* p, float b[6]) {
     for (int k = 0; k < 6; ++k) b[k] = __ldcg(p + k);
 }
 
-__global__ void k_fit(const uint32_t* n_dev, const uint32_t* __restrict__ sorted_prim, const float* tri_box,
-                      const int* __restrict__ child, const int* __restrict__ node_parent,
-                      const int* __restrict__ leaf_parent, float* ibox, int* flags, int* depth) {
-    const int n = (int)*n_dev;
-    int p = blockIdx.x * blockDim.x + threadIdx.x;
+// Per-segment views of the scratch arrays used by K4/K4b/K5.
+#define AGR_SEG_VIEW(c)                                             \
+    const uint32_t* sorted_prim = sorted_all + (c).off;             \
+    int* child = child_all + 2 * (c).off;                           \
+    float* ibox = ibox_all + 6 * (size_t)(c).off
+#define AGR_SEG_PARENTS(c)                                          \
+    int* node_parent = node_parent_all + (c).off;                   \
+    int* leaf_parent = leaf_parent_all + (c).off
+
+__global__ void k_fit(const BlasSeg* segs, const int* seg_of, const uint32_t* bounds, int Ftot,
+                      const uint32_t* __restrict__ sorted_all, const float* tri_box, int* child_all,
+                      int* node_parent_all, int* leaf_parent_all, float* ibox_all, int* flags_all,
+                      int* depth) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= Ftot) return;
+    const SegCtx c = seg_ctx(segs, seg_of, bounds, g);
+    const int n = c.n, p = g - c.off;
     if (n < 2 || p >= n) return;
+    AGR_SEG_VIEW(c);
+    AGR_SEG_PARENTS(c);
+    int* flags = flags_all + c.off;
     // depth of this leaf
     int dd = 0;
     for (int q = leaf_parent[p]; q >= 0; q = node_parent[q]) ++dd;
-    atomicMax(depth, dd);
+    atomicMax(depth + c.s, dd);
     int node = leaf_parent[p];
     while (node >= 0) {
         __threadfence();
         if (atomicAdd(&flags[node], 1) == 0) return;  // first arrival: sibling not ready
         __threadfence();
-        float b[6], c[6];
+        float b[6], cc[6];
         for (int side = 0; side < 2; ++side) {
             int r = child[2 * node + side];
-            float* dst = side == 0 ? b : c;
+            float* dst = side == 0 ? b : cc;
             if (r < 0) load_box_cg(tri_box + 6 * sorted_prim[~r], dst);
             else load_box_cg(ibox + 6 * r, dst);
         }
         for (int k = 0; k < 3; ++k) {
-            __stcg(ibox + 6 * node + k, fminf(b[k], c[k]));
-            __stcg(ibox + 6 * node + 3 + k, fmaxf(b[3 + k], c[3 + k]));
+            __stcg(ibox + 6 * node + k, fminf(b[k], cc[k]));
+            __stcg(ibox + 6 * node + 3 + k, fmaxf(b[3 + k], cc[3 + k]));
         }
         node = node_parent[node];
     }
@@ -348,136 +425,218 @@ __device__ __forceinline__ float box_area(const float b[6]) {
     return dx * dy + dy * dz + dz * dx;
 }
 
-__global__ void k_trbvh(const uint32_t* n_dev, const uint32_t* __restrict__ sorted_prim,
-                        const float* __restrict__ tri_box, int* child, int* node_parent,
-                        int* leaf_parent, float* ibox, float* cost, int* flags) {
-    const int n = (int)*n_dev;
-    const int p = blockIdx.x * blockDim.x + threadIdx.x;
-    if (n < 2 || p >= n) return;
-    int node = __ldcg(leaf_parent + p);
-    while (node >= 0) {
-        __threadfence();
-        if (atomicAdd(&flags[node], 1) == 0) return;  // the sibling subtree is not final yet
-        __threadfence();
-        // treelet leaves (subtree roots) and internal nodes
-        int L[TREELET], I[TREELET - 1];
+// Warp-cooperative form (as in Karras & Aila): lanes walk up from their
+// leaves individually; every node a lane claims (second arrival) is then
+// optimised by the whole warp -- subset areas in parallel, the DP over
+// subsets size by size with one subset per lane, the treelet rewrite by
+// lane 0.  The DP visits partitions in the same order with the same strict
+// comparison as a serial DP, so the tree does not depend on the schedule.
+constexpr int TRB_THREADS = 64;
+struct TrbWarp {
+    float area[1 << TREELET];
+    float copt[1 << TREELET];
+    unsigned char part[1 << TREELET];
+    float lb[TREELET][6];
+    float lc[TREELET];
+    int L[TREELET];
+    int I[TREELET - 1];
+    int m;
+    float ccur;
+};
+
+__device__ __forceinline__ void subset_box(const TrbWarp& w, int sset, float b[6]) {
+    for (int c = 0; c < 3; ++c) { b[c] = INFINITY; b[3 + c] = -INFINITY; }
+    for (int k = 0; k < TREELET; ++k)
+        if ((sset >> k) & 1)
+            for (int c = 0; c < 3; ++c) {
+                b[c] = fminf(b[c], w.lb[k][c]);
+                b[3 + c] = fmaxf(b[3 + c], w.lb[k][3 + c]);
+            }
+}
+
+// Optimise the treelet rooted at local node `node` of the segment at `off`
+// (all 32 lanes, warp-uniform arguments).
+__device__ void trbvh_treelet(TrbWarp& w, int lane, int node, int off, const uint32_t* __restrict__ sorted_all,
+                              const float* __restrict__ tri_box, int* child_all, int* node_parent_all,
+                              int* leaf_parent_all, float* ibox_all, float* cost_all) {
+    const uint32_t* sorted_prim = sorted_all + off;
+    int* child = child_all + 2 * off;
+    int* node_parent = node_parent_all + off;
+    int* leaf_parent = leaf_parent_all + off;
+    float* ibox = ibox_all + 6 * (size_t)off;
+    float* cost = cost_all + off;
+    auto ref_box = [&](int r, float b[6]) {
+        const float* src = r < 0 ? tri_box + 6 * sorted_prim[~r] : ibox + 6 * r;
+        for (int c = 0; c < 6; ++c) b[c] = __ldcg(src + c);
+    };
+    if (lane == 0) {
+        // treelet leaves (subtree roots): open the largest-area one until 7
         int m = 2, ni = 1;
-        L[0] = __ldcg(child + 2 * node);
-        L[1] = __ldcg(child + 2 * node + 1);
-        I[0] = node;
+        w.L[0] = __ldcg(child + 2 * node);
+        w.L[1] = __ldcg(child + 2 * node + 1);
+        w.I[0] = node;
         while (m < TREELET) {
             int best = -1;
             float ba = -1.0f;
             for (int k = 0; k < m; ++k) {
-                if (L[k] < 0) continue;
+                if (w.L[k] < 0) continue;
                 float b[6];
-                for (int c = 0; c < 6; ++c) b[c] = __ldcg(ibox + 6 * L[k] + c);
+                ref_box(w.L[k], b);
                 const float a = box_area(b);
                 if (a > ba) { ba = a; best = k; }
             }
             if (best < 0) break;
-            const int r = L[best];
-            I[ni++] = r;
-            L[best] = __ldcg(child + 2 * r);
-            L[m++] = __ldcg(child + 2 * r + 1);
+            const int r = w.L[best];
+            w.I[ni++] = r;
+            w.L[best] = __ldcg(child + 2 * r);
+            w.L[m++] = __ldcg(child + 2 * r + 1);
         }
-        // leaf boxes / costs
-        float lb[TREELET][6], lc[TREELET];
-        for (int k = 0; k < m; ++k) {
-            const float* src = L[k] < 0 ? tri_box + 6 * sorted_prim[~L[k]] : ibox + 6 * L[k];
-            for (int c = 0; c < 6; ++c) lb[k][c] = __ldcg(src + c);
-            lc[k] = L[k] < 0 ? SAH_CT * box_area(lb[k]) : __ldcg(cost + L[k]);
-        }
+        w.m = m;
         // the node's current cost (children final)
         float nb[6];
         for (int c = 0; c < 6; ++c) nb[c] = __ldcg(ibox + 6 * node + c);
-        float ccur;
-        {
-            const int c0 = __ldcg(child + 2 * node), c1 = __ldcg(child + 2 * node + 1);
-            auto sub_cost = [&](int r) {
-                if (r < 0) {
-                    float b[6];
-                    for (int c = 0; c < 6; ++c) b[c] = __ldcg(tri_box + 6 * sorted_prim[~r] + c);
-                    return SAH_CT * box_area(b);
-                }
-                return __ldcg(cost + r);
-            };
-            ccur = SAH_CI * box_area(nb) + sub_cost(c0) + sub_cost(c1);
-        }
-        if (m >= 3) {
-            const int full = (1 << m) - 1;
-            float sb[1 << TREELET][6];
-            float copt[1 << TREELET];
-            unsigned char part[1 << TREELET];
-            for (int sset = 1; sset <= full; ++sset) {
-                const int low = __ffs(sset) - 1;
-                const int rest = sset & (sset - 1);
-                if (rest == 0) {
-                    for (int c = 0; c < 6; ++c) sb[sset][c] = lb[low][c];
-                    copt[sset] = lc[low];
-                    part[sset] = 0;
-                    continue;
-                }
-                for (int c = 0; c < 3; ++c) {
-                    sb[sset][c] = fminf(sb[rest][c], lb[low][c]);
-                    sb[sset][3 + c] = fmaxf(sb[rest][3 + c], lb[low][3 + c]);
-                }
-                const int lsb = sset & -sset;
-                float best = INFINITY;
-                int bp = 0;
-                for (int q = (sset - 1) & sset; q; q = (q - 1) & sset) {
-                    if (!(q & lsb)) continue;  // each unordered partition once
-                    const float cc = copt[q] + copt[sset ^ q];
-                    if (cc < best) { best = cc; bp = q; }
-                }
-                copt[sset] = SAH_CI * box_area(sb[sset]) + best;
-                part[sset] = (unsigned char)bp;
-            }
-            if (copt[full] < ccur * (1.0f - 1e-6f)) {
-                // rebuild the treelet: root keeps its id, the others are reused
-                int st_s[TREELET], st_n[TREELET], sp = 0, pool = 1;
-                st_s[sp] = full;
-                st_n[sp++] = node;
-                while (sp > 0) {
-                    --sp;
-                    const int sset = st_s[sp], nd = st_n[sp];
-                    const int q0 = part[sset], q1 = sset ^ q0;
-                    for (int side = 0; side < 2; ++side) {
-                        const int sub = side == 0 ? q0 : q1;
-                        int c;
-                        if ((sub & (sub - 1)) == 0) {
-                            c = L[__ffs(sub) - 1];
-                        } else {
-                            c = I[pool++];
-                            st_s[sp] = sub;
-                            st_n[sp++] = c;
-                            for (int k = 0; k < 6; ++k) __stcg(ibox + 6 * c + k, sb[sub][k]);
-                            __stcg(cost + c, copt[sub]);
-                        }
-                        __stcg(child + 2 * nd + side, c);
-                        if (c < 0) __stcg(leaf_parent + ~c, nd);
-                        else __stcg(node_parent + c, nd);
-                    }
-                }
-                __stcg(cost + node, copt[full]);
+        float ccur = SAH_CI * box_area(nb);
+        for (int side = 0; side < 2; ++side) {
+            const int r = __ldcg(child + 2 * node + side);
+            if (r < 0) {
+                float b[6];
+                ref_box(r, b);
+                ccur += SAH_CT * box_area(b);
             } else {
-                __stcg(cost + node, ccur);
+                ccur += __ldcg(cost + r);
             }
+        }
+        w.ccur = ccur;
+    }
+    __syncwarp();
+    const int m = w.m;
+    if (lane < m) {
+        const int r = w.L[lane];
+        ref_box(r, w.lb[lane]);
+        w.lc[lane] = r < 0 ? SAH_CT * box_area(w.lb[lane]) : __ldcg(cost + r);
+    }
+    __syncwarp();
+    if (m < 3) {
+        if (lane == 0) __stcg(cost + node, w.ccur);
+        __syncwarp();
+        return;
+    }
+    const int full = (1 << m) - 1;
+    for (int sset = lane + 1; sset <= full; sset += 32) {
+        float b[6];
+        subset_box(w, sset, b);
+        w.area[sset] = box_area(b);
+        if ((sset & (sset - 1)) == 0) {
+            w.copt[sset] = w.lc[__ffs(sset) - 1];
+            w.part[sset] = 0;
+        }
+    }
+    __syncwarp();
+    for (int k = 2; k <= m; ++k) {
+        for (int sset = lane + 1; sset <= full; sset += 32) {
+            if (__popc(sset) != k) continue;
+            const int lsb = sset & -sset;
+            float best = INFINITY;
+            int bp = 0;
+            for (int q = (sset - 1) & sset; q; q = (q - 1) & sset) {
+                if (!(q & lsb)) continue;  // each unordered partition once
+                const float cc = w.copt[q] + w.copt[sset ^ q];
+                if (cc < best) { best = cc; bp = q; }
+            }
+            w.copt[sset] = SAH_CI * w.area[sset] + best;
+            w.part[sset] = (unsigned char)bp;
+        }
+        __syncwarp();
+    }
+    if (lane == 0) {
+        if (w.copt[full] < w.ccur * (1.0f - 1e-6f)) {
+            // rebuild the treelet: root keeps its id, the others are reused
+            int st_s[TREELET], st_n[TREELET], sp = 0, pool = 1;
+            st_s[sp] = full;
+            st_n[sp++] = node;
+            while (sp > 0) {
+                --sp;
+                const int sset = st_s[sp], nd = st_n[sp];
+                const int q0 = w.part[sset], q1 = sset ^ q0;
+                for (int side = 0; side < 2; ++side) {
+                    const int sub = side == 0 ? q0 : q1;
+                    int c;
+                    if ((sub & (sub - 1)) == 0) {
+                        c = w.L[__ffs(sub) - 1];
+                    } else {
+                        c = w.I[pool++];
+                        st_s[sp] = sub;
+                        st_n[sp++] = c;
+                        float b[6];
+                        subset_box(w, sub, b);
+                        for (int k = 0; k < 6; ++k) __stcg(ibox + 6 * c + k, b[k]);
+                        __stcg(cost + c, w.copt[sub]);
+                    }
+                    __stcg(child + 2 * nd + side, c);
+                    if (c < 0) __stcg(leaf_parent + ~c, nd);
+                    else __stcg(node_parent + c, nd);
+                }
+            }
+            __stcg(cost + node, w.copt[full]);
         } else {
-            __stcg(cost + node, ccur);
+            __stcg(cost + node, w.ccur);
+        }
+    }
+    __syncwarp();
+}
+
+__global__ void __launch_bounds__(TRB_THREADS) k_trbvh(
+        const BlasSeg* segs, const int* seg_of, const uint32_t* bounds, int Ftot,
+        const uint32_t* __restrict__ sorted_all, const float* __restrict__ tri_box, int* child_all,
+        int* node_parent_all, int* leaf_parent_all, float* ibox_all, float* cost_all, int* flags_all) {
+    __shared__ TrbWarp s_w[TRB_THREADS / 32];
+    TrbWarp& w = s_w[threadIdx.x >> 5];
+    const int lane = threadIdx.x & 31;
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    bool active = false;
+    int node = -1, off = 0;
+    if (g < Ftot) {
+        const SegCtx c = seg_ctx(segs, seg_of, bounds, g);
+        const int p = g - c.off;
+        if (c.n >= 2 && p < c.n) {
+            active = true;
+            off = c.off;
+            node = __ldcg(leaf_parent_all + off + p);
+        }
+    }
+    for (;;) {
+        bool claim = false;
+        if (active && node >= 0) {
+            __threadfence();
+            claim = atomicAdd(&flags_all[off + node], 1) != 0;  // second arrival: subtree final
+            __threadfence();
+        }
+        active = claim;
+        unsigned mask = __ballot_sync(FULL, claim);
+        if (mask == 0) break;
+        while (mask) {
+            const int l = __ffs(mask) - 1;
+            mask &= mask - 1;
+            trbvh_treelet(w, lane, __shfl_sync(FULL, node, l), __shfl_sync(FULL, off, l), sorted_all, tri_box,
+                          child_all, node_parent_all, leaf_parent_all, ibox_all, cost_all);
         }
         __threadfence();
-        node = __ldcg(node_parent + node);
+        if (claim) node = __ldcg(node_parent_all + off + node);
     }
 }
 
-__global__ void k_depth(const uint32_t* n_dev, const int* leaf_parent, const int* node_parent, int* depth) {
-    const int n = (int)*n_dev;
-    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+__global__ void k_depth(const BlasSeg* segs, const int* seg_of, const uint32_t* bounds, int Ftot,
+                        const int* leaf_parent_all, const int* node_parent_all, int* depth) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= Ftot) return;
+    const SegCtx c = seg_ctx(segs, seg_of, bounds, g);
+    const int n = c.n, p = g - c.off;
     if (n < 2 || p >= n) return;
+    const int* leaf_parent = leaf_parent_all + c.off;
+    const int* node_parent = node_parent_all + c.off;
     int dd = 0;
     for (int q = leaf_parent[p]; q >= 0; q = node_parent[q]) ++dd;
-    atomicMax(depth, dd);
+    atomicMax(depth + c.s, dd);
 }
 
 // ---- K5: pack -------------------------------------------------------------------------
@@ -504,13 +663,17 @@ __device__ __forceinline__ int global_ref(int r, int node_base, int leaf_base) {
     return r < 0 ? ~(leaf_base + ~r) : node_base + r;
 }
 
-__global__ void k_pack_nodes(const uint32_t* n_dev, const uint32_t* __restrict__ sorted_prim,
-                             const float* tri_box, const int* __restrict__ child,
-                             const float* ibox, float4* nodes, int node_base, int leaf_base) {
-    const int n = (int)*n_dev;
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    int n_int = n > 1 ? n - 1 : 1;
+__global__ void k_pack_nodes(const BlasSeg* segs, const int* seg_of, const uint32_t* bounds, int Ftot,
+                             const uint32_t* __restrict__ sorted_all, const float* tri_box, int* child_all,
+                             float* ibox_all, float4* nodes) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= Ftot) return;
+    const SegCtx c = seg_ctx(segs, seg_of, bounds, g);
+    const int n = c.n, i = g - c.off;
+    const int n_int = n > 1 ? n - 1 : 1;
     if (i >= n_int) return;
+    AGR_SEG_VIEW(c);
+    const int node_base = segs[c.s].node_base, leaf_base = segs[c.s].leaf_base;
     int ra, rb;
     if (n > 1) { ra = child[2 * i]; rb = child[2 * i + 1]; }
     else if (n == 1) { ra = ~0; rb = REF_EMPTY; }
@@ -523,13 +686,17 @@ __global__ void k_pack_nodes(const uint32_t* n_dev, const uint32_t* __restrict__
 }
 
 // K5b: BVH4 node j = greedy 4-wide collapse of binary node j.
-__global__ void k_collapse4(const uint32_t* n_dev, const uint32_t* __restrict__ sorted_prim, const float* tri_box,
-                            const int* __restrict__ child, const float* ibox, float4* nodes,
-                            int node_base, int leaf_base) {
-    const int n = (int)*n_dev;
-    int j = blockIdx.x * blockDim.x + threadIdx.x;
-    int n_int = n > 1 ? n - 1 : 1;
+__global__ void k_collapse4(const BlasSeg* segs, const int* seg_of, const uint32_t* bounds, int Ftot,
+                            const uint32_t* __restrict__ sorted_all, const float* tri_box, int* child_all,
+                            float* ibox_all, float4* nodes) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= Ftot) return;
+    const SegCtx c = seg_ctx(segs, seg_of, bounds, g);
+    const int n = c.n, j = g - c.off;
+    const int n_int = n > 1 ? n - 1 : 1;
     if (j >= n_int) return;
+    AGR_SEG_VIEW(c);
+    const int node_base = segs[c.s].node_base, leaf_base = segs[c.s].leaf_base;
     int refs[4];
     int cnt;
     if (n > 1) {
@@ -544,127 +711,141 @@ __global__ void k_collapse4(const uint32_t* n_dev, const uint32_t* __restrict__ 
         cnt = n == 1 ? 1 : 0;
     }
     float boxes[4][6];
-    int g[4];
+    int gr[4];
     for (int k = 0; k < 4; ++k) {
         child_box(refs[k], sorted_prim, tri_box, ibox, boxes[k]);
-        g[k] = global_ref(refs[k], node_base, leaf_base);
+        gr[k] = global_ref(refs[k], node_base, leaf_base);
     }
-    write_node4(nodes, node_base + j, boxes, g, cnt);
+    write_node4(nodes, node_base + j, boxes, gr, cnt);
 }
 
-__global__ void k_pack_tris(const uint32_t* n_dev, const uint32_t* __restrict__ sorted_prim,
-                            const float* __restrict__ verts, const int* __restrict__ faces,
-                            float4* tris, float* triv, int leaf_base) {
-    const int n = (int)*n_dev;
-    int p = blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= n) return;
-    int f = (int)sorted_prim[p];
-    const float* a = verts + 3 * faces[3 * f];
-    const float* b = verts + 3 * faces[3 * f + 1];
-    const float* c = verts + 3 * faces[3 * f + 2];
-    d3 A = mkd(a[0], a[1], a[2]), B = mkd(b[0], b[1], b[2]), C = mkd(c[0], c[1], c[2]);
+__global__ void k_pack_tris(const BlasSeg* segs, const int* seg_of, const uint32_t* bounds, int Ftot,
+                            const uint32_t* __restrict__ sorted_all, const uint32_t* __restrict__ sk,
+                            float4* tris, float* triv, uint32_t* dbg_morton) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= Ftot) return;
+    const SegCtx c = seg_ctx(segs, seg_of, bounds, g);
+    const int p = g - c.off;
+    const BlasSeg& S = segs[c.s];
+    if (dbg_morton) dbg_morton[S.leaf_base + p] = sk[g];
+    if (p >= c.n) return;
+    const int f = (int)sorted_all[g] - c.off;  // asset-local face id
+    const float* a = S.verts + 3 * S.faces[3 * f];
+    const float* b = S.verts + 3 * S.faces[3 * f + 1];
+    const float* cc = S.verts + 3 * S.faces[3 * f + 2];
+    d3 A = mkd(a[0], a[1], a[2]), B = mkd(b[0], b[1], b[2]), C = mkd(cc[0], cc[1], cc[2]);
     d3 E1 = subd(B, A), E2 = subd(C, A), E3 = subd(C, B);
     d3 N = crossd(E1, E2);
     double two_area = sqrt(dotd(N, N));
     double lmax = fmax(sqrt(dotd(E1, E1)), fmax(sqrt(dotd(E2, E2)), sqrt(dotd(E3, E3))));
     // min altitude = 2A / longest edge; store its inverse, rounded up
     float inv_min_alt = (float)(lmax / two_area) * 1.000001f;
-    int g = leaf_base + p;
-    tris[3 * g + 0] = make_float4(a[0], a[1], a[2], inv_min_alt);
-    tris[3 * g + 1] = make_float4((float)E1.x, (float)E1.y, (float)E1.z, (float)two_area);
-    tris[3 * g + 2] = make_float4((float)E2.x, (float)E2.y, (float)E2.z, __int_as_float(f));
+    int gl = S.leaf_base + p;
+    tris[3 * gl + 0] = make_float4(a[0], a[1], a[2], inv_min_alt);
+    tris[3 * gl + 1] = make_float4((float)E1.x, (float)E1.y, (float)E1.z, (float)two_area);
+    tris[3 * gl + 2] = make_float4((float)E2.x, (float)E2.y, (float)E2.z, __int_as_float(f));
     for (int k = 0; k < 3; ++k) {
-        triv[9 * g + k] = a[k];
-        triv[9 * g + 3 + k] = b[k];
-        triv[9 * g + 6 + k] = c[k];
+        triv[9 * gl + k] = a[k];
+        triv[9 * gl + 3 + k] = b[k];
+        triv[9 * gl + 6 + k] = cc[k];
     }
 }
 
-__global__ void k_asset_info(const uint32_t* n_dev, int F, const uint32_t* bounds, const float* ibox,
-                             const float* tri_box, const uint32_t* sorted_prim, const int* depth,
-                             int node_base, int leaf_base, AssetInfo* info) {
-    const int n = (int)*n_dev;
+__global__ void k_asset_info(const BlasSeg* segs, int B, const uint32_t* bounds, const float* ibox_all,
+                             const float* tri_box, const uint32_t* sorted_all, const int* depth) {
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= B) return;
+    const BlasSeg& S = segs[s];
+    const int n = (int)bounds[8 * s + 7];
     AssetInfo a;
-    a.node_base = node_base;
-    a.leaf_base = leaf_base;
+    a.node_base = S.node_base;
+    a.leaf_base = S.leaf_base;
     a.n_leaves = n;
-    a.n_faces = F;
-    a.radius = ordered_to_float(bounds[6]);
-    a.depth = n > 1 ? *depth + 0 : 1;
+    a.n_faces = S.n_faces;
+    a.radius = ordered_to_float(bounds[8 * s + 6]);
+    a.depth = n > 1 ? depth[s] : 1;
     if (n > 1) {
-        for (int k = 0; k < 3; ++k) { a.lo[k] = ibox[k]; a.hi[k] = ibox[3 + k]; }
+        const float* r = ibox_all + 6 * (size_t)S.off;  // local internal node 0 = root
+        for (int k = 0; k < 3; ++k) { a.lo[k] = r[k]; a.hi[k] = r[3 + k]; }
     } else if (n == 1) {
-        const float* b = tri_box + 6 * sorted_prim[0];
+        const float* b = tri_box + 6 * sorted_all[S.off];
         for (int k = 0; k < 3; ++k) { a.lo[k] = b[k]; a.hi[k] = b[3 + k]; }
     } else {
         for (int k = 0; k < 3; ++k) { a.lo[k] = 0.0f; a.hi[k] = 0.0f; }
     }
-    *info = a;
+    *S.info = a;
 }
 
 }  // namespace
 
-size_t blas_scratch_bytes(int F) {
-    size_t nb = (F + RS_TILE - 1) / RS_TILE;
-    int Fi = F > 1 ? F - 1 : 1;
-    return align_up(sizeof(float) * 6 * F) + align_up(32) + 4 * align_up(sizeof(uint32_t) * F) +
-           align_up(sizeof(uint32_t) * 256 * nb) + align_up(sizeof(int) * 2 * Fi) +
-           align_up(sizeof(int) * Fi) + align_up(sizeof(int) * F) + align_up(sizeof(float) * 6 * Fi) +
-           align_up(sizeof(int) * Fi) + align_up(sizeof(int)) + align_up(sizeof(float) * Fi) + 256;
+size_t blas_scratch_bytes(int64_t total_faces, int n_segs) {
+    return scratch_layout(total_faces, n_segs, nullptr, nullptr);
 }
 
-cudaError_t blas_build(const BlasBuildArgs& a, void* scratch, int* n_leaves_out,
-                       cudaStream_t stream) {
-    const int F = a.n_faces;
-    Scratch s = carve(scratch, F);
-    int gb = (F + T_BLK - 1) / T_BLK;
-    int gv = (a.n_verts + T_BLK - 1) / T_BLK;
-    k_init_bounds<<<1, 32, 0, stream>>>(s.bounds);
-    k_tri_prep<<<max(gb, gv), T_BLK, 0, stream>>>(a.verts, a.faces, F, a.n_verts, s.tri_box,
-                                                 s.vals[1], s.bounds);
-    k_morton<<<gb, T_BLK, 0, stream>>>(s.tri_box, s.vals[1], F, s.bounds, s.keys[0], s.vals[0]);
-    int nb = (F + RS_TILE - 1) / RS_TILE;
+cudaError_t blas_build_batch(BlasSeg* h_segs, int B, const BlasBatchArgs& a, void* scratch,
+                             cudaStream_t stream) {
+    if (B <= 0) return cudaSuccess;
+    int64_t F64 = 0;
+    for (int s = 0; s < B; ++s) {
+        h_segs[s].off = (int)F64;
+        F64 += h_segs[s].n_faces;
+    }
+    if (F64 <= 0 || F64 > 0x3FFFFFFF) return cudaErrorInvalidValue;
+    const int F = (int)F64;
+    Scratch s;
+    scratch_layout(F, B, scratch, &s);
+    cudaError_t e = cudaMemcpyAsync(s.segs, h_segs, sizeof(BlasSeg) * B, cudaMemcpyHostToDevice, stream);
+    if (e != cudaSuccess) return e;
+    const int gb = (F + T_BLK - 1) / T_BLK;
+    k_seg_of<<<B, T_BLK, 0, stream>>>(s.segs, s.seg_of);
+    k_init_bounds<<<(8 * B + T_BLK - 1) / T_BLK, T_BLK, 0, stream>>>(s.bounds, B);
+    k_radius<<<B, 128, 0, stream>>>(s.segs, s.bounds);
+    k_tri_prep<<<gb, T_BLK, 0, stream>>>(s.segs, s.seg_of, F, s.tri_box, s.vals[1], s.bounds);
+    k_morton<<<gb, T_BLK, 0, stream>>>(s.seg_of, s.tri_box, s.vals[1], F, s.bounds, s.mcode, s.keys[0],
+                                       s.vals[0]);
+    const int nb = (F + RS_TILE - 1) / RS_TILE;
     int cur = 0;
-    for (int shift = 0; shift < 32; shift += 8) {
+    auto pass = [&](int shift) {
         k_rs_hist<<<nb, RS_THREADS, 0, stream>>>(s.keys[cur], F, shift, s.hist, nb);
         k_rs_scan<<<1, 1024, 0, stream>>>(s.hist, 256 * nb);
         k_rs_scatter<<<nb, RS_THREADS, 0, stream>>>(s.keys[cur], s.vals[cur], s.keys[cur ^ 1],
                                                     s.vals[cur ^ 1], F, shift, s.hist, nb);
         cur ^= 1;
+    };
+    for (int shift = 0; shift < 32; shift += 8) pass(shift);
+    if (B > 1) {
+        // stable passes over the segment id: (segment, code) order
+        k_key_from<<<gb, T_BLK, 0, stream>>>(s.vals[cur], nullptr, s.seg_of, F, s.keys[cur]);
+        for (int shift = 0; shift < 32 && ((unsigned)(B - 1) >> shift) != 0u; shift += 8) pass(shift);
+        k_key_from<<<gb, T_BLK, 0, stream>>>(s.vals[cur], s.mcode, nullptr, F, s.keys[cur]);
     }
-    // everything below is sized by F and reads the number of non-degenerate
-    // leaves n from the device (no host round trip: updates stay async)
-    const uint32_t* n_dev = s.bounds + 7;
-    if (a.dbg_morton)
-        cudaMemcpyAsync(a.dbg_morton, s.keys[cur], sizeof(uint32_t) * F, cudaMemcpyDeviceToDevice, stream);
+    // everything below reads each segment's leaf count from the device (no
+    // host round trip: builds stay async)
     const uint32_t* sk = s.keys[cur];
     const uint32_t* sv = s.vals[cur];
-    cudaMemsetAsync(s.depth, 0, sizeof(int), stream);
-    const int Fi = F > 1 ? F - 1 : 1;
-    cudaMemsetAsync(s.flags, 0, sizeof(int) * Fi, stream);
-    k_karras<<<(Fi + T_BLK - 1) / T_BLK, T_BLK, 0, stream>>>(sk, n_dev, s.child, s.node_parent, s.leaf_parent);
-    k_fit<<<(F + T_BLK - 1) / T_BLK, T_BLK, 0, stream>>>(n_dev, sv, s.tri_box, s.child, s.node_parent,
-                                                        s.leaf_parent, s.ibox, s.flags, s.depth);
+    cudaMemsetAsync(s.depth, 0, sizeof(int) * B, stream);
+    cudaMemsetAsync(s.flags, 0, sizeof(int) * F, stream);
+    k_karras<<<gb, T_BLK, 0, stream>>>(s.segs, s.seg_of, s.bounds, F, sk, s.child, s.node_parent,
+                                       s.leaf_parent);
+    k_fit<<<gb, T_BLK, 0, stream>>>(s.segs, s.seg_of, s.bounds, F, sv, s.tri_box, s.child, s.node_parent,
+                                    s.leaf_parent, s.ibox, s.flags, s.depth);
     for (int round = 0; round < a.trbvh_rounds; ++round) {
-        cudaMemsetAsync(s.flags, 0, sizeof(int) * Fi, stream);
-        k_trbvh<<<(F + 63) / 64, 64, 0, stream>>>(n_dev, sv, s.tri_box, s.child, s.node_parent, s.leaf_parent,
-                                                  s.ibox, s.cost, s.flags);
+        cudaMemsetAsync(s.flags, 0, sizeof(int) * F, stream);
+        k_trbvh<<<(F + TRB_THREADS - 1) / TRB_THREADS, TRB_THREADS, 0, stream>>>(s.segs, s.seg_of, s.bounds, F, sv, s.tri_box, s.child,
+                                                  s.node_parent, s.leaf_parent, s.ibox, s.cost, s.flags);
     }
     if (a.trbvh_rounds > 0) {
-        cudaMemsetAsync(s.depth, 0, sizeof(int), stream);
-        k_depth<<<(F + T_BLK - 1) / T_BLK, T_BLK, 0, stream>>>(n_dev, s.leaf_parent, s.node_parent, s.depth);
+        cudaMemsetAsync(s.depth, 0, sizeof(int) * B, stream);
+        k_depth<<<gb, T_BLK, 0, stream>>>(s.segs, s.seg_of, s.bounds, F, s.leaf_parent, s.node_parent, s.depth);
     }
-    k_pack_nodes<<<(Fi + T_BLK - 1) / T_BLK, T_BLK, 0, stream>>>(n_dev, sv, s.tri_box, s.child, s.ibox,
-                                                                a.bnodes, a.node_base, a.leaf_base);
-    k_collapse4<<<(Fi + T_BLK - 1) / T_BLK, T_BLK, 0, stream>>>(n_dev, sv, s.tri_box, s.child, s.ibox,
-                                                               a.nodes, a.node_base, a.leaf_base);
-    k_pack_tris<<<(F + T_BLK - 1) / T_BLK, T_BLK, 0, stream>>>(n_dev, sv, a.verts, a.faces, a.tris,
-                                                              a.triv, a.leaf_base);
-    k_asset_info<<<1, 1, 0, stream>>>(n_dev, F, s.bounds, s.ibox, s.tri_box, sv, s.depth, a.node_base,
-                                      a.leaf_base, a.info_dev);
-    if (n_leaves_out) *n_leaves_out = -1;  // known on the device only
+    k_pack_nodes<<<gb, T_BLK, 0, stream>>>(s.segs, s.seg_of, s.bounds, F, sv, s.tri_box, s.child, s.ibox,
+                                           a.bnodes);
+    k_collapse4<<<gb, T_BLK, 0, stream>>>(s.segs, s.seg_of, s.bounds, F, sv, s.tri_box, s.child, s.ibox,
+                                          a.nodes);
+    k_pack_tris<<<gb, T_BLK, 0, stream>>>(s.segs, s.seg_of, s.bounds, F, sv, sk, a.tris, a.triv,
+                                          a.dbg_morton);
+    k_asset_info<<<(B + 127) / 128, 128, 0, stream>>>(s.segs, B, s.bounds, s.ibox, s.tri_box, sv, s.depth);
     return cudaGetLastError();
 }
-
 
 }  // namespace agr

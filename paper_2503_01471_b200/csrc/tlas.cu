@@ -65,16 +65,51 @@ __global__ void k_instances(TlasArgs a, int n_inst) {
     double nAinv = sqrt(nrm2) * (1.0 + 1e-6);
     double err_off = nAinv * b1 + (double)as.radius;
     rec[3] = make_float4(__int_as_float(as.node_base), (float)nAinv, (float)(err_off * (1.0 + 1e-6)), 0.f);
-    // conservative world box: centre/extent form, rounded outward
-    for (int r = 0; r < 3; ++r) {
-        double c = b[r], e = 0.0;
-        for (int k = 0; k < 3; ++k) {
-            double ck = 0.5 * ((double)as.lo[k] + (double)as.hi[k]);
-            double ek = 0.5 * ((double)as.hi[k] - (double)as.lo[k]);
-            c += A[r][k] * ck;
-            e += fabs(A[r][k]) * ek;
+    // conservative world box: the union of the transformed boxes of the
+    // BLAS's second BVH4 level (up to 16 boxes; much tighter than the
+    // transformed root box under rotation), each in centre/extent form and
+    // rounded outward
+    double wlo[3] = {INFINITY, INFINITY, INFINITY}, whi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    auto add_box = [&](const float* lo, const float* hi) {
+        for (int r = 0; r < 3; ++r) {
+            double c = b[r], e = 0.0;
+            for (int k = 0; k < 3; ++k) {
+                double ck = 0.5 * ((double)lo[k] + (double)hi[k]);
+                double ek = 0.5 * ((double)hi[k] - (double)lo[k]);
+                c += A[r][k] * ck;
+                e += fabs(A[r][k]) * ek;
+            }
+            wlo[r] = fmin(wlo[r], c - e);
+            whi[r] = fmax(whi[r], c + e);
         }
-        double lo = c - e, hi = c + e;
+    };
+    auto node_box = [&](int node, int k, float* lo, float* hi) {
+        const float* f = reinterpret_cast<const float*>(a.nodes + 8 * (size_t)node);
+        for (int c = 0; c < 3; ++c) {
+            lo[c] = f[4 * (2 * c) + k];
+            hi[c] = f[4 * (2 * c + 1) + k];
+        }
+    };
+    const int root = as.node_base;
+    const int* rrefs = reinterpret_cast<const int*>(a.nodes + 8 * (size_t)root + 6);
+    for (int k = 0; k < 4; ++k) {
+        const int ref = rrefs[k];
+        if (ref == REF_EMPTY) continue;
+        float lo[3], hi[3];
+        if (ref < 0) {  // a leaf under the root: its own box
+            node_box(root, k, lo, hi);
+            add_box(lo, hi);
+            continue;
+        }
+        const int* crefs = reinterpret_cast<const int*>(a.nodes + 8 * (size_t)ref + 6);
+        for (int j = 0; j < 4; ++j) {
+            if (crefs[j] == REF_EMPTY) continue;
+            node_box(ref, j, lo, hi);
+            add_box(lo, hi);
+        }
+    }
+    for (int r = 0; r < 3; ++r) {
+        double lo = wlo[r], hi = whi[r];
         double pad = (fabs(lo) + fabs(hi)) * 1e-12 + 1e-30;
         box[r] = __double2float_rd(lo - pad);
         box[3 + r] = __double2float_ru(hi + pad);
