@@ -55,8 +55,11 @@ WORKLOADS = {
        "270x480 D455-like pinhole (87 deg hfov) depth + seg + face, max 10 m",
     4: "c4: Table II-shaped room + 15 floating obstacles, 512 envs/GPU (4096 over 8 GPUs), "
        "OS0-128-style LiDAR 128x512 range + seg, max 10 m",
-    5: "c5: Table I-shaped 20 cubes/env re-posed every step (TLAS refit), 2048 envs/GPU "
+    5: "c5: Table I-shaped 20 cubes/env re-posed every step (TLAS rebuild), 2048 envs/GPU "
        "(16384 over 8 GPUs), 135x240 depth + seg + face, max 10 m",
+    6: "c6 (f3): per-env unique terrain (32768 tri/env), every env's mesh re-randomised and "
+       "its BLAS rebuilt every step (agr_update_meshes), 256 envs/GPU, 135x240 depth + seg + face, "
+       "max 20 m",
 }
 
 
@@ -65,14 +68,15 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=3, choices=[3, 4, 5])
+    ap.add_argument("--config", type=int, default=3, choices=[3, 4, 5, 6])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--envs", type=int, default=None, help="envs per GPU (default: config's)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-counters", action="store_true")
-    ap.add_argument("--trbvh-rounds", type=int, default=3,
-                    help="treelet-restructuring passes on each BLAS (0 = plain LBVH)")
+    ap.add_argument("--trbvh-rounds", type=int, default=None,
+                    help="BLAS treelet-restructuring rounds (default 3; 0 for c6, whose BLAS "
+                         "are rebuilt every step: there the LBVH alone is the better trade)")
     ap.add_argument("--tlas-builder", default=None, choices=["lbvh", "sah"],
                     help="TLAS builder for agr_build (default: sah for the static c3/c4 "
                          "scenes, lbvh for c5, whose TLAS is rebuilt every step)")
@@ -87,7 +91,7 @@ def parse():
 def envs_per_gpu(args):
     if args.envs:
         return args.envs
-    return {3: 1024, 4: 512, 5: 2048}[args.config]
+    return {3: 1024, 4: 512, 5: 2048, 6: 256}[args.config]
 
 
 def make_workload(cfg, n_envs, env_base):
@@ -95,7 +99,21 @@ def make_workload(cfg, n_envs, env_base):
         return sg.config3(n_envs=n_envs, env_base=env_base)
     if cfg == 4:
         return sg.config4(n_envs=n_envs, env_base=env_base)
+    if cfg == 6:
+        return sg.config6(n_envs=n_envs, env_base=env_base, ring=2)
     return sg.config5(n_envs=n_envs, env_base=env_base, ring=8)
+
+
+def blas_launches(n_assets, trbvh_rounds):
+    """Kernels one agr_update_meshes batch launches (blas.cu blas_build_batch)."""
+    seg_passes = 0
+    while n_assets > 1 and ((n_assets - 1) >> (8 * seg_passes)) != 0:
+        seg_passes += 1
+    n = 5 + 4 * 3  # seg_of, init_bounds, radius, tri_prep, morton; 4 code passes
+    if n_assets > 1:
+        n += 2 + 3 * seg_passes
+    n += 2 + trbvh_rounds + (1 if trbvh_rounds > 0 else 0) + 4
+    return n
 
 
 def env_base(rank, envs_per_rank):
@@ -203,7 +221,7 @@ def run_reference(args):
     E = envs_per_gpu(args)
     sc, sensor = make_workload(cfg, E, 0)
     kind = "range" if cfg == 4 else "depth"
-    per_step = {3: 2500, 4: 20000, 5: 20000}[cfg]
+    per_step = {3: 2500, 4: 20000, 5: 20000, 6: 2000}[cfg]
     for w in range(args.warmup):
         oracle_rate(sc, sensor, kind, per_step // 4, 100 + w)
     times, rays = [], 0
@@ -256,11 +274,12 @@ def main():
     sc, sensor = make_workload(cfg, E, env_base(rank, E))  # this rank's block of global envs
     kind = agr.AGR_RANGE if cfg == 4 else agr.AGR_DEPTH
     chans = channels_for(cfg)
-    scene = agr.Scene.from_scenegen(sc, device=local, trbvh_rounds=args.trbvh_rounds)
+    trbvh_rounds = args.trbvh_rounds if args.trbvh_rounds is not None else (0 if cfg == 6 else 3)
+    scene = agr.Scene.from_scenegen(sc, device=local, trbvh_rounds=trbvh_rounds)
     scene.set_traversal(0 if args.traversal == "auto" else 1)
-    tlas_builder = args.tlas_builder or ("lbvh" if cfg == 5 else "sah")
+    tlas_builder = args.tlas_builder or ("lbvh" if cfg in (5, 6) else "sah")
     scene.set_tlas_builder(1 if tlas_builder == "sah" else 0)
-    step_refit = (args.tlas_step or ("build" if cfg == 5 else "refit")) == "refit"
+    step_refit = (args.tlas_step or ("build" if cfg in (5, 6) else "refit")) == "refit"
     rpe = rays_per_env(sensor)
     rays_per_step = E * rpe
     # inputs resident in HBM before timing
@@ -269,6 +288,11 @@ def main():
         T_steps = [ring[k] for k in range(ring.shape[0])]
     else:
         T_steps = [torch.from_numpy(sc.inst_T).to(dev)]
+    V_steps = None
+    if cfg == 6:
+        ringv = torch.from_numpy(sc.extra["ring_V"]).to(dev)
+        V_steps = [ringv[k] for k in range(ringv.shape[0])]
+        all_assets = list(range(len(sc.meshes)))
     poses = torch.from_numpy(sensor["poses"]).to(dev)
     beams = torch.from_numpy(sensor["beams"]).to(dev) if sensor["kind"] == "beams" else None
     scene.set_instance_transforms(T_steps[0])
@@ -280,18 +304,27 @@ def main():
     stream = torch.cuda.current_stream(dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
-    def step(k):
-        scene.set_instance_transforms(T_steps[k % len(T_steps)], stream)
+    def update(k):
+        """The per-step scene update: new poses (or, for c6, new meshes) and
+        the TLAS refit / rebuild."""
+        if V_steps is not None:
+            scene.update_meshes(all_assets, V_steps[k % len(V_steps)], stream)
+        else:
+            scene.set_instance_transforms(T_steps[k % len(T_steps)], stream)
         if step_refit:
             scene.refit(stream)
         else:
             scene.build(stream)
+
+    def step(k):
+        update(k)
         if beams is None:
             scene.cast_pinhole(sensor["cam"], poses, sensor["max_range"], kind, out=out, stream=stream)
         else:
             scene.cast_beams(beams, poses, sensor["max_range"], out=out, stream=stream)
 
-    LAUNCHES_PER_STEP = 3  # k_instances + k_tlas + k_cast
+    # k_instances + k_tlas + k_cast (+ the batched BLAS rebuild for c6)
+    LAUNCHES_PER_STEP = 3 + (blas_launches(len(sc.meshes), trbvh_rounds) if cfg == 6 else 0)
     for w in range(args.warmup):
         step(w)
     torch.cuda.synchronize()
@@ -307,11 +340,7 @@ def main():
             flush.zero_()
             e0, e1, e2 = ev[k]
             e0.record(stream)
-            scene.set_instance_transforms(T_steps[k % len(T_steps)], stream)
-            if step_refit:
-                scene.refit(stream)
-            else:
-                scene.build(stream)
+            update(k)
             e1.record(stream)
             if beams is None:
                 scene.cast_pinhole(sensor["cam"], poses, sensor["max_range"], kind, out=out, stream=stream)
@@ -352,9 +381,16 @@ def main():
                                 pin_memory=True) for c in chans}
         beams_h = torch.from_numpy(sensor["beams"]).pin_memory() if beams is not None else None
 
+        V_h = [v.cpu().pin_memory() for v in V_steps] if V_steps is not None else None
+        V_d = torch.empty_like(V_steps[0]) if V_steps is not None else None
+
         def e2e_step(k):
-            scene.set_instance_transforms(T_steps[k % len(T_steps)], stream)
-            scene.refit(stream) if step_refit else scene.build(stream)
+            if V_h is not None:  # c6: the step's new meshes come from the host
+                V_d.copy_(V_h[k % len(V_h)], non_blocking=True)
+                scene.update_meshes(all_assets, V_d, stream)
+                scene.refit(stream) if step_refit else scene.build(stream)
+            else:
+                update(k)
             stream.synchronize()
             if beams_h is None:
                 scene.cast_pinhole_host(sensor["cam"], poses_h, sensor["max_range"], kind, out=out_h)
@@ -372,7 +408,8 @@ def main():
         dt = time.perf_counter() - t0
         tt = reduce_max(torch.tensor([dt], dtype=torch.float64, device=dev), world)
         dt = float(tt[0])
-        h2d = poses_h.numel() * 4 + (beams_h.numel() * 4 if beams_h is not None else 0)
+        h2d = poses_h.numel() * 4 + (beams_h.numel() * 4 if beams_h is not None else 0) + \
+            (V_h[0].numel() * 4 if V_h is not None else 0)
         d2h = sum(v.numel() * 4 for v in out_h.values())
         e2e = {"value": rays_per_step * world * n_e2e / dt, "unit": "rays/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": n_e2e,
@@ -414,7 +451,7 @@ def main():
     cpu = None
     if not args.no_cpu_baseline:
         kind_s = "range" if cfg == 4 else "depth"
-        n_cpu = {3: 40000, 4: 200000, 5: 200000}[cfg]
+        n_cpu = {3: 40000, 4: 200000, 5: 200000, 6: 20000}[cfg]
         rate, tests_rate, dt, n = oracle_rate(sc, sensor, kind_s, n_cpu, 7)
         cpu = {"value": rate, "unit": "rays/s", "cores": cpu_cores(), "kind": "oracle",
                "sample": f"{n} uniform random rays of this rank's {E}-env workload ({dt:.1f} s wall)",
@@ -428,8 +465,11 @@ def main():
         "config": {"workload": WORKLOADS[cfg], "envs_per_gpu": E, "rays_per_step_per_gpu": rays_per_step,
                    "channels": list(chans), "parallelism": f"env-sharded x{world}",
                    "l2": "flushed between timed steps (256 MB write, untimed)",
-                   "step": "set_instance_transforms + TLAS " + ("refit" if step_refit else "rebuild") +
+                   "trbvh_rounds": trbvh_rounds,
+                   "step": ("update_meshes (every env's BLAS rebuilt)" if cfg == 6 else
+                            "set_instance_transforms") + " + TLAS " + ("refit" if step_refit else "rebuild") +
                            " + cast (TLAS builder: " + tlas_builder + ")"},
+        "update_ms_per_step": (total_ms - cast_total) / args.steps,
         "env_frames_per_sec": E * poses.shape[1] * world / (ms_per_step / 1e3),
         "cast_ms_per_step": cast_total / args.steps,
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,

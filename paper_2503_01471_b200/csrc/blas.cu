@@ -34,8 +34,15 @@ namespace {
 
 constexpr int T_BLK = 256;
 constexpr int RS_THREADS = 256;
-constexpr int RS_ROUNDS = 4;
-constexpr int RS_TILE = RS_THREADS * RS_ROUNDS;
+constexpr int RS_MIN_ROUNDS = 4;   // rounds of RS_THREADS keys per sort block
+constexpr int RS_MAX_BLOCKS = 1024;  // keeps the single-CTA histogram scan short
+
+// Keys per sort block: at least RS_MIN_ROUNDS x RS_THREADS, and few enough
+// blocks that the 256 x nblocks histogram scan stays small.
+inline int rs_rounds(int64_t F) {
+    int64_t r = (F + (int64_t)RS_THREADS * RS_MAX_BLOCKS - 1) / ((int64_t)RS_THREADS * RS_MAX_BLOCKS);
+    return (int)(r < RS_MIN_ROUNDS ? RS_MIN_ROUNDS : r);
+}
 constexpr uint32_t DEGENERATE_KEY = 0xFFFFFFFFu;
 constexpr unsigned FULL = 0xFFFFFFFFu;
 
@@ -55,6 +62,8 @@ struct Scratch {
     int* flags;          // [Ftot]
     int* depth;          // [B]
     float* cost;         // [Ftot] SAH cost of each internal node's subtree (TRBVH)
+    int* height;         // [Ftot] edges from each internal node to its deepest leaf
+    int* size;           // [Ftot] leaves under each internal node
 };
 
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
@@ -62,7 +71,8 @@ size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 size_t scratch_layout(int64_t F, int B, void* base, Scratch* out) {
     char* p = (char*)base;
     size_t used = 0;
-    const size_t nb = (size_t)((F + RS_TILE - 1) / RS_TILE);
+    const int64_t tile = (int64_t)RS_THREADS * rs_rounds(F);
+    const size_t nb = (size_t)((F + tile - 1) / tile);
     auto take = [&](size_t bytes) {
         char* q = p ? p + used : nullptr;
         used += align_up(bytes);
@@ -84,6 +94,8 @@ size_t scratch_layout(int64_t F, int B, void* base, Scratch* out) {
     s.flags = (int*)take(sizeof(int) * F);
     s.depth = (int*)take(sizeof(int) * B);
     s.cost = (float*)take(sizeof(float) * F);
+    s.height = (int*)take(sizeof(int) * F);
+    s.size = (int*)take(sizeof(int) * F);
     if (out) *out = s;
     return used + 256;
 }
@@ -222,12 +234,12 @@ __global__ void k_key_from(const uint32_t* __restrict__ vals, const uint32_t* __
 
 // ---- K2: stable LSD radix sort (8-bit digits) --------------------------------
 __global__ void k_rs_hist(const uint32_t* __restrict__ keys, int n, int shift,
-                          uint32_t* __restrict__ hist, int nblocks) {
+                          uint32_t* __restrict__ hist, int nblocks, int rounds) {
     __shared__ uint32_t cnt[256];
     cnt[threadIdx.x] = 0;
     __syncthreads();
-    int base = blockIdx.x * RS_TILE;
-    for (int r = 0; r < RS_ROUNDS; ++r) {
+    int base = blockIdx.x * RS_THREADS * rounds;
+    for (int r = 0; r < rounds; ++r) {
         int i = base + r * RS_THREADS + threadIdx.x;
         if (i < n) atomicAdd(&cnt[(keys[i] >> shift) & 255u], 1u);
     }
@@ -271,16 +283,16 @@ __global__ void k_rs_scan(uint32_t* hist, int total) {
 
 __global__ void k_rs_scatter(const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin,
                              uint32_t* __restrict__ kout, uint32_t* __restrict__ vout, int n,
-                             int shift, const uint32_t* __restrict__ hist, int nblocks) {
+                             int shift, const uint32_t* __restrict__ hist, int nblocks, int rounds) {
     __shared__ uint32_t base[256];
     __shared__ uint32_t wc[RS_THREADS / 32][256];
     base[threadIdx.x] = hist[threadIdx.x * nblocks + blockIdx.x];
     int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const unsigned lt = (1u << lane) - 1u;
-    for (int r = 0; r < RS_ROUNDS; ++r) {
+    for (int r = 0; r < rounds; ++r) {
         for (int k = 0; k < RS_THREADS / 32; ++k) wc[k][threadIdx.x] = 0;
         __syncthreads();
-        int i = blockIdx.x * RS_TILE + r * RS_THREADS + threadIdx.x;
+        int i = (blockIdx.x * rounds + r) * RS_THREADS + threadIdx.x;
         bool valid = i < n;
         uint32_t key = valid ? kin[i] : 0u;
         uint32_t val = valid ? vin[i] : 0u;
@@ -375,7 +387,7 @@ __device__ __forceinline__ void load_box_cg(const float* p, float b[6]) {
 __global__ void k_fit(const BlasSeg* segs, const int* seg_of, const uint32_t* bounds, int Ftot,
                       const uint32_t* __restrict__ sorted_all, const float* tri_box, int* child_all,
                       int* node_parent_all, int* leaf_parent_all, float* ibox_all, int* flags_all,
-                      int* depth) {
+                      int* height_all, int* size_all, int* depth) {
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= Ftot) return;
     const SegCtx c = seg_ctx(segs, seg_of, bounds, g);
@@ -384,26 +396,34 @@ __global__ void k_fit(const BlasSeg* segs, const int* seg_of, const uint32_t* bo
     AGR_SEG_VIEW(c);
     AGR_SEG_PARENTS(c);
     int* flags = flags_all + c.off;
-    // depth of this leaf
-    int dd = 0;
-    for (int q = leaf_parent[p]; q >= 0; q = node_parent[q]) ++dd;
-    atomicMax(depth + c.s, dd);
+    int* height = height_all + c.off;
+    int* size = size_all + c.off;
     int node = leaf_parent[p];
     while (node >= 0) {
         __threadfence();
         if (atomicAdd(&flags[node], 1) == 0) return;  // first arrival: sibling not ready
         __threadfence();
         float b[6], cc[6];
+        int h = 0, sz = 0;
         for (int side = 0; side < 2; ++side) {
             int r = child[2 * node + side];
             float* dst = side == 0 ? b : cc;
-            if (r < 0) load_box_cg(tri_box + 6 * sorted_prim[~r], dst);
-            else load_box_cg(ibox + 6 * r, dst);
+            if (r < 0) {
+                load_box_cg(tri_box + 6 * sorted_prim[~r], dst);
+                sz += 1;
+            } else {
+                load_box_cg(ibox + 6 * r, dst);
+                h = max(h, __ldcg(height + r));
+                sz += __ldcg(size + r);
+            }
         }
         for (int k = 0; k < 3; ++k) {
             __stcg(ibox + 6 * node + k, fminf(b[k], cc[k]));
             __stcg(ibox + 6 * node + 3 + k, fmaxf(b[3 + k], cc[3 + k]));
         }
+        __stcg(height + node, h + 1);
+        __stcg(size + node, sz);
+        if (node == 0) depth[c.s] = h + 1;  // the root: the tree's depth in edges
         node = node_parent[node];
     }
 }
@@ -432,12 +452,21 @@ __device__ __forceinline__ float box_area(const float b[6]) {
 // lane 0.  The DP visits partitions in the same order with the same strict
 // comparison as a serial DP, so the tree does not depend on the schedule.
 constexpr int TRB_THREADS = 64;
+// Treelets are formed only at nodes with at least TRB_GAMMA leaves below
+// (Karras & Aila's gamma): the many small subtrees near the leaves keep
+// their LBVH topology and only get their SAH cost recorded.
+#ifndef AGR_TRB_GAMMA
+#define AGR_TRB_GAMMA 16
+#endif
+constexpr int TRB_GAMMA = AGR_TRB_GAMMA;
 struct TrbWarp {
     float area[1 << TREELET];
     float copt[1 << TREELET];
     unsigned char part[1 << TREELET];
     float lb[TREELET][6];
     float lc[TREELET];
+    float la[TREELET];
+    int lsz[TREELET];
     int L[TREELET];
     int I[TREELET - 1];
     int m;
@@ -458,62 +487,62 @@ __device__ __forceinline__ void subset_box(const TrbWarp& w, int sset, float b[6
 // (all 32 lanes, warp-uniform arguments).
 __device__ void trbvh_treelet(TrbWarp& w, int lane, int node, int off, const uint32_t* __restrict__ sorted_all,
                               const float* __restrict__ tri_box, int* child_all, int* node_parent_all,
-                              int* leaf_parent_all, float* ibox_all, float* cost_all) {
+                              int* leaf_parent_all, float* ibox_all, float* cost_all, int* size_all) {
     const uint32_t* sorted_prim = sorted_all + off;
     int* child = child_all + 2 * off;
     int* node_parent = node_parent_all + off;
     int* leaf_parent = leaf_parent_all + off;
     float* ibox = ibox_all + 6 * (size_t)off;
     float* cost = cost_all + off;
+    int* size = size_all + off;
     auto ref_box = [&](int r, float b[6]) {
         const float* src = r < 0 ? tri_box + 6 * sorted_prim[~r] : ibox + 6 * r;
         for (int c = 0; c < 6; ++c) b[c] = __ldcg(src + c);
     };
-    if (lane == 0) {
-        // treelet leaves (subtree roots): open the largest-area one until 7
-        int m = 2, ni = 1;
-        w.L[0] = __ldcg(child + 2 * node);
-        w.L[1] = __ldcg(child + 2 * node + 1);
-        w.I[0] = node;
-        while (m < TREELET) {
-            int best = -1;
-            float ba = -1.0f;
-            for (int k = 0; k < m; ++k) {
-                if (w.L[k] < 0) continue;
-                float b[6];
-                ref_box(w.L[k], b);
-                const float a = box_area(b);
-                if (a > ba) { ba = a; best = k; }
-            }
-            if (best < 0) break;
-            const int r = w.L[best];
-            w.I[ni++] = r;
-            w.L[best] = __ldcg(child + 2 * r);
-            w.L[m++] = __ldcg(child + 2 * r + 1);
-        }
-        w.m = m;
-        // the node's current cost (children final)
+    // treelet formation: open the largest-area subtree root until 7; the
+    // two children of an opened node are fetched by lanes 0 and 1 at once
+    if (lane < 2) {
+        const int r = __ldcg(child + 2 * node + lane);
+        w.L[lane] = r;
+        ref_box(r, w.lb[lane]);
+        w.la[lane] = box_area(w.lb[lane]);
+        // the node's current cost: children's subtree costs (children final)
+        w.lc[lane] = r < 0 ? SAH_CT * w.la[lane] : __ldcg(cost + r);
+    } else if (lane == 2) {
         float nb[6];
         for (int c = 0; c < 6; ++c) nb[c] = __ldcg(ibox + 6 * node + c);
-        float ccur = SAH_CI * box_area(nb);
-        for (int side = 0; side < 2; ++side) {
-            const int r = __ldcg(child + 2 * node + side);
-            if (r < 0) {
-                float b[6];
-                ref_box(r, b);
-                ccur += SAH_CT * box_area(b);
-            } else {
-                ccur += __ldcg(cost + r);
-            }
-        }
-        w.ccur = ccur;
+        w.ccur = SAH_CI * box_area(nb);
     }
     __syncwarp();
-    const int m = w.m;
+    if (lane == 0) {
+        w.ccur = w.ccur + w.lc[0] + w.lc[1];
+        w.I[0] = node;
+    }
+    int m = 2, ni = 1;
+    while (m < TREELET) {
+        int best = -1;
+        float ba = -1.0f;
+        for (int k = 0; k < m; ++k)
+            if (w.L[k] >= 0 && w.la[k] > ba) { ba = w.la[k]; best = k; }
+        if (best < 0) break;
+        const int r = w.L[best];
+        __syncwarp();  // every lane has read L before it changes
+        if (lane < 2) {
+            const int c = __ldcg(child + 2 * r + lane);
+            const int slot = lane == 0 ? best : m;
+            w.L[slot] = c;
+            ref_box(c, w.lb[slot]);
+            w.la[slot] = box_area(w.lb[slot]);
+        }
+        if (lane == 0) w.I[ni] = r;
+        ++ni;
+        ++m;
+        __syncwarp();
+    }
     if (lane < m) {
         const int r = w.L[lane];
-        ref_box(r, w.lb[lane]);
-        w.lc[lane] = r < 0 ? SAH_CT * box_area(w.lb[lane]) : __ldcg(cost + r);
+        w.lc[lane] = r < 0 ? SAH_CT * w.la[lane] : __ldcg(cost + r);
+        w.lsz[lane] = r < 0 ? 1 : __ldcg(size + r);
     }
     __syncwarp();
     if (m < 3) {
@@ -571,6 +600,10 @@ __device__ void trbvh_treelet(TrbWarp& w, int lane, int node, int off, const uin
                         subset_box(w, sub, b);
                         for (int k = 0; k < 6; ++k) __stcg(ibox + 6 * c + k, b[k]);
                         __stcg(cost + c, w.copt[sub]);
+                        int sz = 0;
+                        for (int k = 0; k < TREELET; ++k)
+                            if ((sub >> k) & 1) sz += w.lsz[k];
+                        __stcg(size + c, sz);
                     }
                     __stcg(child + 2 * nd + side, c);
                     if (c < 0) __stcg(leaf_parent + ~c, nd);
@@ -588,7 +621,8 @@ __device__ void trbvh_treelet(TrbWarp& w, int lane, int node, int off, const uin
 __global__ void __launch_bounds__(TRB_THREADS) k_trbvh(
         const BlasSeg* segs, const int* seg_of, const uint32_t* bounds, int Ftot,
         const uint32_t* __restrict__ sorted_all, const float* __restrict__ tri_box, int* child_all,
-        int* node_parent_all, int* leaf_parent_all, float* ibox_all, float* cost_all, int* flags_all) {
+        int* node_parent_all, int* leaf_parent_all, float* ibox_all, float* cost_all, int* flags_all,
+        int* size_all) {
     __shared__ TrbWarp s_w[TRB_THREADS / 32];
     TrbWarp& w = s_w[threadIdx.x >> 5];
     const int lane = threadIdx.x & 31;
@@ -612,31 +646,69 @@ __global__ void __launch_bounds__(TRB_THREADS) k_trbvh(
             __threadfence();
         }
         active = claim;
-        unsigned mask = __ballot_sync(FULL, claim);
-        if (mask == 0) break;
+        if (!__any_sync(FULL, claim)) break;
+        bool big = false;
+        if (claim) {
+            big = __ldcg(size_all + off + node) >= TRB_GAMMA;
+            if (!big) {
+                // small subtree: keep its topology, record its SAH cost
+                const int* child = child_all + 2 * off;
+                const uint32_t* sorted_prim = sorted_all + off;
+                const float* ibox = ibox_all + 6 * (size_t)off;
+                float b[6];
+                for (int c = 0; c < 6; ++c) b[c] = __ldcg(ibox + 6 * node + c);
+                float cc = SAH_CI * box_area(b);
+                for (int side = 0; side < 2; ++side) {
+                    const int r = __ldcg(child + 2 * node + side);
+                    if (r < 0) {
+                        for (int c = 0; c < 6; ++c) b[c] = __ldcg(tri_box + 6 * sorted_prim[~r] + c);
+                        cc += SAH_CT * box_area(b);
+                    } else {
+                        cc += __ldcg(cost_all + off + r);
+                    }
+                }
+                __stcg(cost_all + off + node, cc);
+            }
+        }
+        unsigned mask = __ballot_sync(FULL, big);
         while (mask) {
             const int l = __ffs(mask) - 1;
             mask &= mask - 1;
             trbvh_treelet(w, lane, __shfl_sync(FULL, node, l), __shfl_sync(FULL, off, l), sorted_all, tri_box,
-                          child_all, node_parent_all, leaf_parent_all, ibox_all, cost_all);
+                          child_all, node_parent_all, leaf_parent_all, ibox_all, cost_all, size_all);
         }
         __threadfence();
         if (claim) node = __ldcg(node_parent_all + off + node);
     }
 }
 
+// Tree depth after restructuring: heights bottom-up (second arrival).
 __global__ void k_depth(const BlasSeg* segs, const int* seg_of, const uint32_t* bounds, int Ftot,
-                        const int* leaf_parent_all, const int* node_parent_all, int* depth) {
+                        const int* child_all, const int* leaf_parent_all, const int* node_parent_all,
+                        int* flags_all, int* height_all, int* depth) {
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= Ftot) return;
     const SegCtx c = seg_ctx(segs, seg_of, bounds, g);
     const int n = c.n, p = g - c.off;
     if (n < 2 || p >= n) return;
-    const int* leaf_parent = leaf_parent_all + c.off;
+    const int* child = child_all + 2 * c.off;
     const int* node_parent = node_parent_all + c.off;
-    int dd = 0;
-    for (int q = leaf_parent[p]; q >= 0; q = node_parent[q]) ++dd;
-    atomicMax(depth + c.s, dd);
+    int* flags = flags_all + c.off;
+    int* height = height_all + c.off;
+    int node = __ldcg(leaf_parent_all + c.off + p);
+    while (node >= 0) {
+        __threadfence();
+        if (atomicAdd(&flags[node], 1) == 0) return;
+        __threadfence();
+        int h = 0;
+        for (int side = 0; side < 2; ++side) {
+            const int r = __ldcg(child + 2 * node + side);
+            if (r >= 0) h = max(h, __ldcg(height + r));
+        }
+        __stcg(height + node, h + 1);
+        if (node == 0) depth[c.s] = h + 1;
+        node = __ldcg(node_parent + node);
+    }
 }
 
 // ---- K5: pack -------------------------------------------------------------------------
@@ -803,13 +875,14 @@ cudaError_t blas_build_batch(BlasSeg* h_segs, int B, const BlasBatchArgs& a, voi
     k_tri_prep<<<gb, T_BLK, 0, stream>>>(s.segs, s.seg_of, F, s.tri_box, s.vals[1], s.bounds);
     k_morton<<<gb, T_BLK, 0, stream>>>(s.seg_of, s.tri_box, s.vals[1], F, s.bounds, s.mcode, s.keys[0],
                                        s.vals[0]);
-    const int nb = (F + RS_TILE - 1) / RS_TILE;
+    const int rounds = rs_rounds(F);
+    const int nb = (F + RS_THREADS * rounds - 1) / (RS_THREADS * rounds);
     int cur = 0;
     auto pass = [&](int shift) {
-        k_rs_hist<<<nb, RS_THREADS, 0, stream>>>(s.keys[cur], F, shift, s.hist, nb);
+        k_rs_hist<<<nb, RS_THREADS, 0, stream>>>(s.keys[cur], F, shift, s.hist, nb, rounds);
         k_rs_scan<<<1, 1024, 0, stream>>>(s.hist, 256 * nb);
         k_rs_scatter<<<nb, RS_THREADS, 0, stream>>>(s.keys[cur], s.vals[cur], s.keys[cur ^ 1],
-                                                    s.vals[cur ^ 1], F, shift, s.hist, nb);
+                                                    s.vals[cur ^ 1], F, shift, s.hist, nb, rounds);
         cur ^= 1;
     };
     for (int shift = 0; shift < 32; shift += 8) pass(shift);
@@ -828,15 +901,18 @@ cudaError_t blas_build_batch(BlasSeg* h_segs, int B, const BlasBatchArgs& a, voi
     k_karras<<<gb, T_BLK, 0, stream>>>(s.segs, s.seg_of, s.bounds, F, sk, s.child, s.node_parent,
                                        s.leaf_parent);
     k_fit<<<gb, T_BLK, 0, stream>>>(s.segs, s.seg_of, s.bounds, F, sv, s.tri_box, s.child, s.node_parent,
-                                    s.leaf_parent, s.ibox, s.flags, s.depth);
+                                    s.leaf_parent, s.ibox, s.flags, s.height, s.size, s.depth);
     for (int round = 0; round < a.trbvh_rounds; ++round) {
         cudaMemsetAsync(s.flags, 0, sizeof(int) * F, stream);
         k_trbvh<<<(F + TRB_THREADS - 1) / TRB_THREADS, TRB_THREADS, 0, stream>>>(s.segs, s.seg_of, s.bounds, F, sv, s.tri_box, s.child,
-                                                  s.node_parent, s.leaf_parent, s.ibox, s.cost, s.flags);
+                                                  s.node_parent, s.leaf_parent, s.ibox, s.cost, s.flags,
+                                                  s.size);
     }
     if (a.trbvh_rounds > 0) {
         cudaMemsetAsync(s.depth, 0, sizeof(int) * B, stream);
-        k_depth<<<gb, T_BLK, 0, stream>>>(s.segs, s.seg_of, s.bounds, F, s.leaf_parent, s.node_parent, s.depth);
+        cudaMemsetAsync(s.flags, 0, sizeof(int) * F, stream);
+        k_depth<<<gb, T_BLK, 0, stream>>>(s.segs, s.seg_of, s.bounds, F, s.child, s.leaf_parent, s.node_parent,
+                                          s.flags, s.height, s.depth);
     }
     k_pack_nodes<<<gb, T_BLK, 0, stream>>>(s.segs, s.seg_of, s.bounds, F, sv, s.tri_box, s.child, s.ibox,
                                            a.bnodes);

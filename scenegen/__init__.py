@@ -303,7 +303,7 @@ def assemble(meshes, per_env):
                  np.asarray(labels, np.int32), T)
 
 
-CONFIG_SEED = {1: 1001, 2: 1002, 3: 1003, 4: 1004, 5: 1005}
+CONFIG_SEED = {1: 1001, 2: 1002, 3: 1003, 4: 1004, 5: 1005, 6: 1006}
 
 
 def config1():
@@ -410,11 +410,53 @@ def config5(n_envs=2048, env_base=0, ring=64):
                     max_range=10.0, kind="pinhole")
 
 
+def terrain_mesh(rng, n=128, size=20.0, amp=1.2, name="terrain") -> Mesh:
+    """Heightfield over x in [0, size], y in [-size/2, size/2]: (n+1)^2
+    vertices, 2 n^2 triangles; height = four random plane waves of
+    decreasing amplitude (a per-env unique, non-instanced mesh)."""
+    x = np.linspace(0.0, size, n + 1)
+    y = np.linspace(-size / 2, size / 2, n + 1)
+    X, Y = np.meshgrid(x, y, indexing="ij")
+    Z = np.zeros_like(X)
+    for k in range(4):
+        kx, ky = rng.uniform(0.2, 1.2, 2) * rng.choice([-1.0, 1.0], 2)
+        Z += amp / (k + 1) * np.sin(kx * X + ky * Y + rng.uniform(0.0, 2.0 * np.pi))
+    verts = np.stack([X, Y, Z], -1).reshape(-1, 3).astype(np.float32)
+    idx = np.arange((n + 1) * (n + 1)).reshape(n + 1, n + 1)
+    a, b, c, d = idx[:-1, :-1], idx[1:, :-1], idx[1:, 1:], idx[:-1, 1:]
+    faces = np.concatenate([np.stack([a, b, c], -1).reshape(-1, 3),
+                            np.stack([a, c, d], -1).reshape(-1, 3)]).astype(np.int32)
+    return Mesh(name, verts, faces)
+
+
+def config6(n_envs=256, env_base=0, ring=2, n=128):
+    """c6 (PAPER.md:226 per-env merged mesh rebuilt at
+    reset): one unique terrain asset per env (2 n^2 = 32768 triangles at
+    n = 128), re-randomised at every step: extra["ring_V"] float32
+    [ring][E * V][3] holds `ring` vertex sets (env-major, as
+    agr_update_meshes takes them); step k uses set k % ring.  135x240 87 deg
+    depth camera 5 m above the terrain's edge, pitched down 25 deg."""
+    meshes, ring_v = [], []
+    for i, e in enumerate(range(env_base, env_base + n_envs)):
+        rng = env_rng(CONFIG_SEED[6], e)
+        ms = [terrain_mesh(rng, n, name=f"terrain{e}") for _ in range(ring)]
+        meshes.append(ms[0])
+        ring_v.append(np.stack([m.verts for m in ms]))
+    per_env = [[(i, 1, make_T(np.eye(3), (0.0, 0.0, 0.0)))] for i in range(n_envs)]
+    sc = assemble(meshes, per_env)
+    sc.env_base = env_base
+    sc.extra["ring_V"] = np.ascontiguousarray(np.concatenate(ring_v, 1))
+    P = np.zeros((n_envs, 1, 3, 4), np.float32)
+    P[:, 0, :, :3] = rot_y(math.radians(25.0))
+    P[:, 0, :, 3] = (-2.0, 0.0, 5.0)
+    return sc, dict(cam=pinhole(240, 135, 87.0), poses=P, max_range=20.0, kind="pinhole")
+
+
 def make_config(c: int, n_envs=None, env_base=0):
     if c == 1:
         return config1()
     kw = {} if n_envs is None else dict(n_envs=n_envs)
-    return {2: config2, 3: config3, 4: config4, 5: config5}[c](env_base=env_base, **kw)
+    return {2: config2, 3: config3, 4: config4, 5: config5, 6: config6}[c](env_base=env_base, **kw)
 
 
 # ----------------------------------------------------------------------------

@@ -502,3 +502,26 @@ def test_update_meshes_batched_equals_one_by_one():
         sa.update_meshes([1, 1], v)
     with pytest.raises(agr.AgrError):
         sa.update_meshes([E], v)
+
+
+def test_c6_unique_terrain_reset_small():
+    """c6 shape at small size: one unique terrain asset
+    per env, every env's mesh replaced at reset by one agr_update_meshes
+    batch; full oracle parity before and after the reset."""
+    sc, sensor = sg.config6(n_envs=6, ring=2, n=24)
+    sensor = dict(sensor, cam=sg.pinhole(40, 24, 87.0))
+    s = make_scene(sc)
+    s.set_tlas_builder(0)
+    got = to_np(cast_sensor(s, sensor, "depth"))
+    ref = oracle.cast(sc, oracle_rays(sensor, "depth"))
+    compare(ref, got["dist"], got["seg"], got["face"], "c6 before reset")
+    assert (got["face"] >= 0).mean() > 0.5
+    ring = sc.extra["ring_V"]
+    s.update_meshes(list(range(6)), torch.from_numpy(ring[1]).to(dev()))
+    s.build()
+    got = to_np(cast_sensor(s, sensor, "depth"))
+    V = len(sc.meshes[0].verts)
+    sc2 = sg.assemble([sg.Mesh(m.name, ring[1][i * V:(i + 1) * V], m.faces) for i, m in enumerate(sc.meshes)],
+                      [[(i, 1, sc.inst_T[i])] for i in range(6)])
+    ref = oracle.cast(sc2, oracle_rays(sensor, "depth"))
+    compare(ref, got["dist"], got["seg"], got["face"], "c6 after reset")
