@@ -50,6 +50,7 @@ class _Scene(ctypes.Structure):
         ("n_envs", ctypes.c_int32), ("env_off", ctypes.c_void_p),
         ("inst_asset", ctypes.c_void_p), ("inst_label", ctypes.c_void_p),
         ("inst_T", ctypes.c_void_p),
+        ("annot", ctypes.c_void_p), ("annot_k", ctypes.c_int32),
     ]
 
 
@@ -78,7 +79,7 @@ def _load():
         _lib.oracle_cast.restype = ctypes.c_int
         _lib.oracle_cast.argtypes = [ctypes.POINTER(_Scene), ctypes.POINTER(_Rays),
                                      ctypes.c_void_p, ctypes.c_int64, ctypes.c_double,
-                                     ctypes.c_int32] + [ctypes.c_void_p] * 11
+                                     ctypes.c_int32] + [ctypes.c_void_p] * 12
         _lib.oracle_last_tests.restype = ctypes.c_int64
         _lib.oracle_certify.restype = ctypes.c_int
         _lib.oracle_certify.argtypes = [ctypes.POINTER(_Scene), ctypes.POINTER(_Rays),
@@ -105,10 +106,11 @@ class OracleResult:
     bary: np.ndarray = None    # float64 [n][2]
     point: np.ndarray = None   # float64 [n][3]
     valid: np.ndarray = None   # int32 [n] stereo shadow mask (stereo=...)
+    annot: np.ndarray = None   # float64 [n][K] interpolated vertex annotations (annot=...)
 
 
 def cast(scene, rays: dict, query=None, n_threads: int = 0, amb_eps: float = AMB_EPS,
-         graze: bool = False, extras: bool = False, stereo=None) -> OracleResult:
+         graze: bool = False, extras: bool = False, stereo=None, annot=None) -> OracleResult:
     """Run the oracle.
 
     ``scene``: an object with numpy fields ``verts, vert_off, faces, face_off,
@@ -116,9 +118,11 @@ def cast(scene, rays: dict, query=None, n_threads: int = 0, amb_eps: float = AMB
     ``rays``: dict with ``model`` and the fields of oracle_rays.
     ``query``: int64 flat ray ids (default: every ray).
     ``stereo``: (offset xyz in the sensor frame, eps) -> also the shadow mask.
+    ``annot``: per-asset list of float [V][K] vertex annotations (None for an
+    asset without any) -> also the interpolated annotation of each hit.
     """
     lib = _load()
-    sc, r, keep, total = _marshal(scene, rays)
+    sc, r, keep, total = _marshal(scene, rays, annot)
     if query is None:
         query = np.arange(total, dtype=np.int64)
     q = np.ascontiguousarray(query, dtype=np.int64)
@@ -134,10 +138,13 @@ def cast(scene, rays: dict, query=None, n_threads: int = 0, amb_eps: float = AMB
         out.normal = np.empty((n, 3), np.float64)
         out.bary = np.empty((n, 2), np.float64)
         out.point = np.empty((n, 3), np.float64)
+    if annot is not None:
+        out.annot = np.empty((n, sc.annot_k), np.float64)
     rc = lib.oracle_cast(ctypes.byref(sc), ctypes.byref(r), _ptr(q), n, amb_eps, n_threads,
                          _ptr(out.t64), _ptr(out.dist), _ptr(out.seg), _ptr(out.face),
                          _ptr(out.amb), _ptr(out.t2), _ptr(out.graze) if graze else None,
-                         _ptr(out.normal), _ptr(out.bary), _ptr(out.point), _ptr(out.valid))
+                         _ptr(out.normal), _ptr(out.bary), _ptr(out.point), _ptr(out.valid),
+                         _ptr(out.annot))
     if rc != 0:
         raise ValueError("oracle_cast rejected its input")
     out.tests = int(lib.oracle_last_tests())
@@ -165,7 +172,7 @@ def certify(scene, rays: dict, face, query=None, n_threads: int = 0):
     return t_face, outside, label
 
 
-def _marshal(scene, rays):
+def _marshal(scene, rays, annot=None):
     keep = []
 
     def arr(x, dt):
@@ -179,7 +186,14 @@ def _marshal(scene, rays):
                 _ptr(arr(scene.faces, np.int32)), _ptr(arr(scene.face_off, np.int64)),
                 len(scene.env_off) - 1, _ptr(arr(scene.env_off, np.int64)),
                 _ptr(arr(scene.inst_asset, np.int32)), _ptr(arr(scene.inst_label, np.int32)),
-                _ptr(arr(scene.inst_T, np.float32)))
+                _ptr(arr(scene.inst_T, np.float32)), None, 0)
+    if annot is not None:
+        K = max(np.asarray(a).reshape(len(m.verts), -1).shape[1]
+                for a, m in zip(annot, scene.meshes) if a is not None)
+        rows = [np.full((len(m.verts), K), np.nan, np.float32) if a is None
+                else np.asarray(a, np.float32).reshape(len(m.verts), K) for a, m in zip(annot, scene.meshes)]
+        A = arr(np.concatenate(rows), np.float32)
+        sc.annot, sc.annot_k = _ptr(A), K
     m = rays["model"]
     r = _Rays()
     r.model = m

@@ -44,6 +44,7 @@ typedef struct {
     int64_t n_tri;
     v3* v;          /* [n_tri][3] world (env-local) vertices */
     int32_t* label; /* [n_tri] label of the owning instance  */
+    int64_t* vid;   /* [n_tri][3] scene-global vertex ids (annotations) */
     int64_t cap;
 } world_mesh;
 
@@ -65,9 +66,11 @@ static int world_triangles(const oracle_scene* sc, int32_t e, world_mesh* w) {
     if (n > w->cap) {
         free(w->v);
         free(w->label);
+        free(w->vid);
         w->v = (v3*)malloc(sizeof(v3) * 3 * (size_t)(n > 0 ? n : 1));
         w->label = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n > 0 ? n : 1));
-        if (!w->v || !w->label) return -1;
+        w->vid = (int64_t*)malloc(sizeof(int64_t) * 3 * (size_t)(n > 0 ? n : 1));
+        if (!w->v || !w->label || !w->vid) return -1;
         w->cap = n;
     }
     int64_t k = 0;
@@ -77,6 +80,7 @@ static int world_triangles(const oracle_scene* sc, int32_t e, world_mesh* w) {
         for (int64_t f = sc->face_off[a]; f < sc->face_off[a + 1]; ++f, ++k) {
             for (int c = 0; c < 3; ++c) {
                 int64_t vi = sc->vert_off[a] + sc->faces[3 * f + c];
+                w->vid[3 * k + c] = vi;
                 const float* p = sc->verts + 3 * vi;
                 double x = p[0], y = p[1], z = p[2];
                 v3 q;
@@ -286,14 +290,14 @@ typedef struct {
     double eps;
     double* t64; float* dist; int32_t* seg; int32_t* face; int32_t* amb;
     double* t2; double* graze;
-    double* normal; double* bary; double* point; int32_t* valid;
+    double* normal; double* bary; double* point; int32_t* valid; double* annot;
     int64_t tests;
     int status;
 } job;
 
 static void* worker(void* arg) {
     job* jb = (job*)arg;
-    world_mesh w = {0, NULL, NULL, 0};
+    world_mesh w = {0, NULL, NULL, NULL, 0};
     int64_t cur_env = -1;
     jb->tests = 0;
     jb->status = 0;
@@ -321,6 +325,21 @@ static void* worker(void* arg) {
             if (jb->point) jb->point[3 * q + k] = rr.point[k];
         }
         if (jb->bary) { jb->bary[2 * q] = rr.bary[0]; jb->bary[2 * q + 1] = rr.bary[1]; }
+        if (jb->annot) {
+            /* PAPER.md:228 vertex-level annotations, interpolated with the
+             * winning face's barycentrics (SPEC S:550 query_annotation) */
+            const int32_t K = jb->sc->annot_k;
+            for (int32_t k = 0; k < K; ++k) {
+                double val = NAN;
+                if (rr.face >= 0) {
+                    const int64_t* vi = w.vid + 3 * (int64_t)rr.face;
+                    const float* A = jb->sc->annot;
+                    val = (1.0 - rr.bary[0] - rr.bary[1]) * (double)A[vi[0] * K + k] +
+                          rr.bary[0] * (double)A[vi[1] * K + k] + rr.bary[1] * (double)A[vi[2] * K + k];
+                }
+                jb->annot[(int64_t)K * q + k] = val;
+            }
+        }
         if (jb->valid) {
             int shadow_amb = 0;
             jb->valid[q] = stereo_valid(jb->r, id, &w, &rr, o, d, jb->eps, &shadow_amb);
@@ -329,6 +348,7 @@ static void* worker(void* arg) {
     }
     free(w.v);
     free(w.label);
+    free(w.vid);
     return NULL;
 }
 
@@ -354,8 +374,9 @@ int oracle_cast(const oracle_scene* sc, const oracle_rays* r,
                 const int64_t* query, int64_t n_query, double eps,
                 int32_t n_threads, double* t64, float* dist, int32_t* seg,
                 int32_t* face, int32_t* amb, double* t2, double* graze,
-                double* normal, double* bary, double* point, int32_t* valid) {
+                double* normal, double* bary, double* point, int32_t* valid, double* annot) {
     if (validate(sc, r) != 0) return -1;
+    if (annot && (!sc->annot || sc->annot_k <= 0)) return -1;
     int64_t n_rays_total;
     if (r->model == ORACLE_RAYS) n_rays_total = (int64_t)sc->n_envs * r->R;
     else if (r->model == ORACLE_PINHOLE) n_rays_total = (int64_t)sc->n_envs * r->S * r->H * r->W;
@@ -386,7 +407,7 @@ int oracle_cast(const oracle_scene* sc, const oracle_rays* r,
         jb->eps = eps;
         jb->t64 = t64; jb->dist = dist; jb->seg = seg; jb->face = face;
         jb->amb = amb; jb->t2 = t2; jb->graze = graze;
-        jb->normal = normal; jb->bary = bary; jb->point = point; jb->valid = valid;
+        jb->normal = normal; jb->bary = bary; jb->point = point; jb->valid = valid; jb->annot = annot;
         if (n_threads == 1) worker(jb);
         else if (pthread_create(&th[i], NULL, worker, jb) != 0) { jb->status = -1; th[i] = 0; }
     }
@@ -419,7 +440,7 @@ typedef struct {
 
 static void* cert_worker(void* arg) {
     cert_job* jb = (cert_job*)arg;
-    world_mesh w = {0, NULL, NULL, 0};
+    world_mesh w = {0, NULL, NULL, NULL, 0};
     int64_t cur_env = -1;
     jb->status = 0;
     for (int64_t i = jb->lo; i < jb->hi; ++i) {
@@ -454,6 +475,7 @@ static void* cert_worker(void* arg) {
     }
     free(w.v);
     free(w.label);
+    free(w.vid);
     return NULL;
 }
 

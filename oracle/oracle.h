@@ -48,6 +48,11 @@ typedef struct {
     const int32_t* inst_asset; /* [n_inst]                                    */
     const int32_t* inst_label; /* [n_inst]                                    */
     const float*   inst_T;     /* [n_inst][3][4] row-major: x' = A x + b      */
+    /* optional per-vertex annotations ("embed vertex-level
+     * annotations that can be queried"): [sum V][annot_k], indexed like
+     * verts; NaN rows = asset without annotations.  NULL / 0 = none.        */
+    const float*   annot;
+    int32_t        annot_k;
 } oracle_scene;
 
 /* Ray models. */
@@ -103,6 +108,9 @@ enum {
  *            face's vertices, from the plane hit point by cross-product
  *            area ratios; -1 on a miss                          [may be NULL]
  *   point[3q..] o + t d (t = the reported distance)             [may be NULL]
+ *   annot[K q..] barycentric interpolation (1-b1-b2) A(v0) + b1 A(v1) +
+ *            b2 A(v2) of the winning face's vertex annotations (scene
+ *            annot, K = annot_k); NaN on a miss              [may be NULL]
  *   valid[q] stereo shadow mask: 0 if the segment from the hit point p to
  *            the second sensor o2 = P (stereo) hits a triangle at a distance
  *            in (eps, |o2 - p| - eps) from p, else 1 (1 on a miss; PINHOLE
@@ -116,7 +124,8 @@ int oracle_cast(const oracle_scene* scene, const oracle_rays* rays,
                 int32_t n_threads,
                 double* t64, float* dist, int32_t* seg, int32_t* face,
                 int32_t* amb, double* t2, double* graze,
-                double* normal, double* bary, double* point, int32_t* valid);
+                double* normal, double* bary, double* point, int32_t* valid,
+                double* annot);
 
 /*
  * Certificate of a reported face (SURVEY.md §8(c) "Full-scale certificate",

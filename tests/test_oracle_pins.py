@@ -689,3 +689,52 @@ def test_certify_agrees_with_cast_on_its_own_answer():
     assert np.all(out[hit] <= 1e-12)
     assert np.array_equal(lab, r.seg)
     assert np.all(np.isnan(t[~hit]))
+
+
+# --------------------------------------------------------------------------
+# vertex annotations (f1; "embed vertex-level annotations that
+# can be queried"; SPEC S:550-556 query_annotation examples)
+# --------------------------------------------------------------------------
+
+def test_annotation_vertex_centroid_and_miss():
+    """Ray through vertex v_k -> exactly A(v_k); through the centroid ->
+    the mean of the three annotations; a miss -> NaN."""
+    v = np.asarray([[2, -1, -1], [2, 1, -1], [2, 0, 1]], np.float32)
+    sc = sg.assemble([sg.Mesh("t", v, np.asarray([[0, 1, 2]], np.int32))],
+                     [[(0, 1, sg.make_T(np.eye(3), (0, 0, 0)))]])
+    A = np.asarray([[1.0, -2.0], [4.0, 0.5], [-3.0, 8.0]], np.float32)
+    cen = v.astype(np.float64).mean(0)
+    d = np.concatenate([v, cen[None], [[-1.0, 0.0, 0.0]]]).astype(np.float32)[None]
+    o = np.zeros_like(d)
+    r = cast_rays(sc, o, d, annot=[A])
+    assert np.allclose(r.annot[:3], A, atol=1e-12)
+    assert np.allclose(r.annot[3], A.astype(np.float64).mean(0), atol=1e-7)  # FP32 centroid direction
+    assert np.all(np.isnan(r.annot[4]))
+
+
+def test_annotation_linear_field_reproduction():
+    """A linear field of the object-space vertex coordinates interpolates to
+    the same field at the object-space hit point A^-1 (p - b) (S:555-556
+    'linear-reproduction oracle'), under a random similarity transform, for
+    K = 3 fields; an asset without annotations yields NaN."""
+    rng = np.random.default_rng(31)
+    verts = rng.uniform(-1, 1, (60, 3)).astype(np.float32)
+    soup = sg.Mesh("soup", verts, np.arange(60, dtype=np.int32).reshape(20, 3))
+    wall = sg.Mesh("wall", np.asarray([[9, -50, -50], [9, 50, -50], [9, 0, 50]], np.float32),
+                   np.asarray([[0, 1, 2]], np.int32))
+    T = sg.make_T(sg.random_rotation(rng), (3.0, 0.2, -0.1), 1.1)
+    sc = sg.assemble([soup, wall], [[(0, 2, T), (1, 3, sg.make_T(np.eye(3), (0, 0, 0)))]])
+    M = np.asarray([[1.0, 0.0, 0.0], [2.0, -1.0, 0.5], [0.0, 0.25, 3.0]])
+    c = np.asarray([0.0, 0.5, -1.0])
+    field = (verts.astype(np.float64) @ M.T + c).astype(np.float32)
+    o = np.zeros((1, 3000, 3), np.float32)
+    d = rng.uniform([2.0, -1.5, -1.5], [4.0, 1.5, 1.5], (1, 3000, 3)).astype(np.float32)
+    r = cast_rays(sc, o, d, extras=True, annot=[field, None])
+    on_soup = (r.face >= 0) & (r.face < 20)
+    assert on_soup.sum() > 200 and (r.face == 20).sum() > 100
+    A, b = T[:, :3].astype(np.float64), T[:, 3].astype(np.float64)
+    p_obj = np.linalg.solve(A, (r.point[on_soup] - b).T).T
+    want = p_obj @ M.T + c
+    # the FP32-rounded field values carry ~1e-7 relative error
+    assert np.allclose(r.annot[on_soup], want, atol=2e-6)
+    assert np.all(np.isnan(r.annot[r.face == 20]))
