@@ -57,7 +57,7 @@
 extern "C" {
 #endif
 
-#define AGR_ABI_VERSION 2
+#define AGR_ABI_VERSION 3
 
 typedef int32_t agr_status;
 enum {
@@ -124,6 +124,11 @@ typedef struct {
                              (eps, L - eps) from the hit point, else 1; 1 on
                              a miss.  Pinhole and beam casts only (explicit
                              rays write 1).                                  */
+    float* annot;         /* [..][k] vertex annotations of the hit face
+                             (agr_set_vertex_annotations) interpolated with
+                             its barycentrics: (1-b1-b2) A(v0) + b1 A(v1) +
+                             b2 A(v2); NaN on a miss or on an asset without
+                             annotations.  EINVAL if none were set.          */
 } agr_outputs;
 
 /* Scene statistics (sizes in elements / bytes of library-owned memory). */
@@ -200,6 +205,19 @@ agr_status agr_set_instance_transforms(agr_scene scene, const float* T, void* st
  */
 agr_status agr_update_mesh(agr_scene scene, int32_t asset, const float* verts, int32_t n_verts,
                            void* stream);
+
+/*
+ * Per-vertex annotations of asset `asset` ("embed vertex-level
+ * annotations that can be queried"): `values` device float [n_verts][k],
+ * k in [1, AGR_MAX_ANNOT], the same k for every asset of the scene (fixed
+ * by the first call).  Copied into library memory on `stream` (async;
+ * `values` may be reused once the stream passes this point).  Assets never
+ * given annotations read NaN.  Casts with out.annot interpolate them.
+ * EINVAL on a bad asset, a vertex-count mismatch or a k mismatch.
+ */
+#define AGR_MAX_ANNOT 8
+agr_status agr_set_vertex_annotations(agr_scene scene, int32_t asset, const float* values, int32_t n_verts,
+                                      int32_t k, void* stream);
 
 /*
  * Batched agr_update_mesh: replace the vertices of the n distinct assets

@@ -55,13 +55,13 @@ class agr_pinhole(ctypes.Structure):
 class agr_outputs(ctypes.Structure):
     _fields_ = [("dist", ctypes.c_void_p), ("seg", ctypes.c_void_p), ("face", ctypes.c_void_p),
                 ("normal", ctypes.c_void_p), ("bary", ctypes.c_void_p), ("point", ctypes.c_void_p),
-                ("valid", ctypes.c_void_p)]
+                ("valid", ctypes.c_void_p), ("annot", ctypes.c_void_p)]
 
 
 # channel -> (torch dtype name, trailing vector size)
 CHANNELS = {"dist": ("float32", None), "seg": ("int32", None), "face": ("int32", None),
             "normal": ("float32", 3), "bary": ("float32", 2), "point": ("float32", 3),
-            "valid": ("int32", None)}
+            "valid": ("int32", None), "annot": ("float32", "k")}  # k: the scene's annotation width
 
 
 class agr_create_options(ctypes.Structure):
@@ -92,6 +92,7 @@ _SIGS = {
     "agr_build": (_I32, [_P, _P]),
     "agr_update_mesh": (_I32, [_P, _I32, _P, _I32, _P]),
     "agr_update_meshes": (_I32, [_P, _I32, _P, _P, _P]),
+    "agr_set_vertex_annotations": (_I32, [_P, _I32, _P, _I32, _I32, _P]),
     "agr_refit": (_I32, [_P, _P]),
     "agr_cast_pinhole": (_I32, [_P, ctypes.POINTER(agr_pinhole), _I32, _P, _I32, ctypes.c_float,
                                 agr_outputs, _P]),
@@ -197,6 +198,7 @@ class Scene:
         self.handle = h
         self.device = device
         self.n_envs = len(env_offsets) - 1
+        self.annot_k = 0
         self.n_inst = n_inst
 
     @classmethod
@@ -226,6 +228,14 @@ class Scene:
         _check(load().agr_update_mesh(self.handle, int(asset), _ptr(verts), int(verts.shape[0]),
                                       _stream_handle(stream)))
 
+    def set_vertex_annotations(self, asset: int, values, stream=None):
+        """values: CUDA float32 [V, k] per-vertex annotations of `asset` (same k
+        for every asset); casts with the "annot" channel interpolate them."""
+        v = values if values.dim() == 2 else values.reshape(values.shape[0], -1)
+        _check(load().agr_set_vertex_annotations(self.handle, int(asset), _ptr(v), int(v.shape[0]),
+                                                 int(v.shape[1]), _stream_handle(stream)))
+        self.annot_k = int(v.shape[1])
+
     def update_meshes(self, assets, verts, stream=None):
         """Batched update_mesh: ``assets`` a sequence of distinct asset ids,
         ``verts`` CUDA float32 [sum V, 3] (their vertex arrays concatenated in
@@ -252,6 +262,10 @@ class Scene:
         out = {}
         for ch in channels:
             dt, vec = CHANNELS[ch]
+            if vec == "k":
+                if not self.annot_k:
+                    raise AgrError(AGR_EINVAL, "annot requested but no vertex annotations set")
+                vec = self.annot_k
             shp = tuple(shape) + ((vec,) if vec else ())
             out[ch] = torch.empty(shp, dtype=getattr(torch, dt), device=dev,
                                   pin_memory=pin and not device_tensors)

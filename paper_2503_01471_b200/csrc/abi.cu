@@ -88,6 +88,10 @@ struct agr_scene_s {
     // asset meshes kept on the device for BLAS rebuilds (agr_update_mesh)
     float* mesh_verts = nullptr;
     int* mesh_faces = nullptr;
+    int* asset_voff = nullptr;  // [n_assets] first vertex / face of each asset (device)
+    int* asset_foff = nullptr;
+    float* annot = nullptr;     // [sum V][annot_k] vertex annotations, NaN = none
+    int annot_k = 0;
     void* blas_scratch = nullptr;
     std::vector<int64_t> h_mvert_off, h_mface_off;
     std::vector<int> h_node_base, h_leaf_base, h_nverts, h_nfaces;
@@ -138,6 +142,11 @@ struct agr_scene_s {
         v.inst_asset = inst_asset;
         v.assets = assets;
         v.n_envs = n_envs;
+        v.annot = annot;
+        v.annot_k = annot_k;
+        v.mesh_faces = mesh_faces;
+        v.asset_voff = asset_voff;
+        v.asset_foff = asset_foff;
         return v;
     }
 
@@ -363,8 +372,20 @@ agr_status agr_scene_create_ex(int32_t device, const agr_mesh* meshes, int32_t n
     }
     s->h_node_base = node_base;
     s->h_leaf_base = leaf_base;
+    if (s->h_mvert_off[n_meshes] > 0x3FFFFFFF) return bail(fail(AGR_EUNSUPPORTED, "too many vertices"));
     CKB(s->alloc(&s->mesh_verts, 3 * (size_t)s->h_mvert_off[n_meshes]));
     CKB(s->alloc(&s->mesh_faces, 3 * (size_t)s->h_mface_off[n_meshes]));
+    {
+        std::vector<int> vo(n_meshes), fo(n_meshes);
+        for (int a = 0; a < n_meshes; ++a) {
+            vo[a] = (int)s->h_mvert_off[a];
+            fo[a] = (int)s->h_mface_off[a];
+        }
+        CKB(s->alloc(&s->asset_voff, n_meshes));
+        CKB(s->alloc(&s->asset_foff, n_meshes));
+        CKB(cudaMemcpy(s->asset_voff, vo.data(), sizeof(int) * n_meshes, cudaMemcpyHostToDevice));
+        CKB(cudaMemcpy(s->asset_foff, fo.data(), sizeof(int) * n_meshes, cudaMemcpyHostToDevice));
+    }
     // scratch for a batch of every asset (any update batch fits in it)
     CKB(s->alloc((char**)&s->blas_scratch, blas_scratch_bytes(s->h_mface_off[n_meshes], n_meshes)));
     cudaError_t err = cudaSuccess;
@@ -496,6 +517,29 @@ agr_status agr_update_meshes(agr_scene s, int32_t n, const int32_t* assets, cons
     return AGR_OK;
 }
 
+agr_status agr_set_vertex_annotations(agr_scene s, int32_t asset, const float* values, int32_t n_verts,
+                                      int32_t k, void* stream) {
+    g_err.clear();
+    if (!s) return fail(AGR_EINVAL, "scene is NULL");
+    if (asset < 0 || asset >= s->n_assets) return fail(AGR_EINVAL, "asset %d out of range", asset);
+    if (!values || n_verts != s->h_nverts[asset])
+        return fail(AGR_EINVAL, "asset %d has %d vertices (got %d)", asset, s->h_nverts[asset], n_verts);
+    if (k < 1 || k > AGR_MAX_ANNOT) return fail(AGR_EINVAL, "k must be in [1, %d]", AGR_MAX_ANNOT);
+    if (s->annot_k != 0 && k != s->annot_k)
+        return fail(AGR_EINVAL, "the scene's annotations have k = %d (got %d)", s->annot_k, k);
+    DeviceGuard guard(s->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (!s->annot) {
+        const size_t n = (size_t)k * s->h_mvert_off[s->n_assets];
+        CK(s->alloc(&s->annot, n));
+        CK(cudaMemsetAsync(s->annot, 0xFF, sizeof(float) * n, st));  // all-ones bits: NaN
+        s->annot_k = k;
+    }
+    CK(cudaMemcpyAsync(s->annot + (size_t)k * s->h_mvert_off[asset], values, sizeof(float) * k * (size_t)n_verts,
+                       cudaMemcpyDeviceToDevice, st));
+    return AGR_OK;
+}
+
 agr_status agr_build(agr_scene s, void* stream) {
     g_err.clear();
     if (!s) return fail(AGR_EINVAL, "scene is NULL");
@@ -516,8 +560,9 @@ agr_status agr_refit(agr_scene s, void* stream) {
     return AGR_OK;
 }
 
-static agr_status check_cast_state(agr_scene s, float max_range) {
+static agr_status check_cast_state(agr_scene s, float max_range, const agr_outputs& out) {
     if (!s) return fail(AGR_EINVAL, "scene is NULL");
+    if (out.annot && s->annot_k == 0) return fail(AGR_EINVAL, "annot requested but no vertex annotations set");
     if (!s->built) return fail(AGR_ESTATE, "cast before the first agr_build");
     if (s->dirty) return fail(AGR_ESTATE, "transforms changed since the last agr_build/agr_refit");
     if (!(max_range > 0.0f) || !std::isfinite(max_range)) return fail(AGR_EINVAL, "max_range must be > 0");
@@ -548,6 +593,7 @@ static CastArgs base_args(agr_scene s, float max_range, agr_outputs out) {
     a.out_bary = out.bary;
     a.out_point = out.point;
     a.out_valid = out.valid;
+    a.out_annot = out.annot;
     for (int k = 0; k < 3; ++k) a.stereo[k] = s->stereo[k];
     a.stereo_eps = s->stereo_eps;
     a.env_begin = 0;
@@ -559,7 +605,7 @@ static CastArgs base_args(agr_scene s, float max_range, agr_outputs out) {
 agr_status agr_cast_pinhole(agr_scene s, const agr_pinhole* cam, agr_distance kind, const float* poses,
                             int32_t n_sensors, float max_range, agr_outputs out, void* stream) {
     g_err.clear();
-    agr_status st = check_cast_state(s, max_range);
+    agr_status st = check_cast_state(s, max_range, out);
     if (st != AGR_OK) return st;
     if (!cam || !poses || n_sensors < 1) return fail(AGR_EINVAL, "need cam, poses and n_sensors >= 1");
     if (cam->width < 1 || cam->height < 1 || !(cam->fx > 0.0f) || !(cam->fy > 0.0f))
@@ -585,7 +631,7 @@ agr_status agr_cast_pinhole(agr_scene s, const agr_pinhole* cam, agr_distance ki
 agr_status agr_cast_beams(agr_scene s, const float* dirs, int32_t C, int32_t K, const float* poses,
                           int32_t n_sensors, float max_range, agr_outputs out, void* stream) {
     g_err.clear();
-    agr_status st = check_cast_state(s, max_range);
+    agr_status st = check_cast_state(s, max_range, out);
     if (st != AGR_OK) return st;
     if (!dirs || !poses || C < 1 || K < 1 || n_sensors < 1)
         return fail(AGR_EINVAL, "need dirs, poses, C, K, n_sensors >= 1");
@@ -603,7 +649,7 @@ agr_status agr_cast_beams(agr_scene s, const float* dirs, int32_t C, int32_t K, 
 agr_status agr_cast_rays(agr_scene s, const float* orig, const float* dir, int32_t R, float max_range,
                          agr_outputs out, void* stream) {
     g_err.clear();
-    agr_status st = check_cast_state(s, max_range);
+    agr_status st = check_cast_state(s, max_range, out);
     if (st != AGR_OK) return st;
     if (!orig || !dir || R < 1) return fail(AGR_EINVAL, "need orig, dir and R >= 1");
     DeviceGuard guard(s->device);
@@ -657,9 +703,10 @@ struct E2EChannel {
 
 static agr_status e2e_run(agr_scene s, CastArgs& a, int64_t elems_per_env, agr_outputs out_host) {
     const int E = s->n_envs;
-    E2EChannel ch[7] = {{out_host.dist, 4}, {out_host.seg, 4}, {out_host.face, 4},
-                        {out_host.normal, 12}, {out_host.bary, 8}, {out_host.point, 12},
-                        {out_host.valid, 4}};
+    constexpr int NCH = 8;
+    E2EChannel ch[NCH] = {{out_host.dist, 4}, {out_host.seg, 4}, {out_host.face, 4},
+                          {out_host.normal, 12}, {out_host.bary, 8}, {out_host.point, 12},
+                          {out_host.valid, 4}, {out_host.annot, 4 * s->annot_k}};
     int64_t bytes_per_elem = 0;
     bool direct = true;
     for (auto& c : ch)
@@ -693,9 +740,9 @@ static agr_status e2e_run(agr_scene s, CastArgs& a, int64_t elems_per_env, agr_o
         c.env_begin = e0;
         c.env_end = e1;
         c.out_env_base = e0;  // the chunk's outputs start at env e0 of the chunk buffer
-        char* dev[7];
+        char* dev[NCH];
         char* p = base;
-        for (int q = 0; q < 7; ++q) {
+        for (int q = 0; q < NCH; ++q) {
             dev[q] = ch[q].host ? p : nullptr;
             if (ch[q].host) p += ch[q].bytes * n;
         }
@@ -706,6 +753,7 @@ static agr_status e2e_run(agr_scene s, CastArgs& a, int64_t elems_per_env, agr_o
         c.out_bary = (float*)dev[4];
         c.out_point = (float*)dev[5];
         c.out_valid = (int*)dev[6];
+        c.out_annot = (float*)dev[7];
         c.sv = s->view();
         c.exact = s->exact;
         c.packet = s->traversal == 0 ? 1 : 0;
@@ -715,7 +763,7 @@ static agr_status e2e_run(agr_scene s, CastArgs& a, int64_t elems_per_env, agr_o
         CK(cudaStreamWaitEvent(xs, s->e2e_event[slot], 0));
         const int64_t off = (int64_t)e0 * elems_per_env;
         if (direct) {
-            for (int q = 0; q < 7; ++q)
+            for (int q = 0; q < NCH; ++q)
                 if (ch[q].host)
                     CK(cudaMemcpyAsync((char*)ch[q].host + off * ch[q].bytes, dev[q], ch[q].bytes * n,
                                        cudaMemcpyDeviceToHost, xs));
@@ -725,7 +773,7 @@ static agr_status e2e_run(agr_scene s, CastArgs& a, int64_t elems_per_env, agr_o
             CK(cudaEventRecord(s->e2e_event[2 + slot], xs));
             CK(cudaEventSynchronize(s->e2e_event[2 + slot]));
             const char* hsrc = (const char*)s->e2e_host[slot];
-            for (int q = 0; q < 7; ++q)
+            for (int q = 0; q < NCH; ++q)
                 if (ch[q].host) {
                     memcpy((char*)ch[q].host + off * ch[q].bytes, hsrc, ch[q].bytes * n);
                     hsrc += ch[q].bytes * n;
@@ -741,7 +789,7 @@ agr_status agr_cast_pinhole_host(agr_scene s, const agr_pinhole* cam, agr_distan
                                  const float* poses_host, int32_t n_sensors, float max_range,
                                  agr_outputs out_host) {
     g_err.clear();
-    agr_status st = check_cast_state(s, max_range);
+    agr_status st = check_cast_state(s, max_range, out_host);
     if (st != AGR_OK) return st;
     if (!cam || !poses_host || n_sensors < 1) return fail(AGR_EINVAL, "need cam, poses and n_sensors >= 1");
     if (cam->width < 1 || cam->height < 1 || !(cam->fx > 0.0f) || !(cam->fy > 0.0f))
@@ -751,7 +799,7 @@ agr_status agr_cast_pinhole_host(agr_scene s, const agr_pinhole* cam, agr_distan
     if (st != AGR_OK) return st;
     CK(cudaMemcpyAsync(s->e2e_poses, poses_host, sizeof(float) * 12 * (size_t)n_sensors * s->n_envs,
                        cudaMemcpyHostToDevice, s->e2e_stream[0]));
-    CastArgs a = base_args(s, max_range, agr_outputs{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr});
+    CastArgs a = base_args(s, max_range, agr_outputs{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr});
     a.model = 1;
     a.kind = (int)kind;
     a.W = cam->width;
@@ -771,7 +819,7 @@ agr_status agr_cast_beams_host(agr_scene s, const float* dirs_host, int32_t C, i
                                const float* poses_host, int32_t n_sensors, float max_range,
                                agr_outputs out_host) {
     g_err.clear();
-    agr_status st = check_cast_state(s, max_range);
+    agr_status st = check_cast_state(s, max_range, out_host);
     if (st != AGR_OK) return st;
     if (!dirs_host || !poses_host || C < 1 || K < 1 || n_sensors < 1)
         return fail(AGR_EINVAL, "need dirs, poses, C, K, n_sensors >= 1");
@@ -788,7 +836,7 @@ agr_status agr_cast_beams_host(agr_scene s, const float* dirs_host, int32_t C, i
     CK(cudaMemcpyAsync(s->e2e_beams, dirs_host, bb, cudaMemcpyHostToDevice, s->e2e_stream[0]));
     CK(cudaMemcpyAsync(s->e2e_poses, poses_host, sizeof(float) * 12 * (size_t)n_sensors * s->n_envs,
                        cudaMemcpyHostToDevice, s->e2e_stream[0]));
-    CastArgs a = base_args(s, max_range, agr_outputs{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr});
+    CastArgs a = base_args(s, max_range, agr_outputs{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr});
     a.model = 2;
     a.W = K;
     a.H = C;

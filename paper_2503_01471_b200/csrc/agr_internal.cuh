@@ -68,6 +68,12 @@ struct SceneView {
     const int* inst_asset;    // [n_inst]
     const AssetInfo* assets;  // [n_assets]
     int n_envs;
+    // vertex annotations (f1): [sum V][annot_k] by asset vertex, NaN = none
+    const float* annot;
+    int annot_k;
+    const int* mesh_faces;    // [sum F][3] asset-local vertex ids (face order)
+    const int* asset_voff;    // [n_assets] first vertex of each asset in annot rows
+    const int* asset_foff;    // [n_assets] first face of each asset in mesh_faces
 };
 
 // ---- small vector helpers --------------------------------------------------
@@ -246,6 +252,7 @@ struct CastArgs {
     float* out_bary;      // [..][2]
     float* out_point;     // [..][3]
     int* out_valid;       // stereo shadow mask (1 valid, 0 shadowed)
+    float* out_annot;     // [..][annot_k] interpolated vertex annotations
     float stereo[3];      // second sensor origin in the sensor frame
     float stereo_eps;     // self-hit guard (metres)
     int env_begin, env_end;  // envs cast by this launch (chunking)

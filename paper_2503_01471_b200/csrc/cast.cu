@@ -790,10 +790,13 @@ __device__ __noinline__ void write_extra(const CastArgs* a, RayId id, Best64 bes
         a->out_point[3 * o + 1] = (float)(r.o.y + t * r.d.y);
         a->out_point[3 * o + 2] = (float)(r.o.z + t * r.d.z);
     }
-    if (!a->out_normal && !a->out_bary) return;
+    if (!a->out_normal && !a->out_bary && !a->out_annot) return;
+    const int K = a->sv.annot_k;
     if (best.face < 0) {
         if (a->out_normal) a->out_normal[3 * o] = a->out_normal[3 * o + 1] = a->out_normal[3 * o + 2] = 0.0f;
         if (a->out_bary) a->out_bary[2 * o] = a->out_bary[2 * o + 1] = -1.0f;
+        if (a->out_annot)
+            for (int k = 0; k < K; ++k) a->out_annot[(int64_t)K * o + k] = __int_as_float(0x7fc00000);
         return;
     }
     const float* T = a->sv.inst_T + 12 * best.inst;
@@ -814,7 +817,7 @@ __device__ __noinline__ void write_extra(const CastArgs* a, RayId id, Best64 bes
         a->out_normal[3 * o + 1] = (float)(n.y * s);
         a->out_normal[3 * o + 2] = (float)(n.z * s);
     }
-    if (a->out_bary) {
+    if (a->out_bary || a->out_annot) {
         // Moller-Trumbore barycentrics of the FP64 ray: weights of v1, v2
         const d3 p = crossd(r.d, e2);
         const double det = dotd(e1, p);
@@ -822,8 +825,25 @@ __device__ __noinline__ void write_extra(const CastArgs* a, RayId id, Best64 bes
         const double b1 = dotd(s, p) / det;
         const d3 q = crossd(s, e1);
         const double b2 = dotd(r.d, q) / det;
-        a->out_bary[2 * o + 0] = (float)b1;
-        a->out_bary[2 * o + 1] = (float)b2;
+        if (a->out_bary) {
+            a->out_bary[2 * o + 0] = (float)b1;
+            a->out_bary[2 * o + 1] = (float)b2;
+        }
+        if (a->out_annot) {
+            // PAPER.md:228 vertex-level annotations of the winning face,
+            // interpolated with its FP64 barycentrics (reading R23)
+            const int asset = __ldg(a->sv.inst_asset + best.inst);
+            const int f = __float_as_int(__ldg(&a->sv.tris[3 * best.leaf + 2].w));  // asset-local face
+            const int* fv = a->sv.mesh_faces + 3 * (int64_t)(__ldg(a->sv.asset_foff + asset) + f);
+            const int vb = __ldg(a->sv.asset_voff + asset);
+            const float* A0 = a->sv.annot + (int64_t)K * (vb + __ldg(fv));
+            const float* A1 = a->sv.annot + (int64_t)K * (vb + __ldg(fv + 1));
+            const float* A2 = a->sv.annot + (int64_t)K * (vb + __ldg(fv + 2));
+            for (int k = 0; k < K; ++k)
+                a->out_annot[(int64_t)K * o + k] =
+                    (float)((1.0 - b1 - b2) * (double)__ldg(A0 + k) + b1 * (double)__ldg(A1 + k) +
+                            b2 * (double)__ldg(A2 + k));
+        }
     }
 }
 
@@ -960,7 +980,7 @@ __global__ void __launch_bounds__(CAST_THREADS, CAST_MIN_BLOCKS) k_cast(const __
     if (a.out_dist) __stcs(a.out_dist + id.out, hit ? (float)best.t : a.max_range);
     if (a.out_seg) __stcs(a.out_seg + id.out, hit ? __ldg(a.sv.inst_label + best.inst) : -1);
     if (a.out_face) __stcs(a.out_face + id.out, hit ? best.face : -1);
-    if (a.out_normal || a.out_bary || a.out_point) write_extra<MODEL>(&a, id, best);
+    if (a.out_normal || a.out_bary || a.out_point || a.out_annot) write_extra<MODEL>(&a, id, best);
     if (a.out_valid) __stcs(a.out_valid + id.out, valid ? 1 : 0);  // 1 without STEREO (explicit rays)
 }
 

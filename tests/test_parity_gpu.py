@@ -525,3 +525,55 @@ def test_c6_unique_terrain_reset_small():
                       [[(i, 1, sc.inst_T[i])] for i in range(6)])
     ref = oracle.cast(sc2, oracle_rays(sensor, "depth"))
     compare(ref, got["dist"], got["seg"], got["face"], "c6 after reset")
+
+
+# ---- f1: interpolated vertex annotations -------------------------------------------
+
+def _c2_annotations(sc, rng):
+    """k = 3 annotations: random values on the cube, the object-space
+    coordinates (a linear field) on the cylinder, none on the panel."""
+    cube, cyl, _ = sc.meshes
+    return [rng.uniform(-5, 5, (len(cube.verts), 3)).astype(np.float32),
+            cyl.verts.astype(np.float32).copy(), None]
+
+
+@pytest.mark.parametrize("kind", ["depth", "range"])
+def test_annotations_c2_vs_oracle(kind):
+    """Interpolated vertex annotations against the oracle on
+    every ray whose face equals the oracle's; NaN on misses and on the
+    un-annotated panel."""
+    sc, sensor = sg.config2(n_envs=16)
+    s = make_scene(sc)
+    A = _c2_annotations(sc, np.random.default_rng(17))
+    for a, vals in enumerate(A):
+        if vals is not None:
+            s.set_vertex_annotations(a, torch.from_numpy(vals).to(dev()))
+    got = to_np(cast_sensor(s, sensor, kind, channels=("dist", "seg", "face", "annot")))
+    ref = oracle.cast(sc, oracle_rays(sensor, kind), annot=A)
+    compare(ref, got["dist"], got["seg"], got["face"], "annot")
+    ann = got["annot"].reshape(-1, 3)
+    same = got["face"] == ref.face
+    finite = np.isfinite(ref.annot).all(1)
+    assert np.array_equal(np.isfinite(ann).all(1)[same], finite[same])
+    err = np.abs(ann[same & finite] - ref.annot[same & finite])
+    assert err.max() <= 1e-5 * (1.0 + np.abs(ref.annot[same & finite]).max()), err.max()
+    assert (same & finite).sum() > 10000 and (same & ~finite & (ref.face >= 0)).sum() > 100
+
+
+def test_annotations_host_path_and_errors():
+    sc, sensor = sg.config2(n_envs=5)
+    s = make_scene(sc)
+    with pytest.raises(agr.AgrError):  # no annotations set yet
+        cast_sensor(s, sensor, "depth", channels=("dist", "annot"))
+    A = _c2_annotations(sc, np.random.default_rng(3))
+    s.set_vertex_annotations(0, torch.from_numpy(A[0]).to(dev()))
+    with pytest.raises(agr.AgrError):  # k differs from the scene's
+        s.set_vertex_annotations(1, torch.from_numpy(A[1][:, :2].copy()).to(dev()))
+    with pytest.raises(agr.AgrError):  # vertex count mismatch
+        s.set_vertex_annotations(1, torch.from_numpy(A[0]).to(dev()))
+    dev_out = to_np(cast_sensor(s, sensor, "depth", channels=("dist", "face", "annot")))
+    poses = torch.from_numpy(np.ascontiguousarray(sensor["poses"])).pin_memory()
+    host = s.cast_pinhole_host(sensor["cam"], poses, sensor["max_range"], agr.AGR_DEPTH,
+                               channels=("dist", "face", "annot"))
+    for k in dev_out:
+        assert np.array_equal(dev_out[k], host[k].numpy().reshape(-1), equal_nan=True), k
