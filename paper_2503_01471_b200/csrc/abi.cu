@@ -262,7 +262,7 @@ agr_status agr_scene_create_ex(int32_t device, const agr_mesh* meshes, int32_t n
         faces_total += m.n_faces;
         verts_total += m.n_verts;
     }
-    if (faces_total > 0x3FFFFFFF) return fail(AGR_EUNSUPPORTED, "too many faces");
+    if (faces_total > LEAF_MASK - 4) return fail(AGR_EUNSUPPORTED, "too many faces");
     for (int64_t j = 0; j < n_inst; ++j) {
         if (inst[j].asset < 0 || inst[j].asset >= n_meshes)
             return fail(AGR_EINVAL, "instance %lld: asset %d out of range", (long long)j, inst[j].asset);

@@ -11,9 +11,13 @@
 //           root are visited).  Boxes of the 4 children stored per axis:
 //             f0 = lo.x[4], f1 = hi.x[4], f2 = lo.y[4], f3 = hi.y[4],
 //             f4 = lo.z[4], f5 = hi.z[4], f6 = ref[4] (int bits), f7 = (n, -)
-//           ref >= 0: global node index; ref < 0: leaf ~index (triangle
-//           record for BLAS nodes, global instance for TLAS nodes);
-//           REF_EMPTY: no child (its box is +inf everywhere, never hit).
+//           ref >= 0: global node index; ref < 0: leaf ~x (TLAS: x = global
+//           instance; BLAS: x = first | (count - 1) << LEAF_SHIFT, a leaf of
+//           `count` <= LEAF_MAX consecutive triangle records whose box is
+//           their union -- a binary subtree over at most LEAF_MAX
+//           consecutive leaves is referenced as one such leaf instead of
+//           getting BVH4 nodes of its own); REF_EMPTY: no child (its box is
+//           +inf everywhere, never hit).
 //   bnodes  the binary LBVH of every BLAS (64-B nodes: child boxes + refs),
 //           kept for structural checks (agr_debug_export_blas).
 //   tris    float4[3] per BLAS leaf, 48 B (FP32 filter test, object space):
@@ -35,6 +39,12 @@
 namespace agr {
 
 constexpr int REF_EMPTY = (int)0x80000000;  // INT32_MIN
+#ifndef AGR_LEAF_MAX
+#define AGR_LEAF_MAX 2
+#endif
+constexpr int LEAF_MAX = AGR_LEAF_MAX;      // triangles per BLAS leaf (1..4)
+constexpr int LEAF_SHIFT = 29;              // BLAS leaf ref: count - 1 in bits 29-30
+constexpr int LEAF_MASK = (1 << LEAF_SHIFT) - 1;  // first record (faces_total < LEAF_MASK - 4, abi.cu)
 constexpr int STACK_SIZE = 96;              // traversal stack entries per ray
 constexpr int MAX_TLAS_N = 1024;            // AGR_MAX_INSTANCES_PER_ENV
 

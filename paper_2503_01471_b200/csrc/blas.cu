@@ -27,6 +27,7 @@
 #include "agr_internal.cuh"
 
 #include <cfloat>
+#include <climits>
 #include <vector>
 
 namespace agr {
@@ -787,6 +788,29 @@ __global__ void k_collapse4(const BlasSeg* segs, const int* seg_of, const uint32
     for (int k = 0; k < 4; ++k) {
         child_box(refs[k], sorted_prim, tri_box, ibox, boxes[k]);
         gr[k] = global_ref(refs[k], node_base, leaf_base);
+        if (refs[k] >= 0 && LEAF_MAX > 1) {
+            // a binary subtree over <= LEAF_MAX consecutive leaves becomes
+            // one multi-triangle leaf
+            int st[2 * LEAF_MAX], sp = 0, nl = 0, lmin = INT_MAX, lmax = -1;
+            bool ok = true;
+            st[sp++] = refs[k];
+            while (sp > 0 && ok) {
+                const int x = st[--sp];
+                if (x < 0) {
+                    ok = nl < LEAF_MAX;
+                    ++nl;
+                    lmin = min(lmin, ~x);
+                    lmax = max(lmax, ~x);
+                } else if (sp + 2 <= 2 * LEAF_MAX) {
+                    st[sp++] = __ldg(child + 2 * x + 1);
+                    st[sp++] = __ldg(child + 2 * x);
+                } else {
+                    ok = false;
+                }
+            }
+            if (ok && lmax - lmin + 1 == nl)
+                gr[k] = ~((leaf_base + lmin) | ((nl - 1) << LEAF_SHIFT));
+        }
     }
     write_node4(nodes, node_base + j, boxes, gr, cnt);
 }

@@ -158,7 +158,10 @@ def test_large_mesh_multiblock_sort():
         assert leaf_face[i] < leaf_face[i + 1]
 
 
-def _walk_bvh4(nodes, root, leaf_boxes=None):
+LEAF_SHIFT = 29  # agr_internal.cuh: BLAS leaf ref x = first | (count - 1) << 29
+
+
+def _walk_bvh4(nodes, root, leaf_boxes=None, blas=True):
     """Collect leaves reachable from BVH4 node 0; check every child box
     contains the boxes of its subtree (exactly: the union)."""
     refs = nodes[:, 24:28].view(np.int32)
@@ -179,9 +182,15 @@ def _walk_bvh4(nodes, root, leaf_boxes=None):
                 continue
             lo, hi = box(n, k)
             if r < 0:
-                leaves.append(~r)
+                x = ~r
+                # BLAS multi-triangle leaf: consecutive records, box = their union
+                first, count = (x & ((1 << LEAF_SHIFT) - 1), (x >> LEAF_SHIFT) + 1) if blas else (x, 1)
+                group = list(range(first, first + count))
+                leaves.extend(group)
                 if leaf_boxes is not None:
-                    blo, bhi = leaf_boxes(~r)
+                    bl = [leaf_boxes(l) for l in group]
+                    blo = np.min([b[0] for b in bl], 0)
+                    bhi = np.max([b[1] for b in bl], 0)
                     assert np.array_equal(lo, blo) and np.array_equal(hi, bhi)
             else:
                 clo, chi = rec(r - root)
@@ -215,7 +224,7 @@ def test_bvh4_tlas_covers_every_instance_once():
     s = make_scene(sc)
     for e in range(5):
         nodes, root = s.debug_export_bvh4(-1 - e)
-        leaves = _walk_bvh4(nodes, root)
+        leaves = _walk_bvh4(nodes, root, blas=False)
         assert sorted(leaves) == list(range(int(sc.env_off[e]), int(sc.env_off[e + 1])))
 
 
