@@ -148,7 +148,8 @@ AGR_HD float half_area(const float b[6]) {
 // internal node, < 0 leaf.  child(r, side) and box(r, b[6]) read the binary
 // tree.  Returns the number of children; unused refs are REF_EMPTY.
 template <class CHILD, class BOX>
-__device__ __forceinline__ int collapse4(int j, const CHILD& child, const BOX& box, int refs[4]) {
+__device__ __forceinline__ int collapse4(int j, const CHILD& child, const BOX& box, int refs[4],
+                                         bool keep_pairs = false) {
     refs[0] = child(j, 0);
     refs[1] = child(j, 1);
     refs[2] = refs[3] = REF_EMPTY;
@@ -157,7 +158,9 @@ __device__ __forceinline__ int collapse4(int j, const CHILD& child, const BOX& b
         int best = -1;
         float best_a = -1.0f;
         for (int k = 0; k < cnt; ++k) {
-            if (refs[k] >= 0) {
+            // keep_pairs: a node over two leaves stays closed (it becomes a
+            // pair leaf) and the slot goes to a larger subtree
+            if (refs[k] >= 0 && !(keep_pairs && child(refs[k], 0) < 0 && child(refs[k], 1) < 0)) {
                 float b[6];
                 box(refs[k], b);
                 float a = half_area(b);

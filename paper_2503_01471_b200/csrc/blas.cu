@@ -28,6 +28,10 @@
 
 #include <cfloat>
 #include <climits>
+
+#ifndef AGR_KEEP_PAIRS
+#define AGR_KEEP_PAIRS 0
+#endif
 #include <vector>
 
 namespace agr {
@@ -777,7 +781,7 @@ __global__ void k_collapse4(const BlasSeg* segs, const int* seg_of, const uint32
         auto bx = [&](int r, float bb[6]) {
             for (int k = 0; k < 6; ++k) bb[k] = __ldcg(ibox + 6 * r + k);
         };
-        cnt = collapse4(j, ch, bx, refs);
+        cnt = collapse4(j, ch, bx, refs, AGR_KEEP_PAIRS != 0);
     } else {
         refs[0] = n == 1 ? ~0 : REF_EMPTY;
         refs[1] = refs[2] = refs[3] = REF_EMPTY;

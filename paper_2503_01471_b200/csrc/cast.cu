@@ -62,9 +62,20 @@ __device__ __forceinline__ float rcp_approx(float x) {
     return r;
 }
 
+// Flush-to-zero variant (one MUFU.RCP, no denormal fix-up): for inputs with
+// 1e-30 <= |x| < 8.5e37, where neither the input nor the result is
+// denormal -- safe_inv's inputs (ray direction components, offset by
+// copysign(1e-30)) are in that range for any ray with finite, sub-1e37
+// object-space direction.
+__device__ __forceinline__ float rcp_approx_ftz(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
 __device__ __forceinline__ float safe_inv(float d) {
     // d + copysign(1e-30, d) == d unless |d| < ~1e-22: never a zero divisor
-    return rcp_approx(d + copysignf(1e-30f, d));
+    return rcp_approx_ftz(d + copysignf(1e-30f, d));
 }
 
 __device__ __forceinline__ SlabRay make_slab(f3 o, f3 d, float delta) {
@@ -453,7 +464,7 @@ constexpr unsigned KEY_MISS = 0x7f800000u;  // +inf bits: sorts after every hit 
 // its U < 0 (shadow queries).
 template <bool ANYHIT, bool COUNT, class LEAF>
 __device__ __forceinline__ void traverse_lane(const SceneView& sv, int env, RayState& rs,
-                                              const LEAF& leaf_fn, bool& sovf, Counters& cnt) {
+                                              const LEAF& leaf_fn, int& sovf, Counters& cnt) {
     int stack[STACK_SIZE];
     int sp = 0;
     int node = __ldg(sv.tlas_root + env);
@@ -485,7 +496,7 @@ __device__ __forceinline__ void traverse_lane(const SceneView& sv, int env, RayS
             for (int k = 3; k >= 1; --k) {
                 if (k < nh) {
                     if (sp < STACK_SIZE) stack[sp++] = ref[k];
-                    else sovf = true;
+                    else sovf = 1;
                 }
             }
             node = ref[0];
@@ -501,7 +512,7 @@ __device__ __forceinline__ void traverse_lane(const SceneView& sv, int env, RayS
         if (rs.cur_inst < 0) {
             if (COUNT) cnt.insts++;
             if (sp < STACK_SIZE) stack[sp++] = SENTINEL;
-            else { sovf = true; break; }
+            else { sovf = 1; break; }
             node = rs.enter_instance(sv, leaf);
             continue;
         }
@@ -528,7 +539,7 @@ constexpr int PSTACK = 96;
 
 template <bool ANYHIT, bool COUNT, class LEAF>
 __device__ __forceinline__ void traverse_packet(const SceneView& sv, int env, RayState& rs,
-                                                const LEAF& leaf_fn, bool& sovf, int* wstack,
+                                                const LEAF& leaf_fn, int& sovf, int* wstack,
                                                 Counters& cnt) {
     const unsigned FULL = 0xFFFFFFFFu;
     const bool leader = (threadIdx.x & 31) == 0;
@@ -545,8 +556,8 @@ __device__ __forceinline__ void traverse_packet(const SceneView& sv, int env, Ra
             bool h[4];
             rs.node4_test(f, tn, h);
             // 4-bit mask of the children some lane hits
-            const unsigned cm = (__ballot_sync(FULL, h[0]) ? 1u : 0u) | (__ballot_sync(FULL, h[1]) ? 2u : 0u) |
-                                (__ballot_sync(FULL, h[2]) ? 4u : 0u) | (__ballot_sync(FULL, h[3]) ? 8u : 0u);
+            const unsigned hm = (h[0] ? 1u : 0u) | (h[1] ? 2u : 0u) | (h[2] ? 4u : 0u) | (h[3] ? 8u : 0u);
+            const unsigned cm = __reduce_or_sync(FULL, hm);
             const int nh = __popc(cm);
             if (nh == 0) {
                 if (sp == 0) break;
@@ -579,7 +590,7 @@ __device__ __forceinline__ void traverse_packet(const SceneView& sv, int env, Ra
                 }
                 sp += nh - 1;  // nh is warp-uniform
             } else {
-                sovf = true;
+                sovf = 1;
             }
             node = ref[0];
             continue;
@@ -599,7 +610,7 @@ __device__ __forceinline__ void traverse_packet(const SceneView& sv, int env, Ra
                 if (leader) wstack[sp] = SENTINEL;
                 ++sp;
             } else {
-                sovf = true;
+                sovf = 1;
                 break;
             }
             node = rs.enter_instance(sv, leaf);
@@ -920,7 +931,7 @@ __global__ void __launch_bounds__(CAST_THREADS, CAST_MIN_BLOCKS) k_cast(const __
         rs.init(o, d, a.max_range, cold);
         const CastArgs* ap = &a;
         auto res = [ap](int inst, int leaf, Best64& b) { resolve_leaf64<MODEL>(ap, inst, leaf, &b); };
-        bool sovf = false;
+        int sovf = 0;
         if (TRAV == 2) {
             auto leaf_fn = [&](int leaf) {
                 if (COUNT) cnt.f64++;
@@ -968,7 +979,7 @@ __global__ void __launch_bounds__(CAST_THREADS, CAST_MIN_BLOCKS) k_cast(const __
         const Best64 prim = best;
         auto sres = [ap, prim](int inst, int leaf) { return shadow_test64<MODEL>(ap, prim.t, inst, leaf); };
         auto leaf_fn = [&](int leaf) { ss.leaf_anyhit<COUNT>(a.sv, leaf, sres, cnt); };
-        bool sovf2 = false;
+        int sovf2 = 0;
         if (TRAV == 1) traverse_packet<true, COUNT>(a.sv, id.env, ss, leaf_fn, sovf2, s_stack[threadIdx.x >> 5], cnt);
         else traverse_lane<true, COUNT>(a.sv, id.env, ss, leaf_fn, sovf2, cnt);
         valid = !tested || ss.U >= 0.0f;
