@@ -56,13 +56,7 @@ struct SlabRay {
 
 // Approximate reciprocal (MUFU.RCP, ~1 ulp): every FP32 quantity it feeds is
 // covered by the error budget of DESIGN.md §5.2, so no IEEE division.
-__device__ __forceinline__ float rcp_approx(float x) {
-    float r;
-    asm("rcp.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
-    return r;
-}
-
-// Flush-to-zero variant (one MUFU.RCP, no denormal fix-up): for inputs with
+// Flush-to-zero (one MUFU.RCP, no denormal fix-up): exact for inputs with
 // 1e-30 <= |x| < 8.5e37, where neither the input nor the result is
 // denormal -- safe_inv's inputs (ray direction components, offset by
 // copysign(1e-30)) are in that range for any ray with finite, sub-1e37
@@ -70,6 +64,14 @@ __device__ __forceinline__ float rcp_approx(float x) {
 __device__ __forceinline__ float rcp_approx_ftz(float x) {
     float r;
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+// |x|^-1/2 without the denormal fix-up; a denormal x gives inf, and the
+// NaN / inf that follow only widen the FP32 filter's bands.
+__device__ __forceinline__ float rsqrt_approx_ftz(float x) {
+    float r;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
     return r;
 }
 
@@ -192,7 +194,9 @@ enum ColdField {
     C_OX, C_OY, C_OZ, C_DX, C_DY, C_DZ, C_Q,
     C_OOX, C_OOY, C_OOZ, C_ODX, C_ODY, C_ODZ, C_DELTA, C_DLEN,
     C_TL0, C_INST0 = C_TL0 + NSLOT, C_LEAF0 = C_INST0 + NSLOT,
-    C_FACE = C_LEAF0 + NSLOT, C_BINST, C_BLEAF, N_COLD
+    C_FACE = C_LEAF0 + NSLOT, C_BINST, C_BLEAF,
+    C_OVF,  // traversal stack overflowed (-> FP64 brute force); kept out of registers
+    N_COLD
 };
 
 struct Cold {
@@ -243,6 +247,7 @@ struct RayState {
         cur_inst = -1;
 #pragma unroll
         for (int k = 0; k < NSLOT; ++k) { c.f(C_TL0 + k) = inf_f(); c.i(C_INST0 + k) = -1; c.i(C_LEAF0 + k) = -1; }
+        c.i(C_OVF) = 0;
         Best64 b;
         b.t = 0.0;
         b.face = -1;
@@ -275,7 +280,7 @@ struct RayState {
         c.f(C_ODX) = od.x; c.f(C_ODY) = od.y; c.f(C_ODZ) = od.z;
         c.f(C_DELTA) = delta;
         const float dd = dot(od, od);
-        c.f(C_DLEN) = dd > 0.0f ? dd * rsqrtf(dd) * 1.000001f : 0.0f;
+        c.f(C_DLEN) = dd > 0.0f ? dd * rsqrt_approx_ftz(dd) * 1.000001f : 0.0f;
         sr = make_slab(oo, od, delta);
         cur_inst = inst;
         return __float_as_int(r3.x);
@@ -325,7 +330,7 @@ struct RayState {
         bool keep, certain = false;
         float tl = 0.0f, th = 0.0f;
         if (det != 0.0f) {
-            float inv = rcp_approx(det);
+            float inv = rcp_approx_ftz(det);  // denormal det -> inf: kept as a candidate (NaN-safe tests below)
             f3 qv = cross(s, e1);
             float u = dot(s, p) * inv;
             float v = dot(od, qv) * inv;
@@ -379,7 +384,7 @@ struct RayState {
         f3 s = sub(oo, v0);
         bool keep, certain = false;
         if (det != 0.0f) {
-            float inv = rcp_approx(det);
+            float inv = rcp_approx_ftz(det);  // denormal det -> inf: kept as a candidate (NaN-safe tests below)
             f3 qv = cross(s, e1);
             float u = dot(s, p) * inv;
             float v = dot(od, qv) * inv;
@@ -464,7 +469,7 @@ constexpr unsigned KEY_MISS = 0x7f800000u;  // +inf bits: sorts after every hit 
 // its U < 0 (shadow queries).
 template <bool ANYHIT, bool COUNT, class LEAF>
 __device__ __forceinline__ void traverse_lane(const SceneView& sv, int env, RayState& rs,
-                                              const LEAF& leaf_fn, int& sovf, Counters& cnt) {
+                                              const LEAF& leaf_fn, Counters& cnt) {
     int stack[STACK_SIZE];
     int sp = 0;
     int node = __ldg(sv.tlas_root + env);
@@ -496,7 +501,7 @@ __device__ __forceinline__ void traverse_lane(const SceneView& sv, int env, RayS
             for (int k = 3; k >= 1; --k) {
                 if (k < nh) {
                     if (sp < STACK_SIZE) stack[sp++] = ref[k];
-                    else sovf = 1;
+                    else rs.c.i(C_OVF) = 1;
                 }
             }
             node = ref[0];
@@ -512,7 +517,7 @@ __device__ __forceinline__ void traverse_lane(const SceneView& sv, int env, RayS
         if (rs.cur_inst < 0) {
             if (COUNT) cnt.insts++;
             if (sp < STACK_SIZE) stack[sp++] = SENTINEL;
-            else { sovf = 1; break; }
+            else { rs.c.i(C_OVF) = 1; break; }
             node = rs.enter_instance(sv, leaf);
             continue;
         }
@@ -539,7 +544,7 @@ constexpr int PSTACK = 96;
 
 template <bool ANYHIT, bool COUNT, class LEAF>
 __device__ __forceinline__ void traverse_packet(const SceneView& sv, int env, RayState& rs,
-                                                const LEAF& leaf_fn, int& sovf, int* wstack,
+                                                const LEAF& leaf_fn, int* wstack,
                                                 Counters& cnt) {
     const unsigned FULL = 0xFFFFFFFFu;
     const bool leader = (threadIdx.x & 31) == 0;
@@ -590,7 +595,7 @@ __device__ __forceinline__ void traverse_packet(const SceneView& sv, int env, Ra
                 }
                 sp += nh - 1;  // nh is warp-uniform
             } else {
-                sovf = 1;
+                rs.c.i(C_OVF) = 1;
             }
             node = ref[0];
             continue;
@@ -610,7 +615,7 @@ __device__ __forceinline__ void traverse_packet(const SceneView& sv, int env, Ra
                 if (leader) wstack[sp] = SENTINEL;
                 ++sp;
             } else {
-                sovf = 1;
+                rs.c.i(C_OVF) = 1;
                 break;
             }
             node = rs.enter_instance(sv, leaf);
@@ -931,25 +936,24 @@ __global__ void __launch_bounds__(CAST_THREADS, CAST_MIN_BLOCKS) k_cast(const __
         rs.init(o, d, a.max_range, cold);
         const CastArgs* ap = &a;
         auto res = [ap](int inst, int leaf, Best64& b) { resolve_leaf64<MODEL>(ap, inst, leaf, &b); };
-        int sovf = 0;
         if (TRAV == 2) {
             auto leaf_fn = [&](int leaf) {
                 if (COUNT) cnt.f64++;
                 rs.resolve64(leaf, res);
             };
-            traverse_lane<false, COUNT>(a.sv, id.env, rs, leaf_fn, sovf, cnt);
+            traverse_lane<false, COUNT>(a.sv, id.env, rs, leaf_fn, cnt);
             best = cold.best();
         } else {
             auto leaf_fn = [&](int leaf) { rs.leaf_filter<COUNT>(a.sv, leaf, res, cnt); };
             if (TRAV == 1) {
                 // whole warps share (env, sensor): pinhole / beams tiles
-                traverse_packet<false, COUNT>(a.sv, id.env, rs, leaf_fn, sovf, s_stack[threadIdx.x >> 5], cnt);
+                traverse_packet<false, COUNT>(a.sv, id.env, rs, leaf_fn, s_stack[threadIdx.x >> 5], cnt);
             } else {
-                traverse_lane<false, COUNT>(a.sv, id.env, rs, leaf_fn, sovf, cnt);
+                traverse_lane<false, COUNT>(a.sv, id.env, rs, leaf_fn, cnt);
             }
             best = rs.arbitrate<COUNT>(res, cnt);
         }
-        if (sovf) {
+        if (cold.i(C_OVF)) {
             if (COUNT) cnt.overflow++;
             best.face = -1;
             brute64(a.sv, id.env, gen_ray64<MODEL>(a, id), (double)a.max_range, &best);
@@ -979,11 +983,10 @@ __global__ void __launch_bounds__(CAST_THREADS, CAST_MIN_BLOCKS) k_cast(const __
         const Best64 prim = best;
         auto sres = [ap, prim](int inst, int leaf) { return shadow_test64<MODEL>(ap, prim.t, inst, leaf); };
         auto leaf_fn = [&](int leaf) { ss.leaf_anyhit<COUNT>(a.sv, leaf, sres, cnt); };
-        int sovf2 = 0;
-        if (TRAV == 1) traverse_packet<true, COUNT>(a.sv, id.env, ss, leaf_fn, sovf2, s_stack[threadIdx.x >> 5], cnt);
-        else traverse_lane<true, COUNT>(a.sv, id.env, ss, leaf_fn, sovf2, cnt);
+        if (TRAV == 1) traverse_packet<true, COUNT>(a.sv, id.env, ss, leaf_fn, s_stack[threadIdx.x >> 5], cnt);
+        else traverse_lane<true, COUNT>(a.sv, id.env, ss, leaf_fn, cnt);
         valid = !tested || ss.U >= 0.0f;
-        if (sovf2 && tested) valid = !shadow_brute64<MODEL>(&a, id.env, best.t);
+        if (cold.i(C_OVF) && tested) valid = !shadow_brute64<MODEL>(&a, id.env, best.t);
     }
     if (COUNT) {
         unsigned v[6] = {cnt.nodes, cnt.leaves, cnt.insts, cnt.f64, cnt.overflow, cnt.tnodes};
