@@ -330,8 +330,9 @@ agr_status agr_set_traversal(agr_scene scene, int32_t mode);
  * are collected only when enabled):  counters[0] rays, [1] internal nodes
  * visited, [2] leaf (triangle) tests, [3] instance entries, [4] FP64
  * arbitration tests, [5] candidate-list overflows / stack fallbacks,
- * [6] internal nodes visited at the TLAS level (node and leaf counts are
- * per lane: in packet mode every lane counts each warp visit).
+ * [6] internal nodes visited at the TLAS level, [7] instance entries whose
+ * BLAS root test hit no child for the lane's own ray (node and leaf counts
+ * are per lane: in packet mode every lane counts each warp visit).
  */
 agr_status agr_enable_counters(agr_scene scene, int32_t enable);
 agr_status agr_get_counters(agr_scene scene, int64_t counters[8]);

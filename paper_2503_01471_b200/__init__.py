@@ -364,7 +364,8 @@ class Scene:
         c = np.zeros(8, np.int64)
         _check(load().agr_get_counters(self.handle, c.ctypes.data))
         return dict(rays=int(c[0]), nodes=int(c[1]), leaves=int(c[2]), instances=int(c[3]),
-                    fp64_tests=int(c[4]), overflow=int(c[5]), tlas_nodes=int(c[6]))
+                    fp64_tests=int(c[4]), overflow=int(c[5]), tlas_nodes=int(c[6]),
+                    empty_entries=int(c[7]))
 
     def debug_export_blas(self, asset: int):
         nn, nl = ctypes.c_int64(), ctypes.c_int64()

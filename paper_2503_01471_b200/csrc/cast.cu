@@ -152,7 +152,7 @@ struct Slots {
     int leaf[NSLOT];
 };
 
-struct Counters { unsigned nodes, leaves, insts, f64, overflow, tnodes; };
+struct Counters { unsigned nodes, leaves, insts, f64, overflow, tnodes, empty; };
 
 struct Best64 {
     double t;
@@ -473,6 +473,7 @@ __device__ __forceinline__ void traverse_lane(const SceneView& sv, int env, RayS
     int stack[STACK_SIZE];
     int sp = 0;
     int node = __ldg(sv.tlas_root + env);
+    bool fresh = false;  // COUNT: the node is the root of a just-entered BLAS
     for (;;) {
         if (node >= 0) {
             if (COUNT) cnt.nodes++;
@@ -489,6 +490,10 @@ __device__ __forceinline__ void traverse_lane(const SceneView& sv, int env, RayS
             for (int k = 0; k < 4; ++k) {
                 key[k] = h[k] ? __float_as_uint(tn[k]) : KEY_MISS;
                 nh += h[k] ? 1 : 0;
+            }
+            if (COUNT && fresh) {
+                if (nh == 0) cnt.empty++;
+                fresh = false;
             }
             if (nh == 0) {
                 if (sp == 0) break;
@@ -516,6 +521,7 @@ __device__ __forceinline__ void traverse_lane(const SceneView& sv, int env, RayS
         const int leaf = ~node;
         if (rs.cur_inst < 0) {
             if (COUNT) cnt.insts++;
+            if (COUNT) fresh = true;
             if (sp < STACK_SIZE) stack[sp++] = SENTINEL;
             else { rs.c.i(C_OVF) = 1; break; }
             node = rs.enter_instance(sv, leaf);
@@ -550,6 +556,7 @@ __device__ __forceinline__ void traverse_packet(const SceneView& sv, int env, Ra
     const bool leader = (threadIdx.x & 31) == 0;
     int sp = 0;
     int node = __ldg(sv.tlas_root + env);
+    bool fresh = false;  // COUNT: the node is the root of a just-entered BLAS
     for (;;) {
         if (node >= 0) {
             if (COUNT) cnt.nodes++;
@@ -562,6 +569,10 @@ __device__ __forceinline__ void traverse_packet(const SceneView& sv, int env, Ra
             rs.node4_test(f, tn, h);
             // 4-bit mask of the children some lane hits
             const unsigned hm = (h[0] ? 1u : 0u) | (h[1] ? 2u : 0u) | (h[2] ? 4u : 0u) | (h[3] ? 8u : 0u);
+            if (COUNT && fresh) {
+                if (hm == 0) cnt.empty++;  // this lane's own ray
+                fresh = false;
+            }
             const unsigned cm = __reduce_or_sync(FULL, hm);
             const int nh = __popc(cm);
             if (nh == 0) {
@@ -610,6 +621,7 @@ __device__ __forceinline__ void traverse_packet(const SceneView& sv, int env, Ra
         const int leaf = ~node;
         if (rs.cur_inst < 0) {
             if (COUNT) cnt.insts++;
+            if (COUNT) fresh = true;
             if (sp < PSTACK) {
                 __syncwarp();  // every lane has read the slot before it is reused
                 if (leader) wstack[sp] = SENTINEL;
@@ -921,7 +933,7 @@ __global__ void __launch_bounds__(CAST_THREADS, CAST_MIN_BLOCKS) k_cast(const __
     const bool trace = id.env < a.env_end && (id.active || MODEL != 0);
     id.col = min(id.col, a.W - 1);
     id.row = min(id.row, a.H - 1);
-    Counters cnt = {0, 0, 0, 0, 0, 0};
+    Counters cnt = {0, 0, 0, 0, 0, 0, 0};
     RayState rs;
     Best64 best;
     best.face = -1;
@@ -989,15 +1001,15 @@ __global__ void __launch_bounds__(CAST_THREADS, CAST_MIN_BLOCKS) k_cast(const __
         if (cold.i(C_OVF) && tested) valid = !shadow_brute64<MODEL>(&a, id.env, best.t);
     }
     if (COUNT) {
-        unsigned v[6] = {cnt.nodes, cnt.leaves, cnt.insts, cnt.f64, cnt.overflow, cnt.tnodes};
+        unsigned v[7] = {cnt.nodes, cnt.leaves, cnt.insts, cnt.f64, cnt.overflow, cnt.tnodes, cnt.empty};
         unsigned rays = id.active ? 1u : 0u;
         for (int o2 = 16; o2 > 0; o2 >>= 1) {
             rays += __shfl_xor_sync(0xFFFFFFFFu, rays, o2);
-            for (int k = 0; k < 6; ++k) v[k] += __shfl_xor_sync(0xFFFFFFFFu, v[k], o2);
+            for (int k = 0; k < 7; ++k) v[k] += __shfl_xor_sync(0xFFFFFFFFu, v[k], o2);
         }
         if ((threadIdx.x & 31) == 0) {
             atomicAdd(a.counters + 0, (unsigned long long)rays);
-            for (int k = 0; k < 6; ++k) atomicAdd(a.counters + 1 + k, (unsigned long long)v[k]);
+            for (int k = 0; k < 7; ++k) atomicAdd(a.counters + 1 + k, (unsigned long long)v[k]);
         }
     }
     if (!id.active) return;
