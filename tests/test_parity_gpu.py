@@ -577,3 +577,60 @@ def test_annotations_host_path_and_errors():
                                channels=("dist", "face", "annot"))
     for k in dev_out:
         assert np.array_equal(dev_out[k], host[k].numpy().reshape(-1), equal_nan=True), k
+
+
+# ---- maximum sizes ---------------------------------------------------------------
+
+@pytest.mark.parametrize("builder", [0, 1])
+def test_max_instances_per_env(builder):
+    """AGR_MAX_INSTANCES_PER_ENV (1024) instances in one env -- the largest
+    one-CTA TLAS build -- with both TLAS builders, rebuild and refit, against
+    the oracle; one more instance is EUNSUPPORTED."""
+    rng = np.random.default_rng(41)
+    n = 1024
+    per_env = []
+    for e in range(2):
+        insts = []
+        for j in range(n if e == 0 else 37):
+            T = sg.make_T(sg.random_rotation(rng), rng.uniform([2, -6, -4], [14, 6, 4]), rng.uniform(0.1, 0.4))
+            insts.append((j % 2, j + 1, T))
+        per_env.append(insts)
+    sc = sg.assemble([sg.cube_mesh(), sg.panel_mesh()], per_env)
+    cam = sg.pinhole(48, 32, 90.0)
+    sensor = dict(kind="pinhole", cam=cam, poses=sg.identity_poses(2), max_range=20.0)
+    s = make_scene(sc, build=False)
+    s.set_tlas_builder(builder)
+    s.build()
+    got = to_np(cast_sensor(s, sensor, "range"))
+    ref = oracle.cast(sc, oracle_rays(sensor, "range"))
+    compare(ref, got["dist"], got["seg"], got["face"], f"1024 instances, builder {builder}")
+    assert (got["face"][: cam["W"] * cam["H"]] >= 0).mean() > 0.3
+    assert s.info()["n_instances"] == n + 37
+    # re-pose everything and refit (topology kept)
+    T2 = sc.inst_T.copy()
+    T2[:, :, 3] += rng.uniform(-0.3, 0.3, (len(T2), 3)).astype(np.float32)
+    s.set_instance_transforms(torch.from_numpy(T2).to(dev()))
+    s.refit()
+    got = to_np(cast_sensor(s, sensor, "range"))
+    sc2 = sg.Scene(sc.meshes, sc.env_off, sc.inst_asset, sc.inst_label, T2)
+    ref = oracle.cast(sc2, oracle_rays(sensor, "range"))
+    compare(ref, got["dist"], got["seg"], got["face"], "1024 instances after refit")
+    with pytest.raises(agr.AgrError):
+        sg_over = sg.assemble([sg.cube_mesh()], [[(0, 1, sg.make_T(np.eye(3), (3, 0, 0)))] * (n + 1)])
+        agr.Scene.from_scenegen(sg_over, device=0)
+
+
+def test_large_image_sampled():
+    """A 1920x1080 frame (2.07 M rays, one env, 2 sensors: grid of 129600
+    warps) against the oracle on sampled rays, plus the full certificate."""
+    sc, _ = sg.config2(n_envs=1)
+    cam = sg.pinhole(1920, 1080, 100.0)
+    P = sg.identity_poses(1, 2)
+    P[0, 1, :, :3] = sg.rot_z(0.3)
+    sensor = dict(kind="pinhole", cam=cam, poses=P, max_range=10.0)
+    s = make_scene(sc)
+    got = to_np(cast_sensor(s, sensor, "depth"))
+    q = np.random.default_rng(5).choice(len(got["dist"]), 20000, replace=False)
+    ref = oracle.cast(sc, oracle_rays(sensor, "depth"), query=q)
+    compare(ref, got["dist"][q], got["seg"][q], got["face"][q], "1080p")
+    certify_all(sc, sensor, "depth", got["dist"], got["seg"], got["face"], "1080p")
