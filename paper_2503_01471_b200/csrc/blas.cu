@@ -40,7 +40,7 @@ namespace {
 constexpr int T_BLK = 256;
 constexpr int RS_THREADS = 256;
 constexpr int RS_MIN_ROUNDS = 4;   // rounds of RS_THREADS keys per sort block
-constexpr int RS_MAX_BLOCKS = 1024;  // keeps the single-CTA histogram scan short
+constexpr int RS_MAX_BLOCKS = 296;   // 2 per SM: keeps the single-CTA histogram scan short
 
 // Keys per sort block: at least RS_MIN_ROUNDS x RS_THREADS, and few enough
 // blocks that the 256 x nblocks histogram scan stays small.
