@@ -273,6 +273,10 @@ struct CastArgs {
     unsigned long long* counters;  // optional [8]
     int exact;
     int packet;           // 1: warp-packet traversal for pinhole / beams tiles
+    // filled by cast_launch: n / d = (n * m) >> s for n < 2^31 (tile decode
+    // of tiles_img, tiles_x, S without integer division)
+    unsigned div_m[3];
+    int div_s[3];
 };
 cudaError_t cast_launch(const CastArgs& a, cudaStream_t stream);
 

@@ -196,8 +196,14 @@ enum ColdField {
     C_TL0, C_INST0 = C_TL0 + NSLOT, C_LEAF0 = C_INST0 + NSLOT,
     C_FACE = C_LEAF0 + NSLOT, C_BINST, C_BLEAF,
     C_OVF,  // traversal stack overflowed (-> FP64 brute force); kept out of registers
+    C_COL, C_ROW, C_IMG,  // pixel / beam and env * S + sensor: the FP64 ray's inputs
     N_COLD
 };
+
+// Per-lane cold columns of the block (file scope so the out-of-line FP64
+// testers can read the lane's ray identity without an extra argument).
+__shared__ float s_cold[N_COLD][CAST_THREADS];
+__shared__ double s_best_t[CAST_THREADS];
 
 struct Cold {
     float* p;     // &s_cold[0][lane of block]
@@ -775,6 +781,22 @@ __device__ __noinline__ float shadow_segment(const CastArgs* a, int env, int sen
 template <int MODEL>
 __device__ __forceinline__ RayId ray_id(const CastArgs& a);
 
+// Ray identity of this lane from its cold column (written once by the
+// kernel), so an FP64 test does not redo the tile decode.
+template <int MODEL>
+__device__ __forceinline__ RayId cold_id(const CastArgs& a) {
+    if (MODEL == 0) return ray_id<MODEL>(a);
+    RayId id;
+    id.col = __float_as_int(s_cold[C_COL][threadIdx.x]);
+    id.row = __float_as_int(s_cold[C_ROW][threadIdx.x]);
+    const int img = __float_as_int(s_cold[C_IMG][threadIdx.x]);
+    id.env = img / a.S;  // only used with id.sensor through env * S + sensor
+    id.sensor = img - id.env * a.S;
+    id.out = 0;
+    id.active = true;
+    return id;
+}
+
 template <int MODEL>
 __device__ __noinline__ bool shadow_test64(const CastArgs* a, double t_hit, int inst, int leaf) {
     RayId id = ray_id<MODEL>(*a);
@@ -810,9 +832,7 @@ __device__ __noinline__ bool shadow_brute64(const CastArgs* a, int env, double t
 // registers out of the traversal loop's allocation.
 template <int MODEL>
 __device__ __noinline__ void resolve_leaf64(const CastArgs* a, int inst, int leaf, Best64* best) {
-    RayId id = ray_id<MODEL>(*a);
-    id.col = min(id.col, a->W - 1);
-    id.row = min(id.row, a->H - 1);
+    const RayId id = cold_id<MODEL>(*a);
     const Ray64 r = gen_ray64<MODEL>(*a, id);
     Best64 b = *best;
     consider64(a->sv, inst, leaf, r, (double)a->max_range, b);
@@ -888,6 +908,13 @@ __device__ __noinline__ void write_extra(const CastArgs* a, RayId id, Best64 bes
     }
 }
 
+// n / d for n < 2^31 with m = floor(2^(31+l) / d) + 1, s = 31 + l,
+// l = ceil(log2 d): n m / 2^s = n / d + n e / 2^s with 0 < e <= 1, and
+// n e / 2^s < 2^-l <= 1 / d, which never carries past the next integer.
+__device__ __forceinline__ unsigned fast_div(unsigned n, unsigned m, int s) {
+    return (unsigned)(((unsigned long long)n * m) >> s);
+}
+
 template <int MODEL>
 __device__ __forceinline__ RayId ray_id(const CastArgs& a) {
     RayId id;
@@ -908,10 +935,10 @@ __device__ __forceinline__ RayId ray_id(const CastArgs& a) {
     const unsigned tiles_img = tiles_x * (unsigned)((a.H + TILE_H - 1) / TILE_H);
     const unsigned warp = blockIdx.x * (unsigned)(CAST_THREADS / 32) + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
-    const unsigned img = warp / tiles_img;
+    const unsigned img = fast_div(warp, a.div_m[0], a.div_s[0]);
     const unsigned tile = warp - img * tiles_img;
-    const unsigned ty = tile / tiles_x, tx = tile - ty * tiles_x;
-    const unsigned env_rel = a.S == 1 ? img : img / (unsigned)a.S;
+    const unsigned ty = fast_div(tile, a.div_m[1], a.div_s[1]), tx = tile - ty * tiles_x;
+    const unsigned env_rel = a.S == 1 ? img : fast_div(img, a.div_m[2], a.div_s[2]);
     id.env = a.env_begin + (int)env_rel;
     id.sensor = (int)(img - env_rel * (unsigned)a.S);
     id.col = (int)tx * TILE_W + (lane % TILE_W);
@@ -925,8 +952,6 @@ __device__ __forceinline__ RayId ray_id(const CastArgs& a) {
 template <int MODEL, int TRAV, bool COUNT, bool STEREO>
 __global__ void __launch_bounds__(CAST_THREADS, CAST_MIN_BLOCKS) k_cast(const __grid_constant__ CastArgs a) {
     __shared__ int s_stack[TRAV == 1 ? CAST_THREADS / 32 : 1][TRAV == 1 ? PSTACK : 1];
-    __shared__ float s_cold[N_COLD][CAST_THREADS];
-    __shared__ double s_best_t[CAST_THREADS];
     RayId id = ray_id<MODEL>(a);
     // ragged tile lanes keep the warp whole for the traversal: they trace a
     // copy of a valid pixel and store nothing
@@ -946,6 +971,9 @@ __global__ void __launch_bounds__(CAST_THREADS, CAST_MIN_BLOCKS) k_cast(const __
         cold.p = &s_cold[0][threadIdx.x];
         cold.bt = &s_best_t[threadIdx.x];
         rs.init(o, d, a.max_range, cold);
+        cold.i(C_COL) = id.col;
+        cold.i(C_ROW) = id.row;
+        cold.i(C_IMG) = id.env * a.S + id.sensor;
         const CastArgs* ap = &a;
         auto res = [ap](int inst, int leaf, Best64& b) { resolve_leaf64<MODEL>(ap, inst, leaf, &b); };
         if (TRAV == 2) {
@@ -1024,7 +1052,7 @@ __global__ void __launch_bounds__(CAST_THREADS, CAST_MIN_BLOCKS) k_cast(const __
 }
 
 template <int MODEL>
-cudaError_t launch_model(const CastArgs& a, cudaStream_t stream) {
+cudaError_t launch_model(CastArgs a, cudaStream_t stream) {
     int64_t blocks;
     int n_envs = a.env_end - a.env_begin;
     if (n_envs <= 0) return cudaSuccess;
@@ -1034,12 +1062,23 @@ cudaError_t launch_model(const CastArgs& a, cudaStream_t stream) {
         const int64_t tiles_img = (int64_t)((a.W + TILE_W - 1) / TILE_W) * ((a.H + TILE_H - 1) / TILE_H);
         if (tiles_img > 0x7FFFFFFF) return cudaErrorInvalidValue;  // ray_id's 32-bit math
         int64_t tiles = tiles_img * n_envs * a.S;
+        if (tiles > 0x7FFFFFFF) return cudaErrorInvalidValue;  // fast_div needs warp < 2^31
         blocks = (tiles + CAST_THREADS / 32 - 1) / (CAST_THREADS / 32);
     }
     if (blocks <= 0) return cudaSuccess;
     if (blocks > 0x7FFFFFFF) return cudaErrorInvalidValue;
     const int trav = a.exact ? 2 : (MODEL != 0 && a.packet ? 1 : 0);
     const unsigned g = (unsigned)blocks;
+    if (MODEL != 0) {
+        const unsigned tiles_x = (unsigned)(a.W + TILE_W - 1) / TILE_W;
+        const unsigned ds[3] = {tiles_x * (unsigned)((a.H + TILE_H - 1) / TILE_H), tiles_x, (unsigned)a.S};
+        for (int k = 0; k < 3; ++k) {
+            int l = 0;
+            while ((1ull << l) < ds[k]) ++l;
+            a.div_m[k] = (unsigned)((1ull << (31 + l)) / ds[k] + 1);
+            a.div_s[k] = 31 + l;
+        }
+    }
     const bool stereo = MODEL != 0 && a.out_valid != nullptr;
 #define AGR_LAUNCH(T, C, S) k_cast<MODEL, T, C, S><<<g, CAST_THREADS, 0, stream>>>(a)
     if (a.counters) {
