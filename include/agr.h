@@ -344,7 +344,9 @@ agr_status agr_get_counters(agr_scene scene, int64_t counters[8]);
  * [n_leaves] (sorted codes).  Pass NULL to query sizes via *n_nodes and
  * *n_leaves.  Node child refs: >= 0 node index relative to the asset's
  * first node, < 0 leaf ~index relative to the asset's first leaf,
- * INT32_MIN empty.
+ * INT32_MIN empty.  The binary nodes are packed by the create-time build
+ * only: after agr_update_mesh(es) of this asset, a request for `nodes`
+ * returns AGR_ESTATE (leaf_face and morton stay available).
  */
 agr_status agr_debug_export_blas(agr_scene scene, int32_t asset, float* nodes,
                                  int32_t* leaf_face, uint32_t* morton,

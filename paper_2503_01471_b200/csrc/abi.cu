@@ -95,6 +95,7 @@ struct agr_scene_s {
     void* blas_scratch = nullptr;
     std::vector<int64_t> h_mvert_off, h_mface_off;
     std::vector<int> h_node_base, h_leaf_base, h_nverts, h_nfaces;
+    std::vector<char> h_bin_stale;  // binary LBVH export out of date (mesh updated)
     bool assets_stale = false;
     int trbvh_rounds = 3;
     unsigned long long* counters = nullptr;
@@ -188,7 +189,10 @@ struct agr_scene_s {
 };
 
 // (Re)build asset a's BLAS from the device copy of its mesh (async on st).
-static cudaError_t build_assets(agr_scene_s* s, const int* assets, int n, cudaStream_t st) {
+// `binary`: also pack the binary LBVH nodes for agr_debug_export_blas (the
+// create-time build only; mesh updates skip it and mark the asset's binary
+// export stale).
+static cudaError_t build_assets(agr_scene_s* s, const int* assets, int n, cudaStream_t st, bool binary) {
     std::vector<BlasSeg> segs(n);
     for (int k = 0; k < n; ++k) {
         const int a = assets[k];
@@ -204,7 +208,7 @@ static cudaError_t build_assets(agr_scene_s* s, const int* assets, int n, cudaSt
     }
     BlasBatchArgs ba;
     ba.nodes = s->nodes;
-    ba.bnodes = s->bnodes;
+    ba.bnodes = binary ? s->bnodes : nullptr;
     ba.tris = s->tris;
     ba.triv = s->triv;
     ba.dbg_morton = s->morton;
@@ -369,6 +373,7 @@ agr_status agr_scene_create_ex(int32_t device, const agr_mesh* meshes, int32_t n
         s->h_mface_off[a + 1] = s->h_mface_off[a] + meshes[a].n_faces;
         s->h_nverts.push_back(meshes[a].n_verts);
         s->h_nfaces.push_back(meshes[a].n_faces);
+        s->h_bin_stale.push_back(0);
     }
     s->h_node_base = node_base;
     s->h_leaf_base = leaf_base;
@@ -400,7 +405,7 @@ agr_status agr_scene_create_ex(int32_t device, const agr_mesh* meshes, int32_t n
     if (err == cudaSuccess) {
         std::vector<int> all(n_meshes);
         for (int a = 0; a < n_meshes; ++a) all[a] = a;
-        err = build_assets(s, all.data(), n_meshes, st);
+        err = build_assets(s, all.data(), n_meshes, st, true);
     }
     if (err == cudaSuccess) err = cudaStreamSynchronize(st);
     if (err != cudaSuccess) {
@@ -510,7 +515,8 @@ agr_status agr_update_meshes(agr_scene s, int32_t n, const int32_t* assets, cons
                            sizeof(float) * 3 * s->h_nverts[a], cudaMemcpyDeviceToDevice, st));
         v += s->h_nverts[a];
     }
-    CK(build_assets(s, assets, n, st));
+    CK(build_assets(s, assets, n, st, false));
+    for (int k = 0; k < n; ++k) s->h_bin_stale[assets[k]] = 1;
     CK(instances_update(s->tlas_args(), (int)s->n_inst, st));  // instance boxes from the new BLAS
     s->assets_stale = true;
     s->dirty = true;
@@ -921,6 +927,8 @@ agr_status agr_debug_export_blas(agr_scene s, int32_t asset, float* nodes, int32
     *n_nodes = nn;
     *n_leaves = a.n_leaves;
     if (!nodes && !leaf_face && !morton) return AGR_OK;
+    if (nodes && s->h_bin_stale[asset])
+        return fail(AGR_ESTATE, "binary LBVH nodes are exported for create-time builds only (mesh updated)");
     CK(cudaDeviceSynchronize());
     if (nodes) {
         std::vector<float4> h(4 * nn);

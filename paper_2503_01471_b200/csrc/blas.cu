@@ -28,6 +28,7 @@
 
 #include <cfloat>
 #include <climits>
+#include <cuda/atomic>
 
 #ifndef AGR_KEEP_PAIRS
 #define AGR_KEEP_PAIRS 0
@@ -376,6 +377,15 @@ __global__ void k_karras(const BlasSeg* segs, const int* seg_of, const uint32_t*
 }
 
 // ---- K4: bottom-up fit (per segment) ------------------------------------------------
+// Arrival counter of the bottom-up passes: one acq_rel atomic (a single
+// MEMBAR.ALL.GPU) publishes this thread's earlier stores and, for the second
+// arrival, makes the sibling's visible -- instead of a sequentially
+// consistent __threadfence() on each side of a relaxed atomic.
+__device__ __forceinline__ int arrive(int* flag) {
+    cuda::atomic_ref<int, cuda::thread_scope_device> a(*flag);
+    return a.fetch_add(1, cuda::memory_order_acq_rel);
+}
+
 __device__ __forceinline__ void load_box_cg(const float* p, float b[6]) {
     for (int k = 0; k < 6; ++k) b[k] = __ldcg(p + k);
 }
@@ -405,9 +415,7 @@ __global__ void k_fit(const BlasSeg* segs, const int* seg_of, const uint32_t* bo
     int* size = size_all + c.off;
     int node = leaf_parent[p];
     while (node >= 0) {
-        __threadfence();
-        if (atomicAdd(&flags[node], 1) == 0) return;  // first arrival: sibling not ready
-        __threadfence();
+        if (arrive(&flags[node]) == 0) return;  // first arrival: sibling not ready
         float b[6], cc[6];
         int h = 0, sz = 0;
         for (int side = 0; side < 2; ++side) {
@@ -646,9 +654,7 @@ __global__ void __launch_bounds__(TRB_THREADS) k_trbvh(
     for (;;) {
         bool claim = false;
         if (active && node >= 0) {
-            __threadfence();
-            claim = atomicAdd(&flags_all[off + node], 1) != 0;  // second arrival: subtree final
-            __threadfence();
+            claim = arrive(&flags_all[off + node]) != 0;  // second arrival: subtree final
         }
         active = claim;
         if (!__any_sync(FULL, claim)) break;
@@ -702,9 +708,7 @@ __global__ void k_depth(const BlasSeg* segs, const int* seg_of, const uint32_t* 
     int* height = height_all + c.off;
     int node = __ldcg(leaf_parent_all + c.off + p);
     while (node >= 0) {
-        __threadfence();
-        if (atomicAdd(&flags[node], 1) == 0) return;
-        __threadfence();
+        if (arrive(&flags[node]) == 0) return;
         int h = 0;
         for (int side = 0; side < 2; ++side) {
             const int r = __ldcg(child + 2 * node + side);
@@ -942,8 +946,9 @@ cudaError_t blas_build_batch(BlasSeg* h_segs, int B, const BlasBatchArgs& a, voi
         k_depth<<<gb, T_BLK, 0, stream>>>(s.segs, s.seg_of, s.bounds, F, s.child, s.leaf_parent, s.node_parent,
                                           s.flags, s.height, s.depth);
     }
-    k_pack_nodes<<<gb, T_BLK, 0, stream>>>(s.segs, s.seg_of, s.bounds, F, sv, s.tri_box, s.child, s.ibox,
-                                           a.bnodes);
+    if (a.bnodes)
+        k_pack_nodes<<<gb, T_BLK, 0, stream>>>(s.segs, s.seg_of, s.bounds, F, sv, s.tri_box, s.child, s.ibox,
+                                               a.bnodes);
     k_collapse4<<<gb, T_BLK, 0, stream>>>(s.segs, s.seg_of, s.bounds, F, sv, s.tri_box, s.child, s.ibox,
                                           a.nodes);
     k_pack_tris<<<gb, T_BLK, 0, stream>>>(s.segs, s.seg_of, s.bounds, F, sv, sk, a.tris, a.triv,
