@@ -180,10 +180,18 @@ __global__ void k_tri_prep(const BlasSeg* segs, const int* seg_of, int Ftot, flo
         }
         vflag[g] = valid ? 1u : 0u;
     }
-    // centroid bounds and valid count: one set of atomics per warp when the
-    // warp lies in one segment (the common case), else per thread
-    const int s0 = __shfl_sync(FULL, s, 0);
-    if (__all_sync(FULL, s == s0)) {
+    // centroid bounds and valid count: one set of atomics per block when the
+    // block lies in one segment (the common case: same-address atomics from
+    // every warp of a segment queue up at L2 and stall the loads), else per
+    // thread
+    __shared__ int s_seg[2];
+    __shared__ uint32_t s_red[7];
+    if (threadIdx.x == 0) { s_seg[0] = s; s_red[6] = 0u; }
+    if (threadIdx.x < 3) { s_red[threadIdx.x] = 0xFFFFFFFFu; s_red[3 + threadIdx.x] = 0u; }
+    if (threadIdx.x == blockDim.x - 1) s_seg[1] = s;
+    __syncthreads();
+    const int s0 = s_seg[0];
+    if (s0 >= 0 && s_seg[1] == s0) {  // segments are contiguous: first == last => one segment
         unsigned cnt = __popc(__ballot_sync(FULL, valid));
         for (int o = 16; o > 0; o >>= 1)
             for (int k = 0; k < 3; ++k) {
@@ -192,10 +200,18 @@ __global__ void k_tri_prep(const BlasSeg* segs, const int* seg_of, int Ftot, flo
             }
         if ((threadIdx.x & 31) == 0 && cnt > 0) {
             for (int k = 0; k < 3; ++k) {
-                atomicMin(&bounds[8 * s0 + k], float_to_ordered(clo[k]));
-                atomicMax(&bounds[8 * s0 + 3 + k], float_to_ordered(chi[k]));
+                atomicMin(&s_red[k], float_to_ordered(clo[k]));
+                atomicMax(&s_red[3 + k], float_to_ordered(chi[k]));
             }
-            atomicAdd(&bounds[8 * s0 + 7], cnt);
+            atomicAdd(&s_red[6], cnt);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0 && s_red[6] > 0) {
+            for (int k = 0; k < 3; ++k) {
+                atomicMin(&bounds[8 * s0 + k], s_red[k]);
+                atomicMax(&bounds[8 * s0 + 3 + k], s_red[3 + k]);
+            }
+            atomicAdd(&bounds[8 * s0 + 7], s_red[6]);
         }
     } else if (valid) {
         for (int k = 0; k < 3; ++k) {
@@ -239,18 +255,49 @@ __global__ void k_key_from(const uint32_t* __restrict__ vals, const uint32_t* __
 }
 
 // ---- K2: stable LSD radix sort (8-bit digits) --------------------------------
-__global__ void k_rs_hist(const uint32_t* __restrict__ keys, int n, int shift,
-                          uint32_t* __restrict__ hist, int nblocks, int rounds) {
-    __shared__ uint32_t cnt[256];
-    cnt[threadIdx.x] = 0;
-    __syncthreads();
-    int base = blockIdx.x * RS_THREADS * rounds;
-    for (int r = 0; r < rounds; ++r) {
-        int i = base + r * RS_THREADS + threadIdx.x;
-        if (i < n) atomicAdd(&cnt[(keys[i] >> shift) & 255u], 1u);
+// Sort block b owns keys [b R 256, (b + 1) R 256) (R = rounds).  The
+// histogram counts them per warp slice (warp-aggregated by
+// __match_any_sync, no shared-memory atomics: a pass over segment ids has
+// one digit per block); the scatter walks them 256 at a time in order with
+// per-round warp-major offsets, so equal digits keep their input order.
+constexpr int RS_WARPS = RS_THREADS / 32;
+constexpr int RS_UNROLL = 4;
+
+// Per-warp digit counts of the warp's slice into wc[w][256] (zeroed by the caller).
+__device__ __forceinline__ void rs_warp_count(const uint32_t* __restrict__ keys, int n, int shift, int start,
+                                              int steps, uint32_t* wc) {
+    const int lane = threadIdx.x & 31;
+    for (int j0 = 0; j0 < steps; j0 += RS_UNROLL) {
+        uint32_t k[RS_UNROLL];
+#pragma unroll
+        for (int u = 0; u < RS_UNROLL; ++u) {
+            const int i = start + (j0 + u) * 32 + lane;
+            k[u] = (j0 + u < steps && i < n) ? __ldg(keys + i) : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < RS_UNROLL; ++u) {
+            const int i = start + (j0 + u) * 32 + lane;
+            const bool valid = j0 + u < steps && i < n;
+            const int digit = valid ? (int)((k[u] >> shift) & 255u) : 256;
+            const unsigned peers = __match_any_sync(FULL, digit);
+            if (valid && (peers & ((1u << lane) - 1u)) == 0u) wc[digit] += __popc(peers);
+            __syncwarp();
+        }
     }
+}
+
+__global__ void __launch_bounds__(RS_THREADS) k_rs_hist(const uint32_t* __restrict__ keys, int n, int shift,
+                                                        uint32_t* __restrict__ hist, int nblocks, int rounds) {
+    __shared__ uint32_t wc[RS_WARPS][256];
+    for (int k = 0; k < RS_WARPS; ++k) wc[k][threadIdx.x] = 0;
     __syncthreads();
-    hist[threadIdx.x * nblocks + blockIdx.x] = cnt[threadIdx.x];
+    const int w = threadIdx.x >> 5;
+    const int start = (blockIdx.x * RS_WARPS + w) * rounds * 32;
+    rs_warp_count(keys, n, shift, start, rounds, wc[w]);
+    __syncthreads();
+    uint32_t c = 0;
+    for (int k = 0; k < RS_WARPS; ++k) c += wc[k][threadIdx.x];
+    hist[threadIdx.x * nblocks + blockIdx.x] = c;
 }
 
 // single-CTA exclusive scan of hist[total] in place
@@ -769,7 +816,7 @@ __global__ void k_pack_nodes(const BlasSeg* segs, const int* seg_of, const uint3
 // K5b: BVH4 node j = greedy 4-wide collapse of binary node j.
 __global__ void k_collapse4(const BlasSeg* segs, const int* seg_of, const uint32_t* bounds, int Ftot,
                             const uint32_t* __restrict__ sorted_all, const float* tri_box, int* child_all,
-                            float* ibox_all, float4* nodes) {
+                            float* ibox_all, const int* __restrict__ size_all, float4* nodes) {
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= Ftot) return;
     const SegCtx c = seg_ctx(segs, seg_of, bounds, g);
@@ -796,7 +843,9 @@ __global__ void k_collapse4(const BlasSeg* segs, const int* seg_of, const uint32
     for (int k = 0; k < 4; ++k) {
         child_box(refs[k], sorted_prim, tri_box, ibox, boxes[k]);
         gr[k] = global_ref(refs[k], node_base, leaf_base);
-        if (refs[k] >= 0 && LEAF_MAX > 1) {
+        // (subtree sizes from the fit / TRBVH: only subtrees of <= LEAF_MAX
+        // leaves are walked)
+        if (refs[k] >= 0 && LEAF_MAX > 1 && __ldcg(size_all + c.off + refs[k]) <= LEAF_MAX) {
             // a binary subtree over <= LEAF_MAX consecutive leaves becomes
             // one multi-triangle leaf
             int st[2 * LEAF_MAX], sp = 0, nl = 0, lmin = INT_MAX, lmax = -1;
@@ -840,10 +889,11 @@ __global__ void k_pack_tris(const BlasSeg* segs, const int* seg_of, const uint32
     d3 A = mkd(a[0], a[1], a[2]), B = mkd(b[0], b[1], b[2]), C = mkd(cc[0], cc[1], cc[2]);
     d3 E1 = subd(B, A), E2 = subd(C, A), E3 = subd(C, B);
     d3 N = crossd(E1, E2);
-    double two_area = sqrt(dotd(N, N));
-    double lmax = fmax(sqrt(dotd(E1, E1)), fmax(sqrt(dotd(E2, E2)), sqrt(dotd(E3, E3))));
+    const double n2 = dotd(N, N);
+    double two_area = sqrt(n2);
+    const double l2max = fmax(dotd(E1, E1), fmax(dotd(E2, E2), dotd(E3, E3)));
     // min altitude = 2A / longest edge; store its inverse, rounded up
-    float inv_min_alt = (float)(lmax / two_area) * 1.000001f;
+    float inv_min_alt = (float)sqrt(l2max / n2) * 1.000001f;
     int gl = S.leaf_base + p;
     tris[3 * gl + 0] = make_float4(a[0], a[1], a[2], inv_min_alt);
     tris[3 * gl + 1] = make_float4((float)E1.x, (float)E1.y, (float)E1.z, (float)two_area);
@@ -950,7 +1000,7 @@ cudaError_t blas_build_batch(BlasSeg* h_segs, int B, const BlasBatchArgs& a, voi
         k_pack_nodes<<<gb, T_BLK, 0, stream>>>(s.segs, s.seg_of, s.bounds, F, sv, s.tri_box, s.child, s.ibox,
                                                a.bnodes);
     k_collapse4<<<gb, T_BLK, 0, stream>>>(s.segs, s.seg_of, s.bounds, F, sv, s.tri_box, s.child, s.ibox,
-                                          a.nodes);
+                                          s.size, a.nodes);
     k_pack_tris<<<gb, T_BLK, 0, stream>>>(s.segs, s.seg_of, s.bounds, F, sv, sk, a.tris, a.triv,
                                           a.dbg_morton);
     k_asset_info<<<(B + 127) / 128, 128, 0, stream>>>(s.segs, B, s.bounds, s.ibox, s.tri_box, sv, s.depth);
