@@ -83,8 +83,10 @@ def parse():
     ap.add_argument("--tlas-step", default=None, choices=["build", "refit"],
                     help="per-step TLAS update (default: refit for c3/c4, whose obstacles "
                          "keep their poses; rebuild for c5, re-posed every step)")
-    ap.add_argument("--traversal", default="auto", choices=["auto", "lane"],
-                    help="auto: warp packets for camera / LiDAR tiles; lane: one ray per lane")
+    ap.add_argument("--traversal", default=None, choices=["auto", "lane"],
+                    help="auto: warp packets for camera / LiDAR tiles; lane: one ray per lane "
+                         "(default: lane for c6, whose terrain seen at grazing angles makes a "
+                         "4x8 packet test ~9x the triangles its rays need; auto elsewhere)")
     return ap.parse_args()
 
 
@@ -276,7 +278,8 @@ def main():
     chans = channels_for(cfg)
     trbvh_rounds = args.trbvh_rounds if args.trbvh_rounds is not None else (0 if cfg == 6 else 3)
     scene = agr.Scene.from_scenegen(sc, device=local, trbvh_rounds=trbvh_rounds)
-    scene.set_traversal(0 if args.traversal == "auto" else 1)
+    traversal = args.traversal or ("lane" if cfg == 6 else "auto")
+    scene.set_traversal(0 if traversal == "auto" else 1)
     tlas_builder = args.tlas_builder or ("lbvh" if cfg in (5, 6) else "sah")
     scene.set_tlas_builder(1 if tlas_builder == "sah" else 0)
     step_refit = (args.tlas_step or ("build" if cfg in (5, 6) else "refit")) == "refit"
@@ -370,7 +373,7 @@ def main():
         step(0)
         torch.cuda.synchronize()
         lane_counters = scene.counters()
-        scene.set_traversal(0 if args.traversal == "auto" else 1)
+        scene.set_traversal(0 if traversal == "auto" else 1)
         scene.enable_counters(False)
 
     # ---- end to end through the public C ABI with host buffers ------------
@@ -465,7 +468,7 @@ def main():
         "config": {"workload": WORKLOADS[cfg], "envs_per_gpu": E, "rays_per_step_per_gpu": rays_per_step,
                    "channels": list(chans), "parallelism": f"env-sharded x{world}",
                    "l2": "flushed between timed steps (256 MB write, untimed)",
-                   "trbvh_rounds": trbvh_rounds,
+                   "trbvh_rounds": trbvh_rounds, "traversal": traversal,
                    "step": ("update_meshes (every env's BLAS rebuilt)" if cfg == 6 else
                             "set_instance_transforms") + " + TLAS " + ("refit" if step_refit else "rebuild") +
                            " + cast (TLAS builder: " + tlas_builder + ")"},

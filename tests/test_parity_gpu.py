@@ -461,6 +461,10 @@ def test_update_mesh_per_env_unique_and_deforming():
         sc2 = sg.assemble(new_meshes, per_env)
         ref = oracle.cast(sc2, oracle_rays(sensor, "range"))
         compare(ref, got["dist"], got["seg"], got["face"], f"update step {step}")
+    # the binary LBVH export is packed by the create-time build only: after
+    # an update it is refused (ESTATE), the leaf order stays available
+    with pytest.raises(agr.AgrError, match="create-time"):
+        s.debug_export_blas(0)
 
 
 def test_update_meshes_batched_equals_one_by_one():
