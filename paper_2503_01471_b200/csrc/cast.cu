@@ -839,6 +839,23 @@ __device__ __noinline__ void resolve_leaf64(const CastArgs* a, int inst, int lea
     *best = b;
 }
 
+// FP64 arbitration of every candidate slot with t_lo <= U,
+// reading the slots and the ray identity from the lane's cold column.
+template <int MODEL>
+__device__ __noinline__ void arbitrate64(const CastArgs* a, float U, Best64* best) {
+    const RayId id = cold_id<MODEL>(*a);
+    const Ray64 r = gen_ray64<MODEL>(*a, id);
+    Best64 b = *best;
+    const int t = threadIdx.x;
+#pragma unroll
+    for (int k = 0; k < NSLOT; ++k) {
+        if (s_cold[C_TL0 + k][t] <= U)
+            consider64(a->sv, __float_as_int(s_cold[C_INST0 + k][t]), __float_as_int(s_cold[C_LEAF0 + k][t]), r,
+                       (double)a->max_range, b);
+    }
+    *best = b;
+}
+
 // Per-hit channels of PAPER.md:218 / :228 (surface normal, barycentrics,
 // point cloud), in FP64 from the winning triangle (reading R20).
 template <int MODEL>
@@ -991,7 +1008,17 @@ __global__ void __launch_bounds__(CAST_THREADS, CAST_MIN_BLOCKS) k_cast(const __
             } else {
                 traverse_lane<false, COUNT>(a.sv, id.env, rs, leaf_fn, cnt);
             }
-            best = rs.arbitrate<COUNT>(res, cnt);
+            // final arbitration: one out-of-line call per lane that builds the
+            // FP64 ray once for all of its surviving candidates
+            best = cold.best();
+            bool any = false;
+#pragma unroll
+            for (int k = 0; k < NSLOT; ++k) {
+                const bool live = cold.f(C_TL0 + k) <= rs.U;
+                if (COUNT && live) cnt.f64++;
+                any |= live;
+            }
+            if (any) arbitrate64<MODEL>(&a, rs.U, &best);
         }
         if (cold.i(C_OVF)) {
             if (COUNT) cnt.overflow++;
