@@ -531,6 +531,32 @@ def test_c6_unique_terrain_reset_small():
     compare(ref, got["dist"], got["seg"], got["face"], "c6 after reset")
 
 
+@pytest.mark.slow
+def test_c6_full_size_lane_mode_after_update():
+    """c6 at bench size in the bench's launch configuration: 256 unique
+    32768-triangle terrains, every mesh replaced by one agr_update_meshes
+    batch (plain LBVH), LBVH TLAS rebuilt, one ray per lane; sampled oracle
+    parity plus the per-ray certificate of all 8.3 M rays."""
+    sc, sensor = sg.config6()
+    s = make_scene(sc, trbvh_rounds=0)
+    s.set_tlas_builder(0)
+    s.set_traversal(1)
+    ring = sc.extra["ring_V"]
+    s.update_meshes(list(range(sc.n_envs)), torch.from_numpy(ring[1]).to(dev()))
+    s.build()
+    got = to_np(cast_sensor(s, sensor, "depth"))
+    V = len(sc.meshes[0].verts)
+    sc2 = sg.assemble([sg.Mesh(m.name, ring[1][i * V:(i + 1) * V], m.faces) for i, m in enumerate(sc.meshes)],
+                      [[(i, 1, sc.inst_T[i])] for i in range(sc.n_envs)])
+    q = np.random.default_rng(6).choice(len(got["dist"]), 20000, replace=False)
+    ref = oracle.cast(sc2, oracle_rays(sensor, "depth"), query=q)
+    compare(ref, got["dist"][q], got["seg"][q], got["face"][q], "c6 full size")
+    hit = got["face"] >= 0
+    assert hit.mean() > 0.5
+    assert certify_all(sc2, sensor, "depth", got["dist"], got["seg"], got["face"], "c6") == hit.sum()
+    s.close()
+
+
 # ---- f1: interpolated vertex annotations -------------------------------------------
 
 def _c2_annotations(sc, rng):
