@@ -31,6 +31,9 @@ namespace {
 #ifndef CAST_BLOCK
 #define CAST_BLOCK 64
 #endif
+#ifndef AGR_IPACKET
+#define AGR_IPACKET 1  // interval packets for primary pinhole / beam tiles
+#endif
 constexpr int CAST_THREADS = CAST_BLOCK;
 // Tile of one warp: TILE_W x TILE_H pixels (beams: columns x channels).
 #ifndef TILE_W
@@ -270,6 +273,16 @@ struct RayState {
     // TLAS leaf: move the ray into instance `inst`'s object space; returns the
     // BLAS root node.
     __device__ __forceinline__ int enter_instance(const SceneView& sv, int inst) {
+        f3 oo, od;
+        float delta;
+        const int root = enter_object(sv, inst, oo, od, delta);
+        sr = make_slab(oo, od, delta);
+        return root;
+    }
+
+    // enter_instance without the per-lane box-test state (interval packets
+    // build their own): object-space ray, its error bound, cold columns.
+    __device__ __forceinline__ int enter_object(const SceneView& sv, int inst, f3& oo_, f3& od_, float& delta_) {
         const float4* rp = sv.irec + 4 * inst;
         float4 r0 = __ldg(rp), r1 = __ldg(rp + 1), r2 = __ldg(rp + 2), r3 = __ldg(rp + 3);
         const f3 o = this->o(), d = this->d();
@@ -287,8 +300,10 @@ struct RayState {
         c.f(C_DELTA) = delta;
         const float dd = dot(od, od);
         c.f(C_DLEN) = dd > 0.0f ? dd * rsqrt_approx_ftz(dd) * 1.000001f : 0.0f;
-        sr = make_slab(oo, od, delta);
         cur_inst = inst;
+        oo_ = oo;
+        od_ = od;
+        delta_ = delta;
         return __float_as_int(r3.x);
     }
 
@@ -652,6 +667,217 @@ __device__ __forceinline__ void traverse_packet(const SceneView& sv, int env, Ra
     }
 }
 
+// ---- interval-packet traversal (primary pinhole / beam tiles) ---------------------
+// The 32 rays of a tile share their origin (the sensor's), so the set of
+// their directions lies in the per-axis interval [dmin, dmax] over the
+// lanes.  A node is visited if the *packet* may reach a child: lanes 0-3
+// each test one child against the whole interval (conservative: any lane's
+// own widened slab test passing implies this one passes),
+// lanes 4-7 test the same child with the tile's centre ray for the visiting
+// order.  One slab test per lane per node instead of four; leaves are still
+// tested by every lane on its own ray.
+//
+// Box-test state of one lane (its role: interval or centre ray) at one
+// level: per axis the widened origin offsets and the reciprocals of the
+// two direction endpoints.
+struct PSlab {
+    float olx, oly, olz;  // o + dp
+    float ohx, ohy, ohz;  // o - dp
+    float i0x, i0y, i0z;  // 1 / (lower direction endpoint)
+    float i1x, i1y, i1z;  // 1 / (upper direction endpoint)
+};
+constexpr int PS_N = 12;
+
+__device__ __forceinline__ int f2ord(float f) {
+    const int k = __float_as_int(f);
+    return k ^ ((k >> 31) & 0x7FFFFFFF);
+}
+__device__ __forceinline__ float ord2f(int k) { return __int_as_float(k ^ ((k >> 31) & 0x7FFFFFFF)); }
+
+// Reciprocal endpoints of a direction interval [lo, hi].  An interval
+// containing 0 keeps i0 = 1 / min(lo, -tiny) < 0 < i1 = 1 / max(hi, tiny):
+// pslab_axis tells it apart by the differing signs.
+__device__ __forceinline__ void iv_recip(float lo, float hi, float& i0, float& i1) {
+    if (lo > 0.0f || hi < 0.0f) {
+        i0 = rcp_approx_ftz(lo);
+        i1 = rcp_approx_ftz(hi);
+    } else {
+        i0 = rcp_approx_ftz(fminf(lo, -1e-30f));
+        i1 = rcp_approx_ftz(fmaxf(hi, 1e-30f));
+    }
+}
+
+// Packet box-test state from every lane's ray (o shared by all lanes, d its
+// own, delta its error bound); lanes with (lane & 4) take the centre ray.
+__device__ __forceinline__ PSlab make_pslab(f3 o, f3 d, float delta) {
+    const unsigned FULL = 0xFFFFFFFFu;
+    const bool centre = (threadIdx.x & 4) != 0;
+    const float dcx = __shfl_sync(FULL, d.x, TILE_CENTRE_LANE);
+    const float dcy = __shfl_sync(FULL, d.y, TILE_CENTRE_LANE);
+    const float dcz = __shfl_sync(FULL, d.z, TILE_CENTRE_LANE);
+    const float mnx = ord2f(__reduce_min_sync(FULL, f2ord(d.x))), mxx = ord2f(__reduce_max_sync(FULL, f2ord(d.x)));
+    const float mny = ord2f(__reduce_min_sync(FULL, f2ord(d.y))), mxy = ord2f(__reduce_max_sync(FULL, f2ord(d.y)));
+    const float mnz = ord2f(__reduce_min_sync(FULL, f2ord(d.z))), mxz = ord2f(__reduce_max_sync(FULL, f2ord(d.z)));
+    // twice the largest lane error bound: the interval arithmetic's own
+    // rounding (a few ulps of t) is far inside one delta
+    const float dp = 2.0f * __int_as_float(__reduce_max_sync(FULL, __float_as_int(delta)));
+    PSlab p;
+    p.olx = o.x + dp; p.oly = o.y + dp; p.olz = o.z + dp;
+    p.ohx = o.x - dp; p.ohy = o.y - dp; p.ohz = o.z - dp;
+    iv_recip(centre ? dcx : mnx, centre ? dcx : mxx, p.i0x, p.i1x);
+    iv_recip(centre ? dcy : mny, centre ? dcy : mxy, p.i0y, p.i1y);
+    iv_recip(centre ? dcz : mnz, centre ? dcz : mxz, p.i0z, p.i1z);
+    return p;
+}
+
+// Slab of one axis over every direction d in the interval (a = lo - o - dp,
+// b = hi - o + dp, b >= a):
+//   same-sign interval: near = min, far = max of {a, b} x {1/d0, 1/d1};
+//   interval containing 0 (i0 < 0 < i1): rays with d of the right sign
+//     enter no earlier than max(a / dmax, b / dmin) (o below lo: a / dmax,
+//     o above hi: b / dmin, o inside: negative) and, as d -> 0, never
+//     leave: far = +inf.
+__device__ __forceinline__ void pslab_axis(float lo, float hi, float ol, float oh, float i0, float i1,
+                                           float& n, float& f) {
+    const float a = lo - ol, b = hi - oh;
+    const float a0 = a * i0, a1 = a * i1, b0 = b * i0, b1 = b * i1;
+    const bool straddle = (__float_as_int(i0) ^ __float_as_int(i1)) < 0;
+    n = straddle ? fmaxf(a1, b0) : fminf(fminf(a0, a1), fminf(b0, b1));
+    f = straddle ? inf_f() : fmaxf(fmaxf(a0, a1), fmaxf(b0, b1));
+}
+
+// Interval slab test of child c of the node at nb against [0, U].
+__device__ __forceinline__ bool pslab_test(const PSlab& p, const float* nb, int c, float U, float& tnear) {
+    float nx, fx, ny, fy, nz, fz;
+    pslab_axis(__ldg(nb + c), __ldg(nb + 4 + c), p.olx, p.ohx, p.i0x, p.i1x, nx, fx);
+    pslab_axis(__ldg(nb + 8 + c), __ldg(nb + 12 + c), p.oly, p.ohy, p.i0y, p.i1y, ny, fy);
+    pslab_axis(__ldg(nb + 16 + c), __ldg(nb + 20 + c), p.olz, p.ohz, p.i0z, p.i1z, nz, fz);
+    const float tn = fmaxf(fmaxf(nx, ny), fmaxf(nz, 0.0f));
+    const float tf = fminf(fminf(fx, fy), fminf(fz, U));
+    tnear = tn;
+    return tn <= tf;
+}
+
+__device__ __forceinline__ void pslab_store(float* dst, const PSlab& p) {
+    dst[0] = p.olx; dst[1] = p.oly; dst[2] = p.olz;
+    dst[3] = p.ohx; dst[4] = p.ohy; dst[5] = p.ohz;
+    dst[6] = p.i0x; dst[7] = p.i0y; dst[8] = p.i0z;
+    dst[9] = p.i1x; dst[10] = p.i1y; dst[11] = p.i1z;
+}
+__device__ __forceinline__ PSlab pslab_load(const float* src) {
+    PSlab p;
+    p.olx = src[0]; p.oly = src[1]; p.olz = src[2];
+    p.ohx = src[3]; p.ohy = src[4]; p.ohz = src[5];
+    p.i0x = src[6]; p.i0y = src[7]; p.i0z = src[8];
+    p.i1x = src[9]; p.i1y = src[10]; p.i1z = src[11];
+    return p;
+}
+
+// Closest-hit traversal of a tile whose rays share their origin.  ps_env /
+// ps_obj: this warp's shared-memory copies of the two roles' box-test state
+// at the env / current object level ([2][PS_N] each).
+template <bool COUNT, class LEAF>
+__device__ __forceinline__ void traverse_ipacket(const SceneView& sv, int env, RayState& rs,
+                                                 const LEAF& leaf_fn, int* wstack, float* ps_env,
+                                                 float* ps_obj, Counters& cnt) {
+    const unsigned FULL = 0xFFFFFFFFu;
+    const int lane = threadIdx.x & 31;
+    const bool leader = lane == 0;
+    const int child = lane & 3;
+    const int role = (lane >> 2) & 1;
+    PSlab ps = make_pslab(rs.o(), rs.d(), K_ERR * rs.c.f(C_Q));
+    if (child == 0 && lane < 8) pslab_store(ps_env + role * PS_N, ps);
+    __syncwarp();
+    float Umax = __int_as_float(__reduce_max_sync(FULL, __float_as_int(rs.U)));
+    int sp = 0;
+    int node = __ldg(sv.tlas_root + env);
+    for (;;) {
+        if (node >= 0) {
+            if (COUNT) cnt.nodes++;
+            if (COUNT && rs.cur_inst < 0) cnt.tnodes++;
+            const float* nb = reinterpret_cast<const float*>(sv.nodes + 8 * (size_t)node);
+            const float4 r4 = __ldg(sv.nodes + 8 * (size_t)node + 6);
+            float tn;
+            const bool h = pslab_test(ps, nb, child, Umax, tn);
+            const unsigned cm = __ballot_sync(FULL, h) & 0xFu;
+            const int nh = __popc(cm);
+            int ref[4] = {__float_as_int(r4.x), __float_as_int(r4.y), __float_as_int(r4.z), __float_as_int(r4.w)};
+            if (nh == 0) {
+                if (sp == 0) break;
+                __syncwarp();
+                node = wstack[--sp];
+                continue;
+            }
+            if (nh == 1) {
+                const int only = __ffs(cm) - 1;
+                node = only == 0 ? ref[0] : only == 1 ? ref[1] : only == 2 ? ref[2] : ref[3];
+                continue;
+            }
+            // order by the centre ray's entry distance (lanes 4-7), misses last
+            unsigned key[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const unsigned kc = __shfl_sync(FULL, __float_as_uint(tn), 4 + k);
+                key[k] = (cm >> k) & 1u ? kc : KEY_MISS;
+            }
+            sort4(key, ref);
+            if (sp + 3 <= PSTACK) {
+                __syncwarp();
+                if (leader) {
+                    int q = sp;
+                    if (nh > 3) wstack[q++] = ref[3];
+                    if (nh > 2) wstack[q++] = ref[2];
+                    wstack[q] = ref[1];
+                }
+                sp += nh - 1;
+            } else {
+                rs.c.i(C_OVF) = 1;
+            }
+            node = ref[0];
+            continue;
+        }
+        if (node == SENTINEL) {  // back to the env level
+            rs.cur_inst = -1;
+            ps = pslab_load(ps_env + role * PS_N);
+            if (sp == 0) break;
+            __syncwarp();
+            node = wstack[--sp];
+            continue;
+        }
+        const int leaf = ~node;
+        if (rs.cur_inst < 0) {
+            if (COUNT) cnt.insts++;
+            if (sp < PSTACK) {
+                __syncwarp();
+                if (leader) wstack[sp] = SENTINEL;
+                ++sp;
+            } else {
+                rs.c.i(C_OVF) = 1;
+                break;
+            }
+            f3 oo, od;
+            float delta;
+            node = rs.enter_object(sv, leaf, oo, od, delta);
+            ps = make_pslab(oo, od, delta);
+            __syncwarp();
+            if (child == 0 && lane < 8) pslab_store(ps_obj + role * PS_N, ps);
+            __syncwarp();
+            continue;
+        }
+        if (COUNT) cnt.leaves++;
+        leaf_fn(leaf & LEAF_MASK);
+        if (leaf >> LEAF_SHIFT) {
+            if (COUNT) cnt.leaves++;
+            leaf_fn((leaf & LEAF_MASK) + 1);
+        }
+        Umax = __int_as_float(__reduce_max_sync(FULL, __float_as_int(rs.U)));
+        __syncwarp();
+        ps = pslab_load(ps_obj + role * PS_N);
+        if (sp == 0) break;
+        node = wstack[--sp];
+    }
+}
+
 // ---- ray generation -----------------------------------------------------------------
 struct RayId {
     int env;
@@ -969,6 +1195,7 @@ __device__ __forceinline__ RayId ray_id(const CastArgs& a) {
 template <int MODEL, int TRAV, bool COUNT, bool STEREO>
 __global__ void __launch_bounds__(CAST_THREADS, CAST_MIN_BLOCKS) k_cast(const __grid_constant__ CastArgs a) {
     __shared__ int s_stack[TRAV == 1 ? CAST_THREADS / 32 : 1][TRAV == 1 ? PSTACK : 1];
+    __shared__ float s_pslab[TRAV == 1 ? CAST_THREADS / 32 : 1][2][2 * PS_N];  // [warp][env, obj][role][PS_N]
     RayId id = ray_id<MODEL>(a);
     // ragged tile lanes keep the warp whole for the traversal: they trace a
     // copy of a valid pixel and store nothing
@@ -1004,7 +1231,12 @@ __global__ void __launch_bounds__(CAST_THREADS, CAST_MIN_BLOCKS) k_cast(const __
             auto leaf_fn = [&](int leaf) { rs.leaf_filter<COUNT>(a.sv, leaf, res, cnt); };
             if (TRAV == 1) {
                 // whole warps share (env, sensor): pinhole / beams tiles
+#if AGR_IPACKET
+                traverse_ipacket<COUNT>(a.sv, id.env, rs, leaf_fn, s_stack[threadIdx.x >> 5],
+                                        s_pslab[threadIdx.x >> 5][0], s_pslab[threadIdx.x >> 5][1], cnt);
+#else
                 traverse_packet<false, COUNT>(a.sv, id.env, rs, leaf_fn, s_stack[threadIdx.x >> 5], cnt);
+#endif
             } else {
                 traverse_lane<false, COUNT>(a.sv, id.env, rs, leaf_fn, cnt);
             }
