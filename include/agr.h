@@ -320,8 +320,13 @@ agr_status agr_set_tlas_builder(agr_scene scene, int32_t builder);
 
 /*
  * Traversal schedule (results are identical either way): 0 = auto (default;
- * the 32 rays of an 8x4 pinhole / beam tile traverse as one warp packet),
- * 1 = one independent ray per lane.  Explicit rays always use 1.
+ * the 32 rays of a 4x8 pinhole / beam tile traverse as one warp packet: a
+ * node is visited when the interval of the tile's ray directions may reach
+ * a child, and every lane still tests each visited leaf on its own ray;
+ * stereo shadow segments, whose origins differ per lane, visit the union
+ * of the lanes' own box tests), 1 = one independent ray per lane (faster
+ * when a tile's rays diverge, e.g. terrain seen at grazing angles).
+ * Explicit rays always use 1.
  */
 agr_status agr_set_traversal(agr_scene scene, int32_t mode);
 
@@ -332,7 +337,8 @@ agr_status agr_set_traversal(agr_scene scene, int32_t mode);
  * arbitration tests, [5] candidate-list overflows / stack fallbacks,
  * [6] internal nodes visited at the TLAS level, [7] instance entries whose
  * BLAS root test hit no child for the lane's own ray (node and leaf counts
- * are per lane: in packet mode every lane counts each warp visit).
+ * are per lane: in packet mode every lane counts each warp visit; [7] is
+ * counted in mode 1 only).
  */
 agr_status agr_enable_counters(agr_scene scene, int32_t enable);
 agr_status agr_get_counters(agr_scene scene, int64_t counters[8]);
