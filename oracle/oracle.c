@@ -149,9 +149,17 @@ typedef struct {
     double normal[3], bary[2], point[3];
 } ray_result;
 
+/* In-plane distance (metres) within which a plane hit just outside a
+ * triangle still counts as a candidate hit for the tie carve-out
+ * (reading R24): a ray through a shared edge or vertex hits both
+ * triangles geometrically, but an FP64 edge test may exclude one of them by
+ * rounding (~1e-15 relative), which would hide the second candidate. */
+#define ORACLE_NEAR_DIST 1e-9
+
 static void cast_one(const world_mesh* w, v3 o, v3 d, double max_range,
                      double eps, int want_graze, ray_result* out, int64_t* tests) {
     double best_t = INFINITY, second_t = INFINITY, graze = INFINITY;
+    double near_t = INFINITY; /* nearest near-candidate (outside by <= ORACLE_NEAR_DIST) */
     int64_t best_f = -1;
     int near_zero = 0;
     /* candidates within eps of max_range, kept to decide AMB_RANGE at the end */
@@ -179,6 +187,14 @@ static void cast_one(const world_mesh* w, v3 o, v3 d, double max_range,
                     second_t = t;
                 }
             }
+        } else if (t > 0.0 && t <= max_range + eps && t < near_t) {
+            /* edge function e_i = |edge_i| |n| (in-plane distance of p to edge i) */
+            const double nn2 = vdot(n, n), lim = ORACLE_NEAR_DIST * ORACLE_NEAR_DIST;
+            v3 ab = vsub(b, a), bc = vsub(c, b), ca = vsub(a, c);
+            int near = (e0 >= 0.0 || e0 * e0 <= lim * vdot(ab, ab) * nn2) &&
+                       (e1 >= 0.0 || e1 * e1 <= lim * vdot(bc, bc) * nn2) &&
+                       (e2 >= 0.0 || e2 * e2 <= lim * vdot(ca, ca) * nn2);
+            if (near) near_t = t;
         }
     }
     *tests += w->n_tri;
@@ -203,6 +219,9 @@ static void cast_one(const world_mesh* w, v3 o, v3 d, double max_range,
     }
     int amb = 0;
     if (second_t - best_t <= eps) amb |= ORACLE_AMB_TIE;
+    /* a near-candidate within eps of the winner, in front of it, or on a
+     * ray that hits nothing: the FP64 edge tests may go either way */
+    if (near_t < INFINITY && near_t <= best_t + eps) amb |= ORACLE_AMB_TIE;
     if (range_cand < INFINITY && range_cand <= best_t) amb |= ORACLE_AMB_RANGE;
     if (near_zero) amb |= ORACLE_AMB_ZERO;
     if (best_f >= 0) {
@@ -215,7 +234,9 @@ static void cast_one(const world_mesh* w, v3 o, v3 d, double max_range,
         out->face = -1;
     }
     out->amb = amb;
-    out->t2 = second_t;
+    /* the other candidate of a tie: the second-best hit, or a nearer
+     * near-candidate (reading R24) */
+    out->t2 = near_t < second_t ? near_t : second_t;
     out->graze = graze;
     /* per-hit channels of the winning face */
     out->point[0] = o.x + out->t * d.x;

@@ -83,7 +83,9 @@ typedef struct {
 
 /* Ambiguity bits (SURVEY.md §8(c) parity rules). */
 enum {
-    ORACLE_AMB_TIE   = 1, /* best and second-best candidate t within amb_eps */
+    ORACLE_AMB_TIE   = 1, /* best and second-best candidate t within amb_eps, or a
+                             plane hit within 1e-9 m outside a triangle at t <=
+                             best + amb_eps (shared edges / vertices)          */
     ORACLE_AMB_RANGE = 2, /* a candidate within amb_eps of max_range         */
     ORACLE_AMB_ZERO  = 4, /* a candidate within amb_eps of t = 0             */
     ORACLE_AMB_SHADOW = 8 /* a shadow-segment candidate within amb_eps of eps
@@ -98,7 +100,9 @@ enum {
  *   dist[q]  (float)t64[q]
  *   seg[q]   instance label or -1;  face[q] per-env face index or -1
  *   amb[q]   ORACLE_AMB_* bits computed with tolerance amb_eps (metres)
- *   t2[q]    second-best candidate t (+inf if none)             [may be NULL]
+ *   t2[q]    the other candidate of a tie: second-best hit t, or a nearer
+ *            plane hit within 1e-9 m outside its triangle (R24);
+ *            +inf if none                                          [may be NULL]
  *   graze[q] smallest distance (scene units) by which the plane hit of a
  *            triangle closer than the winner lies outside that triangle
  *            (diagnostic for silhouette rays; +inf if none)     [may be NULL]

@@ -326,6 +326,37 @@ def test_tie_goes_to_lowest_face_and_is_flagged():
     assert np.all(r.amb & oracle.AMB_TIE)
 
 
+def test_shared_vertex_rays_are_flagged():
+    """A ray aimed exactly at a vertex shared by two triangles (generic FP32
+    coordinates; origin 0, direction = the vertex) hits both geometrically,
+    but the FP64 edge tests of its rounded hit point may exclude one of
+    them.  Every such ray must be flagged AMB_TIE (north_star: 'except for
+    rays whose two candidate hits lie within 1e-5 m of each other'; DESIGN.md
+    reading R24).  Control: rays aimed at the triangles' interiors are not
+    flagged."""
+    rng = np.random.default_rng(11)
+    n_hit = 0
+    for trial in range(200):
+        a, b, c = rng.uniform(-1, 1, (3, 3))
+        e = a + b - c  # across edge ab from c: a planar convex quad
+        a, b, c, e = (np.asarray(v + (4.0, 0.0, 0.0), np.float32) for v in (a, b, c, e))  # in front of 0
+        m = sg.Mesh("two", np.stack([a, b, c, e]).astype(np.float32),
+                    np.asarray([[0, 1, 2], [1, 0, 3]], np.int32))
+        sc = sg.assemble([m], [[(0, 1, sg.make_T(np.eye(3), (0, 0, 0)))]])
+        d = np.stack([a, b])[None].astype(np.float32)  # aimed at the two shared vertices
+        r = cast_rays(sc, np.zeros((1, 2, 3), np.float32), d)
+        hit = r.face >= 0
+        n_hit += int(hit.sum())
+        assert np.all(r.amb[hit] & oracle.AMB_TIE), trial
+        # interior points (barycentric weights >= 0.2 each) are unambiguous
+        w = 0.2 + 0.4 * rng.dirichlet([4, 4, 4], 8)
+        w = w / w.sum(1, keepdims=True)
+        q = w @ np.stack([a, b, c]).astype(np.float64)
+        r2 = cast_rays(sc, np.zeros((1, 8, 3), np.float32), q[None].astype(np.float32))
+        assert np.all(r2.face == 0) and not np.any(r2.amb & oracle.AMB_TIE), trial
+    assert n_hit > 300
+
+
 def test_degenerate_face_kept_for_numbering_never_hit():
     """Zero-area faces keep the numbering and are never hit (reading R12)."""
     v = np.asarray([[0, -5, -5], [0, 5, -5], [0, 5, 5], [0, -5, 5]], np.float32)

@@ -48,6 +48,27 @@ def test_c2_full(kind):
     assert (ref.face >= 0).mean() > 0.1
 
 
+def test_axis_aligned_centre_rays():
+    """Odd image sizes put the centre column / row rays exactly on the
+    sensor axes, so a tile's direction interval touches or straddles 0
+    (the packet traversal's sign-change branch) at the env level and, with
+    identity / 90-degree-yaw instance transforms, at the object level."""
+    sc1, _ = sg.config1()
+    c2, _ = sg.config2(n_envs=3)
+    per_env = [[(0, 1, sg.make_T(np.eye(3), (0.0, 0.0, 0.0)))],
+               [(0, 2, sg.make_T(sg.rot_z(np.pi / 2), (0.0, 0.0, 0.0)))],
+               [(0, 3, sg.make_T(np.eye(3), (0.0, 0.0, 0.0))), (1, 4, c2.inst_T[0])]]
+    sc = sg.assemble([sc1.meshes[0], c2.meshes[c2.inst_asset[0]]], per_env)
+    poses = np.zeros((3, 2, 3, 4), np.float32)
+    for e in range(3):
+        poses[e, 0] = sg.make_T(np.eye(3), (0.0, 0.0, 0.0))
+        poses[e, 1] = sg.make_T(sg.rot_z(np.pi / 2), (2.5, -3.0, 0.0))
+    sensor = dict(kind="pinhole", cam=sg.pinhole(33, 17, 90.0), poses=poses, max_range=10.0)
+    for kind in ("depth", "range"):
+        res, got, ref = _check_full(sc, sensor, kind, f"axis-aligned {kind}")
+        assert (ref.face >= 0).mean() > 0.05
+
+
 def test_ragged_multisensor_random_poses():
     """Image sizes that are not tile multiples, 2 sensors per env, random poses."""
     sc, sensor = sg.config2(n_envs=6)
