@@ -69,6 +69,45 @@ def test_axis_aligned_centre_rays():
         assert (ref.face >= 0).mean() > 0.05
 
 
+@pytest.mark.parametrize("scale", [0.01, 100.0])
+def test_scaled_scene_and_sensor(scale):
+    """The whole c2 scene, the sensor positions and max_range scaled by
+    0.01 / 100 (instances then carry scales of 0.005-0.015 / 50-150): the
+    error model's bounds scale with the scene, so parity
+    holds at the tolerance of the scaled distances."""
+    sc, sensor = sg.config2(n_envs=4)
+    T = sc.inst_T.astype(np.float64) * scale
+    sc = sg.Scene(sc.meshes, sc.env_off, sc.inst_asset, sc.inst_label, T.astype(np.float32))
+    rng = np.random.default_rng(21)
+    poses = np.zeros((4, 1, 3, 4), np.float32)
+    for e in range(4):
+        poses[e, 0] = sg.make_T(sg.rot_z(rng.uniform(-0.4, 0.4)), rng.uniform(-0.5, 0.5, 3) * scale)
+    sensor = dict(sensor, poses=poses, max_range=10.0 * scale, cam=sg.pinhole(96, 64, 87.0))
+    for kind in ("depth", "range"):
+        res, got, ref = _check_full(sc, sensor, kind, f"scale {scale} {kind}")
+        assert (ref.face >= 0).mean() > 0.1
+
+
+def test_sensor_on_a_surface():
+    """Sensors placed exactly on a face plane of the config-1 cube (x = 2,
+    inside the face, on an edge, on a corner) looking in several directions:
+    candidates at t = 0 are excluded by the (0, max_range] rule on both
+    sides (AMB_ZERO flags them for seg / face), distances must still match."""
+    sc, sensor = sg.config1()
+    spots = [(2.0, 0.0, 0.0), (2.0, 0.5, 0.0), (2.0, 0.5, 0.5), (2.0, 0.1, -0.2)]
+    yaws = [0.0, np.pi, np.pi / 2]
+    poses = np.zeros((1, len(spots) * len(yaws), 3, 4), np.float32)
+    k = 0
+    for p_ in spots:
+        for y in yaws:
+            poses[0, k] = sg.make_T(sg.rot_z(y), p_)
+            k += 1
+    sensor = dict(sensor, poses=poses, cam=sg.pinhole(24, 16, 100.0))
+    for kind in ("depth", "range"):
+        res, got, ref = _check_full(sc, sensor, kind, f"on-surface {kind}")
+        assert res["ambiguous"] > 0
+
+
 def test_ragged_multisensor_random_poses():
     """Image sizes that are not tile multiples, 2 sensors per env, random poses."""
     sc, sensor = sg.config2(n_envs=6)
