@@ -131,6 +131,36 @@ def reduce_max(t, world):
     return t
 
 
+def combine_checksums(sums, env0=0):
+    """One 64-bit digest of per-env checksums (agr_checksum) in global env
+    order: sum over envs of checksum_e * (2 e + 1) mod 2^64, so a run on N
+    GPUs and a run of the same global envs on one GPU give the same digest."""
+    mask = (1 << 64) - 1
+    acc = 0
+    for i, v in enumerate(np.asarray(sums, np.int64).tolist()):
+        acc = (acc + (v & mask) * (2 * (env0 + i) + 1)) & mask
+    return f"{acc:016x}"
+
+
+def gather_checksums(sums, local_ms, world):
+    """All-gather every rank's per-env checksums and its local ms/step (the
+    only data-path collective of the bench: NCCL under torchrun, outside the
+    timed region; BASELINE.json north_star).  Returns (digest over all
+    ranks' envs in global order, [ms/step per rank])."""
+    import torch
+    import torch.distributed as dist
+    ms = torch.tensor([local_ms], dtype=torch.float64, device=sums.device)
+    if dist.is_available() and dist.is_initialized() and world > 1:
+        gs = [torch.zeros_like(sums) for _ in range(world)]
+        gm = [torch.zeros_like(ms) for _ in range(world)]
+        dist.all_gather(gs, sums)
+        dist.all_gather(gm, ms)
+        allsums, allms = torch.cat(gs), torch.cat(gm)
+    else:
+        allsums, allms = sums, ms
+    return combine_checksums(allsums.cpu().numpy()), [float(x) for x in allms.cpu()]
+
+
 def rays_per_env(sensor):
     if sensor["kind"] == "pinhole":
         return sensor["cam"]["W"] * sensor["cam"]["H"] * sensor["poses"].shape[1]
@@ -355,6 +385,10 @@ def main():
     cast_ms = [b.elapsed_time(c) for a, b, c in ev]
     total_ms = sum(step_ms)
     cast_total = sum(cast_ms)
+    # per-env checksums of the last step's images and every rank's own
+    # ms/step, all-gathered (untimed)
+    digest, rank_ms = gather_checksums(scene.checksum(out, rays_per_env(sensor), stream),
+                                       total_ms / args.steps, world)
     t = reduce_max(torch.tensor([total_ms, cast_total], dtype=torch.float64, device=dev), world)
     if distributed:
         dist.barrier()
@@ -473,6 +507,8 @@ def main():
                             "set_instance_transforms") + " + TLAS " + ("refit" if step_refit else "rebuild") +
                            " + cast (TLAS builder: " + tlas_builder + ")"},
         "update_ms_per_step": (total_ms - cast_total) / args.steps,
+        "checksum": {"digest": digest, "envs": E * world, "last_step": args.steps - 1,
+                     "rank_ms_per_step": rank_ms},
         "env_frames_per_sec": E * poses.shape[1] * world / (ms_per_step / 1e3),
         "cast_ms_per_step": cast_total / args.steps,
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,

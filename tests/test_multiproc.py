@@ -77,3 +77,39 @@ def test_two_rank_sharding_matches_single_process(cfg):
 
 def test_env_base_is_weak_scaling():
     assert [bench.env_base(r, 1024) for r in range(4)] == [0, 1024, 2048, 3072]
+
+
+def _ck_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    rng = np.random.default_rng(rank)
+    sums = torch.from_numpy(rng.integers(-2**63, 2**63 - 1, 5, dtype=np.int64))
+    digest, ms = bench.gather_checksums(sums, 1.5 + rank, world)
+    if rank == 0:
+        q.put((digest, ms))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_checksum_gather_equals_single_process_digest():
+    """bench.gather_checksums (the bench's one collective): the digest of
+    two ranks' per-env checksums equals the single-process digest of the
+    concatenation in global env order, and every rank's ms is reported."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ck_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    digest, ms = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+    allsums = np.concatenate([np.random.default_rng(r).integers(-2**63, 2**63 - 1, 5, dtype=np.int64)
+                              for r in range(2)])
+    assert digest == bench.combine_checksums(allsums)
+    assert ms == [1.5, 2.5]
+    # order matters (global env order), a single changed checksum changes it
+    assert bench.combine_checksums(allsums[::-1]) != digest
+    alt = allsums.copy()
+    alt[7] ^= 1
+    assert bench.combine_checksums(alt) != digest
