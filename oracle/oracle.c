@@ -188,12 +188,13 @@ static void cast_one(const world_mesh* w, v3 o, v3 d, double max_range,
                 }
             }
         } else if (t > 0.0 && t <= max_range + eps && t < near_t) {
-            /* edge function e_i = |edge_i| |n| (in-plane distance of p to edge i) */
-            const double nn2 = vdot(n, n), lim = ORACLE_NEAR_DIST * ORACLE_NEAR_DIST;
-            v3 ab = vsub(b, a), bc = vsub(c, b), ca = vsub(a, c);
-            int near = (e0 >= 0.0 || e0 * e0 <= lim * vdot(ab, ab) * nn2) &&
-                       (e1 >= 0.0 || e1 * e1 <= lim * vdot(bc, bc) * nn2) &&
-                       (e2 >= 0.0 || e2 * e2 <= lim * vdot(ca, ca) * nn2);
+            /* edge function e_i = |edge_i| |n| (in-plane distance of p to edge i);
+             * each outside edge must be within ORACLE_NEAR_DIST */
+            const double lim = ORACLE_NEAR_DIST * ORACLE_NEAR_DIST * vdot(n, n);
+            int near = 1;
+            if (e0 < 0.0) { v3 ab = vsub(b, a); near = e0 * e0 <= lim * vdot(ab, ab); }
+            if (near && e1 < 0.0) { v3 bc = vsub(c, b); near = e1 * e1 <= lim * vdot(bc, bc); }
+            if (near && e2 < 0.0) { v3 ca = vsub(a, c); near = e2 * e2 <= lim * vdot(ca, ca); }
             if (near) near_t = t;
         }
     }
