@@ -27,7 +27,8 @@ _LIB_PATH = os.path.join(_HERE, "liboracle.so")
 
 RAYS, PINHOLE, BEAMS = 0, 1, 2
 DEPTH, RANGE = 0, 1
-AMB_TIE, AMB_RANGE, AMB_ZERO, AMB_SHADOW = 1, 2, 4, 8
+AMB_TIE, AMB_RANGE, AMB_ZERO, AMB_SHADOW, AMB_GRAZE = 1, 2, 4, 8, 16
+NEAR_REL = 2.0 ** -40  # oracle.c ORACLE_NEAR_REL: near-candidate band nu = NEAR_REL * M
 AMB_EPS = 1e-5  # metres, SURVEY.md §8(c) parity rules / BASELINE.json north_star
 
 

@@ -149,33 +149,73 @@ typedef struct {
     double normal[3], bary[2], point[3];
 } ray_result;
 
-/* In-plane distance (metres) within which a plane hit just outside a
- * triangle still counts as a candidate hit for the tie carve-out
- * (reading R24): a ray through a shared edge or vertex hits both
- * triangles geometrically, but an FP64 edge test may exclude one of them by
- * rounding (~1e-15 relative), which would hide the second candidate. */
-#define ORACLE_NEAR_DIST 1e-9
+/* Near candidates (reading R24).  A ray through a shared edge or
+ * vertex hits both triangles geometrically, but an FP64 edge test of the
+ * rounded hit point (this file's edge functions, the GPU's FP64
+ * Moller-Trumbore) can exclude either of them by rounding.  Both computations
+ * start from the same FP32 inputs promoted to double; every quantity they
+ * form (world vertices A v + b, the hit point o + t d, edge and cross
+ * products) carries a relative error of a few tens of units of 2^-53 of the
+ * largest coordinate magnitude M involved.  A plane hit whose in-plane
+ * distance outside its triangle is at most
+ *     nu = ORACLE_NEAR_REL * M,   M = |o|_inf + |t| |d|_inf + max_vertex |v|_inf,
+ * (2^-40: ~2^8 times that rounding) is therefore a candidate hit that either
+ * FP64 implementation may accept. */
+#define ORACLE_NEAR_REL 9.094947017729282e-13 /* 2^-40 */
+
+static double vmaxabs(v3 a) {
+    double m = fabs(a.x);
+    if (fabs(a.y) > m) m = fabs(a.y);
+    if (fabs(a.z) > m) m = fabs(a.z);
+    return m;
+}
+
+/* Plane hit of ray (o, d) with triangle (a, b, c): t, and whether the hit
+ * point lies inside (inclusive edges) or, for 0 < t <= near_tmax only,
+ * outside by at most nu (near). */
+typedef struct { int parallel, inside, near; double t; } plane_hit;
+
+static plane_hit hit_plane(v3 o, v3 d, v3 a, v3 b, v3 c, double near_tmax) {
+    plane_hit h = {0, 0, 0, 0.0};
+    v3 n = vcross(vsub(b, a), vsub(c, a));
+    double denom = vdot(n, d);
+    if (denom == 0.0) { h.parallel = 1; return h; } /* parallel ray or zero-area triangle */
+    h.t = vdot(n, vsub(a, o)) / denom;
+    v3 p = {o.x + h.t * d.x, o.y + h.t * d.y, o.z + h.t * d.z};
+    /* edge function e_i = ((v_{i+1} - v_i) x (p - v_i)) . n = |edge_i| |n| times
+     * the signed in-plane distance of p to edge i (>= 0 on the inner side) */
+    double e0 = vdot(vcross(vsub(b, a), vsub(p, a)), n);
+    double e1 = vdot(vcross(vsub(c, b), vsub(p, b)), n);
+    double e2 = vdot(vcross(vsub(a, c), vsub(p, c)), n);
+    h.inside = e0 >= 0.0 && e1 >= 0.0 && e2 >= 0.0;
+    if (!h.inside && h.t > 0.0 && h.t <= near_tmax) {
+        double M = vmaxabs(o) + fabs(h.t) * vmaxabs(d);
+        double mv = vmaxabs(a);
+        if (vmaxabs(b) > mv) mv = vmaxabs(b);
+        if (vmaxabs(c) > mv) mv = vmaxabs(c);
+        double nu = ORACLE_NEAR_REL * (M + mv);
+        const double lim = nu * nu * vdot(n, n);
+        int near = 1;
+        if (e0 < 0.0) { v3 ab = vsub(b, a); near = e0 * e0 <= lim * vdot(ab, ab); }
+        if (near && e1 < 0.0) { v3 bc = vsub(c, b); near = e1 * e1 <= lim * vdot(bc, bc); }
+        if (near && e2 < 0.0) { v3 ca = vsub(a, c); near = e2 * e2 <= lim * vdot(ca, ca); }
+        h.near = near;
+    }
+    return h;
+}
 
 static void cast_one(const world_mesh* w, v3 o, v3 d, double max_range,
                      double eps, int want_graze, ray_result* out, int64_t* tests) {
     double best_t = INFINITY, second_t = INFINITY, graze = INFINITY;
-    double near_t = INFINITY; /* nearest near-candidate (outside by <= ORACLE_NEAR_DIST) */
     int64_t best_f = -1;
-    int near_zero = 0;
+    int near_zero = 0, any_near = 0;
     /* candidates within eps of max_range, kept to decide AMB_RANGE at the end */
     double range_cand = INFINITY;
     for (int64_t k = 0; k < w->n_tri; ++k) {
-        v3 a = w->v[3 * k], b = w->v[3 * k + 1], c = w->v[3 * k + 2];
-        v3 n = vcross(vsub(b, a), vsub(c, a));
-        double denom = vdot(n, d);
-        if (denom == 0.0) continue; /* parallel ray or zero-area triangle */
-        double t = vdot(n, vsub(a, o)) / denom;
-        v3 p = {o.x + t * d.x, o.y + t * d.y, o.z + t * d.z};
-        /* inclusive inside test: p on the inner side of all three edges */
-        double e0 = vdot(vcross(vsub(b, a), vsub(p, a)), n);
-        double e1 = vdot(vcross(vsub(c, b), vsub(p, b)), n);
-        double e2 = vdot(vcross(vsub(a, c), vsub(p, c)), n);
-        if (e0 >= 0.0 && e1 >= 0.0 && e2 >= 0.0) {
+        plane_hit h = hit_plane(o, d, w->v[3 * k], w->v[3 * k + 1], w->v[3 * k + 2], max_range + eps);
+        if (h.parallel) continue;
+        double t = h.t;
+        if (h.inside) {
             if (fabs(t) <= eps) near_zero = 1;
             if (fabs(t - max_range) <= eps && t < range_cand) range_cand = t;
             if (t > 0.0 && t <= max_range) {
@@ -187,15 +227,25 @@ static void cast_one(const world_mesh* w, v3 o, v3 d, double max_range,
                     second_t = t;
                 }
             }
-        } else if (t > 0.0 && t <= max_range + eps && t < near_t) {
-            /* edge function e_i = |edge_i| |n| (in-plane distance of p to edge i);
-             * each outside edge must be within ORACLE_NEAR_DIST */
-            const double lim = ORACLE_NEAR_DIST * ORACLE_NEAR_DIST * vdot(n, n);
-            int near = 1;
-            if (e0 < 0.0) { v3 ab = vsub(b, a); near = e0 * e0 <= lim * vdot(ab, ab); }
-            if (near && e1 < 0.0) { v3 bc = vsub(c, b); near = e1 * e1 <= lim * vdot(bc, bc); }
-            if (near && e2 < 0.0) { v3 ca = vsub(a, c); near = e2 * e2 <= lim * vdot(ca, ca); }
-            if (near) near_t = t;
+        } else if (h.near) {
+            any_near = 1;
+        }
+    }
+    /* near candidates against the winner (second pass, only on the rare rays
+     * that have one): one within eps of the winner is a tie (AMB_TIE, t2 is
+     * its t); one more than eps in front of it -- or on a ray that otherwise
+     * misses -- is a silhouette graze (AMB_GRAZE: hit it or pass it, t2 is
+     * the nearest such t) */
+    double tie_near = INFINITY, graze_near = INFINITY;
+    if (any_near) {
+        for (int64_t k = 0; k < w->n_tri; ++k) {
+            plane_hit h = hit_plane(o, d, w->v[3 * k], w->v[3 * k + 1], w->v[3 * k + 2], max_range + eps);
+            if (h.parallel || h.inside || !h.near) continue;
+            if (best_f >= 0 && fabs(h.t - best_t) <= eps) {
+                if (fabs(h.t - best_t) < fabs(tie_near - best_t)) tie_near = h.t;
+            } else if (best_f < 0 || h.t < best_t - eps) {
+                if (h.t < graze_near) graze_near = h.t;
+            }
         }
     }
     *tests += w->n_tri;
@@ -220,9 +270,8 @@ static void cast_one(const world_mesh* w, v3 o, v3 d, double max_range,
     }
     int amb = 0;
     if (second_t - best_t <= eps) amb |= ORACLE_AMB_TIE;
-    /* a near-candidate within eps of the winner, in front of it, or on a
-     * ray that hits nothing: the FP64 edge tests may go either way */
-    if (near_t < INFINITY && near_t <= best_t + eps) amb |= ORACLE_AMB_TIE;
+    if (tie_near < INFINITY) amb |= ORACLE_AMB_TIE;
+    if (graze_near < INFINITY) amb |= ORACLE_AMB_GRAZE;
     if (range_cand < INFINITY && range_cand <= best_t) amb |= ORACLE_AMB_RANGE;
     if (near_zero) amb |= ORACLE_AMB_ZERO;
     if (best_f >= 0) {
@@ -235,9 +284,11 @@ static void cast_one(const world_mesh* w, v3 o, v3 d, double max_range,
         out->face = -1;
     }
     out->amb = amb;
-    /* the other candidate of a tie: the second-best hit, or a nearer
-     * near-candidate (reading R24) */
-    out->t2 = near_t < second_t ? near_t : second_t;
+    /* the other candidate: a graze in front of the winner first (its t is
+     * the alternative distance), else the closer of the second-best hit and
+     * a tied near candidate (both within eps of the winner when flagged) */
+    if (graze_near < INFINITY) out->t2 = graze_near;
+    else out->t2 = tie_near < second_t ? tie_near : second_t;
     out->graze = graze;
     /* per-hit channels of the winning face */
     out->point[0] = o.x + out->t * d.x;

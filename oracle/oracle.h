@@ -81,15 +81,21 @@ typedef struct {
     float stereo_eps;
 } oracle_rays;
 
-/* Ambiguity bits (SURVEY.md §8(c) parity rules). */
+/* Ambiguity bits (SURVEY.md §8(c) parity rules; reading R24). */
 enum {
     ORACLE_AMB_TIE   = 1, /* best and second-best candidate t within amb_eps, or a
-                             plane hit within 1e-9 m outside a triangle at t <=
-                             best + amb_eps (shared edges / vertices)          */
+                             near candidate (a plane hit outside its triangle by
+                             at most nu = 2^-40 M, the FP64 rounding band of
+                             hit_plane()) within amb_eps of the best t
+                             (shared edges / vertices)                       */
     ORACLE_AMB_RANGE = 2, /* a candidate within amb_eps of max_range         */
     ORACLE_AMB_ZERO  = 4, /* a candidate within amb_eps of t = 0             */
-    ORACLE_AMB_SHADOW = 8 /* a shadow-segment candidate within amb_eps of eps
+    ORACLE_AMB_SHADOW = 8, /* a shadow-segment candidate within amb_eps of eps
                              or of L - eps                                   */
+    ORACLE_AMB_GRAZE = 16 /* a near candidate more than amb_eps in front of the
+                             best hit, or on a ray that otherwise misses: a
+                             silhouette graze within FP64 rounding (hit it or
+                             pass it; t2 = its t)                            */
 };
 
 /*
@@ -100,9 +106,10 @@ enum {
  *   dist[q]  (float)t64[q]
  *   seg[q]   instance label or -1;  face[q] per-env face index or -1
  *   amb[q]   ORACLE_AMB_* bits computed with tolerance amb_eps (metres)
- *   t2[q]    the other candidate of a tie: second-best hit t, or a nearer
- *            plane hit within 1e-9 m outside its triangle (R24);
- *            +inf if none                                          [may be NULL]
+ *   t2[q]    the other candidate: on an AMB_GRAZE ray the nearest grazing
+ *            near candidate's t; otherwise the second-best hit t or a tied
+ *            near candidate's t, whichever is closer (within amb_eps of
+ *            t64 when AMB_TIE is set; R24); +inf if none [may be NULL]
  *   graze[q] smallest distance (scene units) by which the plane hit of a
  *            triangle closer than the winner lies outside that triangle
  *            (diagnostic for silhouette rays; +inf if none)     [may be NULL]

@@ -27,25 +27,51 @@ DIST_ABS = 1e-5
 DIST_REL = 1e-6
 
 
-def compare(ref: "oracle.OracleResult", dist, seg, face, what=""):
+def amb_bound(n: int, frac: float = 2e-4, floor: int = 8) -> int:
+    """Default upper bound on the rays a parity test may exclude as ambiguous:
+    near-ties of generic workloads are rare (measured: 2 of 388 800 c2
+    stereo rays), so a flag that fired on every silhouette or edge ray would
+    exceed it."""
+    return max(floor, int(frac * n))
+
+
+def compare(ref: "oracle.OracleResult", dist, seg, face, what="", max_amb=None, max_graze=None):
     """Apply the parity rules; returns a dict of counts, raises on failure.
 
     distance: every ray within max(1e-5, 1e-6*ref) of the oracle's FP64 t;
-    on a tie ray (AMB_TIE) the other candidate's t (ref.t2) is accepted too
-    -- the two only differ when that candidate is a plane hit within 1e-9 m
-    of a triangle boundary, e.g. a silhouette edge (reading R24).
+    on a tie ray (AMB_TIE) the other tied candidate's t (ref.t2, within
+    1e-5 m of t by construction) is accepted too, and on a graze ray
+    (AMB_GRAZE: a near candidate within FP64 rounding of its triangle's
+    boundary in front of the winner, reading R24) the grazed
+    candidate's t.
     seg / face: bit-exact on every ray that is not ambiguous (oracle AMB_*).
+    Bounds: at most ``max_amb`` ambiguous rays (default amb_bound(n)) and at
+    most ``max_graze`` graze rays (default max(2, 1e-5 n)) -- tests that aim
+    rays at edges on purpose pass their own bounds.
     """
     dist = np.asarray(dist, np.float64).reshape(-1)
+    n = len(dist)
     tol = np.maximum(DIST_ABS, DIST_REL * np.abs(ref.t64))
     err = np.abs(dist - ref.t64)
     tie = (ref.amb & oracle.AMB_TIE) != 0
+    graze = (ref.amb & oracle.AMB_GRAZE) != 0
     with np.errstate(invalid="ignore"):
-        alt = tie & (np.abs(dist - ref.t2) <= np.maximum(DIST_ABS, DIST_REL * np.abs(ref.t2)))
+        tol2 = np.maximum(DIST_ABS, DIST_REL * np.abs(ref.t2))
+        # the oracle only flags a tie whose other candidate is within AMB_EPS
+        assert np.all(~tie | graze | (np.abs(ref.t2 - ref.t64) <= oracle.AMB_EPS)), f"{what}: tie t2 too far"
+        alt = (tie | graze) & (np.abs(dist - ref.t2) <= tol2)
     bad_d = np.nonzero((err > tol) & ~alt)[0]
     amb = ref.amb != 0
-    out = dict(n=len(dist), ambiguous=int(amb.sum()), max_err=float(err.max()) if len(err) else 0.0)
+    out = dict(n=n, ambiguous=int(amb.sum()), ties=int(tie.sum()), grazes=int(graze.sum()),
+               graze_alt=int((graze & alt & (err > tol)).sum()),
+               max_err=float(err.max()) if len(err) else 0.0)
     msgs = []
+    lim_amb = amb_bound(n) if max_amb is None else max_amb
+    lim_graze = max(2, int(1e-5 * n)) if max_graze is None else max_graze
+    if out["ambiguous"] > lim_amb:
+        msgs.append(f"{what}: {out['ambiguous']} ambiguous rays of {n} exceed the bound {lim_amb}")
+    if out["grazes"] > lim_graze:
+        msgs.append(f"{what}: {out['grazes']} graze rays of {n} exceed the bound {lim_graze}")
     if len(bad_d):
         i = bad_d[0]
         msgs.append(f"{what}: {len(bad_d)} distance mismatches; first #{i}: gpu={dist[i]!r} "
@@ -67,6 +93,20 @@ def compare(ref: "oracle.OracleResult", dist, seg, face, what=""):
     if msgs:
         raise AssertionError("\n".join(msgs))
     return out
+
+
+def valid_compare(ref: "oracle.OracleResult", valid, what="", max_amb=None):
+    """Stereo shadow mask (f2) parity: bit-exact on every ray the oracle does
+    not flag ambiguous, with the ambiguous count bounded (amb_bound(n) by
+    default).  Returns the number of shadowed (invalid) pixels."""
+    valid = np.asarray(valid).reshape(-1)
+    amb = ref.amb != 0
+    n_amb = int(amb.sum())
+    lim = amb_bound(len(valid)) if max_amb is None else max_amb
+    assert n_amb <= lim, f"{what}: {n_amb} ambiguous rays of {len(valid)} exceed the bound {lim}"
+    bad = np.nonzero((valid != ref.valid) & ~amb)[0]
+    assert len(bad) == 0, f"{what}: {len(bad)} valid mismatches, first {bad[:5]}"
+    return int((ref.valid == 0).sum())
 
 
 def compare_extras(ref: "oracle.OracleResult", normal=None, bary=None, point=None, face=None, what=""):

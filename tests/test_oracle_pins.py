@@ -769,3 +769,160 @@ def test_annotation_linear_field_reproduction():
     # the FP32-rounded field values carry ~1e-7 relative error
     assert np.allclose(r.annot[on_soup], want, atol=2e-6)
     assert np.all(np.isnan(r.annot[r.face == 20]))
+
+
+# --------------------------------------------------------------------------
+# ambiguity flags: the near-candidate band (reading R24) and the
+# stereo shadow band edges (reading R21), pinned on both sides
+# --------------------------------------------------------------------------
+
+def _outside_distance(p, a, b, c):
+    """In-plane distance (FP64) by which point p (on the triangle's plane)
+    lies outside triangle abc, from its barycentric coordinates (a different
+    formula from the oracle's edge functions): 0 inside."""
+    e1, e2 = b - a, c - a
+    G = np.array([[e1 @ e1, e1 @ e2], [e1 @ e2, e2 @ e2]])
+    u, v = np.linalg.solve(G, np.array([(p - a) @ e1, (p - a) @ e2]))
+    w = 1.0 - u - v
+    dist = 0.0
+    for lam, (q0, q1, opp) in ((w, (b, c, a)), (u, (c, a, b)), (v, (a, b, c))):
+        if lam < 0:  # p beyond the edge opposite the vertex with weight lam
+            ed = q1 - q0
+            h = np.linalg.norm(np.cross(ed, opp - q0)) / np.linalg.norm(ed)  # altitude
+            dist = max(dist, -lam * h)
+    return dist
+
+
+def test_near_candidate_band_is_fp64_rounding():
+    """A plane hit just outside an isolated triangle is a near candidate
+    (AMB_GRAZE on the otherwise-missing ray) only within FP64 rounding of the
+    scene's magnitudes (nu = 2^-40 M, R24), not within a fixed
+    1e-9 m: rays that pass the edge by more than 2^-36 M (16 nu) and less
+    than 1e-9 m are clean misses; rays through a vertex, or within 2^-46 M of
+    the edge, are hits or grazes.  A millimetre-sized triangle puts FP32
+    direction quantisation (~1e-10 m) between the two bands."""
+    rng = np.random.default_rng(5)
+    n_band = n_vert = 0
+    for trial in range(60):
+        a, b, c = (rng.uniform(-1e-3, 1e-3, 3) + np.array([4e-3, 0, 0]) for _ in range(3))
+        a, b, c = (np.asarray(v, np.float32) for v in (a, b, c))
+        m = sg.Mesh("tri", np.stack([a, b, c]), np.asarray([[0, 1, 2]], np.int32))
+        sc = sg.assemble([m], [[(0, 1, sg.make_T(np.eye(3), (0, 0, 0)))]])
+        A, B, C = (v.astype(np.float64) for v in (a, b, c))
+        # aim just outside edge AB (away from C), and at the three vertices
+        w = rng.uniform(0.1, 0.9, 40)
+        out_dir = (A + B) / 2 - C
+        off = rng.uniform(0.0, 1e-9, 40)[:, None] * out_dir / np.linalg.norm(out_dir)
+        tgt = A + w[:, None] * (B - A) + off
+        dirs = np.concatenate([tgt, np.stack([A, B, C])]).astype(np.float32)[None]
+        r = cast_rays(sc, np.zeros_like(dirs), dirs, max_range=2.0)
+        n = np.cross(B - A, C - A)
+        M = 2.0 * np.abs(dirs[0]).max() + np.abs(np.stack([A, B, C])).max()
+        for i in range(40):
+            dd = dirs[0, i].astype(np.float64)
+            t = n @ A / (n @ dd)
+            dist = _outside_distance(t * dd, A, B, C)
+            if dist > 2.0 ** -36 * M:
+                assert r.face[i] == -1 and r.amb[i] == 0, (trial, i, dist)
+                n_band += dist < 1e-9
+            elif dist <= 2.0 ** -46 * M:  # on the edge within rounding: a hit, or a flagged graze
+                assert r.face[i] == 0 or r.amb[i] & oracle.AMB_GRAZE, (trial, i, dist)
+        for i in range(40, 43):  # vertex-aimed: a hit, or a flagged graze
+            assert r.face[i] == 0 or (r.amb[i] & oracle.AMB_GRAZE and r.t2[i] > 0), (trial, i)
+            n_vert += 1
+    assert n_band > 1000  # these all sat inside the old fixed 1e-9 m band
+
+
+def test_graze_never_flags_generic_rays():
+    """Negative pin of AMB_GRAZE / AMB_TIE: 20 000 random rays through the
+    cluttered c2 scene (generic FP32 directions) come nowhere near FP64
+    rounding of an edge, so no ray is a graze and almost none a tie (a
+    flag that fired on silhouettes or on every edge crossing would fail)."""
+    sc, _ = sg.config2(n_envs=4)
+    rng = np.random.default_rng(9)
+    o = rng.uniform([-1, -3, -2], [1, 3, 2], (4, 5000, 3)).astype(np.float32)
+    d = (rng.uniform([2, -3, -1.5], [8, 3, 1.5], (4, 5000, 3)) - o).astype(np.float32)
+    r = cast_rays(sc, o, d, max_range=2.0)
+    assert (r.face >= 0).mean() > 0.2
+    assert not np.any(r.amb & oracle.AMB_GRAZE)
+    assert np.count_nonzero(r.amb & oracle.AMB_TIE) <= 2
+
+
+def _beams_at(points, pose_T=None):
+    """Unit beam table [1][K][3] aimed from the sensor origin at `points`."""
+    d = np.asarray(points, np.float64)
+    d = d / np.linalg.norm(d, axis=1, keepdims=True)
+    return d[None].astype(np.float32)
+
+
+def _shadow_case(occluder, o2, wall_x=2.0, eps=1e-4, ys=None, zs=None):
+    """Wall x = wall_x (200 m quad) + one occluder quad; beams (range) from
+    the origin aimed at wall points (wall_x, y, z); second sensor at o2."""
+    wall = quad_mesh(200.0)
+    sc = sg.assemble([wall, occluder], [[(0, 1, sg.make_T(np.eye(3), (wall_x, 0, 0))),
+                                         (1, 2, sg.make_T(np.eye(3), (0, 0, 0)))]])
+    pts = np.stack([np.full_like(ys, wall_x), ys, zs], 1)
+    beams = _beams_at(pts)
+    rays = dict(model=oracle.BEAMS, beams=beams, poses=sg.identity_poses(1), max_range=20.0)
+    r = oracle.cast(sc, rays, stereo=(tuple(o2), eps))
+    # the hit point in FP64 from the FP32 beam (normalised in FP64, reading R19)
+    bd = beams[0].astype(np.float64)
+    bd = bd / np.linalg.norm(bd, axis=1, keepdims=True)
+    p = bd * (wall_x / bd[:, :1])
+    u = np.asarray(o2, np.float64) - p
+    L = np.linalg.norm(u, axis=1)
+    u = u / L[:, None]
+    return r, p, u, L
+
+
+def test_stereo_shadow_flag_at_eps_closed_form():
+    """AMB_SHADOW at the self-hit guard: an occluder in the plane y = y0
+    (x in [1, wall_x), never crossed by the primary rays, which stay at
+    y > y0) crosses each shadow segment at distance s = (p_y - y0) / -u_y
+    from its hit point p.  The oracle must flag exactly the rays with
+    |s - eps| <= 1e-5 and mark a pixel invalid exactly when eps < s < L - eps
+    (reading R21); both sides of the band are pinned, so a
+    flag set on every shadowed ray, or on none, fails."""
+    y0, eps, wall_x = -0.25, 1e-4, 2.0
+    occ = sg.Mesh("occ", np.asarray([[1.0, y0, -1], [wall_x - 1e-7, y0, -1], [wall_x - 1e-7, y0, 1],
+                                     [1.0, y0, 1]], np.float32), np.asarray([[0, 1, 2], [0, 2, 3]], np.int32))
+    ys = y0 + np.linspace(0.0, 3e-4, 601)
+    zs = np.linspace(-0.3, 0.3, 601)
+    r, p, u, L = _shadow_case(occ, (0.0, -4.0, 0.0), wall_x, eps, ys, zs)
+    assert np.all(r.face >= 0) and np.all(r.seg == 1)  # every beam reaches the wall
+    s = (p[:, 1] - y0) / -u[:, 1]
+    x_cross = p[:, 0] + s * u[:, 0]
+    crosses = (x_cross >= 1.0) & (np.abs(p[:, 2] + s * u[:, 2]) <= 1.0)
+    assert crosses.all()
+    clear = np.abs(np.abs(s - eps) - 1e-5) > 1e-9  # off the flag band's own edges
+    want_flag = np.abs(s - eps) <= 1e-5
+    got_flag = (r.amb & oracle.AMB_SHADOW) != 0
+    assert np.array_equal(got_flag[clear], want_flag[clear])
+    assert want_flag[clear].sum() >= 20 and (~want_flag[clear]).sum() >= 200
+    sharp = np.abs(s - eps) > 1e-9
+    assert np.array_equal(r.valid[sharp] == 0, ((s > eps) & (s < L - eps))[sharp])
+    assert (r.valid == 0).sum() >= 100 and (r.valid == 1).sum() >= 50
+
+
+def test_stereo_shadow_flag_at_far_end_closed_form():
+    """AMB_SHADOW at the far end L - eps: an occluder in the plane
+    y = -b + delta just in front of the second sensor o2 = (0, -b, 0) meets
+    each segment at distance s' = delta / -u_y before o2; flagged exactly
+    when |s' - eps| <= 1e-5, invalid exactly when s' > eps."""
+    b, eps, wall_x = 4.0, 1e-4, 2.0
+    delta = 1.2e-4 * 0.7
+    occ = sg.Mesh("occ", np.asarray([[-1, -b + delta, -1], [1, -b + delta, -1], [1, -b + delta, 1],
+                                     [-1, -b + delta, 1]], np.float32), np.asarray([[0, 1, 2], [0, 2, 3]], np.int32))
+    delta = float(np.float32(-b + delta)) + b  # the plane's FP32 position
+    ys = np.linspace(-0.5, 0.5, 41).repeat(41)
+    zs = np.tile(np.linspace(-6.0, 6.0, 41), 41)
+    r, p, u, L = _shadow_case(occ, (0.0, -b, 0.0), wall_x, eps, ys, zs)
+    assert np.all(r.face >= 0)
+    s2 = delta / -u[:, 1]
+    clear = np.abs(np.abs(s2 - eps) - 1e-5) > 1e-9
+    want_flag = np.abs(s2 - eps) <= 1e-5
+    got_flag = (r.amb & oracle.AMB_SHADOW) != 0
+    assert np.array_equal(got_flag[clear], want_flag[clear])
+    assert want_flag[clear].sum() >= 20 and (~want_flag[clear]).sum() >= 200
+    sharp = np.abs(s2 - eps) > 1e-9
+    assert np.array_equal(r.valid[sharp] == 0, (s2 > eps)[sharp])

@@ -16,17 +16,17 @@ import torch
 import oracle
 import paper_2503_01471_b200 as agr
 import scenegen as sg
-from helpers import certify_all, compare, compare_extras, oracle_rays
+from helpers import certify_all, compare, compare_extras, oracle_rays, valid_compare
 from gpu_util import cast_sensor, dev, make_scene, to_np
 
 pytestmark = pytest.mark.gpu
 
 
-def _check_full(sc, sensor, kind="depth", what=""):
+def _check_full(sc, sensor, kind="depth", what="", **bounds):
     s = make_scene(sc)
     got = to_np(cast_sensor(s, sensor, kind))
     ref = oracle.cast(sc, oracle_rays(sensor, kind))
-    res = compare(ref, got["dist"], got["seg"], got["face"], what)
+    res = compare(ref, got["dist"], got["seg"], got["face"], what, **bounds)
     s.close()
     return res, got, ref
 
@@ -65,7 +65,8 @@ def test_axis_aligned_centre_rays():
         poses[e, 1] = sg.make_T(sg.rot_z(np.pi / 2), (2.5, -3.0, 0.0))
     sensor = dict(kind="pinhole", cam=sg.pinhole(33, 17, 90.0), poses=poses, max_range=10.0)
     for kind in ("depth", "range"):
-        res, got, ref = _check_full(sc, sensor, kind, f"axis-aligned {kind}")
+        # rays exactly on the cube faces' diagonals: 63 ties / 4 grazes of 3366
+        res, got, ref = _check_full(sc, sensor, kind, f"axis-aligned {kind}", max_amb=100, max_graze=8)
         assert (ref.face >= 0).mean() > 0.05
 
 
@@ -104,7 +105,8 @@ def test_sensor_on_a_surface():
             k += 1
     sensor = dict(sensor, poses=poses, cam=sg.pinhole(24, 16, 100.0))
     for kind in ("depth", "range"):
-        res, got, ref = _check_full(sc, sensor, kind, f"on-surface {kind}")
+        # every ray starts on the face plane: all AMB_ZERO by construction
+        res, got, ref = _check_full(sc, sensor, kind, f"on-surface {kind}", max_amb=sensor["poses"].shape[1] * 24 * 16)
         assert res["ambiguous"] > 0
 
 
@@ -175,7 +177,9 @@ def test_edge_and_vertex_targeted_rays():
     s = make_scene(sc)
     got = to_np(s.cast_rays(torch.from_numpy(o).to(dev()), torch.from_numpy(d).to(dev()), 12.0))
     ref = oracle.cast(sc, dict(model=oracle.RAYS, orig=o, dir=d, max_range=12.0))
-    res = compare(ref, got["dist"], got["seg"], got["face"], "edge rays")
+    # shared-edge rays are ties by construction (11 % of them), never grazes
+    # of more than a few
+    res = compare(ref, got["dist"], got["seg"], got["face"], "edge rays", max_amb=len(ref.amb) // 5)
     assert res["ambiguous"] > 100  # the generator really produces near-ties
 
 
@@ -247,7 +251,9 @@ def test_degenerate_faces_and_max_range_boundary():
     s = make_scene(sc)
     got = to_np(s.cast_rays(torch.from_numpy(o).to(dev()), torch.from_numpy(d).to(dev()), 10.0))
     ref = oracle.cast(sc, dict(model=oracle.RAYS, orig=o, dir=d, max_range=10.0))
-    compare(ref, got["dist"], got["seg"], got["face"], "degenerate/max-range")
+    # envs 0 and 1 put the quad within 1e-5 of max_range: their 128 rays are AMB_RANGE
+    res = compare(ref, got["dist"], got["seg"], got["face"], "degenerate/max-range", max_amb=128)
+    assert res["ambiguous"] == 128
     f = got["face"].reshape(3, 64)
     assert set(np.unique(f[2])) <= {2, 3}
 
@@ -397,7 +403,7 @@ def test_extras_lidar_and_rays():
     out = s2.cast_rays(torch.from_numpy(o).to(dev()), torch.from_numpy(d).to(dev()), 12.0, channels=ALL)
     got = to_np(out)
     ref = oracle.cast(sc2, dict(model=oracle.RAYS, orig=o, dir=d, max_range=12.0), extras=True)
-    compare(ref, got["dist"], got["seg"], got["face"], "edge extras")
+    compare(ref, got["dist"], got["seg"], got["face"], "edge extras", max_amb=len(ref.amb) // 5)
     compare_extras(ref, got["normal"], got["bary"], got["point"], got["face"], "edge extras")
 
 
@@ -413,13 +419,6 @@ def test_extras_host_path():
 
 # ---- f2: stereo shadow mask --------------------------------------------------------
 
-def _valid_compare(ref, got, what):
-    amb = ref.amb != 0
-    bad = np.nonzero((got["valid"] != ref.valid) & ~amb)[0]
-    assert len(bad) == 0, f"{what}: {len(bad)} valid mismatches, first {bad[:5]}"
-    return int((ref.valid == 0).sum())
-
-
 @pytest.mark.parametrize("baseline", [0.095, 0.5])
 def test_stereo_mask_c2(baseline):
     """Stereo shadow mask vs the oracle on c2 envs."""
@@ -429,7 +428,7 @@ def test_stereo_mask_c2(baseline):
     got = to_np(cast_sensor(s, sensor, "depth", channels=("dist", "seg", "face", "valid")))
     ref = oracle.cast(sc, oracle_rays(sensor, "depth"), stereo=((0.0, -baseline, 0.0), 1e-4))
     compare(ref, got["dist"], got["seg"], got["face"], "stereo")
-    n_shadow = _valid_compare(ref, got, f"stereo b={baseline}")
+    n_shadow = valid_compare(ref, got["valid"], f"stereo b={baseline}")
     assert n_shadow > 100
     # the mask does not change the other channels
     core = to_np(cast_sensor(s, sensor, "depth"))
@@ -445,7 +444,7 @@ def test_stereo_mask_lidar_and_lane_mode():
     chans = ("dist", "seg", "face", "valid")
     got = to_np(cast_sensor(s, sensor, "range", channels=chans))
     ref = oracle.cast(sc, oracle_rays(sensor, "range"), stereo=((0.0, 0.0, 0.3), 1e-4))
-    _valid_compare(ref, got, "lidar stereo")
+    valid_compare(ref, got["valid"], "lidar stereo")
     s.set_traversal(1)
     lane = to_np(cast_sensor(s, sensor, "range", channels=chans))
     for k in got:
