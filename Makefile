@@ -10,7 +10,7 @@ HDR := $(PKG)/csrc/agr_internal.cuh include/agr.h
 OBJ := $(patsubst $(PKG)/csrc/%.cu,build/%.o,$(SRC))
 LIB := $(PKG)/lib/libagr.so
 
-all: $(LIB) oracle/liboracle.so
+all: $(LIB) oracle/liboracle.so tools/fma_peak
 
 build/%.o: $(PKG)/csrc/%.cu $(HDR)
 	@mkdir -p build
@@ -23,10 +23,13 @@ $(LIB): $(OBJ)
 oracle/liboracle.so: oracle/oracle.c oracle/oracle.h
 	gcc -O2 -std=c11 -fPIC -shared -pthread -Wall -o $@ oracle/oracle.c -lm
 
+tools/fma_peak: tools/fma_peak.cu
+	$(NVCC) $(ARCH) -O3 -o $@ $<
+
 ptxas: $(SRC) $(HDR)
 	$(NVCC) $(NVFLAGS) -Xptxas -v -c $(PKG)/csrc/cast.cu -o /dev/null
 
 clean:
-	rm -rf build $(LIB) oracle/liboracle.so
+	rm -rf build $(LIB) oracle/liboracle.so tools/fma_peak
 
 .PHONY: all clean ptxas

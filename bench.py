@@ -3,21 +3,30 @@
 rays/sec and env-frames/sec at 1/2/4/8 B200; % of roofline).
 
 One step = one pass of the whole per-step hot path over one batch of envs
-(SURVEY.md §8(a)): set the instance transforms (a3) + per-env TLAS build
-(a2; c5 uses the in-place refit) + one fused cast (a4 ray generation, a5
-traversal, a6 FP64 epilogue + stores).  The per-asset BLAS (a1) is built
-once at scene creation, as in the paper (the BVH is computed
-"exclusively for randomization").
+(SURVEY.md §8(a)): set the instance transforms (a3) + per-env TLAS refit or
+rebuild (a2/a3) + one fused cast (a4 ray generation, a5 traversal, a6 FP64
+epilogue + stores).  The per-asset BLAS (a1) is built once at scene
+creation, as in the paper (the BVH is computed "exclusively
+for randomization"); c6 (f3) rebuilds every env's BLAS inside the step.
 
-Default workload (N=1): config 3 -- 1024 envs per GPU, forest scene (ground
-+ 40 trees + 10 rocks, ~56k triangles per env), 270x480 D455-like depth
-camera, depth + segmentation + face index (BASELINE.json configs[2], the
-north-star target).  Multi-GPU: one process per GPU (torchrun), each rank
-casts its own block of envs (weak scaling: per-GPU work fixed); the step
-time is the max over ranks; no data-path collective (envs are independent,
-PAPER.md:226).
+Default workload (N=1): config 3 -- 1024 envs, forest scene (ground + 40
+trees + 10 rocks, ~56k triangles per env), 270x480 D455-like depth camera,
+depth + segmentation + face index (BASELINE.json configs[2], the north-star
+target).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 3|4|5]
+Multi-GPU: one process per GPU.  Under
+torchrun the ranks come from the environment; `python bench.py --gpus N`
+without it re-launches itself under `torch.distributed.run` (the driver's
+own launch line).  Scaling is STRONG by default: the config's total envs
+(c3 1024, c4 4096, c5 16384, c6 256) are split into contiguous blocks, GPU g
+owning [floor(g E / n), floor((g + 1) E / n)); `--scaling weak` keeps the
+per-GPU envs fixed instead.  No collective on the data path (envs are
+independent); after the timed region one NCCL all-gather
+carries every rank's per-env image checksums and ms/step, and for N > 1
+rank 0 re-casts the same global envs alone and checks that the 1-GPU digest
+equals the N-GPU one.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 3|4|5|6]
     python bench.py --impl reference ...   # the CPU oracle arm
 """
 from __future__ import annotations
@@ -25,7 +34,10 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import platform
+import socket
 import statistics
+import subprocess
 import sys
 import threading
 import time
@@ -50,30 +62,39 @@ TRAFFIC_PATH = os.path.join(ROOT, "profiles", "cast_traffic.json")
 C_BOX, C_LOOP, C_TRI, C_XF, C_RAY = 20, 15, 40, 25, 70
 BVH_WIDTH = 4
 
+# Total envs of each config (strong scaling splits them over the GPUs) and
+# the per-GPU envs of --scaling weak.
+TOTAL_ENVS = {3: 1024, 4: 4096, 5: 16384, 6: 256}
+WEAK_ENVS = {3: 1024, 4: 512, 5: 2048, 6: 256}
+
 WORKLOADS = {
-    3: "c3: forest, 1024 envs/GPU (ground + 40 trees + 10 rocks, ~56k tri/env), "
-       "270x480 D455-like pinhole (87 deg hfov) depth + seg + face, max 10 m",
-    4: "c4: Table II-shaped room + 15 floating obstacles, 512 envs/GPU (4096 over 8 GPUs), "
-       "OS0-128-style LiDAR 128x512 range + seg, max 10 m",
-    5: "c5: Table I-shaped 20 cubes/env re-posed every step (TLAS rebuild), 2048 envs/GPU "
-       "(16384 over 8 GPUs), 135x240 depth + seg + face, max 10 m",
+    3: "c3: forest (ground + 40 trees + 10 rocks, ~56k tri/env), 270x480 D455-like pinhole "
+       "(87 deg hfov) depth + seg + face, max 10 m",
+    4: "c4: Table II-shaped room + 15 floating obstacles, OS0-128-style LiDAR 128x512 "
+       "range + seg, max 10 m",
+    5: "c5: Table I-shaped 20 cubes/env re-posed every step, 135x240 depth + seg + face, max 10 m",
     6: "c6 (f3): per-env unique terrain (32768 tri/env), every env's mesh re-randomised and "
-       "its BLAS rebuilt every step (agr_update_meshes), 256 envs/GPU, 135x240 depth + seg + face, "
-       "max 20 m",
+       "its BLAS rebuilt every step (agr_update_meshes), 135x240 depth + seg + face, max 20 m",
 }
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=3, choices=[3, 4, 5, 6])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--envs", type=int, default=None, help="envs per GPU (default: config's)")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="strong: the config's total envs split over the GPUs (default); "
+                         "weak: a fixed number of envs per GPU")
+    ap.add_argument("--envs", type=int, default=None,
+                    help="total envs (strong) or envs per GPU (weak); default: the config's")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-counters", action="store_true")
+    ap.add_argument("--no-verify", action="store_true",
+                    help="skip rank 0's 1-GPU re-cast of all envs (digest check, N > 1)")
     ap.add_argument("--trbvh-rounds", type=int, default=None,
                     help="BLAS treelet-restructuring rounds (default 3; 0 for c6, whose BLAS "
                          "are rebuilt every step: there the LBVH alone is the better trade)")
@@ -87,13 +108,49 @@ def parse():
                     help="auto: warp packets for camera / LiDAR tiles; lane: one ray per lane "
                          "(default: lane for c6, whose terrain seen at grazing angles makes a "
                          "4x8 packet test ~9x the triangles its rays need; auto elsewhere)")
-    return ap.parse_args()
+    ap.add_argument("--selftest", action="store_true",
+                    help="CPU-only check of the multi-rank plumbing (gloo): spawn, env "
+                         "sharding, all-gather, digest; no CUDA")
+    return ap.parse_args(argv)
 
 
-def envs_per_gpu(args):
-    if args.envs:
-        return args.envs
-    return {3: 1024, 4: 512, 5: 2048, 6: 256}[args.config]
+# --------------------------------------------------------------------------
+# ranks, sharding, collectives
+# --------------------------------------------------------------------------
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def spawn_ranks(n, argv):
+    """Re-launch this script as n ranks under torch.distributed.run (the
+    same launch line the driver uses); rank 0's JSON line reaches our
+    stdout.  Returns the launcher's exit code."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__)] + list(argv)
+    return subprocess.call(cmd)
+
+
+def total_envs(args, world):
+    if args.scaling == "weak":
+        return (args.envs or WEAK_ENVS[args.config]) * world
+    return args.envs or TOTAL_ENVS[args.config]
+
+
+def shard(E_total, rank, world):
+    """GPU g owns global envs [floor(g E / n), floor((g + 1) E / n))
+    (SURVEY.md §8(e)): (first env, env count)."""
+    lo = E_total * rank // world
+    hi = E_total * (rank + 1) // world
+    return lo, hi - lo
+
+
+def env_base(rank, envs_per_rank):
+    """Weak scaling: rank r owns global envs [r E, (r+1) E)."""
+    return rank * envs_per_rank
 
 
 def make_workload(cfg, n_envs, env_base):
@@ -118,11 +175,6 @@ def blas_launches(n_assets, trbvh_rounds):
     return n
 
 
-def env_base(rank, envs_per_rank):
-    """Weak scaling: rank r owns global envs [r E, (r+1) E) (DESIGN.md §9)."""
-    return rank * envs_per_rank
-
-
 def reduce_max(t, world):
     """Max over ranks (step times are max-over-ranks, never wall clock)."""
     import torch.distributed as dist
@@ -144,18 +196,26 @@ def combine_checksums(sums, env0=0):
 
 def gather_checksums(sums, local_ms, world):
     """All-gather every rank's per-env checksums and its local ms/step (the
-    only data-path collective of the bench: NCCL under torchrun, outside the
-    timed region; BASELINE.json north_star).  Returns (digest over all
-    ranks' envs in global order, [ms/step per rank])."""
+    only collective of the bench: NCCL under torchrun, outside the timed
+    region; BASELINE.json north_star).  Ranks may own different env counts
+    (strong scaling), so the counts are gathered first and the sums padded.
+    Returns (digest over all ranks' envs in global order, [ms/step per rank])."""
     import torch
     import torch.distributed as dist
     ms = torch.tensor([local_ms], dtype=torch.float64, device=sums.device)
     if dist.is_available() and dist.is_initialized() and world > 1:
-        gs = [torch.zeros_like(sums) for _ in range(world)]
+        cnt = torch.tensor([sums.numel()], dtype=torch.int64, device=sums.device)
+        gc = [torch.zeros_like(cnt) for _ in range(world)]
+        dist.all_gather(gc, cnt)
+        counts = [int(c.item()) for c in gc]
+        pad = torch.zeros(max(counts), dtype=sums.dtype, device=sums.device)
+        pad[:sums.numel()] = sums
+        gs = [torch.zeros_like(pad) for _ in range(world)]
         gm = [torch.zeros_like(ms) for _ in range(world)]
-        dist.all_gather(gs, sums)
+        dist.all_gather(gs, pad)
         dist.all_gather(gm, ms)
-        allsums, allms = torch.cat(gs), torch.cat(gm)
+        allsums = torch.cat([g[:c] for g, c in zip(gs, counts)])
+        allms = torch.cat(gm)
     else:
         allsums, allms = sums, ms
     return combine_checksums(allsums.cpu().numpy()), [float(x) for x in allms.cpu()]
@@ -169,6 +229,21 @@ def rays_per_env(sensor):
 
 def channels_for(cfg):
     return ("dist", "seg") if cfg == 4 else ("dist", "seg", "face")
+
+
+def input_checksums(sc, sensor):
+    """Per-env 64-bit digests of the workload INPUTS (instance table,
+    transforms, sensor poses) -- the --selftest stand-in for image checksums."""
+    import hashlib
+    out = []
+    P = sensor["poses"].reshape(sc.n_envs, -1)
+    for e in range(sc.n_envs):
+        i0, i1 = int(sc.env_off[e]), int(sc.env_off[e + 1])
+        h = hashlib.sha256()
+        for a in (sc.inst_asset[i0:i1], sc.inst_label[i0:i1], sc.inst_T[i0:i1], P[e]):
+            h.update(np.ascontiguousarray(a).tobytes())
+        out.append(np.frombuffer(h.digest()[:8], np.int64)[0])
+    return np.asarray(out, np.int64)
 
 
 # --------------------------------------------------------------------------
@@ -205,7 +280,7 @@ class ClockSampler:
                         self.reasons.add(name)
             except Exception:
                 pass
-            time.sleep(0.05)
+            time.sleep(0.02)
 
     def __enter__(self):
         if self.nv:
@@ -227,64 +302,187 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------------------
-# CPU oracle (reported baseline; never the target)
+# CPU oracle (reported baseline and parity spot check; never the target)
 # --------------------------------------------------------------------------
-def oracle_rate(sc, sensor, kind, n_rays, seed):
+def _oracle_imports():
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     import oracle
-    from helpers import oracle_rays
-    total = sc.n_envs * rays_per_env(sensor)
-    q = np.random.default_rng(seed).choice(total, min(n_rays, total), replace=False)
+    import helpers
+    return oracle, helpers
+
+
+def oracle_sample(sc, sensor, kind, q, n_threads=0):
+    """The oracle on ray ids q; returns (result, wall seconds)."""
+    oracle, helpers = _oracle_imports()
     t0 = time.perf_counter()
-    r = oracle.cast(sc, oracle_rays(sensor, kind), query=q)
-    dt = time.perf_counter() - t0
-    return len(q) / dt, r.tests / dt, dt, len(q)
+    r = oracle.cast(sc, helpers.oracle_rays(sensor, kind), query=q, n_threads=n_threads)
+    return r, time.perf_counter() - t0
 
 
 def cpu_cores():
     return os.cpu_count() or 1
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return platform.processor() or "unknown"
+
+
 def run_reference(args):
+    """The reference arm = the oracle as it stands, on this box's host cores,
+    one bounded sample of the workload per step (rank 0 only)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     cfg = args.config
-    E = envs_per_gpu(args)
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    E = total_envs(args, world)
     sc, sensor = make_workload(cfg, E, 0)
     kind = "range" if cfg == 4 else "depth"
     per_step = {3: 2500, 4: 20000, 5: 20000, 6: 2000}[cfg]
+    total = sc.n_envs * rays_per_env(sensor)
     for w in range(args.warmup):
-        oracle_rate(sc, sensor, kind, per_step // 4, 100 + w)
+        q = np.random.default_rng(100 + w).choice(total, per_step // 4, replace=False)
+        oracle_sample(sc, sensor, kind, q)
     times, rays = [], 0
     for k in range(args.steps):
-        _, _, dt, n = oracle_rate(sc, sensor, kind, per_step, 1000 + k)
+        q = np.random.default_rng(1000 + k).choice(total, per_step, replace=False)
+        _, dt = oracle_sample(sc, sensor, kind, q)
         times.append(dt)
-        rays += n
+        rays += len(q)
     tot = sum(times)
     value = rays / tot
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "rays/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1000 * tot / args.steps, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": 1000 * tot / args.steps, "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOADS[cfg], "envs_per_gpu": E,
+        "config": {"workload": WORKLOADS[cfg], "envs_total": E,
                    "rays_per_step": per_step, "sample": "uniform random rays of the workload"},
         "cpu_baseline": {"value": value, "unit": "rays/s", "cores": cpu_cores(), "kind": "oracle",
+                         "cpu_model": cpu_model(),
                          "sample": f"{per_step} random rays per step of the {E}-env workload"},
         "e2e": {"value": value, "unit": "rays/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line))
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------------
+# --selftest: the multi-rank plumbing on CPU (gloo), no CUDA
+# --------------------------------------------------------------------------
+def run_selftest(args):
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        dist.init_process_group("gloo")
+    E = total_envs(args, world)
+    if args.scaling == "weak":
+        e0, n = env_base(rank, E // world), E // world
+    else:
+        e0, n = shard(E, rank, world)
+    sc, sensor = make_workload(args.config, n, e0)
+    sums = torch.from_numpy(input_checksums(sc, sensor))
+    t = time.perf_counter()
+    digest, rank_ms = gather_checksums(sums, 1000.0 * (rank + 1), world)
+    tmax = reduce_max(torch.tensor([float(rank + 1)], dtype=torch.float64), world)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps({"selftest": True, "n_gpus": world, "envs_total": E, "scaling": args.scaling,
+                          "shards": [list(shard(E, r, world)) for r in range(world)]
+                          if args.scaling == "strong" else None,
+                          "digest": digest, "rank_ms_per_step": rank_ms,
+                          "max_over_ranks": float(tmax[0]), "wall_s": time.perf_counter() - t}),
+              flush=True)
     return 0
 
 
 # --------------------------------------------------------------------------
 # our arm
 # --------------------------------------------------------------------------
+class Workload:
+    """One rank's scene, inputs and per-step update, resident on its GPU."""
+
+    def __init__(self, args, cfg, n_envs, e0, dev, agr, torch):
+        self.cfg = cfg
+        self.sc, self.sensor = make_workload(cfg, n_envs, e0)
+        sc, sensor = self.sc, self.sensor
+        self.E = n_envs
+        self.kind = agr.AGR_RANGE if cfg == 4 else agr.AGR_DEPTH
+        self.chans = channels_for(cfg)
+        self.trbvh_rounds = args.trbvh_rounds if args.trbvh_rounds is not None else (0 if cfg == 6 else 3)
+        self.scene = agr.Scene.from_scenegen(sc, device=dev.index, trbvh_rounds=self.trbvh_rounds)
+        self.traversal = args.traversal or ("lane" if cfg == 6 else "auto")
+        self.scene.set_traversal(0 if self.traversal == "auto" else 1)
+        self.tlas_builder = args.tlas_builder or ("lbvh" if cfg in (5, 6) else "sah")
+        self.scene.set_tlas_builder(1 if self.tlas_builder == "sah" else 0)
+        self.step_refit = (args.tlas_step or ("build" if cfg in (5, 6) else "refit")) == "refit"
+        self.rpe = rays_per_env(sensor)
+        # inputs resident in HBM before timing
+        if cfg == 5:
+            ring = torch.from_numpy(sc.extra["ring_T"]).to(dev)
+            self.T_steps = [ring[k] for k in range(ring.shape[0])]
+        else:
+            self.T_steps = [torch.from_numpy(sc.inst_T).to(dev)]
+        self.V_steps = None
+        if cfg == 6:
+            ringv = torch.from_numpy(sc.extra["ring_V"]).to(dev)
+            self.V_steps = [ringv[k] for k in range(ringv.shape[0])]
+            self.all_assets = list(range(len(sc.meshes)))
+        self.poses = torch.from_numpy(sensor["poses"]).to(dev)
+        self.beams = torch.from_numpy(sensor["beams"]).to(dev) if sensor["kind"] == "beams" else None
+        self.scene.set_instance_transforms(self.T_steps[0])
+        self.scene.build()
+        self.shape = (n_envs, self.poses.shape[1]) + (
+            (sensor["cam"]["H"], sensor["cam"]["W"]) if self.beams is None else tuple(self.beams.shape[:2]))
+        self.out = {c: torch.empty(self.shape, dtype=torch.float32 if c == "dist" else torch.int32, device=dev)
+                    for c in self.chans}
+
+    def update(self, k, stream):
+        """The per-step scene update: new poses (or, for c6, new meshes) and
+        the TLAS refit / rebuild."""
+        if self.V_steps is not None:
+            self.scene.update_meshes(self.all_assets, self.V_steps[k % len(self.V_steps)], stream)
+        else:
+            self.scene.set_instance_transforms(self.T_steps[k % len(self.T_steps)], stream)
+        if self.step_refit:
+            self.scene.refit(stream)
+        else:
+            self.scene.build(stream)
+
+    def cast(self, stream):
+        s = self.sensor
+        if self.beams is None:
+            self.scene.cast_pinhole(s["cam"], self.poses, s["max_range"], self.kind, out=self.out, stream=stream)
+        else:
+            self.scene.cast_beams(self.beams, self.poses, s["max_range"], out=self.out, stream=stream)
+
+    def step(self, k, stream):
+        self.update(k, stream)
+        self.cast(stream)
+
+    def checksums(self, stream):
+        return self.scene.checksum(self.out, self.rpe, stream)
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return spawn_ranks(args.gpus, sys.argv[1:])
+    if args.selftest:
+        return run_selftest(args)
     import torch
     import torch.distributed as dist
     import paper_2503_01471_b200 as agr
@@ -292,7 +490,8 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE={world}"
+    if world != args.gpus:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}; using WORLD_SIZE", file=sys.stderr)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     # one process per GPU under torchrun (also for a 1-process torchrun, so
@@ -302,64 +501,22 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
 
     cfg = args.config
-    E = envs_per_gpu(args)
-    sc, sensor = make_workload(cfg, E, env_base(rank, E))  # this rank's block of global envs
-    kind = agr.AGR_RANGE if cfg == 4 else agr.AGR_DEPTH
-    chans = channels_for(cfg)
-    trbvh_rounds = args.trbvh_rounds if args.trbvh_rounds is not None else (0 if cfg == 6 else 3)
-    scene = agr.Scene.from_scenegen(sc, device=local, trbvh_rounds=trbvh_rounds)
-    traversal = args.traversal or ("lane" if cfg == 6 else "auto")
-    scene.set_traversal(0 if traversal == "auto" else 1)
-    tlas_builder = args.tlas_builder or ("lbvh" if cfg in (5, 6) else "sah")
-    scene.set_tlas_builder(1 if tlas_builder == "sah" else 0)
-    step_refit = (args.tlas_step or ("build" if cfg in (5, 6) else "refit")) == "refit"
-    rpe = rays_per_env(sensor)
-    rays_per_step = E * rpe
-    # inputs resident in HBM before timing
-    if cfg == 5:
-        ring = torch.from_numpy(sc.extra["ring_T"]).to(dev)
-        T_steps = [ring[k] for k in range(ring.shape[0])]
+    E_total = total_envs(args, world)
+    if args.scaling == "weak":
+        e0, E = env_base(rank, E_total // world), E_total // world
     else:
-        T_steps = [torch.from_numpy(sc.inst_T).to(dev)]
-    V_steps = None
-    if cfg == 6:
-        ringv = torch.from_numpy(sc.extra["ring_V"]).to(dev)
-        V_steps = [ringv[k] for k in range(ringv.shape[0])]
-        all_assets = list(range(len(sc.meshes)))
-    poses = torch.from_numpy(sensor["poses"]).to(dev)
-    beams = torch.from_numpy(sensor["beams"]).to(dev) if sensor["kind"] == "beams" else None
-    scene.set_instance_transforms(T_steps[0])
-    scene.build()
-    shape = (E, poses.shape[1]) + ((sensor["cam"]["H"], sensor["cam"]["W"]) if beams is None
-                                   else tuple(beams.shape[:2]))
-    out = {c: torch.empty(shape, dtype=torch.float32 if c == "dist" else torch.int32, device=dev)
-           for c in chans}
+        e0, E = shard(E_total, rank, world)
+    wl = Workload(args, cfg, E, e0, dev, agr, torch)
+    scene, sensor = wl.scene, wl.sensor
+    rays_per_step = E * wl.rpe
+    rays_total = E_total * wl.rpe
     stream = torch.cuda.current_stream(dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
-    def update(k):
-        """The per-step scene update: new poses (or, for c6, new meshes) and
-        the TLAS refit / rebuild."""
-        if V_steps is not None:
-            scene.update_meshes(all_assets, V_steps[k % len(V_steps)], stream)
-        else:
-            scene.set_instance_transforms(T_steps[k % len(T_steps)], stream)
-        if step_refit:
-            scene.refit(stream)
-        else:
-            scene.build(stream)
-
-    def step(k):
-        update(k)
-        if beams is None:
-            scene.cast_pinhole(sensor["cam"], poses, sensor["max_range"], kind, out=out, stream=stream)
-        else:
-            scene.cast_beams(beams, poses, sensor["max_range"], out=out, stream=stream)
-
     # k_instances + k_tlas + k_cast (+ the batched BLAS rebuild for c6)
-    LAUNCHES_PER_STEP = 3 + (blas_launches(len(sc.meshes), trbvh_rounds) if cfg == 6 else 0)
+    LAUNCHES_PER_STEP = 3 + (blas_launches(len(wl.sc.meshes), wl.trbvh_rounds) if cfg == 6 else 0)
     for w in range(args.warmup):
-        step(w)
+        wl.step(w, stream)
     torch.cuda.synchronize()
 
     # ---- timed region: K steps, L2 flushed (untimed) between steps -------
@@ -371,15 +528,12 @@ def main():
     with ClockSampler(local) as clk:
         for k in range(args.steps):
             flush.zero_()
-            e0, e1, e2 = ev[k]
-            e0.record(stream)
-            update(k)
-            e1.record(stream)
-            if beams is None:
-                scene.cast_pinhole(sensor["cam"], poses, sensor["max_range"], kind, out=out, stream=stream)
-            else:
-                scene.cast_beams(beams, poses, sensor["max_range"], out=out, stream=stream)
-            e2.record(stream)
+            e0_, e1_, e2_ = ev[k]
+            e0_.record(stream)
+            wl.update(k, stream)
+            e1_.record(stream)
+            wl.cast(stream)
+            e2_.record(stream)
         torch.cuda.synchronize()
     step_ms = [a.elapsed_time(c) for a, b, c in ev]
     cast_ms = [b.elapsed_time(c) for a, b, c in ev]
@@ -387,50 +541,48 @@ def main():
     cast_total = sum(cast_ms)
     # per-env checksums of the last step's images and every rank's own
     # ms/step, all-gathered (untimed)
-    digest, rank_ms = gather_checksums(scene.checksum(out, rays_per_env(sensor), stream),
-                                       total_ms / args.steps, world)
+    digest, rank_ms = gather_checksums(wl.checksums(stream), total_ms / args.steps, world)
     t = reduce_max(torch.tensor([total_ms, cast_total], dtype=torch.float64, device=dev), world)
     if distributed:
         dist.barrier()
     total_ms, cast_total = float(t[0]), float(t[1])
     ms_per_step = total_ms / args.steps
-    value = rays_per_step * world / (total_ms / 1e3 / args.steps)
+    value = rays_total / (total_ms / 1e3 / args.steps)
 
     # ---- per-ray work counters (separate, untimed counting launch) --------
     counters = lane_counters = None
     if not args.no_counters:
         scene.enable_counters(True)
-        step(0)
+        wl.step(0, stream)
         torch.cuda.synchronize()
         counters = scene.counters()
         scene.set_traversal(1)  # each ray's own units (algorithmic work)
-        step(0)
+        wl.step(0, stream)
         torch.cuda.synchronize()
         lane_counters = scene.counters()
-        scene.set_traversal(0 if traversal == "auto" else 1)
+        scene.set_traversal(0 if wl.traversal == "auto" else 1)
         scene.enable_counters(False)
 
     # ---- end to end through the public C ABI with host buffers ------------
     e2e = None
     if not args.no_e2e:
         poses_h = torch.from_numpy(sensor["poses"]).pin_memory()
-        out_h = {c: torch.empty(shape, dtype=torch.float32 if c == "dist" else torch.int32,
-                                pin_memory=True) for c in chans}
-        beams_h = torch.from_numpy(sensor["beams"]).pin_memory() if beams is not None else None
-
-        V_h = [v.cpu().pin_memory() for v in V_steps] if V_steps is not None else None
-        V_d = torch.empty_like(V_steps[0]) if V_steps is not None else None
+        out_h = {c: torch.empty(wl.shape, dtype=torch.float32 if c == "dist" else torch.int32,
+                                pin_memory=True) for c in wl.chans}
+        beams_h = torch.from_numpy(sensor["beams"]).pin_memory() if wl.beams is not None else None
+        V_h = [v.cpu().pin_memory() for v in wl.V_steps] if wl.V_steps is not None else None
+        V_d = torch.empty_like(wl.V_steps[0]) if wl.V_steps is not None else None
 
         def e2e_step(k):
             if V_h is not None:  # c6: the step's new meshes come from the host
                 V_d.copy_(V_h[k % len(V_h)], non_blocking=True)
-                scene.update_meshes(all_assets, V_d, stream)
-                scene.refit(stream) if step_refit else scene.build(stream)
+                scene.update_meshes(wl.all_assets, V_d, stream)
+                scene.refit(stream) if wl.step_refit else scene.build(stream)
             else:
-                update(k)
-            stream.synchronize()
+                wl.update(k, stream)
+            # no sync: the host casts wait for the queued scene work themselves
             if beams_h is None:
-                scene.cast_pinhole_host(sensor["cam"], poses_h, sensor["max_range"], kind, out=out_h)
+                scene.cast_pinhole_host(sensor["cam"], poses_h, sensor["max_range"], wl.kind, out=out_h)
             else:
                 scene.cast_beams_host(beams_h, poses_h, sensor["max_range"], out=out_h)
 
@@ -448,11 +600,23 @@ def main():
         h2d = poses_h.numel() * 4 + (beams_h.numel() * 4 if beams_h is not None else 0) + \
             (V_h[0].numel() * 4 if V_h is not None else 0)
         d2h = sum(v.numel() * 4 for v in out_h.values())
-        e2e = {"value": rays_per_step * world * n_e2e / dt, "unit": "rays/s",
-               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": n_e2e,
+        e2e = {"value": rays_total * n_e2e / dt, "unit": "rays/s",
+               "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world, "steps": n_e2e,
                "note": "agr_cast_*_host: H2D poses, chunked cast, D2H of every output image"}
 
+    # ---- rank 0 re-casts every global env alone: 1-GPU digest == N-GPU digest
+    verify = None
+    if world > 1 and not args.no_verify and rank == 0:
+        full = Workload(args, cfg, E_total, 0, dev, agr, torch)
+        full.update(args.steps - 1, stream)  # the last timed step's scene
+        full.cast(stream)
+        torch.cuda.synchronize()
+        d1 = combine_checksums(full.checksums(stream).cpu().numpy())
+        verify = {"one_gpu_digest": d1, "equal": d1 == digest}
+        del full
+        torch.cuda.empty_cache()
     if distributed:
+        dist.barrier()
         dist.destroy_process_group()
     if rank != 0:
         return 0
@@ -460,7 +624,7 @@ def main():
     # ---- roofline of the dominant kernel (k_cast) -------------------------
     peaks = json.load(open(PEAKS_PATH)) if os.path.exists(PEAKS_PATH) else {}
     clocks = clk.summary()
-    cast_s = cast_total / 1e3 / args.steps  # per launch (per rank)
+    cast_s = cast_total / 1e3 / args.steps  # per launch (max over ranks)
     roof = None
     if lane_counters and lane_counters["rays"] > 0:
         per = {k: lane_counters[k] / lane_counters["rays"] for k in ("nodes", "leaves", "instances")}
@@ -478,48 +642,76 @@ def main():
                 "kernel": "k_cast", "kernel_ms": 1e3 * cast_s,
                 "work_per_ray_inst": w_ray, "per_ray": per,
                 "peak_note": "148 SMs x 128 FP32/INT lanes x measured median SM clock "
-                             "(DESIGN.md §8); algorithmic instr = counted units x unit costs"}
-        out_bytes = rays_per_step * 4 * len(chans)
+                             "(DESIGN.md §8; FMA-loop check in profiles/fma_peak.json); "
+                             "algorithmic instr = counted units x unit costs"}
+        out_bytes = rays_per_step * 4 * len(wl.chans)
         hbm_peak = peaks.get("hbm_gbs", 6553.3)
         roof["hbm"] = {"achieved_gbs": out_bytes / cast_s / 1e9, "peak_gbs": hbm_peak,
                        "frac": out_bytes / cast_s / 1e9 / hbm_peak,
                        "bytes_per_launch": out_bytes, "peak_note": "of measured (MEASURED_PEAKS.json)"}
 
-    cpu = None
+    # ---- CPU oracle: baseline rate + parity spot check of step 0's images --
+    cpu = parity = None
     if not args.no_cpu_baseline:
         kind_s = "range" if cfg == 4 else "depth"
+        wl.step(0, stream)
+        torch.cuda.synchronize()
+        got = {c: v.cpu().numpy().reshape(-1) for c, v in wl.out.items()}
+        total = wl.E * wl.rpe
         n_cpu = {3: 40000, 4: 200000, 5: 200000, 6: 20000}[cfg]
-        rate, tests_rate, dt, n = oracle_rate(sc, sensor, kind_s, n_cpu, 7)
+        q = np.random.default_rng(7).choice(total, min(n_cpu, total), replace=False)
+        # after update(0) the scene is the generated one: c5 poses ring set 0
+        # (= sc.inst_T), c6 meshes ring set 0 (= sc.meshes), c3/c4 never change
+        osc = wl.sc
+        ref, dt = oracle_sample(osc, sensor, kind_s, q)
+        rate = len(q) / dt
+        q1 = q[: max(1, len(q) // 32)]
+        _, dt1 = oracle_sample(osc, sensor, kind_s, q1, n_threads=1)
+        rate1 = len(q1) / dt1
         cpu = {"value": rate, "unit": "rays/s", "cores": cpu_cores(), "kind": "oracle",
-               "sample": f"{n} uniform random rays of this rank's {E}-env workload ({dt:.1f} s wall)",
-               "tri_tests_per_s": tests_rate}
+               "cpu_model": cpu_model(),
+               "sample": f"{len(q)} uniform random rays of rank 0's {wl.E}-env workload ({dt:.1f} s wall)",
+               "tri_tests_per_s": ref.tests / dt,
+               "one_core": {"value": rate1, "unit": "rays/s", "sample": f"{len(q1)} of those rays"},
+               "full_frame_s": rays_total / rate,
+               "full_frame_note": "extrapolated: one step of the whole workload at the all-core rate"}
+        _, helpers = _oracle_imports()
+        try:
+            res = helpers.compare(ref, got["dist"][q], got["seg"][q], got["face"][q] if "face" in got else None,
+                                  f"bench c{cfg} parity sample")
+            parity = {"n": res["n"], "mismatch": 0, "ambiguous": res["ambiguous"], "ties": res["ties"],
+                      "grazes": res["grazes"], "max_dist_err_m": res["max_err"],
+                      "images": "step 0 (update + cast) after the timed loop"}
+        except AssertionError as e:  # reported, never hidden
+            parity = {"n": len(q), "failed": str(e)[:1000]}
 
     line = {
         "metric": METRIC, "value": value, "unit": "rays/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32+f64",
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f32+f64",
         "data": "synthetic",
-        "config": {"workload": WORKLOADS[cfg], "envs_per_gpu": E, "rays_per_step_per_gpu": rays_per_step,
-                   "channels": list(chans), "parallelism": f"env-sharded x{world}",
+        "config": {"workload": WORKLOADS[cfg], "envs_total": E_total, "envs_rank0": E,
+                   "rays_per_step": rays_total, "channels": list(wl.chans),
+                   "parallelism": f"env-sharded x{world} ({args.scaling} scaling)",
                    "l2": "flushed between timed steps (256 MB write, untimed)",
-                   "trbvh_rounds": trbvh_rounds, "traversal": traversal,
+                   "trbvh_rounds": wl.trbvh_rounds, "traversal": wl.traversal,
                    "step": ("update_meshes (every env's BLAS rebuilt)" if cfg == 6 else
-                            "set_instance_transforms") + " + TLAS " + ("refit" if step_refit else "rebuild") +
-                           " + cast (TLAS builder: " + tlas_builder + ")"},
+                            "set_instance_transforms") + " + TLAS " + ("refit" if wl.step_refit else "rebuild") +
+                           " + cast (TLAS builder: " + wl.tlas_builder + ")"},
         "update_ms_per_step": (total_ms - cast_total) / args.steps,
-        "checksum": {"digest": digest, "envs": E * world, "last_step": args.steps - 1,
-                     "rank_ms_per_step": rank_ms},
-        "env_frames_per_sec": E * poses.shape[1] * world / (ms_per_step / 1e3),
+        "checksum": {"digest": digest, "envs": E_total, "last_step": args.steps - 1,
+                     "rank_ms_per_step": rank_ms, "verify": verify},
+        "env_frames_per_sec": E_total * wl.poses.shape[1] / (ms_per_step / 1e3),
         "cast_ms_per_step": cast_total / args.steps,
-        "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+        "roofline": roof, "cpu_baseline": cpu, "parity_sample": parity, "e2e": e2e,
         "gpu_launches": LAUNCHES_PER_STEP * args.steps, "clocks": clocks,
         "counters_per_ray": ({k: v / counters["rays"] for k, v in counters.items() if k != "rays"}
                              if counters else None),
         "counters_per_ray_own": ({k: v / lane_counters["rays"] for k, v in lane_counters.items()
                                   if k != "rays"} if lane_counters else None),
     }
-    print(json.dumps(line))
-    return 0
+    print(json.dumps(line), flush=True)
+    return 0 if (verify is None or verify["equal"]) else 3
 
 
 if __name__ == "__main__":

@@ -71,7 +71,15 @@ enum {
 
 /* Documented limits. */
 #define AGR_MAX_INSTANCES_PER_ENV 1024 /* per-env TLAS is built in one CTA   */
-#define AGR_MAX_BVH_DEPTH 60           /* BLAS depth + TLAS depth + 1        */
+#define AGR_MAX_BVH_DEPTH 94           /* binary BLAS depth accepted at create
+                                          (the traversal stack holds 96
+                                          entries).  A mesh update that makes a
+                                          BLAS deeper is still correct: a ray
+                                          whose stack would overflow is
+                                          re-solved by an FP64 test of every
+                                          triangle of its env (counter [5];
+                                          agr_scene_get_info reports the new
+                                          blas_max_depth).                  */
 
 typedef struct agr_scene_s* agr_scene;
 
@@ -277,7 +285,12 @@ agr_status agr_cast_rays(agr_scene scene, const float* orig, const float* dir, i
  * (pageable or pinned host memory) to the device, casts, and copies the
  * images back into the host pointers of `out_host`, pipelining the
  * device->host copies with the casts of later env chunks on internal
- * streams.  Synchronous: returns when out_host is filled.
+ * streams.  The internal streams first wait (cudaStreamWaitEvent, no host
+ * sync) for the scene work of the last agr_set_instance_transforms /
+ * agr_update_mesh(es) / agr_set_vertex_annotations / agr_build / agr_refit
+ * on whatever stream it was queued, so no caller-side sync is needed
+ * between those calls and this one.  Synchronous: returns when out_host
+ * is filled.  EINVAL on bad intrinsics or an invalid `kind`.
  */
 agr_status agr_cast_pinhole_host(agr_scene scene, const agr_pinhole* cam, agr_distance kind,
                                  const float* poses_host, int32_t n_sensors, float max_range,

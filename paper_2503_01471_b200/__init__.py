@@ -350,7 +350,7 @@ class Scene:
         _check(load().agr_set_stereo(self.handle, *(float(x) for x in offset), float(eps)))
 
     def set_tlas_builder(self, builder: int):
-        """1 binned SAH (default), 0 LBVH (Morton + Karras) for agr_build."""
+        """0 LBVH (Morton + Karras; the default), 1 binned SAH for agr_build."""
         _check(load().agr_set_tlas_builder(self.handle, int(builder)))
 
     def set_traversal(self, mode: int):

@@ -5,6 +5,8 @@
 #include "../../include/agr.h"
 #include "agr_internal.cuh"
 
+#include <nvtx3/nvToolsExt.h>
+
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -51,6 +53,13 @@ struct DeviceGuard {
     ~DeviceGuard() {
         if (prev >= 0) cudaSetDevice(prev);
     }
+};
+
+// NVTX range over one ABI call (visible in nsys / ncu --nvtx timelines;
+// header-only NVTX3, a no-op without a tool attached).
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
 };
 
 }  // namespace
@@ -107,6 +116,10 @@ struct agr_scene_s {
     int tlas_builder = 0;  // 0 LBVH (default), 1 binned SAH
     bool counting = false;
     // end-to-end staging (lazily allocated)
+    // recorded on the caller's stream after every call that changes scene
+    // data (transforms, meshes, annotations, build, refit): the host-buffer
+    // casts run on internal streams and wait on it first
+    cudaEvent_t ready = nullptr;
     cudaStream_t e2e_stream[2] = {nullptr, nullptr};
     cudaEvent_t e2e_event[4] = {nullptr, nullptr, nullptr, nullptr};
     float* e2e_poses = nullptr;
@@ -179,6 +192,7 @@ struct agr_scene_s {
             if (s) cudaStreamDestroy(s);
         for (auto& e : e2e_event)
             if (e) cudaEventDestroy(e);
+        if (ready) cudaEventDestroy(ready);
         for (auto& h : e2e_host)
             if (h) cudaFreeHost(h);
         if (e2e_poses) cudaFree(e2e_poses);
@@ -224,6 +238,12 @@ static agr_status refresh_assets(agr_scene_s* s) {
     return AGR_OK;
 }
 
+// Marks the end of the scene-changing work just queued on `st` (see `ready`).
+static agr_status mark_ready(agr_scene_s* s, cudaStream_t st) {
+    CK(cudaEventRecord(s->ready, st));
+    return AGR_OK;
+}
+
 extern "C" {
 
 int32_t agr_abi_version(void) { return AGR_ABI_VERSION; }
@@ -238,6 +258,7 @@ agr_status agr_scene_create(int32_t device, const agr_mesh* meshes, int32_t n_me
 agr_status agr_scene_create_ex(int32_t device, const agr_mesh* meshes, int32_t n_meshes, int32_t n_envs,
                                const int64_t* env_offsets, const agr_instance* inst,
                                const agr_create_options* opts, agr_scene* out) {
+    NvtxRange nvtx_range("agr_scene_create_ex");
     g_err.clear();
     if (!out) return fail(AGR_EINVAL, "out is NULL");
     *out = nullptr;
@@ -426,8 +447,11 @@ agr_status agr_scene_create_ex(int32_t device, const agr_mesh* meshes, int32_t n
     if (err == cudaSuccess) err = cudaStreamSynchronize(st);
     cudaStreamDestroy(st);
     if (err != cudaSuccess) return bail(cuda_fail(err, "instances_update"));
-    if (max_depth + 2 > STACK_SIZE)
-        return bail(fail(AGR_EUNSUPPORTED, "BLAS depth %d exceeds the traversal stack", max_depth));
+    if (max_depth > AGR_MAX_BVH_DEPTH)
+        return bail(fail(AGR_EUNSUPPORTED, "BLAS depth %d exceeds AGR_MAX_BVH_DEPTH (%d)", max_depth,
+                         AGR_MAX_BVH_DEPTH));
+    CKB(cudaEventCreateWithFlags(&s->ready, cudaEventDisableTiming));
+    CKB(cudaEventRecord(s->ready, 0));
 #undef CKB
     *out = s;
     return AGR_OK;
@@ -474,6 +498,7 @@ agr_status agr_scene_get_info(agr_scene s, agr_scene_info* info) {
 }
 
 agr_status agr_set_instance_transforms(agr_scene s, const float* T, void* stream) {
+    NvtxRange nvtx_range("agr_set_instance_transforms");
     g_err.clear();
     if (!s) return fail(AGR_EINVAL, "scene is NULL");
     if (s->n_inst == 0) return AGR_OK;
@@ -483,7 +508,7 @@ agr_status agr_set_instance_transforms(agr_scene s, const float* T, void* stream
     CK(cudaMemcpyAsync(s->inst_T, T, sizeof(float) * 12 * s->n_inst, cudaMemcpyDeviceToDevice, st));
     CK(instances_update(s->tlas_args(), (int)s->n_inst, st));
     s->dirty = true;
-    return AGR_OK;
+    return mark_ready(s, st);
 }
 
 agr_status agr_update_mesh(agr_scene s, int32_t asset, const float* verts, int32_t n_verts, void* stream) {
@@ -496,6 +521,7 @@ agr_status agr_update_mesh(agr_scene s, int32_t asset, const float* verts, int32
 }
 
 agr_status agr_update_meshes(agr_scene s, int32_t n, const int32_t* assets, const float* verts, void* stream) {
+    NvtxRange nvtx_range("agr_update_meshes");
     g_err.clear();
     if (!s) return fail(AGR_EINVAL, "scene is NULL");
     if (n == 0) return AGR_OK;
@@ -520,7 +546,7 @@ agr_status agr_update_meshes(agr_scene s, int32_t n, const int32_t* assets, cons
     CK(instances_update(s->tlas_args(), (int)s->n_inst, st));  // instance boxes from the new BLAS
     s->assets_stale = true;
     s->dirty = true;
-    return AGR_OK;
+    return mark_ready(s, st);
 }
 
 agr_status agr_set_vertex_annotations(agr_scene s, int32_t asset, const float* values, int32_t n_verts,
@@ -543,27 +569,29 @@ agr_status agr_set_vertex_annotations(agr_scene s, int32_t asset, const float* v
     }
     CK(cudaMemcpyAsync(s->annot + (size_t)k * s->h_mvert_off[asset], values, sizeof(float) * k * (size_t)n_verts,
                        cudaMemcpyDeviceToDevice, st));
-    return AGR_OK;
+    return mark_ready(s, st);
 }
 
 agr_status agr_build(agr_scene s, void* stream) {
+    NvtxRange nvtx_range("agr_build");
     g_err.clear();
     if (!s) return fail(AGR_EINVAL, "scene is NULL");
     DeviceGuard guard(s->device);
     CK(tlas_build(s->tlas_args(), true, (cudaStream_t)stream));
     s->built = true;
     s->dirty = false;
-    return AGR_OK;
+    return mark_ready(s, (cudaStream_t)stream);
 }
 
 agr_status agr_refit(agr_scene s, void* stream) {
+    NvtxRange nvtx_range("agr_refit");
     g_err.clear();
     if (!s) return fail(AGR_EINVAL, "scene is NULL");
     if (!s->built) return fail(AGR_ESTATE, "agr_refit before the first agr_build");
     DeviceGuard guard(s->device);
     CK(tlas_build(s->tlas_args(), false, (cudaStream_t)stream));
     s->dirty = false;
-    return AGR_OK;
+    return mark_ready(s, (cudaStream_t)stream);
 }
 
 static agr_status check_cast_state(agr_scene s, float max_range, const agr_outputs& out) {
@@ -610,6 +638,7 @@ static CastArgs base_args(agr_scene s, float max_range, agr_outputs out) {
 
 agr_status agr_cast_pinhole(agr_scene s, const agr_pinhole* cam, agr_distance kind, const float* poses,
                             int32_t n_sensors, float max_range, agr_outputs out, void* stream) {
+    NvtxRange nvtx_range("agr_cast_pinhole");
     g_err.clear();
     agr_status st = check_cast_state(s, max_range, out);
     if (st != AGR_OK) return st;
@@ -636,6 +665,7 @@ agr_status agr_cast_pinhole(agr_scene s, const agr_pinhole* cam, agr_distance ki
 
 agr_status agr_cast_beams(agr_scene s, const float* dirs, int32_t C, int32_t K, const float* poses,
                           int32_t n_sensors, float max_range, agr_outputs out, void* stream) {
+    NvtxRange nvtx_range("agr_cast_beams");
     g_err.clear();
     agr_status st = check_cast_state(s, max_range, out);
     if (st != AGR_OK) return st;
@@ -654,6 +684,7 @@ agr_status agr_cast_beams(agr_scene s, const float* dirs, int32_t C, int32_t K, 
 
 agr_status agr_cast_rays(agr_scene s, const float* orig, const float* dir, int32_t R, float max_range,
                          agr_outputs out, void* stream) {
+    NvtxRange nvtx_range("agr_cast_rays");
     g_err.clear();
     agr_status st = check_cast_state(s, max_range, out);
     if (st != AGR_OK) return st;
@@ -673,6 +704,9 @@ static agr_status e2e_prepare(agr_scene s, size_t pose_bytes, size_t chunk_out_b
         for (auto& x : s->e2e_stream) CK(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
         for (auto& x : s->e2e_event) CK(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
     }
+    // order the internal streams after the scene work queued on the
+    // caller's stream (agr.h: the host casts need no caller-side sync)
+    CK(cudaStreamWaitEvent(s->e2e_stream[0], s->ready, 0));
     if (pose_bytes > s->e2e_poses_bytes) {
         if (s->e2e_poses) cudaFree(s->e2e_poses);
         s->e2e_poses = nullptr;
@@ -794,12 +828,14 @@ static agr_status e2e_run(agr_scene s, CastArgs& a, int64_t elems_per_env, agr_o
 agr_status agr_cast_pinhole_host(agr_scene s, const agr_pinhole* cam, agr_distance kind,
                                  const float* poses_host, int32_t n_sensors, float max_range,
                                  agr_outputs out_host) {
+    NvtxRange nvtx_range("agr_cast_pinhole_host");
     g_err.clear();
     agr_status st = check_cast_state(s, max_range, out_host);
     if (st != AGR_OK) return st;
     if (!cam || !poses_host || n_sensors < 1) return fail(AGR_EINVAL, "need cam, poses and n_sensors >= 1");
     if (cam->width < 1 || cam->height < 1 || !(cam->fx > 0.0f) || !(cam->fy > 0.0f))
         return fail(AGR_EINVAL, "bad pinhole intrinsics");
+    if (kind != AGR_DEPTH && kind != AGR_RANGE) return fail(AGR_EINVAL, "bad distance kind");
     DeviceGuard guard(s->device);
     st = e2e_prepare(s, sizeof(float) * 12 * (size_t)n_sensors * s->n_envs, 0);
     if (st != AGR_OK) return st;
@@ -824,6 +860,7 @@ agr_status agr_cast_pinhole_host(agr_scene s, const agr_pinhole* cam, agr_distan
 agr_status agr_cast_beams_host(agr_scene s, const float* dirs_host, int32_t C, int32_t K,
                                const float* poses_host, int32_t n_sensors, float max_range,
                                agr_outputs out_host) {
+    NvtxRange nvtx_range("agr_cast_beams_host");
     g_err.clear();
     agr_status st = check_cast_state(s, max_range, out_host);
     if (st != AGR_OK) return st;
@@ -853,6 +890,7 @@ agr_status agr_cast_beams_host(agr_scene s, const float* dirs_host, int32_t C, i
 }
 
 agr_status agr_checksum(agr_scene s, agr_outputs out, int64_t elems_per_env, uint64_t* sums, void* stream) {
+    NvtxRange nvtx_range("agr_checksum");
     g_err.clear();
     if (!s || !sums || elems_per_env < 0) return fail(AGR_EINVAL, "bad argument");
     DeviceGuard guard(s->device);

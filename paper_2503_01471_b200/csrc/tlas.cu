@@ -40,8 +40,11 @@ __global__ void k_instances(TlasArgs a, int n_inst) {
     float* box = a.inst_box + 6 * i;
     bool ok = det != 0.0 && isfinite(det) && as.n_leaves > 0;
     if (!ok) {
-        // singular transform or an all-degenerate asset: the instance is never hit
-        for (int k = 0; k < 6; ++k) box[k] = inf_f();
+        // singular transform or an all-degenerate asset: the instance is never
+        // hit.  Its box is the empty box (lo = +inf, hi = -inf), the identity
+        // of the fit's union, so its TLAS ancestors keep their tight boxes;
+        // BVH4 child slots turn it into the never-hit sentinel (slot_box)
+        for (int k = 0; k < 3; ++k) { box[k] = inf_f(); box[3 + k] = -inf_f(); }
         for (int k = 0; k < 4; ++k) rec[k] = make_float4(0.f, 0.f, 0.f, 0.f);
         return;
     }
@@ -114,6 +117,14 @@ __global__ void k_instances(TlasArgs a, int n_inst) {
         box[r] = __double2float_rd(lo - pad);
         box[3 + r] = __double2float_ru(hi + pad);
     }
+}
+
+// BVH4 child-slot box of a fitted box: an empty box (lo > hi, an instance
+// that is never hit or a subtree of them) becomes the +inf sentinel, which
+// every slab test misses (an inverted box would pass the min/max slab test).
+__device__ __forceinline__ void slot_box(const float* src, float* dst) {
+    const bool empty = !(src[0] <= src[3]);
+    for (int k = 0; k < 6; ++k) dst[k] = empty ? inf_f() : src[k];
 }
 
 // ---- K7/K8: per-env TLAS build / refit -----------------------------------------
@@ -345,7 +356,7 @@ __global__ void k_tlas(TlasArgs a, int rebuild) {
             for (int c = 0; c < 4; ++c)
                 for (int k = 0; k < 6; ++k) b[c][k] = EMPTY[k];
             if (n == 1) {
-                for (int k = 0; k < 6; ++k) b[0][k] = a.inst_box[6 * i0 + k];
+                slot_box(a.inst_box + 6 * i0, b[0]);
                 refs[0] = ~i0;
                 a.tlas_inst_parent[i0] = 0;
             }
@@ -522,7 +533,7 @@ __global__ void k_tlas(TlasArgs a, int rebuild) {
         for (int c = 0; c < 4; ++c) {
             const int r = refs[c];
             const float* src = r == REF_EMPTY ? EMPTY : (r < 0 ? s.box + 6 * ~r : s.ibox + 6 * r);
-            for (int k = 0; k < 6; ++k) b[c][k] = src[k];
+            slot_box(src, b[c]);
             g[c] = r == REF_EMPTY ? REF_EMPTY : (r < 0 ? ~(i0 + ~r) : nodebase + r);
         }
         write_node4(a.nodes, nodebase + j, b, g, cnt);

@@ -389,22 +389,47 @@ def config4(n_envs=4096, env_base=0):
     return sc, dict(beams=lidar_beams(128, 512), poses=poses, max_range=10.0, kind="beams")
 
 
+def _quat_rotations(q):
+    """Rotation matrices [..][3][3] of (unnormalised) quaternions q [..][4]
+    (w, x, y, z), normalised first: uniform random rotations for normal q."""
+    q = q / np.linalg.norm(q, axis=-1, keepdims=True)
+    w, x, y, z = (q[..., i] for i in range(4))
+    R = np.empty(q.shape[:-1] + (3, 3))
+    R[..., 0, 0] = 1 - 2 * (y * y + z * z)
+    R[..., 0, 1] = 2 * (x * y - z * w)
+    R[..., 0, 2] = 2 * (x * z + y * w)
+    R[..., 1, 0] = 2 * (x * y + z * w)
+    R[..., 1, 1] = 1 - 2 * (x * x + z * z)
+    R[..., 1, 2] = 2 * (y * z - x * w)
+    R[..., 2, 0] = 2 * (x * z - y * w)
+    R[..., 2, 1] = 2 * (y * z + x * w)
+    R[..., 2, 2] = 1 - 2 * (x * x + y * y)
+    return R
+
+
 def config5(n_envs=2048, env_base=0, ring=64):
     """c5: Table I-shaped 20 cubes per env at c2's pose
-    distribution, re-sampled every step: a ring of `ring` transform sets
-    (float32 [ring][I][3][4]); step k uses set k % ring.  135x240 camera."""
+    distribution (position U(x in [2,8], y in [-3,3], z in [-1.5,1.5]),
+    uniform rotation, scale U[0.5,1.5]), re-sampled every step: a ring of
+    `ring` transform sets (float32 [ring][I][3][4]); step k uses set k % ring.
+    135x240 camera.  Each env draws its whole ring from its own stream in
+    one batch per quantity (16384 envs in seconds)."""
     meshes = [cube_mesh()]
     n_inst = 20
-    ring_T = np.zeros((ring, n_envs * n_inst, 3, 4), np.float32)
+    ring_T = np.zeros((ring, n_envs, n_inst, 3, 4), np.float32)
     for i, e in enumerate(range(env_base, env_base + n_envs)):
         rng = env_rng(CONFIG_SEED[5], e)
-        for k in range(ring):
-            for j in range(n_inst):
-                _, T = _c2_obstacle(rng, [0])
-                ring_T[k, i * n_inst + j] = T
-    per_env = [[(0, j + 1, ring_T[0, i * n_inst + j]) for j in range(n_inst)] for i in range(n_envs)]
-    sc = assemble(meshes, per_env)
-    sc.env_base = env_base
+        p = rng.uniform([2.0, -3.0, -1.5], [8.0, 3.0, 1.5], (ring, n_inst, 3))
+        R = _quat_rotations(rng.normal(size=(ring, n_inst, 4)))
+        sc_ = rng.uniform(0.5, 1.5, (ring, n_inst))
+        T = np.empty((ring, n_inst, 3, 4))
+        T[..., :3] = R * sc_[..., None, None]
+        T[..., 3] = p
+        ring_T[:, i] = T.astype(np.float32)
+    ring_T = ring_T.reshape(ring, n_envs * n_inst, 3, 4)
+    env_off = np.arange(n_envs + 1, dtype=np.int64) * n_inst
+    labels = np.tile(np.arange(1, n_inst + 1, dtype=np.int32), n_envs)
+    sc = Scene(meshes, env_off, np.zeros(n_envs * n_inst, np.int32), labels, ring_T[0].copy(), env_base)
     sc.extra["ring_T"] = ring_T
     return sc, dict(cam=pinhole(240, 135, 87.0), poses=identity_poses(n_envs),
                     max_range=10.0, kind="pinhole")

@@ -113,3 +113,38 @@ def test_checksum_gather_equals_single_process_digest():
     alt = allsums.copy()
     alt[7] ^= 1
     assert bench.combine_checksums(alt) != digest
+
+
+def test_shard_is_strong_scaling():
+    """GPU g owns [floor(gN/n), floor((g+1)N/n)); the
+    blocks tile [0, N) exactly, also when n does not divide N."""
+    for N, n in ((1024, 8), (1024, 3), (16384, 7), (5, 8)):
+        blocks = [bench.shard(N, g, n) for g in range(n)]
+        assert blocks[0][0] == 0 and sum(c for _, c in blocks) == N
+        for (a, c), (b, _) in zip(blocks, blocks[1:]):
+            assert a + c == b
+    assert [bench.shard(1024, g, 8) for g in range(2)] == [(0, 128), (128, 128)]
+
+
+@pytest.mark.parametrize("world,cfg,scaling", [(2, 5, "strong"), (3, 3, "strong"), (2, 4, "weak")])
+def test_bench_spawn_path_gloo(world, cfg, scaling):
+    """`python bench.py --gpus N` without torchrun re-launches itself as N
+    ranks under torch.distributed.run (bench.spawn_ranks, the driver's launch
+    line); --selftest runs the same sharding + all-gather + digest on CPU
+    (gloo).  The N-rank digest of the per-env input checksums equals the
+    single-process digest of the same global envs."""
+    import json
+    import subprocess
+    import sys
+    E = {5: 40, 3: 7, 4: 6}[cfg]
+    cmd = [sys.executable, os.path.join(os.path.dirname(bench.__file__), "bench.py"), "--gpus", str(world),
+           "--selftest", "--config", str(cfg), "--envs", str(E), "--scaling", scaling]
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=300)
+    assert p.returncode == 0, p.stderr[-2000:]
+    line = json.loads([ln for ln in p.stdout.splitlines() if ln.startswith("{")][-1])
+    total = E if scaling == "strong" else E * world
+    assert line["n_gpus"] == world and line["envs_total"] == total
+    assert line["rank_ms_per_step"] == [1000.0 * (r + 1) for r in range(world)]
+    assert line["max_over_ranks"] == float(world)
+    sc, sensor = bench.make_workload(cfg, total, 0)
+    assert line["digest"] == bench.combine_checksums(bench.input_checksums(sc, sensor))

@@ -341,6 +341,54 @@ def test_c3_full_size_sampled():
     assert certify_all(sc, sensor, "depth", got["dist"], got["seg"], got["face"], "c3") == hit.sum()
 
 
+def _silhouette_pixels(seg_img):
+    """Flat indices of pixels whose segmentation differs from a 4-neighbour
+    (both sides of every outline) in [E][S][H][W] images."""
+    e = np.zeros(seg_img.shape, bool)
+    dx = seg_img[..., :, 1:] != seg_img[..., :, :-1]
+    dy = seg_img[..., 1:, :] != seg_img[..., :-1, :]
+    e[..., :, 1:] |= dx
+    e[..., :, :-1] |= dx
+    e[..., 1:, :] |= dy
+    e[..., :-1, :] |= dy
+    return np.flatnonzero(e)
+
+
+@pytest.mark.slow
+def test_c3_bench_step_exact_equals_filter_and_silhouettes():
+    """Full-size optimality evidence in the launch configuration bench.py
+    times (binned-SAH TLAS built once, then set_instance_transforms + refit,
+    interval-packet traversal): (a) the all-FP64 per-lane traversal (exact
+    mode: every leaf tested in FP64, a different traversal order) equals
+    the FP32-filter packet cast bitwise on all 132.7 M c3 rays -- no ray
+    loses a closer hit to the FP32 filter or the packet culling; (b) 50 000
+    silhouette pixels (a 4-neighbour with another segment: where a culled
+    closer hit would show) against the oracle.  The oracle's inputs are the
+    scene and the ray ids; the GPU image only chooses which rays to ask."""
+    sc, sensor = sg.config3()
+    s = make_scene(sc, build=False)
+    s.set_tlas_builder(1)
+    s.build()
+    s.set_instance_transforms(torch.from_numpy(sc.inst_T).to(dev()))  # the bench step
+    s.refit()
+    a = cast_sensor(s, sensor, "depth")
+    s.set_exact_mode(True)
+    b = cast_sensor(s, sensor, "depth")
+    s.set_exact_mode(False)
+    for k in a:
+        assert torch.equal(a[k], b[k]), k
+    del b
+    seg = a["seg"].cpu().numpy()
+    got = to_np(a)
+    sil = _silhouette_pixels(seg)
+    assert len(sil) > 1_000_000
+    q = np.random.default_rng(33).choice(sil, 50000, replace=False)
+    ref = oracle.cast(sc, oracle_rays(sensor, "depth"), query=q)
+    res = compare(ref, got["dist"][q], got["seg"][q], got["face"][q], "c3 silhouettes")
+    print("c3 silhouettes:", res)
+    s.close()
+
+
 @pytest.mark.slow
 def test_c4_full_size_sampled():
     sc, sensor = sg.config4()
@@ -723,3 +771,62 @@ def test_large_image_sampled():
     ref = oracle.cast(sc, oracle_rays(sensor, "depth"), query=q)
     compare(ref, got["dist"][q], got["seg"][q], got["face"][q], "1080p")
     certify_all(sc, sensor, "depth", got["dist"], got["seg"], got["face"], "1080p")
+
+
+# ---- ordering and degenerate instances ---------------------------------
+
+def test_host_cast_waits_for_scene_work_on_the_caller_stream():
+    """agr_cast_pinhole_host runs on internal streams: it must wait for a
+    refit still queued on the caller's stream (delayed here by a long
+    sleep kernel) without a caller-side sync, and return the images of the
+    new transforms."""
+    sc, sensor = sg.config5(n_envs=16, ring=2)
+    ring = sc.extra["ring_T"]
+    s = make_scene(sc)
+    T1 = torch.from_numpy(ring[1]).to(dev())
+    poses = torch.from_numpy(np.ascontiguousarray(sensor["poses"])).pin_memory()
+    torch.cuda.synchronize()
+    torch.cuda._sleep(200_000_000)  # ~0.1 s of GPU time ahead of the update
+    s.set_instance_transforms(T1)
+    s.refit()
+    host = s.cast_pinhole_host(sensor["cam"], poses, sensor["max_range"], agr.AGR_DEPTH)
+    dev_out = to_np(cast_sensor(s, sensor, "depth"))
+    for k in dev_out:
+        assert np.array_equal(dev_out[k], host[k].numpy().reshape(-1)), k
+    sc2 = sg.Scene(sc.meshes, sc.env_off, sc.inst_asset, sc.inst_label, ring[1])
+    ref = oracle.cast(sc2, oracle_rays(sensor, "depth"))
+    compare(ref, host["dist"].numpy().reshape(-1), host["seg"].numpy().reshape(-1),
+            host["face"].numpy().reshape(-1), "host cast after queued refit")
+    with pytest.raises(agr.AgrError, match="kind"):
+        s.cast_pinhole_host(sensor["cam"], poses, sensor["max_range"], 7)
+
+
+def test_singular_instance_keeps_tlas_boxes_tight():
+    """An instance hidden by a zero scale (a common reset trick) is never
+    hit and must not widen its TLAS ancestors' boxes to infinity: the env's
+    TLAS boxes stay finite, and the images match the oracle."""
+    cube = sg.cube_mesh()
+    Z = sg.make_T(np.eye(3), (3.0, 0.0, 0.0), 0.0)
+    per_env = [[(0, 1, sg.make_T(np.eye(3), (3.0, 0.5, 0.0))), (0, 2, Z),
+                (0, 3, sg.make_T(sg.rot_z(0.4), (5.0, -1.0, 0.3))), (0, 4, Z), (0, 5, Z)]]
+    sc = sg.assemble([cube], per_env)
+    sensor = dict(kind="pinhole", cam=sg.pinhole(64, 48, 90.0), poses=sg.identity_poses(1), max_range=10.0)
+    for builder in (0, 1):
+        s = make_scene(sc, build=False)
+        s.set_tlas_builder(builder)
+        s.build()
+        nodes, root = s.debug_export_bvh4(-1)
+        f = nodes.reshape(-1, 8, 4)
+        boxes = f[:, :6, :].transpose(0, 2, 1)  # [node][child][lo.x hi.x lo.y hi.y lo.z hi.z]
+        refs = f[:, 6, :].view(np.int32)
+        used = refs != np.int32(-2 ** 31)
+        b = boxes[used]
+        # every child box is finite (and small) or the all-+inf never-hit
+        # sentinel of an empty subtree -- never half-infinite
+        fin = np.isfinite(b).all(1)
+        assert np.all(fin | (b == np.inf).all(1)), builder
+        assert fin.sum() >= 2 and np.abs(b[fin]).max() < 10.0, builder
+        got = to_np(cast_sensor(s, sensor, "depth"))
+        ref = oracle.cast(sc, oracle_rays(sensor, "depth"))
+        compare(ref, got["dist"], got["seg"], got["face"], f"singular instances, builder {builder}")
+        assert set(np.unique(got["seg"])) <= {-1, 1, 3}
