@@ -212,7 +212,10 @@ static void cast_one(const world_mesh* w, v3 o, v3 d, double max_range,
     /* candidates within eps of max_range, kept to decide AMB_RANGE at the end */
     double range_cand = INFINITY;
     for (int64_t k = 0; k < w->n_tri; ++k) {
-        plane_hit h = hit_plane(o, d, w->v[3 * k], w->v[3 * k + 1], w->v[3 * k + 2], max_range + eps);
+        /* a near candidate behind the best hit so far (+ eps) can never be
+         * within eps of, or in front of, the final winner: not examined */
+        plane_hit h = hit_plane(o, d, w->v[3 * k], w->v[3 * k + 1], w->v[3 * k + 2],
+                                (best_t < max_range ? best_t : max_range) + eps);
         if (h.parallel) continue;
         double t = h.t;
         if (h.inside) {
