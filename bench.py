@@ -108,6 +108,9 @@ def parse(argv=None):
                     help="auto: warp packets for camera / LiDAR tiles; lane: one ray per lane "
                          "(default: lane for c6, whose terrain seen at grazing angles makes a "
                          "4x8 packet test ~9x the triangles its rays need; auto elsewhere)")
+    ap.add_argument("--no-parts", action="store_true",
+                    help="one BLAS per asset (agr_create_options.part_policy 1) instead of splitting "
+                         "multi-component assets (trees: trunk + canopy) into parts")
     ap.add_argument("--selftest", action="store_true",
                     help="CPU-only check of the multi-rank plumbing (gloo): spawn, env "
                          "sharding, all-gather, digest; no CUDA")
@@ -421,7 +424,8 @@ class Workload:
         self.kind = agr.AGR_RANGE if cfg == 4 else agr.AGR_DEPTH
         self.chans = channels_for(cfg)
         self.trbvh_rounds = args.trbvh_rounds if args.trbvh_rounds is not None else (0 if cfg == 6 else 3)
-        self.scene = agr.Scene.from_scenegen(sc, device=dev.index, trbvh_rounds=self.trbvh_rounds)
+        self.scene = agr.Scene.from_scenegen(sc, device=dev.index, trbvh_rounds=self.trbvh_rounds,
+                                             parts=not args.no_parts)
         self.traversal = args.traversal or ("lane" if cfg == 6 else "auto")
         self.scene.set_traversal(0 if self.traversal == "auto" else 1)
         self.tlas_builder = args.tlas_builder or ("lbvh" if cfg in (5, 6) else "sah")
@@ -695,6 +699,7 @@ def main():
                    "parallelism": f"env-sharded x{world} ({args.scaling} scaling)",
                    "l2": "flushed between timed steps (256 MB write, untimed)",
                    "trbvh_rounds": wl.trbvh_rounds, "traversal": wl.traversal,
+                   "blas_parts": wl.scene.info()["n_parts"], "tlas_items": wl.scene.info()["n_items"],
                    "step": ("update_meshes (every env's BLAS rebuilt)" if cfg == 6 else
                             "set_instance_transforms") + " + TLAS " + ("refit" if wl.step_refit else "rebuild") +
                            " + cast (TLAS builder: " + wl.tlas_builder + ")"},

@@ -57,7 +57,7 @@
 extern "C" {
 #endif
 
-#define AGR_ABI_VERSION 3
+#define AGR_ABI_VERSION 4
 
 typedef int32_t agr_status;
 enum {
@@ -146,6 +146,9 @@ typedef struct {
     int32_t blas_max_depth, tlas_max_depth;
     int64_t device_bytes;
     int32_t built;        /* 1 after the first agr_build                     */
+    int32_t n_parts;      /* BLAS parts over all assets (>= n_assets; see
+                             agr_create_options.part_policy)                 */
+    int64_t n_items;      /* TLAS leaves over all envs: (instance, part)     */
 } agr_scene_info;
 
 int32_t agr_abi_version(void);
@@ -177,7 +180,18 @@ typedef struct {
                              BLAS after the LBVH (Karras & Aila 2013; SAH-
                              optimal treelets of 7 subtrees), 0..16; default 3.
                              0 keeps the plain Karras LBVH.                  */
-    int32_t reserved[7];  /* must be 0                                        */
+    int32_t part_policy;  /* 0 (default): an asset whose faces form several
+                             connected components that fill much less than
+                             their common box (a tree's trunk and canopy) is
+                             split into up to 4 parts, each with its own BLAS
+                             and its own TLAS leaf per instance, so rays only
+                             enter the parts they approach; kept when the
+                             parts' box areas sum to < 0.85 of the whole
+                             box's and no env exceeds 2048 TLAS leaves.
+                             Results are identical either way (the BVH only
+                             accelerates the plain definition).
+                             1: one BLAS per asset.                          */
+    int32_t reserved[6];  /* must be 0                                        */
 } agr_create_options;
 
 agr_status agr_scene_create_ex(int32_t device, const agr_mesh* meshes, int32_t n_meshes,
@@ -366,6 +380,8 @@ agr_status agr_get_counters(agr_scene scene, int64_t counters[8]);
  * INT32_MIN empty.  The binary nodes are packed by the create-time build
  * only: after agr_update_mesh(es) of this asset, a request for `nodes`
  * returns AGR_ESTATE (leaf_face and morton stay available).
+ * AGR_EUNSUPPORTED for an asset split into several BLAS parts
+ * (agr_create_options.part_policy).
  */
 agr_status agr_debug_export_blas(agr_scene scene, int32_t asset, float* nodes,
                                  int32_t* leaf_face, uint32_t* morton,
@@ -373,14 +389,23 @@ agr_status agr_debug_export_blas(agr_scene scene, int32_t asset, float* nodes,
 
 /*
  * Debug export of the traversal BVH4 (synchronous).  which >= 0: the BLAS of
- * asset `which`; which < 0: the TLAS of env (-1 - which) (after agr_build).
+ * asset `which` (AGR_EUNSUPPORTED if it is split into parts); which < 0:
+ * the TLAS of env (-1 - which) (after agr_build).
  * nodes float [n_nodes][32]: per node lo.x[4] hi.x[4] lo.y[4] hi.y[4]
  * lo.z[4] hi.z[4] ref[4] (int bits) cnt; refs are global (>= 0 node index,
- * < 0 ~leaf: triangle record or global instance; INT32_MIN empty).
+ * < 0 ~leaf: triangle record, or global TLAS item = (instance, part) in
+ * instance order; INT32_MIN empty).
  * *root = global index of node 0 of the export.  NULL nodes: size query.
  */
 agr_status agr_debug_export_bvh4(agr_scene scene, int32_t which, float* nodes, int32_t* root,
                                  int64_t* n_nodes);
+
+/*
+ * Debug export of asset `asset`'s BLAS parts (agr_create_options.
+ * part_policy): *n_parts, and, if part_of_face is not NULL, the part
+ * (0 .. n_parts - 1) of each of its faces (host int32 [n_faces]).
+ */
+agr_status agr_debug_asset_parts(agr_scene scene, int32_t asset, int32_t* part_of_face, int32_t* n_parts);
 
 #ifdef __cplusplus
 }

@@ -65,7 +65,8 @@ CHANNELS = {"dist": ("float32", None), "seg": ("int32", None), "face": ("int32",
 
 
 class agr_create_options(ctypes.Structure):
-    _fields_ = [("trbvh_rounds", ctypes.c_int32), ("reserved", ctypes.c_int32 * 7)]
+    _fields_ = [("trbvh_rounds", ctypes.c_int32), ("part_policy", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 6)]
 
 
 class agr_scene_info(ctypes.Structure):
@@ -73,7 +74,8 @@ class agr_scene_info(ctypes.Structure):
                 ("n_instances", ctypes.c_int64), ("n_blas_nodes", ctypes.c_int64),
                 ("n_blas_tris", ctypes.c_int64), ("n_tlas_nodes", ctypes.c_int64),
                 ("blas_max_depth", ctypes.c_int32), ("tlas_max_depth", ctypes.c_int32),
-                ("device_bytes", ctypes.c_int64), ("built", ctypes.c_int32)]
+                ("device_bytes", ctypes.c_int64), ("built", ctypes.c_int32),
+                ("n_parts", ctypes.c_int32), ("n_items", ctypes.c_int64)]
 
 
 _P = ctypes.c_void_p
@@ -112,6 +114,7 @@ _SIGS = {
                                      ctypes.POINTER(ctypes.c_int64)]),
     "agr_debug_export_bvh4": (_I32, [_P, _I32, _P, ctypes.POINTER(ctypes.c_int32),
                                      ctypes.POINTER(ctypes.c_int64)]),
+    "agr_debug_asset_parts": (_I32, [_P, _I32, _P, ctypes.POINTER(ctypes.c_int32)]),
 }
 
 _lib = None
@@ -172,9 +175,11 @@ class Scene:
     """Owner of an ``agr_scene`` handle (one CUDA device)."""
 
     def __init__(self, meshes, env_offsets, inst_asset, inst_label, device: int = 0,
-                 trbvh_rounds: int = 3):
+                 trbvh_rounds: int = 3, parts: bool = True):
         """meshes: list of (verts float32 [V][3], faces int32 [F][3]) host arrays.
-        trbvh_rounds: treelet-restructuring passes on every BLAS (0 = LBVH)."""
+        trbvh_rounds: treelet-restructuring passes on every BLAS (0 = LBVH).
+        parts: split multi-component assets into BLAS parts when it pays
+        (agr_create_options.part_policy 0); False: one BLAS per asset."""
         lib = load()
         self._keep = []
         arr = (agr_mesh * len(meshes))()
@@ -191,7 +196,7 @@ class Scene:
         for j in range(n_inst):
             inst[j] = agr_instance(int(ia[j]), int(il[j]))
         h = _P()
-        opts = agr_create_options(int(trbvh_rounds))
+        opts = agr_create_options(int(trbvh_rounds), 0 if parts else 1)
         _check(lib.agr_scene_create_ex(device, arr, len(meshes), len(env_offsets) - 1,
                                        env_offsets.ctypes.data, inst, ctypes.byref(opts), ctypes.byref(h)))
         self._keep = []
@@ -202,10 +207,10 @@ class Scene:
         self.n_inst = n_inst
 
     @classmethod
-    def from_scenegen(cls, sc, device: int = 0, trbvh_rounds: int = 3):
+    def from_scenegen(cls, sc, device: int = 0, trbvh_rounds: int = 3, parts: bool = True):
         """Build from a ``scenegen.Scene`` (inputs only; no arithmetic)."""
         return cls([(m.verts, m.faces) for m in sc.meshes], sc.env_off, sc.inst_asset,
-                   sc.inst_label, device, trbvh_rounds)
+                   sc.inst_label, device, trbvh_rounds, parts)
 
     def close(self):
         if getattr(self, "handle", None):
@@ -379,6 +384,13 @@ class Scene:
                                          codes.ctypes.data, ctypes.byref(nn), ctypes.byref(nl)))
         return nodes, faces[:nl.value], codes[:nl.value]
 
+
+    def debug_asset_parts(self, asset: int, n_faces: int):
+        """(n_parts, part of each of the asset's n_faces faces)."""
+        n = ctypes.c_int32()
+        part = np.zeros(n_faces, np.int32)
+        _check(load().agr_debug_asset_parts(self.handle, int(asset), part.ctypes.data, ctypes.byref(n)))
+        return n.value, part
 
     def debug_export_bvh4(self, which: int):
         """BVH4 nodes of asset `which` (>= 0) or of env (-1 - which)'s TLAS."""

@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <algorithm>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -66,11 +67,16 @@ struct NvtxRange {
 
 struct agr_scene_s {
     int device = 0;
-    int n_assets = 0, n_envs = 0;
-    int64_t n_inst = 0;
+    int n_assets = 0, n_envs = 0, n_parts = 0;
+    int64_t n_inst = 0, n_items = 0;
     int nb_blas = 0, nt_tlas = 0, n_leaves_cap = 0, max_n = 0;
-    std::vector<AssetInfo> h_assets;
+    std::vector<BlasInfo> h_parts;    // per part (BLAS), refreshed after mesh updates
+    std::vector<int> h_part_off;      // [n_assets + 1] parts of each asset
+    std::vector<int> h_part_nfaces;   // [n_parts]
+    std::vector<int64_t> h_part_foff; // [n_parts] first face of the part in part_faces (-1: the asset's
+                                      // own face array, single-part assets)
     std::vector<int> h_env_off;
+    std::vector<int> h_item_off;      // [n_envs + 1] TLAS items (instance, part) of each env
     std::vector<int> h_tlas_off;
     std::vector<void*> allocs;
     size_t device_bytes = 0;
@@ -79,9 +85,12 @@ struct agr_scene_s {
     float4* bnodes = nullptr;  // binary BLAS nodes, 4 float4 per node (debug export)
     float4* tris = nullptr;
     float* triv = nullptr;
-    float4* irec = nullptr;
+    float4* irec = nullptr;    // per item
     float* inst_T = nullptr;
-    float* inst_box = nullptr;
+    float* item_box = nullptr;
+    int* item_inst = nullptr;
+    int* item_part = nullptr;
+    int* item_off = nullptr;
     int* inst_asset = nullptr;
     int* inst_label = nullptr;
     int* inst_face_off = nullptr;
@@ -89,10 +98,13 @@ struct agr_scene_s {
     int* tlas_off = nullptr;
     int* tlas_root = nullptr;
     int* tlas_child = nullptr;
-    int* tlas_inst_parent = nullptr;
+    int* tlas_item_parent = nullptr;
     int* tlas_node_parent = nullptr;
     int* tlas_depth = nullptr;
-    AssetInfo* assets = nullptr;
+    BlasInfo* parts = nullptr;      // [n_parts]
+    int* part_off = nullptr;        // [n_assets + 1]
+    int* part_faces = nullptr;      // gathered face triples of the multi-part assets, by part
+    int* part_face_ids = nullptr;   // their asset-local face ids
     uint32_t* morton = nullptr;  // sorted BLAS Morton codes (debug export)
     // asset meshes kept on the device for BLAS rebuilds (agr_update_mesh)
     float* mesh_verts = nullptr;
@@ -105,7 +117,7 @@ struct agr_scene_s {
     std::vector<int64_t> h_mvert_off, h_mface_off;
     std::vector<int> h_node_base, h_leaf_base, h_nverts, h_nfaces;
     std::vector<char> h_bin_stale;  // binary LBVH export out of date (mesh updated)
-    bool assets_stale = false;
+    bool parts_stale = false;       // h_parts out of date (mesh updated)
     int trbvh_rounds = 3;
     unsigned long long* counters = nullptr;
     bool built = false, dirty = false;
@@ -154,7 +166,8 @@ struct agr_scene_s {
         v.env_off = env_off;
         v.tlas_root = tlas_root;
         v.inst_asset = inst_asset;
-        v.assets = assets;
+        v.parts = parts;
+        v.part_off = part_off;
         v.n_envs = n_envs;
         v.annot = annot;
         v.annot_k = annot_k;
@@ -168,15 +181,16 @@ struct agr_scene_s {
         TlasArgs a;
         a.nodes = nodes;
         a.irec = irec;
-        a.inst_box = inst_box;
+        a.item_box = item_box;
         a.inst_T = inst_T;
-        a.inst_asset = inst_asset;
-        a.assets = assets;
-        a.env_off = env_off;
+        a.item_inst = item_inst;
+        a.item_part = item_part;
+        a.parts = parts;
+        a.item_off = item_off;
         a.tlas_off = tlas_off;
         a.nb_blas = nb_blas;
         a.tlas_child = tlas_child;
-        a.tlas_inst_parent = tlas_inst_parent;
+        a.tlas_item_parent = tlas_item_parent;
         a.tlas_node_parent = tlas_node_parent;
         a.tlas_depth = tlas_depth;
         a.n_envs = n_envs;
@@ -202,23 +216,32 @@ struct agr_scene_s {
     }
 };
 
-// (Re)build asset a's BLAS from the device copy of its mesh (async on st).
-// `binary`: also pack the binary LBVH nodes for agr_debug_export_blas (the
-// create-time build only; mesh updates skip it and mark the asset's binary
-// export stale).
+// (Re)build the BLAS of every part of the assets `assets[0, n)` from the
+// device copy of their meshes, in one batch (async on st).  `binary`: also
+// pack the binary LBVH nodes for agr_debug_export_blas (the create-time build
+// only; mesh updates skip it and mark the asset's binary export stale).
 static cudaError_t build_assets(agr_scene_s* s, const int* assets, int n, cudaStream_t st, bool binary) {
-    std::vector<BlasSeg> segs(n);
+    std::vector<BlasSeg> segs;
     for (int k = 0; k < n; ++k) {
         const int a = assets[k];
-        BlasSeg& g = segs[k];
-        g.verts = s->mesh_verts + 3 * s->h_mvert_off[a];
-        g.faces = s->mesh_faces + 3 * s->h_mface_off[a];
-        g.n_verts = s->h_nverts[a];
-        g.n_faces = s->h_nfaces[a];
-        g.off = 0;
-        g.node_base = s->h_node_base[a];
-        g.leaf_base = s->h_leaf_base[a];
-        g.info = s->assets + a;
+        for (int p = s->h_part_off[a]; p < s->h_part_off[a + 1]; ++p) {
+            BlasSeg g;
+            g.verts = s->mesh_verts + 3 * s->h_mvert_off[a];
+            g.n_verts = s->h_nverts[a];
+            if (s->h_part_foff[p] < 0) {  // the whole asset
+                g.faces = s->mesh_faces + 3 * s->h_mface_off[a];
+                g.face_ids = nullptr;
+            } else {
+                g.faces = s->part_faces + 3 * s->h_part_foff[p];
+                g.face_ids = s->part_face_ids + s->h_part_foff[p];
+            }
+            g.n_faces = s->h_part_nfaces[p];
+            g.off = 0;
+            g.node_base = s->h_node_base[p];
+            g.leaf_base = s->h_leaf_base[p];
+            g.info = s->parts + p;
+            segs.push_back(g);
+        }
     }
     BlasBatchArgs ba;
     ba.nodes = s->nodes;
@@ -227,15 +250,105 @@ static cudaError_t build_assets(agr_scene_s* s, const int* assets, int n, cudaSt
     ba.triv = s->triv;
     ba.dbg_morton = s->morton;
     ba.trbvh_rounds = s->trbvh_rounds;
-    return blas_build_batch(segs.data(), n, ba, s->blas_scratch, st);
+    return blas_build_batch(segs.data(), (int)segs.size(), ba, s->blas_scratch, st);
 }
 
-static agr_status refresh_assets(agr_scene_s* s) {
-    if (!s->assets_stale) return AGR_OK;
+static agr_status refresh_parts(agr_scene_s* s) {
+    if (!s->parts_stale) return AGR_OK;
     CK(cudaDeviceSynchronize());
-    CK(cudaMemcpy(s->h_assets.data(), s->assets, sizeof(AssetInfo) * s->n_assets, cudaMemcpyDeviceToHost));
-    s->assets_stale = false;
+    CK(cudaMemcpy(s->h_parts.data(), s->parts, sizeof(BlasInfo) * s->n_parts, cudaMemcpyDeviceToHost));
+    s->parts_stale = false;
     return AGR_OK;
+}
+
+// Partition of an asset's faces into BLAS parts (DESIGN.md §8 "instance
+// parts"): connected components of the face-vertex graph (union-find),
+// merged greedily -- the pair whose union box grows the summed box surface
+// area least -- down to MAX_PARTS; kept only if the parts' boxes have less
+// than PART_SA_RATIO of the whole asset's box surface area (a random ray
+// crosses a box with probability ~ its area, so that many fewer entries).
+// Returns the part of every face (0 .. n_parts - 1, numbered by first face).
+constexpr double PART_SA_RATIO = 0.85;
+constexpr int PART_MAX_COMPONENTS = 64;
+
+static std::vector<int> asset_parts(const agr_mesh& m, int* n_parts) {
+    const int F = m.n_faces, V = m.n_verts;
+    std::vector<int> part(F, 0);
+    *n_parts = 1;
+    std::vector<int> up(V);
+    for (int v = 0; v < V; ++v) up[v] = v;
+    auto find = [&](int x) {
+        while (up[x] != x) x = up[x] = up[up[x]];
+        return x;
+    };
+    for (int f = 0; f < F; ++f)
+        for (int c = 1; c < 3; ++c) {
+            const int a = find(m.faces[3 * f]), b = find(m.faces[3 * f + c]);
+            if (a != b) up[a] = b;
+        }
+    std::vector<int> comp_of_root(V, -1), comp(F);
+    int k = 0;
+    for (int f = 0; f < F; ++f) {
+        const int r = find(m.faces[3 * f]);
+        if (comp_of_root[r] < 0) {
+            if (k == PART_MAX_COMPONENTS) return part;  // a triangle soup: one part
+            comp_of_root[r] = k++;
+        }
+        comp[f] = comp_of_root[r];
+    }
+    if (k < 2) return part;
+    struct Box { double lo[3], hi[3]; };
+    auto area = [](const Box& b) {
+        const double dx = b.hi[0] - b.lo[0], dy = b.hi[1] - b.lo[1], dz = b.hi[2] - b.lo[2];
+        return dx * dy + dy * dz + dz * dx;
+    };
+    auto join = [](const Box& a, const Box& b) {
+        Box r;
+        for (int c = 0; c < 3; ++c) { r.lo[c] = std::min(a.lo[c], b.lo[c]); r.hi[c] = std::max(a.hi[c], b.hi[c]); }
+        return r;
+    };
+    std::vector<Box> box(k, Box{{1e300, 1e300, 1e300}, {-1e300, -1e300, -1e300}});
+    Box all{{1e300, 1e300, 1e300}, {-1e300, -1e300, -1e300}};
+    for (int f = 0; f < F; ++f)
+        for (int c = 0; c < 3; ++c) {
+            const float* v = m.verts + 3 * m.faces[3 * f + c];
+            for (int q = 0; q < 3; ++q) {
+                box[comp[f]].lo[q] = std::min(box[comp[f]].lo[q], (double)v[q]);
+                box[comp[f]].hi[q] = std::max(box[comp[f]].hi[q], (double)v[q]);
+            }
+        }
+    for (auto& b : box) all = join(all, b);
+    std::vector<int> group(k);  // component -> group (merged components)
+    for (int c = 0; c < k; ++c) group[c] = c;
+    int live = k;
+    std::vector<char> alive(k, 1);
+    while (live > MAX_PARTS) {
+        int bi = -1, bj = -1;
+        double best = 1e300;
+        for (int i = 0; i < k; ++i)
+            for (int j = i + 1; j < k; ++j)
+                if (alive[i] && alive[j]) {
+                    const double g = area(join(box[i], box[j])) - area(box[i]) - area(box[j]);
+                    if (g < best) { best = g; bi = i; bj = j; }
+                }
+        box[bi] = join(box[bi], box[bj]);
+        alive[bj] = 0;
+        for (int c = 0; c < k; ++c) if (group[c] == bj) group[c] = bi;
+        --live;
+    }
+    double sum = 0.0;
+    for (int i = 0; i < k; ++i) if (alive[i]) sum += area(box[i]);
+    if (!(sum < PART_SA_RATIO * area(all))) return part;
+    // number the parts by their first face
+    std::vector<int> id(k, -1);
+    int np = 0;
+    for (int f = 0; f < F; ++f) {
+        const int g = group[comp[f]];
+        if (id[g] < 0) id[g] = np++;
+        part[f] = id[g];
+    }
+    *n_parts = np;
+    return part;
 }
 
 // Marks the end of the scene-changing work just queued on `st` (see `ready`).
@@ -301,34 +414,84 @@ agr_status agr_scene_create_ex(int32_t device, const agr_mesh* meshes, int32_t n
 
     if (opts && (opts->trbvh_rounds < 0 || opts->trbvh_rounds > 16))
         return fail(AGR_EINVAL, "trbvh_rounds must be in [0, 16]");
+    if (opts && (opts->part_policy < 0 || opts->part_policy > 1))
+        return fail(AGR_EINVAL, "part_policy must be 0 (auto) or 1 (one BLAS per asset)");
     agr_scene_s* s = new agr_scene_s();
     s->device = device;
     if (opts) s->trbvh_rounds = opts->trbvh_rounds;
     s->n_assets = n_meshes;
     s->n_envs = n_envs;
     s->n_inst = n_inst;
-    // host-side layout
-    std::vector<int> node_base(n_meshes), leaf_base(n_meshes);
-    int nb = 0, nl = 0;
+    // ---- asset parts (one BLAS each) and the TLAS items (instance, part) ----
+    std::vector<std::vector<int>> part_of(n_meshes);
+    std::vector<int> np_asset(n_meshes, 1);
+    if (!opts || opts->part_policy == 0)
+        for (int a = 0; a < n_meshes; ++a) part_of[a] = asset_parts(meshes[a], &np_asset[a]);
+    // a split that would push an env past the one-CTA TLAS limit is dropped
+    for (int e = 0; e < n_envs; ++e) {
+        int64_t items = 0;
+        for (int64_t j = env_offsets[e]; j < env_offsets[e + 1]; ++j) items += np_asset[inst[j].asset];
+        if (items > MAX_TLAS_N) {
+            for (int a = 0; a < n_meshes; ++a) np_asset[a] = 1;
+            break;
+        }
+    }
+    s->h_part_off.assign(n_meshes + 1, 0);
+    for (int a = 0; a < n_meshes; ++a) s->h_part_off[a + 1] = s->h_part_off[a] + np_asset[a];
+    const int n_parts = s->h_part_off[n_meshes];
+    s->n_parts = n_parts;
+    // gathered faces of the multi-part assets, part by part, faces ascending
+    std::vector<int> h_pfaces, h_pface_ids;
+    s->h_part_nfaces.assign(n_parts, 0);
+    s->h_part_foff.assign(n_parts, -1);
     for (int a = 0; a < n_meshes; ++a) {
-        node_base[a] = nb;
-        leaf_base[a] = nl;
-        nb += meshes[a].n_faces > 1 ? meshes[a].n_faces - 1 : 1;
-        nl += meshes[a].n_faces;
+        const int p0 = s->h_part_off[a];
+        if (np_asset[a] == 1) {
+            s->h_part_nfaces[p0] = meshes[a].n_faces;
+            continue;
+        }
+        for (int p = 0; p < np_asset[a]; ++p) {
+            s->h_part_foff[p0 + p] = (int64_t)h_pface_ids.size();
+            for (int f = 0; f < meshes[a].n_faces; ++f)
+                if (part_of[a][f] == p) {
+                    for (int c = 0; c < 3; ++c) h_pfaces.push_back(meshes[a].faces[3 * f + c]);
+                    h_pface_ids.push_back(f);
+                    ++s->h_part_nfaces[p0 + p];
+                }
+        }
+    }
+    std::vector<int> node_base(n_parts), leaf_base(n_parts);
+    int nb = 0, nl = 0;
+    for (int p = 0; p < n_parts; ++p) {
+        node_base[p] = nb;
+        leaf_base[p] = nl;
+        nb += s->h_part_nfaces[p] > 1 ? s->h_part_nfaces[p] - 1 : 1;
+        nl += s->h_part_nfaces[p];
     }
     s->nb_blas = nb;
     s->n_leaves_cap = nl;
     s->h_env_off.resize(n_envs + 1);
+    s->h_item_off.resize(n_envs + 1);
     s->h_tlas_off.resize(n_envs);
+    std::vector<int> h_item_inst, h_item_part;
     int nt = 0, max_n = 0;
     for (int e = 0; e < n_envs; ++e) {
-        int n = (int)(env_offsets[e + 1] - env_offsets[e]);
         s->h_env_off[e] = (int)env_offsets[e];
+        s->h_item_off[e] = (int)h_item_inst.size();
+        for (int64_t j = env_offsets[e]; j < env_offsets[e + 1]; ++j)
+            for (int p = s->h_part_off[inst[j].asset]; p < s->h_part_off[inst[j].asset + 1]; ++p) {
+                h_item_inst.push_back((int)j);
+                h_item_part.push_back(p);
+            }
+        const int n = (int)h_item_inst.size() - s->h_item_off[e];
         s->h_tlas_off[e] = nt;
         nt += n > 1 ? n - 1 : 1;
         max_n = n > max_n ? n : max_n;
     }
     s->h_env_off[n_envs] = (int)n_inst;
+    const int64_t n_items = (int64_t)h_item_inst.size();
+    s->h_item_off[n_envs] = (int)n_items;
+    s->n_items = n_items;
     s->nt_tlas = nt;
     s->max_n = max_n;
     std::vector<int> h_asset(n_inst), h_label(n_inst), h_face_off(n_inst), h_root(n_envs);
@@ -358,9 +521,12 @@ agr_status agr_scene_create_ex(int32_t device, const agr_mesh* meshes, int32_t n
     CKB(s->alloc(&s->bnodes, 4 * (size_t)nb));
     CKB(s->alloc(&s->tris, 3 * (size_t)nl));
     CKB(s->alloc(&s->triv, 9 * (size_t)nl));
-    CKB(s->alloc(&s->irec, 4 * (size_t)n_inst));
+    CKB(s->alloc(&s->irec, 4 * (size_t)n_items));
     CKB(s->alloc(&s->inst_T, 12 * (size_t)n_inst));
-    CKB(s->alloc(&s->inst_box, 6 * (size_t)n_inst));
+    CKB(s->alloc(&s->item_box, 6 * (size_t)n_items));
+    CKB(s->alloc(&s->item_inst, (size_t)n_items));
+    CKB(s->alloc(&s->item_part, (size_t)n_items));
+    CKB(s->alloc(&s->item_off, (size_t)n_envs + 1));
     CKB(s->alloc(&s->inst_asset, (size_t)n_inst));
     CKB(s->alloc(&s->inst_label, (size_t)n_inst));
     CKB(s->alloc(&s->inst_face_off, (size_t)n_inst));
@@ -368,10 +534,13 @@ agr_status agr_scene_create_ex(int32_t device, const agr_mesh* meshes, int32_t n
     CKB(s->alloc(&s->tlas_off, (size_t)n_envs));
     CKB(s->alloc(&s->tlas_root, (size_t)n_envs));
     CKB(s->alloc(&s->tlas_child, 2 * (size_t)nt));
-    CKB(s->alloc(&s->tlas_inst_parent, (size_t)n_inst));
+    CKB(s->alloc(&s->tlas_item_parent, (size_t)n_items));
     CKB(s->alloc(&s->tlas_node_parent, (size_t)nt));
     CKB(s->alloc(&s->tlas_depth, (size_t)n_envs));
-    CKB(s->alloc(&s->assets, (size_t)n_meshes));
+    CKB(s->alloc(&s->parts, (size_t)n_parts));
+    CKB(s->alloc(&s->part_off, (size_t)n_meshes + 1));
+    CKB(s->alloc(&s->part_faces, h_pfaces.size()));
+    CKB(s->alloc(&s->part_face_ids, h_pface_ids.size()));
     CKB(s->alloc(&s->morton, (size_t)nl));
     CKB(s->alloc(&s->counters, 8));
     CKB(cudaMemset(s->morton, 0xFF, sizeof(uint32_t) * (size_t)nl));
@@ -382,6 +551,15 @@ agr_status agr_scene_create_ex(int32_t device, const agr_mesh* meshes, int32_t n
     CKB(cudaMemcpy(s->env_off, s->h_env_off.data(), sizeof(int) * (n_envs + 1), cudaMemcpyHostToDevice));
     CKB(cudaMemcpy(s->tlas_off, s->h_tlas_off.data(), sizeof(int) * n_envs, cudaMemcpyHostToDevice));
     CKB(cudaMemcpy(s->tlas_root, h_root.data(), sizeof(int) * n_envs, cudaMemcpyHostToDevice));
+    CKB(cudaMemcpy(s->item_inst, h_item_inst.data(), sizeof(int) * n_items, cudaMemcpyHostToDevice));
+    CKB(cudaMemcpy(s->item_part, h_item_part.data(), sizeof(int) * n_items, cudaMemcpyHostToDevice));
+    CKB(cudaMemcpy(s->item_off, s->h_item_off.data(), sizeof(int) * (n_envs + 1), cudaMemcpyHostToDevice));
+    CKB(cudaMemcpy(s->part_off, s->h_part_off.data(), sizeof(int) * (n_meshes + 1), cudaMemcpyHostToDevice));
+    if (!h_pfaces.empty()) {
+        CKB(cudaMemcpy(s->part_faces, h_pfaces.data(), sizeof(int) * h_pfaces.size(), cudaMemcpyHostToDevice));
+        CKB(cudaMemcpy(s->part_face_ids, h_pface_ids.data(), sizeof(int) * h_pface_ids.size(),
+                       cudaMemcpyHostToDevice));
+    }
 
     // BLAS build: all asset meshes stay on the device (for agr_update_mesh),
     // and every asset is built in one batch (one set of launches)
@@ -413,7 +591,7 @@ agr_status agr_scene_create_ex(int32_t device, const agr_mesh* meshes, int32_t n
         CKB(cudaMemcpy(s->asset_foff, fo.data(), sizeof(int) * n_meshes, cudaMemcpyHostToDevice));
     }
     // scratch for a batch of every asset (any update batch fits in it)
-    CKB(s->alloc((char**)&s->blas_scratch, blas_scratch_bytes(s->h_mface_off[n_meshes], n_meshes)));
+    CKB(s->alloc((char**)&s->blas_scratch, blas_scratch_bytes(s->h_mface_off[n_meshes], n_parts)));
     cudaError_t err = cudaSuccess;
     for (int a = 0; a < n_meshes && err == cudaSuccess; ++a) {
         err = cudaMemcpyAsync(s->mesh_verts + 3 * s->h_mvert_off[a], meshes[a].verts,
@@ -433,20 +611,20 @@ agr_status agr_scene_create_ex(int32_t device, const agr_mesh* meshes, int32_t n
         cudaStreamDestroy(st);
         return bail(cuda_fail(err, "BLAS build"));
     }
-    s->h_assets.resize(n_meshes);
-    CKB(cudaMemcpy(s->h_assets.data(), s->assets, sizeof(AssetInfo) * n_meshes, cudaMemcpyDeviceToHost));
+    s->h_parts.resize(n_parts);
+    CKB(cudaMemcpy(s->h_parts.data(), s->parts, sizeof(BlasInfo) * n_parts, cudaMemcpyDeviceToHost));
     int max_depth = 0;
-    for (auto& a : s->h_assets) max_depth = a.depth > max_depth ? a.depth : max_depth;
+    for (auto& a : s->h_parts) max_depth = a.depth > max_depth ? a.depth : max_depth;
     // identity transforms until the caller sets them
     {
         std::vector<float> I(12 * (size_t)n_inst, 0.0f);
         for (int64_t j = 0; j < n_inst; ++j) I[12 * j + 0] = I[12 * j + 5] = I[12 * j + 10] = 1.0f;
         CKB(cudaMemcpy(s->inst_T, I.data(), sizeof(float) * I.size(), cudaMemcpyHostToDevice));
     }
-    err = instances_update(s->tlas_args(), (int)n_inst, st);
+    err = items_update(s->tlas_args(), (int)n_items, st);
     if (err == cudaSuccess) err = cudaStreamSynchronize(st);
     cudaStreamDestroy(st);
-    if (err != cudaSuccess) return bail(cuda_fail(err, "instances_update"));
+    if (err != cudaSuccess) return bail(cuda_fail(err, "items_update"));
     if (max_depth > AGR_MAX_BVH_DEPTH)
         return bail(fail(AGR_EUNSUPPORTED, "BLAS depth %d exceeds AGR_MAX_BVH_DEPTH (%d)", max_depth,
                          AGR_MAX_BVH_DEPTH));
@@ -475,11 +653,11 @@ agr_status agr_scene_get_info(agr_scene s, agr_scene_info* info) {
     info->n_envs = s->n_envs;
     info->n_instances = s->n_inst;
     info->n_blas_nodes = s->nb_blas;
-    agr_status rs = refresh_assets(s);
+    agr_status rs = refresh_parts(s);
     if (rs != AGR_OK) return rs;
     int64_t leaves = 0;
     int bd = 0;
-    for (auto& a : s->h_assets) {
+    for (auto& a : s->h_parts) {
         leaves += a.n_leaves;
         bd = a.depth > bd ? a.depth : bd;
     }
@@ -494,6 +672,8 @@ agr_status agr_scene_get_info(agr_scene s, agr_scene_info* info) {
     }
     info->device_bytes = (int64_t)s->device_bytes;
     info->built = s->built ? 1 : 0;
+    info->n_parts = s->n_parts;
+    info->n_items = s->n_items;
     return AGR_OK;
 }
 
@@ -506,7 +686,7 @@ agr_status agr_set_instance_transforms(agr_scene s, const float* T, void* stream
     DeviceGuard guard(s->device);
     cudaStream_t st = (cudaStream_t)stream;
     CK(cudaMemcpyAsync(s->inst_T, T, sizeof(float) * 12 * s->n_inst, cudaMemcpyDeviceToDevice, st));
-    CK(instances_update(s->tlas_args(), (int)s->n_inst, st));
+    CK(items_update(s->tlas_args(), (int)s->n_items, st));
     s->dirty = true;
     return mark_ready(s, st);
 }
@@ -543,8 +723,8 @@ agr_status agr_update_meshes(agr_scene s, int32_t n, const int32_t* assets, cons
     }
     CK(build_assets(s, assets, n, st, false));
     for (int k = 0; k < n; ++k) s->h_bin_stale[assets[k]] = 1;
-    CK(instances_update(s->tlas_args(), (int)s->n_inst, st));  // instance boxes from the new BLAS
-    s->assets_stale = true;
+    CK(items_update(s->tlas_args(), (int)s->n_items, st));  // item boxes from the new BLAS
+    s->parts_stale = true;
     s->dirty = true;
     return mark_ready(s, st);
 }
@@ -957,10 +1137,13 @@ agr_status agr_debug_export_blas(agr_scene s, int32_t asset, float* nodes, int32
     g_err.clear();
     if (!s || !n_nodes || !n_leaves) return fail(AGR_EINVAL, "bad argument");
     if (asset < 0 || asset >= s->n_assets) return fail(AGR_EINVAL, "asset out of range");
+    if (s->h_part_off[asset + 1] - s->h_part_off[asset] != 1)
+        return fail(AGR_EUNSUPPORTED, "asset %d is split into %d BLAS parts (create with part_policy = 1 to "
+                    "export it as one LBVH)", asset, s->h_part_off[asset + 1] - s->h_part_off[asset]);
     DeviceGuard guard(s->device);
-    agr_status rs = refresh_assets(s);
+    agr_status rs = refresh_parts(s);
     if (rs != AGR_OK) return rs;
-    const AssetInfo& a = s->h_assets[asset];
+    const BlasInfo& a = s->h_parts[s->h_part_off[asset]];
     int64_t nn = a.n_leaves > 1 ? a.n_leaves - 1 : 1;
     *n_nodes = nn;
     *n_leaves = a.n_leaves;
@@ -1003,19 +1186,22 @@ agr_status agr_debug_export_bvh4(agr_scene s, int32_t which, float* nodes, int32
     int64_t base, count;
     if (which >= 0) {
         if (which >= s->n_assets) return fail(AGR_EINVAL, "asset out of range");
+        if (s->h_part_off[which + 1] - s->h_part_off[which] != 1)
+            return fail(AGR_EUNSUPPORTED, "asset %d is split into BLAS parts (part_policy = 1 exports it whole)",
+                        which);
         {
             DeviceGuard g2(s->device);
-            agr_status rs = refresh_assets(s);
+            agr_status rs = refresh_parts(s);
             if (rs != AGR_OK) return rs;
         }
-        const AssetInfo& a = s->h_assets[which];
+        const BlasInfo& a = s->h_parts[s->h_part_off[which]];
         base = a.node_base;
         count = a.n_leaves > 1 ? a.n_leaves - 1 : 1;
     } else {
         const int e = -1 - which;
         if (e >= s->n_envs) return fail(AGR_EINVAL, "env out of range");
         if (!s->built) return fail(AGR_ESTATE, "TLAS not built");
-        int n = s->h_env_off[e + 1] - s->h_env_off[e];
+        int n = s->h_item_off[e + 1] - s->h_item_off[e];
         base = (int64_t)s->nb_blas + s->h_tlas_off[e];
         count = n > 1 ? n - 1 : 1;
     }
@@ -1025,6 +1211,27 @@ agr_status agr_debug_export_bvh4(agr_scene s, int32_t which, float* nodes, int32
     DeviceGuard guard(s->device);
     CK(cudaDeviceSynchronize());
     CK(cudaMemcpy(nodes, s->nodes + 8 * (size_t)base, sizeof(float4) * 8 * count, cudaMemcpyDeviceToHost));
+    return AGR_OK;
+}
+
+agr_status agr_debug_asset_parts(agr_scene s, int32_t asset, int32_t* part_of_face, int32_t* n_parts) {
+    g_err.clear();
+    if (!s || !n_parts) return fail(AGR_EINVAL, "bad argument");
+    if (asset < 0 || asset >= s->n_assets) return fail(AGR_EINVAL, "asset out of range");
+    const int p0 = s->h_part_off[asset], p1 = s->h_part_off[asset + 1];
+    *n_parts = p1 - p0;
+    if (!part_of_face) return AGR_OK;
+    if (p1 - p0 == 1) {
+        for (int f = 0; f < s->h_nfaces[asset]; ++f) part_of_face[f] = 0;
+        return AGR_OK;
+    }
+    DeviceGuard guard(s->device);
+    for (int p = p0; p < p1; ++p) {
+        std::vector<int> ids(s->h_part_nfaces[p]);
+        CK(cudaMemcpy(ids.data(), s->part_face_ids + s->h_part_foff[p], sizeof(int) * ids.size(),
+                      cudaMemcpyDeviceToHost));
+        for (int f : ids) part_of_face[f] = p - p0;
+    }
     return AGR_OK;
 }
 

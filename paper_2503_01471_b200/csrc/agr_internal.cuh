@@ -12,7 +12,7 @@
 //             f0 = lo.x[4], f1 = hi.x[4], f2 = lo.y[4], f3 = hi.y[4],
 //             f4 = lo.z[4], f5 = hi.z[4], f6 = ref[4] (int bits), f7 = (n, -)
 //           ref >= 0: global node index; ref < 0: leaf ~x (TLAS: x = global
-//           instance; BLAS: x = first | (count - 1) << LEAF_SHIFT, a leaf of
+//           item; BLAS: x = first | (count - 1) << LEAF_SHIFT, a leaf of
 //           `count` <= LEAF_MAX consecutive triangle records whose box is
 //           their union -- a binary subtree over at most LEAF_MAX
 //           consecutive leaves is referenced as one such leaf instead of
@@ -26,9 +26,17 @@
 //             t2 = (e2.xyz, local face id as int bits)
 //   triv    float[9] per BLAS leaf: the exact FP32 input vertices v0 v1 v2
 //           (read only by the FP64 arbitration / epilogue).
-//   irec    float4[4] per instance, 64 B (ray -> object space):
+//   irec    float4[4] per TLAS item, 64 B (ray -> object space):
 //             r0..r2 = rows of [Ainv | binv] (FP64 inverse rounded to FP32)
-//             r3 = (blas root node (int bits), nAinv, err_off, -)
+//             r3 = (blas root node (int bits), nAinv, err_off, instance (int bits))
+//
+// Parts and items.  An asset whose faces form several connected components
+// spread over a much larger box than they fill (a tree: thin trunk + round
+// canopy) is split at create into up to MAX_PARTS parts, each with a BLAS
+// of its own (a "part" = one BLAS; BlasInfo is per part).  The TLAS leaves
+// are ITEMS = (instance, part) pairs, so a ray enters only the parts whose
+// world boxes it crosses.  Triangle records keep the asset-local face id, so
+// face numbering, labels and every output are unchanged.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -46,7 +54,8 @@ constexpr int LEAF_MAX = AGR_LEAF_MAX;      // triangles per BLAS leaf (1..4)
 constexpr int LEAF_SHIFT = 29;              // BLAS leaf ref: count - 1 in bits 29-30
 constexpr int LEAF_MASK = (1 << LEAF_SHIFT) - 1;  // first record (faces_total < LEAF_MASK - 4, abi.cu)
 constexpr int STACK_SIZE = 96;              // traversal stack entries per ray
-constexpr int MAX_TLAS_N = 1024;            // AGR_MAX_INSTANCES_PER_ENV
+constexpr int MAX_PARTS = 4;                // BLAS parts per asset
+constexpr int MAX_TLAS_N = 2048;            // TLAS leaves (items) per env: one-CTA build
 
 // Relative error budget of the FP32 object-space ray:
 // position error <= K_ERR * (nAinv * (|o|_1 + |b|_1 + t_max |d|_1) + r_asset).
@@ -54,11 +63,12 @@ constexpr float K_ERR = 7.62939453125e-06f;  // 2^-17
 // Relative slack on FP32 t values (ray direction rounding etc.).
 constexpr float T_REL = 9.5367431640625e-07f;  // 2^-20
 
-struct AssetInfo {
-    int node_base;   // global index of the asset's root node
-    int leaf_base;   // global index of the asset's first leaf record
+// One BLAS (an asset part).
+struct BlasInfo {
+    int node_base;   // global index of the BLAS root node
+    int leaf_base;   // global index of its first leaf record
     int n_leaves;    // non-degenerate triangles in the BLAS
-    int n_faces;     // faces in the asset (numbering)
+    int n_faces;     // faces of the part
     float lo[3], hi[3];  // root box (object space, exact min/max)
     float radius;    // max |v| over the asset's vertices (object units)
     int depth;       // BLAS depth (edges from root to deepest leaf)
@@ -69,14 +79,15 @@ struct SceneView {
     const float4* nodes;      // [n_nodes][4]
     const float4* tris;       // [n_leaves][3]
     const float* triv;        // [n_leaves][9]
-    const float4* irec;       // [n_inst][4]
+    const float4* irec;       // [n_items][4] (TLAS leaf ~item)
     const float* inst_T;      // [n_inst][12] forward transforms (FP32 input)
     const int* inst_face_off; // [n_inst] per-env face offset of the instance
     const int* inst_label;    // [n_inst]
     const int* env_off;       // [n_envs + 1]
     const int* tlas_root;     // [n_envs] global node index of the env's TLAS root
     const int* inst_asset;    // [n_inst]
-    const AssetInfo* assets;  // [n_assets]
+    const BlasInfo* parts;    // [n_parts]
+    const int* part_off;      // [n_assets + 1] parts of asset a: [part_off[a], part_off[a+1])
     int n_envs;
     // vertex annotations (f1): [sum V][annot_k] by asset vertex, NaN = none
     const float* annot;
@@ -194,17 +205,18 @@ __device__ __forceinline__ void write_node4(float4* nodes, int g, const float b[
 
 // Host launch wrappers implemented in the .cu files (all async on `stream`).
 namespace agr {
-// One asset of a batched BLAS build: all kernels of the build run once over
-// the concatenation of the batch's faces (face g of the batch belongs to the
-// asset whose [off, off + n_faces) contains it).
+// One BLAS (asset part) of a batched BLAS build: all kernels of the build
+// run once over the concatenation of the batch's faces (face g of the batch
+// belongs to the segment whose [off, off + n_faces) contains it).
 struct BlasSeg {
-    const float* verts;    // device [V][3]
-    const int* faces;      // device [F][3], asset-local vertex ids
+    const float* verts;    // device [V][3] (the asset's vertices)
+    const int* faces;      // device [F][3], asset-local vertex ids (this part's faces)
+    const int* face_ids;   // device [F]: asset-local face id of each face, or null (identity)
     int n_verts, n_faces;
     int off;               // first batch face of this asset (set by blas_build_batch)
     int node_base;         // global index of this asset's first node (F - 1 reserved, >= 1)
     int leaf_base;         // global leaf-record index of this asset's first leaf (F reserved)
-    AssetInfo* info;       // this asset's AssetInfo (device)
+    BlasInfo* info;        // this part's BlasInfo (device)
 };
 struct BlasBatchArgs {
     float4* nodes;         // global BVH4 node array
@@ -223,24 +235,25 @@ cudaError_t blas_build_batch(BlasSeg* h_segs, int n_segs, const BlasBatchArgs& a
 
 struct TlasArgs {
     float4* nodes;            // global node array (TLAS part written)
-    float4* irec;             // [n_inst][4] written
-    float* inst_box;          // [n_inst][6] written
+    float4* irec;             // [n_items][4] written
+    float* item_box;          // [n_items][6] written
     const float* inst_T;      // [n_inst][12]
-    const int* inst_asset;    // [n_inst]
-    const AssetInfo* assets;  // [n_assets]
-    const int* env_off;       // [n_envs+1]
+    const int* item_inst;     // [n_items] instance of each item
+    const int* item_part;     // [n_items] part (BLAS) of each item
+    const BlasInfo* parts;    // [n_parts]
+    const int* item_off;      // [n_envs+1] items of env e: [item_off[e], item_off[e+1])
     const int* tlas_off;      // [n_envs] offset of the env's first node within the TLAS part
     int nb_blas;              // number of BLAS nodes (TLAS node j of env e is global
                               // node nb_blas + tlas_off[e] + j)
-    int* tlas_child;          // [2 * n_tlas_nodes] local child refs (>=0 node, <0 ~local inst)
-    int* tlas_inst_parent;    // [n_inst] local parent (internal node) of each instance leaf
+    int* tlas_child;          // [2 * n_tlas_nodes] local child refs (>=0 node, <0 ~local item)
+    int* tlas_item_parent;    // [n_items] local parent (internal node) of each item leaf
     int* tlas_node_parent;    // [n_tlas_nodes] local parent of each internal node
     int* tlas_depth;          // [n_envs] depth of each env's TLAS (written by build)
     int n_envs;
-    int max_n;                // max instances in one env (sizes shared memory)
+    int max_n;                // max items in one env (sizes shared memory)
     int builder;              // 0: LBVH (Morton + Karras), 1: binned SAH (default)
 };
-cudaError_t instances_update(const TlasArgs& a, int n_inst, cudaStream_t stream);
+cudaError_t items_update(const TlasArgs& a, int n_items, cudaStream_t stream);
 cudaError_t tlas_build(const TlasArgs& a, bool rebuild, cudaStream_t stream);
 
 // Casts.  Model: 0 rays, 1 pinhole, 2 beams.

@@ -882,7 +882,7 @@ __global__ void k_pack_tris(const BlasSeg* segs, const int* seg_of, const uint32
     const BlasSeg& S = segs[c.s];
     if (dbg_morton) dbg_morton[S.leaf_base + p] = sk[g];
     if (p >= c.n) return;
-    const int f = (int)sorted_all[g] - c.off;  // asset-local face id
+    const int f = (int)sorted_all[g] - c.off;  // segment-local face
     const float* a = S.verts + 3 * S.faces[3 * f];
     const float* b = S.verts + 3 * S.faces[3 * f + 1];
     const float* cc = S.verts + 3 * S.faces[3 * f + 2];
@@ -897,7 +897,9 @@ __global__ void k_pack_tris(const BlasSeg* segs, const int* seg_of, const uint32
     int gl = S.leaf_base + p;
     tris[3 * gl + 0] = make_float4(a[0], a[1], a[2], inv_min_alt);
     tris[3 * gl + 1] = make_float4((float)E1.x, (float)E1.y, (float)E1.z, (float)two_area);
-    tris[3 * gl + 2] = make_float4((float)E2.x, (float)E2.y, (float)E2.z, __int_as_float(f));
+    // the asset-local face id (a part's faces are a subset of its asset's)
+    const int face_id = S.face_ids ? S.face_ids[f] : f;
+    tris[3 * gl + 2] = make_float4((float)E2.x, (float)E2.y, (float)E2.z, __int_as_float(face_id));
     for (int k = 0; k < 3; ++k) {
         triv[9 * gl + k] = a[k];
         triv[9 * gl + 3 + k] = b[k];
@@ -911,7 +913,7 @@ __global__ void k_asset_info(const BlasSeg* segs, int B, const uint32_t* bounds,
     if (s >= B) return;
     const BlasSeg& S = segs[s];
     const int n = (int)bounds[8 * s + 7];
-    AssetInfo a;
+    BlasInfo a;
     a.node_base = S.node_base;
     a.leaf_base = S.leaf_base;
     a.n_leaves = n;

@@ -182,8 +182,11 @@ __device__ __forceinline__ void consider64(const SceneView& sv, int inst, int le
 __device__ __noinline__ void brute64(SceneView sv, int env, Ray64 r64, double tmax, Best64* best) {
     Best64 b = *best;
     for (int inst = __ldg(sv.env_off + env); inst < __ldg(sv.env_off + env + 1); ++inst) {
-        const AssetInfo& as = sv.assets[__ldg(sv.inst_asset + inst)];
-        for (int l = 0; l < as.n_leaves; ++l) consider64(sv, inst, as.leaf_base + l, r64, tmax, b);
+        const int a = __ldg(sv.inst_asset + inst);
+        for (int p = __ldg(sv.part_off + a); p < __ldg(sv.part_off + a + 1); ++p) {
+            const BlasInfo& bl = sv.parts[p];
+            for (int l = 0; l < bl.n_leaves; ++l) consider64(sv, inst, bl.leaf_base + l, r64, tmax, b);
+        }
     }
     *best = b;
 }
@@ -270,20 +273,20 @@ struct RayState {
         cur_inst = -1;
     }
 
-    // TLAS leaf: move the ray into instance `inst`'s object space; returns the
-    // BLAS root node.
-    __device__ __forceinline__ int enter_instance(const SceneView& sv, int inst) {
+    // TLAS leaf: move the ray into the object space of item `item` (an
+    // instance's part); returns the part's BLAS root node.
+    __device__ __forceinline__ int enter_instance(const SceneView& sv, int item) {
         f3 oo, od;
         float delta;
-        const int root = enter_object(sv, inst, oo, od, delta);
+        const int root = enter_object(sv, item, oo, od, delta);
         sr = make_slab(oo, od, delta);
         return root;
     }
 
     // enter_instance without the per-lane box-test state (interval packets
     // build their own): object-space ray, its error bound, cold columns.
-    __device__ __forceinline__ int enter_object(const SceneView& sv, int inst, f3& oo_, f3& od_, float& delta_) {
-        const float4* rp = sv.irec + 4 * inst;
+    __device__ __forceinline__ int enter_object(const SceneView& sv, int item, f3& oo_, f3& od_, float& delta_) {
+        const float4* rp = sv.irec + 4 * item;
         float4 r0 = __ldg(rp), r1 = __ldg(rp + 1), r2 = __ldg(rp + 2), r3 = __ldg(rp + 3);
         const f3 o = this->o(), d = this->d();
         const float q = c.f(C_Q);
@@ -300,7 +303,7 @@ struct RayState {
         c.f(C_DELTA) = delta;
         const float dd = dot(od, od);
         c.f(C_DLEN) = dd > 0.0f ? dd * rsqrt_approx_ftz(dd) * 1.000001f : 0.0f;
-        cur_inst = inst;
+        cur_inst = __float_as_int(r3.w);  // the item's instance (FP64 tests, face offset, label)
         oo_ = oo;
         od_ = od;
         delta_ = delta;
@@ -1045,10 +1048,13 @@ __device__ __noinline__ bool shadow_brute64(const CastArgs* a, int env, double t
     const double L = shadow_ray64<MODEL>(a, env, id.sensor, id.col, id.row, t_hit, sr);
     const double eps = (double)a->stereo_eps;
     for (int inst = __ldg(a->sv.env_off + env); inst < __ldg(a->sv.env_off + env + 1); ++inst) {
-        const AssetInfo& as = a->sv.assets[__ldg(a->sv.inst_asset + inst)];
-        for (int l = 0; l < as.n_leaves; ++l) {
-            double t;
-            if (tri64(a->sv, inst, as.leaf_base + l, sr, t) && t > eps && t < L - eps) return true;
+        const int as = __ldg(a->sv.inst_asset + inst);
+        for (int p = __ldg(a->sv.part_off + as); p < __ldg(a->sv.part_off + as + 1); ++p) {
+            const BlasInfo& bl = a->sv.parts[p];
+            for (int l = 0; l < bl.n_leaves; ++l) {
+                double t;
+                if (tri64(a->sv, inst, bl.leaf_base + l, sr, t) && t > eps && t < L - eps) return true;
+            }
         }
     }
     return false;

@@ -7,7 +7,8 @@
 // rays are moved into object space instead, and each env
 // gets a TLAS over its instance boxes (north_star: "a per-env TLAS over
 // instances, refit in place when obstacles are re-posed").
-//   K6 k_instances   inverse affine (FP64 -> FP32), conservative world box
+//   K6 k_items       per TLAS item (instance, part): inverse affine (FP64 ->
+//                    FP32), conservative world box of the part
 //   K7 k_tlas        (rebuild) per-env Morton sort + Karras + fit, one CTA/env
 //   K8 k_tlas        (refit)   same CTA shape, stored topology, boxes only
 #include "agr_internal.cuh"
@@ -21,12 +22,16 @@ constexpr int TLAS_THREADS = 256;
 
 __device__ __forceinline__ float inf_f() { return __int_as_float(0x7f800000); }
 
-// ---- K6: per-instance record and world box ------------------------------------
-__global__ void k_instances(TlasArgs a, int n_inst) {
+// ---- K6: per-item record and world box -----------------------------------------
+// Item i = part item_part[i] of instance item_inst[i]: the instance's inverse
+// transform (recomputed per part: a few FP64 flops) and the world box of the
+// part's BLAS.
+__global__ void k_items(TlasArgs a, int n_items) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n_inst) return;
-    const float* T = a.inst_T + 12 * i;
-    const AssetInfo& as = a.assets[a.inst_asset[i]];
+    if (i >= n_items) return;
+    const int inst = a.item_inst[i];
+    const float* T = a.inst_T + 12 * inst;
+    const BlasInfo& as = a.parts[a.item_part[i]];
     double A[3][3], b[3];
     for (int r = 0; r < 3; ++r) {
         for (int c = 0; c < 3; ++c) A[r][c] = T[4 * r + c];
@@ -37,7 +42,7 @@ __global__ void k_instances(TlasArgs a, int n_inst) {
     double c02 = A[1][0] * A[2][1] - A[1][1] * A[2][0];
     double det = A[0][0] * c00 + A[0][1] * c01 + A[0][2] * c02;
     float4* rec = a.irec + 4 * i;
-    float* box = a.inst_box + 6 * i;
+    float* box = a.item_box + 6 * i;
     bool ok = det != 0.0 && isfinite(det) && as.n_leaves > 0;
     if (!ok) {
         // singular transform or an all-degenerate asset: the instance is never
@@ -67,7 +72,8 @@ __global__ void k_instances(TlasArgs a, int n_inst) {
     }
     double nAinv = sqrt(nrm2) * (1.0 + 1e-6);
     double err_off = nAinv * b1 + (double)as.radius;
-    rec[3] = make_float4(__int_as_float(as.node_base), (float)nAinv, (float)(err_off * (1.0 + 1e-6)), 0.f);
+    rec[3] = make_float4(__int_as_float(as.node_base), (float)nAinv, (float)(err_off * (1.0 + 1e-6)),
+                         __int_as_float(inst));
     // conservative world box: the union of the transformed boxes of the
     // BLAS's second BVH4 level (up to 16 boxes; much tighter than the
     // transformed root box under rotation), each in centre/extent form and
@@ -342,8 +348,8 @@ __device__ void sah_build_cta(const TlasSmem& s, int n) {
 __global__ void k_tlas(TlasArgs a, int rebuild) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int e = blockIdx.x;
-    const int i0 = a.env_off[e];
-    const int n = a.env_off[e + 1] - i0;
+    const int i0 = a.item_off[e];
+    const int n = a.item_off[e + 1] - i0;
     const int nodebase = a.nb_blas + a.tlas_off[e];
     const int toff = a.tlas_off[e];
     const int tid = threadIdx.x;
@@ -356,9 +362,9 @@ __global__ void k_tlas(TlasArgs a, int rebuild) {
             for (int c = 0; c < 4; ++c)
                 for (int k = 0; k < 6; ++k) b[c][k] = EMPTY[k];
             if (n == 1) {
-                slot_box(a.inst_box + 6 * i0, b[0]);
+                slot_box(a.item_box + 6 * i0, b[0]);
                 refs[0] = ~i0;
-                a.tlas_inst_parent[i0] = 0;
+                a.tlas_item_parent[i0] = 0;
             }
             write_node4(a.nodes, nodebase, b, refs, n);
             a.tlas_node_parent[toff] = -1;
@@ -380,7 +386,7 @@ __global__ void k_tlas(TlasArgs a, int rebuild) {
     s.flags = (int*)p;
 
     for (int i = tid; i < n; i += blockDim.x)
-        for (int k = 0; k < 6; ++k) s.box[6 * i + k] = a.inst_box[6 * (i0 + i) + k];
+        for (int k = 0; k < 6; ++k) s.box[6 * i + k] = a.item_box[6 * (i0 + i) + k];
     for (int j = tid; j < n - 1; j += blockDim.x) s.flags[j] = 0;
     __syncthreads();
 
@@ -477,7 +483,7 @@ __global__ void k_tlas(TlasArgs a, int rebuild) {
             a.tlas_child[2 * (toff + j) + 1] = s.child[2 * j + 1];
             a.tlas_node_parent[toff + j] = s.nparent[j];
         }
-        for (int i = tid; i < n; i += blockDim.x) a.tlas_inst_parent[i0 + i] = s.lparent[i];
+        for (int i = tid; i < n; i += blockDim.x) a.tlas_item_parent[i0 + i] = s.lparent[i];
         // depth: longest leaf-to-root path
         int dmax = 0;
         for (int i = tid; i < n; i += blockDim.x) {
@@ -493,7 +499,7 @@ __global__ void k_tlas(TlasArgs a, int rebuild) {
             s.child[2 * j + 1] = a.tlas_child[2 * (toff + j) + 1];
             s.nparent[j] = a.tlas_node_parent[toff + j];
         }
-        for (int i = tid; i < n; i += blockDim.x) s.lparent[i] = a.tlas_inst_parent[i0 + i];
+        for (int i = tid; i < n; i += blockDim.x) s.lparent[i] = a.tlas_item_parent[i0 + i];
         __syncthreads();
     }
 
@@ -550,8 +556,8 @@ size_t tlas_smem_bytes(int n) {
 
 }  // namespace
 
-cudaError_t instances_update(const TlasArgs& a, int n_inst, cudaStream_t stream) {
-    if (n_inst > 0) k_instances<<<(n_inst + 127) / 128, 128, 0, stream>>>(a, n_inst);
+cudaError_t items_update(const TlasArgs& a, int n_items, cudaStream_t stream) {
+    if (n_items > 0) k_items<<<(n_items + 127) / 128, 128, 0, stream>>>(a, n_items);
     return cudaGetLastError();
 }
 

@@ -13,8 +13,8 @@ def dev():
     return torch.device("cuda", 0)
 
 
-def make_scene(sc, transforms=None, build=True, trbvh_rounds=3):
-    s = agr.Scene.from_scenegen(sc, device=0, trbvh_rounds=trbvh_rounds)
+def make_scene(sc, transforms=None, build=True, trbvh_rounds=3, parts=True):
+    s = agr.Scene.from_scenegen(sc, device=0, trbvh_rounds=trbvh_rounds, parts=parts)
     T = sc.inst_T if transforms is None else transforms
     if s.n_inst:
         s.set_instance_transforms(torch.from_numpy(np.ascontiguousarray(T, np.float32)).to(dev()))

@@ -17,7 +17,7 @@ def test_library_loads_and_exports_header_symbols():
     assert len(syms) >= 18
     for name in syms:
         assert hasattr(lib, name), name
-    assert agr.abi_version() == 3
+    assert agr.abi_version() == 4
 
 
 def test_exports_match_nm():

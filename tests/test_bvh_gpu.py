@@ -35,7 +35,7 @@ def test_morton_ref_known_values():
 def _check_blas(mesh):
     """Plain LBVH (no treelet restructuring): the Karras topology is checked."""
     sc = sg.assemble([mesh], [[(0, 0, sg.make_T(np.eye(3), (0, 0, 0)))]])
-    s = make_scene(sc, build=False, trbvh_rounds=0)
+    s = make_scene(sc, build=False, trbvh_rounds=0, parts=False)
     nodes, leaf_face, codes = s.debug_export_blas(0)
     v = mesh.verts
     tri = v[mesh.faces]
@@ -150,7 +150,7 @@ def test_large_mesh_multiblock_sort():
     """A mesh big enough for a multi-block radix sort (> 1024 keys per tile)."""
     m = sg.sphere_mesh(2.0, 5)  # 20480 faces
     sc = sg.assemble([m], [[(0, 0, sg.make_T(np.eye(3), (0, 0, 0)))]])
-    s = make_scene(sc, build=False)
+    s = make_scene(sc, build=False, parts=False)
     nodes, leaf_face, codes = s.debug_export_blas(0)
     assert sorted(leaf_face.tolist()) == list(range(len(m.faces)))
     assert np.all(np.diff(codes.astype(np.int64)) >= 0)
@@ -207,7 +207,7 @@ def _walk_bvh4(nodes, root, leaf_boxes=None, blas=True):
 def test_bvh4_blas_covers_every_leaf_once(mesh_fn):
     mesh = mesh_fn()
     sc = sg.assemble([mesh], [[(0, 0, sg.make_T(np.eye(3), (0, 0, 0)))]])
-    s = make_scene(sc, build=False)
+    s = make_scene(sc, build=False, parts=False)
     _, leaf_face, _ = s.debug_export_blas(0)
     nodes, root = s.debug_export_bvh4(0)
     tri = mesh.verts[mesh.faces]
@@ -259,7 +259,7 @@ def test_trbvh_keeps_leaves_and_boxes_and_lowers_sah(mesh_fn):
     costs = {}
     for rounds in (0, 3):
         sc = sg.assemble([mesh], [[(0, 0, sg.make_T(np.eye(3), (0, 0, 0)))]])
-        s = make_scene(sc, build=False, trbvh_rounds=rounds)
+        s = make_scene(sc, build=False, trbvh_rounds=rounds, parts=False)
         nodes, leaf_face, _ = s.debug_export_blas(0)
         refs = nodes[:, 12:14].view(np.int32)
         seen = []

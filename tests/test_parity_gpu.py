@@ -830,3 +830,106 @@ def test_singular_instance_keeps_tlas_boxes_tight():
         ref = oracle.cast(sc, oracle_rays(sensor, "depth"))
         compare(ref, got["dist"], got["seg"], got["face"], f"singular instances, builder {builder}")
         assert set(np.unique(got["seg"])) <= {-1, 1, 3}
+
+
+# ---- asset parts: one BLAS per connected-component group ---------------
+
+def _faces_sharing_a_vertex_share_a_part(mesh, part):
+    first = {}
+    for f, tri in enumerate(mesh.faces):
+        for v in tri:
+            if int(v) in first and part[first[int(v)]] != part[f]:
+                return False
+            first.setdefault(int(v), f)
+    return True
+
+
+def test_asset_parts_partition():
+    """A tree (open trunk + canopy: two connected components whose boxes
+    fill far less than their union box) is split into 2 BLAS parts; a face
+    never leaves its component's part; single-component assets and triangle
+    soups (> 64 components) stay whole; part_policy 1 never splits."""
+    rng = np.random.default_rng(1)
+    tree = sg.tree_mesh(rng)
+    rock = sg.rock_mesh(rng)
+    tris = rng.uniform(-1, 1, (80, 3, 3)).astype(np.float32)
+    soup = sg.Mesh("soup", tris.reshape(-1, 3), np.arange(240, dtype=np.int32).reshape(-1, 3))
+    meshes = [tree, rock, sg.cube_mesh(), soup]
+    sc = sg.assemble(meshes, [[(a, a + 1, sg.make_T(np.eye(3), (3.0 * a, 0, 0))) for a in range(4)]])
+    s = make_scene(sc)
+    n, part = s.debug_asset_parts(0, len(tree.faces))
+    assert n == 2 and set(part.tolist()) == {0, 1}
+    assert _faces_sharing_a_vertex_share_a_part(tree, part)
+    trunk = part == part[0]
+    assert trunk.sum() == 32 and (~trunk).sum() == 1280  # 16-segment trunk, icosphere-3 canopy
+    for a in (1, 2, 3):
+        assert s.debug_asset_parts(a, len(meshes[a].faces))[0] == 1, a
+    info = s.info()
+    assert info["n_parts"] == 5 and info["n_items"] == 5
+    with pytest.raises(agr.AgrError, match="parts"):
+        s.debug_export_blas(0)
+    whole = make_scene(sc, parts=False)
+    assert whole.debug_asset_parts(0, len(tree.faces))[0] == 1
+    assert whole.info()["n_items"] == 4
+
+
+@pytest.mark.parametrize("builder", [0, 1])
+def test_parts_equal_whole_asset_bitwise(builder):
+    """Splitting assets into parts changes only the acceleration structure:
+    c3-shaped envs cast with and without parts give bitwise identical
+    depth, seg, face, normals and barycentrics, after a rebuild and after a
+    refit with new poses, in packet and per-lane traversal; and match the
+    oracle."""
+    sc, sensor = sg.config3(n_envs=8)
+    chans = ("dist", "seg", "face", "normal", "bary")
+    out = {}
+    for parts in (True, False):
+        s = make_scene(sc, build=False, parts=parts)
+        s.set_tlas_builder(builder)
+        s.build()
+        a = to_np(cast_sensor(s, sensor, "depth", channels=chans))
+        T2 = sc.inst_T.copy()
+        T2[:, :2, 3] += np.random.default_rng(4).uniform(-0.5, 0.5, (len(T2), 2)).astype(np.float32)
+        s.set_instance_transforms(torch.from_numpy(T2).to(dev()))
+        s.refit()
+        b = to_np(cast_sensor(s, sensor, "range", channels=chans))
+        s.set_traversal(1)
+        c = to_np(cast_sensor(s, sensor, "range", channels=chans))
+        out[parts] = (a, b, c, s.info())
+    for i in range(3):
+        for k in chans:
+            assert np.array_equal(out[True][i][k].view(np.uint32), out[False][i][k].view(np.uint32)), (i, k)
+    assert out[True][3]["n_items"] == out[False][3]["n_items"] + 40 * 8  # every tree: trunk + canopy
+    q = np.random.default_rng(12).choice(len(out[True][0]["dist"]), 20000, replace=False)
+    ref = oracle.cast(sc, oracle_rays(sensor, "depth"), query=q)
+    compare(ref, out[True][0]["dist"][q], out[True][0]["seg"][q], out[True][0]["face"][q], "c3 parts")
+
+
+def test_parts_update_mesh_stereo_and_exact():
+    """A split asset (tree) deformed by agr_update_mesh rebuilds both part
+    BLAS and the item boxes; stereo shadows and exact mode run over parts;
+    everything matches the oracle / the filter bitwise."""
+    rng = np.random.default_rng(6)
+    tree = sg.tree_mesh(rng)
+    per_env = [[(0, 1, sg.make_T(sg.rot_z(0.3 * e), (4.0, 0.5 * e - 1, -2.5))),
+                (1, 2, sg.make_T(np.eye(3), (9.0, 0, 0)))] for e in range(4)]
+    sc = sg.assemble([tree, sg.cube_mesh(4.0)], per_env)
+    cam = sg.pinhole(96, 64, 90.0)
+    sensor = dict(kind="pinhole", cam=cam, poses=sg.identity_poses(4), max_range=12.0)
+    s = make_scene(sc)
+    assert s.info()["n_parts"] == 3
+    v = tree.verts.astype(np.float64) * 1.1 + rng.uniform(-0.05, 0.05, tree.verts.shape)
+    vf = v.astype(np.float32)
+    s.update_mesh(0, torch.from_numpy(vf).to(dev()))
+    s.build()
+    sc2 = sg.assemble([sg.Mesh("t", vf, tree.faces), sg.cube_mesh(4.0)], per_env)
+    s.set_stereo((0.0, -0.3, 0.0), 1e-4)
+    got = to_np(cast_sensor(s, sensor, "depth", channels=("dist", "seg", "face", "valid")))
+    ref = oracle.cast(sc2, oracle_rays(sensor, "depth"), stereo=((0.0, -0.3, 0.0), 1e-4))
+    compare(ref, got["dist"], got["seg"], got["face"], "tree parts after update")
+    assert valid_compare(ref, got["valid"], "tree parts stereo") > 50
+    assert (got["seg"] == 1).sum() > 500
+    s.set_exact_mode(True)
+    ex = to_np(cast_sensor(s, sensor, "depth", channels=("dist", "seg", "face", "valid")))
+    for k in got:
+        assert np.array_equal(got[k], ex[k]), k
