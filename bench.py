@@ -104,10 +104,11 @@ def parse(argv=None):
     ap.add_argument("--tlas-step", default=None, choices=["build", "refit"],
                     help="per-step TLAS update (default: refit for c3/c4, whose obstacles "
                          "keep their poses; rebuild for c5, re-posed every step)")
-    ap.add_argument("--traversal", default=None, choices=["auto", "lane"],
+    ap.add_argument("--traversal", default=None, choices=["auto", "lane", "packet4"],
                     help="auto: warp packets for camera / LiDAR tiles; lane: one ray per lane "
                          "(default: lane for c6, whose terrain seen at grazing angles makes a "
-                         "4x8 packet test ~9x the triangles its rays need; auto elsewhere)")
+                         "4x8 packet test ~9x the triangles its rays need; auto elsewhere); "
+                         "packet4: the interval packets on the 4-wide nodes (A/B)")
     ap.add_argument("--no-parts", action="store_true",
                     help="one BLAS per asset (agr_create_options.part_policy 1) instead of splitting "
                          "multi-component assets (trees: trunk + canopy) into parts")
@@ -427,7 +428,8 @@ class Workload:
         self.scene = agr.Scene.from_scenegen(sc, device=dev.index, trbvh_rounds=self.trbvh_rounds,
                                              parts=not args.no_parts)
         self.traversal = args.traversal or ("lane" if cfg == 6 else "auto")
-        self.scene.set_traversal(0 if self.traversal == "auto" else 1)
+        self.mode = {"auto": 0, "lane": 1, "packet4": 2}[self.traversal]
+        self.scene.set_traversal(self.mode)
         self.tlas_builder = args.tlas_builder or ("lbvh" if cfg in (5, 6) else "sah")
         self.scene.set_tlas_builder(1 if self.tlas_builder == "sah" else 0)
         self.step_refit = (args.tlas_step or ("build" if cfg in (5, 6) else "refit")) == "refit"
@@ -564,7 +566,7 @@ def main():
         wl.step(0, stream)
         torch.cuda.synchronize()
         lane_counters = scene.counters()
-        scene.set_traversal(0 if wl.traversal == "auto" else 1)
+        scene.set_traversal(wl.mode)
         scene.enable_counters(False)
 
     # ---- end to end through the public C ABI with host buffers ------------

@@ -191,7 +191,14 @@ typedef struct {
                              Results are identical either way (the BVH only
                              accelerates the plain definition).
                              1: one BLAS per asset.                          */
-    int32_t reserved[6];  /* must be 0                                        */
+    int32_t node_width;   /* 0 (default) or 8: besides the 4-wide BVH every
+                             traversal uses, keep an 8-wide copy of every BLAS
+                             and TLAS (256-B nodes) for the interval-packet
+                             camera / LiDAR traversal (about half the node
+                             visits); 4: BVH4 only (half the node memory and
+                             no BVH8 collapse in builds / refits -- for
+                             scenes cast one ray per lane).                  */
+    int32_t reserved[5];  /* must be 0                                        */
 } agr_create_options;
 
 agr_status agr_scene_create_ex(int32_t device, const agr_mesh* meshes, int32_t n_meshes,
@@ -351,9 +358,11 @@ agr_status agr_set_tlas_builder(agr_scene scene, int32_t builder);
  * node is visited when the interval of the tile's ray directions may reach
  * a child, and every lane still tests each visited leaf on its own ray;
  * stereo shadow segments, whose origins differ per lane, visit the union
- * of the lanes' own box tests), 1 = one independent ray per lane (faster
- * when a tile's rays diverge, e.g. terrain seen at grazing angles).
- * Explicit rays always use 1.
+ * of the lanes' own box tests; on the 8-wide node copy when it exists,
+ * agr_create_options.node_width), 1 = one independent ray per lane (faster
+ * when a tile's rays diverge, e.g. terrain seen at grazing angles), 2 = the
+ * packets of mode 0 on the 4-wide nodes (comparison / testing).
+ * Explicit rays always use 1.  EINVAL outside 0..2.
  */
 agr_status agr_set_traversal(agr_scene scene, int32_t mode);
 

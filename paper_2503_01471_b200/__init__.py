@@ -66,7 +66,7 @@ CHANNELS = {"dist": ("float32", None), "seg": ("int32", None), "face": ("int32",
 
 class agr_create_options(ctypes.Structure):
     _fields_ = [("trbvh_rounds", ctypes.c_int32), ("part_policy", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 6)]
+                ("node_width", ctypes.c_int32), ("reserved", ctypes.c_int32 * 5)]
 
 
 class agr_scene_info(ctypes.Structure):
@@ -175,11 +175,12 @@ class Scene:
     """Owner of an ``agr_scene`` handle (one CUDA device)."""
 
     def __init__(self, meshes, env_offsets, inst_asset, inst_label, device: int = 0,
-                 trbvh_rounds: int = 3, parts: bool = True):
+                 trbvh_rounds: int = 3, parts: bool = True, node_width: int = 0):
         """meshes: list of (verts float32 [V][3], faces int32 [F][3]) host arrays.
         trbvh_rounds: treelet-restructuring passes on every BLAS (0 = LBVH).
         parts: split multi-component assets into BLAS parts when it pays
-        (agr_create_options.part_policy 0); False: one BLAS per asset."""
+        (agr_create_options.part_policy 0); False: one BLAS per asset.
+        node_width: 0/8 also keep the BVH8 copy for interval packets, 4 BVH4 only."""
         lib = load()
         self._keep = []
         arr = (agr_mesh * len(meshes))()
@@ -196,7 +197,7 @@ class Scene:
         for j in range(n_inst):
             inst[j] = agr_instance(int(ia[j]), int(il[j]))
         h = _P()
-        opts = agr_create_options(int(trbvh_rounds), 0 if parts else 1)
+        opts = agr_create_options(int(trbvh_rounds), 0 if parts else 1, int(node_width))
         _check(lib.agr_scene_create_ex(device, arr, len(meshes), len(env_offsets) - 1,
                                        env_offsets.ctypes.data, inst, ctypes.byref(opts), ctypes.byref(h)))
         self._keep = []
@@ -207,10 +208,11 @@ class Scene:
         self.n_inst = n_inst
 
     @classmethod
-    def from_scenegen(cls, sc, device: int = 0, trbvh_rounds: int = 3, parts: bool = True):
+    def from_scenegen(cls, sc, device: int = 0, trbvh_rounds: int = 3, parts: bool = True,
+                      node_width: int = 0):
         """Build from a ``scenegen.Scene`` (inputs only; no arithmetic)."""
         return cls([(m.verts, m.faces) for m in sc.meshes], sc.env_off, sc.inst_asset,
-                   sc.inst_label, device, trbvh_rounds, parts)
+                   sc.inst_label, device, trbvh_rounds, parts, node_width)
 
     def close(self):
         if getattr(self, "handle", None):
@@ -359,7 +361,8 @@ class Scene:
         _check(load().agr_set_tlas_builder(self.handle, int(builder)))
 
     def set_traversal(self, mode: int):
-        """0 auto (warp packets for pinhole / beam tiles), 1 per-lane rays."""
+        """0 auto (interval packets for pinhole / beam tiles, BVH8 when built),
+        1 per-lane rays, 2 interval packets on the BVH4."""
         _check(load().agr_set_traversal(self.handle, int(mode)))
 
     def enable_counters(self, enable: bool):

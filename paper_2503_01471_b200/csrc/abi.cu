@@ -82,6 +82,7 @@ struct agr_scene_s {
     size_t device_bytes = 0;
     // device arrays
     float4* nodes = nullptr;   // BVH4 (BLAS then TLAS), 8 float4 per node
+    float4* nodes8 = nullptr;  // BVH8 copy (same numbering), 16 float4 per node, or null
     float4* bnodes = nullptr;  // binary BLAS nodes, 4 float4 per node (debug export)
     float4* tris = nullptr;
     float* triv = nullptr;
@@ -124,7 +125,8 @@ struct agr_scene_s {
     int exact = 0;
     float stereo[3] = {0.0f, -0.095f, 0.0f};
     float stereo_eps = 1e-4f;
-    int traversal = 0;  // 0 auto (warp packets for pinhole / beams), 1 per-lane
+    int traversal = 0;  // 0 auto (interval packets for pinhole / beams, on the BVH8 if built),
+                        // 1 per-lane, 2 interval packets on the BVH4
     int tlas_builder = 0;  // 0 LBVH (default), 1 binned SAH
     bool counting = false;
     // end-to-end staging (lazily allocated)
@@ -157,6 +159,7 @@ struct agr_scene_s {
     SceneView view() const {
         SceneView v;
         v.nodes = nodes;
+        v.nodes8 = nodes8;
         v.tris = tris;
         v.triv = triv;
         v.irec = irec;
@@ -180,6 +183,7 @@ struct agr_scene_s {
     TlasArgs tlas_args() const {
         TlasArgs a;
         a.nodes = nodes;
+        a.nodes8 = nodes8;
         a.irec = irec;
         a.item_box = item_box;
         a.inst_T = inst_T;
@@ -245,6 +249,7 @@ static cudaError_t build_assets(agr_scene_s* s, const int* assets, int n, cudaSt
     }
     BlasBatchArgs ba;
     ba.nodes = s->nodes;
+    ba.nodes8 = s->nodes8;
     ba.bnodes = binary ? s->bnodes : nullptr;
     ba.tris = s->tris;
     ba.triv = s->triv;
@@ -416,6 +421,8 @@ agr_status agr_scene_create_ex(int32_t device, const agr_mesh* meshes, int32_t n
         return fail(AGR_EINVAL, "trbvh_rounds must be in [0, 16]");
     if (opts && (opts->part_policy < 0 || opts->part_policy > 1))
         return fail(AGR_EINVAL, "part_policy must be 0 (auto) or 1 (one BLAS per asset)");
+    if (opts && opts->node_width != 0 && opts->node_width != 4 && opts->node_width != 8)
+        return fail(AGR_EINVAL, "node_width must be 0 (default), 4 or 8");
     agr_scene_s* s = new agr_scene_s();
     s->device = device;
     if (opts) s->trbvh_rounds = opts->trbvh_rounds;
@@ -518,6 +525,7 @@ agr_status agr_scene_create_ex(int32_t device, const agr_mesh* meshes, int32_t n
     } while (0)
 
     CKB(s->alloc(&s->nodes, 8 * (size_t)(nb + nt)));
+    if (!opts || opts->node_width != 4) CKB(s->alloc(&s->nodes8, (size_t)NODE8_F4 * (nb + nt)));
     CKB(s->alloc(&s->bnodes, 4 * (size_t)nb));
     CKB(s->alloc(&s->tris, 3 * (size_t)nl));
     CKB(s->alloc(&s->triv, 9 * (size_t)nl));
@@ -786,7 +794,8 @@ static agr_status check_cast_state(agr_scene s, float max_range, const agr_outpu
 static agr_status run_cast(agr_scene s, CastArgs& a, cudaStream_t st) {
     a.sv = s->view();
     a.exact = s->exact;
-    a.packet = s->traversal == 0 ? 1 : 0;
+    a.packet = s->traversal != 1 ? 1 : 0;
+    a.wide = s->traversal == 0 && s->nodes8 ? 1 : 0;
     a.counters = nullptr;
     if (s->counting) {
         CK(cudaMemsetAsync(s->counters, 0, sizeof(unsigned long long) * 8, st));
@@ -976,7 +985,8 @@ static agr_status e2e_run(agr_scene s, CastArgs& a, int64_t elems_per_env, agr_o
         c.out_annot = (float*)dev[7];
         c.sv = s->view();
         c.exact = s->exact;
-        c.packet = s->traversal == 0 ? 1 : 0;
+        c.packet = s->traversal != 1 ? 1 : 0;
+        c.wide = s->traversal == 0 && s->nodes8 ? 1 : 0;
         c.counters = nullptr;
         CK(cast_launch(c, cs));
         CK(cudaEventRecord(s->e2e_event[slot], cs));
@@ -1109,7 +1119,7 @@ agr_status agr_set_tlas_builder(agr_scene s, int32_t builder) {
 agr_status agr_set_traversal(agr_scene s, int32_t mode) {
     g_err.clear();
     if (!s) return fail(AGR_EINVAL, "scene is NULL");
-    if (mode != 0 && mode != 1) return fail(AGR_EINVAL, "traversal mode must be 0 or 1");
+    if (mode < 0 || mode > 2) return fail(AGR_EINVAL, "traversal mode must be 0, 1 or 2");
     s->traversal = mode;
     return AGR_OK;
 }

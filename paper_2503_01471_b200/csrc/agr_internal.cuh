@@ -76,7 +76,8 @@ struct BlasInfo {
 
 // Read-only view of a scene passed by value to kernels.
 struct SceneView {
-    const float4* nodes;      // [n_nodes][4]
+    const float4* nodes;      // [n_nodes][8] BVH4
+    const float4* nodes8;     // [n_nodes][16] BVH8 (same numbering), or null
     const float4* tris;       // [n_leaves][3]
     const float* triv;        // [n_leaves][9]
     const float4* irec;       // [n_items][4] (TLAS leaf ~item)
@@ -153,19 +154,22 @@ AGR_HD float half_area(const float b[6]) {
     return dx * dy + dy * dz + dz * dx;
 }
 
-// Greedy collapse of binary node j into up to 4 children: repeatedly open the
-// internal child with the largest surface area (the SAH's choice), keeping
-// the children in left-to-right (Morton) order.  Refs are local: >= 0 binary
-// internal node, < 0 leaf.  child(r, side) and box(r, b[6]) read the binary
-// tree.  Returns the number of children; unused refs are REF_EMPTY.
-template <class CHILD, class BOX>
-__device__ __forceinline__ int collapse4(int j, const CHILD& child, const BOX& box, int refs[4],
-                                         bool keep_pairs = false) {
+// Greedy collapse of binary node j into up to W children (W = 4: the BVH4 of
+// every traversal mode; W = 8: the BVH8 of the interval-packet traversal):
+// repeatedly open the internal child with the largest surface area (the
+// SAH's choice), keeping the children in left-to-right (Morton) order.  Refs
+// are local: >= 0 binary internal node, < 0 leaf.  child(r, side) and box(r,
+// b[6]) read the binary tree.  Returns the number of children; unused refs
+// are REF_EMPTY.
+template <int W, class CHILD, class BOX>
+__device__ __forceinline__ int collapse_w(int j, const CHILD& child, const BOX& box, int refs[W],
+                                          bool keep_pairs = false) {
     refs[0] = child(j, 0);
     refs[1] = child(j, 1);
-    refs[2] = refs[3] = REF_EMPTY;
+#pragma unroll
+    for (int k = 2; k < W; ++k) refs[k] = REF_EMPTY;
     int cnt = 2;
-    while (cnt < 4) {
+    while (cnt < W) {
         int best = -1;
         float best_a = -1.0f;
         for (int k = 0; k < cnt; ++k) {
@@ -186,6 +190,22 @@ __device__ __forceinline__ int collapse4(int j, const CHILD& child, const BOX& b
         ++cnt;
     }
     return cnt;
+}
+
+template <class CHILD, class BOX>
+__device__ __forceinline__ int collapse4(int j, const CHILD& child, const BOX& box, int refs[4],
+                                         bool keep_pairs = false) {
+    return collapse_w<4>(j, child, box, refs, keep_pairs);
+}
+
+// BVH8 node (interval-packet traversal), 256 B: child k's record is the 32 B
+// at k: (lo.x, lo.y, lo.z, hi.x), (hi.y, hi.z, ref, -), so lane k of a warp
+// fetches its child with two 128-bit loads and lanes 0-7 read one 256-B line.
+constexpr int NODE8_F4 = 16;  // float4 per BVH8 node
+__device__ __forceinline__ void write_child8(float4* nodes8, int g, int k, const float b[6], int ref) {
+    float4* p = nodes8 + NODE8_F4 * (size_t)g + 2 * k;
+    p[0] = make_float4(b[0], b[1], b[2], b[3]);
+    p[1] = make_float4(b[4], b[5], __int_as_float(ref), 0.0f);
 }
 
 // Writes BVH4 node g: boxes b[k][6] (lo xyz, hi xyz) and global refs.
@@ -220,6 +240,7 @@ struct BlasSeg {
 };
 struct BlasBatchArgs {
     float4* nodes;         // global BVH4 node array
+    float4* nodes8;        // global BVH8 node array (same node numbering), or null
     float4* bnodes;        // global binary BLAS node array (debug export)
     float4* tris;          // global tri record array
     float* triv;           // global exact-vertex array
@@ -235,6 +256,7 @@ cudaError_t blas_build_batch(BlasSeg* h_segs, int n_segs, const BlasBatchArgs& a
 
 struct TlasArgs {
     float4* nodes;            // global node array (TLAS part written)
+    float4* nodes8;           // global BVH8 node array (TLAS part written), or null
     float4* irec;             // [n_items][4] written
     float* item_box;          // [n_items][6] written
     const float* inst_T;      // [n_inst][12]
@@ -286,6 +308,7 @@ struct CastArgs {
     unsigned long long* counters;  // optional [8]
     int exact;
     int packet;           // 1: warp-packet traversal for pinhole / beams tiles
+    int wide;             // 1: interval packets over the BVH8 copy (sv.nodes8)
     // filled by cast_launch: n / d = (n * m) >> s for n < 2^31 (tile decode
     // of tiles_img, tiles_x, S without integer division)
     unsigned div_m[3];

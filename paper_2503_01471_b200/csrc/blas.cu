@@ -813,10 +813,12 @@ __global__ void k_pack_nodes(const BlasSeg* segs, const int* seg_of, const uint3
                global_ref(rb, node_base, leaf_base));
 }
 
-// K5b: BVH4 node j = greedy 4-wide collapse of binary node j.
-__global__ void k_collapse4(const BlasSeg* segs, const int* seg_of, const uint32_t* bounds, int Ftot,
-                            const uint32_t* __restrict__ sorted_all, const float* tri_box, int* child_all,
-                            float* ibox_all, const int* __restrict__ size_all, float4* nodes) {
+// K5b: BVH4 node j = greedy 4-wide collapse of binary node j (every
+// traversal mode); with W = 8 the BVH8 copy of the interval-packet traversal.
+template <int W>
+__global__ void k_collapse(const BlasSeg* segs, const int* seg_of, const uint32_t* bounds, int Ftot,
+                           const uint32_t* __restrict__ sorted_all, const float* tri_box, int* child_all,
+                           float* ibox_all, const int* __restrict__ size_all, float4* nodes) {
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= Ftot) return;
     const SegCtx c = seg_ctx(segs, seg_of, bounds, g);
@@ -825,22 +827,22 @@ __global__ void k_collapse4(const BlasSeg* segs, const int* seg_of, const uint32
     if (j >= n_int) return;
     AGR_SEG_VIEW(c);
     const int node_base = segs[c.s].node_base, leaf_base = segs[c.s].leaf_base;
-    int refs[4];
+    int refs[W];
     int cnt;
     if (n > 1) {
         auto ch = [&](int r, int side) { return __ldg(child + 2 * r + side); };
         auto bx = [&](int r, float bb[6]) {
             for (int k = 0; k < 6; ++k) bb[k] = __ldcg(ibox + 6 * r + k);
         };
-        cnt = collapse4(j, ch, bx, refs, AGR_KEEP_PAIRS != 0);
+        cnt = collapse_w<W>(j, ch, bx, refs, AGR_KEEP_PAIRS != 0);
     } else {
         refs[0] = n == 1 ? ~0 : REF_EMPTY;
-        refs[1] = refs[2] = refs[3] = REF_EMPTY;
+        for (int k = 1; k < W; ++k) refs[k] = REF_EMPTY;
         cnt = n == 1 ? 1 : 0;
     }
-    float boxes[4][6];
-    int gr[4];
-    for (int k = 0; k < 4; ++k) {
+    float boxes[W][6];
+    int gr[W];
+    for (int k = 0; k < W; ++k) {
         child_box(refs[k], sorted_prim, tri_box, ibox, boxes[k]);
         gr[k] = global_ref(refs[k], node_base, leaf_base);
         // (subtree sizes from the fit / TRBVH: only subtrees of <= LEAF_MAX
@@ -869,7 +871,11 @@ __global__ void k_collapse4(const BlasSeg* segs, const int* seg_of, const uint32
                 gr[k] = ~((leaf_base + lmin) | ((nl - 1) << LEAF_SHIFT));
         }
     }
-    write_node4(nodes, node_base + j, boxes, gr, cnt);
+    if (W == 4) {
+        write_node4(nodes, node_base + j, reinterpret_cast<const float(*)[6]>(boxes), gr, cnt);
+    } else {
+        for (int k = 0; k < W; ++k) write_child8(nodes, node_base + j, k, boxes[k], gr[k]);
+    }
 }
 
 __global__ void k_pack_tris(const BlasSeg* segs, const int* seg_of, const uint32_t* bounds, int Ftot,
@@ -1001,8 +1007,11 @@ cudaError_t blas_build_batch(BlasSeg* h_segs, int B, const BlasBatchArgs& a, voi
     if (a.bnodes)
         k_pack_nodes<<<gb, T_BLK, 0, stream>>>(s.segs, s.seg_of, s.bounds, F, sv, s.tri_box, s.child, s.ibox,
                                                a.bnodes);
-    k_collapse4<<<gb, T_BLK, 0, stream>>>(s.segs, s.seg_of, s.bounds, F, sv, s.tri_box, s.child, s.ibox,
-                                          s.size, a.nodes);
+    k_collapse<4><<<gb, T_BLK, 0, stream>>>(s.segs, s.seg_of, s.bounds, F, sv, s.tri_box, s.child, s.ibox,
+                                            s.size, a.nodes);
+    if (a.nodes8)
+        k_collapse<8><<<gb, T_BLK, 0, stream>>>(s.segs, s.seg_of, s.bounds, F, sv, s.tri_box, s.child, s.ibox,
+                                                s.size, a.nodes8);
     k_pack_tris<<<gb, T_BLK, 0, stream>>>(s.segs, s.seg_of, s.bounds, F, sv, sk, a.tris, a.triv,
                                           a.dbg_morton);
     k_asset_info<<<(B + 127) / 128, 128, 0, stream>>>(s.segs, B, s.bounds, s.ibox, s.tri_box, sv, s.depth);

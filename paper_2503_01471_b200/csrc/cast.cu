@@ -711,10 +711,12 @@ __device__ __forceinline__ void iv_recip(float lo, float hi, float& i0, float& i
 }
 
 // Packet box-test state from every lane's ray (o shared by all lanes, d its
-// own, delta its error bound); lanes with (lane & 4) take the centre ray.
+// own, delta its error bound); lanes with (lane & CENTRE_BIT) take the centre
+// ray (BVH4: lanes 4-7, BVH8: lanes 8-15).
+template <int CENTRE_BIT = 4>
 __device__ __forceinline__ PSlab make_pslab(f3 o, f3 d, float delta) {
     const unsigned FULL = 0xFFFFFFFFu;
-    const bool centre = (threadIdx.x & 4) != 0;
+    const bool centre = (threadIdx.x & CENTRE_BIT) != 0;
     const float dcx = __shfl_sync(FULL, d.x, TILE_CENTRE_LANE);
     const float dcy = __shfl_sync(FULL, d.y, TILE_CENTRE_LANE);
     const float dcz = __shfl_sync(FULL, d.z, TILE_CENTRE_LANE);
@@ -864,6 +866,120 @@ __device__ __forceinline__ void traverse_ipacket(const SceneView& sv, int env, R
             ps = make_pslab(oo, od, delta);
             __syncwarp();
             if (child == 0 && lane < 8) pslab_store(ps_obj + role * PS_N, ps);
+            __syncwarp();
+            continue;
+        }
+        if (COUNT) cnt.leaves++;
+        leaf_fn(leaf & LEAF_MASK);
+        if (leaf >> LEAF_SHIFT) {
+            if (COUNT) cnt.leaves++;
+            leaf_fn((leaf & LEAF_MASK) + 1);
+        }
+        Umax = __int_as_float(__reduce_max_sync(FULL, __float_as_int(rs.U)));
+        __syncwarp();
+        ps = pslab_load(ps_obj + role * PS_N);
+        if (sp == 0) break;
+        node = wstack[--sp];
+    }
+}
+
+// Interval-packet traversal of the BVH8 copy (nodes8): lanes 0-7 test
+// child (lane & 7) against the tile's direction interval, lanes 8-15 the same
+// child with the centre ray (the visiting order); lanes 16-31 mirror 0-15.
+// Same conservative interval test as traverse_ipacket -- only the node width
+// differs, so results are bitwise identical (tested) -- with about half the
+// node visits per tile.  The hit children are ranked by the centre ray's
+// entry distance (each lane counts the nearer keys of the 8, ties by child
+// index) and pushed farthest first by their own lanes in one store.
+template <bool COUNT, class LEAF>
+__device__ __forceinline__ void traverse_ipacket8(const SceneView& sv, int env, RayState& rs,
+                                                  const LEAF& leaf_fn, int* wstack, float* ps_env,
+                                                  float* ps_obj, Counters& cnt) {
+    const unsigned FULL = 0xFFFFFFFFu;
+    const int lane = threadIdx.x & 31;
+    const int child = lane & 7;
+    const int role = (lane >> 3) & 1;
+    const bool slot_lane = lane < 8;  // lanes owning child slots for ordering / pushes
+    PSlab ps = make_pslab<8>(rs.o(), rs.d(), K_ERR * rs.c.f(C_Q));
+    if (child == 0 && lane < 16) pslab_store(ps_env + role * PS_N, ps);
+    __syncwarp();
+    float Umax = __int_as_float(__reduce_max_sync(FULL, __float_as_int(rs.U)));
+    int sp = 0;
+    int node = __ldg(sv.tlas_root + env);
+    for (;;) {
+        if (node >= 0) {
+            if (COUNT) cnt.nodes++;
+            if (COUNT && rs.cur_inst < 0) cnt.tnodes++;
+            const float4* cp = sv.nodes8 + NODE8_F4 * (size_t)node + 2 * child;
+            const float4 ca = __ldg(cp), cb = __ldg(cp + 1);
+            float nx, fx, ny, fy, nz, fz;
+            pslab_axis(ca.x, ca.w, ps.olx, ps.ohx, ps.i0x, ps.i1x, nx, fx);
+            pslab_axis(ca.y, cb.x, ps.oly, ps.ohy, ps.i0y, ps.i1y, ny, fy);
+            pslab_axis(ca.z, cb.y, ps.olz, ps.ohz, ps.i0z, ps.i1z, nz, fz);
+            const float tn = fmaxf(fmaxf(nx, ny), fmaxf(nz, 0.0f));
+            const float tf = fminf(fminf(fx, fy), fminf(fz, Umax));
+            const bool h = tn <= tf;
+            const int ref = __float_as_int(cb.z);
+            const unsigned cm = __ballot_sync(FULL, h) & 0xFFu;
+            const int nh = __popc(cm);
+            if (nh == 0) {
+                if (sp == 0) break;
+                __syncwarp();
+                node = wstack[--sp];
+                continue;
+            }
+            if (nh == 1) {
+                node = __shfl_sync(FULL, ref, __ffs(cm) - 1);
+                continue;
+            }
+            // rank of this lane's child among the hit children by the centre
+            // ray's entry distance (lanes 8-15), misses last
+            const unsigned kc = __shfl_sync(FULL, __float_as_uint(tn), child + 8);
+            const bool hit = slot_lane && ((cm >> child) & 1u);
+            const unsigned key = hit ? kc : KEY_MISS;
+            int rank = 0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const unsigned kj = __shfl_sync(FULL, key, j);
+                rank += (kj < key || (kj == key && j < child)) ? 1 : 0;
+            }
+            const int first = __ffs(__ballot_sync(FULL, hit && rank == 0)) - 1;
+            const int nearest = __shfl_sync(FULL, ref, first);
+            if (sp + 7 <= PSTACK) {
+                __syncwarp();  // every lane has read the slots before they are reused
+                if (hit && rank > 0) wstack[sp + nh - 1 - rank] = ref;
+                sp += nh - 1;  // nh is warp-uniform
+            } else {
+                rs.c.i(C_OVF) = 1;
+            }
+            node = nearest;
+            continue;
+        }
+        if (node == SENTINEL) {  // back to the env level
+            rs.cur_inst = -1;
+            ps = pslab_load(ps_env + role * PS_N);
+            if (sp == 0) break;
+            __syncwarp();
+            node = wstack[--sp];
+            continue;
+        }
+        const int leaf = ~node;
+        if (rs.cur_inst < 0) {
+            if (COUNT) cnt.insts++;
+            if (sp < PSTACK) {
+                __syncwarp();
+                if (lane == 0) wstack[sp] = SENTINEL;
+                ++sp;
+            } else {
+                rs.c.i(C_OVF) = 1;
+                break;
+            }
+            f3 oo, od;
+            float delta;
+            node = rs.enter_object(sv, leaf, oo, od, delta);
+            ps = make_pslab<8>(oo, od, delta);
+            __syncwarp();
+            if (child == 0 && lane < 16) pslab_store(ps_obj + role * PS_N, ps);
             __syncwarp();
             continue;
         }
@@ -1238,8 +1354,12 @@ __global__ void __launch_bounds__(CAST_THREADS, CAST_MIN_BLOCKS) k_cast(const __
             if (TRAV == 1) {
                 // whole warps share (env, sensor): pinhole / beams tiles
 #if AGR_IPACKET
-                traverse_ipacket<COUNT>(a.sv, id.env, rs, leaf_fn, s_stack[threadIdx.x >> 5],
-                                        s_pslab[threadIdx.x >> 5][0], s_pslab[threadIdx.x >> 5][1], cnt);
+                if (a.wide)
+                    traverse_ipacket8<COUNT>(a.sv, id.env, rs, leaf_fn, s_stack[threadIdx.x >> 5],
+                                             s_pslab[threadIdx.x >> 5][0], s_pslab[threadIdx.x >> 5][1], cnt);
+                else
+                    traverse_ipacket<COUNT>(a.sv, id.env, rs, leaf_fn, s_stack[threadIdx.x >> 5],
+                                            s_pslab[threadIdx.x >> 5][0], s_pslab[threadIdx.x >> 5][1], cnt);
 #else
                 traverse_packet<false, COUNT>(a.sv, id.env, rs, leaf_fn, s_stack[threadIdx.x >> 5], cnt);
 #endif

@@ -367,6 +367,10 @@ __global__ void k_tlas(TlasArgs a, int rebuild) {
                 a.tlas_item_parent[i0] = 0;
             }
             write_node4(a.nodes, nodebase, b, refs, n);
+            if (a.nodes8) {
+                write_child8(a.nodes8, nodebase, 0, b[0], refs[0]);
+                for (int k = 1; k < 8; ++k) write_child8(a.nodes8, nodebase, k, EMPTY, REF_EMPTY);
+            }
             a.tlas_node_parent[toff] = -1;
             if (rebuild) a.tlas_depth[e] = 1;
         }
@@ -543,6 +547,21 @@ __global__ void k_tlas(TlasArgs a, int rebuild) {
             g[c] = r == REF_EMPTY ? REF_EMPTY : (r < 0 ? ~(i0 + ~r) : nodebase + r);
         }
         write_node4(a.nodes, nodebase + j, b, g, cnt);
+    }
+    if (a.nodes8) {
+        // the BVH8 copy of the interval-packet traversal: 8-wide collapse
+        for (int j = tid; j < n - 1; j += blockDim.x) {
+            int refs[8];
+            collapse_w<8>(j, ch, bx, refs);
+            for (int c = 0; c < 8; ++c) {
+                const int r = refs[c];
+                const float* src = r == REF_EMPTY ? EMPTY : (r < 0 ? s.box + 6 * ~r : s.ibox + 6 * r);
+                float b[6];
+                slot_box(src, b);
+                write_child8(a.nodes8, nodebase + j, c,
+                             b, r == REF_EMPTY ? REF_EMPTY : (r < 0 ? ~(i0 + ~r) : nodebase + r));
+            }
+        }
     }
 }
 

@@ -926,10 +926,56 @@ def test_parts_update_mesh_stereo_and_exact():
     s.set_stereo((0.0, -0.3, 0.0), 1e-4)
     got = to_np(cast_sensor(s, sensor, "depth", channels=("dist", "seg", "face", "valid")))
     ref = oracle.cast(sc2, oracle_rays(sensor, "depth"), stereo=((0.0, -0.3, 0.0), 1e-4))
-    compare(ref, got["dist"], got["seg"], got["face"], "tree parts after update")
-    assert valid_compare(ref, got["valid"], "tree parts stereo") > 50
+    # the cube's front face (x = 7) is centred on the optical axis: its
+    # diagonal pixels are exact ties (61 of 24576), as in config 1
+    compare(ref, got["dist"], got["seg"], got["face"], "tree parts after update", max_amb=64)
+    assert valid_compare(ref, got["valid"], "tree parts stereo", max_amb=64) > 50
     assert (got["seg"] == 1).sum() > 500
     s.set_exact_mode(True)
     ex = to_np(cast_sensor(s, sensor, "depth", channels=("dist", "seg", "face", "valid")))
     for k in got:
         assert np.array_equal(got[k], ex[k]), k
+
+
+# ---- 8-wide nodes for the interval packets ------------------------------
+
+@pytest.mark.parametrize("cfg", [2, 3, 4])
+def test_bvh8_packets_equal_bvh4_packets_bitwise(cfg):
+    """The interval-packet traversal over the BVH8 copy (default), over the
+    BVH4 (traversal mode 2), a BVH4-only scene (node_width 4) and the
+    per-lane traversal give bitwise identical images, after a rebuild and
+    after a refit; and match the oracle on samples."""
+    if cfg == 2:
+        sc, sensor = sg.config2(n_envs=8)
+    elif cfg == 3:
+        sc, sensor = sg.config3(n_envs=6)
+    else:
+        sc, sensor = sg.config4(n_envs=6)
+        sensor = dict(sensor, beams=sg.lidar_beams(64, 256))
+    kind = "range" if cfg == 4 else "depth"
+    chans = ("dist", "seg", "face", "normal")
+    s = make_scene(sc, build=False)
+    s4 = agr.Scene.from_scenegen(sc, device=0, node_width=4)
+    s4.set_instance_transforms(torch.from_numpy(sc.inst_T).to(dev()))
+    for sc_ in (s, s4):
+        sc_.set_tlas_builder(1)
+        sc_.build()
+    imgs = []
+    for step in range(2):
+        if step == 1:
+            T2 = sc.inst_T.copy()
+            T2[:, :2, 3] += np.random.default_rng(5).uniform(-0.3, 0.3, (len(T2), 2)).astype(np.float32)
+            for sc_ in (s, s4):
+                sc_.set_instance_transforms(torch.from_numpy(T2).to(dev()))
+                sc_.refit()
+        runs = []
+        for sc_, mode in ((s, 0), (s, 2), (s4, 0), (s, 1)):
+            sc_.set_traversal(mode)
+            runs.append(to_np(cast_sensor(sc_, sensor, kind, channels=chans)))
+        for r in runs[1:]:
+            for k in chans:
+                assert np.array_equal(runs[0][k].view(np.uint32), r[k].view(np.uint32)), (step, k)
+        imgs.append(runs[0])
+    q = np.random.default_rng(8).choice(len(imgs[0]["dist"]), 10000, replace=False)
+    ref = oracle.cast(sc, oracle_rays(sensor, kind), query=q)
+    compare(ref, imgs[0]["dist"][q], imgs[0]["seg"][q], imgs[0]["face"][q], f"c{cfg} bvh8")
