@@ -688,8 +688,15 @@ struct PSlab {
     float ohx, ohy, ohz;  // o - dp
     float i0x, i0y, i0z;  // 1 / (lower direction endpoint)
     float i1x, i1y, i1z;  // 1 / (upper direction endpoint)
+    int strad;            // warp-uniform: some lane's interval contains 0 on some axis
 };
-constexpr int PS_N = 12;
+constexpr int PS_N = 13;
+#ifndef AGR_STRAD_FAST
+#define AGR_STRAD_FAST 1  // BVH8 packets: no-straddle slab specialisation
+#endif
+#ifndef AGR_PS_RELOAD
+#define AGR_PS_RELOAD 1   // reload the packet slab state from shared memory after a leaf
+#endif
 
 __device__ __forceinline__ int f2ord(float f) {
     const int k = __float_as_int(f);
@@ -732,6 +739,10 @@ __device__ __forceinline__ PSlab make_pslab(f3 o, f3 d, float delta) {
     iv_recip(centre ? dcx : mnx, centre ? dcx : mxx, p.i0x, p.i1x);
     iv_recip(centre ? dcy : mny, centre ? dcy : mxy, p.i0y, p.i1y);
     iv_recip(centre ? dcz : mnz, centre ? dcz : mxz, p.i0z, p.i1z);
+    // the interval straddles 0 on an axis (same test as iv_recip's); the
+    // centre lanes only order children, so only the interval's counts
+    const bool st = !(mnx > 0.0f || mxx < 0.0f) || !(mny > 0.0f || mxy < 0.0f) || !(mnz > 0.0f || mxz < 0.0f);
+    p.strad = st ? 1 : 0;
     return p;
 }
 
@@ -768,6 +779,7 @@ __device__ __forceinline__ void pslab_store(float* dst, const PSlab& p) {
     dst[3] = p.ohx; dst[4] = p.ohy; dst[5] = p.ohz;
     dst[6] = p.i0x; dst[7] = p.i0y; dst[8] = p.i0z;
     dst[9] = p.i1x; dst[10] = p.i1y; dst[11] = p.i1z;
+    dst[12] = __int_as_float(p.strad);
 }
 __device__ __forceinline__ PSlab pslab_load(const float* src) {
     PSlab p;
@@ -775,7 +787,18 @@ __device__ __forceinline__ PSlab pslab_load(const float* src) {
     p.ohx = src[3]; p.ohy = src[4]; p.ohz = src[5];
     p.i0x = src[6]; p.i0y = src[7]; p.i0z = src[8];
     p.i1x = src[9]; p.i1y = src[10]; p.i1z = src[11];
+    p.strad = __float_as_int(src[12]);
     return p;
+}
+
+// pslab_axis for an interval of one sign (every lane's, i.e. !strad): near
+// and far are the min and max of the four products (no straddle branch).
+__device__ __forceinline__ void pslab_axis_fast(float lo, float hi, float ol, float oh, float i0, float i1,
+                                                float& n, float& f) {
+    const float a = lo - ol, b = hi - oh;
+    const float a0 = a * i0, a1 = a * i1, b0 = b * i0, b1 = b * i1;
+    n = fminf(fminf(a0, a1), fminf(b0, b1));
+    f = fmaxf(fmaxf(a0, a1), fmaxf(b0, b1));
 }
 
 // Closest-hit traversal of a tile whose rays share their origin.  ps_env /
@@ -901,6 +924,7 @@ __device__ __forceinline__ void traverse_ipacket8(const SceneView& sv, int env, 
     const int role = (lane >> 3) & 1;
     const bool slot_lane = lane < 8;  // lanes owning child slots for ordering / pushes
     PSlab ps = make_pslab<8>(rs.o(), rs.d(), K_ERR * rs.c.f(C_Q));
+    ps.strad = __any_sync(FULL, ps.strad && role == 0) ? 1 : 0;
     if (child == 0 && lane < 16) pslab_store(ps_env + role * PS_N, ps);
     __syncwarp();
     float Umax = __int_as_float(__reduce_max_sync(FULL, __float_as_int(rs.U)));
@@ -913,9 +937,15 @@ __device__ __forceinline__ void traverse_ipacket8(const SceneView& sv, int env, 
             const float4* cp = sv.nodes8 + NODE8_F4 * (size_t)node + 2 * child;
             const float4 ca = __ldg(cp), cb = __ldg(cp + 1);
             float nx, fx, ny, fy, nz, fz;
-            pslab_axis(ca.x, ca.w, ps.olx, ps.ohx, ps.i0x, ps.i1x, nx, fx);
-            pslab_axis(ca.y, cb.x, ps.oly, ps.ohy, ps.i0y, ps.i1y, ny, fy);
-            pslab_axis(ca.z, cb.y, ps.olz, ps.ohz, ps.i0z, ps.i1z, nz, fz);
+            if (AGR_STRAD_FAST && !ps.strad) {
+                pslab_axis_fast(ca.x, ca.w, ps.olx, ps.ohx, ps.i0x, ps.i1x, nx, fx);
+                pslab_axis_fast(ca.y, cb.x, ps.oly, ps.ohy, ps.i0y, ps.i1y, ny, fy);
+                pslab_axis_fast(ca.z, cb.y, ps.olz, ps.ohz, ps.i0z, ps.i1z, nz, fz);
+            } else {
+                pslab_axis(ca.x, ca.w, ps.olx, ps.ohx, ps.i0x, ps.i1x, nx, fx);
+                pslab_axis(ca.y, cb.x, ps.oly, ps.ohy, ps.i0y, ps.i1y, ny, fy);
+                pslab_axis(ca.z, cb.y, ps.olz, ps.ohz, ps.i0z, ps.i1z, nz, fz);
+            }
             const float tn = fmaxf(fmaxf(nx, ny), fmaxf(nz, 0.0f));
             const float tf = fminf(fminf(fx, fy), fminf(fz, Umax));
             const bool h = tn <= tf;
@@ -978,6 +1008,7 @@ __device__ __forceinline__ void traverse_ipacket8(const SceneView& sv, int env, 
             float delta;
             node = rs.enter_object(sv, leaf, oo, od, delta);
             ps = make_pslab<8>(oo, od, delta);
+            ps.strad = __any_sync(FULL, ps.strad && role == 0) ? 1 : 0;
             __syncwarp();
             if (child == 0 && lane < 16) pslab_store(ps_obj + role * PS_N, ps);
             __syncwarp();
@@ -991,7 +1022,7 @@ __device__ __forceinline__ void traverse_ipacket8(const SceneView& sv, int env, 
         }
         Umax = __int_as_float(__reduce_max_sync(FULL, __float_as_int(rs.U)));
         __syncwarp();
-        ps = pslab_load(ps_obj + role * PS_N);
+        if (AGR_PS_RELOAD) ps = pslab_load(ps_obj + role * PS_N);
         if (sp == 0) break;
         node = wstack[--sp];
     }
