@@ -5,8 +5,8 @@ NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall \
            --expt-relaxed-constexpr
 PKG := paper_2503_01471_b200
 SRC := $(PKG)/csrc/blas.cu $(PKG)/csrc/tlas.cu $(PKG)/csrc/cast.cu \
-       $(PKG)/csrc/checksum.cu $(PKG)/csrc/abi.cu
-HDR := $(PKG)/csrc/agr_internal.cuh include/agr.h
+       $(PKG)/csrc/checksum.cu $(PKG)/csrc/sim.cu $(PKG)/csrc/abi.cu
+HDR := $(PKG)/csrc/agr_internal.cuh include/agr.h include/agr_sim.h
 OBJ := $(patsubst $(PKG)/csrc/%.cu,build/%.o,$(SRC))
 LIB := $(PKG)/lib/libagr.so
 

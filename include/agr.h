@@ -359,10 +359,15 @@ agr_status agr_set_tlas_builder(agr_scene scene, int32_t builder);
  * a child, and every lane still tests each visited leaf on its own ray;
  * stereo shadow segments, whose origins differ per lane, visit the union
  * of the lanes' own box tests; on the 8-wide node copy when it exists,
- * agr_create_options.node_width), 1 = one independent ray per lane (faster
- * when a tile's rays diverge, e.g. terrain seen at grazing angles), 2 = the
- * packets of mode 0 on the 4-wide nodes (comparison / testing).
- * Explicit rays always use 1.  EINVAL outside 0..2.
+ * agr_create_options.node_width; a pinhole whose 4x8 tile spans more than
+ * 0.12 rad -- 4 / fx or 8 / fy, i.e. fx or fy below ~67 px: small images
+ * with a wide field of view -- is cast one ray per lane instead, because a
+ * wide direction interval culls little), 1 = one independent ray per lane
+ * (faster when a tile's rays diverge, e.g. terrain seen at grazing angles),
+ * 2 = the packets of mode 0 on the 4-wide nodes, for every camera
+ * (comparison / testing), 3 = the packets of mode 0 on the 8-wide nodes
+ * (the 4-wide ones if there is no BVH8 copy) for every camera.
+ * Explicit rays always use 1.  EINVAL outside 0..3.
  */
 agr_status agr_set_traversal(agr_scene scene, int32_t mode);
 

@@ -24,6 +24,7 @@ LIB_PATH = os.path.join(_HERE, "lib", "libagr.so")
 # experiments only: load an alternative build of the same library
 LIB_PATH = os.environ.get("AGR_LIB_PATH", LIB_PATH)
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "agr.h")
+SIM_HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "agr_sim.h")
 
 AGR_OK, AGR_EINVAL, AGR_ENOMEM, AGR_ECUDA, AGR_ESTATE, AGR_EUNSUPPORTED = 0, -1, -2, -3, -4, -5
 AGR_DEPTH, AGR_RANGE = 0, 1
@@ -78,6 +79,17 @@ class agr_scene_info(ctypes.Structure):
                 ("n_parts", ctypes.c_int32), ("n_items", ctypes.c_int64)]
 
 
+class agr_sim_params(ctypes.Structure):
+    """include/agr_sim.h: the kinematic env-step stand-in's parameters."""
+    _fields_ = [("dt", ctypes.c_float), ("v_max", ctypes.c_float), ("tau", ctypes.c_float),
+                ("yaw_rate_max", ctypes.c_float), ("goal_radius", ctypes.c_float),
+                ("lo", ctypes.c_float * 3), ("hi", ctypes.c_float * 3),
+                ("seed", ctypes.c_uint32), ("env_base", ctypes.c_int32)]
+
+
+SIM_ROBOT_FLOATS = 12     # sizeof(agr_sim_robot) / 4
+SIM_OBSTACLE_FLOATS = 20  # sizeof(agr_sim_obstacle) / 4
+
 _P = ctypes.c_void_p
 _I32 = ctypes.c_int32
 _SIGS = {
@@ -115,6 +127,8 @@ _SIGS = {
     "agr_debug_export_bvh4": (_I32, [_P, _I32, _P, ctypes.POINTER(ctypes.c_int32),
                                      ctypes.POINTER(ctypes.c_int64)]),
     "agr_debug_asset_parts": (_I32, [_P, _I32, _P, ctypes.POINTER(ctypes.c_int32)]),
+    "agr_sim_kinematic_step": (_I32, [_P, _I32, _P, _P, ctypes.c_int64, _P,
+                                      ctypes.POINTER(agr_sim_params), _P]),
 }
 
 _lib = None
@@ -136,9 +150,11 @@ def load():
 
 
 def header_symbols():
-    """Function names declared in include/agr.h."""
-    with open(HEADER_PATH) as f:
-        txt = f.read()
+    """Function names declared in include/agr.h and include/agr_sim.h."""
+    txt = ""
+    for path in (HEADER_PATH, SIM_HEADER_PATH):
+        with open(path) as f:
+            txt += f.read()
     return sorted(set(re.findall(r"^\s*(?:agr_status|int32_t|const char\*)\s+(agr_\w+)\s*\(", txt, re.M)))
 
 
@@ -361,8 +377,10 @@ class Scene:
         _check(load().agr_set_tlas_builder(self.handle, int(builder)))
 
     def set_traversal(self, mode: int):
-        """0 auto (interval packets for pinhole / beam tiles, BVH8 when built),
-        1 per-lane rays, 2 interval packets on the BVH4."""
+        """0 auto (interval packets for pinhole / beam tiles on the BVH8 when
+        built; per-lane rays for pinholes whose 4x8 tile spans > 0.12 rad),
+        1 per-lane rays, 2 interval packets on the BVH4 for every camera,
+        3 interval packets on the BVH8 for every camera."""
         _check(load().agr_set_traversal(self.handle, int(mode)))
 
     def enable_counters(self, enable: bool):
@@ -405,6 +423,18 @@ class Scene:
         _check(lib.agr_debug_export_bvh4(self.handle, which, nodes.ctypes.data, ctypes.byref(root),
                                          ctypes.byref(n)))
         return nodes, root.value
+
+
+def sim_kinematic_step(robots, poses, obstacles, obst_T, params: agr_sim_params, stream=None):
+    """agr_sim_kinematic_step (include/agr_sim.h): the simulator stand-in of
+    the Table-II env-step benchmark.  robots: CUDA float32 [E, 12] (one
+    agr_sim_robot per env); poses: CUDA float32 [E, 1, 3, 4] (written);
+    obstacles: CUDA float32 [I, 20] (agr_sim_obstacle records) or None;
+    obst_T: CUDA float32 [I, 3, 4] (written) or None."""
+    n_obst = 0 if obstacles is None else int(obstacles.shape[0])
+    _check(load().agr_sim_kinematic_step(_ptr(robots), int(robots.shape[0]), _ptr(poses),
+                                         _ptr(obstacles), n_obst, _ptr(obst_T),
+                                         ctypes.byref(params), _stream_handle(stream)))
 
 
 def abi_version() -> int:

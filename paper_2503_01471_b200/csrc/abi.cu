@@ -125,7 +125,8 @@ struct agr_scene_s {
     int exact = 0;
     float stereo[3] = {0.0f, -0.095f, 0.0f};
     float stereo_eps = 1e-4f;
-    int traversal = 0;  // 0 auto (interval packets for pinhole / beams, on the BVH8 if built),
+    int traversal = 0;  // 0 auto (interval packets for pinhole / beams, on the BVH8 if built;
+                        //   per-lane for wide-tile pinholes, set_schedule),
                         // 1 per-lane, 2 interval packets on the BVH4
     int tlas_builder = 0;  // 0 LBVH (default), 1 binned SAH
     bool counting = false;
@@ -357,10 +358,25 @@ static std::vector<int> asset_parts(const agr_mesh& m, int* n_parts) {
 }
 
 // Marks the end of the scene-changing work just queued on `st` (see `ready`).
+// Inside a CUDA-graph capture the record becomes an external event-record
+// node, so every replay of the graph re-records `ready`.
 static agr_status mark_ready(agr_scene_s* s, cudaStream_t st) {
-    CK(cudaEventRecord(s->ready, st));
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    CK(cudaStreamIsCapturing(st, &cap));
+    if (cap == cudaStreamCaptureStatusActive)
+        CK(cudaEventRecordWithFlags(s->ready, st, cudaEventRecordExternal));
+    else
+        CK(cudaEventRecord(s->ready, st));
     return AGR_OK;
 }
+
+// agr_last_error for the other translation units (sim.cu).
+namespace agr {
+agr_status set_error(agr_status st, const char* msg) {
+    g_err = msg;
+    return st;
+}
+}  // namespace agr
 
 extern "C" {
 
@@ -791,11 +807,27 @@ static agr_status check_cast_state(agr_scene s, float max_range, const agr_outpu
     return AGR_OK;
 }
 
+// Interval packets pay when a 4x8 tile's rays are nearly parallel: with the
+// tile spanning more than ~0.12 rad (a pinhole with fx, fy below ~67 px:
+// 8x8 .. 64x64 images at 87 deg hfov) the direction interval culls little
+// and the warp walks most of the env, one slow packet per tile, while
+// independent lanes finish 1.4-5x sooner (bench.py --table2).
+// Mode 0 (auto) therefore casts such cameras one ray per lane.
+constexpr float PACKET_MAX_TILE_RAD = 0.12f;
+
+static void set_schedule(const agr_scene_s* s, CastArgs& a) {
+    bool packet = s->traversal != 1;
+    if (s->traversal == 0 && a.model == 1 &&
+        (4.0f / a.fx > PACKET_MAX_TILE_RAD || 8.0f / a.fy > PACKET_MAX_TILE_RAD))
+        packet = false;
+    a.packet = packet ? 1 : 0;
+    a.wide = packet && (s->traversal == 0 || s->traversal == 3) && s->nodes8 ? 1 : 0;
+}
+
 static agr_status run_cast(agr_scene s, CastArgs& a, cudaStream_t st) {
     a.sv = s->view();
     a.exact = s->exact;
-    a.packet = s->traversal != 1 ? 1 : 0;
-    a.wide = s->traversal == 0 && s->nodes8 ? 1 : 0;
+    set_schedule(s, a);
     a.counters = nullptr;
     if (s->counting) {
         CK(cudaMemsetAsync(s->counters, 0, sizeof(unsigned long long) * 8, st));
@@ -985,8 +1017,7 @@ static agr_status e2e_run(agr_scene s, CastArgs& a, int64_t elems_per_env, agr_o
         c.out_annot = (float*)dev[7];
         c.sv = s->view();
         c.exact = s->exact;
-        c.packet = s->traversal != 1 ? 1 : 0;
-        c.wide = s->traversal == 0 && s->nodes8 ? 1 : 0;
+        set_schedule(s, c);
         c.counters = nullptr;
         CK(cast_launch(c, cs));
         CK(cudaEventRecord(s->e2e_event[slot], cs));
@@ -1119,7 +1150,7 @@ agr_status agr_set_tlas_builder(agr_scene s, int32_t builder) {
 agr_status agr_set_traversal(agr_scene s, int32_t mode) {
     g_err.clear();
     if (!s) return fail(AGR_EINVAL, "scene is NULL");
-    if (mode < 0 || mode > 2) return fail(AGR_EINVAL, "traversal mode must be 0, 1 or 2");
+    if (mode < 0 || mode > 3) return fail(AGR_EINVAL, "traversal mode must be 0, 1, 2 or 3");
     s->traversal = mode;
     return AGR_OK;
 }

@@ -389,6 +389,34 @@ def config4(n_envs=4096, env_base=0):
     return sc, dict(beams=lidar_beams(128, 512), poses=poses, max_range=10.0, kind="beams")
 
 
+def table2_sim_records(sc, poses, seed=CONFIG_SEED[4] + 7):
+    """Initial records of the kinematic env-step stand-in (include/agr_sim.h)
+    for a c4-shaped room scene: robots float32 [E][12] (agr_sim_robot: p from
+    the env's sensor pose, v = 0, goal unset, yaw of the pose, 0 goals) and
+    obstacles float32 [I][20] (agr_sim_obstacle: T0 = the instance transform;
+    the room (label 0) never moves, each floating obstacle gets a yaw rate
+    U(-0.5, 0.5) rad/s, a bobbing amplitude U(0, 0.2) m, frequency U(0.5, 2)
+    rad/s and phase U(0, 2 pi), from its env's own stream)."""
+    E = sc.n_envs
+    robots = np.zeros((E, 12), np.float32)
+    P = np.asarray(poses, np.float64).reshape(E, -1, 3, 4)[:, 0]
+    robots[:, 0:3] = P[:, :, 3]
+    robots[:, 9] = np.arctan2(P[:, 1, 0], P[:, 0, 0])
+    obst = np.zeros((sc.n_inst, 20), np.float32)
+    obst[:, 0:12] = sc.inst_T.reshape(-1, 12)
+    for i in range(E):
+        e = sc.env_base + i
+        i0, i1 = int(sc.env_off[i]), int(sc.env_off[i + 1])
+        rng = env_rng(seed, e)
+        m = i1 - i0
+        mov = sc.inst_label[i0:i1] != 0
+        obst[i0:i1, 12] = np.where(mov, rng.uniform(-0.5, 0.5, m), 0.0)
+        obst[i0:i1, 13] = np.where(mov, rng.uniform(0.0, 0.2, m), 0.0)
+        obst[i0:i1, 14] = np.where(mov, rng.uniform(0.5, 2.0, m), 0.0)
+        obst[i0:i1, 16] = np.where(mov, rng.uniform(0.0, 2 * math.pi, m), 0.0)
+    return robots, obst
+
+
 def _quat_rotations(q):
     """Rotation matrices [..][3][3] of (unnormalised) quaternions q [..][4]
     (w, x, y, z), normalised first: uniform random rotations for normal q."""

@@ -969,7 +969,7 @@ def test_bvh8_packets_equal_bvh4_packets_bitwise(cfg):
                 sc_.set_instance_transforms(torch.from_numpy(T2).to(dev()))
                 sc_.refit()
         runs = []
-        for sc_, mode in ((s, 0), (s, 2), (s4, 0), (s, 1)):
+        for sc_, mode in ((s, 0), (s, 2), (s4, 0), (s, 1), (s, 3)):
             sc_.set_traversal(mode)
             runs.append(to_np(cast_sensor(sc_, sensor, kind, channels=chans)))
         for r in runs[1:]:
@@ -979,3 +979,141 @@ def test_bvh8_packets_equal_bvh4_packets_bitwise(cfg):
     q = np.random.default_rng(8).choice(len(imgs[0]["dist"]), 10000, replace=False)
     ref = oracle.cast(sc, oracle_rays(sensor, kind), query=q)
     compare(ref, imgs[0]["dist"][q], imgs[0]["seg"][q], imgs[0]["face"][q], f"c{cfg} bvh8")
+
+
+def test_wide_tile_cameras_all_schedules_bitwise():
+    """Small wide-angle images (8x8 .. 64x64 at 87 deg: a 4x8 tile spans
+    0.24-2 rad) are cast one ray per lane in auto mode (agr.h); the
+    interval packets forced on them (modes 2 / 3, the sign-change branches
+    of the interval slab everywhere) give bitwise the same images, and
+    those match the oracle in full."""
+    sc, sensor = sg.config4(n_envs=8)
+    s = make_scene(sc, build=False)
+    s.set_tlas_builder(1)
+    s.build()
+    for H, W in ((8, 8), (16, 16), (31, 33), (64, 64)):
+        cam = sg.pinhole(W, H, 87.0)
+        sen = dict(kind="pinhole", cam=cam, poses=sensor["poses"], max_range=10.0)
+        runs = []
+        for mode in (0, 1, 2, 3):
+            s.set_traversal(mode)
+            runs.append(to_np(cast_sensor(s, sen, "depth", channels=("dist", "seg", "face", "normal"))))
+        for r in runs[1:]:
+            for k in r:
+                assert np.array_equal(runs[0][k].view(np.uint32), r[k].view(np.uint32)), (H, W, k)
+        ref = oracle.cast(sc, oracle_rays(sen, "depth"))
+        compare(ref, runs[0]["dist"], runs[0]["seg"], runs[0]["face"], f"wide tiles {H}x{W}")
+    with pytest.raises(agr.AgrError):
+        s.set_traversal(4)
+    s.close()
+
+
+# --------------------------------------------------------------------------
+# Table II-shaped env step (SURVEY.md §8(f) f4; PAPER.md:276-304): the
+# kinematic stand-in (include/agr_sim.h) + refit + cast, eager and as a
+# CUDA graph, against the oracle on the scene the step produced
+# --------------------------------------------------------------------------
+def _t2_setup(E=16, H=48, W=64):
+    sc, sensor = sg.config4(n_envs=E)
+    robots0, obst0 = sg.table2_sim_records(sc, sensor["poses"])
+    prm = agr.agr_sim_params(dt=0.05, v_max=2.0, tau=0.2, yaw_rate_max=1.5, goal_radius=0.5,
+                             lo=(-4.0, -4.0, 0.5), hi=(4.0, 4.0, 3.5), seed=7, env_base=0)
+    cam = sg.pinhole(W, H, 87.0)
+    return sc, robots0, obst0, prm, cam
+
+
+def test_sim_step_records():
+    """The stand-in keeps static instances exactly, moves obstacles rigidly
+    (rotation part stays R_z(angle) A0), keeps robots inside the box and
+    writes orthonormal poses; two runs are bitwise identical."""
+    sc, robots0, obst0, prm, _ = _t2_setup()
+    runs = []
+    for _ in range(2):
+        robots = torch.from_numpy(robots0.copy()).to(dev())
+        obst = torch.from_numpy(obst0.copy()).to(dev())
+        poses = torch.empty((sc.n_envs, 1, 3, 4), device=dev())
+        T = torch.empty((sc.n_inst, 3, 4), device=dev())
+        for _k in range(50):
+            agr.sim_kinematic_step(robots, poses, obst, T, prm)
+        torch.cuda.synchronize()
+        runs.append((poses.cpu().numpy(), T.cpu().numpy(), robots.cpu().numpy()))
+    assert all(np.array_equal(a, b) for a, b in zip(runs[0], runs[1]))
+    P, Tn, R = runs[0]
+    static = sc.inst_label == 0
+    assert np.array_equal(Tn[static], sc.inst_T[static])
+    A0 = sc.inst_T[:, :, :3].astype(np.float64)
+    A = Tn[:, :, :3].astype(np.float64)
+    # same column norms and the z row untouched: a yaw rotation of A0
+    assert np.allclose(np.linalg.norm(A, axis=1), np.linalg.norm(A0, axis=1), rtol=1e-5, atol=1e-6)
+    assert np.array_equal(Tn[:, 2, :3], sc.inst_T[:, 2, :3])
+    assert np.array_equal(Tn[:, :2, 3], sc.inst_T[:, :2, 3])
+    assert np.any(Tn[~static] != sc.inst_T[~static])
+    Rp = P[:, 0, :, :3].astype(np.float64)
+    assert np.allclose(Rp @ np.swapaxes(Rp, 1, 2), np.eye(3), atol=1e-6)
+    p = P[:, 0, :, 3]
+    assert np.all(p >= np.asarray(prm.lo) - 1e-6) and np.all(p <= np.asarray(prm.hi) + 1e-6)
+    assert np.all(R.view(np.int32)[:, 10] >= 1)  # every robot drew a goal
+    assert np.any(np.abs(p - robots0[:, 0:3]) > 0.1)
+
+
+def test_sim_step_rejects_bad_params():
+    sc, robots0, obst0, prm, _ = _t2_setup(E=2)
+    robots = torch.from_numpy(robots0.copy()).to(dev())
+    poses = torch.empty((2, 1, 3, 4), device=dev())
+    bad = agr.agr_sim_params(dt=0.0, v_max=1.0, tau=0.1)
+    with pytest.raises(agr.AgrError):
+        agr.sim_kinematic_step(robots, poses, None, None, bad)
+
+
+def test_table2_env_step_graph_matches_eager_and_oracle():
+    """20 dynamic env steps (robots + obstacles move, transforms set, TLAS
+    refit, depth + seg cast) replayed from a CUDA graph give bitwise the
+    images of the same steps run eagerly, and those images match the oracle
+    on the scene and poses the last step produced."""
+    sc, robots0, obst0, prm, cam = _t2_setup()
+    E, H, W = sc.n_envs, cam["H"], cam["W"]
+    results = []
+    for use_graph in (False, True):
+        s = make_scene(sc)
+        s.set_tlas_builder(1)
+        s.build()
+        robots = torch.from_numpy(robots0.copy()).to(dev())
+        obst = torch.from_numpy(obst0.copy()).to(dev())
+        poses = torch.empty((E, 1, 3, 4), device=dev())
+        T = torch.from_numpy(sc.inst_T.copy()).to(dev())
+        out = {"dist": torch.empty((E, 1, H, W), device=dev()),
+               "seg": torch.empty((E, 1, H, W), dtype=torch.int32, device=dev()),
+               "face": torch.empty((E, 1, H, W), dtype=torch.int32, device=dev())}
+
+        def step():
+            agr.sim_kinematic_step(robots, poses, obst, T, prm)
+            s.set_instance_transforms(T)
+            s.refit()
+            s.cast_pinhole(cam, poses, 10.0, agr.AGR_DEPTH, out=out)
+
+        if use_graph:
+            step()  # step 1 eagerly, then 19 graph replays
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            # capture records the launches without running them
+            with torch.cuda.graph(g):
+                step()
+            for _ in range(19):
+                g.replay()
+        else:
+            for _ in range(20):
+                step()
+        torch.cuda.synchronize()
+        results.append(({k: v.cpu().numpy() for k, v in out.items()}, poses.cpu().numpy(), T.cpu().numpy()))
+        s.close()
+    (img_e, P_e, T_e), (img_g, P_g, T_g) = results
+    assert np.array_equal(P_e, P_g) and np.array_equal(T_e, T_g)
+    for k in img_e:
+        assert np.array_equal(img_e[k].view(np.int32), img_g[k].view(np.int32)), k
+    sc2 = sc.env_slice(0, E)
+    sc2.inst_T = T_e
+    sensor = dict(kind="pinhole", cam=cam, poses=P_e, max_range=10.0)
+    ref = oracle.cast(sc2, oracle_rays(sensor, "depth"))
+    res = compare(ref, img_e["dist"].reshape(-1), img_e["seg"].reshape(-1), img_e["face"].reshape(-1),
+                  "t2 env step")
+    assert (ref.face >= 0).mean() > 0.5
