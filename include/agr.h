@@ -410,6 +410,9 @@ agr_status agr_debug_export_blas(agr_scene scene, int32_t asset, float* nodes,
  * < 0 ~leaf: triangle record, or global TLAS item = (instance, part) in
  * instance order; INT32_MIN empty).
  * *root = global index of node 0 of the export.  NULL nodes: size query.
+ * A BLAS export holds exactly the nodes reachable from its root (the BVH4
+ * is compacted at every build); a TLAS export holds one node per binary
+ * node, unreachable ones included.
  */
 agr_status agr_debug_export_bvh4(agr_scene scene, int32_t which, float* nodes, int32_t* root,
                                  int64_t* n_nodes);

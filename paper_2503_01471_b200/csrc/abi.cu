@@ -115,6 +115,9 @@ struct agr_scene_s {
     float* annot = nullptr;     // [sum V][annot_k] vertex annotations, NaN = none
     int annot_k = 0;
     void* blas_scratch = nullptr;
+    void* blas_stage = nullptr;          // pinned upload staging of the BLAS batch tables
+    size_t blas_stage_bytes = 0;
+    cudaEvent_t blas_stage_free = nullptr;
     std::vector<int64_t> h_mvert_off, h_mface_off;
     std::vector<int> h_node_base, h_leaf_base, h_nverts, h_nfaces;
     std::vector<char> h_bin_stale;  // binary LBVH export out of date (mesh updated)
@@ -212,6 +215,8 @@ struct agr_scene_s {
         for (auto& e : e2e_event)
             if (e) cudaEventDestroy(e);
         if (ready) cudaEventDestroy(ready);
+        if (blas_stage) cudaFreeHost(blas_stage);
+        if (blas_stage_free) cudaEventDestroy(blas_stage_free);
         for (auto& h : e2e_host)
             if (h) cudaFreeHost(h);
         if (e2e_poses) cudaFree(e2e_poses);
@@ -256,6 +261,9 @@ static cudaError_t build_assets(agr_scene_s* s, const int* assets, int n, cudaSt
     ba.triv = s->triv;
     ba.dbg_morton = s->morton;
     ba.trbvh_rounds = s->trbvh_rounds;
+    ba.h_stage = s->blas_stage;
+    ba.h_stage_bytes = s->blas_stage_bytes;
+    ba.stage_free = s->blas_stage_free;
     return blas_build_batch(segs.data(), (int)segs.size(), ba, s->blas_scratch, st);
 }
 
@@ -544,7 +552,7 @@ agr_status agr_scene_create_ex(int32_t device, const agr_mesh* meshes, int32_t n
     if (!opts || opts->node_width != 4) CKB(s->alloc(&s->nodes8, (size_t)NODE8_F4 * (nb + nt)));
     CKB(s->alloc(&s->bnodes, 4 * (size_t)nb));
     CKB(s->alloc(&s->tris, 3 * (size_t)nl));
-    CKB(s->alloc(&s->triv, 9 * (size_t)nl));
+    CKB(s->alloc(&s->triv, 12 * (size_t)nl));  // 3 x float4 (v.xyz, 0) per leaf
     CKB(s->alloc(&s->irec, 4 * (size_t)n_items));
     CKB(s->alloc(&s->inst_T, 12 * (size_t)n_inst));
     CKB(s->alloc(&s->item_box, 6 * (size_t)n_items));
@@ -616,6 +624,9 @@ agr_status agr_scene_create_ex(int32_t device, const agr_mesh* meshes, int32_t n
     }
     // scratch for a batch of every asset (any update batch fits in it)
     CKB(s->alloc((char**)&s->blas_scratch, blas_scratch_bytes(s->h_mface_off[n_meshes], n_parts)));
+    s->blas_stage_bytes = blas_stage_bytes(s->h_mface_off[n_meshes], n_parts);
+    CKB(cudaMallocHost(&s->blas_stage, s->blas_stage_bytes));
+    CKB(cudaEventCreateWithFlags(&s->blas_stage_free, cudaEventDisableTiming));
     cudaError_t err = cudaSuccess;
     for (int a = 0; a < n_meshes && err == cudaSuccess; ++a) {
         err = cudaMemcpyAsync(s->mesh_verts + 3 * s->h_mvert_off[a], meshes[a].verts,
@@ -738,12 +749,18 @@ agr_status agr_update_meshes(agr_scene s, int32_t n, const int32_t* assets, cons
     }
     DeviceGuard guard(s->device);
     cudaStream_t st = (cudaStream_t)stream;
+    // one copy per run of consecutive asset ids (their vertex arrays are
+    // contiguous on both sides): a whole-scene reset is a single copy
     int64_t v = 0;
-    for (int k = 0; k < n; ++k) {
-        const int a = assets[k];
-        CK(cudaMemcpyAsync(s->mesh_verts + 3 * s->h_mvert_off[a], verts + 3 * v,
-                           sizeof(float) * 3 * s->h_nverts[a], cudaMemcpyDeviceToDevice, st));
-        v += s->h_nverts[a];
+    for (int k = 0; k < n;) {
+        const int a0 = assets[k];
+        int64_t nv = s->h_nverts[a0];
+        int k1 = k + 1;
+        while (k1 < n && assets[k1] == assets[k1 - 1] + 1) nv += s->h_nverts[assets[k1++]];
+        CK(cudaMemcpyAsync(s->mesh_verts + 3 * s->h_mvert_off[a0], verts + 3 * v, sizeof(float) * 3 * nv,
+                           cudaMemcpyDeviceToDevice, st));
+        v += nv;
+        k = k1;
     }
     CK(build_assets(s, assets, n, st, false));
     for (int k = 0; k < n; ++k) s->h_bin_stale[assets[k]] = 1;
@@ -1237,7 +1254,7 @@ agr_status agr_debug_export_bvh4(agr_scene s, int32_t which, float* nodes, int32
         }
         const BlasInfo& a = s->h_parts[s->h_part_off[which]];
         base = a.node_base;
-        count = a.n_leaves > 1 ? a.n_leaves - 1 : 1;
+        count = a.n_nodes4;  // the compacted BVH4 (every node reachable from the root)
     } else {
         const int e = -1 - which;
         if (e >= s->n_envs) return fail(AGR_EINVAL, "env out of range");

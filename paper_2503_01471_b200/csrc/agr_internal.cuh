@@ -6,9 +6,12 @@
 //
 // HBM layout:
 //   nodes   BVH4 nodes, float4[8] = 128 B, BLAS nodes of every asset first,
-//           then every env's TLAS nodes.  BVH4 node j is the greedy 4-wide
-//           collapse of binary LBVH node j (only nodes reachable from the
-//           root are visited).  Boxes of the 4 children stored per axis:
+//           then every env's TLAS nodes.  A BLAS's BVH4 holds only the
+//           nodes reachable from its root: BVH4 node k (from node_base) is
+//           the greedy 4-wide collapse of the k-th reachable binary node in
+//           binary order (root = 0; BlasInfo.n_nodes4 in use).  A TLAS's
+//           BVH4 node j is the collapse of its binary node j (reachable or
+//           not).  Boxes of the 4 children stored per axis:
 //             f0 = lo.x[4], f1 = hi.x[4], f2 = lo.y[4], f3 = hi.y[4],
 //             f4 = lo.z[4], f5 = hi.z[4], f6 = ref[4] (int bits), f7 = (n, -)
 //           ref >= 0: global node index; ref < 0: leaf ~x (TLAS: x = global
@@ -24,7 +27,7 @@
 //             t0 = (v0.xyz, inv_min_alt)   inv_min_alt = 1 / min altitude
 //             t1 = (e1.xyz, two_area)      e1 = v1 - v0, two_area = |e1 x e2|
 //             t2 = (e2.xyz, local face id as int bits)
-//   triv    float[9] per BLAS leaf: the exact FP32 input vertices v0 v1 v2
+//   triv    float4[3] per BLAS leaf: the exact FP32 input vertices v0 v1 v2 (w = 0)
 //           (read only by the FP64 arbitration / epilogue).
 //   irec    float4[4] per TLAS item, 64 B (ray -> object space):
 //             r0..r2 = rows of [Ainv | binv] (FP64 inverse rounded to FP32)
@@ -72,6 +75,7 @@ struct BlasInfo {
     float lo[3], hi[3];  // root box (object space, exact min/max)
     float radius;    // max |v| over the asset's vertices (object units)
     int depth;       // BLAS depth (edges from root to deepest leaf)
+    int n_nodes4;    // BVH4 nodes in use from node_base (the reachable collapse, compacted)
 };
 
 // Read-only view of a scene passed by value to kernels.
@@ -79,7 +83,7 @@ struct SceneView {
     const float4* nodes;      // [n_nodes][8] BVH4
     const float4* nodes8;     // [n_nodes][16] BVH8 (same numbering), or null
     const float4* tris;       // [n_leaves][3]
-    const float* triv;        // [n_leaves][9]
+    const float* triv;        // [n_leaves][3] float4 (v.xyz, 0)
     const float4* irec;       // [n_items][4] (TLAS leaf ~item)
     const float* inst_T;      // [n_inst][12] forward transforms (FP32 input)
     const int* inst_face_off; // [n_inst] per-env face offset of the instance
@@ -246,11 +250,17 @@ struct BlasBatchArgs {
     float* triv;           // global exact-vertex array
     uint32_t* dbg_morton;  // optional: sorted codes at leaf_base + p (device) or null
     int trbvh_rounds;      // treelet-restructuring passes after the LBVH (0 = plain LBVH)
+    void* h_stage;         // optional pinned host staging for the segment / sort-block tables
+    size_t h_stage_bytes;
+    cudaEvent_t stage_free;  // recorded after each upload from h_stage
 };
 // Builds the BLAS of every asset in h_segs[0, n) (host array; `off` is
 // filled in) in one set of launches.  `scratch` must hold
 // blas_scratch_bytes(sum of n_faces, n) bytes.  Async on `stream`.
 size_t blas_scratch_bytes(int64_t total_faces, int n_segs);
+// Pinned host staging a batch of n_segs segments over total_faces faces needs
+// (BlasBatchArgs.h_stage).
+size_t blas_stage_bytes(int64_t total_faces, int n_segs);
 cudaError_t blas_build_batch(BlasSeg* h_segs, int n_segs, const BlasBatchArgs& a, void* scratch,
                              cudaStream_t stream);
 

@@ -28,6 +28,8 @@
 
 #include <cfloat>
 #include <climits>
+#include <cstring>
+#include <cooperative_groups.h>
 #include <cuda/atomic>
 
 #ifndef AGR_KEEP_PAIRS
@@ -40,36 +42,89 @@ namespace {
 
 constexpr int T_BLK = 256;
 constexpr int RS_THREADS = 256;
-constexpr int RS_MIN_ROUNDS = 4;   // rounds of RS_THREADS keys per sort block
-constexpr int RS_MAX_BLOCKS = 296;   // 2 per SM: keeps the single-CTA histogram scan short
+constexpr int RS_ROUNDS = 8;        // rounds of RS_THREADS keys per sort block
+constexpr int RS_TILE = RS_THREADS * RS_ROUNDS;
+constexpr int SCAN_THREADS = 1024, SCAN_CHUNK = 4 * SCAN_THREADS;  // multi-CTA scan
 
-// Keys per sort block: at least RS_MIN_ROUNDS x RS_THREADS, and few enough
-// blocks that the 256 x nblocks histogram scan stays small.
-inline int rs_rounds(int64_t F) {
-    int64_t r = (F + (int64_t)RS_THREADS * RS_MAX_BLOCKS - 1) / ((int64_t)RS_THREADS * RS_MAX_BLOCKS);
-    return (int)(r < RS_MIN_ROUNDS ? RS_MIN_ROUNDS : r);
-}
+// Sort blocks never straddle segments: segment s gets ceil(F_s / RS_TILE)
+// blocks of its own, so the LSD passes sort every segment by its codes in
+// place and no pass over segment ids is needed.  Upper bound on the blocks.
+inline int64_t rs_max_blocks(int64_t F, int B) { return F / RS_TILE + B; }
 constexpr uint32_t DEGENERATE_KEY = 0xFFFFFFFFu;
 constexpr unsigned FULL = 0xFFFFFFFFu;
 
+// Box records of the build scratch: 32 B (lo.xyz, -, hi.xyz, -), so one box
+// is two 128-bit loads / stores instead of six scalar ones (the bottom-up
+// passes are bound by L2 requests, not bytes).
+constexpr int BX = 8;
+constexpr int MAX_LEVELS = 512;  // BVH4 levels of the compaction queue (>= any binary depth)
+
+__device__ __forceinline__ void load_box_cg(const float* p, float b[6]) {
+    const float4 u = __ldcg(reinterpret_cast<const float4*>(p)), v = __ldcg(reinterpret_cast<const float4*>(p) + 1);
+    b[0] = u.x; b[1] = u.y; b[2] = u.z; b[3] = v.x; b[4] = v.y; b[5] = v.z;
+}
+// + the ints in lo.w / hi.w (the fit keeps subtree size / height there)
+__device__ __forceinline__ int2 load_box_cg_w(const float* p, float b[6]) {
+    const float4 u = __ldcg(reinterpret_cast<const float4*>(p)), v = __ldcg(reinterpret_cast<const float4*>(p) + 1);
+    b[0] = u.x; b[1] = u.y; b[2] = u.z; b[3] = v.x; b[4] = v.y; b[5] = v.z;
+    return make_int2(__float_as_int(u.w), __float_as_int(v.w));
+}
+__device__ __forceinline__ int2 load_box_w(const float* p, float b[6]) {
+    const float4 u = reinterpret_cast<const float4*>(p)[0], v = reinterpret_cast<const float4*>(p)[1];
+    b[0] = u.x; b[1] = u.y; b[2] = u.z; b[3] = v.x; b[4] = v.y; b[5] = v.z;
+    return make_int2(__float_as_int(u.w), __float_as_int(v.w));
+}
+__device__ __forceinline__ void store_box_w(float* p, const float b[6], int w0, int w1) {
+    reinterpret_cast<float4*>(p)[0] = make_float4(b[0], b[1], b[2], __int_as_float(w0));
+    reinterpret_cast<float4*>(p)[1] = make_float4(b[3], b[4], b[5], __int_as_float(w1));
+}
+__device__ __forceinline__ void store_box(float* p, const float b[6]) {
+    reinterpret_cast<float4*>(p)[0] = make_float4(b[0], b[1], b[2], 0.0f);
+    reinterpret_cast<float4*>(p)[1] = make_float4(b[3], b[4], b[5], 0.0f);
+}
+__device__ __forceinline__ void store_box_cg(float* p, const float b[6]) {
+    __stcg(reinterpret_cast<float4*>(p), make_float4(b[0], b[1], b[2], 0.0f));
+    __stcg(reinterpret_cast<float4*>(p) + 1, make_float4(b[3], b[4], b[5], 0.0f));
+}
+
+// Child records for the top-down pass (one coalesced pass over the internal
+// nodes): rec[i] = child 0 box, child 1 box, refs, and per child the
+// pair-leaf ref it becomes if the collapse leaves it closed (0: none), so
+// each collapse step reads one 64-B record instead of refs, boxes and sizes
+// from four scattered arrays.
+__device__ __forceinline__ void write_rec(float4* rec, const float a[6], const float b[6], int ra, int rb, int xa,
+                                          int xb) {
+    rec[0] = make_float4(a[0], a[1], a[2], a[3]);
+    rec[1] = make_float4(a[4], a[5], b[0], b[1]);
+    rec[2] = make_float4(b[2], b[3], b[4], b[5]);
+    rec[3] = make_float4(__int_as_float(ra), __int_as_float(rb), __int_as_float(xa), __int_as_float(xb));
+}
 struct Scratch {
-    float* tri_box;      // [Ftot][6] (lo xyz, hi xyz), by batch face
+    float* tri_box;      // [Ftot][BX] leaf boxes (lo xyz, -, hi xyz, -) by SORTED batch position
+    float4* cent;        // [Ftot] triangle centroids (xyz, -) by batch face (Morton input)
     uint32_t* bounds;    // [B][8]: ordered-int centroid lo xyz, hi xyz, radius, n_valid
     uint32_t* mcode;     // [Ftot] Morton code of each batch face
     uint32_t* keys[2];   // [Ftot]
     uint32_t* vals[2];   // [Ftot] batch face ids
-    uint32_t* hist;      // [256 * nblocks]
+    uint32_t* hist;      // [256 * nblocks], (segment, digit, block) order
+    int4* rs_blk;        // [nblocks] sort block: first key, end, hist base, hist stride
+    uint32_t* scan_part; // [256 * nblocks / SCAN_CHUNK + 1] multi-CTA scan partials
     int* seg_of;         // [Ftot] segment of each batch face
     BlasSeg* segs;       // [B]
     int* child;          // [2 Ftot] local refs; segment s at 2 off_s
     int* node_parent;    // [Ftot]   segment s at off_s
     int* leaf_parent;    // [Ftot]
-    float* ibox;         // [Ftot][6]
+    float* ibox;         // [Ftot][BX] internal node boxes, same layout
     int* flags;          // [Ftot]
     int* depth;          // [B]
     float* cost;         // [Ftot] SAH cost of each internal node's subtree (TRBVH)
     int* height;         // [Ftot] edges from each internal node to its deepest leaf
     int* size;           // [Ftot] leaves under each internal node
+    int2* range;         // [Ftot] leaf range [lo, hi] of each Karras node (segment-local)
+    int* seg4;           // [B] BVH4 nodes allocated in each segment (compaction)
+    int2* queue;         // [Ftot] (binary node, BVH4 slot) of every reachable node, level by level
+    float4* rec;         // [Ftot][4] per internal node: both children's boxes, refs and pair-leaf codes
+    int* qctl;           // [2 + MAX_LEVELS]: [0] items in the queue, [2 + L] items of BVH4 level L
 };
 
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
@@ -77,31 +132,38 @@ size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 size_t scratch_layout(int64_t F, int B, void* base, Scratch* out) {
     char* p = (char*)base;
     size_t used = 0;
-    const int64_t tile = (int64_t)RS_THREADS * rs_rounds(F);
-    const size_t nb = (size_t)((F + tile - 1) / tile);
+    const size_t nb = (size_t)rs_max_blocks(F, B);
     auto take = [&](size_t bytes) {
         char* q = p ? p + used : nullptr;
         used += align_up(bytes);
         return q;
     };
     Scratch s;
-    s.tri_box = (float*)take(sizeof(float) * 6 * F);
+    s.tri_box = (float*)take(sizeof(float) * BX * F);
+    s.cent = (float4*)take(sizeof(float4) * F);
     s.bounds = (uint32_t*)take(sizeof(uint32_t) * 8 * B);
     s.mcode = (uint32_t*)take(sizeof(uint32_t) * F);
     for (int i = 0; i < 2; ++i) s.keys[i] = (uint32_t*)take(sizeof(uint32_t) * F);
     for (int i = 0; i < 2; ++i) s.vals[i] = (uint32_t*)take(sizeof(uint32_t) * F);
     s.hist = (uint32_t*)take(sizeof(uint32_t) * 256 * nb);
+    s.rs_blk = (int4*)take(sizeof(int4) * nb);
+    s.scan_part = (uint32_t*)take(sizeof(uint32_t) * (256 * nb / SCAN_CHUNK + 2));
     s.seg_of = (int*)take(sizeof(int) * F);
     s.segs = (BlasSeg*)take(sizeof(BlasSeg) * B);
     s.child = (int*)take(sizeof(int) * 2 * F);
     s.node_parent = (int*)take(sizeof(int) * F);
     s.leaf_parent = (int*)take(sizeof(int) * F);
-    s.ibox = (float*)take(sizeof(float) * 6 * F);
+    s.ibox = (float*)take(sizeof(float) * BX * F);
     s.flags = (int*)take(sizeof(int) * F);
     s.depth = (int*)take(sizeof(int) * B);
     s.cost = (float*)take(sizeof(float) * F);
     s.height = (int*)take(sizeof(int) * F);
     s.size = (int*)take(sizeof(int) * F);
+    s.range = (int2*)take(sizeof(int2) * F);
+    s.seg4 = (int*)take(sizeof(int) * B);
+    s.queue = (int2*)take(sizeof(int2) * F);
+    s.rec = (float4*)take(sizeof(float4) * 4 * F);
+    s.qctl = (int*)take(sizeof(int) * (2 + MAX_LEVELS));
     if (out) *out = s;
     return used + 256;
 }
@@ -155,7 +217,7 @@ __global__ void k_radius(const BlasSeg* segs, uint32_t* bounds) {
     if ((threadIdx.x & 31) == 0) atomicMax(&bounds[8 * s + 6], float_to_ordered(r));
 }
 
-__global__ void k_tri_prep(const BlasSeg* segs, const int* seg_of, int Ftot, float* __restrict__ tri_box,
+__global__ void k_tri_prep(const BlasSeg* segs, const int* seg_of, int Ftot, float4* __restrict__ cent,
                            uint32_t* __restrict__ vflag, uint32_t* bounds) {
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
     const int s = g < Ftot ? __ldg(seg_of + g) : -1;
@@ -171,13 +233,14 @@ __global__ void k_tri_prep(const BlasSeg* segs, const int* seg_of, int Ftot, flo
         d3 A = mkd(a[0], a[1], a[2]), B = mkd(b[0], b[1], b[2]), C = mkd(c[0], c[1], c[2]);
         d3 n = crossd(subd(B, A), subd(C, A));
         valid = (n.x != 0.0 || n.y != 0.0 || n.z != 0.0);
+        float cc[3];
         for (int k = 0; k < 3; ++k) {
             const float lo = fminf(a[k], fminf(b[k], c[k]));
             const float hi = fmaxf(a[k], fmaxf(b[k], c[k]));
-            tri_box[6 * g + k] = lo;
-            tri_box[6 * g + 3 + k] = hi;
-            if (valid) clo[k] = chi[k] = 0.5f * lo + 0.5f * hi;
+            cc[k] = 0.5f * lo + 0.5f * hi;
+            if (valid) clo[k] = chi[k] = cc[k];
         }
+        cent[g] = make_float4(cc[0], cc[1], cc[2], 0.0f);
         vflag[g] = valid ? 1u : 0u;
     }
     // centroid bounds and valid count: one set of atomics per block when the
@@ -223,7 +286,7 @@ __global__ void k_tri_prep(const BlasSeg* segs, const int* seg_of, int Ftot, flo
 }
 
 // ---- K1b: Morton codes ------------------------------------------------------
-__global__ void k_morton(const int* seg_of, const float* __restrict__ tri_box, const uint32_t* __restrict__ vflag,
+__global__ void k_morton(const int* seg_of, const float4* __restrict__ cent, const uint32_t* __restrict__ vflag,
                          int Ftot, const uint32_t* __restrict__ bounds, uint32_t* __restrict__ mcode,
                          uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
@@ -232,10 +295,11 @@ __global__ void k_morton(const int* seg_of, const float* __restrict__ tri_box, c
     uint32_t key = DEGENERATE_KEY;
     if (vflag[g]) {
         float u[3];
+        const float4 cg = cent[g];
+        const float cc[3] = {cg.x, cg.y, cg.z};
         for (int k = 0; k < 3; ++k) {
             float lo = ordered_to_float(b[k]), hi = ordered_to_float(b[3 + k]);
-            float c = 0.5f * tri_box[6 * g + k] + 0.5f * tri_box[6 * g + 3 + k];
-            u[k] = unit_coord(c, lo, hi);
+            u[k] = unit_coord(cc[k], lo, hi);
         }
         key = morton30(u[0], u[1], u[2]);
     }
@@ -244,27 +308,22 @@ __global__ void k_morton(const int* seg_of, const float* __restrict__ tri_box, c
     vals[g] = (uint32_t)g;
 }
 
-// key of each sorted element := its segment (for the segment passes), or
-// back to its Morton code (after them)
-__global__ void k_key_from(const uint32_t* __restrict__ vals, const uint32_t* __restrict__ table_u,
-                           const int* __restrict__ table_i, int Ftot, uint32_t* __restrict__ keys) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= Ftot) return;
-    const uint32_t g = vals[i];
-    keys[i] = table_u ? table_u[g] : (uint32_t)table_i[g];
-}
-
 // ---- K2: stable LSD radix sort (8-bit digits) --------------------------------
-// Sort block b owns keys [b R 256, (b + 1) R 256) (R = rounds).  The
-// histogram counts them per warp slice (warp-aggregated by
-// __match_any_sync, no shared-memory atomics: a pass over segment ids has
-// one digit per block); the scatter walks them 256 at a time in order with
+// Sort block b owns keys [blk.x, blk.y) of ONE segment (rs_blk, built on the
+// host); its digit-d count goes to hist[blk.z + d * blk.w], where blk.z =
+// 256 b0 + (b - b0) and blk.w = the segment's block count (b0 = its first
+// block).  One exclusive scan over hist in that (segment, digit, block)
+// order then yields every block's output offset for every digit: the
+// segments stay where they are and each is sorted by its codes, stably (a
+// face's order among equal codes is its input order).  The histogram counts
+// per warp slice (warp-aggregated by __match_any_sync, no shared-memory
+// atomics); the scatter walks the block's keys 256 at a time in order with
 // per-round warp-major offsets, so equal digits keep their input order.
 constexpr int RS_WARPS = RS_THREADS / 32;
 constexpr int RS_UNROLL = 4;
 
-// Per-warp digit counts of the warp's slice into wc[w][256] (zeroed by the caller).
-__device__ __forceinline__ void rs_warp_count(const uint32_t* __restrict__ keys, int n, int shift, int start,
+// Per-warp digit counts of keys [start, start + steps 32) & [.., end) into wc[256].
+__device__ __forceinline__ void rs_warp_count(const uint32_t* __restrict__ keys, int end, int shift, int start,
                                               int steps, uint32_t* wc) {
     const int lane = threadIdx.x & 31;
     for (int j0 = 0; j0 < steps; j0 += RS_UNROLL) {
@@ -272,12 +331,12 @@ __device__ __forceinline__ void rs_warp_count(const uint32_t* __restrict__ keys,
 #pragma unroll
         for (int u = 0; u < RS_UNROLL; ++u) {
             const int i = start + (j0 + u) * 32 + lane;
-            k[u] = (j0 + u < steps && i < n) ? __ldg(keys + i) : 0u;
+            k[u] = (j0 + u < steps && i < end) ? __ldg(keys + i) : 0u;
         }
 #pragma unroll
         for (int u = 0; u < RS_UNROLL; ++u) {
             const int i = start + (j0 + u) * 32 + lane;
-            const bool valid = j0 + u < steps && i < n;
+            const bool valid = j0 + u < steps && i < end;
             const int digit = valid ? (int)((k[u] >> shift) & 255u) : 256;
             const unsigned peers = __match_any_sync(FULL, digit);
             if (valid && (peers & ((1u << lane) - 1u)) == 0u) wc[digit] += __popc(peers);
@@ -286,67 +345,112 @@ __device__ __forceinline__ void rs_warp_count(const uint32_t* __restrict__ keys,
     }
 }
 
-__global__ void __launch_bounds__(RS_THREADS) k_rs_hist(const uint32_t* __restrict__ keys, int n, int shift,
-                                                        uint32_t* __restrict__ hist, int nblocks, int rounds) {
+__global__ void __launch_bounds__(RS_THREADS) k_rs_hist(const uint32_t* __restrict__ keys, const int4* __restrict__ blk,
+                                                        int shift, uint32_t* __restrict__ hist) {
     __shared__ uint32_t wc[RS_WARPS][256];
     for (int k = 0; k < RS_WARPS; ++k) wc[k][threadIdx.x] = 0;
     __syncthreads();
+    const int4 b = blk[blockIdx.x];
     const int w = threadIdx.x >> 5;
-    const int start = (blockIdx.x * RS_WARPS + w) * rounds * 32;
-    rs_warp_count(keys, n, shift, start, rounds, wc[w]);
+    rs_warp_count(keys, b.y, shift, b.x + w * RS_ROUNDS * 32, RS_ROUNDS, wc[w]);
     __syncthreads();
     uint32_t c = 0;
     for (int k = 0; k < RS_WARPS; ++k) c += wc[k][threadIdx.x];
-    hist[threadIdx.x * nblocks + blockIdx.x] = c;
+    hist[b.z + threadIdx.x * b.w] = c;
 }
 
-// single-CTA exclusive scan of hist[total] in place
-__global__ void k_rs_scan(uint32_t* hist, int total) {
-    __shared__ uint32_t warp_sums[32];
+// Exclusive scan of x[0, n) in place, three launches: per-chunk sums,
+// a one-CTA scan of the sums, per-chunk scans with the carried offset.
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* warp_sums, uint32_t* total) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    uint32_t x = v;
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(FULL, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_sums[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        uint32_t t = lane < nw ? warp_sums[lane] : 0u;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(FULL, t, o);
+            if (lane >= o) t += y;
+        }
+        if (lane < nw) warp_sums[lane] = t;  // inclusive
+    }
+    __syncthreads();
+    const uint32_t r = (w > 0 ? warp_sums[w - 1] : 0u) + x - v;
+    if (total) *total = warp_sums[nw - 1];
+    __syncthreads();
+    return r;
+}
+
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_sums(const uint32_t* __restrict__ x, int n,
+                                                            uint32_t* __restrict__ part) {
+    __shared__ uint32_t ws[32];
+    const int i0 = blockIdx.x * SCAN_CHUNK + 4 * threadIdx.x;
+    uint32_t v = 0;
+    for (int k = 0; k < 4; ++k) v += i0 + k < n ? x[i0 + k] : 0u;
+    uint32_t tot;
+    block_excl_scan(v, ws, &tot);
+    if (threadIdx.x == 0) part[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_top(uint32_t* part, int n) {
+    __shared__ uint32_t ws[32];
     __shared__ uint32_t carry;
     if (threadIdx.x == 0) carry = 0;
     __syncthreads();
-    int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    for (int base = 0; base < total; base += blockDim.x) {
-        int i = base + threadIdx.x;
-        uint32_t v = i < total ? hist[i] : 0u;
-        uint32_t x = v;
-        for (int o = 1; o < 32; o <<= 1) {
-            uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
-            if (lane >= o) x += y;
-        }
-        if (lane == 31) warp_sums[w] = x;
+    for (int base = 0; base < n; base += SCAN_THREADS) {
+        const int i = base + threadIdx.x;
+        const uint32_t v = i < n ? part[i] : 0u;
+        uint32_t tot;
+        const uint32_t e = block_excl_scan(v, ws, &tot);
+        if (i < n) part[i] = carry + e;
         __syncthreads();
-        if (w == 0) {
-            uint32_t s = lane < (int)(blockDim.x >> 5) ? warp_sums[lane] : 0u;
-            for (int o = 1; o < 32; o <<= 1) {
-                uint32_t y = __shfl_up_sync(0xFFFFFFFFu, s, o);
-                if (lane >= o) s += y;
-            }
-            if (lane < (int)(blockDim.x >> 5)) warp_sums[lane] = s;  // inclusive
-        }
-        __syncthreads();
-        uint32_t excl = carry + (w > 0 ? warp_sums[w - 1] : 0u) + x - v;
-        if (i < total) hist[i] = excl;
-        __syncthreads();
-        if (threadIdx.x == blockDim.x - 1) carry = excl + v;
+        if (threadIdx.x == 0) carry += tot;
         __syncthreads();
     }
 }
 
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_apply(uint32_t* x, int n, const uint32_t* __restrict__ part) {
+    __shared__ uint32_t ws[32];
+    const int i0 = blockIdx.x * SCAN_CHUNK + 4 * threadIdx.x;
+    uint32_t v[4], s = 0;
+    for (int k = 0; k < 4; ++k) {
+        v[k] = i0 + k < n ? x[i0 + k] : 0u;
+        s += v[k];
+    }
+    uint32_t e = part[blockIdx.x] + block_excl_scan(s, ws, nullptr);
+    for (int k = 0; k < 4; ++k)
+        if (i0 + k < n) {
+            x[i0 + k] = e;
+            e += v[k];
+        }
+}
+
+cudaError_t excl_scan(uint32_t* x, int n, uint32_t* part, cudaStream_t stream) {
+    const int nc = (n + SCAN_CHUNK - 1) / SCAN_CHUNK;
+    k_scan_sums<<<nc, SCAN_THREADS, 0, stream>>>(x, n, part);
+    k_scan_top<<<1, SCAN_THREADS, 0, stream>>>(part, nc);
+    k_scan_apply<<<nc, SCAN_THREADS, 0, stream>>>(x, n, part);
+    return cudaGetLastError();
+}
+
 __global__ void k_rs_scatter(const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin,
-                             uint32_t* __restrict__ kout, uint32_t* __restrict__ vout, int n,
-                             int shift, const uint32_t* __restrict__ hist, int nblocks, int rounds) {
+                             uint32_t* __restrict__ kout, uint32_t* __restrict__ vout, const int4* __restrict__ blk,
+                             int shift, const uint32_t* __restrict__ hist) {
     __shared__ uint32_t base[256];
     __shared__ uint32_t wc[RS_THREADS / 32][256];
-    base[threadIdx.x] = hist[threadIdx.x * nblocks + blockIdx.x];
+    const int4 b = blk[blockIdx.x];
+    base[threadIdx.x] = hist[b.z + threadIdx.x * b.w];
     int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const unsigned lt = (1u << lane) - 1u;
-    for (int r = 0; r < rounds; ++r) {
+    for (int r = 0; r < RS_ROUNDS; ++r) {
         for (int k = 0; k < RS_THREADS / 32; ++k) wc[k][threadIdx.x] = 0;
         __syncthreads();
-        int i = (blockIdx.x * rounds + r) * RS_THREADS + threadIdx.x;
-        bool valid = i < n;
+        int i = b.x + r * RS_THREADS + threadIdx.x;
+        bool valid = i < b.y;
         uint32_t key = valid ? kin[i] : 0u;
         uint32_t val = valid ? vin[i] : 0u;
         int digit = valid ? (int)((key >> shift) & 255u) : 256;
@@ -384,7 +488,8 @@ __device__ __forceinline__ int kdelta(const uint32_t* k, int n, int i, int j) {
 
 __global__ void k_karras(const BlasSeg* segs, const int* seg_of, const uint32_t* bounds, int Ftot,
                          const uint32_t* __restrict__ sk, int* __restrict__ child_all,
-                         int* __restrict__ node_parent_all, int* __restrict__ leaf_parent_all) {
+                         int* __restrict__ node_parent_all, int* __restrict__ leaf_parent_all,
+                         int2* __restrict__ range_all) {
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= Ftot) return;
     const SegCtx c = seg_ctx(segs, seg_of, bounds, g);
@@ -414,6 +519,7 @@ __global__ void k_karras(const BlasSeg* segs, const int* seg_of, const uint32_t*
     } while (t > 1);
     int gamma = i + s * d + (d < 0 ? -1 : 0);
     int lo = min(i, j), hi = max(i, j);
+    range_all[c.off + i] = make_int2(lo, hi);
     int left = (lo == gamma) ? ~gamma : gamma;
     int right = (hi == gamma + 1) ? ~(gamma + 1) : gamma + 1;
     child[2 * i] = left;
@@ -433,24 +539,36 @@ __device__ __forceinline__ int arrive(int* flag) {
     return a.fetch_add(1, cuda::memory_order_acq_rel);
 }
 
-__device__ __forceinline__ void load_box_cg(const float* p, float b[6]) {
-    for (int k = 0; k < 6; ++k) b[k] = __ldcg(p + k);
-}
 
 // Per-segment views of the scratch arrays used by K4/K4b/K5.
 #define AGR_SEG_VIEW(c)                                             \
-    const uint32_t* sorted_prim = sorted_all + (c).off;             \
     int* child = child_all + 2 * (c).off;                           \
-    float* ibox = ibox_all + 6 * (size_t)(c).off
+    float* ibox = ibox_all + BX * (size_t)(c).off
 #define AGR_SEG_PARENTS(c)                                          \
     int* node_parent = node_parent_all + (c).off;                   \
     int* leaf_parent = leaf_parent_all + (c).off
 
-__global__ void k_fit(const BlasSeg* segs, const int* seg_of, const uint32_t* bounds, int Ftot,
-                      const uint32_t* __restrict__ sorted_all, const float* tri_box, int* child_all,
-                      int* node_parent_all, int* leaf_parent_all, float* ibox_all, int* flags_all,
-                      int* height_all, int* size_all, int* depth) {
-    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+__device__ __forceinline__ int arrive_cta(int* flag) {
+    cuda::atomic_ref<int, cuda::thread_scope_block> a(*flag);
+    return a.fetch_add(1, cuda::memory_order_acq_rel);
+}
+
+// Arrivals at a node whose whole leaf range lies inside this thread block's
+// faces come only from threads of this block, so they synchronise through
+// a shared-memory flag at block scope (no device-wide fence); only nodes
+// straddling a block boundary (a few per cent) use the global flag and the
+// acq_rel device-scope atomic.  Internal node i's range contains leaf i, so
+// a block-local node's flag is its face slot in the block.
+__global__ void __launch_bounds__(T_BLK) k_fit(const BlasSeg* segs, const int* seg_of, const uint32_t* bounds,
+                                              int Ftot, const uint32_t* __restrict__ sorted_all, const float* tri_box,
+                                              int* child_all, int* node_parent_all, int* leaf_parent_all,
+                                              float* ibox_all, int* flags_all, int* depth,
+                                              const int2* __restrict__ range_all) {
+    __shared__ int sflag[T_BLK];
+    sflag[threadIdx.x] = 0;
+    __syncthreads();
+    const int blk0 = blockIdx.x * T_BLK;
+    const int g = blk0 + threadIdx.x;
     if (g >= Ftot) return;
     const SegCtx c = seg_ctx(segs, seg_of, bounds, g);
     const int n = c.n, p = g - c.off;
@@ -458,34 +576,47 @@ __global__ void k_fit(const BlasSeg* segs, const int* seg_of, const uint32_t* bo
     AGR_SEG_VIEW(c);
     AGR_SEG_PARENTS(c);
     int* flags = flags_all + c.off;
-    int* height = height_all + c.off;
-    int* size = size_all + c.off;
+    const int2* range = range_all + c.off;
+    const int lo_ok = blk0 - c.off, hi_ok = blk0 + T_BLK - c.off;  // block's faces, segment-local
     int node = leaf_parent[p];
     while (node >= 0) {
-        if (arrive(&flags[node]) == 0) return;  // first arrival: sibling not ready
+        const int2 r = __ldg(range + node);
+        const bool local = r.x >= lo_ok && r.y < hi_ok;
+        if (local ? arrive_cta(&sflag[c.off + node - blk0]) == 0 : arrive(&flags[node]) == 0)
+            return;  // first arrival: sibling not ready
         float b[6], cc[6];
         int h = 0, sz = 0;
         for (int side = 0; side < 2; ++side) {
-            int r = child[2 * node + side];
+            int rr = child[2 * node + side];
             float* dst = side == 0 ? b : cc;
-            if (r < 0) {
-                load_box_cg(tri_box + 6 * sorted_prim[~r], dst);
+            if (rr < 0) {
+                load_box_cg(tri_box + BX * (size_t)(c.off + ~rr), dst);
                 sz += 1;
             } else {
-                load_box_cg(ibox + 6 * r, dst);
-                h = max(h, __ldcg(height + r));
-                sz += __ldcg(size + r);
+                // a child's subtree size and height ride in its box record
+                const int2 w = local ? load_box_w(ibox + BX * rr, dst) : load_box_cg_w(ibox + BX * rr, dst);
+                sz += w.x;
+                h = max(h, w.y);
             }
         }
+        float u[6];
         for (int k = 0; k < 3; ++k) {
-            __stcg(ibox + 6 * node + k, fminf(b[k], cc[k]));
-            __stcg(ibox + 6 * node + 3 + k, fmaxf(b[3 + k], cc[3 + k]));
+            u[k] = fminf(b[k], cc[k]);
+            u[3 + k] = fmaxf(b[3 + k], cc[3 + k]);
         }
-        __stcg(height + node, h + 1);
-        __stcg(size + node, sz);
+        // one record per level: the stores before the next (device-scope)
+        // arrival are what its release waits for
+        store_box_w(ibox + BX * node, u, sz, h + 1);
         if (node == 0) depth[c.s] = h + 1;  // the root: the tree's depth in edges
         node = node_parent[node];
     }
+}
+
+// Subtree sizes out of the box records into their own array (read by the
+// treelet rounds and the collapses).
+__global__ void k_size_from_box(const float* __restrict__ ibox, int F, int* __restrict__ size) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < F) size[i] = __float_as_int(__ldg(ibox + BX * (size_t)i + 3));
 }
 
 // ---- K4b: treelet restructuring (TRBVH) ------------------------------------------------
@@ -548,16 +679,14 @@ __device__ __forceinline__ void subset_box(const TrbWarp& w, int sset, float b[6
 __device__ void trbvh_treelet(TrbWarp& w, int lane, int node, int off, const uint32_t* __restrict__ sorted_all,
                               const float* __restrict__ tri_box, int* child_all, int* node_parent_all,
                               int* leaf_parent_all, float* ibox_all, float* cost_all, int* size_all) {
-    const uint32_t* sorted_prim = sorted_all + off;
     int* child = child_all + 2 * off;
     int* node_parent = node_parent_all + off;
     int* leaf_parent = leaf_parent_all + off;
-    float* ibox = ibox_all + 6 * (size_t)off;
+    float* ibox = ibox_all + BX * (size_t)off;
     float* cost = cost_all + off;
     int* size = size_all + off;
     auto ref_box = [&](int r, float b[6]) {
-        const float* src = r < 0 ? tri_box + 6 * sorted_prim[~r] : ibox + 6 * r;
-        for (int c = 0; c < 6; ++c) b[c] = __ldcg(src + c);
+        load_box_cg(r < 0 ? tri_box + BX * (size_t)(off + ~r) : ibox + BX * r, b);
     };
     // treelet formation: open the largest-area subtree root until 7; the
     // two children of an opened node are fetched by lanes 0 and 1 at once
@@ -570,7 +699,7 @@ __device__ void trbvh_treelet(TrbWarp& w, int lane, int node, int off, const uin
         w.lc[lane] = r < 0 ? SAH_CT * w.la[lane] : __ldcg(cost + r);
     } else if (lane == 2) {
         float nb[6];
-        for (int c = 0; c < 6; ++c) nb[c] = __ldcg(ibox + 6 * node + c);
+        load_box_cg(ibox + BX * node, nb);
         w.ccur = SAH_CI * box_area(nb);
     }
     __syncwarp();
@@ -658,7 +787,7 @@ __device__ void trbvh_treelet(TrbWarp& w, int lane, int node, int off, const uin
                         st_n[sp++] = c;
                         float b[6];
                         subset_box(w, sub, b);
-                        for (int k = 0; k < 6; ++k) __stcg(ibox + 6 * c + k, b[k]);
+                        store_box_cg(ibox + BX * c, b);
                         __stcg(cost + c, w.copt[sub]);
                         int sz = 0;
                         for (int k = 0; k < TREELET; ++k)
@@ -711,15 +840,14 @@ __global__ void __launch_bounds__(TRB_THREADS) k_trbvh(
             if (!big) {
                 // small subtree: keep its topology, record its SAH cost
                 const int* child = child_all + 2 * off;
-                const uint32_t* sorted_prim = sorted_all + off;
-                const float* ibox = ibox_all + 6 * (size_t)off;
+                const float* ibox = ibox_all + BX * (size_t)off;
                 float b[6];
-                for (int c = 0; c < 6; ++c) b[c] = __ldcg(ibox + 6 * node + c);
+                load_box_cg(ibox + BX * node, b);
                 float cc = SAH_CI * box_area(b);
                 for (int side = 0; side < 2; ++side) {
                     const int r = __ldcg(child + 2 * node + side);
                     if (r < 0) {
-                        for (int c = 0; c < 6; ++c) b[c] = __ldcg(tri_box + 6 * sorted_prim[~r] + c);
+                        load_box_cg(tri_box + BX * (size_t)(off + ~r), b);
                         cc += SAH_CT * box_area(b);
                     } else {
                         cc += __ldcg(cost_all + off + r);
@@ -768,14 +896,14 @@ __global__ void k_depth(const BlasSeg* segs, const int* seg_of, const uint32_t* 
 }
 
 // ---- K5: pack -------------------------------------------------------------------------
-__device__ __forceinline__ void child_box(int r, const uint32_t* sorted_prim, const float* tri_box,
-                                          const float* ibox, float b[6]) {
+// Box of a binary ref: lbox = the segment's leaf boxes (sorted order), ibox
+// its internal-node boxes.
+__device__ __forceinline__ void child_box(int r, const float* lbox, const float* ibox, float b[6]) {
     if (r == REF_EMPTY) {
         for (int k = 0; k < 6; ++k) b[k] = __int_as_float(0x7f800000);  // +inf: never hit
         return;
     }
-    const float* src = r < 0 ? tri_box + 6 * sorted_prim[~r] : ibox + 6 * r;
-    for (int k = 0; k < 6; ++k) b[k] = __ldcg(src + k);
+    load_box_cg(r < 0 ? lbox + BX * (size_t)(~r) : ibox + BX * r, b);
 }
 
 __device__ __forceinline__ void write_node(float4* nodes, int g, const float a[6], const float b[6],
@@ -807,8 +935,8 @@ __global__ void k_pack_nodes(const BlasSeg* segs, const int* seg_of, const uint3
     else if (n == 1) { ra = ~0; rb = REF_EMPTY; }
     else { ra = REF_EMPTY; rb = REF_EMPTY; }
     float a[6], b[6];
-    child_box(ra, sorted_prim, tri_box, ibox, a);
-    child_box(rb, sorted_prim, tri_box, ibox, b);
+    child_box(ra, tri_box + BX * (size_t)c.off, ibox, a);
+    child_box(rb, tri_box + BX * (size_t)c.off, ibox, b);
     write_node(nodes, node_base + i, a, b, global_ref(ra, node_base, leaf_base),
                global_ref(rb, node_base, leaf_base));
 }
@@ -832,7 +960,7 @@ __global__ void k_collapse(const BlasSeg* segs, const int* seg_of, const uint32_
     if (n > 1) {
         auto ch = [&](int r, int side) { return __ldg(child + 2 * r + side); };
         auto bx = [&](int r, float bb[6]) {
-            for (int k = 0; k < 6; ++k) bb[k] = __ldcg(ibox + 6 * r + k);
+            load_box_cg(ibox + BX * r, bb);
         };
         cnt = collapse_w<W>(j, ch, bx, refs, AGR_KEEP_PAIRS != 0);
     } else {
@@ -843,7 +971,7 @@ __global__ void k_collapse(const BlasSeg* segs, const int* seg_of, const uint32_
     float boxes[W][6];
     int gr[W];
     for (int k = 0; k < W; ++k) {
-        child_box(refs[k], sorted_prim, tri_box, ibox, boxes[k]);
+        child_box(refs[k], tri_box + BX * (size_t)c.off, ibox, boxes[k]);
         gr[k] = global_ref(refs[k], node_base, leaf_base);
         // (subtree sizes from the fit / TRBVH: only subtrees of <= LEAF_MAX
         // leaves are walked)
@@ -878,9 +1006,241 @@ __global__ void k_collapse(const BlasSeg* segs, const int* seg_of, const uint32_
     }
 }
 
+// ---- K5b': compacted BVH4 ------------------------------------------------------
+// The greedy collapse keeps only the binary nodes it does not open as BVH4
+// nodes (about a fifth with pair leaves), so writing a BVH4 node for every
+// binary node (k_collapse<4>) moved ~5x the bytes the traversal can reach
+// and did ~5x the work.  Here the BVH4 is built top-down, one level per grid
+// barrier of a single cooperative launch: a queue of (binary node, BVH4
+// slot) pairs; each is collapsed, gets slots for its internal children from
+// its segment's counter (the root is slot 0) and writes its node at once.
+// Slot order within a level depends on the schedule, so the node numbering
+// (not the tree) may differ between builds; results do not.
+// A slot of a collapse: a leaf, a pair leaf (binary subtree over <= LEAF_MAX
+// consecutive leaves, referenced as one multi-triangle leaf) or an internal
+// node that becomes a BVH4 node of its own (returns -1 with *internal set).
+// (size_r < 0: read the subtree size from size[r])
+__device__ __forceinline__ int slot_ref(int r, const int* child, const int* size, int leaf_base, bool* internal,
+                                        int size_r = -1) {
+    *internal = false;
+    if (r == REF_EMPTY) return REF_EMPTY;
+    if (r < 0) return ~(leaf_base + ~r);
+    if (LEAF_MAX > 1 && (size_r >= 0 ? size_r : __ldcg(size + r)) <= LEAF_MAX) {
+        int st[2 * LEAF_MAX], sp = 0, nl = 0, lmin = INT_MAX, lmax = -1;
+        bool ok = true;
+        st[sp++] = r;
+        while (sp > 0 && ok) {
+            const int x = st[--sp];
+            if (x < 0) {
+                ok = nl < LEAF_MAX;
+                ++nl;
+                lmin = min(lmin, ~x);
+                lmax = max(lmax, ~x);
+            } else if (sp + 2 <= 2 * LEAF_MAX) {
+                st[sp++] = __ldcg(child + 2 * x + 1);
+                st[sp++] = __ldcg(child + 2 * x);
+            } else {
+                ok = false;
+            }
+        }
+        if (ok && lmax - lmin + 1 == nl) return ~((leaf_base + lmin) | ((nl - 1) << LEAF_SHIFT));
+    }
+    *internal = true;
+    return -1;
+}
+
+__global__ void k_reach_init(const BlasSeg* segs, int B, const uint32_t* bounds, int* seg4, int2* queue,
+                             int* qctl) {
+    const int sgi = blockIdx.x * blockDim.x + threadIdx.x;
+    if (sgi >= B) return;
+    const bool tree = (int)bounds[8 * sgi + 7] >= 2;  // else a single-leaf / empty BLAS: no binary root
+    seg4[sgi] = 1;
+    if (tree) queue[atomicAdd(qctl + 2, 1)] = make_int2(segs[sgi].off, 0);  // level 0
+}
+
+__device__ __forceinline__ void read_rec(const float4* rec, float a[6], float b[6], int& ra, int& rb, int& xa,
+                                         int& xb) {
+    const float4 q0 = __ldcg(rec), q1 = __ldcg(rec + 1), q2 = __ldcg(rec + 2), q3 = __ldcg(rec + 3);
+    a[0] = q0.x; a[1] = q0.y; a[2] = q0.z; a[3] = q0.w; a[4] = q1.x; a[5] = q1.y;
+    b[0] = q1.z; b[1] = q1.w; b[2] = q2.x; b[3] = q2.y; b[4] = q2.z; b[5] = q2.w;
+    ra = __float_as_int(q3.x); rb = __float_as_int(q3.y); xa = __float_as_int(q3.z); xb = __float_as_int(q3.w);
+}
+
+__global__ void k_make_rec(const BlasSeg* segs, const int* seg_of, const uint32_t* bounds, int Ftot,
+                           const float* __restrict__ tri_box, const int* __restrict__ child_all,
+                           const float* __restrict__ ibox_all, const int* __restrict__ size_all, float4* rec_all) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= Ftot) return;
+    const SegCtx c = seg_ctx(segs, seg_of, bounds, g);
+    const int i = g - c.off;
+    if (c.n < 2 || i >= c.n - 1) return;
+    const int* child = child_all + 2 * c.off;
+    const float* lbox = tri_box + BX * (size_t)c.off;
+    const float* ibox = ibox_all + BX * (size_t)c.off;
+    const int* size = size_all ? size_all + c.off : nullptr;
+    const int leaf_base = segs[c.s].leaf_base;
+    int r[2], x[2];
+    float bb[2][6];
+    for (int k = 0; k < 2; ++k) {
+        r[k] = __ldg(child + 2 * i + k);
+        x[k] = 0;
+        if (r[k] >= 0) {
+            // subtree size: from the fit's box record, or from size[] after treelet rounds
+            const int2 w = load_box_cg_w(ibox + BX * r[k], bb[k]);
+            bool internal;
+            x[k] = slot_ref(r[k], child, size, leaf_base, &internal, size ? -1 : w.x);
+            if (internal) x[k] = 0;
+        } else {
+            child_box(r[k], lbox, ibox, bb[k]);
+        }
+    }
+    write_rec(rec_all + 4 * (size_t)g, bb[0], bb[1], r[0], r[1], x[0], x[1]);
+}
+
+// One cooperative launch: level L's items are queue[begin_L, begin_L + n_L)
+// (n_L = qctl[2 + L]); each is collapsed (the greedy largest-area opening of
+// collapse_w, from the child records) and written, and its internal slots
+// are appended as level L + 1 through their own counter qctl[3 + L]
+// (warp-aggregated), so one grid barrier per level suffices.
+__global__ void __launch_bounds__(T_BLK) k_bvh4_topdown(const BlasSeg* segs, const int* seg_of,
+                                                       const float4* __restrict__ rec_all, int* seg4, int2* queue,
+                                                       int* qctl, float4* nodes) {
+    cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+    const int lane = threadIdx.x & 31;
+    const int stride = gridDim.x * blockDim.x;
+    int begin = 0, L = 0;
+    int n_lvl = *(volatile int*)(qctl + 2);  // level 0: the roots (k_reach_init)
+    while (n_lvl > 0 && L + 1 < MAX_LEVELS) {
+        const int next = begin + n_lvl;
+        for (int t0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31); t0 < n_lvl; t0 += stride) {
+            const int t = t0 + lane;
+            int2 push[4];
+            int npush = 0;
+            if (t < n_lvl) {
+                const int2 item = __ldcg(queue + begin + t);
+                const int x = item.x;
+                const int sgi = __ldg(seg_of + x);
+                const BlasSeg& S = segs[sgi];
+                const int off = S.off;
+                const float4* rec = rec_all + 4 * (size_t)off;
+                float bx[4][6];
+                int refs[4] = {REF_EMPTY, REF_EMPTY, REF_EMPTY, REF_EMPTY}, aux[4] = {0, 0, 0, 0};
+                read_rec(rec + 4 * (size_t)(x - off), bx[0], bx[1], refs[0], refs[1], aux[0], aux[1]);
+                int cnt = 2;
+                while (cnt < 4) {  // collapse_w<4>: open the largest-area internal member
+                    int best = -1;
+                    float best_a = -1.0f;
+                    for (int k = 0; k < cnt; ++k)
+                        if (refs[k] >= 0) {
+                            const float a = half_area(bx[k]);
+                            if (a > best_a) { best_a = a; best = k; }
+                        }
+                    if (best < 0) break;
+                    float ca[6], cb[6];
+                    int ra, rb, xa, xb;
+                    read_rec(rec + 4 * (size_t)refs[best], ca, cb, ra, rb, xa, xb);
+                    for (int k = 3; k > best + 1; --k)
+                        if (k <= cnt) {
+                            refs[k] = refs[k - 1];
+                            aux[k] = aux[k - 1];
+                            for (int q = 0; q < 6; ++q) bx[k][q] = bx[k - 1][q];
+                        }
+                    refs[best] = ra; aux[best] = xa;
+                    refs[best + 1] = rb; aux[best + 1] = xb;
+                    for (int q = 0; q < 6; ++q) { bx[best][q] = ca[q]; bx[best + 1][q] = cb[q]; }
+                    ++cnt;
+                }
+                int gr[4];
+                bool internal[4];
+                for (int k = 0; k < 4; ++k) {
+                    internal[k] = false;
+                    if (k >= cnt) {
+                        refs[k] = REF_EMPTY;
+                        for (int q = 0; q < 6; ++q) bx[k][q] = __int_as_float(0x7f800000);  // +inf: never hit
+                        gr[k] = REF_EMPTY;
+                    } else if (refs[k] < 0) {
+                        gr[k] = ~(S.leaf_base + ~refs[k]);
+                    } else if (aux[k] != 0) {
+                        gr[k] = aux[k];  // a closed subtree over <= LEAF_MAX consecutive leaves
+                    } else {
+                        internal[k] = true;
+                        ++npush;
+                    }
+                }
+                // child slots from the segment counter, one atomic per segment per warp
+                int first = 0;
+                {
+                    const unsigned grp = __match_any_sync(__activemask(), sgi);
+                    const int leader = __ffs(grp) - 1;
+                    const unsigned below = grp & ((1u << lane) - 1u);
+                    int tot = npush, pre = 0;
+                    for (unsigned m = grp; m; m &= m - 1) {
+                        const int l = __ffs(m) - 1;
+                        const int v = __shfl_sync(grp, npush, l);
+                        if (l != lane) tot += v;
+                        if ((1u << l) & below) pre += v;
+                    }
+                    int base = 0;
+                    if (lane == leader && tot) base = atomicAdd(seg4 + sgi, tot);
+                    first = __shfl_sync(grp, base, leader) + pre;
+                }
+                int q = 0;
+                for (int k = 0; k < 4; ++k)
+                    if (internal[k]) {
+                        const int slot = first + q;
+                        gr[k] = S.node_base + slot;
+                        push[q++] = make_int2(off + refs[k], slot);
+                    }
+                write_node4(nodes, S.node_base + item.y, reinterpret_cast<const float(*)[6]>(bx), gr, cnt);
+            }
+            // warp-aggregated append of the next level
+            unsigned incl = npush;
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned y = __shfl_up_sync(FULL, incl, o);
+                if (lane >= o) incl += y;
+            }
+            const unsigned tot = __shfl_sync(FULL, incl, 31);
+            int base = 0;
+            if (lane == 31 && tot) base = atomicAdd(qctl + 3 + L, (int)tot);
+            base = __shfl_sync(FULL, base, 31);
+            const int pos = next + base + (int)(incl - npush);
+            for (int k = 0; k < npush; ++k) queue[pos + k] = push[k];
+        }
+        grid.sync();
+        begin = next;
+        ++L;
+        n_lvl = *(volatile int*)(qctl + 2 + L);
+    }
+}
+
+// A BLAS with fewer than 2 leaves has no binary node: its BVH4 root holds
+// the single leaf (or nothing).
+__global__ void k_write4_small(const BlasSeg* segs, int B, const uint32_t* bounds, const uint32_t* sorted_all,
+                               const float* tri_box, float4* nodes) {
+    const int sgi = blockIdx.x * blockDim.x + threadIdx.x;
+    if (sgi >= B) return;
+    const int n = (int)bounds[8 * sgi + 7];
+    if (n >= 2) return;
+    const BlasSeg& S = segs[sgi];
+    float boxes[4][6];
+    int gr[4];
+    const int r0 = n == 1 ? ~0 : REF_EMPTY;
+    child_box(r0, tri_box + BX * (size_t)S.off, nullptr, boxes[0]);
+    gr[0] = global_ref(r0, S.node_base, S.leaf_base);
+    for (int k = 1; k < 4; ++k) {
+        child_box(REF_EMPTY, nullptr, nullptr, boxes[k]);
+        gr[k] = REF_EMPTY;
+    }
+    write_node4(nodes, S.node_base, reinterpret_cast<const float(*)[6]>(boxes), gr, n == 1 ? 1 : 0);
+}
+
+// Leaf records in sorted order, right after the sort: the 48-B triangle
+// record, the exact vertices (3 x float4) and the leaf's box for the
+// hierarchy passes (so they read leaf boxes by position, coalesced, instead
+// of gathering them by face id).
 __global__ void k_pack_tris(const BlasSeg* segs, const int* seg_of, const uint32_t* bounds, int Ftot,
                             const uint32_t* __restrict__ sorted_all, const uint32_t* __restrict__ sk,
-                            float4* tris, float* triv, uint32_t* dbg_morton) {
+                            float4* tris, float* triv, uint32_t* dbg_morton, float* __restrict__ lbox) {
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= Ftot) return;
     const SegCtx c = seg_ctx(segs, seg_of, bounds, g);
@@ -906,15 +1266,21 @@ __global__ void k_pack_tris(const BlasSeg* segs, const int* seg_of, const uint32
     // the asset-local face id (a part's faces are a subset of its asset's)
     const int face_id = S.face_ids ? S.face_ids[f] : f;
     tris[3 * gl + 2] = make_float4((float)E2.x, (float)E2.y, (float)E2.z, __int_as_float(face_id));
+    float4* tv = reinterpret_cast<float4*>(triv) + 3 * (size_t)gl;
+    tv[0] = make_float4(a[0], a[1], a[2], 0.0f);
+    tv[1] = make_float4(b[0], b[1], b[2], 0.0f);
+    tv[2] = make_float4(cc[0], cc[1], cc[2], 0.0f);
+    float bb[6];
     for (int k = 0; k < 3; ++k) {
-        triv[9 * gl + k] = a[k];
-        triv[9 * gl + 3 + k] = b[k];
-        triv[9 * gl + 6 + k] = cc[k];
+        bb[k] = fminf(a[k], fminf(b[k], cc[k]));
+        bb[3 + k] = fmaxf(a[k], fmaxf(b[k], cc[k]));
     }
+    store_box(lbox + BX * (size_t)g, bb);
 }
 
 __global__ void k_asset_info(const BlasSeg* segs, int B, const uint32_t* bounds, const float* ibox_all,
-                             const float* tri_box, const uint32_t* sorted_all, const int* depth) {
+                             const float* tri_box, const uint32_t* sorted_all, const int* depth,
+                             const int* seg4) {
     const int s = blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= B) return;
     const BlasSeg& S = segs[s];
@@ -926,12 +1292,13 @@ __global__ void k_asset_info(const BlasSeg* segs, int B, const uint32_t* bounds,
     a.n_faces = S.n_faces;
     a.radius = ordered_to_float(bounds[8 * s + 6]);
     a.depth = n > 1 ? depth[s] : 1;
+    a.n_nodes4 = seg4[s];
     if (n > 1) {
-        const float* r = ibox_all + 6 * (size_t)S.off;  // local internal node 0 = root
-        for (int k = 0; k < 3; ++k) { a.lo[k] = r[k]; a.hi[k] = r[3 + k]; }
+        const float* r = ibox_all + BX * (size_t)S.off;  // local internal node 0 = root
+        for (int k = 0; k < 3; ++k) { a.lo[k] = r[k]; a.hi[k] = r[4 + k]; }
     } else if (n == 1) {
-        const float* b = tri_box + 6 * sorted_all[S.off];
-        for (int k = 0; k < 3; ++k) { a.lo[k] = b[k]; a.hi[k] = b[3 + k]; }
+        const float* b = tri_box + BX * (size_t)S.off;
+        for (int k = 0; k < 3; ++k) { a.lo[k] = b[k]; a.hi[k] = b[4 + k]; }
     } else {
         for (int k = 0; k < 3; ++k) { a.lo[k] = 0.0f; a.hi[k] = 0.0f; }
     }
@@ -942,6 +1309,11 @@ __global__ void k_asset_info(const BlasSeg* segs, int B, const uint32_t* bounds,
 
 size_t blas_scratch_bytes(int64_t total_faces, int n_segs) {
     return scratch_layout(total_faces, n_segs, nullptr, nullptr);
+}
+
+size_t blas_stage_bytes(int64_t total_faces, int n_segs) {
+    return ((sizeof(BlasSeg) * (size_t)n_segs + 15) & ~size_t(15)) +
+           sizeof(int4) * (size_t)rs_max_blocks(total_faces, n_segs);
 }
 
 cudaError_t blas_build_batch(BlasSeg* h_segs, int B, const BlasBatchArgs& a, void* scratch,
@@ -956,31 +1328,52 @@ cudaError_t blas_build_batch(BlasSeg* h_segs, int B, const BlasBatchArgs& a, voi
     const int F = (int)F64;
     Scratch s;
     scratch_layout(F, B, scratch, &s);
-    cudaError_t e = cudaMemcpyAsync(s.segs, h_segs, sizeof(BlasSeg) * B, cudaMemcpyHostToDevice, stream);
+    // the segment table and the sort-block table (below) go up in one copy,
+    // from pinned staging when the caller provides it (a pageable copy
+    // would wait for the stream to drain first)
+    std::vector<int4> blk;
+    for (int g = 0; g < B; ++g) {
+        const int nbs = (h_segs[g].n_faces + RS_TILE - 1) / RS_TILE;
+        const int b0 = (int)blk.size();
+        for (int q = 0; q < nbs; ++q) {
+            const int st = h_segs[g].off + q * RS_TILE;
+            blk.push_back(make_int4(st, min(st + RS_TILE, h_segs[g].off + h_segs[g].n_faces), 256 * b0 + q, nbs));
+        }
+    }
+    const int nb = (int)blk.size();
+    const size_t seg_bytes = sizeof(BlasSeg) * B, blk_off = (seg_bytes + 15) & ~size_t(15),
+                 blk_bytes = sizeof(int4) * nb;
+    cudaError_t e;
+    if (a.h_stage && blk_off + blk_bytes <= a.h_stage_bytes) {
+        e = cudaEventSynchronize(a.stage_free);  // the previous build's upload has left the buffer
+        if (e != cudaSuccess) return e;
+        memcpy(a.h_stage, h_segs, seg_bytes);
+        memcpy((char*)a.h_stage + blk_off, blk.data(), blk_bytes);
+        e = cudaMemcpyAsync(s.segs, a.h_stage, seg_bytes, cudaMemcpyHostToDevice, stream);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(s.rs_blk, (char*)a.h_stage + blk_off, blk_bytes, cudaMemcpyHostToDevice, stream);
+        if (e == cudaSuccess) e = cudaEventRecord(a.stage_free, stream);
+    } else {
+        e = cudaMemcpyAsync(s.segs, h_segs, seg_bytes, cudaMemcpyHostToDevice, stream);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(s.rs_blk, blk.data(), blk_bytes, cudaMemcpyHostToDevice, stream);
+    }
     if (e != cudaSuccess) return e;
     const int gb = (F + T_BLK - 1) / T_BLK;
     k_seg_of<<<B, T_BLK, 0, stream>>>(s.segs, s.seg_of);
     k_init_bounds<<<(8 * B + T_BLK - 1) / T_BLK, T_BLK, 0, stream>>>(s.bounds, B);
     k_radius<<<B, 128, 0, stream>>>(s.segs, s.bounds);
-    k_tri_prep<<<gb, T_BLK, 0, stream>>>(s.segs, s.seg_of, F, s.tri_box, s.vals[1], s.bounds);
-    k_morton<<<gb, T_BLK, 0, stream>>>(s.seg_of, s.tri_box, s.vals[1], F, s.bounds, s.mcode, s.keys[0],
+    k_tri_prep<<<gb, T_BLK, 0, stream>>>(s.segs, s.seg_of, F, s.cent, s.vals[1], s.bounds);
+    k_morton<<<gb, T_BLK, 0, stream>>>(s.seg_of, s.cent, s.vals[1], F, s.bounds, s.mcode, s.keys[0],
                                        s.vals[0]);
-    const int rounds = rs_rounds(F);
-    const int nb = (F + RS_THREADS * rounds - 1) / (RS_THREADS * rounds);
+    // sort: segment-local blocks of RS_TILE keys (see K2), 4 passes
     int cur = 0;
-    auto pass = [&](int shift) {
-        k_rs_hist<<<nb, RS_THREADS, 0, stream>>>(s.keys[cur], F, shift, s.hist, nb, rounds);
-        k_rs_scan<<<1, 1024, 0, stream>>>(s.hist, 256 * nb);
-        k_rs_scatter<<<nb, RS_THREADS, 0, stream>>>(s.keys[cur], s.vals[cur], s.keys[cur ^ 1],
-                                                    s.vals[cur ^ 1], F, shift, s.hist, nb, rounds);
+    for (int shift = 0; shift < 32; shift += 8) {
+        k_rs_hist<<<nb, RS_THREADS, 0, stream>>>(s.keys[cur], s.rs_blk, shift, s.hist);
+        e = excl_scan(s.hist, 256 * nb, s.scan_part, stream);
+        if (e != cudaSuccess) return e;
+        k_rs_scatter<<<nb, RS_THREADS, 0, stream>>>(s.keys[cur], s.vals[cur], s.keys[cur ^ 1], s.vals[cur ^ 1],
+                                                    s.rs_blk, shift, s.hist);
         cur ^= 1;
-    };
-    for (int shift = 0; shift < 32; shift += 8) pass(shift);
-    if (B > 1) {
-        // stable passes over the segment id: (segment, code) order
-        k_key_from<<<gb, T_BLK, 0, stream>>>(s.vals[cur], nullptr, s.seg_of, F, s.keys[cur]);
-        for (int shift = 0; shift < 32 && ((unsigned)(B - 1) >> shift) != 0u; shift += 8) pass(shift);
-        k_key_from<<<gb, T_BLK, 0, stream>>>(s.vals[cur], s.mcode, nullptr, F, s.keys[cur]);
     }
     // everything below reads each segment's leaf count from the device (no
     // host round trip: builds stay async)
@@ -988,10 +1381,16 @@ cudaError_t blas_build_batch(BlasSeg* h_segs, int B, const BlasBatchArgs& a, voi
     const uint32_t* sv = s.vals[cur];
     cudaMemsetAsync(s.depth, 0, sizeof(int) * B, stream);
     cudaMemsetAsync(s.flags, 0, sizeof(int) * F, stream);
+    k_pack_tris<<<gb, T_BLK, 0, stream>>>(s.segs, s.seg_of, s.bounds, F, sv, sk, a.tris, a.triv, a.dbg_morton,
+                                          s.tri_box);
     k_karras<<<gb, T_BLK, 0, stream>>>(s.segs, s.seg_of, s.bounds, F, sk, s.child, s.node_parent,
-                                       s.leaf_parent);
+                                       s.leaf_parent, s.range);
     k_fit<<<gb, T_BLK, 0, stream>>>(s.segs, s.seg_of, s.bounds, F, sv, s.tri_box, s.child, s.node_parent,
-                                    s.leaf_parent, s.ibox, s.flags, s.height, s.size, s.depth);
+                                    s.leaf_parent, s.ibox, s.flags, s.depth, s.range);
+    // subtree sizes into their own array for the treelet rounds / the BVH8
+    // collapse (the BVH4 path reads them from the box records)
+    const bool need_size = a.trbvh_rounds > 0 || a.nodes8 != nullptr;
+    if (need_size) k_size_from_box<<<gb, T_BLK, 0, stream>>>(s.ibox, F, s.size);
     for (int round = 0; round < a.trbvh_rounds; ++round) {
         cudaMemsetAsync(s.flags, 0, sizeof(int) * F, stream);
         k_trbvh<<<(F + TRB_THREADS - 1) / TRB_THREADS, TRB_THREADS, 0, stream>>>(s.segs, s.seg_of, s.bounds, F, sv, s.tri_box, s.child,
@@ -1007,14 +1406,46 @@ cudaError_t blas_build_batch(BlasSeg* h_segs, int B, const BlasBatchArgs& a, voi
     if (a.bnodes)
         k_pack_nodes<<<gb, T_BLK, 0, stream>>>(s.segs, s.seg_of, s.bounds, F, sv, s.tri_box, s.child, s.ibox,
                                                a.bnodes);
-    k_collapse<4><<<gb, T_BLK, 0, stream>>>(s.segs, s.seg_of, s.bounds, F, sv, s.tri_box, s.child, s.ibox,
-                                            s.size, a.nodes);
+    {
+    // compacted BVH4 (K5b'): top-down, one cooperative launch
+    cudaMemsetAsync(s.qctl, 0, sizeof(int) * (2 + MAX_LEVELS), stream);
+    k_make_rec<<<gb, T_BLK, 0, stream>>>(s.segs, s.seg_of, s.bounds, F, s.tri_box, s.child, s.ibox,
+                                         a.trbvh_rounds > 0 ? s.size : nullptr, s.rec);
+    k_reach_init<<<(B + 127) / 128, 128, 0, stream>>>(s.segs, B, s.bounds, s.seg4, s.queue, s.qctl);
+    {
+        static int coop_blocks = 0;  // co-resident blocks (device 0's count serves all B200s)
+        int dev = 0, sms = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (coop_blocks == 0) {
+            int per_sm = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bvh4_topdown, T_BLK, 0);
+            coop_blocks = sms * (per_sm < 1 ? 1 : per_sm);
+        }
+        // every co-resident block: the levels are latency-bound chains of
+        // dependent loads, so more threads in flight beat cheaper barriers
+#ifndef AGR_TOPDOWN_PER_SM
+#define AGR_TOPDOWN_PER_SM 64
+#endif
+        const int grid = AGR_TOPDOWN_PER_SM * sms < coop_blocks ? AGR_TOPDOWN_PER_SM * sms : coop_blocks;
+        const BlasSeg* a0 = s.segs;
+        const int* a1 = s.seg_of;
+        const float4* a2 = s.rec;
+        int* a3 = s.seg4;
+        int2* a4 = s.queue;
+        int* a5 = s.qctl;
+        float4* a6 = a.nodes;
+        void* args[] = {&a0, &a1, &a2, &a3, &a4, &a5, &a6};
+        e = cudaLaunchCooperativeKernel((const void*)k_bvh4_topdown, dim3(grid), dim3(T_BLK), args, 0, stream);
+        if (e != cudaSuccess) return e;
+    }
+    }
+    k_write4_small<<<(B + 127) / 128, 128, 0, stream>>>(s.segs, B, s.bounds, sv, s.tri_box, a.nodes);
     if (a.nodes8)
         k_collapse<8><<<gb, T_BLK, 0, stream>>>(s.segs, s.seg_of, s.bounds, F, sv, s.tri_box, s.child, s.ibox,
                                                 s.size, a.nodes8);
-    k_pack_tris<<<gb, T_BLK, 0, stream>>>(s.segs, s.seg_of, s.bounds, F, sv, sk, a.tris, a.triv,
-                                          a.dbg_morton);
-    k_asset_info<<<(B + 127) / 128, 128, 0, stream>>>(s.segs, B, s.bounds, s.ibox, s.tri_box, sv, s.depth);
+    k_asset_info<<<(B + 127) / 128, 128, 0, stream>>>(s.segs, B, s.bounds, s.ibox, s.tri_box, sv, s.depth,
+                                                      s.seg4);
     return cudaGetLastError();
 }
 

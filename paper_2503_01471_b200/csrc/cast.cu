@@ -116,14 +116,15 @@ struct Ray64 { d3 o, d; };
 // double-sided); returns the ray parameter t of the plane hit.
 __device__ __forceinline__ bool tri64(const SceneView& sv, int inst, int leaf, const Ray64& r, double& t) {
     const float* T = sv.inst_T + 12 * inst;
-    const float* v = sv.triv + 9 * leaf;
+    const float4* v = reinterpret_cast<const float4*>(sv.triv) + 3 * (size_t)leaf;
     double A[12];
 #pragma unroll
     for (int k = 0; k < 12; ++k) A[k] = (double)__ldg(T + k);
     d3 w[3];
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-        double x = __ldg(v + 3 * c), y = __ldg(v + 3 * c + 1), z = __ldg(v + 3 * c + 2);
+        const float4 q = __ldg(v + c);
+        double x = q.x, y = q.y, z = q.z;
         w[c].x = A[0] * x + A[1] * y + A[2] * z + A[3];
         w[c].y = A[4] * x + A[5] * y + A[6] * z + A[7];
         w[c].z = A[8] * x + A[9] * y + A[10] * z + A[11];
@@ -1257,10 +1258,11 @@ __device__ __noinline__ void write_extra(const CastArgs* a, RayId id, Best64 bes
         return;
     }
     const float* T = a->sv.inst_T + 12 * best.inst;
-    const float* v = a->sv.triv + 9 * best.leaf;
+    const float4* v = reinterpret_cast<const float4*>(a->sv.triv) + 3 * (size_t)best.leaf;
     d3 w[3];
     for (int c = 0; c < 3; ++c) {
-        double x = v[3 * c], y = v[3 * c + 1], z = v[3 * c + 2];
+        const float4 q = v[c];
+        double x = q.x, y = q.y, z = q.z;
         w[c].x = (double)T[0] * x + (double)T[1] * y + (double)T[2] * z + (double)T[3];
         w[c].y = (double)T[4] * x + (double)T[5] * y + (double)T[6] * z + (double)T[7];
         w[c].z = (double)T[8] * x + (double)T[9] * y + (double)T[10] * z + (double)T[11];

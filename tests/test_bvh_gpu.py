@@ -8,7 +8,9 @@ import numpy as np
 import pytest
 
 import scenegen as sg
-from gpu_util import make_scene
+import torch
+
+from gpu_util import dev, make_scene
 
 pytestmark = pytest.mark.gpu
 
@@ -217,6 +219,41 @@ def test_bvh4_blas_covers_every_leaf_once(mesh_fn):
     # greedy collapse: nodes have up to 4 children, most internal nodes 4
     cnt = nodes[:, 28].view(np.int32)
     assert cnt.max() <= 4
+
+
+@pytest.mark.parametrize("trbvh_rounds", [0, 3])
+def test_bvh4_blas_is_compact_and_reachable(trbvh_rounds):
+    """The BLAS BVH4 is compacted at every build (blas.cu K5b'): the export
+    holds exactly the nodes reachable from the root, each reached once, the
+    root first, internal refs in range; far fewer nodes than binary nodes;
+    the same after a batched mesh update (the c6 path)."""
+    meshes = [sg.terrain_mesh(np.random.default_rng(3), n=32), sg.sphere_mesh(1.0, 3), sg.cube_mesh()]
+    sc = sg.assemble(meshes, [[(a, a + 1, sg.make_T(np.eye(3), (0, 0, 0)))] for a in range(3)])
+    s = make_scene(sc, build=False, trbvh_rounds=trbvh_rounds, parts=False)
+    for step in range(2):
+        if step == 1:
+            v = np.concatenate([m.verts * 1.1 + 0.05 for m in meshes]).astype(np.float32)
+            s.update_meshes([0, 1, 2], torch.from_numpy(v).to(dev()))
+            torch.cuda.synchronize()
+        for a, m in enumerate(meshes):
+            nodes, root = s.debug_export_bvh4(a)
+            refs = nodes[:, 24:28].view(np.int32)
+            seen = np.zeros(len(nodes), np.int32)
+            stack = [root]
+            while stack:
+                n = stack.pop()
+                assert root <= n < root + len(nodes)
+                seen[n - root] += 1
+                stack.extend(int(r) for r in refs[n - root] if r >= 0)
+            assert np.all(seen == 1), (a, step)
+            if len(m.faces) > 100:
+                assert len(nodes) < 0.6 * (len(m.faces) - 1), (a, len(nodes))
+            tri = (m.verts * (1.1 if step else 1.0) + (0.05 if step else 0.0)).astype(np.float32)[m.faces]
+            if step == 0:
+                lb = sum(len(mm.faces) for mm in meshes[:a])  # the asset's first leaf record
+                leaves = _walk_bvh4(nodes, root, lambda l, t=tri, lf=s.debug_export_blas(a)[1]:
+                                    (t[lf[l - lb]].min(0), t[lf[l - lb]].max(0)))
+                assert sorted(leaves) == list(range(lb, lb + len(m.faces)))
 
 
 def test_bvh4_tlas_covers_every_instance_once():

@@ -574,6 +574,21 @@ def test_update_mesh_per_env_unique_and_deforming():
         s.debug_export_blas(0)
 
 
+def _bvh4_canonical(nodes, root):
+    """A BLAS BVH4 export as a nested tuple from its root (child boxes as
+    bits, leaf refs as stored, internal children recursively): equal for
+    equal trees whatever the node numbering."""
+    refs = nodes[:, 24:28].view(np.int32)
+    bits = nodes[:, :24].view(np.uint32)
+
+    def rec(n):
+        out = [bits[n].tobytes()]
+        for r in refs[n]:
+            out.append(rec(int(r) - root) if r >= 0 else int(r))
+        return tuple(out)
+    return rec(0)
+
+
 def test_update_meshes_batched_equals_one_by_one():
     """agr_update_meshes rebuilds several assets of different sizes in one
     batch: every asset's BVH4 is bit-identical to the one agr_update_mesh
@@ -590,16 +605,18 @@ def test_update_meshes_batched_equals_one_by_one():
     for a in which:
         v = meshes[a].verts.astype(np.float64)
         new[a] = (v * rng.uniform(0.8, 1.2, (len(v), 1)) + rng.uniform(-0.2, 0.2, 3)).astype(np.float32)
-    before = [sa.debug_export_bvh4(a)[0] for a in range(E)]
+    before = [sa.debug_export_bvh4(a) for a in range(E)]
     sa.update_meshes(which, torch.from_numpy(np.concatenate([new[a] for a in which])).to(dev()))
     for a in which:
         sb.update_mesh(a, torch.from_numpy(new[a]).to(dev()))
     torch.cuda.synchronize()
     for a in range(E):
-        na, nb = sa.debug_export_bvh4(a)[0], sb.debug_export_bvh4(a)[0]
-        assert np.array_equal(na.view(np.uint32), nb.view(np.uint32)), f"asset {a}"
+        # the BVH4 node numbering depends on the build's schedule (blas.cu
+        # K5b'); the tree -- boxes, leaves and shape from the root -- does not
+        ca, cb = _bvh4_canonical(*sa.debug_export_bvh4(a)), _bvh4_canonical(*sb.debug_export_bvh4(a))
+        assert ca == cb, f"asset {a}"
         if a not in which:
-            assert np.array_equal(na.view(np.uint32), before[a].view(np.uint32))
+            assert ca == _bvh4_canonical(*before[a])
     sa.build()
     cam = sg.pinhole(48, 32, 70.0)
     sensor = dict(kind="pinhole", cam=cam, poses=sg.identity_poses(E), max_range=10.0)
