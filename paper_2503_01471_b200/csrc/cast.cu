@@ -692,8 +692,15 @@ struct PSlab {
     int strad;            // warp-uniform: some lane's interval contains 0 on some axis
 };
 constexpr int PS_N = 13;
+constexpr int PS_MAXN = 20;  // >= PS_N and the BVH8 FMA form's PS8_N
 #ifndef AGR_STRAD_FAST
 #define AGR_STRAD_FAST 1  // BVH8 packets: no-straddle slab specialisation
+#endif
+#ifndef AGR_RANK_MODE
+#define AGR_RANK_MODE 1   // BVH8 child order: 0 full rank with ties, 1 REDUX nearest + rank for nh > 2, 2 nearest only
+#endif
+#ifndef AGR_SLAB_FMA
+#define AGR_SLAB_FMA 1    // BVH8 packets: FMA-form interval slab with the entry / exit planes by direction sign
 #endif
 #ifndef AGR_PS_RELOAD
 #define AGR_PS_RELOAD 1   // reload the packet slab state from shared memory after a leaf
@@ -792,6 +799,7 @@ __device__ __forceinline__ PSlab pslab_load(const float* src) {
     return p;
 }
 
+#if !AGR_SLAB_FMA
 // pslab_axis for an interval of one sign (every lane's, i.e. !strad): near
 // and far are the min and max of the four products (no straddle branch).
 __device__ __forceinline__ void pslab_axis_fast(float lo, float hi, float ol, float oh, float i0, float i1,
@@ -801,6 +809,92 @@ __device__ __forceinline__ void pslab_axis_fast(float lo, float hi, float ol, fl
     n = fminf(fminf(a0, a1), fminf(b0, b1));
     f = fmaxf(fmaxf(a0, a1), fmaxf(b0, b1));
 }
+#endif
+
+#if AGR_SLAB_FMA
+// BVH8 packet box-test state in FMA form: per axis the two reciprocal
+// endpoints and, for the entry plane E (lo if the directions are positive,
+// hi if negative) and the exit plane X, the products -o_E i and -o_X i, so
+// each of the four candidate distances is one FMA of the node's plane:
+//   entry = min(E i0 + cE0, E i1 + cE1), exit = max(X i0 + cX0, X i1 + cX1)
+// (the min / max over the interval of a monotone 1/d, i.e. the same values
+// as pslab_axis's min / max of all four products, rounded once instead of
+// twice: the difference is ~2^-24 |o| in position, inside the 2 delta
+// widening, which is >= 2^-16 |o|).  An axis whose interval contains 0
+// keeps E = lo, X = hi: entry = max(lo i1 + cE1, hi i0 + cX0), exit = inf.
+struct PSlab8 {
+    float i0x, i0y, i0z, i1x, i1y, i1z;
+    float ex0, ex1, xx0, xx1;  // x: cE0, cE1, cX0, cX1
+    float ey0, ey1, xy0, xy1;
+    float ez0, ez1, xz0, xz1;
+    int neg;    // bit k: axis k's directions are negative (E = hi)
+    int strad;  // warp-uniform: some lane's interval contains 0 on some axis
+};
+constexpr int PS8_N = 20;
+
+__device__ __forceinline__ void ps8_axis(float o, float dp, float lo, float hi, float& i0, float& i1, float& e0,
+                                         float& e1, float& x0, float& x1, int& neg, int bit) {
+    iv_recip(lo, hi, i0, i1);
+    const bool straddle = (__float_as_int(i0) ^ __float_as_int(i1)) < 0;
+    const bool n = !straddle && i0 < 0.0f;
+    const float oe = n ? o - dp : o + dp, ox = n ? o + dp : o - dp;
+    e0 = -oe * i0; e1 = -oe * i1; x0 = -ox * i0; x1 = -ox * i1;
+    neg |= n ? bit : 0;
+}
+
+__device__ __forceinline__ PSlab8 make_pslab8(f3 o, f3 d, float delta) {
+    const unsigned FULL = 0xFFFFFFFFu;
+    const bool centre = (threadIdx.x & 8) != 0;
+    const float dcx = __shfl_sync(FULL, d.x, TILE_CENTRE_LANE);
+    const float dcy = __shfl_sync(FULL, d.y, TILE_CENTRE_LANE);
+    const float dcz = __shfl_sync(FULL, d.z, TILE_CENTRE_LANE);
+    const float mnx = ord2f(__reduce_min_sync(FULL, f2ord(d.x))), mxx = ord2f(__reduce_max_sync(FULL, f2ord(d.x)));
+    const float mny = ord2f(__reduce_min_sync(FULL, f2ord(d.y))), mxy = ord2f(__reduce_max_sync(FULL, f2ord(d.y)));
+    const float mnz = ord2f(__reduce_min_sync(FULL, f2ord(d.z))), mxz = ord2f(__reduce_max_sync(FULL, f2ord(d.z)));
+    const float dp = 2.0f * __int_as_float(__reduce_max_sync(FULL, __float_as_int(delta)));
+    PSlab8 p;
+    p.neg = 0;
+    ps8_axis(o.x, dp, centre ? dcx : mnx, centre ? dcx : mxx, p.i0x, p.i1x, p.ex0, p.ex1, p.xx0, p.xx1, p.neg, 1);
+    ps8_axis(o.y, dp, centre ? dcy : mny, centre ? dcy : mxy, p.i0y, p.i1y, p.ey0, p.ey1, p.xy0, p.xy1, p.neg, 2);
+    ps8_axis(o.z, dp, centre ? dcz : mnz, centre ? dcz : mxz, p.i0z, p.i1z, p.ez0, p.ez1, p.xz0, p.xz1, p.neg, 4);
+    const bool st = !(mnx > 0.0f || mxx < 0.0f) || !(mny > 0.0f || mxy < 0.0f) || !(mnz > 0.0f || mxz < 0.0f);
+    p.strad = __any_sync(FULL, st && !centre) ? 1 : 0;
+    return p;
+}
+
+__device__ __forceinline__ void ps8_store(float* dst, const PSlab8& p) {
+    const float* q = reinterpret_cast<const float*>(&p);
+#pragma unroll
+    for (int k = 0; k < PS8_N; ++k) dst[k] = q[k];
+}
+__device__ __forceinline__ PSlab8 ps8_load(const float* src) {
+    PSlab8 p;
+    p.i0x = src[0]; p.i0y = src[1]; p.i0z = src[2]; p.i1x = src[3]; p.i1y = src[4]; p.i1z = src[5];
+    p.ex0 = src[6]; p.ex1 = src[7]; p.xx0 = src[8]; p.xx1 = src[9];
+    p.ey0 = src[10]; p.ey1 = src[11]; p.xy0 = src[12]; p.xy1 = src[13];
+    p.ez0 = src[14]; p.ez1 = src[15]; p.xz0 = src[16]; p.xz1 = src[17];
+    p.neg = __float_as_int(src[18]); p.strad = __float_as_int(src[19]);
+    return p;
+}
+
+// One axis, intervals of one sign (the warp-uniform fast path).
+__device__ __forceinline__ void ps8_axis_fast(float lo, float hi, bool neg, float i0, float i1, float e0, float e1,
+                                              float x0, float x1, float& n, float& f) {
+    const float E = neg ? hi : lo, X = neg ? lo : hi;
+    n = fminf(fmaf(E, i0, e0), fmaf(E, i1, e1));
+    f = fmaxf(fmaf(X, i0, x0), fmaf(X, i1, x1));
+}
+// One axis, any interval (some lane straddles somewhere).
+__device__ __forceinline__ void ps8_axis_any(float lo, float hi, bool neg, float i0, float i1, float e0, float e1,
+                                             float x0, float x1, float& n, float& f) {
+    if ((__float_as_int(i0) ^ __float_as_int(i1)) < 0) {
+        n = fmaxf(fmaf(lo, i1, e1), fmaf(hi, i0, x0));
+        f = inf_f();
+    } else {
+        ps8_axis_fast(lo, hi, neg, i0, i1, e0, e1, x0, x1, n, f);
+    }
+}
+#endif
 
 // Closest-hit traversal of a tile whose rays share their origin.  ps_env /
 // ps_obj: this warp's shared-memory copies of the two roles' box-test state
@@ -924,9 +1018,14 @@ __device__ __forceinline__ void traverse_ipacket8(const SceneView& sv, int env, 
     const int child = lane & 7;
     const int role = (lane >> 3) & 1;
     const bool slot_lane = lane < 8;  // lanes owning child slots for ordering / pushes
+#if AGR_SLAB_FMA
+    PSlab8 ps = make_pslab8(rs.o(), rs.d(), K_ERR * rs.c.f(C_Q));
+    if (child == 0 && lane < 16) ps8_store(ps_env + role * PS8_N, ps);
+#else
     PSlab ps = make_pslab<8>(rs.o(), rs.d(), K_ERR * rs.c.f(C_Q));
     ps.strad = __any_sync(FULL, ps.strad && role == 0) ? 1 : 0;
     if (child == 0 && lane < 16) pslab_store(ps_env + role * PS_N, ps);
+#endif
     __syncwarp();
     float Umax = __int_as_float(__reduce_max_sync(FULL, __float_as_int(rs.U)));
     int sp = 0;
@@ -938,6 +1037,17 @@ __device__ __forceinline__ void traverse_ipacket8(const SceneView& sv, int env, 
             const float4* cp = sv.nodes8 + NODE8_F4 * (size_t)node + 2 * child;
             const float4 ca = __ldg(cp), cb = __ldg(cp + 1);
             float nx, fx, ny, fy, nz, fz;
+#if AGR_SLAB_FMA
+            if (!ps.strad) {
+                ps8_axis_fast(ca.x, ca.w, ps.neg & 1, ps.i0x, ps.i1x, ps.ex0, ps.ex1, ps.xx0, ps.xx1, nx, fx);
+                ps8_axis_fast(ca.y, cb.x, ps.neg & 2, ps.i0y, ps.i1y, ps.ey0, ps.ey1, ps.xy0, ps.xy1, ny, fy);
+                ps8_axis_fast(ca.z, cb.y, ps.neg & 4, ps.i0z, ps.i1z, ps.ez0, ps.ez1, ps.xz0, ps.xz1, nz, fz);
+            } else {
+                ps8_axis_any(ca.x, ca.w, ps.neg & 1, ps.i0x, ps.i1x, ps.ex0, ps.ex1, ps.xx0, ps.xx1, nx, fx);
+                ps8_axis_any(ca.y, cb.x, ps.neg & 2, ps.i0y, ps.i1y, ps.ey0, ps.ey1, ps.xy0, ps.xy1, ny, fy);
+                ps8_axis_any(ca.z, cb.y, ps.neg & 4, ps.i0z, ps.i1z, ps.ez0, ps.ez1, ps.xz0, ps.xz1, nz, fz);
+            }
+#else
             if (AGR_STRAD_FAST && !ps.strad) {
                 pslab_axis_fast(ca.x, ca.w, ps.olx, ps.ohx, ps.i0x, ps.i1x, nx, fx);
                 pslab_axis_fast(ca.y, cb.x, ps.oly, ps.ohy, ps.i0y, ps.i1y, ny, fy);
@@ -947,6 +1057,7 @@ __device__ __forceinline__ void traverse_ipacket8(const SceneView& sv, int env, 
                 pslab_axis(ca.y, cb.x, ps.oly, ps.ohy, ps.i0y, ps.i1y, ny, fy);
                 pslab_axis(ca.z, cb.y, ps.olz, ps.ohz, ps.i0z, ps.i1z, nz, fz);
             }
+#endif
             const float tn = fmaxf(fmaxf(nx, ny), fmaxf(nz, 0.0f));
             const float tf = fminf(fminf(fx, fy), fminf(fz, Umax));
             const bool h = tn <= tf;
@@ -963,6 +1074,7 @@ __device__ __forceinline__ void traverse_ipacket8(const SceneView& sv, int env, 
                 node = __shfl_sync(FULL, ref, __ffs(cm) - 1);
                 continue;
             }
+#if AGR_RANK_MODE == 0
             // rank of this lane's child among the hit children by the centre
             // ray's entry distance (lanes 8-15), misses last
             const unsigned kc = __shfl_sync(FULL, __float_as_uint(tn), child + 8);
@@ -985,10 +1097,42 @@ __device__ __forceinline__ void traverse_ipacket8(const SceneView& sv, int env, 
             }
             node = nearest;
             continue;
+#else
+            // order keys: the centre ray's entry distance (lanes 8-15) with
+            // the child index in the 3 low bits (distinct; near-equal
+            // distances go by index), misses last; the nearest by one REDUX
+            const unsigned kc = __shfl_sync(FULL, __float_as_uint(tn), child + 8);
+            const bool hit = slot_lane && ((cm >> child) & 1u);
+            const unsigned key = hit ? ((kc & ~7u) | (unsigned)child) : 0xFFFFFFFFu;
+            const int near_child = (int)(__reduce_min_sync(FULL, key) & 7u);
+            const int nearest = __shfl_sync(FULL, ref, near_child);
+            if (sp + 7 <= PSTACK) {
+                __syncwarp();  // every lane has read the slots before they are reused
+                if (AGR_RANK_MODE == 1 && nh > 2) {
+                    int rank = 0;  // among the hits, farthest pushed first
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) rank += __shfl_sync(FULL, key, j) < key ? 1 : 0;
+                    if (hit && rank > 0) wstack[sp + nh - 1 - rank] = ref;
+                } else if (hit && child != near_child) {
+                    // nh == 2 (exact), or mode 2: the other hits in child order
+                    const unsigned others = cm & ~(1u << near_child);
+                    wstack[sp + __popc(others & ((1u << child) - 1u))] = ref;
+                }
+                sp += nh - 1;  // nh is warp-uniform
+            } else {
+                rs.c.i(C_OVF) = 1;
+            }
+            node = nearest;
+            continue;
+#endif
         }
         if (node == SENTINEL) {  // back to the env level
             rs.cur_inst = -1;
+#if AGR_SLAB_FMA
+            ps = ps8_load(ps_env + role * PS8_N);
+#else
             ps = pslab_load(ps_env + role * PS_N);
+#endif
             if (sp == 0) break;
             __syncwarp();
             node = wstack[--sp];
@@ -1008,10 +1152,16 @@ __device__ __forceinline__ void traverse_ipacket8(const SceneView& sv, int env, 
             f3 oo, od;
             float delta;
             node = rs.enter_object(sv, leaf, oo, od, delta);
+#if AGR_SLAB_FMA
+            ps = make_pslab8(oo, od, delta);
+            __syncwarp();
+            if (child == 0 && lane < 16) ps8_store(ps_obj + role * PS8_N, ps);
+#else
             ps = make_pslab<8>(oo, od, delta);
             ps.strad = __any_sync(FULL, ps.strad && role == 0) ? 1 : 0;
             __syncwarp();
             if (child == 0 && lane < 16) pslab_store(ps_obj + role * PS_N, ps);
+#endif
             __syncwarp();
             continue;
         }
@@ -1023,7 +1173,11 @@ __device__ __forceinline__ void traverse_ipacket8(const SceneView& sv, int env, 
         }
         Umax = __int_as_float(__reduce_max_sync(FULL, __float_as_int(rs.U)));
         __syncwarp();
+#if AGR_SLAB_FMA
+        if (AGR_PS_RELOAD) ps = ps8_load(ps_obj + role * PS8_N);
+#else
         if (AGR_PS_RELOAD) ps = pslab_load(ps_obj + role * PS_N);
+#endif
         if (sp == 0) break;
         node = wstack[--sp];
     }
@@ -1350,7 +1504,7 @@ __device__ __forceinline__ RayId ray_id(const CastArgs& a) {
 template <int MODEL, int TRAV, bool COUNT, bool STEREO>
 __global__ void __launch_bounds__(CAST_THREADS, CAST_MIN_BLOCKS) k_cast(const __grid_constant__ CastArgs a) {
     __shared__ int s_stack[TRAV == 1 ? CAST_THREADS / 32 : 1][TRAV == 1 ? PSTACK : 1];
-    __shared__ float s_pslab[TRAV == 1 ? CAST_THREADS / 32 : 1][2][2 * PS_N];  // [warp][env, obj][role][PS_N]
+    __shared__ float s_pslab[TRAV == 1 ? CAST_THREADS / 32 : 1][2][2 * PS_MAXN];  // [warp][env, obj][role][..]
     RayId id = ray_id<MODEL>(a);
     // ragged tile lanes keep the warp whole for the traversal: they trace a
     // copy of a valid pixel and store nothing
