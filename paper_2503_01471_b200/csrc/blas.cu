@@ -614,9 +614,12 @@ __global__ void __launch_bounds__(T_BLK) k_fit(const BlasSeg* segs, const int* s
 
 // Subtree sizes out of the box records into their own array (read by the
 // treelet rounds and the collapses).
-__global__ void k_size_from_box(const float* __restrict__ ibox, int F, int* __restrict__ size) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < F) size[i] = __float_as_int(__ldg(ibox + BX * (size_t)i + 3));
+__global__ void k_size_from_box(const BlasSeg* segs, const int* seg_of, const uint32_t* bounds, int Ftot,
+                                const float* __restrict__ ibox, int* __restrict__ size) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= Ftot) return;
+    const SegCtx c = seg_ctx(segs, seg_of, bounds, g);
+    if (g - c.off < c.n - 1) size[g] = __float_as_int(__ldg(ibox + BX * (size_t)g + 3));  // internal nodes only
 }
 
 // ---- K4b: treelet restructuring (TRBVH) ------------------------------------------------
@@ -1390,7 +1393,7 @@ cudaError_t blas_build_batch(BlasSeg* h_segs, int B, const BlasBatchArgs& a, voi
     // subtree sizes into their own array for the treelet rounds / the BVH8
     // collapse (the BVH4 path reads them from the box records)
     const bool need_size = a.trbvh_rounds > 0 || a.nodes8 != nullptr;
-    if (need_size) k_size_from_box<<<gb, T_BLK, 0, stream>>>(s.ibox, F, s.size);
+    if (need_size) k_size_from_box<<<gb, T_BLK, 0, stream>>>(s.segs, s.seg_of, s.bounds, F, s.ibox, s.size);
     for (int round = 0; round < a.trbvh_rounds; ++round) {
         cudaMemsetAsync(s.flags, 0, sizeof(int) * F, stream);
         k_trbvh<<<(F + TRB_THREADS - 1) / TRB_THREADS, TRB_THREADS, 0, stream>>>(s.segs, s.seg_of, s.bounds, F, sv, s.tri_box, s.child,
