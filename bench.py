@@ -177,15 +177,18 @@ def make_workload(cfg, n_envs, env_base):
     return sg.config5(n_envs=n_envs, env_base=env_base, ring=8)
 
 
-def blas_launches(n_assets, trbvh_rounds):
-    """Kernels one agr_update_meshes batch launches (blas.cu blas_build_batch)."""
-    seg_passes = 0
-    while n_assets > 1 and ((n_assets - 1) >> (8 * seg_passes)) != 0:
-        seg_passes += 1
-    n = 5 + 4 * 3  # seg_of, init_bounds, radius, tri_prep, morton; 4 code passes
-    if n_assets > 1:
-        n += 2 + 3 * seg_passes
-    n += 2 + trbvh_rounds + (1 if trbvh_rounds > 0 else 0) + 4
+def blas_launches(trbvh_rounds, bvh8):
+    """Kernels one agr_update_meshes batch launches (blas.cu blas_build_batch):
+    seg_of, init_bounds, radius, tri_prep, morton; 4 sort passes of hist +
+    3-launch scan + scatter; pack_tris, karras, fit; [size copy for the
+    treelet rounds / the BVH8 collapse]; treelet rounds [+ depth]; child
+    records, top-down init, top-down BVH4, single-leaf roots; [BVH8
+    collapse]; asset info (checked against the ncu launch list,
+    profiles/r02l_launches_c6.csv)."""
+    n = 5 + 4 * 5 + 3
+    n += 1 if (trbvh_rounds > 0 or bvh8) else 0
+    n += trbvh_rounds + (1 if trbvh_rounds > 0 else 0)
+    n += 4 + (1 if bvh8 else 0) + 1
     return n
 
 
@@ -664,7 +667,7 @@ def main():
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
     # k_instances + k_tlas + k_cast (+ the batched BLAS rebuild for c6)
-    LAUNCHES_PER_STEP = 3 + (blas_launches(len(wl.sc.meshes), wl.trbvh_rounds) if cfg == 6 else 0)
+    LAUNCHES_PER_STEP = 3 + (blas_launches(wl.trbvh_rounds, wl.traversal != "lane") if cfg == 6 else 0)
     for w in range(args.warmup):
         wl.step(w, stream)
     torch.cuda.synchronize()

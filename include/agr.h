@@ -212,9 +212,14 @@ agr_status agr_scene_destroy(agr_scene scene);
 agr_status agr_scene_get_info(agr_scene scene, agr_scene_info* info);
 
 /*
- * Copy new instance transforms (device float [n_instances][3][4], row-major
- * object -> env-local x' = A x + b; A must be invertible) into the scene
- * and recompute the per-instance ray transforms and bounds.  Async on
+ * PAPER.md:226 (§III.D.1): "transformations for each sub-mesh at time t are
+ * maintained as T_{i,t} = {T_{j,t}}" and "the vertices of the mesh are
+ * transformed to match the obstacles in the simulator at time t as
+ * M_{i,t} = T^T_{i,t} o M^base_i".  Here the transform is applied to the rays instead
+ * (instancing): copy new instance transforms (device float
+ * [n_instances][3][4], row-major object -> env-local x' = A x + b; A must
+ * be invertible; EINVAL for a NULL T with instances) into the scene and
+ * recompute the per-instance ray transforms and bounds.  Async on
  * `stream`; T may be reused once the stream passes this point.  The TLAS is
  * stale until agr_build or agr_refit.
  */
@@ -262,14 +267,19 @@ agr_status agr_set_vertex_annotations(agr_scene scene, int32_t asset, const floa
 agr_status agr_update_meshes(agr_scene scene, int32_t n, const int32_t* assets, const float* verts,
                              void* stream);
 
-/* Full per-env TLAS rebuild (one CTA per env: LBVH -- Morton order + Karras
+/* "a bounding volume hierarchy is calculated for M_{i,t} for
+ * efficient ray-casting" -- here the per-env top level over the instances
+ * (the per-asset bottom levels are built at create / agr_update_mesh(es)).
+ * Full per-env TLAS rebuild (one CTA per env: LBVH -- Morton order + Karras
  * hierarchy -- or, after agr_set_tlas_builder(scene, 1), a binned-SAH
- * top-down split of the instance boxes), bottom-up fit and 4-wide collapse.
- * Async. */
+ * top-down split of the instance boxes), bottom-up fit and 4- / 8-wide
+ * collapse.  Async; EINVAL for a NULL scene. */
 agr_status agr_build(agr_scene scene, void* stream);
 
-/* In-place TLAS refit: keeps the topology of the last agr_build and
- * recomputes all boxes bottom-up.  ESTATE before the first agr_build. */
+/* In-place TLAS refit (the transformations T_{i,t} change with
+ * t while the env's sub-meshes M^base_i stay): keeps the topology of the last
+ * agr_build and recomputes all boxes bottom-up.  Async.  ESTATE before the
+ * first agr_build. */
 agr_status agr_refit(agr_scene scene, void* stream);
 
 /*
