@@ -1,0 +1,5 @@
+mkdir -p build/var/base && cp paper_2503_01471_b200/lib/libagr.so build/var/base/
+for c in 3 4 5; do
+  echo "== c$c"
+  bash tools/runvar.sh oc_c$c "--config $c --no-table2" base b12 b12n b16n b14
+done
