@@ -559,15 +559,19 @@ __device__ __forceinline__ int arrive_cta(int* flag) {
 // straddling a block boundary (a few per cent) use the global flag and the
 // acq_rel device-scope atomic.  Internal node i's range contains leaf i, so
 // a block-local node's flag is its face slot in the block.
-__global__ void __launch_bounds__(T_BLK) k_fit(const BlasSeg* segs, const int* seg_of, const uint32_t* bounds,
+#ifndef AGR_FIT_BLK
+#define AGR_FIT_BLK 256
+#endif
+constexpr int FIT_BLK = AGR_FIT_BLK;  // larger blocks keep more of the climb at block scope
+__global__ void __launch_bounds__(FIT_BLK) k_fit(const BlasSeg* segs, const int* seg_of, const uint32_t* bounds,
                                               int Ftot, const uint32_t* __restrict__ sorted_all, const float* tri_box,
                                               int* child_all, int* node_parent_all, int* leaf_parent_all,
                                               float* ibox_all, int* flags_all, int* depth,
                                               const int2* __restrict__ range_all) {
-    __shared__ int sflag[T_BLK];
+    __shared__ int sflag[FIT_BLK];
     sflag[threadIdx.x] = 0;
     __syncthreads();
-    const int blk0 = blockIdx.x * T_BLK;
+    const int blk0 = blockIdx.x * FIT_BLK;
     const int g = blk0 + threadIdx.x;
     if (g >= Ftot) return;
     const SegCtx c = seg_ctx(segs, seg_of, bounds, g);
@@ -577,7 +581,7 @@ __global__ void __launch_bounds__(T_BLK) k_fit(const BlasSeg* segs, const int* s
     AGR_SEG_PARENTS(c);
     int* flags = flags_all + c.off;
     const int2* range = range_all + c.off;
-    const int lo_ok = blk0 - c.off, hi_ok = blk0 + T_BLK - c.off;  // block's faces, segment-local
+    const int lo_ok = blk0 - c.off, hi_ok = blk0 + FIT_BLK - c.off;  // block's faces, segment-local
     int node = leaf_parent[p];
     while (node >= 0) {
         const int2 r = __ldg(range + node);
@@ -1388,7 +1392,7 @@ cudaError_t blas_build_batch(BlasSeg* h_segs, int B, const BlasBatchArgs& a, voi
                                           s.tri_box);
     k_karras<<<gb, T_BLK, 0, stream>>>(s.segs, s.seg_of, s.bounds, F, sk, s.child, s.node_parent,
                                        s.leaf_parent, s.range);
-    k_fit<<<gb, T_BLK, 0, stream>>>(s.segs, s.seg_of, s.bounds, F, sv, s.tri_box, s.child, s.node_parent,
+    k_fit<<<(F + FIT_BLK - 1) / FIT_BLK, FIT_BLK, 0, stream>>>(s.segs, s.seg_of, s.bounds, F, sv, s.tri_box, s.child, s.node_parent,
                                     s.leaf_parent, s.ibox, s.flags, s.depth, s.range);
     // subtree sizes into their own array for the treelet rounds / the BVH8
     // collapse (the BVH4 path reads them from the box records)
@@ -1416,15 +1420,14 @@ cudaError_t blas_build_batch(BlasSeg* h_segs, int B, const BlasBatchArgs& a, voi
                                          a.trbvh_rounds > 0 ? s.size : nullptr, s.rec);
     k_reach_init<<<(B + 127) / 128, 128, 0, stream>>>(s.segs, B, s.bounds, s.seg4, s.queue, s.qctl);
     {
-        static int coop_blocks = 0;  // co-resident blocks (device 0's count serves all B200s)
-        int dev = 0, sms = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (coop_blocks == 0) {
-            int per_sm = 0;
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bvh4_topdown, T_BLK, 0);
-            coop_blocks = sms * (per_sm < 1 ? 1 : per_sm);
-        }
+        // co-resident blocks of the cooperative launch (per device: the
+        // grid must fit at once or the launch fails)
+        int dev = 0, sms = 0, per_sm = 0;
+        e = cudaGetDevice(&dev);
+        if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bvh4_topdown, T_BLK, 0);
+        if (e != cudaSuccess) return e;
+        const int coop_blocks = sms * (per_sm < 1 ? 1 : per_sm);
         // every co-resident block: the levels are latency-bound chains of
         // dependent loads, so more threads in flight beat cheaper barriers
 #ifndef AGR_TOPDOWN_PER_SM

@@ -1,0 +1,7 @@
+mkdir -p build/var/base && cp paper_2503_01471_b200/lib/libagr.so build/var/base/
+for v in base fit512 fit1024; do
+  AGR_LIB_PATH=$PWD/build/var/$v/libagr.so timeout 600 python bench.py --config 6 --no-table2 --no-cpu-baseline --no-e2e --no-counters > gpurun_out/abf_$v.json 2>&1
+  python -c "
+import json; d=json.loads(open('gpurun_out/abf_$v.json').read().strip().splitlines()[-1]); print('$v', '%.4g'%d['value'], 'upd %.3f cast %.3f'%(d['update_ms_per_step'], d['cast_ms_per_step']))"
+done
+AGR_LIB_PATH=$PWD/build/var/fit1024/libagr.so timeout 600 python -m pytest tests/test_bvh_gpu.py tests/test_parity_gpu.py -m gpu -q -x -k "bvh or update_mesh or c6 or parts or trbvh" 2>&1 | tail -2
