@@ -1025,6 +1025,41 @@ def test_wide_tile_cameras_all_schedules_bitwise():
     s.close()
 
 
+def test_tlas_warp_path_equals_cta_path_bitwise():
+    """Envs of <= 32 TLAS items are built / refit by one warp each
+    (tlas.cu k_tlas_warp) unless some env of the scene is larger (then every
+    env takes the CTA path): the same envs give bitwise the same BVH4 TLAS
+    and images either way, after an LBVH build and after a refit."""
+    sc, sensor = sg.config2(n_envs=3)  # 10 items per env
+    big = [(int(a), 40 + k, T) for k, (a, T) in enumerate(zip(sc.inst_asset[:10], sc.inst_T[:10]))] * 4
+    per_env = [[(int(sc.inst_asset[i]), int(sc.inst_label[i]), sc.inst_T[i])
+                for i in range(int(sc.env_off[e]), int(sc.env_off[e + 1]))] for e in range(3)]
+    small = sg.assemble(sc.meshes, per_env)
+    mixed = sg.assemble(sc.meshes, per_env + [big])  # a 40-item env appended last
+    scenes = [make_scene(small), make_scene(mixed)]
+    poses = sensor["poses"][:3]
+    sen = dict(sensor, poses=poses)
+    for step in range(2):
+        if step == 1:
+            for x, scx in zip(scenes, (small, mixed)):
+                T2 = scx.inst_T.copy()
+                T2[:, :2, 3] += 0.2
+                x.set_instance_transforms(torch.from_numpy(T2).to(dev()))
+                x.refit()
+        for e in range(3):
+            a, ra = scenes[0].debug_export_bvh4(-1 - e)
+            b, rb = scenes[1].debug_export_bvh4(-1 - e)
+            assert ra == rb
+            assert np.array_equal(a.view(np.uint32), b.view(np.uint32)), (step, e)
+        img = [to_np(cast_sensor(x, sen if i == 0 else dict(sen, poses=np.concatenate([poses, poses[:1]]))))
+               for i, x in enumerate(scenes)]
+        n = len(img[0]["dist"])
+        for k in img[0]:
+            assert np.array_equal(img[0][k].view(np.uint32), img[1][k][:n].view(np.uint32)), (step, k)
+    for x in scenes:
+        x.close()
+
+
 # --------------------------------------------------------------------------
 # Table II-shaped env step (SURVEY.md §8(f) f4; PAPER.md:276-304): the
 # kinematic stand-in (include/agr_sim.h) + refit + cast, eager and as a
