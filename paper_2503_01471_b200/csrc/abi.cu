@@ -82,7 +82,7 @@ struct agr_scene_s {
     size_t device_bytes = 0;
     // device arrays
     float4* nodes = nullptr;   // BVH4 (BLAS then TLAS), 8 float4 per node
-    float4* nodes8 = nullptr;  // BVH8 copy (same numbering), 16 float4 per node, or null
+    float4* nodes8 = nullptr;  // BVH8 copy (BLAS compacted, roots / TLAS at the BVH4's indices), 16 float4 per node, or null
     float4* bnodes = nullptr;  // binary BLAS nodes, 4 float4 per node (debug export)
     float4* tris = nullptr;
     float* triv = nullptr;

@@ -81,7 +81,8 @@ struct BlasInfo {
 // Read-only view of a scene passed by value to kernels.
 struct SceneView {
     const float4* nodes;      // [n_nodes][8] BVH4
-    const float4* nodes8;     // [n_nodes][16] BVH8 (same numbering), or null
+    const float4* nodes8;     // [n_nodes][16] BVH8 copy (its own numbering; BLAS roots and TLAS nodes at the
+                              // same indices as the BVH4), or null
     const float4* tris;       // [n_leaves][3]
     const float* triv;        // [n_leaves][3] float4 (v.xyz, 0)
     const float4* irec;       // [n_items][4] (TLAS leaf ~item)
@@ -244,7 +245,7 @@ struct BlasSeg {
 };
 struct BlasBatchArgs {
     float4* nodes;         // global BVH4 node array
-    float4* nodes8;        // global BVH8 node array (same node numbering), or null
+    float4* nodes8;        // global BVH8 node array (compacted like the BVH4; root at node_base), or null
     float4* bnodes;        // global binary BLAS node array (debug export)
     float4* tris;          // global tri record array
     float* triv;           // global exact-vertex array

@@ -122,6 +122,7 @@ struct Scratch {
     int* size;           // [Ftot] leaves under each internal node
     int2* range;         // [Ftot] leaf range [lo, hi] of each Karras node (segment-local)
     int* seg4;           // [B] BVH4 nodes allocated in each segment (compaction)
+    int* seg8;           // [B] the same for the BVH8 copy
     int2* queue;         // [Ftot] (binary node, BVH4 slot) of every reachable node, level by level
     float4* rec;         // [Ftot][4] per internal node: both children's boxes, refs and pair-leaf codes
     int* qctl;           // [2 + MAX_LEVELS]: [0] items in the queue, [2 + L] items of BVH4 level L
@@ -161,6 +162,7 @@ size_t scratch_layout(int64_t F, int B, void* base, Scratch* out) {
     s.size = (int*)take(sizeof(int) * F);
     s.range = (int2*)take(sizeof(int2) * F);
     s.seg4 = (int*)take(sizeof(int) * B);
+    s.seg8 = (int*)take(sizeof(int) * B);
     s.queue = (int2*)take(sizeof(int2) * F);
     s.rec = (float4*)take(sizeof(float4) * 4 * F);
     s.qctl = (int*)take(sizeof(int) * (2 + MAX_LEVELS));
@@ -948,71 +950,6 @@ __global__ void k_pack_nodes(const BlasSeg* segs, const int* seg_of, const uint3
                global_ref(rb, node_base, leaf_base));
 }
 
-// K5b: BVH4 node j = greedy 4-wide collapse of binary node j (every
-// traversal mode); with W = 8 the BVH8 copy of the interval-packet traversal.
-template <int W>
-__global__ void k_collapse(const BlasSeg* segs, const int* seg_of, const uint32_t* bounds, int Ftot,
-                           const uint32_t* __restrict__ sorted_all, const float* tri_box, int* child_all,
-                           float* ibox_all, const int* __restrict__ size_all, float4* nodes) {
-    const int g = blockIdx.x * blockDim.x + threadIdx.x;
-    if (g >= Ftot) return;
-    const SegCtx c = seg_ctx(segs, seg_of, bounds, g);
-    const int n = c.n, j = g - c.off;
-    const int n_int = n > 1 ? n - 1 : 1;
-    if (j >= n_int) return;
-    AGR_SEG_VIEW(c);
-    const int node_base = segs[c.s].node_base, leaf_base = segs[c.s].leaf_base;
-    int refs[W];
-    int cnt;
-    if (n > 1) {
-        auto ch = [&](int r, int side) { return __ldg(child + 2 * r + side); };
-        auto bx = [&](int r, float bb[6]) {
-            load_box_cg(ibox + BX * r, bb);
-        };
-        cnt = collapse_w<W>(j, ch, bx, refs, AGR_KEEP_PAIRS != 0);
-    } else {
-        refs[0] = n == 1 ? ~0 : REF_EMPTY;
-        for (int k = 1; k < W; ++k) refs[k] = REF_EMPTY;
-        cnt = n == 1 ? 1 : 0;
-    }
-    float boxes[W][6];
-    int gr[W];
-    for (int k = 0; k < W; ++k) {
-        child_box(refs[k], tri_box + BX * (size_t)c.off, ibox, boxes[k]);
-        gr[k] = global_ref(refs[k], node_base, leaf_base);
-        // (subtree sizes from the fit / TRBVH: only subtrees of <= LEAF_MAX
-        // leaves are walked)
-        if (refs[k] >= 0 && LEAF_MAX > 1 && __ldcg(size_all + c.off + refs[k]) <= LEAF_MAX) {
-            // a binary subtree over <= LEAF_MAX consecutive leaves becomes
-            // one multi-triangle leaf
-            int st[2 * LEAF_MAX], sp = 0, nl = 0, lmin = INT_MAX, lmax = -1;
-            bool ok = true;
-            st[sp++] = refs[k];
-            while (sp > 0 && ok) {
-                const int x = st[--sp];
-                if (x < 0) {
-                    ok = nl < LEAF_MAX;
-                    ++nl;
-                    lmin = min(lmin, ~x);
-                    lmax = max(lmax, ~x);
-                } else if (sp + 2 <= 2 * LEAF_MAX) {
-                    st[sp++] = __ldg(child + 2 * x + 1);
-                    st[sp++] = __ldg(child + 2 * x);
-                } else {
-                    ok = false;
-                }
-            }
-            if (ok && lmax - lmin + 1 == nl)
-                gr[k] = ~((leaf_base + lmin) | ((nl - 1) << LEAF_SHIFT));
-        }
-    }
-    if (W == 4) {
-        write_node4(nodes, node_base + j, reinterpret_cast<const float(*)[6]>(boxes), gr, cnt);
-    } else {
-        for (int k = 0; k < W; ++k) write_child8(nodes, node_base + j, k, boxes[k], gr[k]);
-    }
-}
-
 // ---- K5b': compacted BVH4 ------------------------------------------------------
 // The greedy collapse keeps only the binary nodes it does not open as BVH4
 // nodes (about a fifth with pair leaves), so writing a BVH4 node for every
@@ -1109,8 +1046,11 @@ __global__ void k_make_rec(const BlasSeg* segs, const int* seg_of, const uint32_
 // collapse_w, from the child records) and written, and its internal slots
 // are appended as level L + 1 through their own counter qctl[3 + L]
 // (warp-aggregated), so one grid barrier per level suffices.
-__global__ void __launch_bounds__(T_BLK) k_bvh4_topdown(const BlasSeg* segs, const int* seg_of,
-                                                       const float4* __restrict__ rec_all, int* seg4, int2* queue,
+// W = 4: the BVH4 every traversal uses; W = 8: the BVH8 copy of the
+// interval packets (its own compacted numbering; both roots are node_base).
+template <int W>
+__global__ void __launch_bounds__(T_BLK) k_bvhw_topdown(const BlasSeg* segs, const int* seg_of,
+                                                       const float4* __restrict__ rec_all, int* segw, int2* queue,
                                                        int* qctl, float4* nodes) {
     cooperative_groups::grid_group grid = cooperative_groups::this_grid();
     const int lane = threadIdx.x & 31;
@@ -1121,7 +1061,7 @@ __global__ void __launch_bounds__(T_BLK) k_bvh4_topdown(const BlasSeg* segs, con
         const int next = begin + n_lvl;
         for (int t0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31); t0 < n_lvl; t0 += stride) {
             const int t = t0 + lane;
-            int2 push[4];
+            int2 push[W];
             int npush = 0;
             if (t < n_lvl) {
                 const int2 item = __ldcg(queue + begin + t);
@@ -1130,11 +1070,13 @@ __global__ void __launch_bounds__(T_BLK) k_bvh4_topdown(const BlasSeg* segs, con
                 const BlasSeg& S = segs[sgi];
                 const int off = S.off;
                 const float4* rec = rec_all + 4 * (size_t)off;
-                float bx[4][6];
-                int refs[4] = {REF_EMPTY, REF_EMPTY, REF_EMPTY, REF_EMPTY}, aux[4] = {0, 0, 0, 0};
+                float bx[W][6];
+                int refs[W], aux[W];
+#pragma unroll
+                for (int k = 0; k < W; ++k) { refs[k] = REF_EMPTY; aux[k] = 0; }
                 read_rec(rec + 4 * (size_t)(x - off), bx[0], bx[1], refs[0], refs[1], aux[0], aux[1]);
                 int cnt = 2;
-                while (cnt < 4) {  // collapse_w<4>: open the largest-area internal member
+                while (cnt < W) {  // collapse_w<W>: open the largest-area internal member
                     int best = -1;
                     float best_a = -1.0f;
                     for (int k = 0; k < cnt; ++k)
@@ -1146,7 +1088,7 @@ __global__ void __launch_bounds__(T_BLK) k_bvh4_topdown(const BlasSeg* segs, con
                     float ca[6], cb[6];
                     int ra, rb, xa, xb;
                     read_rec(rec + 4 * (size_t)refs[best], ca, cb, ra, rb, xa, xb);
-                    for (int k = 3; k > best + 1; --k)
+                    for (int k = W - 1; k > best + 1; --k)
                         if (k <= cnt) {
                             refs[k] = refs[k - 1];
                             aux[k] = aux[k - 1];
@@ -1157,9 +1099,9 @@ __global__ void __launch_bounds__(T_BLK) k_bvh4_topdown(const BlasSeg* segs, con
                     for (int q = 0; q < 6; ++q) { bx[best][q] = ca[q]; bx[best + 1][q] = cb[q]; }
                     ++cnt;
                 }
-                int gr[4];
-                bool internal[4];
-                for (int k = 0; k < 4; ++k) {
+                int gr[W];
+                bool internal[W];
+                for (int k = 0; k < W; ++k) {
                     internal[k] = false;
                     if (k >= cnt) {
                         refs[k] = REF_EMPTY;
@@ -1188,17 +1130,20 @@ __global__ void __launch_bounds__(T_BLK) k_bvh4_topdown(const BlasSeg* segs, con
                         if ((1u << l) & below) pre += v;
                     }
                     int base = 0;
-                    if (lane == leader && tot) base = atomicAdd(seg4 + sgi, tot);
+                    if (lane == leader && tot) base = atomicAdd(segw + sgi, tot);
                     first = __shfl_sync(grp, base, leader) + pre;
                 }
                 int q = 0;
-                for (int k = 0; k < 4; ++k)
+                for (int k = 0; k < W; ++k)
                     if (internal[k]) {
                         const int slot = first + q;
                         gr[k] = S.node_base + slot;
                         push[q++] = make_int2(off + refs[k], slot);
                     }
-                write_node4(nodes, S.node_base + item.y, reinterpret_cast<const float(*)[6]>(bx), gr, cnt);
+                if (W == 4)
+                    write_node4(nodes, S.node_base + item.y, reinterpret_cast<const float(*)[6]>(bx), gr, cnt);
+                else
+                    for (int k = 0; k < W; ++k) write_child8(nodes, S.node_base + item.y, k, bx[k], gr[k]);
             }
             // warp-aggregated append of the next level
             unsigned incl = npush;
@@ -1245,6 +1190,21 @@ __global__ void k_write4_small(const BlasSeg* segs, int B, const uint32_t* bound
 // record, the exact vertices (3 x float4) and the leaf's box for the
 // hierarchy passes (so they read leaf boxes by position, coalesced, instead
 // of gathering them by face id).
+__global__ void k_write8_small(const BlasSeg* segs, int B, const uint32_t* bounds, const float* tri_box,
+                               float4* nodes8) {
+    const int sgi = blockIdx.x * blockDim.x + threadIdx.x;
+    if (sgi >= B) return;
+    const int n = (int)bounds[8 * sgi + 7];
+    if (n >= 2) return;
+    const BlasSeg& S = segs[sgi];
+    for (int k = 0; k < 8; ++k) {
+        const int r = (k == 0 && n == 1) ? ~0 : REF_EMPTY;
+        float b[6];
+        child_box(r, tri_box + BX * (size_t)S.off, nullptr, b);
+        write_child8(nodes8, S.node_base, k, b, global_ref(r, S.node_base, S.leaf_base));
+    }
+}
+
 __global__ void k_pack_tris(const BlasSeg* segs, const int* seg_of, const uint32_t* bounds, int Ftot,
                             const uint32_t* __restrict__ sorted_all, const uint32_t* __restrict__ sk,
                             float4* tris, float* triv, uint32_t* dbg_morton, float* __restrict__ lbox) {
@@ -1394,9 +1354,9 @@ cudaError_t blas_build_batch(BlasSeg* h_segs, int B, const BlasBatchArgs& a, voi
                                        s.leaf_parent, s.range);
     k_fit<<<(F + FIT_BLK - 1) / FIT_BLK, FIT_BLK, 0, stream>>>(s.segs, s.seg_of, s.bounds, F, sv, s.tri_box, s.child, s.node_parent,
                                     s.leaf_parent, s.ibox, s.flags, s.depth, s.range);
-    // subtree sizes into their own array for the treelet rounds / the BVH8
-    // collapse (the BVH4 path reads them from the box records)
-    const bool need_size = a.trbvh_rounds > 0 || a.nodes8 != nullptr;
+    // subtree sizes into their own array for the treelet rounds (the
+    // collapses read them from the box records)
+    const bool need_size = a.trbvh_rounds > 0;
     if (need_size) k_size_from_box<<<gb, T_BLK, 0, stream>>>(s.segs, s.seg_of, s.bounds, F, s.ibox, s.size);
     for (int round = 0; round < a.trbvh_rounds; ++round) {
         cudaMemsetAsync(s.flags, 0, sizeof(int) * F, stream);
@@ -1413,43 +1373,42 @@ cudaError_t blas_build_batch(BlasSeg* h_segs, int B, const BlasBatchArgs& a, voi
     if (a.bnodes)
         k_pack_nodes<<<gb, T_BLK, 0, stream>>>(s.segs, s.seg_of, s.bounds, F, sv, s.tri_box, s.child, s.ibox,
                                                a.bnodes);
-    {
-    // compacted BVH4 (K5b'): top-down, one cooperative launch
-    cudaMemsetAsync(s.qctl, 0, sizeof(int) * (2 + MAX_LEVELS), stream);
+    // compacted BVH4 / BVH8 (K5b'): top-down from the child records, one
+    // cooperative launch per node width
     k_make_rec<<<gb, T_BLK, 0, stream>>>(s.segs, s.seg_of, s.bounds, F, s.tri_box, s.child, s.ibox,
                                          a.trbvh_rounds > 0 ? s.size : nullptr, s.rec);
-    k_reach_init<<<(B + 127) / 128, 128, 0, stream>>>(s.segs, B, s.bounds, s.seg4, s.queue, s.qctl);
-    {
-        // co-resident blocks of the cooperative launch (per device: the
-        // grid must fit at once or the launch fails)
-        int dev = 0, sms = 0, per_sm = 0;
-        e = cudaGetDevice(&dev);
-        if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bvh4_topdown, T_BLK, 0);
-        if (e != cudaSuccess) return e;
-        const int coop_blocks = sms * (per_sm < 1 ? 1 : per_sm);
-        // every co-resident block: the levels are latency-bound chains of
-        // dependent loads, so more threads in flight beat cheaper barriers
-#ifndef AGR_TOPDOWN_PER_SM
-#define AGR_TOPDOWN_PER_SM 64
-#endif
-        const int grid = AGR_TOPDOWN_PER_SM * sms < coop_blocks ? AGR_TOPDOWN_PER_SM * sms : coop_blocks;
+    int dev = 0, sms = 0;
+    e = cudaGetDevice(&dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e != cudaSuccess) return e;
+    auto topdown = [&](const void* kern, int* segw, float4* out) -> cudaError_t {
+        cudaMemsetAsync(s.qctl, 0, sizeof(int) * (2 + MAX_LEVELS), stream);
+        k_reach_init<<<(B + 127) / 128, 128, 0, stream>>>(s.segs, B, s.bounds, segw, s.queue, s.qctl);
+        // co-resident blocks (per device: the grid must fit at once or the
+        // cooperative launch fails); all of them -- the levels are
+        // latency-bound chains of dependent loads
+        int per_sm = 0;
+        cudaError_t err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T_BLK, 0);
+        if (err != cudaSuccess) return err;
+        const int grid = sms * (per_sm < 1 ? 1 : per_sm);
         const BlasSeg* a0 = s.segs;
         const int* a1 = s.seg_of;
         const float4* a2 = s.rec;
-        int* a3 = s.seg4;
+        int* a3 = segw;
         int2* a4 = s.queue;
         int* a5 = s.qctl;
-        float4* a6 = a.nodes;
+        float4* a6 = out;
         void* args[] = {&a0, &a1, &a2, &a3, &a4, &a5, &a6};
-        e = cudaLaunchCooperativeKernel((const void*)k_bvh4_topdown, dim3(grid), dim3(T_BLK), args, 0, stream);
-        if (e != cudaSuccess) return e;
-    }
-    }
+        return cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(T_BLK), args, 0, stream);
+    };
+    e = topdown((const void*)k_bvhw_topdown<4>, s.seg4, a.nodes);
+    if (e != cudaSuccess) return e;
     k_write4_small<<<(B + 127) / 128, 128, 0, stream>>>(s.segs, B, s.bounds, sv, s.tri_box, a.nodes);
-    if (a.nodes8)
-        k_collapse<8><<<gb, T_BLK, 0, stream>>>(s.segs, s.seg_of, s.bounds, F, sv, s.tri_box, s.child, s.ibox,
-                                                s.size, a.nodes8);
+    if (a.nodes8) {
+        e = topdown((const void*)k_bvhw_topdown<8>, s.seg8, a.nodes8);
+        if (e != cudaSuccess) return e;
+        k_write8_small<<<(B + 127) / 128, 128, 0, stream>>>(s.segs, B, s.bounds, s.tri_box, a.nodes8);
+    }
     k_asset_info<<<(B + 127) / 128, 128, 0, stream>>>(s.segs, B, s.bounds, s.ibox, s.tri_box, sv, s.depth,
                                                       s.seg4);
     return cudaGetLastError();
