@@ -47,6 +47,14 @@
  * stream) with no hidden synchronisation, except where a call says so.  One
  * scene must be used by one stream at a time; different scenes may be used
  * concurrently from different threads.
+ *
+ * CUDA graphs: agr_set_instance_transforms, agr_build, agr_refit, the device
+ * casts, agr_checksum and agr_sim_kinematic_step enqueue only kernels,
+ * device copies and event records, so a step made of them can be captured
+ * (cudaStreamBeginCapture / torch.cuda.graph) and replayed -- bench.py's
+ * Table-II env step does.  agr_update_mesh(es) uploads host-side tables
+ * through a staging buffer that later calls overwrite, and the *_host casts
+ * synchronise: do not capture those.
  */
 #ifndef AGR_H
 #define AGR_H
