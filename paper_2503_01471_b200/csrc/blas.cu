@@ -1062,6 +1062,8 @@ __global__ void __launch_bounds__(T_BLK) k_bvhw_topdown(const BlasSeg* segs, con
         for (int t0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31); t0 < n_lvl; t0 += stride) {
             const int t = t0 + lane;
             int2 push[W];
+#pragma unroll
+            for (int k = 0; k < W; ++k) push[k] = make_int2(-1, -1);
             int npush = 0;
             if (t < n_lvl) {
                 const int2 item = __ldcg(queue + begin + t);
@@ -1076,35 +1078,47 @@ __global__ void __launch_bounds__(T_BLK) k_bvhw_topdown(const BlasSeg* segs, con
                 for (int k = 0; k < W; ++k) { refs[k] = REF_EMPTY; aux[k] = 0; }
                 read_rec(rec + 4 * (size_t)(x - off), bx[0], bx[1], refs[0], refs[1], aux[0], aux[1]);
                 int cnt = 2;
-                while (cnt < W) {  // collapse_w<W>: open the largest-area internal member
-                    int best = -1;
+                // collapse_w<W>: open the largest-area internal member (every
+                // array index static, so the frontier stays in registers)
+                bool open = true;
+#pragma unroll
+                for (int step = 2; step < W; ++step) {
+                    int best = -1, best_ref = 0;
                     float best_a = -1.0f;
-                    for (int k = 0; k < cnt; ++k)
-                        if (refs[k] >= 0) {
+#pragma unroll
+                    for (int k = 0; k < W; ++k)
+                        if (k < step && refs[k] >= 0) {
                             const float a = half_area(bx[k]);
-                            if (a > best_a) { best_a = a; best = k; }
+                            if (a > best_a) { best_a = a; best = k; best_ref = refs[k]; }
                         }
-                    if (best < 0) break;
+                    open = open && best >= 0;
+                    if (!open) continue;
                     float ca[6], cb[6];
                     int ra, rb, xa, xb;
-                    read_rec(rec + 4 * (size_t)refs[best], ca, cb, ra, rb, xa, xb);
-                    for (int k = W - 1; k > best + 1; --k)
-                        if (k <= cnt) {
-                            refs[k] = refs[k - 1];
-                            aux[k] = aux[k - 1];
-                            for (int q = 0; q < 6; ++q) bx[k][q] = bx[k - 1][q];
-                        }
-                    refs[best] = ra; aux[best] = xa;
-                    refs[best + 1] = rb; aux[best + 1] = xb;
-                    for (int q = 0; q < 6; ++q) { bx[best][q] = ca[q]; bx[best + 1][q] = cb[q]; }
-                    ++cnt;
+                    read_rec(rec + 4 * (size_t)best_ref, ca, cb, ra, rb, xa, xb);
+                    // shift the members after `best` up by one and put the
+                    // opened node's children at best, best + 1 (selects, not
+                    // indexed stores)
+#pragma unroll
+                    for (int k = W - 1; k >= 0; --k) {
+                        const bool sh = k > best + 1 && k <= step, is_b = k == best, is_b1 = k == best + 1;
+                        const int kk = k > 0 ? k - 1 : 0;
+                        refs[k] = sh ? refs[kk] : is_b ? ra : is_b1 ? rb : refs[k];
+                        aux[k] = sh ? aux[kk] : is_b ? xa : is_b1 ? xb : aux[k];
+#pragma unroll
+                        for (int q = 0; q < 6; ++q)
+                            bx[k][q] = sh ? bx[kk][q] : is_b ? ca[q] : is_b1 ? cb[q] : bx[k][q];
+                    }
+                    cnt = step + 1;
                 }
                 int gr[W];
                 bool internal[W];
+#pragma unroll
                 for (int k = 0; k < W; ++k) {
                     internal[k] = false;
                     if (k >= cnt) {
                         refs[k] = REF_EMPTY;
+#pragma unroll
                         for (int q = 0; q < 6; ++q) bx[k][q] = __int_as_float(0x7f800000);  // +inf: never hit
                         gr[k] = REF_EMPTY;
                     } else if (refs[k] < 0) {
@@ -1134,16 +1148,31 @@ __global__ void __launch_bounds__(T_BLK) k_bvhw_topdown(const BlasSeg* segs, con
                     first = __shfl_sync(grp, base, leader) + pre;
                 }
                 int q = 0;
-                for (int k = 0; k < W; ++k)
+#pragma unroll
+                for (int k = 0; k < W; ++k) {
+                    push[k] = make_int2(-1, -1);
                     if (internal[k]) {
-                        const int slot = first + q;
+                        const int slot = first + q++;
                         gr[k] = S.node_base + slot;
-                        push[q++] = make_int2(off + refs[k], slot);
+                        push[k] = make_int2(off + refs[k], slot);
                     }
-                if (W == 4)
-                    write_node4(nodes, S.node_base + item.y, reinterpret_cast<const float(*)[6]>(bx), gr, cnt);
-                else
-                    for (int k = 0; k < W; ++k) write_child8(nodes, S.node_base + item.y, k, bx[k], gr[k]);
+                }
+                const int g = S.node_base + item.y;
+                if (W == 4) {
+                    float4* p = nodes + 8 * (size_t)g;  // write_node4's layout, static indices
+                    p[0] = make_float4(bx[0][0], bx[1][0], bx[2][0], bx[3 % W][0]);
+                    p[1] = make_float4(bx[0][3], bx[1][3], bx[2][3], bx[3 % W][3]);
+                    p[2] = make_float4(bx[0][1], bx[1][1], bx[2][1], bx[3 % W][1]);
+                    p[3] = make_float4(bx[0][4], bx[1][4], bx[2][4], bx[3 % W][4]);
+                    p[4] = make_float4(bx[0][2], bx[1][2], bx[2][2], bx[3 % W][2]);
+                    p[5] = make_float4(bx[0][5], bx[1][5], bx[2][5], bx[3 % W][5]);
+                    p[6] = make_float4(__int_as_float(gr[0]), __int_as_float(gr[1]), __int_as_float(gr[2]),
+                                       __int_as_float(gr[3 % W]));
+                    p[7] = make_float4(__int_as_float(cnt), 0.0f, 0.0f, 0.0f);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < W; ++k) write_child8(nodes, g, k, bx[k], gr[k]);
+                }
             }
             // warp-aggregated append of the next level
             unsigned incl = npush;
@@ -1155,8 +1184,10 @@ __global__ void __launch_bounds__(T_BLK) k_bvhw_topdown(const BlasSeg* segs, con
             int base = 0;
             if (lane == 31 && tot) base = atomicAdd(qctl + 3 + L, (int)tot);
             base = __shfl_sync(FULL, base, 31);
-            const int pos = next + base + (int)(incl - npush);
-            for (int k = 0; k < npush; ++k) queue[pos + k] = push[k];
+            int pos = next + base + (int)(incl - npush);
+#pragma unroll
+            for (int k = 0; k < W; ++k)
+                if (push[k].x >= 0) queue[pos++] = push[k];
         }
         grid.sync();
         begin = next;
