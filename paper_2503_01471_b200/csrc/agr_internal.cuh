@@ -174,25 +174,32 @@ __device__ __forceinline__ int collapse_w(int j, const CHILD& child, const BOX& 
 #pragma unroll
     for (int k = 2; k < W; ++k) refs[k] = REF_EMPTY;
     int cnt = 2;
-    while (cnt < W) {
-        int best = -1;
+    bool open = true;
+    // static indices and selects only, so refs[] stays in registers
+#pragma unroll
+    for (int step = 2; step < W; ++step) {
+        int best = -1, r = 0;
         float best_a = -1.0f;
-        for (int k = 0; k < cnt; ++k) {
+#pragma unroll
+        for (int k = 0; k < W; ++k) {
             // keep_pairs: a node over two leaves stays closed (it becomes a
             // pair leaf) and the slot goes to a larger subtree
-            if (refs[k] >= 0 && !(keep_pairs && child(refs[k], 0) < 0 && child(refs[k], 1) < 0)) {
+            if (k < step && refs[k] >= 0 && !(keep_pairs && child(refs[k], 0) < 0 && child(refs[k], 1) < 0)) {
                 float b[6];
                 box(refs[k], b);
                 float a = half_area(b);
-                if (a > best_a) { best_a = a; best = k; }
+                if (a > best_a) { best_a = a; best = k; r = refs[k]; }
             }
         }
-        if (best < 0) break;
-        const int r = refs[best];
-        for (int k = cnt; k > best + 1; --k) refs[k] = refs[k - 1];
-        refs[best] = child(r, 0);
-        refs[best + 1] = child(r, 1);
-        ++cnt;
+        open = open && best >= 0;
+        if (!open) continue;
+        const int c0 = child(r, 0), c1 = child(r, 1);
+#pragma unroll
+        for (int k = W - 1; k >= 0; --k) {
+            const int kk = k > 0 ? k - 1 : 0;
+            refs[k] = (k > best + 1 && k <= step) ? refs[kk] : k == best ? c0 : k == best + 1 ? c1 : refs[k];
+        }
+        cnt = step + 1;
     }
     return cnt;
 }
