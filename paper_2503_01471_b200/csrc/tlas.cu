@@ -572,15 +572,19 @@ __global__ void k_tlas(TlasArgs a, int rebuild) {
 // internal node per lane, the fit iterates "every node := union of its
 // children" until nothing changes (min / max are exact, so the boxes equal
 // the CTA path's bottom-up fit bit for bit) and the collapses are the same
-// code.  2048 16-item envs: 124 -> ~10 us per refit (ncu).
-constexpr int TW_WARPS = 4;  // warps (envs) per block
+// code.  Refits go this way for envs of up to 128 items (4 nodes per lane).
+// 2048 16-item envs: 124 -> ~10 us per refit (ncu); c3 (91 items): update
+// 0.110 -> 0.061 ms.
+constexpr int TW_WARPS = 4;    // warps (envs) per block
+constexpr int TW_MAX = 128;    // refit: up to 4 items / nodes per lane (builds: 32)
+constexpr int TW_PER = TW_MAX / 32;
 struct TlasWarpSmem {
     uint64_t keys[32];
-    float box[32][6];
-    float ibox[31][6];
-    int child[62];
-    int nparent[31];
-    int lparent[32];
+    float box[TW_MAX][6];
+    float ibox[TW_MAX - 1][6];
+    int child[2 * (TW_MAX - 1)];
+    int nparent[TW_MAX - 1];
+    int lparent[TW_MAX];
 };
 
 __global__ void __launch_bounds__(32 * TW_WARPS) k_tlas_warp(TlasArgs a, int rebuild) {
@@ -617,11 +621,12 @@ __global__ void __launch_bounds__(32 * TW_WARPS) k_tlas_warp(TlasArgs a, int reb
         return;
     }
     float bl[6];
-    if (lane < n) {
-        for (int k = 0; k < 6; ++k) bl[k] = a.item_box[6 * (i0 + lane) + k];
-        for (int k = 0; k < 6; ++k) s.box[lane][k] = bl[k];
-    }
-    if (rebuild) {
+    for (int i = lane; i < n; i += 32)
+        for (int k = 0; k < 6; ++k) s.box[i][k] = a.item_box[6 * (i0 + i) + k];
+    __syncwarp();
+    if (lane < n)
+        for (int k = 0; k < 6; ++k) bl[k] = s.box[lane][k];
+    if (rebuild) {  // n <= 32 (tlas_build)
         // centroid bounds of the non-empty boxes, Morton keys, lane bitonic sort
         float lo[3] = {FLT_MAX, FLT_MAX, FLT_MAX}, hi[3] = {-FLT_MAX, -FLT_MAX, -FLT_MAX};
         const bool valid = lane < n && !isinf(bl[0]);
@@ -691,36 +696,43 @@ __global__ void __launch_bounds__(32 * TW_WARPS) k_tlas_warp(TlasArgs a, int reb
         for (int o = 16; o > 0; o >>= 1) dd = max(dd, __shfl_xor_sync(FULL, dd, o));
         if (lane == 0) atomicMax(&a.tlas_depth[e], dd);
     } else {
-        if (lane < n - 1) {
-            s.child[2 * lane] = a.tlas_child[2 * (toff + lane)];
-            s.child[2 * lane + 1] = a.tlas_child[2 * (toff + lane) + 1];
+        for (int j = lane; j < n - 1; j += 32) {
+            s.child[2 * j] = a.tlas_child[2 * (toff + j)];
+            s.child[2 * j + 1] = a.tlas_child[2 * (toff + j) + 1];
         }
-        if (lane < n) s.lparent[lane] = a.tlas_item_parent[i0 + lane];
     }
-    // fit: every internal node := union of its children, until nothing changes
-    float ib[6] = {inf_f(), inf_f(), inf_f(), -inf_f(), -inf_f(), -inf_f()};
-    int ra = 0, rb = 0;
-    if (lane < n - 1) {
-        ra = s.child[2 * lane];
-        rb = s.child[2 * lane + 1];
-        for (int k = 0; k < 6; ++k) s.ibox[lane][k] = ib[k];
+    // fit: every internal node := union of its children, until nothing
+    // changes (lane l owns nodes l, l + 32, ...)
+    __syncwarp();
+    for (int j = lane; j < n - 1; j += 32) {
+        s.ibox[j][0] = s.ibox[j][1] = s.ibox[j][2] = inf_f();
+        s.ibox[j][3] = s.ibox[j][4] = s.ibox[j][5] = -inf_f();
     }
     __syncwarp();
     for (bool changed = true; __any_sync(FULL, changed);) {
         changed = false;
-        float nb[6];
-        if (lane < n - 1) {
-            const float* pa = ra < 0 ? s.box[~ra] : s.ibox[ra];
-            const float* pb = rb < 0 ? s.box[~rb] : s.ibox[rb];
-            for (int k = 0; k < 3; ++k) {
-                nb[k] = fminf(pa[k], pb[k]);
-                nb[3 + k] = fmaxf(pa[3 + k], pb[3 + k]);
+        float nb[TW_PER][6];
+#pragma unroll
+        for (int m = 0; m < TW_PER; ++m) {
+            const int j = lane + 32 * m;
+            if (j < n - 1) {
+                const int ra = s.child[2 * j], rb = s.child[2 * j + 1];
+                const float* pa = ra < 0 ? s.box[~ra] : s.ibox[ra];
+                const float* pb = rb < 0 ? s.box[~rb] : s.ibox[rb];
+                for (int k = 0; k < 3; ++k) {
+                    nb[m][k] = fminf(pa[k], pb[k]);
+                    nb[m][3 + k] = fmaxf(pa[3 + k], pb[3 + k]);
+                }
+                for (int k = 0; k < 6; ++k) changed |= __float_as_int(nb[m][k]) != __float_as_int(s.ibox[j][k]);
             }
-            for (int k = 0; k < 6; ++k) changed |= __float_as_int(nb[k]) != __float_as_int(ib[k]);
         }
         __syncwarp();
-        if (lane < n - 1)
-            for (int k = 0; k < 6; ++k) s.ibox[lane][k] = ib[k] = nb[k];
+#pragma unroll
+        for (int m = 0; m < TW_PER; ++m) {
+            const int j = lane + 32 * m;
+            if (j < n - 1)
+                for (int k = 0; k < 6; ++k) s.ibox[j][k] = nb[m][k];
+        }
         __syncwarp();
     }
     // BVH4 node j = greedy 4-wide collapse of binary node j (and the BVH8 copy)
@@ -728,8 +740,7 @@ __global__ void __launch_bounds__(32 * TW_WARPS) k_tlas_warp(TlasArgs a, int reb
     auto bx = [&](int r, float b[6]) {
         for (int k = 0; k < 6; ++k) b[k] = s.ibox[r][k];
     };
-    if (lane < n - 1) {
-        const int j = lane;
+    for (int j = lane; j < n - 1; j += 32) {
         int refs[4];
         const int cnt = collapse4(j, ch, bx, refs);
         float b[4][6];
@@ -781,7 +792,7 @@ cudaError_t tlas_build(const TlasArgs& a, bool rebuild, cudaStream_t stream) {
         cudaError_t e = cudaMemsetAsync(a.tlas_depth, 0, sizeof(int) * a.n_envs, stream);
         if (e != cudaSuccess) return e;
     }
-    if (a.max_n <= 32 && (!rebuild || a.builder == 0)) {
+    if (rebuild ? (a.max_n <= 32 && a.builder == 0) : a.max_n <= TW_MAX) {
         k_tlas_warp<<<(a.n_envs + TW_WARPS - 1) / TW_WARPS, 32 * TW_WARPS, 0, stream>>>(a, rebuild ? 1 : 0);
         return cudaGetLastError();
     }

@@ -1025,17 +1025,44 @@ def test_wide_tile_cameras_all_schedules_bitwise():
     s.close()
 
 
+@pytest.mark.parametrize("builder", [0, 1])
+def test_tlas_warp_refit_equals_cta_refit_c3_bitwise(builder):
+    """c3-shaped envs (91 TLAS items: warp refit, CTA build) refit after new
+    transforms give bitwise the TLAS a 140-item-env scene (CTA refit) gives."""
+    sc, sensor = sg.config3(n_envs=3)
+    per_env = [[(int(sc.inst_asset[i]), int(sc.inst_label[i]), sc.inst_T[i])
+                for i in range(int(sc.env_off[e]), int(sc.env_off[e + 1]))] for e in range(3)]
+    big = per_env[0] + per_env[1][:89]
+    scs = [sg.assemble(sc.meshes, per_env), sg.assemble(sc.meshes, per_env + [big])]
+    scenes = [make_scene(x, build=False) for x in scs]
+    for x in scenes:
+        x.set_tlas_builder(builder)
+        x.build()
+    for x, scx in zip(scenes, scs):
+        T2 = scx.inst_T.copy()
+        T2[:, :2, 3] += 0.3
+        x.set_instance_transforms(torch.from_numpy(T2).to(dev()))
+        x.refit()
+    for e in range(3):
+        a, ra = scenes[0].debug_export_bvh4(-1 - e)
+        b, rb = scenes[1].debug_export_bvh4(-1 - e)
+        assert ra == rb and np.array_equal(a.view(np.uint32), b.view(np.uint32)), e
+    for x in scenes:
+        x.close()
+
+
 def test_tlas_warp_path_equals_cta_path_bitwise():
-    """Envs of <= 32 TLAS items are built / refit by one warp each
-    (tlas.cu k_tlas_warp) unless some env of the scene is larger (then every
-    env takes the CTA path): the same envs give bitwise the same BVH4 TLAS
-    and images either way, after an LBVH build and after a refit."""
+    """Envs of <= 32 TLAS items are LBVH-built, and envs of <= 128 items
+    refit, by one warp each (tlas.cu k_tlas_warp) unless some env of the
+    scene is larger (then every env takes the CTA path): the same envs give
+    bitwise the same BVH4 TLAS and images either way, after an LBVH build
+    and after a refit."""
     sc, sensor = sg.config2(n_envs=3)  # 10 items per env
-    big = [(int(a), 40 + k, T) for k, (a, T) in enumerate(zip(sc.inst_asset[:10], sc.inst_T[:10]))] * 4
+    big = [(int(a), 40 + k, T) for k, (a, T) in enumerate(zip(sc.inst_asset[:10], sc.inst_T[:10]))] * 14
     per_env = [[(int(sc.inst_asset[i]), int(sc.inst_label[i]), sc.inst_T[i])
                 for i in range(int(sc.env_off[e]), int(sc.env_off[e + 1]))] for e in range(3)]
     small = sg.assemble(sc.meshes, per_env)
-    mixed = sg.assemble(sc.meshes, per_env + [big])  # a 40-item env appended last
+    mixed = sg.assemble(sc.meshes, per_env + [big])  # a 140-item env appended last
     scenes = [make_scene(small), make_scene(mixed)]
     poses = sensor["poses"][:3]
     sen = dict(sensor, poses=poses)
