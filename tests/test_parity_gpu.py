@@ -1046,7 +1046,10 @@ def test_tlas_warp_refit_equals_cta_refit_c3_bitwise(builder):
     for e in range(3):
         a, ra = scenes[0].debug_export_bvh4(-1 - e)
         b, rb = scenes[1].debug_export_bvh4(-1 - e)
-        assert ra == rb and np.array_equal(a.view(np.uint32), b.view(np.uint32)), e
+        if builder == 0:  # LBVH: deterministic node numbering
+            assert ra == rb and np.array_equal(a.view(np.uint32), b.view(np.uint32)), e
+        else:  # the SAH build numbers nodes in the order its warps claim tasks
+            assert _bvh4_canonical(a, ra) == _bvh4_canonical(b, rb), e
     for x in scenes:
         x.close()
 
