@@ -187,7 +187,7 @@ def blas_launches(trbvh_rounds, bvh8):
     n = 5 + 4 * 5 + 3
     if trbvh_rounds > 0:
         n += 1 + trbvh_rounds + 1
-    n += 1 + 3 + (3 if bvh8 else 0) + 1
+    n += 1 + 3 + (3 if bvh8 else 0) + 1  # (mesh updates keep the greedy BVH8 collapse: no DP pass)
     return n
 
 

@@ -258,6 +258,7 @@ struct BlasBatchArgs {
     float* triv;           // global exact-vertex array
     uint32_t* dbg_morton;  // optional: sorted codes at leaf_base + p (device) or null
     int trbvh_rounds;      // treelet-restructuring passes after the LBVH (0 = plain LBVH)
+    int opt_collapse;      // 1: SAH-optimal BVH8 collapse (creation-time builds); 0: greedy (mesh updates)
     void* h_stage;         // optional pinned host staging for the segment / sort-block tables
     size_t h_stage_bytes;
     cudaEvent_t stage_free;  // recorded after each upload from h_stage

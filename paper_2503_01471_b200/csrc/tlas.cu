@@ -133,6 +133,85 @@ __device__ __forceinline__ void slot_box(const float* src, float* dst) {
     for (int k = 0; k < 6; ++k) dst[k] = empty ? inf_f() : src[k];
 }
 
+// ---- SAH-optimal BVH8 collapse of a TLAS (Ylitie, Karras & Laine 2017) -----------
+// As for the BLAS (blas.cu k_dp8): C(n, i) = the lowest SAH cost of n's
+// subtree as <= i BVH8 child slots; here a leaf is an instance entry and
+// there are no pair leaves, so every leaf's term is the same in every
+// collapse and only the node terms decide (TDP_CT 1.5, 3 and 5 give the
+// same trees).
+// Tables are computed by a fixed-point iteration over all internal nodes
+// (each := its formula over the children's current tables, from +inf, until
+// nothing changes -- min and + of decreasing values converge in height
+// steps), so both the warp and the CTA builders get the same tables.  Envs
+// of at most TDP_MAX items use it; larger ones keep the greedy collapse.
+#ifndef AGR_TDP_CT
+#define AGR_TDP_CT 1.5f
+#endif
+constexpr float TDP_CN = 1.0f, TDP_CT = AGR_TDP_CT;
+constexpr int TDP_MAX = 128;
+__device__ __forceinline__ float box_cost_area(const float* b) { return b[0] <= b[3] ? half_area(b) : 0.0f; }
+
+// New table of internal node j from its children's current tables.
+template <class CH, class LB, class NB, class TB>
+__device__ __forceinline__ void tdp_node(int j, const CH& child, const LB& lbox, const NB& nbox, const TB& tab,
+                                         float C[8]) {
+    float cl[2][8];
+    for (int side = 0; side < 2; ++side) {
+        const int r = child(j, side);
+        if (r < 0) {
+            const float v = TDP_CT * box_cost_area(lbox(~r));
+            for (int i = 0; i < 8; ++i) cl[side][i] = v;
+        } else {
+            for (int i = 0; i < 8; ++i) cl[side][i] = tab(r)[i];
+        }
+    }
+    float cd[9];
+    for (int jj = 2; jj <= 8; ++jj) {
+        float m = INFINITY;
+        for (int k = 1; k < jj; ++k) m = fminf(m, cl[0][k - 1] + cl[1][jj - k - 1]);
+        cd[jj] = m;
+    }
+    C[0] = TDP_CN * box_cost_area(nbox(j)) + cd[8];
+    for (int i = 1; i < 8; ++i) C[i] = fminf(C[i - 1], cd[i + 1]);
+}
+
+// The BVH8 children (binary refs, REF_EMPTY padded) of internal node j.
+template <class CH, class LB, class TB>
+__device__ __forceinline__ void tdp_children(int j, const CH& child, const LB& lbox, const TB& tab, int refs[8]) {
+    for (int k = 0; k < 8; ++k) refs[k] = REF_EMPTY;
+    int st_n[8], st_j[8], sp = 0, cnt = 0;
+    st_n[sp] = j; st_j[sp] = 8; ++sp;
+    while (sp > 0) {
+        --sp;
+        const int nn = st_n[sp], jj = st_j[sp];
+        int rc[2];
+        float t[2][8];
+        for (int side = 0; side < 2; ++side) {
+            rc[side] = child(nn, side);
+            if (rc[side] < 0) {
+                const float v = TDP_CT * box_cost_area(lbox(~rc[side]));
+                for (int i = 0; i < 8; ++i) t[side][i] = v;
+            } else {
+                for (int i = 0; i < 8; ++i) t[side][i] = tab(rc[side])[i];
+            }
+        }
+        int kb = 1;
+        float m = t[0][0] + t[1][jj - 2];
+        for (int k = 2; k < jj; ++k) {
+            const float v = t[0][k - 1] + t[1][jj - k - 1];
+            if (v < m) { m = v; kb = k; }
+        }
+        for (int side = 0; side < 2; ++side) {
+            int b = side == 0 ? kb : jj - kb;
+            if (rc[side] >= 0) {
+                while (b > 1 && t[side][b - 1] == t[side][b - 2]) --b;
+                if (b > 1) { st_n[sp] = rc[side]; st_j[sp] = b; ++sp; continue; }
+            }
+            refs[cnt++] = rc[side];
+        }
+    }
+}
+
 // ---- K7/K8: per-env TLAS build / refit -----------------------------------------
 struct TlasSmem {
     int* task;       // [4 (n-1)] SAH build tasks (start, end, ready, -) by node id
@@ -549,10 +628,35 @@ __global__ void k_tlas(TlasArgs a, int rebuild) {
         write_node4(a.nodes, nodebase + j, b, g, cnt);
     }
     if (a.nodes8) {
-        // the BVH8 copy of the interval-packet traversal: 8-wide collapse
+        // the BVH8 copy of the interval-packet traversal: SAH-optimal 8-wide
+        // collapse for envs of <= TDP_MAX items, greedy above
+        __shared__ float dpt[TDP_MAX - 1][8];
+        const bool opt = n <= TDP_MAX;
+        auto lbf = [&](int i) { return s.box + 6 * i; };
+        auto nbf = [&](int r) { return s.ibox + 6 * r; };
+        auto tbf = [&](int r) { return dpt[r]; };
+        if (opt) {
+            for (int j = tid; j < n - 1; j += blockDim.x)
+                for (int i = 0; i < 8; ++i) dpt[j][i] = INFINITY;
+            __syncthreads();
+            for (bool changed = true; changed;) {
+                float C[8];
+                bool mine = false;
+                const int j = tid;  // n - 1 <= 127 < blockDim.x
+                if (j < n - 1) {
+                    tdp_node(j, ch, lbf, nbf, tbf, C);
+                    for (int i = 0; i < 8; ++i) mine |= __float_as_int(C[i]) != __float_as_int(dpt[j][i]);
+                }
+                __syncthreads();
+                if (j < n - 1)
+                    for (int i = 0; i < 8; ++i) dpt[j][i] = C[i];
+                changed = __syncthreads_or(mine) != 0;
+            }
+        }
         for (int j = tid; j < n - 1; j += blockDim.x) {
             int refs[8];
-            collapse_w<8>(j, ch, bx, refs);
+            if (opt) tdp_children(j, ch, lbf, tbf, refs);
+            else collapse_w<8>(j, ch, bx, refs);
             for (int c = 0; c < 8; ++c) {
                 const int r = refs[c];
                 const float* src = r == REF_EMPTY ? EMPTY : (r < 0 ? s.box + 6 * ~r : s.ibox + 6 * r);
@@ -582,13 +686,15 @@ struct TlasWarpSmem {
     uint64_t keys[32];
     float box[TW_MAX][6];
     float ibox[TW_MAX - 1][6];
+    float dpt[TW_MAX - 1][8];  // SAH-optimal BVH8 tables
     int child[2 * (TW_MAX - 1)];
     int nparent[TW_MAX - 1];
     int lparent[TW_MAX];
 };
 
 __global__ void __launch_bounds__(32 * TW_WARPS) k_tlas_warp(TlasArgs a, int rebuild) {
-    __shared__ TlasWarpSmem sm[TW_WARPS];
+    extern __shared__ __align__(16) unsigned char tw_raw[];
+    TlasWarpSmem* sm = reinterpret_cast<TlasWarpSmem*>(tw_raw);
     const unsigned FULL = 0xFFFFFFFFu;
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int e = blockIdx.x * TW_WARPS + w;
@@ -740,6 +846,34 @@ __global__ void __launch_bounds__(32 * TW_WARPS) k_tlas_warp(TlasArgs a, int reb
     auto bx = [&](int r, float b[6]) {
         for (int k = 0; k < 6; ++k) b[k] = s.ibox[r][k];
     };
+    if (a.nodes8) {  // SAH-optimal BVH8 tables (n <= TW_MAX = TDP_MAX)
+        auto lbf = [&](int i) { return s.box[i]; };
+        auto nbf = [&](int r) { return s.ibox[r]; };
+        auto tbf = [&](int r) { return s.dpt[r]; };
+        for (int j = lane; j < n - 1; j += 32)
+            for (int i = 0; i < 8; ++i) s.dpt[j][i] = INFINITY;
+        __syncwarp();
+        for (bool changed = true; __any_sync(FULL, changed);) {
+            changed = false;
+            float C[TW_PER][8];
+#pragma unroll
+            for (int m = 0; m < TW_PER; ++m) {
+                const int j = lane + 32 * m;
+                if (j < n - 1) {
+                    tdp_node(j, ch, lbf, nbf, tbf, C[m]);
+                    for (int i = 0; i < 8; ++i) changed |= __float_as_int(C[m][i]) != __float_as_int(s.dpt[j][i]);
+                }
+            }
+            __syncwarp();
+#pragma unroll
+            for (int m = 0; m < TW_PER; ++m) {
+                const int j = lane + 32 * m;
+                if (j < n - 1)
+                    for (int i = 0; i < 8; ++i) s.dpt[j][i] = C[m][i];
+            }
+            __syncwarp();
+        }
+    }
     for (int j = lane; j < n - 1; j += 32) {
         int refs[4];
         const int cnt = collapse4(j, ch, bx, refs);
@@ -754,7 +888,7 @@ __global__ void __launch_bounds__(32 * TW_WARPS) k_tlas_warp(TlasArgs a, int reb
         write_node4(a.nodes, nodebase + j, b, g, cnt);
         if (a.nodes8) {
             int refs8[8];
-            collapse_w<8>(j, ch, bx, refs8);
+            tdp_children(j, ch, [&](int i) { return s.box[i]; }, [&](int r) { return s.dpt[r]; }, refs8);
             for (int c = 0; c < 8; ++c) {
                 const int r = refs8[c];
                 const float* src = r == REF_EMPTY ? EMPTY : (r < 0 ? s.box[~r] : s.ibox[r]);
@@ -793,7 +927,10 @@ cudaError_t tlas_build(const TlasArgs& a, bool rebuild, cudaStream_t stream) {
         if (e != cudaSuccess) return e;
     }
     if (rebuild ? (a.max_n <= 32 && a.builder == 0) : a.max_n <= TW_MAX) {
-        k_tlas_warp<<<(a.n_envs + TW_WARPS - 1) / TW_WARPS, 32 * TW_WARPS, 0, stream>>>(a, rebuild ? 1 : 0);
+        const int tw_smem = (int)sizeof(TlasWarpSmem) * TW_WARPS;
+        cudaError_t e = cudaFuncSetAttribute(k_tlas_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, tw_smem);
+        if (e != cudaSuccess) return e;
+        k_tlas_warp<<<(a.n_envs + TW_WARPS - 1) / TW_WARPS, 32 * TW_WARPS, tw_smem, stream>>>(a, rebuild ? 1 : 0);
         return cudaGetLastError();
     }
     k_tlas<<<a.n_envs, TLAS_THREADS, smem, stream>>>(a, rebuild ? 1 : 0);
