@@ -237,7 +237,10 @@ __device__ __forceinline__ int kdelta64(const uint64_t* k, int n, int i, int j) 
 // lowest SAH cost A_L N_L + A_R N_R, and partitions the items stably.  The
 // result is the same binary form as the Karras build (child refs + parents),
 // so the fit, the BVH4 collapse and the refit are shared.
-constexpr int SAH_BINS = 16;
+#ifndef AGR_SAH_BINS
+#define AGR_SAH_BINS 48  // 16 / 32 / 48: c3 9.53 / 9.57 / 9.58 Grays/s (64 exceeds the static shared memory)
+#endif
+constexpr int SAH_BINS = AGR_SAH_BINS;
 
 __device__ void sah_build_cta(const TlasSmem& s, int n) {
     __shared__ int q_head, next_node;
