@@ -258,6 +258,38 @@ def test_degenerate_faces_and_max_range_boundary():
     assert set(np.unique(f[2])) <= {2, 3}
 
 
+@pytest.mark.parametrize("node_width", [0, 4])
+def test_update_meshes_single_and_degenerate_assets(node_width):
+    """A batched mesh update over assets that become a single triangle, all
+    zero-area (no leaf at all) and ordinary again: the single-leaf and empty
+    BLAS roots (BVH4 and BVH8), the top-down builds around them, and the
+    casts in every schedule against the oracle."""
+    quad = np.asarray([[0, -2, -2], [0, 2, -2], [0, 2, 2], [0, -2, 2]], np.float32)
+    faces = np.asarray([[0, 1, 2], [0, 2, 3]], np.int32)
+    sph = sg.sphere_mesh(0.8, 2)
+    meshes = [sg.Mesh("a", quad, faces), sg.Mesh("b", quad.copy(), faces), sg.Mesh("c", sph.verts, sph.faces)]
+    pos = [(4.0, -0.6, 0.0), (5.0, 0.0, 0.0), (6.0, 3.5, 0.0)]
+    per_env = [[(a, a + 1, sg.make_T(np.eye(3), pos[a])) for a in range(3)]] * 2  # two envs, all three assets
+    sc = sg.assemble(meshes, per_env)
+    s = agr.Scene.from_scenegen(sc, device=0, node_width=node_width)
+    s.set_instance_transforms(torch.from_numpy(sc.inst_T).to(dev()))
+    s.build()
+    new = [quad.copy(), quad.copy(), (sph.verts * 1.1).astype(np.float32)]
+    new[0][3] = new[0][0]          # face 1 of asset 0 degenerate: one leaf left
+    new[1][:] = new[1][0]          # every vertex of asset 1 equal: no leaf at all
+    s.update_meshes([0, 1, 2], torch.from_numpy(np.concatenate(new)).to(dev()))
+    s.build()
+    sc2 = sg.assemble([sg.Mesh(m.name, v, m.faces) for m, v in zip(meshes, new)], per_env)
+    sensor = dict(kind="pinhole", cam=sg.pinhole(48, 32, 90.0), poses=sg.identity_poses(2), max_range=20.0)
+    ref = oracle.cast(sc2, oracle_rays(sensor, "depth"))
+    for mode in (0, 1, 2, 3):
+        s.set_traversal(mode)
+        got = to_np(cast_sensor(s, sensor, "depth"))
+        compare(ref, got["dist"], got["seg"], got["face"], f"degenerate update mode {mode}", max_amb=64)
+    assert set(np.unique(ref.seg)) >= {1, 3} and 2 not in set(np.unique(ref.seg))
+    s.close()
+
+
 def test_lidar_beams_small():
     sc, sensor = sg.config4(n_envs=8)
     sensor = dict(sensor, beams=sg.lidar_beams(32, 64))
