@@ -446,6 +446,72 @@ def test_c5_sampled_with_refit_steps():
         certify_all(sc2, sensor, "depth", got["dist"], got["seg"], got["face"], f"c5 step {step}")
 
 
+def _flat(out):
+    return {k: v.reshape(-1) for k, v in out.items()}
+
+
+@pytest.mark.slow
+def test_c5_bench_step_full_size():
+    """c5 at its stated 16384 envs in bench.py's launch configuration: every
+    step sets a new transform set and rebuilds the LBVH TLAS (warp-per-env
+    build with the SAH-optimal BVH8 collapse), then casts; 20 000 sampled rays
+    per step against the oracle and every ray of the first 2048 envs
+    certified."""
+    sc, sensor = sg.config5(n_envs=16384, ring=3)
+    ring = sc.extra["ring_T"]
+    s = make_scene(sc, build=False)
+    s.set_tlas_builder(0)
+    poses = torch.from_numpy(np.ascontiguousarray(sensor["poses"])).to(dev())
+    rng = np.random.default_rng(11)
+    E_cert = 2048
+    per_env = sensor["cam"]["W"] * sensor["cam"]["H"]
+    for step in (1, 2):
+        s.set_instance_transforms(torch.from_numpy(ring[step]).to(dev()))
+        s.build()
+        out = _flat(s.cast_pinhole(sensor["cam"], poses, sensor["max_range"], agr.AGR_DEPTH))
+        n = out["dist"].numel()
+        q = rng.choice(n, 20000, replace=False)
+        qt = torch.from_numpy(q).to(dev())
+        got = {k: v[qt].cpu().numpy() for k, v in out.items()}
+        sc2 = sg.Scene(sc.meshes, sc.env_off, sc.inst_asset, sc.inst_label, ring[step])
+        ref = oracle.cast(sc2, oracle_rays(sensor, "depth"), query=q)
+        compare(ref, got["dist"], got["seg"], got["face"], f"c5 full step {step}")
+        head = {k: v[: E_cert * per_env].cpu().numpy() for k, v in out.items()}
+        sub = sc2.env_slice(0, E_cert)
+        sen = dict(sensor, poses=sensor["poses"][:E_cert])
+        assert certify_all(sub, sen, "depth", head["dist"], head["seg"], head["face"], f"c5 step {step}") > 0
+        del out
+    s.close()
+
+
+@pytest.mark.slow
+def test_c4_bench_step_full_size():
+    """c4 at its stated 4096 envs in bench.py's launch configuration (SAH
+    TLAS built once, transforms set + refit, interval packets on the BVH8):
+    40 000 sampled beams against the oracle and every ray of the first 1024
+    envs certified."""
+    sc, sensor = sg.config4()
+    s = make_scene(sc, build=False)
+    s.set_tlas_builder(1)
+    s.build()
+    s.set_instance_transforms(torch.from_numpy(sc.inst_T).to(dev()))
+    s.refit()
+    beams = torch.from_numpy(np.ascontiguousarray(sensor["beams"])).to(dev())
+    poses = torch.from_numpy(np.ascontiguousarray(sensor["poses"])).to(dev())
+    out = _flat(s.cast_beams(beams, poses, sensor["max_range"]))
+    q = np.random.default_rng(12).choice(out["dist"].numel(), 40000, replace=False)
+    qt = torch.from_numpy(q).to(dev())
+    got = {k: v[qt].cpu().numpy() for k, v in out.items()}
+    ref = oracle.cast(sc, oracle_rays(sensor, "range"), query=q)
+    compare(ref, got["dist"], got["seg"], got["face"], "c4 full bench step")
+    E_cert = 1024
+    per_env = sensor["beams"].shape[0] * sensor["beams"].shape[1]
+    head = {k: v[: E_cert * per_env].cpu().numpy() for k, v in out.items()}
+    sen = dict(sensor, poses=sensor["poses"][:E_cert])
+    assert certify_all(sc.env_slice(0, E_cert), sen, "range", head["dist"], head["seg"], head["face"], "c4") > 0
+    s.close()
+
+
 # ---- per-hit channels (normal, barycentrics, point cloud) -------------------
 
 ALL = ("dist", "seg", "face", "normal", "bary", "point")
