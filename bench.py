@@ -179,12 +179,12 @@ def make_workload(cfg, n_envs, env_base):
 
 def blas_launches(trbvh_rounds, bvh8):
     """Kernels one agr_update_meshes batch launches (blas.cu blas_build_batch):
-    seg_of, init_bounds, radius, tri_prep, morton; 4 sort passes of hist +
+    seg_of, init_bounds, tri_prep (+ radius), morton; 4 sort passes of hist +
     3-launch scan + scatter; pack_tris, karras, fit; [size copy + treelet
     rounds + depth]; top-down init + top-down BVH4 +
     single-leaf roots [the same three for the BVH8 copy]; asset info
     (checked against the ncu launch list, profiles/r02l_launches_c6.csv)."""
-    n = 5 + 4 * 5 + 3
+    n = 4 + 4 * 5 + 3
     if trbvh_rounds > 0:
         n += 1 + trbvh_rounds + 1
     n += 3 + (3 if bvh8 else 0) + 1  # (no child-record pass; mesh updates keep the greedy BVH8 collapse)

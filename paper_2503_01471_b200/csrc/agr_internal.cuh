@@ -73,7 +73,7 @@ struct BlasInfo {
     int n_leaves;    // non-degenerate triangles in the BLAS
     int n_faces;     // faces of the part
     float lo[3], hi[3];  // root box (object space, exact min/max)
-    float radius;    // max |v| over the asset's vertices (object units)
+    float radius;    // max |v| over the vertices of the part's faces (object units)
     int depth;       // BLAS depth (edges from root to deepest leaf)
     int n_nodes4;    // BVH4 nodes in use from node_base (the reachable collapse, compacted)
 };

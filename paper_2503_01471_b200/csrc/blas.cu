@@ -211,25 +211,12 @@ __global__ void k_init_bounds(uint32_t* b, int B) {
 }
 
 // ---- K1: triangle prep --------------------------------------------------------
-// asset radius over its vertices: one CTA per segment
-__global__ void k_radius(const BlasSeg* segs, uint32_t* bounds) {
-    const int s = blockIdx.x;
-    const float* verts = segs[s].verts;
-    const int V = segs[s].n_verts;
-    float r = 0.0f;
-    for (int v = threadIdx.x; v < V; v += blockDim.x) {
-        float x = verts[3 * v], y = verts[3 * v + 1], z = verts[3 * v + 2];
-        r = fmaxf(r, sqrtf(x * x + y * y + z * z) * 1.000001f);
-    }
-    for (int o = 16; o > 0; o >>= 1) r = fmaxf(r, __shfl_xor_sync(FULL, r, o));
-    if ((threadIdx.x & 31) == 0) atomicMax(&bounds[8 * s + 6], float_to_ordered(r));
-}
-
 __global__ void k_tri_prep(const BlasSeg* segs, const int* seg_of, int Ftot, float4* __restrict__ cent,
                            uint32_t* __restrict__ vflag, uint32_t* bounds) {
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
     const int s = g < Ftot ? __ldg(seg_of + g) : -1;
     float clo[3] = {FLT_MAX, FLT_MAX, FLT_MAX}, chi[3] = {-FLT_MAX, -FLT_MAX, -FLT_MAX};
+    float rad = 0.0f;  // the segment's radius: max |v| over its faces' vertices
     bool valid = false;
     if (s >= 0) {
         const BlasSeg& S = segs[s];
@@ -237,6 +224,8 @@ __global__ void k_tri_prep(const BlasSeg* segs, const int* seg_of, int Ftot, flo
         const float* a = S.verts + 3 * S.faces[3 * f];
         const float* b = S.verts + 3 * S.faces[3 * f + 1];
         const float* c = S.verts + 3 * S.faces[3 * f + 2];
+        for (const float* v : {a, b, c})
+            rad = fmaxf(rad, sqrtf(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]) * 1.000001f);
         // exact-input FP64 area: zero only for genuinely degenerate input
         d3 A = mkd(a[0], a[1], a[2]), B = mkd(b[0], b[1], b[2]), C = mkd(c[0], c[1], c[2]);
         d3 n = crossd(subd(B, A), subd(C, A));
@@ -256,40 +245,51 @@ __global__ void k_tri_prep(const BlasSeg* segs, const int* seg_of, int Ftot, flo
     // every warp of a segment queue up at L2 and stall the loads), else per
     // thread
     __shared__ int s_seg[2];
-    __shared__ uint32_t s_red[7];
-    if (threadIdx.x == 0) { s_seg[0] = s; s_red[6] = 0u; }
+    __shared__ uint32_t s_red[8];
+    if (threadIdx.x == 0) { s_seg[0] = s; s_red[6] = 0u; s_red[7] = 0u; }
     if (threadIdx.x < 3) { s_red[threadIdx.x] = 0xFFFFFFFFu; s_red[3 + threadIdx.x] = 0u; }
     if (threadIdx.x == blockDim.x - 1) s_seg[1] = s;
     __syncthreads();
     const int s0 = s_seg[0];
     if (s0 >= 0 && s_seg[1] == s0) {  // segments are contiguous: first == last => one segment
         unsigned cnt = __popc(__ballot_sync(FULL, valid));
-        for (int o = 16; o > 0; o >>= 1)
+        for (int o = 16; o > 0; o >>= 1) {
             for (int k = 0; k < 3; ++k) {
                 clo[k] = fminf(clo[k], __shfl_xor_sync(FULL, clo[k], o));
                 chi[k] = fmaxf(chi[k], __shfl_xor_sync(FULL, chi[k], o));
             }
-        if ((threadIdx.x & 31) == 0 && cnt > 0) {
-            for (int k = 0; k < 3; ++k) {
-                atomicMin(&s_red[k], float_to_ordered(clo[k]));
-                atomicMax(&s_red[3 + k], float_to_ordered(chi[k]));
+            rad = fmaxf(rad, __shfl_xor_sync(FULL, rad, o));
+        }
+        if ((threadIdx.x & 31) == 0) {
+            if (cnt > 0) {
+                for (int k = 0; k < 3; ++k) {
+                    atomicMin(&s_red[k], float_to_ordered(clo[k]));
+                    atomicMax(&s_red[3 + k], float_to_ordered(chi[k]));
+                }
+                atomicAdd(&s_red[6], cnt);
             }
-            atomicAdd(&s_red[6], cnt);
+            atomicMax(&s_red[7], float_to_ordered(rad));
         }
         __syncthreads();
-        if (threadIdx.x == 0 && s_red[6] > 0) {
-            for (int k = 0; k < 3; ++k) {
-                atomicMin(&bounds[8 * s0 + k], s_red[k]);
-                atomicMax(&bounds[8 * s0 + 3 + k], s_red[3 + k]);
+        if (threadIdx.x == 0) {
+            if (s_red[6] > 0) {
+                for (int k = 0; k < 3; ++k) {
+                    atomicMin(&bounds[8 * s0 + k], s_red[k]);
+                    atomicMax(&bounds[8 * s0 + 3 + k], s_red[3 + k]);
+                }
+                atomicAdd(&bounds[8 * s0 + 7], s_red[6]);
             }
-            atomicAdd(&bounds[8 * s0 + 7], s_red[6]);
+            atomicMax(&bounds[8 * s0 + 6], s_red[7]);
         }
-    } else if (valid) {
-        for (int k = 0; k < 3; ++k) {
-            atomicMin(&bounds[8 * s + k], float_to_ordered(clo[k]));
-            atomicMax(&bounds[8 * s + 3 + k], float_to_ordered(chi[k]));
+    } else if (s >= 0) {
+        if (valid) {
+            for (int k = 0; k < 3; ++k) {
+                atomicMin(&bounds[8 * s + k], float_to_ordered(clo[k]));
+                atomicMax(&bounds[8 * s + 3 + k], float_to_ordered(chi[k]));
+            }
+            atomicAdd(&bounds[8 * s + 7], 1u);
         }
-        atomicAdd(&bounds[8 * s + 7], 1u);
+        atomicMax(&bounds[8 * s + 6], float_to_ordered(rad));
     }
 }
 
@@ -1532,7 +1532,6 @@ cudaError_t blas_build_batch(BlasSeg* h_segs, int B, const BlasBatchArgs& a, voi
     const int gb = (F + T_BLK - 1) / T_BLK;
     k_seg_of<<<B, T_BLK, 0, stream>>>(s.segs, s.seg_of);
     k_init_bounds<<<(8 * B + T_BLK - 1) / T_BLK, T_BLK, 0, stream>>>(s.bounds, B);
-    k_radius<<<B, 128, 0, stream>>>(s.segs, s.bounds);
     k_tri_prep<<<gb, T_BLK, 0, stream>>>(s.segs, s.seg_of, F, s.cent, s.vals[1], s.bounds);
     k_morton<<<gb, T_BLK, 0, stream>>>(s.seg_of, s.cent, s.vals[1], F, s.bounds, s.mcode, s.keys[0],
                                        s.vals[0]);
