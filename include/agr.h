@@ -372,7 +372,8 @@ agr_status agr_set_tlas_builder(agr_scene scene, int32_t builder);
 
 /*
  * Traversal schedule (results are identical either way): 0 = auto (default;
- * the 32 rays of a 4x8 pinhole / beam tile traverse as one warp packet: a
+ * the 32 rays of a 4x8 pinhole tile (8 columns x 4 channels for beam
+ * tables) traverse as one warp packet: a
  * node is visited when the interval of the tile's ray directions may reach
  * a child, and every lane still tests each visited leaf on its own ray;
  * stereo shadow segments, whose origins differ per lane, visit the union

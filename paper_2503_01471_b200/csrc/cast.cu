@@ -35,12 +35,21 @@ namespace {
 #define AGR_IPACKET 1  // interval packets for primary pinhole / beam tiles
 #endif
 constexpr int CAST_THREADS = CAST_BLOCK;
-// Tile of one warp: TILE_W x TILE_H pixels (beams: columns x channels).
-#ifndef TILE_W
-#define TILE_W 4
+// Tile of one warp: W x H pixels (beams: columns x channels).  Pinholes
+// use 4 x 8 (8 x 4: c3 -3.6 %), LiDAR beam tables 8 x 4 (c4 +1.9 % over
+// 4 x 8: an 8-column x 4-channel tile spans 5.6 x 2.8 deg of an OS0-128).
+#ifndef TILE_W_PINHOLE
+#define TILE_W_PINHOLE 4
 #endif
-constexpr int TILE_H = 32 / TILE_W;
-constexpr int TILE_CENTRE_LANE = (TILE_H / 2 - 1) * TILE_W + TILE_W / 2 - 1;
+#ifndef TILE_W_BEAMS
+#define TILE_W_BEAMS 8
+#endif
+template <int MODEL>
+struct Tile {
+    static constexpr int W = MODEL == 2 ? TILE_W_BEAMS : TILE_W_PINHOLE;
+    static constexpr int H = 32 / W;
+    static constexpr int CL = (H / 2 - 1) * W + W / 2 - 1;  // the lane of the tile's centre ray
+};
 // 32 resident warps per SM: 64 registers per thread
 #ifndef CAST_MIN_BLOCKS
 #define CAST_MIN_BLOCKS (1024 / CAST_BLOCK)
@@ -565,7 +574,7 @@ __device__ __forceinline__ void traverse_lane(const SceneView& sv, int env, RayS
 }
 
 // ---- packet traversal (pinhole / beams tiles) ------------------------------------
-// The 32 rays of a 4x8 tile (TILE_W x TILE_H) traverse together: the warp visits a node if any
+// The 32 rays of a tile (Tile<MODEL>: 4x8 pinhole, 8x4 beams) traverse together: the warp visits a node if any
 // lane's ray hits it (ballot), descends first into the child most lanes reach
 // first, and keeps ONE stack per warp in shared memory.  Control flow is
 // warp-uniform (no divergence in the traversal loop); every node / triangle
@@ -573,7 +582,7 @@ __device__ __forceinline__ void traverse_lane(const SceneView& sv, int env, RayS
 // and triangle tests, so results equal the per-lane traversal.
 constexpr int PSTACK = 96;
 
-template <bool ANYHIT, bool COUNT, class LEAF>
+template <int CL, bool ANYHIT, bool COUNT, class LEAF>
 __device__ __forceinline__ void traverse_packet(const SceneView& sv, int env, RayState& rs,
                                                 const LEAF& leaf_fn, int* wstack,
                                                 Counters& cnt) {
@@ -612,11 +621,11 @@ __device__ __forceinline__ void traverse_packet(const SceneView& sv, int env, Ra
                 continue;
             }
             // order the children by the entry distance of the tile's centre
-            // ray (TILE_CENTRE_LANE), misses last
+            // ray (lane CL), misses last
             unsigned key[4];
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-                const unsigned kc = __shfl_sync(FULL, __float_as_uint(tn[k]), TILE_CENTRE_LANE);
+                const unsigned kc = __shfl_sync(FULL, __float_as_uint(tn[k]), CL);
                 key[k] = (cm >> k) & 1u ? kc : KEY_MISS;
             }
             sort4(key, ref);
@@ -728,13 +737,13 @@ __device__ __forceinline__ void iv_recip(float lo, float hi, float& i0, float& i
 // Packet box-test state from every lane's ray (o shared by all lanes, d its
 // own, delta its error bound); lanes with (lane & CENTRE_BIT) take the centre
 // ray (BVH4: lanes 4-7, BVH8: lanes 8-15).
-template <int CENTRE_BIT = 4>
+template <int CL, int CENTRE_BIT = 4>
 __device__ __forceinline__ PSlab make_pslab(f3 o, f3 d, float delta) {
     const unsigned FULL = 0xFFFFFFFFu;
     const bool centre = (threadIdx.x & CENTRE_BIT) != 0;
-    const float dcx = __shfl_sync(FULL, d.x, TILE_CENTRE_LANE);
-    const float dcy = __shfl_sync(FULL, d.y, TILE_CENTRE_LANE);
-    const float dcz = __shfl_sync(FULL, d.z, TILE_CENTRE_LANE);
+    const float dcx = __shfl_sync(FULL, d.x, CL);
+    const float dcy = __shfl_sync(FULL, d.y, CL);
+    const float dcz = __shfl_sync(FULL, d.z, CL);
     const float mnx = ord2f(__reduce_min_sync(FULL, f2ord(d.x))), mxx = ord2f(__reduce_max_sync(FULL, f2ord(d.x)));
     const float mny = ord2f(__reduce_min_sync(FULL, f2ord(d.y))), mxy = ord2f(__reduce_max_sync(FULL, f2ord(d.y)));
     const float mnz = ord2f(__reduce_min_sync(FULL, f2ord(d.z))), mxz = ord2f(__reduce_max_sync(FULL, f2ord(d.z)));
@@ -842,12 +851,13 @@ __device__ __forceinline__ void ps8_axis(float o, float dp, float lo, float hi, 
     neg |= n ? bit : 0;
 }
 
+template <int CL>
 __device__ __forceinline__ PSlab8 make_pslab8(f3 o, f3 d, float delta) {
     const unsigned FULL = 0xFFFFFFFFu;
     const bool centre = (threadIdx.x & 8) != 0;
-    const float dcx = __shfl_sync(FULL, d.x, TILE_CENTRE_LANE);
-    const float dcy = __shfl_sync(FULL, d.y, TILE_CENTRE_LANE);
-    const float dcz = __shfl_sync(FULL, d.z, TILE_CENTRE_LANE);
+    const float dcx = __shfl_sync(FULL, d.x, CL);
+    const float dcy = __shfl_sync(FULL, d.y, CL);
+    const float dcz = __shfl_sync(FULL, d.z, CL);
     const float mnx = ord2f(__reduce_min_sync(FULL, f2ord(d.x))), mxx = ord2f(__reduce_max_sync(FULL, f2ord(d.x)));
     const float mny = ord2f(__reduce_min_sync(FULL, f2ord(d.y))), mxy = ord2f(__reduce_max_sync(FULL, f2ord(d.y)));
     const float mnz = ord2f(__reduce_min_sync(FULL, f2ord(d.z))), mxz = ord2f(__reduce_max_sync(FULL, f2ord(d.z)));
@@ -899,7 +909,7 @@ __device__ __forceinline__ void ps8_axis_any(float lo, float hi, bool neg, float
 // Closest-hit traversal of a tile whose rays share their origin.  ps_env /
 // ps_obj: this warp's shared-memory copies of the two roles' box-test state
 // at the env / current object level ([2][PS_N] each).
-template <bool COUNT, class LEAF>
+template <int CL, bool COUNT, class LEAF>
 __device__ __forceinline__ void traverse_ipacket(const SceneView& sv, int env, RayState& rs,
                                                  const LEAF& leaf_fn, int* wstack, float* ps_env,
                                                  float* ps_obj, Counters& cnt) {
@@ -908,7 +918,7 @@ __device__ __forceinline__ void traverse_ipacket(const SceneView& sv, int env, R
     const bool leader = lane == 0;
     const int child = lane & 3;
     const int role = (lane >> 2) & 1;
-    PSlab ps = make_pslab(rs.o(), rs.d(), K_ERR * rs.c.f(C_Q));
+    PSlab ps = make_pslab<CL>(rs.o(), rs.d(), K_ERR * rs.c.f(C_Q));
     if (child == 0 && lane < 8) pslab_store(ps_env + role * PS_N, ps);
     __syncwarp();
     float Umax = __int_as_float(__reduce_max_sync(FULL, __float_as_int(rs.U)));
@@ -981,7 +991,7 @@ __device__ __forceinline__ void traverse_ipacket(const SceneView& sv, int env, R
             f3 oo, od;
             float delta;
             node = rs.enter_object(sv, leaf, oo, od, delta);
-            ps = make_pslab(oo, od, delta);
+            ps = make_pslab<CL>(oo, od, delta);
             __syncwarp();
             if (child == 0 && lane < 8) pslab_store(ps_obj + role * PS_N, ps);
             __syncwarp();
@@ -1009,7 +1019,7 @@ __device__ __forceinline__ void traverse_ipacket(const SceneView& sv, int env, R
 // node visits per tile.  The hit children are ranked by the centre ray's
 // entry distance (each lane counts the nearer keys of the 8, ties by child
 // index) and pushed farthest first by their own lanes in one store.
-template <bool COUNT, class LEAF>
+template <int CL, bool COUNT, class LEAF>
 __device__ __forceinline__ void traverse_ipacket8(const SceneView& sv, int env, RayState& rs,
                                                   const LEAF& leaf_fn, int* wstack, float* ps_env,
                                                   float* ps_obj, Counters& cnt) {
@@ -1019,10 +1029,10 @@ __device__ __forceinline__ void traverse_ipacket8(const SceneView& sv, int env, 
     const int role = (lane >> 3) & 1;
     const bool slot_lane = lane < 8;  // lanes owning child slots for ordering / pushes
 #if AGR_SLAB_FMA
-    PSlab8 ps = make_pslab8(rs.o(), rs.d(), K_ERR * rs.c.f(C_Q));
+    PSlab8 ps = make_pslab8<CL>(rs.o(), rs.d(), K_ERR * rs.c.f(C_Q));
     if (child == 0 && lane < 16) ps8_store(ps_env + role * PS8_N, ps);
 #else
-    PSlab ps = make_pslab<8>(rs.o(), rs.d(), K_ERR * rs.c.f(C_Q));
+    PSlab ps = make_pslab<CL, 8>(rs.o(), rs.d(), K_ERR * rs.c.f(C_Q));
     ps.strad = __any_sync(FULL, ps.strad && role == 0) ? 1 : 0;
     if (child == 0 && lane < 16) pslab_store(ps_env + role * PS_N, ps);
 #endif
@@ -1153,11 +1163,11 @@ __device__ __forceinline__ void traverse_ipacket8(const SceneView& sv, int env, 
             float delta;
             node = rs.enter_object(sv, leaf, oo, od, delta);
 #if AGR_SLAB_FMA
-            ps = make_pslab8(oo, od, delta);
+            ps = make_pslab8<CL>(oo, od, delta);
             __syncwarp();
             if (child == 0 && lane < 16) ps8_store(ps_obj + role * PS8_N, ps);
 #else
-            ps = make_pslab<8>(oo, od, delta);
+            ps = make_pslab<CL, 8>(oo, od, delta);
             ps.strad = __any_sync(FULL, ps.strad && role == 0) ? 1 : 0;
             __syncwarp();
             if (child == 0 && lane < 16) pslab_store(ps_obj + role * PS_N, ps);
@@ -1483,6 +1493,7 @@ __device__ __forceinline__ RayId ray_id(const CastArgs& a) {
     }
     // 32-bit index math: a launch covers < 2^32 warps (grid.x < 2^31 blocks
     // of CAST_THREADS / 32 = 2 warps) and tiles_img < 2^31 (cast_launch)
+    constexpr int TILE_W = Tile<MODEL>::W, TILE_H = Tile<MODEL>::H;
     const unsigned tiles_x = (unsigned)(a.W + TILE_W - 1) / TILE_W;
     const unsigned tiles_img = tiles_x * (unsigned)((a.H + TILE_H - 1) / TILE_H);
     const unsigned warp = blockIdx.x * (unsigned)(CAST_THREADS / 32) + (threadIdx.x >> 5);
@@ -1542,13 +1553,13 @@ __global__ void __launch_bounds__(CAST_THREADS, CAST_MIN_BLOCKS) k_cast(const __
                 // whole warps share (env, sensor): pinhole / beams tiles
 #if AGR_IPACKET
                 if (a.wide)
-                    traverse_ipacket8<COUNT>(a.sv, id.env, rs, leaf_fn, s_stack[threadIdx.x >> 5],
+                    traverse_ipacket8<Tile<MODEL>::CL, COUNT>(a.sv, id.env, rs, leaf_fn, s_stack[threadIdx.x >> 5],
                                              s_pslab[threadIdx.x >> 5][0], s_pslab[threadIdx.x >> 5][1], cnt);
                 else
-                    traverse_ipacket<COUNT>(a.sv, id.env, rs, leaf_fn, s_stack[threadIdx.x >> 5],
+                    traverse_ipacket<Tile<MODEL>::CL, COUNT>(a.sv, id.env, rs, leaf_fn, s_stack[threadIdx.x >> 5],
                                             s_pslab[threadIdx.x >> 5][0], s_pslab[threadIdx.x >> 5][1], cnt);
 #else
-                traverse_packet<false, COUNT>(a.sv, id.env, rs, leaf_fn, s_stack[threadIdx.x >> 5], cnt);
+                traverse_packet<Tile<MODEL>::CL, false, COUNT>(a.sv, id.env, rs, leaf_fn, s_stack[threadIdx.x >> 5], cnt);
 #endif
             } else {
                 traverse_lane<false, COUNT>(a.sv, id.env, rs, leaf_fn, cnt);
@@ -1595,7 +1606,7 @@ __global__ void __launch_bounds__(CAST_THREADS, CAST_MIN_BLOCKS) k_cast(const __
         const Best64 prim = best;
         auto sres = [ap, prim](int inst, int leaf) { return shadow_test64<MODEL>(ap, prim.t, inst, leaf); };
         auto leaf_fn = [&](int leaf) { ss.leaf_anyhit<COUNT>(a.sv, leaf, sres, cnt); };
-        if (TRAV == 1) traverse_packet<true, COUNT>(a.sv, id.env, ss, leaf_fn, s_stack[threadIdx.x >> 5], cnt);
+        if (TRAV == 1) traverse_packet<Tile<MODEL>::CL, true, COUNT>(a.sv, id.env, ss, leaf_fn, s_stack[threadIdx.x >> 5], cnt);
         else traverse_lane<true, COUNT>(a.sv, id.env, ss, leaf_fn, cnt);
         valid = !tested || ss.U >= 0.0f;
         if (cold.i(C_OVF) && tested) valid = !shadow_brute64<MODEL>(&a, id.env, best.t);
@@ -1625,6 +1636,7 @@ __global__ void __launch_bounds__(CAST_THREADS, CAST_MIN_BLOCKS) k_cast(const __
 
 template <int MODEL>
 cudaError_t launch_model(CastArgs a, cudaStream_t stream) {
+    constexpr int TILE_W = Tile<MODEL>::W, TILE_H = Tile<MODEL>::H;
     int64_t blocks;
     int n_envs = a.env_end - a.env_begin;
     if (n_envs <= 0) return cudaSuccess;
