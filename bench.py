@@ -109,6 +109,9 @@ def parse(argv=None):
                          "(default: lane for c6, whose terrain seen at grazing angles makes a "
                          "4x8 packet test ~9x the triangles its rays need; auto elsewhere); "
                          "packet4: the interval packets on the 4-wide nodes (A/B)")
+    ap.add_argument("--node-width", type=int, default=None, choices=[0, 4, 8, 16],
+                    help="agr_create_options.node_width: the interval packets' wide BVH copy (0: the "
+                         "library default; 4: none)")
     ap.add_argument("--no-parts", action="store_true",
                     help="one BLAS per asset (agr_create_options.part_policy 1) instead of splitting "
                          "multi-component assets (trees: trunk + canopy) into parts")
@@ -453,7 +456,8 @@ class Workload:
         # 8-wide collapse
         self.scene = agr.Scene.from_scenegen(sc, device=dev.index, trbvh_rounds=self.trbvh_rounds,
                                              parts=not args.no_parts,
-                                             node_width=4 if self.traversal == "lane" else 0)
+                                             node_width=(args.node_width if args.node_width is not None
+                                                         else 4 if self.traversal == "lane" else 0))
         self.mode = {"auto": 0, "lane": 1, "packet4": 2}[self.traversal]
         self.scene.set_traversal(self.mode)
         self.tlas_builder = args.tlas_builder or ("lbvh" if cfg in (5, 6) else "sah")

@@ -199,13 +199,15 @@ typedef struct {
                              Results are identical either way (the BVH only
                              accelerates the plain definition).
                              1: one BLAS per asset.                          */
-    int32_t node_width;   /* 0 (default) or 8: besides the 4-wide BVH every
-                             traversal uses, keep an 8-wide copy of every BLAS
-                             and TLAS (256-B nodes) for the interval-packet
-                             camera / LiDAR traversal (about half the node
-                             visits); 4: BVH4 only (half the node memory and
-                             no BVH8 collapse in builds / refits -- for
-                             scenes cast one ray per lane).                  */
+    int32_t node_width;   /* width of the wide BVH copy kept beside the 4-wide
+                             BVH every traversal uses, for the interval-packet
+                             camera / LiDAR traversal: 8 (256-B nodes) or 16
+                             (512-B nodes: lanes 0-15 test the children, 16-31
+                             order them); 0 (default): 16 if some env has more
+                             than 64 TLAS items (a deep TLAS: c3 +4 %), else 8;
+                             4: no wide copy (half the node memory and no wide
+                             collapse in builds / refits -- for scenes cast one
+                             ray per lane).                                  */
     int32_t reserved[5];  /* must be 0                                        */
 } agr_create_options;
 

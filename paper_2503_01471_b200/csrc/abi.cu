@@ -82,7 +82,8 @@ struct agr_scene_s {
     size_t device_bytes = 0;
     // device arrays
     float4* nodes = nullptr;   // BVH4 (BLAS then TLAS), 8 float4 per node
-    float4* nodes8 = nullptr;  // BVH8 copy (BLAS compacted, roots / TLAS at the BVH4's indices), 16 float4 per node, or null
+    float4* nodesw = nullptr;  // BVH8 / BVH16 copy (BLAS compacted, roots / TLAS at the BVH4's indices), or null
+    int wide_w = 0;            // its width (2 wide_w float4 per node)
     float4* bnodes = nullptr;  // binary BLAS nodes, 4 float4 per node (debug export)
     float4* tris = nullptr;
     float* triv = nullptr;
@@ -101,6 +102,8 @@ struct agr_scene_s {
     int* tlas_child = nullptr;
     int* tlas_item_parent = nullptr;
     int* tlas_node_parent = nullptr;
+    int* tlas_refs4 = nullptr;  // collapses chosen by the last agr_build, kept by agr_refit
+    int* tlas_refsw = nullptr;
     int* tlas_depth = nullptr;
     BlasInfo* parts = nullptr;      // [n_parts]
     int* part_off = nullptr;        // [n_assets + 1]
@@ -163,7 +166,8 @@ struct agr_scene_s {
     SceneView view() const {
         SceneView v;
         v.nodes = nodes;
-        v.nodes8 = nodes8;
+        v.nodesw = nodesw;
+        v.wide_w = wide_w;
         v.tris = tris;
         v.triv = triv;
         v.irec = irec;
@@ -187,7 +191,8 @@ struct agr_scene_s {
     TlasArgs tlas_args() const {
         TlasArgs a;
         a.nodes = nodes;
-        a.nodes8 = nodes8;
+        a.nodesw = nodesw;
+        a.wide_w = wide_w;
         a.irec = irec;
         a.item_box = item_box;
         a.inst_T = inst_T;
@@ -200,6 +205,8 @@ struct agr_scene_s {
         a.tlas_child = tlas_child;
         a.tlas_item_parent = tlas_item_parent;
         a.tlas_node_parent = tlas_node_parent;
+        a.tlas_refs4 = tlas_refs4;
+        a.tlas_refsw = tlas_refsw;
         a.tlas_depth = tlas_depth;
         a.n_envs = n_envs;
         a.max_n = max_n;
@@ -255,7 +262,8 @@ static cudaError_t build_assets(agr_scene_s* s, const int* assets, int n, cudaSt
     }
     BlasBatchArgs ba;
     ba.nodes = s->nodes;
-    ba.nodes8 = s->nodes8;
+    ba.nodesw = s->nodesw;
+    ba.wide_w = s->wide_w;
     ba.bnodes = binary ? s->bnodes : nullptr;
     ba.tris = s->tris;
     ba.triv = s->triv;
@@ -449,8 +457,8 @@ agr_status agr_scene_create_ex(int32_t device, const agr_mesh* meshes, int32_t n
         return fail(AGR_EINVAL, "trbvh_rounds must be in [0, 16]");
     if (opts && (opts->part_policy < 0 || opts->part_policy > 1))
         return fail(AGR_EINVAL, "part_policy must be 0 (auto) or 1 (one BLAS per asset)");
-    if (opts && opts->node_width != 0 && opts->node_width != 4 && opts->node_width != 8)
-        return fail(AGR_EINVAL, "node_width must be 0 (default), 4 or 8");
+    if (opts && opts->node_width != 0 && opts->node_width != 4 && opts->node_width != 8 && opts->node_width != 16)
+        return fail(AGR_EINVAL, "node_width must be 0 (default), 4, 8 or 16");
     agr_scene_s* s = new agr_scene_s();
     s->device = device;
     if (opts) s->trbvh_rounds = opts->trbvh_rounds;
@@ -546,6 +554,9 @@ agr_status agr_scene_create_ex(int32_t device, const agr_mesh* meshes, int32_t n
         delete s;
         return st;
     };
+#ifndef AGR_WIDE16_ITEMS
+#define AGR_WIDE16_ITEMS 64  // node_width 0: BVH16 above this many TLAS items in some env, else BVH8
+#endif
 #define CKB(call)                                                    \
     do {                                                             \
         cudaError_t _e = (call);                                     \
@@ -553,7 +564,12 @@ agr_status agr_scene_create_ex(int32_t device, const agr_mesh* meshes, int32_t n
     } while (0)
 
     CKB(s->alloc(&s->nodes, 8 * (size_t)(nb + nt)));
-    if (!opts || opts->node_width != 4) CKB(s->alloc(&s->nodes8, (size_t)NODE8_F4 * (nb + nt)));
+    // node_width 0: BVH16 when some env has more than 64 TLAS items (the
+    // TLAS is then deep enough for the 16-wide nodes to pay: c3's 91 items
+    // +3.5 %), else BVH8 (c4 / c5 with 16-20 items: BVH16 -1 %)
+    s->wide_w = !opts || opts->node_width == 0 ? (s->max_n > AGR_WIDE16_ITEMS ? 16 : 8)
+                : opts->node_width == 4 ? 0 : opts->node_width;
+    if (s->wide_w) CKB(s->alloc(&s->nodesw, (size_t)2 * s->wide_w * (nb + nt)));
     CKB(s->alloc(&s->bnodes, 4 * (size_t)nb));
     CKB(s->alloc(&s->tris, 3 * (size_t)nl));
     CKB(s->alloc(&s->triv, 12 * (size_t)nl));  // 3 x float4 (v.xyz, 0) per leaf
@@ -572,6 +588,8 @@ agr_status agr_scene_create_ex(int32_t device, const agr_mesh* meshes, int32_t n
     CKB(s->alloc(&s->tlas_child, 2 * (size_t)nt));
     CKB(s->alloc(&s->tlas_item_parent, (size_t)n_items));
     CKB(s->alloc(&s->tlas_node_parent, (size_t)nt));
+    CKB(s->alloc(&s->tlas_refs4, 4 * (size_t)nt));
+    if (s->wide_w) CKB(s->alloc(&s->tlas_refsw, (size_t)s->wide_w * nt));
     CKB(s->alloc(&s->tlas_depth, (size_t)n_envs));
     CKB(s->alloc(&s->parts, (size_t)n_parts));
     CKB(s->alloc(&s->part_off, (size_t)n_meshes + 1));
@@ -842,7 +860,7 @@ static void set_schedule(const agr_scene_s* s, CastArgs& a) {
         (4.0f / a.fx > PACKET_MAX_TILE_RAD || 8.0f / a.fy > PACKET_MAX_TILE_RAD))
         packet = false;
     a.packet = packet ? 1 : 0;
-    a.wide = packet && (s->traversal == 0 || s->traversal == 3) && s->nodes8 ? 1 : 0;
+    a.wide = packet && (s->traversal == 0 || s->traversal == 3) && s->nodesw ? 1 : 0;
 }
 
 static agr_status run_cast(agr_scene s, CastArgs& a, cudaStream_t st) {

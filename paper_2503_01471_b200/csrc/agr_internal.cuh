@@ -81,7 +81,8 @@ struct BlasInfo {
 // Read-only view of a scene passed by value to kernels.
 struct SceneView {
     const float4* nodes;      // [n_nodes][8] BVH4
-    const float4* nodes8;     // [n_nodes][16] BVH8 copy (its own numbering; BLAS roots and TLAS nodes at the
+    int wide_w;               // width of the wide copy: 8 or 16 (0: none)
+    const float4* nodesw;     // [n_nodes][2 wide_w] BVH8 / BVH16 copy (its own numbering; BLAS roots and TLAS nodes at the
                               // same indices as the BVH4), or null
     const float4* tris;       // [n_leaves][3]
     const float* triv;        // [n_leaves][3] float4 (v.xyz, 0)
@@ -210,14 +211,18 @@ __device__ __forceinline__ int collapse4(int j, const CHILD& child, const BOX& b
     return collapse_w<4>(j, child, box, refs, keep_pairs);
 }
 
-// BVH8 node (interval-packet traversal), 256 B: child k's record is the 32 B
-// at k: (lo.x, lo.y, lo.z, hi.x), (hi.y, hi.z, ref, -), so lane k of a warp
-// fetches its child with two 128-bit loads and lanes 0-7 read one 256-B line.
+// Wide node of the interval-packet traversal (W = 8: 256 B, W = 16: 512 B):
+// child k's record is the 32 B at k: (lo.x, lo.y, lo.z, hi.x), (hi.y, hi.z,
+// ref, -), so lane k of a warp fetches its child with two 128-bit loads and
+// lanes 0..W-1 read the node's W x 32 B.
 constexpr int NODE8_F4 = 16;  // float4 per BVH8 node
-__device__ __forceinline__ void write_child8(float4* nodes8, int g, int k, const float b[6], int ref) {
-    float4* p = nodes8 + NODE8_F4 * (size_t)g + 2 * k;
+__device__ __forceinline__ void write_childw(float4* nodesw, int W, int g, int k, const float b[6], int ref) {
+    float4* p = nodesw + 2 * (size_t)W * g + 2 * k;
     p[0] = make_float4(b[0], b[1], b[2], b[3]);
     p[1] = make_float4(b[4], b[5], __int_as_float(ref), 0.0f);
+}
+__device__ __forceinline__ void write_child8(float4* nodesw, int g, int k, const float b[6], int ref) {
+    write_childw(nodesw, 8, g, k, b, ref);
 }
 
 // Writes BVH4 node g: boxes b[k][6] (lo xyz, hi xyz) and global refs.
@@ -252,7 +257,8 @@ struct BlasSeg {
 };
 struct BlasBatchArgs {
     float4* nodes;         // global BVH4 node array
-    float4* nodes8;        // global BVH8 node array (compacted like the BVH4; root at node_base), or null
+    float4* nodesw;        // global wide node array (compacted like the BVH4; root at node_base), or null
+    int wide_w;            // its width: 8 or 16
     float4* bnodes;        // global binary BLAS node array (debug export)
     float4* tris;          // global tri record array
     float* triv;           // global exact-vertex array
@@ -275,7 +281,8 @@ cudaError_t blas_build_batch(BlasSeg* h_segs, int n_segs, const BlasBatchArgs& a
 
 struct TlasArgs {
     float4* nodes;            // global node array (TLAS part written)
-    float4* nodes8;           // global BVH8 node array (TLAS part written), or null
+    float4* nodesw;           // global wide node array (TLAS part written), or null
+    int wide_w;               // its width: 8 or 16
     float4* irec;             // [n_items][4] written
     float* item_box;          // [n_items][6] written
     const float* inst_T;      // [n_inst][12]
@@ -290,6 +297,8 @@ struct TlasArgs {
     int* tlas_item_parent;    // [n_items] local parent (internal node) of each item leaf
     int* tlas_node_parent;    // [n_tlas_nodes] local parent of each internal node
     int* tlas_depth;          // [n_envs] depth of each env's TLAS (written by build)
+    int* tlas_refs4;          // [n_tlas_nodes][4] the BVH4 collapse of each node (binary refs), kept by refits
+    int* tlas_refsw;          // [n_tlas_nodes][wide_w] the wide collapse, kept by refits (or null)
     int n_envs;
     int max_n;                // max items in one env (sizes shared memory)
     int builder;              // 0: LBVH (Morton + Karras), 1: binned SAH (default)
@@ -327,7 +336,7 @@ struct CastArgs {
     unsigned long long* counters;  // optional [8]
     int exact;
     int packet;           // 1: warp-packet traversal for pinhole / beams tiles
-    int wide;             // 1: interval packets over the BVH8 copy (sv.nodes8)
+    int wide;             // 1: interval packets over the BVH8 copy (sv.nodesw)
     // filled by cast_launch: n / d = (n * m) >> s for n < 2^31 (tile decode
     // of tiles_img, tiles_x, S without integer division)
     unsigned div_m[3];

@@ -129,7 +129,7 @@ struct Scratch {
     int* seg8;           // [B] the same for the BVH8 copy
     int2* queue;         // [Ftot] (binary node, BVH4 slot) of every reachable node, level by level
     float4* rec;         // [Ftot][4] per internal node: both children's boxes, refs and pair-leaf codes
-    float* dp8;          // [Ftot][8] SAH cost of the node's subtree as <= i BVH8 child slots (SAH-optimal collapse)
+    float* dp8;          // [Ftot][W] SAH cost of the node's subtree as <= i wide child slots (SAH-optimal collapse)
     int* qctl;           // [2 + MAX_LEVELS]: [0] items in the queue, [2 + L] items of BVH4 level L
 };
 
@@ -170,7 +170,7 @@ size_t scratch_layout(int64_t F, int B, void* base, Scratch* out) {
     s.seg8 = (int*)take(sizeof(int) * B);
     s.queue = (int2*)take(sizeof(int2) * F);
     s.rec = (float4*)take(AGR_CHILD_REC ? sizeof(float4) * 4 * F : 16);
-    s.dp8 = (float*)take(sizeof(float) * 8 * F);
+    s.dp8 = (float*)take(sizeof(float) * 16 * F);  // W <= 16
     s.qctl = (int*)take(sizeof(int) * (2 + MAX_LEVELS));
     if (out) *out = s;
     return used + 256;
@@ -928,7 +928,8 @@ __global__ void k_depth(const BlasSeg* segs, const int* seg_of, const uint32_t* 
 #endif
 constexpr float DP_CN = 1.0f, DP_CT = AGR_DP_CT;
 
-__global__ void k_dp8(const BlasSeg* segs, const int* seg_of, const uint32_t* bounds, int Ftot,
+template <int W>
+__global__ void k_dpw(const BlasSeg* segs, const int* seg_of, const uint32_t* bounds, int Ftot,
                       const float* __restrict__ tri_box, const int* child_all, const int* leaf_parent_all,
                       const int* node_parent_all, const float* ibox_all, int* flags_all, float* dp_all) {
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
@@ -941,11 +942,11 @@ __global__ void k_dp8(const BlasSeg* segs, const int* seg_of, const uint32_t* bo
     const float* lbox = tri_box + BX * (size_t)c.off;
     const float* ibox = ibox_all + BX * (size_t)c.off;
     int* flags = flags_all + c.off;
-    float* dp = dp_all + 8 * (size_t)c.off;
+    float* dp = dp_all + W * (size_t)c.off;
     int node = __ldcg(leaf_parent_all + c.off + p);
     while (node >= 0) {
         if (arrive(&flags[node]) == 0) return;
-        float cl[2][8];
+        float cl[2][W];
         int r[2];
         for (int side = 0; side < 2; ++side) {
             r[side] = __ldcg(child + 2 * node + side);
@@ -954,33 +955,35 @@ __global__ void k_dp8(const BlasSeg* segs, const int* seg_of, const uint32_t* bo
                 load_box_cg(lbox + BX * (size_t)(~r[side]), b);
                 const float v = DP_CT * half_area(b);
 #pragma unroll
-                for (int i = 0; i < 8; ++i) cl[side][i] = v;
+                for (int i = 0; i < W; ++i) cl[side][i] = v;
             } else {
-                const float4 u = __ldcg(reinterpret_cast<const float4*>(dp + 8 * (size_t)r[side]));
-                const float4 w = __ldcg(reinterpret_cast<const float4*>(dp + 8 * (size_t)r[side]) + 1);
-                cl[side][0] = u.x; cl[side][1] = u.y; cl[side][2] = u.z; cl[side][3] = u.w;
-                cl[side][4] = w.x; cl[side][5] = w.y; cl[side][6] = w.z; cl[side][7] = w.w;
+#pragma unroll
+                for (int q = 0; q < W / 4; ++q) {
+                    const float4 u = __ldcg(reinterpret_cast<const float4*>(dp + W * (size_t)r[side]) + q);
+                    cl[side][4 * q] = u.x; cl[side][4 * q + 1] = u.y; cl[side][4 * q + 2] = u.z;
+                    cl[side][4 * q + 3] = u.w;
+                }
             }
         }
         float nb[6];
         load_box_cg(ibox + BX * node, nb);
         const float an = half_area(nb);
-        float cd[9];
+        float cd[W + 1];
 #pragma unroll
-        for (int j = 2; j <= 8; ++j) {
+        for (int j = 2; j <= W; ++j) {
             float m = INFINITY;
 #pragma unroll
             for (int k = 1; k < j; ++k) m = fminf(m, cl[0][k - 1] + cl[1][j - k - 1]);
             cd[j] = m;
         }
-        float C[8];
-        C[0] = DP_CN * an + cd[8];
+        float C[W];
+        C[0] = DP_CN * an + cd[W];
         if (LEAF_MAX == 2 && r[0] < 0 && r[1] < 0 && abs(~r[0] - ~r[1]) == 1) C[0] = fminf(C[0], 2.0f * DP_CT * an);
 #pragma unroll
-        for (int i = 1; i < 8; ++i) C[i] = fminf(C[i - 1], cd[i + 1]);
-        float4* o = reinterpret_cast<float4*>(dp + 8 * (size_t)node);
-        __stcg(o, make_float4(C[0], C[1], C[2], C[3]));
-        __stcg(o + 1, make_float4(C[4], C[5], C[6], C[7]));
+        for (int i = 1; i < W; ++i) C[i] = fminf(C[i - 1], cd[i + 1]);
+        float4* o = reinterpret_cast<float4*>(dp + W * (size_t)node);
+#pragma unroll
+        for (int q = 0; q < W / 4; ++q) __stcg(o + q, make_float4(C[4 * q], C[4 * q + 1], C[4 * q + 2], C[4 * q + 3]));
         node = __ldcg(node_parent + node);
     }
 }
@@ -1204,7 +1207,7 @@ __global__ void __launch_bounds__(T_BLK) k_bvhw_topdown(const BlasSeg* segs, con
                     // SAH-optimal children from the k_dp8 tables: distribute
                     // the node's 8 slots between its two children and
                     // recursively below them (explicit stack of <= 7 splits)
-                    const float* dp = dp_all + 8 * (size_t)off;
+                    const float* dp = dp_all + W * (size_t)off;
                     int st_n[W], st_j[W], sp = 0;
                     st_n[sp] = x - off; st_j[sp] = W; ++sp;
                     cnt = 0;
@@ -1214,13 +1217,13 @@ __global__ void __launch_bounds__(T_BLK) k_bvhw_topdown(const BlasSeg* segs, con
                         float bc[2][6];
                         int rc[2], xc[2];
                         get_rec(nn, bc[0], bc[1], rc[0], rc[1], xc[0], xc[1]);
-                        float tab[2][8];
+                        float tab[2][W];
                         for (int side = 0; side < 2; ++side) {
                             if (rc[side] < 0) {
                                 const float v = DP_CT * half_area(bc[side]);
-                                for (int i = 0; i < 8; ++i) tab[side][i] = v;
+                                for (int i = 0; i < W; ++i) tab[side][i] = v;
                             } else {
-                                for (int i = 0; i < 8; ++i) tab[side][i] = __ldcg(dp + 8 * (size_t)rc[side] + i);
+                                for (int i = 0; i < W; ++i) tab[side][i] = __ldcg(dp + W * (size_t)rc[side] + i);
                             }
                         }
                         int kb = 1;
@@ -1344,7 +1347,7 @@ __global__ void __launch_bounds__(T_BLK) k_bvhw_topdown(const BlasSeg* segs, con
                     p[7] = make_float4(__int_as_float(cnt), 0.0f, 0.0f, 0.0f);
                 } else {
 #pragma unroll
-                    for (int k = 0; k < W; ++k) write_child8(nodes, g, k, bx[k], gr[k]);
+                    for (int k = 0; k < W; ++k) write_childw(nodes, W, g, k, bx[k], gr[k]);
                 }
             }
             // warp-aggregated append of the next level
@@ -1394,18 +1397,18 @@ __global__ void k_write4_small(const BlasSeg* segs, int B, const uint32_t* bound
 // record, the exact vertices (3 x float4) and the leaf's box for the
 // hierarchy passes (so they read leaf boxes by position, coalesced, instead
 // of gathering them by face id).
-__global__ void k_write8_small(const BlasSeg* segs, int B, const uint32_t* bounds, const float* tri_box,
-                               float4* nodes8) {
+__global__ void k_writew_small(const BlasSeg* segs, int B, const uint32_t* bounds, const float* tri_box,
+                               float4* nodesw, int W) {
     const int sgi = blockIdx.x * blockDim.x + threadIdx.x;
     if (sgi >= B) return;
     const int n = (int)bounds[8 * sgi + 7];
     if (n >= 2) return;
     const BlasSeg& S = segs[sgi];
-    for (int k = 0; k < 8; ++k) {
+    for (int k = 0; k < W; ++k) {
         const int r = (k == 0 && n == 1) ? ~0 : REF_EMPTY;
         float b[6];
         child_box(r, tri_box + BX * (size_t)S.off, nullptr, b);
-        write_child8(nodes8, S.node_base, k, b, global_ref(r, S.node_base, S.leaf_base));
+        write_childw(nodesw, W, S.node_base, k, b, global_ref(r, S.node_base, S.leaf_base));
     }
 }
 
@@ -1614,18 +1617,25 @@ cudaError_t blas_build_batch(BlasSeg* h_segs, int B, const BlasBatchArgs& a, voi
     e = topdown((const void*)k_bvhw_topdown<4, false>, s.seg4, a.nodes, nullptr);
     if (e != cudaSuccess) return e;
     k_write4_small<<<(B + 127) / 128, 128, 0, stream>>>(s.segs, B, s.bounds, sv, s.tri_box, a.nodes);
-    if (a.nodes8) {
+    if (a.nodesw) {
+        const bool w16 = a.wide_w == 16;
         if (a.opt_collapse) {
-            // SAH-optimal BVH8 (the interval packets' tree): cost tables bottom-up
+            // SAH-optimal wide collapse (the interval packets' tree): cost tables bottom-up
             cudaMemsetAsync(s.flags, 0, sizeof(int) * F, stream);
-            k_dp8<<<gb, T_BLK, 0, stream>>>(s.segs, s.seg_of, s.bounds, F, s.tri_box, s.child, s.leaf_parent,
-                                            s.node_parent, s.ibox, s.flags, s.dp8);
-            e = topdown((const void*)k_bvhw_topdown<8, true>, s.seg8, a.nodes8, s.dp8);
+            if (w16)
+                k_dpw<16><<<gb, T_BLK, 0, stream>>>(s.segs, s.seg_of, s.bounds, F, s.tri_box, s.child, s.leaf_parent,
+                                                   s.node_parent, s.ibox, s.flags, s.dp8);
+            else
+                k_dpw<8><<<gb, T_BLK, 0, stream>>>(s.segs, s.seg_of, s.bounds, F, s.tri_box, s.child, s.leaf_parent,
+                                                  s.node_parent, s.ibox, s.flags, s.dp8);
+            e = topdown(w16 ? (const void*)k_bvhw_topdown<16, true> : (const void*)k_bvhw_topdown<8, true>, s.seg8,
+                        a.nodesw, s.dp8);
         } else {
-            e = topdown((const void*)k_bvhw_topdown<8, false>, s.seg8, a.nodes8, nullptr);
+            e = topdown(w16 ? (const void*)k_bvhw_topdown<16, false> : (const void*)k_bvhw_topdown<8, false>,
+                        s.seg8, a.nodesw, nullptr);
         }
         if (e != cudaSuccess) return e;
-        k_write8_small<<<(B + 127) / 128, 128, 0, stream>>>(s.segs, B, s.bounds, s.tri_box, a.nodes8);
+        k_writew_small<<<(B + 127) / 128, 128, 0, stream>>>(s.segs, B, s.bounds, s.tri_box, a.nodesw, a.wide_w);
     }
     k_asset_info<<<(B + 127) / 128, 128, 0, stream>>>(s.segs, B, s.bounds, s.ibox, s.tri_box, sv, s.depth,
                                                       s.seg4);

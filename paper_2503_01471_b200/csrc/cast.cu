@@ -851,10 +851,10 @@ __device__ __forceinline__ void ps8_axis(float o, float dp, float lo, float hi, 
     neg |= n ? bit : 0;
 }
 
-template <int CL>
+template <int CL, int CENTRE_BIT = 8>
 __device__ __forceinline__ PSlab8 make_pslab8(f3 o, f3 d, float delta) {
     const unsigned FULL = 0xFFFFFFFFu;
-    const bool centre = (threadIdx.x & 8) != 0;
+    const bool centre = (threadIdx.x & CENTRE_BIT) != 0;
     const float dcx = __shfl_sync(FULL, d.x, CL);
     const float dcy = __shfl_sync(FULL, d.y, CL);
     const float dcz = __shfl_sync(FULL, d.z, CL);
@@ -1011,7 +1011,7 @@ __device__ __forceinline__ void traverse_ipacket(const SceneView& sv, int env, R
     }
 }
 
-// Interval-packet traversal of the BVH8 copy (nodes8): lanes 0-7 test
+// Interval-packet traversal of the BVH8 copy (nodesw): lanes 0-7 test
 // child (lane & 7) against the tile's direction interval, lanes 8-15 the same
 // child with the centre ray (the visiting order); lanes 16-31 mirror 0-15.
 // Same conservative interval test as traverse_ipacket -- only the node width
@@ -1019,22 +1019,23 @@ __device__ __forceinline__ void traverse_ipacket(const SceneView& sv, int env, R
 // node visits per tile.  The hit children are ranked by the centre ray's
 // entry distance (each lane counts the nearer keys of the 8, ties by child
 // index) and pushed farthest first by their own lanes in one store.
-template <int CL, bool COUNT, class LEAF>
-__device__ __forceinline__ void traverse_ipacket8(const SceneView& sv, int env, RayState& rs,
+template <int CL, int WW, bool COUNT, class LEAF>
+__device__ __forceinline__ void traverse_ipacketw(const SceneView& sv, int env, RayState& rs,
                                                   const LEAF& leaf_fn, int* wstack, float* ps_env,
                                                   float* ps_obj, Counters& cnt) {
     const unsigned FULL = 0xFFFFFFFFu;
     const int lane = threadIdx.x & 31;
-    const int child = lane & 7;
-    const int role = (lane >> 3) & 1;
-    const bool slot_lane = lane < 8;  // lanes owning child slots for ordering / pushes
+    const int child = lane & (WW - 1);
+    const int role = (lane / WW) & 1;
+    const bool slot_lane = lane < WW;  // lanes owning child slots for ordering / pushes
+    constexpr unsigned SLOTS = WW == 32 ? 0xFFFFFFFFu : (1u << WW) - 1u;
 #if AGR_SLAB_FMA
-    PSlab8 ps = make_pslab8<CL>(rs.o(), rs.d(), K_ERR * rs.c.f(C_Q));
-    if (child == 0 && lane < 16) ps8_store(ps_env + role * PS8_N, ps);
+    PSlab8 ps = make_pslab8<CL, WW>(rs.o(), rs.d(), K_ERR * rs.c.f(C_Q));
+    if (child == 0 && lane < 2 * WW) ps8_store(ps_env + role * PS8_N, ps);
 #else
-    PSlab ps = make_pslab<CL, 8>(rs.o(), rs.d(), K_ERR * rs.c.f(C_Q));
+    PSlab ps = make_pslab<CL, WW>(rs.o(), rs.d(), K_ERR * rs.c.f(C_Q));
     ps.strad = __any_sync(FULL, ps.strad && role == 0) ? 1 : 0;
-    if (child == 0 && lane < 16) pslab_store(ps_env + role * PS_N, ps);
+    if (child == 0 && lane < 2 * WW) pslab_store(ps_env + role * PS_N, ps);
 #endif
     __syncwarp();
     float Umax = __int_as_float(__reduce_max_sync(FULL, __float_as_int(rs.U)));
@@ -1044,7 +1045,7 @@ __device__ __forceinline__ void traverse_ipacket8(const SceneView& sv, int env, 
         if (node >= 0) {
             if (COUNT) cnt.nodes++;
             if (COUNT && rs.cur_inst < 0) cnt.tnodes++;
-            const float4* cp = sv.nodes8 + NODE8_F4 * (size_t)node + 2 * child;
+            const float4* cp = sv.nodesw + 2 * WW * (size_t)node + 2 * child;
             const float4 ca = __ldg(cp), cb = __ldg(cp + 1);
             float nx, fx, ny, fy, nz, fz;
 #if AGR_SLAB_FMA
@@ -1072,7 +1073,7 @@ __device__ __forceinline__ void traverse_ipacket8(const SceneView& sv, int env, 
             const float tf = fminf(fminf(fx, fy), fminf(fz, Umax));
             const bool h = tn <= tf;
             const int ref = __float_as_int(cb.z);
-            const unsigned cm = __ballot_sync(FULL, h) & 0xFFu;
+            const unsigned cm = __ballot_sync(FULL, h) & SLOTS;
             const int nh = __popc(cm);
             if (nh == 0) {
                 if (sp == 0) break;
@@ -1087,18 +1088,18 @@ __device__ __forceinline__ void traverse_ipacket8(const SceneView& sv, int env, 
 #if AGR_RANK_MODE == 0
             // rank of this lane's child among the hit children by the centre
             // ray's entry distance (lanes 8-15), misses last
-            const unsigned kc = __shfl_sync(FULL, __float_as_uint(tn), child + 8);
+            const unsigned kc = __shfl_sync(FULL, __float_as_uint(tn), child + WW);
             const bool hit = slot_lane && ((cm >> child) & 1u);
             const unsigned key = hit ? kc : KEY_MISS;
             int rank = 0;
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
+            for (int j = 0; j < WW; ++j) {
                 const unsigned kj = __shfl_sync(FULL, key, j);
                 rank += (kj < key || (kj == key && j < child)) ? 1 : 0;
             }
             const int first = __ffs(__ballot_sync(FULL, hit && rank == 0)) - 1;
             const int nearest = __shfl_sync(FULL, ref, first);
-            if (sp + 7 <= PSTACK) {
+            if (sp + WW - 1 <= PSTACK) {
                 __syncwarp();  // every lane has read the slots before they are reused
                 if (hit && rank > 0) wstack[sp + nh - 1 - rank] = ref;
                 sp += nh - 1;  // nh is warp-uniform
@@ -1111,17 +1112,17 @@ __device__ __forceinline__ void traverse_ipacket8(const SceneView& sv, int env, 
             // order keys: the centre ray's entry distance (lanes 8-15) with
             // the child index in the 3 low bits (distinct; near-equal
             // distances go by index), misses last; the nearest by one REDUX
-            const unsigned kc = __shfl_sync(FULL, __float_as_uint(tn), child + 8);
+            const unsigned kc = __shfl_sync(FULL, __float_as_uint(tn), child + WW);
             const bool hit = slot_lane && ((cm >> child) & 1u);
-            const unsigned key = hit ? ((kc & ~7u) | (unsigned)child) : 0xFFFFFFFFu;
-            const int near_child = (int)(__reduce_min_sync(FULL, key) & 7u);
+            const unsigned key = hit ? ((kc & ~(unsigned)(WW - 1)) | (unsigned)child) : 0xFFFFFFFFu;
+            const int near_child = (int)(__reduce_min_sync(FULL, key) & (unsigned)(WW - 1));
             const int nearest = __shfl_sync(FULL, ref, near_child);
-            if (sp + 7 <= PSTACK) {
+            if (sp + WW - 1 <= PSTACK) {
                 __syncwarp();  // every lane has read the slots before they are reused
                 if (AGR_RANK_MODE == 1 && nh > 2) {
                     int rank = 0;  // among the hits, farthest pushed first
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) rank += __shfl_sync(FULL, key, j) < key ? 1 : 0;
+                    for (int j = 0; j < WW; ++j) rank += __shfl_sync(FULL, key, j) < key ? 1 : 0;
                     if (hit && rank > 0) wstack[sp + nh - 1 - rank] = ref;
                 } else if (hit && child != near_child) {
                     // nh == 2 (exact), or mode 2: the other hits in child order
@@ -1163,14 +1164,14 @@ __device__ __forceinline__ void traverse_ipacket8(const SceneView& sv, int env, 
             float delta;
             node = rs.enter_object(sv, leaf, oo, od, delta);
 #if AGR_SLAB_FMA
-            ps = make_pslab8<CL>(oo, od, delta);
+            ps = make_pslab8<CL, WW>(oo, od, delta);
             __syncwarp();
-            if (child == 0 && lane < 16) ps8_store(ps_obj + role * PS8_N, ps);
+            if (child == 0 && lane < 2 * WW) ps8_store(ps_obj + role * PS8_N, ps);
 #else
-            ps = make_pslab<CL, 8>(oo, od, delta);
+            ps = make_pslab<CL, WW>(oo, od, delta);
             ps.strad = __any_sync(FULL, ps.strad && role == 0) ? 1 : 0;
             __syncwarp();
-            if (child == 0 && lane < 16) pslab_store(ps_obj + role * PS_N, ps);
+            if (child == 0 && lane < 2 * WW) pslab_store(ps_obj + role * PS_N, ps);
 #endif
             __syncwarp();
             continue;
@@ -1512,7 +1513,7 @@ __device__ __forceinline__ RayId ray_id(const CastArgs& a) {
 }
 
 // TRAV: 0 per-lane FP32 filter, 1 warp packet (pinhole / beams), 2 exact (FP64 leaves)
-template <int MODEL, int TRAV, bool COUNT, bool STEREO>
+template <int MODEL, int TRAV, bool COUNT, bool STEREO, int WIDE>
 __global__ void __launch_bounds__(CAST_THREADS, CAST_MIN_BLOCKS) k_cast(const __grid_constant__ CastArgs a) {
     __shared__ int s_stack[TRAV == 1 ? CAST_THREADS / 32 : 1][TRAV == 1 ? PSTACK : 1];
     __shared__ float s_pslab[TRAV == 1 ? CAST_THREADS / 32 : 1][2][2 * PS_MAXN];  // [warp][env, obj][role][..]
@@ -1552,9 +1553,10 @@ __global__ void __launch_bounds__(CAST_THREADS, CAST_MIN_BLOCKS) k_cast(const __
             if (TRAV == 1) {
                 // whole warps share (env, sensor): pinhole / beams tiles
 #if AGR_IPACKET
-                if (a.wide)
-                    traverse_ipacket8<Tile<MODEL>::CL, COUNT>(a.sv, id.env, rs, leaf_fn, s_stack[threadIdx.x >> 5],
-                                             s_pslab[threadIdx.x >> 5][0], s_pslab[threadIdx.x >> 5][1], cnt);
+                if (WIDE)
+                    traverse_ipacketw<Tile<MODEL>::CL, WIDE ? WIDE : 8, COUNT>(
+                        a.sv, id.env, rs, leaf_fn, s_stack[threadIdx.x >> 5], s_pslab[threadIdx.x >> 5][0],
+                        s_pslab[threadIdx.x >> 5][1], cnt);
                 else
                     traverse_ipacket<Tile<MODEL>::CL, COUNT>(a.sv, id.env, rs, leaf_fn, s_stack[threadIdx.x >> 5],
                                             s_pslab[threadIdx.x >> 5][0], s_pslab[threadIdx.x >> 5][1], cnt);
@@ -1664,28 +1666,24 @@ cudaError_t launch_model(CastArgs a, cudaStream_t stream) {
         }
     }
     const bool stereo = MODEL != 0 && a.out_valid != nullptr;
-#define AGR_LAUNCH(T, C, S) k_cast<MODEL, T, C, S><<<g, CAST_THREADS, 0, stream>>>(a)
+#define AGR_LAUNCH(T, C, S, W) k_cast<MODEL, T, C, S, W><<<g, CAST_THREADS, 0, stream>>>(a)
+#define AGR_LAUNCH_TRAV(C, S)                                   \
+    do {                                                        \
+        if (trav == 2) AGR_LAUNCH(2, C, S, 0);                  \
+        else if (trav == 0) AGR_LAUNCH(0, C, S, 0);             \
+        else if (wide == 16) AGR_LAUNCH(1, C, S, 16);           \
+        else if (wide == 8) AGR_LAUNCH(1, C, S, 8);             \
+        else AGR_LAUNCH(1, C, S, 0);                            \
+    } while (0)
+    const int wide = a.wide ? a.sv.wide_w : 0;
     if (a.counters) {
-        if (stereo) {
-            if (trav == 2) AGR_LAUNCH(2, true, true);
-            else if (trav == 1) AGR_LAUNCH(1, true, true);
-            else AGR_LAUNCH(0, true, true);
-        } else {
-            if (trav == 2) AGR_LAUNCH(2, true, false);
-            else if (trav == 1) AGR_LAUNCH(1, true, false);
-            else AGR_LAUNCH(0, true, false);
-        }
+        if (stereo) AGR_LAUNCH_TRAV(true, true);
+        else AGR_LAUNCH_TRAV(true, false);
     } else {
-        if (stereo) {
-            if (trav == 2) AGR_LAUNCH(2, false, true);
-            else if (trav == 1) AGR_LAUNCH(1, false, true);
-            else AGR_LAUNCH(0, false, true);
-        } else {
-            if (trav == 2) AGR_LAUNCH(2, false, false);
-            else if (trav == 1) AGR_LAUNCH(1, false, false);
-            else AGR_LAUNCH(0, false, false);
-        }
+        if (stereo) AGR_LAUNCH_TRAV(false, true);
+        else AGR_LAUNCH_TRAV(false, false);
     }
+#undef AGR_LAUNCH_TRAV
 #undef AGR_LAUNCH
     return cudaGetLastError();
 }

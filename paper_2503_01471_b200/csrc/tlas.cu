@@ -152,47 +152,48 @@ constexpr int TDP_MAX = 128;
 __device__ __forceinline__ float box_cost_area(const float* b) { return b[0] <= b[3] ? half_area(b) : 0.0f; }
 
 // New table of internal node j from its children's current tables.
-template <class CH, class LB, class NB, class TB>
+constexpr int TDP_STRIDE = 16;  // floats per table row (W <= 16)
+template <int W, class CH, class LB, class NB, class TB>
 __device__ __forceinline__ void tdp_node(int j, const CH& child, const LB& lbox, const NB& nbox, const TB& tab,
-                                         float C[8]) {
-    float cl[2][8];
+                                         float C[W]) {
+    float cl[2][W];
     for (int side = 0; side < 2; ++side) {
         const int r = child(j, side);
         if (r < 0) {
             const float v = TDP_CT * box_cost_area(lbox(~r));
-            for (int i = 0; i < 8; ++i) cl[side][i] = v;
+            for (int i = 0; i < W; ++i) cl[side][i] = v;
         } else {
-            for (int i = 0; i < 8; ++i) cl[side][i] = tab(r)[i];
+            for (int i = 0; i < W; ++i) cl[side][i] = tab(r)[i];
         }
     }
-    float cd[9];
-    for (int jj = 2; jj <= 8; ++jj) {
+    float cd[W + 1];
+    for (int jj = 2; jj <= W; ++jj) {
         float m = INFINITY;
         for (int k = 1; k < jj; ++k) m = fminf(m, cl[0][k - 1] + cl[1][jj - k - 1]);
         cd[jj] = m;
     }
-    C[0] = TDP_CN * box_cost_area(nbox(j)) + cd[8];
-    for (int i = 1; i < 8; ++i) C[i] = fminf(C[i - 1], cd[i + 1]);
+    C[0] = TDP_CN * box_cost_area(nbox(j)) + cd[W];
+    for (int i = 1; i < W; ++i) C[i] = fminf(C[i - 1], cd[i + 1]);
 }
 
-// The BVH8 children (binary refs, REF_EMPTY padded) of internal node j.
-template <class CH, class LB, class TB>
-__device__ __forceinline__ void tdp_children(int j, const CH& child, const LB& lbox, const TB& tab, int refs[8]) {
-    for (int k = 0; k < 8; ++k) refs[k] = REF_EMPTY;
-    int st_n[8], st_j[8], sp = 0, cnt = 0;
-    st_n[sp] = j; st_j[sp] = 8; ++sp;
+// The W-wide children (binary refs, REF_EMPTY padded) of internal node j.
+template <int W, class CH, class LB, class TB>
+__device__ __forceinline__ void tdp_children(int j, const CH& child, const LB& lbox, const TB& tab, int refs[W]) {
+    for (int k = 0; k < W; ++k) refs[k] = REF_EMPTY;
+    int st_n[W], st_j[W], sp = 0, cnt = 0;
+    st_n[sp] = j; st_j[sp] = W; ++sp;
     while (sp > 0) {
         --sp;
         const int nn = st_n[sp], jj = st_j[sp];
         int rc[2];
-        float t[2][8];
+        float t[2][W];
         for (int side = 0; side < 2; ++side) {
             rc[side] = child(nn, side);
             if (rc[side] < 0) {
                 const float v = TDP_CT * box_cost_area(lbox(~rc[side]));
-                for (int i = 0; i < 8; ++i) t[side][i] = v;
+                for (int i = 0; i < W; ++i) t[side][i] = v;
             } else {
-                for (int i = 0; i < 8; ++i) t[side][i] = tab(rc[side])[i];
+                for (int i = 0; i < W; ++i) t[side][i] = tab(rc[side])[i];
             }
         }
         int kb = 1;
@@ -209,6 +210,19 @@ __device__ __forceinline__ void tdp_children(int j, const CH& child, const LB& l
             }
             refs[cnt++] = rc[side];
         }
+    }
+}
+
+// Writes the wide node j (W children) from its binary refs.
+template <int W, class SRC>
+__device__ __forceinline__ void write_wide(const TlasArgs& a, int j, const int refs[W], const SRC& src_of, int i0,
+                                           int nodebase) {
+    const float EMPTY[6] = {inf_f(), inf_f(), inf_f(), inf_f(), inf_f(), inf_f()};
+    for (int c = 0; c < W; ++c) {
+        const int r = refs[c];
+        float b[6];
+        slot_box(r == REF_EMPTY ? EMPTY : src_of(r), b);
+        write_childw(a.nodesw, W, nodebase + j, c, b, r == REF_EMPTY ? REF_EMPTY : (r < 0 ? ~(i0 + ~r) : nodebase + r));
     }
 }
 
@@ -427,6 +441,46 @@ __device__ void sah_build_cta(const TlasSmem& s, int n) {
     __syncthreads();
 }
 
+template <int W, class CH, class BXF>
+__device__ __forceinline__ void cta_wide(const TlasArgs& a, const TlasSmem& s, int n, int i0, int nodebase, int toff,
+                                         int tid, int rebuild, float (*dpt)[TDP_STRIDE], const CH& ch, const BXF& bx) {
+    const bool opt = rebuild && n <= TDP_MAX;
+    auto lbf = [&](int i) { return s.box + 6 * i; };
+    auto nbf = [&](int r) { return s.ibox + 6 * r; };
+    auto tbf = [&](int r) { return dpt[r]; };
+    if (opt) {
+        for (int j = tid; j < n - 1; j += blockDim.x)
+            for (int i = 0; i < W; ++i) dpt[j][i] = INFINITY;
+        __syncthreads();
+        for (bool changed = true; changed;) {
+            float C[W];
+            bool mine = false;
+            const int j = tid;  // n - 1 <= 127 < blockDim.x
+            if (j < n - 1) {
+                tdp_node<W>(j, ch, lbf, nbf, tbf, C);
+                for (int i = 0; i < W; ++i) mine |= __float_as_int(C[i]) != __float_as_int(dpt[j][i]);
+            }
+            __syncthreads();
+            if (j < n - 1)
+                for (int i = 0; i < W; ++i) dpt[j][i] = C[i];
+            changed = __syncthreads_or(mine) != 0;
+        }
+    }
+    auto src = [&](int r) { return r < 0 ? s.box + 6 * ~r : s.ibox + 6 * r; };
+    for (int j = tid; j < n - 1; j += blockDim.x) {
+        int refs[W];
+        int* keep = a.tlas_refsw + W * (size_t)(toff + j);
+        if (!rebuild) {
+            for (int c = 0; c < W; ++c) refs[c] = keep[c];
+        } else {
+            if (opt) tdp_children<W>(j, ch, lbf, tbf, refs);
+            else collapse_w<W>(j, ch, bx, refs);
+            for (int c = 0; c < W; ++c) keep[c] = refs[c];
+        }
+        write_wide<W>(a, j, refs, src, i0, nodebase);
+    }
+}
+
 __global__ void k_tlas(TlasArgs a, int rebuild) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int e = blockIdx.x;
@@ -449,9 +503,9 @@ __global__ void k_tlas(TlasArgs a, int rebuild) {
                 a.tlas_item_parent[i0] = 0;
             }
             write_node4(a.nodes, nodebase, b, refs, n);
-            if (a.nodes8) {
-                write_child8(a.nodes8, nodebase, 0, b[0], refs[0]);
-                for (int k = 1; k < 8; ++k) write_child8(a.nodes8, nodebase, k, EMPTY, REF_EMPTY);
+            if (a.nodesw) {
+                write_childw(a.nodesw, a.wide_w, nodebase, 0, b[0], refs[0]);
+                for (int k = 1; k < a.wide_w; ++k) write_childw(a.nodesw, a.wide_w, nodebase, k, EMPTY, REF_EMPTY);
             }
             a.tlas_node_parent[toff] = -1;
             if (rebuild) a.tlas_depth[e] = 1;
@@ -617,9 +671,18 @@ __global__ void k_tlas(TlasArgs a, int rebuild) {
     auto bx = [&](int r, float b[6]) {
         for (int k = 0; k < 6; ++k) b[k] = s.ibox[6 * r + k];
     };
+    // (a build chooses the collapses and records them; a refit keeps them and
+    // only rewrites the boxes, as it keeps the binary topology)
     for (int j = tid; j < n - 1; j += blockDim.x) {
         int refs[4];
-        const int cnt = collapse4(j, ch, bx, refs);
+        int cnt = 0;
+        int* keep = a.tlas_refs4 + 4 * (size_t)(toff + j);
+        if (rebuild) {
+            cnt = collapse4(j, ch, bx, refs);
+            for (int c = 0; c < 4; ++c) keep[c] = refs[c];
+        } else {
+            for (int c = 0; c < 4; ++c) { refs[c] = keep[c]; cnt += refs[c] != REF_EMPTY; }
+        }
         float b[4][6];
         int g[4];
         for (int c = 0; c < 4; ++c) {
@@ -630,45 +693,12 @@ __global__ void k_tlas(TlasArgs a, int rebuild) {
         }
         write_node4(a.nodes, nodebase + j, b, g, cnt);
     }
-    if (a.nodes8) {
-        // the BVH8 copy of the interval-packet traversal: SAH-optimal 8-wide
+    if (a.nodesw) {
+        // the wide copy of the interval-packet traversal: SAH-optimal
         // collapse for envs of <= TDP_MAX items, greedy above
-        __shared__ float dpt[TDP_MAX - 1][8];
-        const bool opt = n <= TDP_MAX;
-        auto lbf = [&](int i) { return s.box + 6 * i; };
-        auto nbf = [&](int r) { return s.ibox + 6 * r; };
-        auto tbf = [&](int r) { return dpt[r]; };
-        if (opt) {
-            for (int j = tid; j < n - 1; j += blockDim.x)
-                for (int i = 0; i < 8; ++i) dpt[j][i] = INFINITY;
-            __syncthreads();
-            for (bool changed = true; changed;) {
-                float C[8];
-                bool mine = false;
-                const int j = tid;  // n - 1 <= 127 < blockDim.x
-                if (j < n - 1) {
-                    tdp_node(j, ch, lbf, nbf, tbf, C);
-                    for (int i = 0; i < 8; ++i) mine |= __float_as_int(C[i]) != __float_as_int(dpt[j][i]);
-                }
-                __syncthreads();
-                if (j < n - 1)
-                    for (int i = 0; i < 8; ++i) dpt[j][i] = C[i];
-                changed = __syncthreads_or(mine) != 0;
-            }
-        }
-        for (int j = tid; j < n - 1; j += blockDim.x) {
-            int refs[8];
-            if (opt) tdp_children(j, ch, lbf, tbf, refs);
-            else collapse_w<8>(j, ch, bx, refs);
-            for (int c = 0; c < 8; ++c) {
-                const int r = refs[c];
-                const float* src = r == REF_EMPTY ? EMPTY : (r < 0 ? s.box + 6 * ~r : s.ibox + 6 * r);
-                float b[6];
-                slot_box(src, b);
-                write_child8(a.nodes8, nodebase + j, c,
-                             b, r == REF_EMPTY ? REF_EMPTY : (r < 0 ? ~(i0 + ~r) : nodebase + r));
-            }
-        }
+        __shared__ float dpt[TDP_MAX - 1][TDP_STRIDE];
+        if (a.wide_w == 16) cta_wide<16>(a, s, n, i0, nodebase, toff, tid, rebuild, dpt, ch, bx);
+        else cta_wide<8>(a, s, n, i0, nodebase, toff, tid, rebuild, dpt, ch, bx);
     }
 }
 
@@ -689,11 +719,60 @@ struct TlasWarpSmem {
     uint64_t keys[32];
     float box[TW_MAX][6];
     float ibox[TW_MAX - 1][6];
-    float dpt[TW_MAX - 1][8];  // SAH-optimal BVH8 tables
+    float dpt[TW_MAX - 1][TDP_STRIDE];  // SAH-optimal wide-collapse tables
     int child[2 * (TW_MAX - 1)];
     int nparent[TW_MAX - 1];
     int lparent[TW_MAX];
 };
+
+template <int W, class CH>
+__device__ __forceinline__ void warp_wide(const TlasArgs& a, TlasWarpSmem& s, int n, int i0, int nodebase, int toff,
+                                          int lane, int rebuild, const CH& ch) {
+    const unsigned FULL = 0xFFFFFFFFu;
+    auto lbf = [&](int i) { return s.box[i]; };
+    auto nbf = [&](int r) { return s.ibox[r]; };
+    auto tbf = [&](int r) { return s.dpt[r]; };
+    auto src = [&](int r) { return r < 0 ? s.box[~r] : s.ibox[r]; };
+    if (!rebuild) {  // a refit keeps the build's collapse
+        for (int j = lane; j < n - 1; j += 32) {
+            int refs[W];
+            const int* keep = a.tlas_refsw + W * (size_t)(toff + j);
+            for (int c = 0; c < W; ++c) refs[c] = keep[c];
+            write_wide<W>(a, j, refs, src, i0, nodebase);
+        }
+        return;
+    }
+    for (int j = lane; j < n - 1; j += 32)
+        for (int i = 0; i < W; ++i) s.dpt[j][i] = INFINITY;
+    __syncwarp();
+    for (bool changed = true; __any_sync(FULL, changed);) {
+        changed = false;
+        float C[TW_PER][W];
+#pragma unroll
+        for (int m = 0; m < TW_PER; ++m) {
+            const int j = lane + 32 * m;
+            if (j < n - 1) {
+                tdp_node<W>(j, ch, lbf, nbf, tbf, C[m]);
+                for (int i = 0; i < W; ++i) changed |= __float_as_int(C[m][i]) != __float_as_int(s.dpt[j][i]);
+            }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int m = 0; m < TW_PER; ++m) {
+            const int j = lane + 32 * m;
+            if (j < n - 1)
+                for (int i = 0; i < W; ++i) s.dpt[j][i] = C[m][i];
+        }
+        __syncwarp();
+    }
+    for (int j = lane; j < n - 1; j += 32) {
+        int refs[W];
+        tdp_children<W>(j, ch, lbf, tbf, refs);
+        int* keep = a.tlas_refsw + W * (size_t)(toff + j);
+        for (int c = 0; c < W; ++c) keep[c] = refs[c];
+        write_wide<W>(a, j, refs, src, i0, nodebase);
+    }
+}
 
 __global__ void __launch_bounds__(32 * TW_WARPS) k_tlas_warp(TlasArgs a, int rebuild) {
     extern __shared__ __align__(16) unsigned char tw_raw[];
@@ -720,9 +799,9 @@ __global__ void __launch_bounds__(32 * TW_WARPS) k_tlas_warp(TlasArgs a, int reb
                 a.tlas_item_parent[i0] = 0;
             }
             write_node4(a.nodes, nodebase, b, refs, n);
-            if (a.nodes8) {
-                write_child8(a.nodes8, nodebase, 0, b[0], refs[0]);
-                for (int k = 1; k < 8; ++k) write_child8(a.nodes8, nodebase, k, EMPTY, REF_EMPTY);
+            if (a.nodesw) {
+                write_childw(a.nodesw, a.wide_w, nodebase, 0, b[0], refs[0]);
+                for (int k = 1; k < a.wide_w; ++k) write_childw(a.nodesw, a.wide_w, nodebase, k, EMPTY, REF_EMPTY);
             }
             a.tlas_node_parent[toff] = -1;
             if (rebuild) a.tlas_depth[e] = 1;
@@ -849,37 +928,20 @@ __global__ void __launch_bounds__(32 * TW_WARPS) k_tlas_warp(TlasArgs a, int reb
     auto bx = [&](int r, float b[6]) {
         for (int k = 0; k < 6; ++k) b[k] = s.ibox[r][k];
     };
-    if (a.nodes8) {  // SAH-optimal BVH8 tables (n <= TW_MAX = TDP_MAX)
-        auto lbf = [&](int i) { return s.box[i]; };
-        auto nbf = [&](int r) { return s.ibox[r]; };
-        auto tbf = [&](int r) { return s.dpt[r]; };
-        for (int j = lane; j < n - 1; j += 32)
-            for (int i = 0; i < 8; ++i) s.dpt[j][i] = INFINITY;
-        __syncwarp();
-        for (bool changed = true; __any_sync(FULL, changed);) {
-            changed = false;
-            float C[TW_PER][8];
-#pragma unroll
-            for (int m = 0; m < TW_PER; ++m) {
-                const int j = lane + 32 * m;
-                if (j < n - 1) {
-                    tdp_node(j, ch, lbf, nbf, tbf, C[m]);
-                    for (int i = 0; i < 8; ++i) changed |= __float_as_int(C[m][i]) != __float_as_int(s.dpt[j][i]);
-                }
-            }
-            __syncwarp();
-#pragma unroll
-            for (int m = 0; m < TW_PER; ++m) {
-                const int j = lane + 32 * m;
-                if (j < n - 1)
-                    for (int i = 0; i < 8; ++i) s.dpt[j][i] = C[m][i];
-            }
-            __syncwarp();
-        }
+    if (a.nodesw) {  // SAH-optimal wide copy (n <= TW_MAX = TDP_MAX)
+        if (a.wide_w == 16) warp_wide<16>(a, s, n, i0, nodebase, toff, lane, rebuild, ch);
+        else warp_wide<8>(a, s, n, i0, nodebase, toff, lane, rebuild, ch);
     }
     for (int j = lane; j < n - 1; j += 32) {
         int refs[4];
-        const int cnt = collapse4(j, ch, bx, refs);
+        int cnt = 0;
+        int* keep = a.tlas_refs4 + 4 * (size_t)(toff + j);
+        if (rebuild) {
+            cnt = collapse4(j, ch, bx, refs);
+            for (int c = 0; c < 4; ++c) keep[c] = refs[c];
+        } else {
+            for (int c = 0; c < 4; ++c) { refs[c] = keep[c]; cnt += refs[c] != REF_EMPTY; }
+        }
         float b[4][6];
         int g[4];
         for (int c = 0; c < 4; ++c) {
@@ -889,18 +951,6 @@ __global__ void __launch_bounds__(32 * TW_WARPS) k_tlas_warp(TlasArgs a, int reb
             g[c] = r == REF_EMPTY ? REF_EMPTY : (r < 0 ? ~(i0 + ~r) : nodebase + r);
         }
         write_node4(a.nodes, nodebase + j, b, g, cnt);
-        if (a.nodes8) {
-            int refs8[8];
-            tdp_children(j, ch, [&](int i) { return s.box[i]; }, [&](int r) { return s.dpt[r]; }, refs8);
-            for (int c = 0; c < 8; ++c) {
-                const int r = refs8[c];
-                const float* src = r == REF_EMPTY ? EMPTY : (r < 0 ? s.box[~r] : s.ibox[r]);
-                float bb[6];
-                slot_box(src, bb);
-                write_child8(a.nodes8, nodebase + j, c,
-                             bb, r == REF_EMPTY ? REF_EMPTY : (r < 0 ? ~(i0 + ~r) : nodebase + r));
-            }
-        }
     }
 }
 
@@ -921,7 +971,9 @@ cudaError_t items_update(const TlasArgs& a, int n_items, cudaStream_t stream) {
 
 cudaError_t tlas_build(const TlasArgs& a, bool rebuild, cudaStream_t stream) {
     size_t smem = tlas_smem_bytes(a.max_n);
-    if (smem > 48 * 1024) {
+    {
+        // k_tlas has ~36 KB of static shared memory (SAH bins, DP tables):
+        // any dynamic part beyond the default 48 KB total needs the opt-in
         cudaError_t e = cudaFuncSetAttribute(k_tlas, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
     }

@@ -833,13 +833,15 @@ def test_annotations_host_path_and_errors():
 
 # ---- maximum sizes ---------------------------------------------------------------
 
+@pytest.mark.parametrize("n", [300, 1024])
 @pytest.mark.parametrize("builder", [0, 1])
-def test_max_instances_per_env(builder):
+def test_max_instances_per_env(builder, n):
     """AGR_MAX_INSTANCES_PER_ENV (1024) instances in one env -- the largest
-    one-CTA TLAS build -- with both TLAS builders, rebuild and refit, against
-    the oracle; one more instance is EUNSUPPORTED."""
+    one-CTA TLAS build -- and 300 (a CTA build whose shared memory crosses
+    48 KB only with the static part counted), with both TLAS builders,
+    rebuild and refit, against the oracle; one more instance is
+    EUNSUPPORTED."""
     rng = np.random.default_rng(41)
-    n = 1024
     per_env = []
     for e in range(2):
         insts = []
@@ -855,8 +857,8 @@ def test_max_instances_per_env(builder):
     s.build()
     got = to_np(cast_sensor(s, sensor, "range"))
     ref = oracle.cast(sc, oracle_rays(sensor, "range"))
-    compare(ref, got["dist"], got["seg"], got["face"], f"1024 instances, builder {builder}")
-    assert (got["face"][: cam["W"] * cam["H"]] >= 0).mean() > 0.3
+    compare(ref, got["dist"], got["seg"], got["face"], f"{n} instances, builder {builder}")
+    assert (got["face"][: cam["W"] * cam["H"]] >= 0).mean() > (0.3 if n == 1024 else 0.1)
     assert s.info()["n_instances"] == n + 37
     # re-pose everything and refit (topology kept)
     T2 = sc.inst_T.copy()
@@ -866,10 +868,11 @@ def test_max_instances_per_env(builder):
     got = to_np(cast_sensor(s, sensor, "range"))
     sc2 = sg.Scene(sc.meshes, sc.env_off, sc.inst_asset, sc.inst_label, T2)
     ref = oracle.cast(sc2, oracle_rays(sensor, "range"))
-    compare(ref, got["dist"], got["seg"], got["face"], "1024 instances after refit")
-    with pytest.raises(agr.AgrError):
-        sg_over = sg.assemble([sg.cube_mesh()], [[(0, 1, sg.make_T(np.eye(3), (3, 0, 0)))] * (n + 1)])
-        agr.Scene.from_scenegen(sg_over, device=0)
+    compare(ref, got["dist"], got["seg"], got["face"], f"{n} instances after refit")
+    if n == 1024:
+        with pytest.raises(agr.AgrError):
+            sg_over = sg.assemble([sg.cube_mesh()], [[(0, 1, sg.make_T(np.eye(3), (3, 0, 0)))] * (n + 1)])
+            agr.Scene.from_scenegen(sg_over, device=0)
 
 
 def test_large_image_sampled():
@@ -1056,10 +1059,11 @@ def test_parts_update_mesh_stereo_and_exact():
 
 @pytest.mark.parametrize("cfg", [2, 3, 4])
 def test_bvh8_packets_equal_bvh4_packets_bitwise(cfg):
-    """The interval-packet traversal over the BVH8 copy (default), over the
-    BVH4 (traversal mode 2), a BVH4-only scene (node_width 4) and the
-    per-lane traversal give bitwise identical images, after a rebuild and
-    after a refit; and match the oracle on samples."""
+    """The interval-packet traversal over the BVH8 copy (default), over a
+    BVH16 copy (node_width 16), over the BVH4 (traversal mode 2), a
+    BVH4-only scene (node_width 4) and the per-lane traversal give bitwise
+    identical images, after a rebuild and after a refit; and match the
+    oracle on samples."""
     if cfg == 2:
         sc, sensor = sg.config2(n_envs=8)
     elif cfg == 3:
@@ -1071,8 +1075,10 @@ def test_bvh8_packets_equal_bvh4_packets_bitwise(cfg):
     chans = ("dist", "seg", "face", "normal")
     s = make_scene(sc, build=False)
     s4 = agr.Scene.from_scenegen(sc, device=0, node_width=4)
-    s4.set_instance_transforms(torch.from_numpy(sc.inst_T).to(dev()))
-    for sc_ in (s, s4):
+    s16 = agr.Scene.from_scenegen(sc, device=0, node_width=16)
+    for sc_ in (s4, s16):
+        sc_.set_instance_transforms(torch.from_numpy(sc.inst_T).to(dev()))
+    for sc_ in (s, s4, s16):
         sc_.set_tlas_builder(1)
         sc_.build()
     imgs = []
@@ -1080,11 +1086,11 @@ def test_bvh8_packets_equal_bvh4_packets_bitwise(cfg):
         if step == 1:
             T2 = sc.inst_T.copy()
             T2[:, :2, 3] += np.random.default_rng(5).uniform(-0.3, 0.3, (len(T2), 2)).astype(np.float32)
-            for sc_ in (s, s4):
+            for sc_ in (s, s4, s16):
                 sc_.set_instance_transforms(torch.from_numpy(T2).to(dev()))
                 sc_.refit()
         runs = []
-        for sc_, mode in ((s, 0), (s, 2), (s4, 0), (s, 1), (s, 3)):
+        for sc_, mode in ((s, 0), (s, 2), (s4, 0), (s, 1), (s, 3), (s16, 0), (s16, 3)):
             sc_.set_traversal(mode)
             runs.append(to_np(cast_sensor(sc_, sensor, kind, channels=chans)))
         for r in runs[1:]:
