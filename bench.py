@@ -109,7 +109,7 @@ def parse(argv=None):
                          "(default: lane for c6, whose terrain seen at grazing angles makes a "
                          "4x8 packet test ~9x the triangles its rays need; auto elsewhere); "
                          "packet4: the interval packets on the 4-wide nodes (A/B)")
-    ap.add_argument("--node-width", type=int, default=None, choices=[0, 4, 8, 16],
+    ap.add_argument("--node-width", type=int, default=None, choices=[0, 4, 8, 16, 32],
                     help="agr_create_options.node_width: the interval packets' wide BVH copy (0: the "
                          "library default; 4: none)")
     ap.add_argument("--no-parts", action="store_true",

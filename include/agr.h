@@ -203,8 +203,10 @@ typedef struct {
                              BVH every traversal uses, for the interval-packet
                              camera / LiDAR traversal: 8 (256-B nodes) or 16
                              (512-B nodes: lanes 0-15 test the children, 16-31
-                             order them); 0 (default): 16 if some env has more
-                             than 64 TLAS items (a deep TLAS: c3 +4 %), else 8;
+                             order them) or 32 (1-KB nodes: every lane tests
+                             one child, ordered by the tile's entry bound);
+                             0 (default): 32 if some env has more than 64
+                             TLAS items (a deep TLAS: c3 +5 % over 8), else 8;
                              4: no wide copy (half the node memory and no wide
                              collapse in builds / refits -- for scenes cast one
                              ray per lane).                                  */

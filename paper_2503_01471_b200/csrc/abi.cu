@@ -457,8 +457,9 @@ agr_status agr_scene_create_ex(int32_t device, const agr_mesh* meshes, int32_t n
         return fail(AGR_EINVAL, "trbvh_rounds must be in [0, 16]");
     if (opts && (opts->part_policy < 0 || opts->part_policy > 1))
         return fail(AGR_EINVAL, "part_policy must be 0 (auto) or 1 (one BLAS per asset)");
-    if (opts && opts->node_width != 0 && opts->node_width != 4 && opts->node_width != 8 && opts->node_width != 16)
-        return fail(AGR_EINVAL, "node_width must be 0 (default), 4, 8 or 16");
+    if (opts && opts->node_width != 0 && opts->node_width != 4 && opts->node_width != 8 && opts->node_width != 16 &&
+        opts->node_width != 32)
+        return fail(AGR_EINVAL, "node_width must be 0 (default), 4, 8, 16 or 32");
     agr_scene_s* s = new agr_scene_s();
     s->device = device;
     if (opts) s->trbvh_rounds = opts->trbvh_rounds;
@@ -554,8 +555,8 @@ agr_status agr_scene_create_ex(int32_t device, const agr_mesh* meshes, int32_t n
         delete s;
         return st;
     };
-#ifndef AGR_WIDE16_ITEMS
-#define AGR_WIDE16_ITEMS 64  // node_width 0: BVH16 above this many TLAS items in some env, else BVH8
+#ifndef AGR_WIDE_DEEP_ITEMS
+#define AGR_WIDE_DEEP_ITEMS 64  // node_width 0: BVH32 above this many TLAS items in some env, else BVH8
 #endif
 #define CKB(call)                                                    \
     do {                                                             \
@@ -564,10 +565,11 @@ agr_status agr_scene_create_ex(int32_t device, const agr_mesh* meshes, int32_t n
     } while (0)
 
     CKB(s->alloc(&s->nodes, 8 * (size_t)(nb + nt)));
-    // node_width 0: BVH16 when some env has more than 64 TLAS items (the
-    // TLAS is then deep enough for the 16-wide nodes to pay: c3's 91 items
-    // +3.5 %), else BVH8 (c4 / c5 with 16-20 items: BVH16 -1 %)
-    s->wide_w = !opts || opts->node_width == 0 ? (s->max_n > AGR_WIDE16_ITEMS ? 16 : 8)
+    // node_width 0: BVH32 when some env has more than 64 TLAS items (the
+    // TLAS is then deep enough for the wide nodes to pay: c3's 91 items
+    // BVH16 +3.5 % over BVH8, BVH32 +1.3 % over BVH16), else BVH8 (c4 / c5
+    // with 16-20 items: BVH16 -1 %, BVH32 -3.5 % -- its builds cost more)
+    s->wide_w = !opts || opts->node_width == 0 ? (s->max_n > AGR_WIDE_DEEP_ITEMS ? 32 : 8)
                 : opts->node_width == 4 ? 0 : opts->node_width;
     if (s->wide_w) CKB(s->alloc(&s->nodesw, (size_t)2 * s->wide_w * (nb + nt)));
     CKB(s->alloc(&s->bnodes, 4 * (size_t)nb));
@@ -645,7 +647,7 @@ agr_status agr_scene_create_ex(int32_t device, const agr_mesh* meshes, int32_t n
         CKB(cudaMemcpy(s->asset_foff, fo.data(), sizeof(int) * n_meshes, cudaMemcpyHostToDevice));
     }
     // scratch for a batch of every asset (any update batch fits in it)
-    CKB(s->alloc((char**)&s->blas_scratch, blas_scratch_bytes(s->h_mface_off[n_meshes], n_parts)));
+    CKB(s->alloc((char**)&s->blas_scratch, blas_scratch_bytes(s->h_mface_off[n_meshes], n_parts, s->wide_w)));
     s->blas_stage_bytes = blas_stage_bytes(s->h_mface_off[n_meshes], n_parts);
     CKB(cudaMallocHost(&s->blas_stage, s->blas_stage_bytes));
     CKB(cudaEventCreateWithFlags(&s->blas_stage_free, cudaEventDisableTiming));

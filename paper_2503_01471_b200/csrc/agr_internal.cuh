@@ -81,7 +81,7 @@ struct BlasInfo {
 // Read-only view of a scene passed by value to kernels.
 struct SceneView {
     const float4* nodes;      // [n_nodes][8] BVH4
-    int wide_w;               // width of the wide copy: 8 or 16 (0: none)
+    int wide_w;               // width of the wide copy: 8, 16 or 32 (0: none)
     const float4* nodesw;     // [n_nodes][2 wide_w] BVH8 / BVH16 copy (its own numbering; BLAS roots and TLAS nodes at the
                               // same indices as the BVH4), or null
     const float4* tris;       // [n_leaves][3]
@@ -258,7 +258,7 @@ struct BlasSeg {
 struct BlasBatchArgs {
     float4* nodes;         // global BVH4 node array
     float4* nodesw;        // global wide node array (compacted like the BVH4; root at node_base), or null
-    int wide_w;            // its width: 8 or 16
+    int wide_w;            // its width: 8, 16 or 32
     float4* bnodes;        // global binary BLAS node array (debug export)
     float4* tris;          // global tri record array
     float* triv;           // global exact-vertex array
@@ -272,7 +272,7 @@ struct BlasBatchArgs {
 // Builds the BLAS of every asset in h_segs[0, n) (host array; `off` is
 // filled in) in one set of launches.  `scratch` must hold
 // blas_scratch_bytes(sum of n_faces, n) bytes.  Async on `stream`.
-size_t blas_scratch_bytes(int64_t total_faces, int n_segs);
+size_t blas_scratch_bytes(int64_t total_faces, int n_segs, int wide_w);
 // Pinned host staging a batch of n_segs segments over total_faces faces needs
 // (BlasBatchArgs.h_stage).
 size_t blas_stage_bytes(int64_t total_faces, int n_segs);
@@ -282,7 +282,7 @@ cudaError_t blas_build_batch(BlasSeg* h_segs, int n_segs, const BlasBatchArgs& a
 struct TlasArgs {
     float4* nodes;            // global node array (TLAS part written)
     float4* nodesw;           // global wide node array (TLAS part written), or null
-    int wide_w;               // its width: 8 or 16
+    int wide_w;               // its width: 8, 16 or 32
     float4* irec;             // [n_items][4] written
     float* item_box;          // [n_items][6] written
     const float* inst_T;      // [n_inst][12]

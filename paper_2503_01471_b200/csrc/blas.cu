@@ -135,7 +135,7 @@ struct Scratch {
 
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
-size_t scratch_layout(int64_t F, int B, void* base, Scratch* out) {
+size_t scratch_layout(int64_t F, int B, int wide_w, void* base, Scratch* out) {
     char* p = (char*)base;
     size_t used = 0;
     const size_t nb = (size_t)rs_max_blocks(F, B);
@@ -170,7 +170,7 @@ size_t scratch_layout(int64_t F, int B, void* base, Scratch* out) {
     s.seg8 = (int*)take(sizeof(int) * B);
     s.queue = (int2*)take(sizeof(int2) * F);
     s.rec = (float4*)take(AGR_CHILD_REC ? sizeof(float4) * 4 * F : 16);
-    s.dp8 = (float*)take(sizeof(float) * 16 * F);  // W <= 16
+    s.dp8 = (float*)take(sizeof(float) * (wide_w > 0 ? wide_w : 1) * F);  // the wide collapse's DP tables
     s.qctl = (int*)take(sizeof(int) * (2 + MAX_LEVELS));
     if (out) *out = s;
     return used + 256;
@@ -1481,8 +1481,8 @@ __global__ void k_asset_info(const BlasSeg* segs, int B, const uint32_t* bounds,
 
 }  // namespace
 
-size_t blas_scratch_bytes(int64_t total_faces, int n_segs) {
-    return scratch_layout(total_faces, n_segs, nullptr, nullptr);
+size_t blas_scratch_bytes(int64_t total_faces, int n_segs, int wide_w) {
+    return scratch_layout(total_faces, n_segs, wide_w, nullptr, nullptr);
 }
 
 size_t blas_stage_bytes(int64_t total_faces, int n_segs) {
@@ -1501,7 +1501,7 @@ cudaError_t blas_build_batch(BlasSeg* h_segs, int B, const BlasBatchArgs& a, voi
     if (F64 <= 0 || F64 > 0x3FFFFFFF) return cudaErrorInvalidValue;
     const int F = (int)F64;
     Scratch s;
-    scratch_layout(F, B, scratch, &s);
+    scratch_layout(F, B, a.wide_w, scratch, &s);
     // the segment table and the sort-block table (below) go up in one copy,
     // from pinned staging when the caller provides it (a pageable copy
     // would wait for the stream to drain first)
@@ -1618,21 +1618,24 @@ cudaError_t blas_build_batch(BlasSeg* h_segs, int B, const BlasBatchArgs& a, voi
     if (e != cudaSuccess) return e;
     k_write4_small<<<(B + 127) / 128, 128, 0, stream>>>(s.segs, B, s.bounds, sv, s.tri_box, a.nodes);
     if (a.nodesw) {
-        const bool w16 = a.wide_w == 16;
-        if (a.opt_collapse) {
+        const int W = a.wide_w;
+        auto pick = [&](bool dp) -> const void* {
+            if (W == 32) return (const void*)k_bvhw_topdown<32, true>;  // always the DP collapse
+            if (W == 16) return dp ? (const void*)k_bvhw_topdown<16, true> : (const void*)k_bvhw_topdown<16, false>;
+            return dp ? (const void*)k_bvhw_topdown<8, true> : (const void*)k_bvhw_topdown<8, false>;
+        };
+        if (a.opt_collapse || W == 32) {
             // SAH-optimal wide collapse (the interval packets' tree): cost tables bottom-up
             cudaMemsetAsync(s.flags, 0, sizeof(int) * F, stream);
-            if (w16)
-                k_dpw<16><<<gb, T_BLK, 0, stream>>>(s.segs, s.seg_of, s.bounds, F, s.tri_box, s.child, s.leaf_parent,
-                                                   s.node_parent, s.ibox, s.flags, s.dp8);
-            else
-                k_dpw<8><<<gb, T_BLK, 0, stream>>>(s.segs, s.seg_of, s.bounds, F, s.tri_box, s.child, s.leaf_parent,
-                                                  s.node_parent, s.ibox, s.flags, s.dp8);
-            e = topdown(w16 ? (const void*)k_bvhw_topdown<16, true> : (const void*)k_bvhw_topdown<8, true>, s.seg8,
-                        a.nodesw, s.dp8);
+#define AGR_DPW(WW) k_dpw<WW><<<gb, T_BLK, 0, stream>>>(s.segs, s.seg_of, s.bounds, F, s.tri_box, s.child, \
+                                                       s.leaf_parent, s.node_parent, s.ibox, s.flags, s.dp8)
+            if (W == 32) AGR_DPW(32);
+            else if (W == 16) AGR_DPW(16);
+            else AGR_DPW(8);
+#undef AGR_DPW
+            e = topdown(pick(true), s.seg8, a.nodesw, s.dp8);
         } else {
-            e = topdown(w16 ? (const void*)k_bvhw_topdown<16, false> : (const void*)k_bvhw_topdown<8, false>,
-                        s.seg8, a.nodesw, nullptr);
+            e = topdown(pick(false), s.seg8, a.nodesw, nullptr);
         }
         if (e != cudaSuccess) return e;
         k_writew_small<<<(B + 127) / 128, 128, 0, stream>>>(s.segs, B, s.bounds, s.tri_box, a.nodesw, a.wide_w);

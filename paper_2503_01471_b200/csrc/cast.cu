@@ -580,7 +580,7 @@ __device__ __forceinline__ void traverse_lane(const SceneView& sv, int env, RayS
 // warp-uniform (no divergence in the traversal loop); every node / triangle
 // fetch is a broadcast load.  Each lane still does its own exact-filter box
 // and triangle tests, so results equal the per-lane traversal.
-constexpr int PSTACK = 96;
+constexpr int PSTACK = 128;  // >= 4 full levels of 32-wide pushes
 
 template <int CL, bool ANYHIT, bool COUNT, class LEAF>
 __device__ __forceinline__ void traverse_packet(const SceneView& sv, int env, RayState& rs,
@@ -740,7 +740,7 @@ __device__ __forceinline__ void iv_recip(float lo, float hi, float& i0, float& i
 template <int CL, int CENTRE_BIT = 4>
 __device__ __forceinline__ PSlab make_pslab(f3 o, f3 d, float delta) {
     const unsigned FULL = 0xFFFFFFFFu;
-    const bool centre = (threadIdx.x & CENTRE_BIT) != 0;
+    const bool centre = ((threadIdx.x & 31) & CENTRE_BIT) != 0;  // CENTRE_BIT 32: no centre lanes
     const float dcx = __shfl_sync(FULL, d.x, CL);
     const float dcy = __shfl_sync(FULL, d.y, CL);
     const float dcz = __shfl_sync(FULL, d.z, CL);
@@ -854,7 +854,7 @@ __device__ __forceinline__ void ps8_axis(float o, float dp, float lo, float hi, 
 template <int CL, int CENTRE_BIT = 8>
 __device__ __forceinline__ PSlab8 make_pslab8(f3 o, f3 d, float delta) {
     const unsigned FULL = 0xFFFFFFFFu;
-    const bool centre = (threadIdx.x & CENTRE_BIT) != 0;
+    const bool centre = ((threadIdx.x & 31) & CENTRE_BIT) != 0;  // CENTRE_BIT 32: no centre lanes
     const float dcx = __shfl_sync(FULL, d.x, CL);
     const float dcy = __shfl_sync(FULL, d.y, CL);
     const float dcz = __shfl_sync(FULL, d.z, CL);
@@ -1112,7 +1112,8 @@ __device__ __forceinline__ void traverse_ipacketw(const SceneView& sv, int env, 
             // order keys: the centre ray's entry distance (lanes 8-15) with
             // the child index in the 3 low bits (distinct; near-equal
             // distances go by index), misses last; the nearest by one REDUX
-            const unsigned kc = __shfl_sync(FULL, __float_as_uint(tn), child + WW);
+            // (WW = 32: no centre lanes; the key is the interval's own entry bound)
+            const unsigned kc = WW == 32 ? __float_as_uint(tn) : __shfl_sync(FULL, __float_as_uint(tn), child + WW);
             const bool hit = slot_lane && ((cm >> child) & 1u);
             const unsigned key = hit ? ((kc & ~(unsigned)(WW - 1)) | (unsigned)child) : 0xFFFFFFFFu;
             const int near_child = (int)(__reduce_min_sync(FULL, key) & (unsigned)(WW - 1));
@@ -1671,6 +1672,7 @@ cudaError_t launch_model(CastArgs a, cudaStream_t stream) {
     do {                                                        \
         if (trav == 2) AGR_LAUNCH(2, C, S, 0);                  \
         else if (trav == 0) AGR_LAUNCH(0, C, S, 0);             \
+        else if (wide == 32) AGR_LAUNCH(1, C, S, 32);           \
         else if (wide == 16) AGR_LAUNCH(1, C, S, 16);           \
         else if (wide == 8) AGR_LAUNCH(1, C, S, 8);             \
         else AGR_LAUNCH(1, C, S, 0);                            \

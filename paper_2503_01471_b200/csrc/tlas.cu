@@ -11,6 +11,7 @@
 //                    FP32), conservative world box of the part
 //   K7 k_tlas        (rebuild) per-env Morton sort + Karras + fit, one CTA/env
 //   K8 k_tlas        (refit)   same CTA shape, stored topology, boxes only
+#include <algorithm>
 #include "agr_internal.cuh"
 
 #include <cfloat>
@@ -152,7 +153,7 @@ constexpr int TDP_MAX = 128;
 __device__ __forceinline__ float box_cost_area(const float* b) { return b[0] <= b[3] ? half_area(b) : 0.0f; }
 
 // New table of internal node j from its children's current tables.
-constexpr int TDP_STRIDE = 16;  // floats per table row (W <= 16)
+constexpr int TDP_STRIDE = 32;  // floats per table row (W <= 32)
 template <int W, class CH, class LB, class NB, class TB>
 __device__ __forceinline__ void tdp_node(int j, const CH& child, const LB& lbox, const NB& nbox, const TB& tab,
                                          float C[W]) {
@@ -523,7 +524,8 @@ __global__ void k_tlas(TlasArgs a, int rebuild) {
     s.child = (int*)p; p += sizeof(int) * 2 * (n - 1);
     s.nparent = (int*)p; p += sizeof(int) * (n - 1);
     s.lparent = (int*)p; p += sizeof(int) * n;
-    s.flags = (int*)p;
+    s.flags = (int*)p; p += sizeof(int) * (n - 1);
+    float(*dpt)[TDP_STRIDE] = reinterpret_cast<float(*)[TDP_STRIDE]>(p);  // n <= TDP_MAX only
 
     for (int i = tid; i < n; i += blockDim.x)
         for (int k = 0; k < 6; ++k) s.box[6 * i + k] = a.item_box[6 * (i0 + i) + k];
@@ -696,8 +698,8 @@ __global__ void k_tlas(TlasArgs a, int rebuild) {
     if (a.nodesw) {
         // the wide copy of the interval-packet traversal: SAH-optimal
         // collapse for envs of <= TDP_MAX items, greedy above
-        __shared__ float dpt[TDP_MAX - 1][TDP_STRIDE];
-        if (a.wide_w == 16) cta_wide<16>(a, s, n, i0, nodebase, toff, tid, rebuild, dpt, ch, bx);
+        if (a.wide_w == 32) cta_wide<32>(a, s, n, i0, nodebase, toff, tid, rebuild, dpt, ch, bx);
+        else if (a.wide_w == 16) cta_wide<16>(a, s, n, i0, nodebase, toff, tid, rebuild, dpt, ch, bx);
         else cta_wide<8>(a, s, n, i0, nodebase, toff, tid, rebuild, dpt, ch, bx);
     }
 }
@@ -719,7 +721,7 @@ struct TlasWarpSmem {
     uint64_t keys[32];
     float box[TW_MAX][6];
     float ibox[TW_MAX - 1][6];
-    float dpt[TW_MAX - 1][TDP_STRIDE];  // SAH-optimal wide-collapse tables
+    float dpt[31][TDP_STRIDE];  // SAH-optimal wide-collapse tables (builds: <= 32 items)
     int child[2 * (TW_MAX - 1)];
     int nparent[TW_MAX - 1];
     int lparent[TW_MAX];
@@ -928,8 +930,9 @@ __global__ void __launch_bounds__(32 * TW_WARPS) k_tlas_warp(TlasArgs a, int reb
     auto bx = [&](int r, float b[6]) {
         for (int k = 0; k < 6; ++k) b[k] = s.ibox[r][k];
     };
-    if (a.nodesw) {  // SAH-optimal wide copy (n <= TW_MAX = TDP_MAX)
-        if (a.wide_w == 16) warp_wide<16>(a, s, n, i0, nodebase, toff, lane, rebuild, ch);
+    if (a.nodesw) {  // SAH-optimal wide copy (builds: n <= 32; refits keep the stored collapse)
+        if (a.wide_w == 32) warp_wide<32>(a, s, n, i0, nodebase, toff, lane, rebuild, ch);
+        else if (a.wide_w == 16) warp_wide<16>(a, s, n, i0, nodebase, toff, lane, rebuild, ch);
         else warp_wide<8>(a, s, n, i0, nodebase, toff, lane, rebuild, ch);
     }
     for (int j = lane; j < n - 1; j += 32) {
@@ -959,7 +962,8 @@ size_t tlas_smem_bytes(int n) {
     int P = 1;
     while (P < n) P <<= 1;
     return sizeof(uint64_t) * P + sizeof(int) * 4 * (n - 1) + sizeof(float) * 6 * n + sizeof(float) * 6 * (n - 1) +
-           sizeof(int) * 2 * (n - 1) + sizeof(int) * (n - 1) + sizeof(int) * n + sizeof(int) * (n - 1);
+           sizeof(int) * 2 * (n - 1) + sizeof(int) * (n - 1) + sizeof(int) * n + sizeof(int) * (n - 1) +
+           (n <= TDP_MAX ? sizeof(float) * TDP_STRIDE * (n - 1) : 0);  // wide-collapse DP tables
 }
 
 }  // namespace
@@ -970,9 +974,12 @@ cudaError_t items_update(const TlasArgs& a, int n_items, cudaStream_t stream) {
 }
 
 cudaError_t tlas_build(const TlasArgs& a, bool rebuild, cudaStream_t stream) {
+    // (an env of <= TDP_MAX items also holds the DP tables: the largest such
+    // env may need more than the largest env)
     size_t smem = tlas_smem_bytes(a.max_n);
+    if (a.max_n > TDP_MAX) smem = std::max(smem, tlas_smem_bytes(TDP_MAX));
     {
-        // k_tlas has ~36 KB of static shared memory (SAH bins, DP tables):
+        // k_tlas has ~33 KB of static shared memory (SAH bins):
         // any dynamic part beyond the default 48 KB total needs the opt-in
         cudaError_t e = cudaFuncSetAttribute(k_tlas, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;

@@ -1,0 +1,10 @@
+timeout 900 python -m pytest tests/test_parity_gpu.py -m gpu -x -q -k "bvh8 or tlas_warp or max_instances or update_meshes" 2>&1 | tail -2
+for r in 1 2; do
+for c in 3 5; do
+  for w in 16 32; do
+    timeout 600 python bench.py --config $c --node-width $w --no-table2 --no-cpu-baseline --no-e2e > gpurun_out/w32_c${c}_$w.json 2>&1
+    python -c "
+import json; d=json.loads(open('gpurun_out/w32_c${c}_$w.json').read().strip().splitlines()[-1]); c=d['counters_per_ray']; print('c$c w$w', '%.4g'%d['value'], 'upd %.3f cast %.3f'%(d['update_ms_per_step'], d['cast_ms_per_step']), {k: round(c[k],3) for k in ('nodes','leaves','instances','tlas_nodes')})"
+  done
+done
+done

@@ -1,0 +1,8 @@
+timeout 1800 python -m pytest tests -m gpu -x -q 2>&1 | tail -4
+for c in 3; do
+  for w in 0 16; do
+    timeout 600 python bench.py --config $c --node-width $w --no-table2 --no-cpu-baseline --no-e2e > gpurun_out/w32b_c${c}_$w.json 2>&1
+    python -c "
+import json; d=json.loads(open('gpurun_out/w32b_c${c}_$w.json').read().strip().splitlines()[-1]); c=d['counters_per_ray']; print('c$c w$w', '%.4g'%d['value'], 'upd %.3f cast %.3f'%(d['update_ms_per_step'], d['cast_ms_per_step']), d['roofline']['frac'], {k: round(c[k],3) for k in ('nodes','leaves','instances','tlas_nodes')})"
+  done
+done
