@@ -1118,12 +1118,21 @@ __device__ __forceinline__ void traverse_ipacketw(const SceneView& sv, int env, 
             const unsigned key = hit ? ((kc & ~(unsigned)(WW - 1)) | (unsigned)child) : 0xFFFFFFFFu;
             const int near_child = (int)(__reduce_min_sync(FULL, key) & (unsigned)(WW - 1));
             const int nearest = __shfl_sync(FULL, ref, near_child);
-            if (sp + WW - 1 <= PSTACK) {
+            if (sp + nh - 1 <= PSTACK) {
                 __syncwarp();  // every lane has read the slots before they are reused
                 if (AGR_RANK_MODE == 1 && nh > 2) {
                     int rank = 0;  // among the hits, farthest pushed first
+                    if (WW <= 8) {
 #pragma unroll
-                    for (int j = 0; j < WW; ++j) rank += __shfl_sync(FULL, key, j) < key ? 1 : 0;
+                        for (int j = 0; j < WW; ++j) rank += __shfl_sync(FULL, key, j) < key ? 1 : 0;
+                    } else {
+                        // wide nodes: compare with the other hits only (a
+                        // warp-uniform loop of nh - 1 steps, not WW)
+                        rank = 1;
+                        for (unsigned m = cm & ~(1u << near_child); m; m &= m - 1u)
+                            rank += __shfl_sync(FULL, key, __ffs(m) - 1) < key ? 1 : 0;
+                        if (child == near_child) rank = 0;
+                    }
                     if (hit && rank > 0) wstack[sp + nh - 1 - rank] = ref;
                 } else if (hit && child != near_child) {
                     // nh == 2 (exact), or mode 2: the other hits in child order
