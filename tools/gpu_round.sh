@@ -14,3 +14,11 @@ timeout 600 python bench.py --config 5 --tlas-step refit --no-table2 --no-e2e --
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/${tag}_bench_reference.json 2>&1
 bash tools/profile_round.sh $tag 3 4 5 6 > gpurun_out/${tag}_profile.log 2>&1
 tail -2 gpurun_out/${tag}_gputests.txt
+# gpurun copies back at most 64 MiB of gpurun_out/: summarise the captures on
+# the box and keep only the c3 capture (plus its SASS-by-line page).
+PROFILES_OUT=gpurun_out/prof_${tag} python tools/ncu_extract.py $tag > gpurun_out/${tag}_extract.txt 2>&1
+cuobjdump -xelf all paper_2503_01471_b200/lib/libagr.so > /dev/null 2>&1; rm -rf /tmp/cubins; mkdir -p /tmp/cubins; mv *.cubin /tmp/cubins/ 2>/dev/null
+cub=$(ls /tmp/cubins/*cast* 2>/dev/null | head -1)
+[ -n "$cub" ] && python tools/sass_lines.py gpurun_out/${tag}_cast_c3.ncu-rep $cub k_cast 60 > gpurun_out/${tag}_c3_sass_lines.txt 2>&1
+mkdir -p /tmp/reps; for c in 4 5 6; do mv gpurun_out/${tag}_cast_c$c.ncu-rep /tmp/reps/ 2>/dev/null; done
+du -sh gpurun_out

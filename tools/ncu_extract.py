@@ -3,7 +3,8 @@
   tools/ncu_extract.py TAG [configs...]
 reads gpurun_out/TAG_cast_cN.ncu-rep (`--set full`) and
 gpurun_out/TAG_launches_cN.csv (per-launch gpu__time_duration), writes
-profiles/TAG_cast_cN_ncu_metrics.json and profiles/TAG_launches_cN.csv, and
+profiles/TAG_cast_cN_ncu_metrics.json and profiles/TAG_launches_cN.csv (or
+under $PROFILES_OUT), and
 prints each kernel's share of the launch list."""
 import csv
 import io
@@ -70,18 +71,20 @@ def main():
     tag = sys.argv[1]
     cfgs = sys.argv[2:] or ["3", "4", "5", "6"]
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = os.environ.get("PROFILES_OUT", os.path.join(root, "profiles"))
+    os.makedirs(out, exist_ok=True)
     for c in cfgs:
         rep = os.path.join(root, "gpurun_out", f"{tag}_cast_c{c}.ncu-rep")
         if os.path.exists(rep):
             m = raw(rep)
             d = {k: m[k] for k in KEYS if k in m}
             d["kernel"] = m.get("Kernel Name", ["?"])[0]
-            with open(os.path.join(root, "profiles", f"{tag}_cast_c{c}_ncu_metrics.json"), "w") as f:
+            with open(os.path.join(out, f"{tag}_cast_c{c}_ncu_metrics.json"), "w") as f:
                 json.dump(d, f, indent=1)
             print(f"c{c}", {k.split("__")[-1][:40]: v[0] for k, v in d.items() if k != "kernel"})
         lc = os.path.join(root, "gpurun_out", f"{tag}_launches_c{c}.csv")
         if os.path.exists(lc):
-            shutil.copy(lc, os.path.join(root, "profiles", f"{tag}_launches_c{c}.csv"))
+            shutil.copy(lc, os.path.join(out, f"{tag}_launches_c{c}.csv"))
             print(f"c{c} launch shares %:", shares(lc))
 
 
