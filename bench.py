@@ -766,9 +766,26 @@ def main():
         h2d = poses_h.numel() * 4 + (beams_h.numel() * 4 if beams_h is not None else 0) + \
             (V_h[0].numel() * 4 if V_h is not None else 0)
         d2h = sum(v.numel() * 4 for v in out_h.values())
+        # the PCIe ceiling of this path: pinned device->host copy bandwidth of
+        # one step's image bytes (torch copies, best of 3; tools/pcie_d2h.py)
+        probe_d = torch.empty(d2h // 4, dtype=torch.int32, device=dev)
+        probe_h = torch.empty(d2h // 4, dtype=torch.int32, pin_memory=True)
+        d2h_gbs = 0.0
+        for _ in range(3):
+            ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ea.record()
+            probe_h.copy_(probe_d, non_blocking=True)
+            eb.record()
+            torch.cuda.synchronize()
+            d2h_gbs = max(d2h_gbs, d2h / (ea.elapsed_time(eb) / 1e3) / 1e9)
+        del probe_d, probe_h
+        e2e_gbs = d2h * n_e2e / dt / 1e9
         e2e = {"value": rays_total * n_e2e / dt, "unit": "rays/s",
                "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world, "steps": n_e2e,
-               "note": "agr_cast_*_host: H2D poses, chunked cast, D2H of every output image"}
+               "d2h_gbs": e2e_gbs, "d2h_peak_gbs": d2h_gbs, "d2h_frac": e2e_gbs / d2h_gbs if d2h_gbs else None,
+               "note": "agr_cast_*_host: H2D poses, cast in 32 env chunks on one stream while the finished "
+                       "chunks' images are copied to pinned host memory on another; d2h_peak_gbs = one "
+                       "pinned copy of the same bytes (the PCIe ceiling of this path)"}
 
     # ---- rank 0 re-casts every global env alone: 1-GPU digest == N-GPU digest
     verify = None

@@ -998,6 +998,9 @@ static bool is_pinned(const void* p) {
 
 // Casts env chunks into a double-buffered device area and streams each chunk
 // back to the host while the next one is traced.
+#ifndef AGR_E2E_CHUNKS
+#define AGR_E2E_CHUNKS 32  // env chunks of a host cast: chunk k + 1 is cast while chunk k is copied back
+#endif
 struct E2EChannel {
     void* host;   // caller's host pointer (whole output)
     int bytes;    // bytes per element
@@ -1016,8 +1019,8 @@ static agr_status e2e_run(agr_scene s, CastArgs& a, int64_t elems_per_env, agr_o
             bytes_per_elem += c.bytes;
             direct = direct && is_pinned(c.host);
         }
-    // ~8 chunks, at least 1 env each
-    int chunk = (E + 7) / 8;
+    // ~AGR_E2E_CHUNKS chunks, at least 1 env each
+    int chunk = (E + AGR_E2E_CHUNKS - 1) / AGR_E2E_CHUNKS;
     if (chunk < 1) chunk = 1;
     size_t chunk_bytes = (size_t)(chunk * elems_per_env * bytes_per_elem);
     agr_status st = e2e_prepare(s, a.S * 12 * sizeof(float) * (size_t)E, chunk_bytes);

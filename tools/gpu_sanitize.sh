@@ -1,7 +1,9 @@
+# compute-sanitizer over tools/sanitize_run.py: tools/gpu_sanitize.sh [TAG]
 CS=/usr/local/cuda/bin/compute-sanitizer
+out=gpurun_out/${1:-sanitize}.txt
 for t in memcheck initcheck racecheck synccheck; do
-  echo "== $t" >> gpurun_out/sanitize.txt
-  timeout 1200 $CS --tool $t --kernel-name kns=agr --print-limit 20 python tools/sanitize_run.py >> gpurun_out/sanitize.txt 2>&1
-  echo "exit $?" >> gpurun_out/sanitize.txt
+  echo "== $t" >> $out
+  timeout 1200 $CS --tool $t --kernel-name kns=agr --print-limit 20 python tools/sanitize_run.py >> $out 2>&1
+  echo "exit $?" >> $out
 done
-grep -E '^==|ERROR SUMMARY|exit|done' gpurun_out/sanitize.txt
+grep -E '^==|ERROR SUMMARY|exit|done' $out

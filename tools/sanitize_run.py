@@ -3,7 +3,8 @@ racecheck / synccheck): every kernel family of libagr.so once -- BLAS
 builds (create + a batched mesh update with the cooperative top-down
 BVH4), TLAS LBVH / SAH builds and refit, pinhole casts in every traversal
 schedule (packets BVH8 / BVH4, lanes, exact), beams, explicit rays, extras,
-stereo, checksums and the simulator stand-in."""
+stereo, checksums, deep TLAS (BVH16 / BVH32 copies, the wide SAH-optimal
+DP collapses, warp and CTA TLAS paths) and the simulator stand-in."""
 import os
 import sys
 
@@ -49,6 +50,29 @@ d = T(np.random.default_rng(0).normal(size=(3, R, 3)).astype(np.float32))
 s.cast_rays(o, d, 10.0)
 torch.cuda.synchronize()
 s.close()
+
+# deep TLAS (round 2): c3 forest envs (91 items: BVH32 by default, the CTA
+# TLAS build with the 32-wide DP), the BVH16 copy, and 300 items in one env
+# (beyond the DP's 128: greedy wide collapse), both builders + refit, every
+# pinhole schedule
+sc3, sen3 = sg.config3(n_envs=2)
+rng = np.random.default_rng(41)
+big = [[(j % 2, j + 1, sg.make_T(sg.random_rotation(rng), rng.uniform([2, -6, -4], [14, 6, 4]),
+                                 rng.uniform(0.1, 0.4))) for j in range(n)] for n in (300, 37)]
+scb = sg.assemble([sg.cube_mesh(), sg.panel_mesh()], big)
+for scx, nw, poses_x in ((sc3, 0, sen3["poses"]), (sc3, 16, sen3["poses"]), (scb, 0, sg.identity_poses(2))):
+    sx = agr.Scene.from_scenegen(scx, node_width=nw)
+    sx.set_instance_transforms(T(scx.inst_T))
+    for builder in (0, 1):
+        sx.set_tlas_builder(builder)
+        sx.build()
+        sx.refit()
+        for mode in (0, 3):
+            sx.set_traversal(mode)
+            sx.cast_pinhole(sg.pinhole(40, 24, 87.0), T(poses_x), 10.0, agr.AGR_DEPTH,
+                            channels=("dist", "seg", "face"))
+    torch.cuda.synchronize()
+    sx.close()
 
 # per-env unique meshes: batched BLAS rebuild (sort, fit, records, top-down BVH4)
 E = 4
