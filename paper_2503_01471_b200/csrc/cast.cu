@@ -831,7 +831,7 @@ __device__ __forceinline__ void pslab_axis_fast(float lo, float hi, float ol, fl
 // twice: the difference is ~2^-24 |o| in position, inside the 2 delta
 // widening, which is >= 2^-16 |o|).  An axis whose interval contains 0
 // keeps E = lo, X = hi: entry = max(lo i1 + cE1, hi i0 + cX0), exit = inf.
-struct PSlab8 {
+struct __align__(16) PSlab8 {
     float i0x, i0y, i0z, i1x, i1y, i1z;
     float ex0, ex1, xx0, xx1;  // x: cE0, cE1, cX0, cX1
     float ey0, ey1, xy0, xy1;
@@ -872,18 +872,21 @@ __device__ __forceinline__ PSlab8 make_pslab8(f3 o, f3 d, float delta) {
     return p;
 }
 
+// The state is 5 float4s in a 16-B aligned shared-memory slot: stored and
+// reloaded (at instance exits and after every leaf) with 128-bit accesses.
+static_assert(PS8_N == 20 && sizeof(PSlab8) == 80, "PSlab8 is 5 float4s");
 __device__ __forceinline__ void ps8_store(float* dst, const PSlab8& p) {
-    const float* q = reinterpret_cast<const float*>(&p);
+    const float4* q = reinterpret_cast<const float4*>(&p);
+    float4* d = reinterpret_cast<float4*>(dst);
 #pragma unroll
-    for (int k = 0; k < PS8_N; ++k) dst[k] = q[k];
+    for (int k = 0; k < 5; ++k) d[k] = q[k];
 }
 __device__ __forceinline__ PSlab8 ps8_load(const float* src) {
     PSlab8 p;
-    p.i0x = src[0]; p.i0y = src[1]; p.i0z = src[2]; p.i1x = src[3]; p.i1y = src[4]; p.i1z = src[5];
-    p.ex0 = src[6]; p.ex1 = src[7]; p.xx0 = src[8]; p.xx1 = src[9];
-    p.ey0 = src[10]; p.ey1 = src[11]; p.xy0 = src[12]; p.xy1 = src[13];
-    p.ez0 = src[14]; p.ez1 = src[15]; p.xz0 = src[16]; p.xz1 = src[17];
-    p.neg = __float_as_int(src[18]); p.strad = __float_as_int(src[19]);
+    const float4* q = reinterpret_cast<const float4*>(src);
+    float4* d = reinterpret_cast<float4*>(&p);
+#pragma unroll
+    for (int k = 0; k < 5; ++k) d[k] = q[k];
     return p;
 }
 
@@ -1526,7 +1529,7 @@ __device__ __forceinline__ RayId ray_id(const CastArgs& a) {
 template <int MODEL, int TRAV, bool COUNT, bool STEREO, int WIDE>
 __global__ void __launch_bounds__(CAST_THREADS, CAST_MIN_BLOCKS) k_cast(const __grid_constant__ CastArgs a) {
     __shared__ int s_stack[TRAV == 1 ? CAST_THREADS / 32 : 1][TRAV == 1 ? PSTACK : 1];
-    __shared__ float s_pslab[TRAV == 1 ? CAST_THREADS / 32 : 1][2][2 * PS_MAXN];  // [warp][env, obj][role][..]
+    __shared__ __align__(16) float s_pslab[TRAV == 1 ? CAST_THREADS / 32 : 1][2][2 * PS_MAXN];  // [warp][env, obj][role][..]
     RayId id = ray_id<MODEL>(a);
     // ragged tile lanes keep the warp whole for the traversal: they trace a
     // copy of a valid pixel and store nothing
