@@ -51,7 +51,7 @@ import scenegen as sg  # noqa: E402
 
 METRIC = "rays/sec and env-frames/sec at 1/2/4/8 B200; % of HBM/FP32 roofline"
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
-TRAFFIC_PATH = os.path.join(ROOT, "profiles", "cast_traffic.json")
+NCU_PATH = os.path.join(ROOT, "profiles", "cast_ncu.json")  # tools/cast_ncu_summary.py
 
 # Algorithmic thread-instruction costs of one unit of traversal work
 # (DESIGN.md §8 "ALU roofline"): per child box test, per
@@ -817,12 +817,14 @@ def main():
         achieved = w_ray * rays_per_step / cast_s / 1e12
         mhz = clocks.get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)
         peak = 148 * 128 * mhz * 1e6 / 1e12
-        traffic = None
-        if os.path.exists(TRAFFIC_PATH):
-            traffic = json.load(open(TRAFFIC_PATH)).get(f"c{cfg}")
+        traffic = ncu = None
+        if os.path.exists(NCU_PATH):  # the committed ncu capture of this config's cast
+            ncu = json.load(open(NCU_PATH)).get(f"c{cfg}")
+            traffic = ncu["traffic"] if ncu else None
         roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tinst/s",
                 "frac": achieved / peak, "traffic": traffic,
                 "kernel": "k_cast", "kernel_ms": 1e3 * cast_s,
+                "ncu": ncu,  # L2 / L1 hit, FMA / ALU / FP64 pipes, issue activity of the same launch shape
                 "work_per_ray_inst": w_ray, "per_ray": per,
                 "peak_note": "148 SMs x 128 FP32/INT lanes x measured median SM clock "
                              "(DESIGN.md §8; FMA-loop check in profiles/fma_peak.json); "
