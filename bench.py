@@ -783,7 +783,7 @@ def main():
         e2e = {"value": rays_total * n_e2e / dt, "unit": "rays/s",
                "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world, "steps": n_e2e,
                "d2h_gbs": e2e_gbs, "d2h_peak_gbs": d2h_gbs, "d2h_frac": e2e_gbs / d2h_gbs if d2h_gbs else None,
-               "note": "agr_cast_*_host: H2D poses, cast in 32 env chunks on one stream while the finished "
+               "note": "agr_cast_*_host: H2D poses, cast in up to 32 env chunks of >= 2^20 rays on one stream while the finished "
                        "chunks' images are copied to pinned host memory on another; d2h_peak_gbs = one "
                        "pinned copy of the same bytes (the PCIe ceiling of this path)"}
 

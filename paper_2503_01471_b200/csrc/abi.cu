@@ -1001,6 +1001,9 @@ static bool is_pinned(const void* p) {
 #ifndef AGR_E2E_CHUNKS
 #define AGR_E2E_CHUNKS 32  // env chunks of a host cast: chunk k + 1 is cast while chunk k is copied back
 #endif
+#ifndef AGR_E2E_MIN_ELEMS
+#define AGR_E2E_MIN_ELEMS (1 << 20)  // rays per chunk at least (so each chunk's cast fills the GPU)
+#endif
 struct E2EChannel {
     void* host;   // caller's host pointer (whole output)
     int bytes;    // bytes per element
@@ -1019,8 +1022,13 @@ static agr_status e2e_run(agr_scene s, CastArgs& a, int64_t elems_per_env, agr_o
             bytes_per_elem += c.bytes;
             direct = direct && is_pinned(c.host);
         }
-    // ~AGR_E2E_CHUNKS chunks, at least 1 env each
-    int chunk = (E + AGR_E2E_CHUNKS - 1) / AGR_E2E_CHUNKS;
+    // up to AGR_E2E_CHUNKS chunks of at least AGR_E2E_MIN_ELEMS rays (a
+    // smaller cast leaves the GPU in its launch tail: c6's 8-env chunks of
+    // 32 ran at 0.87 Grays/s end to end, 8 chunks at 1.19), >= 1 env each
+    int64_t n_chunks = (int64_t)E * elems_per_env / AGR_E2E_MIN_ELEMS;
+    if (n_chunks > AGR_E2E_CHUNKS) n_chunks = AGR_E2E_CHUNKS;
+    if (n_chunks < 1) n_chunks = 1;
+    int chunk = (int)((E + n_chunks - 1) / n_chunks);
     if (chunk < 1) chunk = 1;
     size_t chunk_bytes = (size_t)(chunk * elems_per_env * bytes_per_elem);
     agr_status st = e2e_prepare(s, a.S * 12 * sizeof(float) * (size_t)E, chunk_bytes);
