@@ -459,9 +459,10 @@ def _flat(out):
 def test_c5_bench_step_full_size():
     """c5 at its stated 16384 envs in bench.py's launch configuration: every
     step sets a new transform set and rebuilds the LBVH TLAS (warp-per-env
-    build with the SAH-optimal BVH8 collapse), then casts; 20 000 sampled rays
-    per step against the oracle and every ray of the first 2048 envs
-    certified."""
+    build with the SAH-optimal BVH8 collapse), then casts; in step 1 exact
+    mode == filter mode bitwise on all 530.8 M rays and 20 000 silhouette rays
+    against the oracle; 20 000 sampled rays per step against the oracle and
+    every ray of the first 2048 envs certified."""
     sc, sensor = sg.config5(n_envs=16384, ring=3)
     ring = sc.extra["ring_T"]
     s = make_scene(sc, build=False)
@@ -473,12 +474,29 @@ def test_c5_bench_step_full_size():
     for step in (1, 2):
         s.set_instance_transforms(torch.from_numpy(ring[step]).to(dev()))
         s.build()
-        out = _flat(s.cast_pinhole(sensor["cam"], poses, sensor["max_range"], agr.AGR_DEPTH))
+        img = s.cast_pinhole(sensor["cam"], poses, sensor["max_range"], agr.AGR_DEPTH)
+        sc2 = sg.Scene(sc.meshes, sc.env_off, sc.inst_asset, sc.inst_label, ring[step])
+        if step == 1:
+            # exact mode == the filtered packet cast on all 530.8 M rays, and
+            # 20 000 silhouette rays against the oracle
+            s.set_exact_mode(True)
+            ex = s.cast_pinhole(sensor["cam"], poses, sensor["max_range"], agr.AGR_DEPTH)
+            s.set_exact_mode(False)
+            for k in img:
+                assert torch.equal(img[k], ex[k]), k
+            del ex
+            sil = _silhouette_pixels(img["seg"].cpu().numpy())
+            qs = np.random.default_rng(14).choice(sil, 20000, replace=False)
+            qst = torch.from_numpy(qs).to(dev())
+            ref = oracle.cast(sc2, oracle_rays(sensor, "depth"), query=qs)
+            compare(ref, img["dist"].reshape(-1)[qst].cpu().numpy(), img["seg"].reshape(-1)[qst].cpu().numpy(),
+                    img["face"].reshape(-1)[qst].cpu().numpy(), "c5 silhouettes")
+        out = _flat(img)
+        del img
         n = out["dist"].numel()
         q = rng.choice(n, 20000, replace=False)
         qt = torch.from_numpy(q).to(dev())
         got = {k: v[qt].cpu().numpy() for k, v in out.items()}
-        sc2 = sg.Scene(sc.meshes, sc.env_off, sc.inst_asset, sc.inst_label, ring[step])
         ref = oracle.cast(sc2, oracle_rays(sensor, "depth"), query=q)
         compare(ref, got["dist"], got["seg"], got["face"], f"c5 full step {step}")
         head = {k: v[: E_cert * per_env].cpu().numpy() for k, v in out.items()}
@@ -493,8 +511,9 @@ def test_c5_bench_step_full_size():
 def test_c4_bench_step_full_size():
     """c4 at its stated 4096 envs in bench.py's launch configuration (SAH
     TLAS built once, transforms set + refit, interval packets on the BVH8):
-    40 000 sampled beams against the oracle and every ray of the first 1024
-    envs certified."""
+    exact mode == filter mode bitwise on all 268 M beams, 20 000 silhouette
+    beams and 40 000 sampled beams against the oracle, and every ray of the
+    first 1024 envs certified."""
     sc, sensor = sg.config4()
     s = make_scene(sc, build=False)
     s.set_tlas_builder(1)
@@ -503,7 +522,22 @@ def test_c4_bench_step_full_size():
     s.refit()
     beams = torch.from_numpy(np.ascontiguousarray(sensor["beams"])).to(dev())
     poses = torch.from_numpy(np.ascontiguousarray(sensor["poses"])).to(dev())
-    out = _flat(s.cast_beams(beams, poses, sensor["max_range"]))
+    img = s.cast_beams(beams, poses, sensor["max_range"])
+    # exact mode (all-FP64 per-lane traversal) == the filtered packet cast on
+    # all 268 M beams, and 20 000 silhouette beams against the oracle
+    s.set_exact_mode(True)
+    ex = s.cast_beams(beams, poses, sensor["max_range"])
+    s.set_exact_mode(False)
+    for k in img:
+        assert torch.equal(img[k], ex[k]), k
+    del ex
+    out = _flat(img)
+    sil = _silhouette_pixels(img["seg"].cpu().numpy())
+    qs = np.random.default_rng(13).choice(sil, 20000, replace=False)
+    qst = torch.from_numpy(qs).to(dev())
+    ref = oracle.cast(sc, oracle_rays(sensor, "range"), query=qs)
+    compare(ref, out["dist"][qst].cpu().numpy(), out["seg"][qst].cpu().numpy(), out["face"][qst].cpu().numpy(),
+            "c4 silhouettes")
     q = np.random.default_rng(12).choice(out["dist"].numel(), 40000, replace=False)
     qt = torch.from_numpy(q).to(dev())
     got = {k: v[qt].cpu().numpy() for k, v in out.items()}
