@@ -487,11 +487,14 @@ __global__ void k_rs_scatter(const uint32_t* __restrict__ kin, const uint32_t* _
 }
 
 // ---- K3: Karras radix tree (per segment) ------------------------------------------
-__device__ __forceinline__ int kdelta(const uint32_t* k, int n, int i, int j) {
+// Karras's delta(i, j): the common-prefix length of keys i and j (index
+// bits break ties), -1 outside [0, n); ki = k[i] is loaded once by the
+// caller, whose searches compare one key against many others.
+__device__ __forceinline__ int kdelta_i(const uint32_t* __restrict__ k, int n, uint32_t ki, int i, int j) {
     if (j < 0 || j >= n) return -1;
-    uint32_t a = k[i], b = k[j];
-    if (a == b) return 32 + __clz((unsigned)(i ^ j));
-    return __clz(a ^ b);
+    const uint32_t b = __ldg(k + j);
+    if (ki == b) return 32 + __clz((unsigned)(i ^ j));
+    return __clz(ki ^ b);
 }
 
 __global__ void k_karras(const BlasSeg* segs, const int* seg_of, const uint32_t* bounds, int Ftot,
@@ -507,15 +510,16 @@ __global__ void k_karras(const BlasSeg* segs, const int* seg_of, const uint32_t*
     int* child = child_all + 2 * c.off;
     int* node_parent = node_parent_all + c.off;
     int* leaf_parent = leaf_parent_all + c.off;
-    int d = (kdelta(k, n, i, i + 1) - kdelta(k, n, i, i - 1)) >= 0 ? 1 : -1;
-    int dmin = kdelta(k, n, i, i - d);
+    const uint32_t ki = __ldg(k + i);
+    int d = (kdelta_i(k, n, ki, i, i + 1) - kdelta_i(k, n, ki, i, i - 1)) >= 0 ? 1 : -1;
+    int dmin = kdelta_i(k, n, ki, i, i - d);
     int lmax = 2;
-    while (kdelta(k, n, i, i + lmax * d) > dmin) lmax <<= 1;
+    while (kdelta_i(k, n, ki, i, i + lmax * d) > dmin) lmax <<= 1;
     int l = 0;
     for (int t = lmax >> 1; t >= 1; t >>= 1)
-        if (kdelta(k, n, i, i + (l + t) * d) > dmin) l += t;
+        if (kdelta_i(k, n, ki, i, i + (l + t) * d) > dmin) l += t;
     int j = i + l * d;
-    int dnode = kdelta(k, n, i, j);
+    int dnode = kdelta_i(k, n, ki, i, j);
     // binary search for the split: the last position (from i towards j) whose
     // prefix with key i is longer than the node's common prefix.  Positions
     // beyond j never qualify (keys are sorted), so no bound check is needed.
@@ -523,7 +527,7 @@ __global__ void k_karras(const BlasSeg* segs, const int* seg_of, const uint32_t*
     int t = l;
     do {
         t = (t + 1) >> 1;
-        if (kdelta(k, n, i, i + (s + t) * d) > dnode) s += t;
+        if (kdelta_i(k, n, ki, i, i + (s + t) * d) > dnode) s += t;
     } while (t > 1);
     int gamma = i + s * d + (d < 0 ? -1 : 0);
     int lo = min(i, j), hi = max(i, j);
