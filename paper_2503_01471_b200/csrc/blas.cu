@@ -574,6 +574,9 @@ __device__ __forceinline__ int arrive_cta(int* flag) {
 #ifndef AGR_FIT_BLK
 #define AGR_FIT_BLK 256
 #endif
+#ifndef AGR_FIT_SMEM
+#define AGR_FIT_SMEM 1  // block-local node boxes of the fit also in shared memory
+#endif
 constexpr int FIT_BLK = AGR_FIT_BLK;  // larger blocks keep more of the climb at block scope
 __global__ void __launch_bounds__(FIT_BLK) k_fit(const BlasSeg* segs, const int* seg_of, const uint32_t* bounds,
                                               int Ftot, const uint32_t* __restrict__ sorted_all, const float* tri_box,
@@ -581,6 +584,12 @@ __global__ void __launch_bounds__(FIT_BLK) k_fit(const BlasSeg* segs, const int*
                                               float* ibox_all, int* flags_all, int* depth,
                                               const int2* __restrict__ range_all) {
     __shared__ int sflag[FIT_BLK];
+#if AGR_FIT_SMEM
+    // boxes of the block-local internal nodes, also kept here: a child box is
+    // read back by the second arrival right after its sibling wrote it, and
+    // global stores do not stay in L1 (an L2 round trip per level otherwise)
+    __shared__ __align__(16) float sbox[FIT_BLK][BX];
+#endif
     sflag[threadIdx.x] = 0;
     __syncthreads();
     const int blk0 = blockIdx.x * FIT_BLK;
@@ -610,7 +619,13 @@ __global__ void __launch_bounds__(FIT_BLK) k_fit(const BlasSeg* segs, const int*
                 sz += 1;
             } else {
                 // a child's subtree size and height ride in its box record
+#if AGR_FIT_SMEM
+                // a local node's children are local too (their ranges nest)
+                const int2 w = local ? load_box_w(&sbox[c.off + rr - blk0][0], dst)
+                                     : load_box_cg_w(ibox + BX * rr, dst);
+#else
                 const int2 w = local ? load_box_w(ibox + BX * rr, dst) : load_box_cg_w(ibox + BX * rr, dst);
+#endif
                 sz += w.x;
                 h = max(h, w.y);
             }
@@ -623,6 +638,9 @@ __global__ void __launch_bounds__(FIT_BLK) k_fit(const BlasSeg* segs, const int*
         // one record per level: the stores before the next (device-scope)
         // arrival are what its release waits for
         store_box_w(ibox + BX * node, u, sz, h + 1);
+#if AGR_FIT_SMEM
+        if (local) store_box_w(&sbox[c.off + node - blk0][0], u, sz, h + 1);
+#endif
         if (node == 0) depth[c.s] = h + 1;  // the root: the tree's depth in edges
         node = node_parent[node];
     }
