@@ -205,8 +205,9 @@ typedef struct {
                              (512-B nodes: lanes 0-15 test the children, 16-31
                              order them) or 32 (1-KB nodes: every lane tests
                              one child, ordered by the tile's entry bound);
-                             0 (default): 32 if some env has more than 64
-                             TLAS items (a deep TLAS: c3 +5 % over 8), else 8;
+                             0 (default): 32 (c3 +5 % over 8; an env of at
+                             most 32 TLAS items is one wide node: c4 +2 %,
+                             c5 +4 %);
                              4: no wide copy (half the node memory and no wide
                              collapse in builds / refits -- for scenes cast one
                              ray per lane).                                  */

@@ -196,8 +196,8 @@ class Scene:
         trbvh_rounds: treelet-restructuring passes on every BLAS (0 = LBVH).
         parts: split multi-component assets into BLAS parts when it pays
         (agr_create_options.part_policy 0); False: one BLAS per asset.
-        node_width: the interval packets' wide BVH copy: 8, 16 or 32 (0: 32 for
-        envs of more than 64 TLAS items, else 8), 4: BVH4 only."""
+        node_width: the interval packets' wide BVH copy: 8, 16 or 32 (0: 32),
+        4: BVH4 only."""
         lib = load()
         self._keep = []
         arr = (agr_mesh * len(meshes))()

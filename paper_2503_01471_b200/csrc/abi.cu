@@ -555,9 +555,6 @@ agr_status agr_scene_create_ex(int32_t device, const agr_mesh* meshes, int32_t n
         delete s;
         return st;
     };
-#ifndef AGR_WIDE_DEEP_ITEMS
-#define AGR_WIDE_DEEP_ITEMS 64  // node_width 0: BVH32 above this many TLAS items in some env, else BVH8
-#endif
 #define CKB(call)                                                    \
     do {                                                             \
         cudaError_t _e = (call);                                     \
@@ -565,12 +562,10 @@ agr_status agr_scene_create_ex(int32_t device, const agr_mesh* meshes, int32_t n
     } while (0)
 
     CKB(s->alloc(&s->nodes, 8 * (size_t)(nb + nt)));
-    // node_width 0: BVH32 when some env has more than 64 TLAS items (the
-    // TLAS is then deep enough for the wide nodes to pay: c3's 91 items
-    // BVH16 +3.5 % over BVH8, BVH32 +1.3 % over BVH16), else BVH8 (c4 / c5
-    // with 16-20 items: BVH16 -1 %, BVH32 -3.5 % -- its builds cost more)
-    s->wide_w = !opts || opts->node_width == 0 ? (s->max_n > AGR_WIDE_DEEP_ITEMS ? 32 : 8)
-                : opts->node_width == 4 ? 0 : opts->node_width;
+    // node_width 0: BVH32 (c3's 91-item envs: BVH16 +3.5 % over BVH8,
+    // BVH32 +1.3 % over BVH16; c4 / c5's 16-20-item envs: one 32-wide TLAS
+    // node, built without DP tables: c4 +1.8 %, c5 +3.6 % over BVH8)
+    s->wide_w = !opts || opts->node_width == 0 ? 32 : opts->node_width == 4 ? 0 : opts->node_width;
     if (s->wide_w) CKB(s->alloc(&s->nodesw, (size_t)2 * s->wide_w * (nb + nt)));
     CKB(s->alloc(&s->bnodes, 4 * (size_t)nb));
     CKB(s->alloc(&s->tris, 3 * (size_t)nl));

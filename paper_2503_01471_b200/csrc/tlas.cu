@@ -214,6 +214,25 @@ __device__ __forceinline__ void tdp_children(int j, const CH& child, const LB& l
     }
 }
 
+// An env of n <= W items fits one wide node: the SAH-optimal collapse is the
+// root holding every item (a wide child node would only add its own term),
+// so no DP tables are needed.  The items in the DP extraction's order (the
+// same stack walk with every internal child expanded).
+template <int W, class CH>
+__device__ __forceinline__ void all_items(const CH& child, int refs[W]) {
+    for (int k = 0; k < W; ++k) refs[k] = REF_EMPTY;
+    int st[W], sp = 0, cnt = 0;
+    st[sp++] = 0;
+    while (sp > 0) {
+        const int nn = st[--sp];
+        for (int side = 0; side < 2; ++side) {
+            const int r = child(nn, side);
+            if (r >= 0) st[sp++] = r;
+            else refs[cnt++] = r;
+        }
+    }
+}
+
 // Writes the wide node j (W children) from its binary refs.
 template <int W, class SRC>
 __device__ __forceinline__ void write_wide(const TlasArgs& a, int j, const int refs[W], const SRC& src_of, int i0,
@@ -445,6 +464,21 @@ __device__ void sah_build_cta(const TlasSmem& s, int n) {
 template <int W, class CH, class BXF>
 __device__ __forceinline__ void cta_wide(const TlasArgs& a, const TlasSmem& s, int n, int i0, int nodebase, int toff,
                                          int tid, int rebuild, float (*dpt)[TDP_STRIDE], const CH& ch, const BXF& bx) {
+    if (n <= W) {  // one wide node (the other binary nodes are unreachable and not written)
+        if (tid == 0) {
+            int refs[W];
+            int* keep = a.tlas_refsw + W * (size_t)toff;
+            if (rebuild) {
+                all_items<W>(ch, refs);
+                for (int c = 0; c < W; ++c) keep[c] = refs[c];
+            } else {
+                for (int c = 0; c < W; ++c) refs[c] = keep[c];
+            }
+            auto src = [&](int r) { return r < 0 ? s.box + 6 * ~r : s.ibox + 6 * r; };
+            write_wide<W>(a, 0, refs, src, i0, nodebase);
+        }
+        return;
+    }
     const bool opt = rebuild && n <= TDP_MAX;
     auto lbf = [&](int i) { return s.box + 6 * i; };
     auto nbf = [&](int r) { return s.ibox + 6 * r; };
@@ -735,6 +769,20 @@ __device__ __forceinline__ void warp_wide(const TlasArgs& a, TlasWarpSmem& s, in
     auto nbf = [&](int r) { return s.ibox[r]; };
     auto tbf = [&](int r) { return s.dpt[r]; };
     auto src = [&](int r) { return r < 0 ? s.box[~r] : s.ibox[r]; };
+    if (n <= W) {  // one wide node (the other binary nodes are unreachable and not written)
+        if (lane == 0) {
+            int refs[W];
+            int* keep = a.tlas_refsw + W * (size_t)toff;
+            if (rebuild) {
+                all_items<W>(ch, refs);
+                for (int c = 0; c < W; ++c) keep[c] = refs[c];
+            } else {
+                for (int c = 0; c < W; ++c) refs[c] = keep[c];
+            }
+            write_wide<W>(a, 0, refs, src, i0, nodebase);
+        }
+        return;
+    }
     if (!rebuild) {  // a refit keeps the build's collapse
         for (int j = lane; j < n - 1; j += 32) {
             int refs[W];

@@ -1098,11 +1098,12 @@ def test_parts_update_mesh_stereo_and_exact():
 
 @pytest.mark.parametrize("cfg", [2, 3, 4])
 def test_bvh8_packets_equal_bvh4_packets_bitwise(cfg):
-    """The interval-packet traversal over the BVH8 copy (default), over a
-    BVH16 / BVH32 copy (node_width 16 / 32), over the BVH4 (traversal mode 2), a
+    """The interval-packet traversal over the BVH32 copy (default), over a
+    BVH8 / BVH16 copy (node_width 8 / 16), over the BVH4 (traversal mode 2), a
     BVH4-only scene (node_width 4) and the per-lane traversal give bitwise
     identical images, after a rebuild and after a refit; and match the
-    oracle on samples."""
+    oracle on samples.  (c2 / c4 envs of <= 32 items have a one-node 32-wide
+    TLAS, c3's 91-item envs a deep one.)"""
     if cfg == 2:
         sc, sensor = sg.config2(n_envs=8)
     elif cfg == 3:
@@ -1115,10 +1116,10 @@ def test_bvh8_packets_equal_bvh4_packets_bitwise(cfg):
     s = make_scene(sc, build=False)
     s4 = agr.Scene.from_scenegen(sc, device=0, node_width=4)
     s16 = agr.Scene.from_scenegen(sc, device=0, node_width=16)
-    s32 = agr.Scene.from_scenegen(sc, device=0, node_width=32)
-    for sc_ in (s4, s16, s32):
+    s8 = agr.Scene.from_scenegen(sc, device=0, node_width=8)  # the default is 32
+    for sc_ in (s4, s16, s8):
         sc_.set_instance_transforms(torch.from_numpy(sc.inst_T).to(dev()))
-    for sc_ in (s, s4, s16, s32):
+    for sc_ in (s, s4, s16, s8):
         sc_.set_tlas_builder(1)
         sc_.build()
     imgs = []
@@ -1126,11 +1127,11 @@ def test_bvh8_packets_equal_bvh4_packets_bitwise(cfg):
         if step == 1:
             T2 = sc.inst_T.copy()
             T2[:, :2, 3] += np.random.default_rng(5).uniform(-0.3, 0.3, (len(T2), 2)).astype(np.float32)
-            for sc_ in (s, s4, s16, s32):
+            for sc_ in (s, s4, s16, s8):
                 sc_.set_instance_transforms(torch.from_numpy(T2).to(dev()))
                 sc_.refit()
         runs = []
-        for sc_, mode in ((s, 0), (s, 2), (s4, 0), (s, 1), (s, 3), (s16, 0), (s16, 3), (s32, 0), (s32, 3)):
+        for sc_, mode in ((s, 0), (s, 2), (s4, 0), (s, 1), (s, 3), (s16, 0), (s16, 3), (s8, 0), (s8, 3)):
             sc_.set_traversal(mode)
             runs.append(to_np(cast_sensor(sc_, sensor, kind, channels=chans)))
         for r in runs[1:]:
